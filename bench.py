@@ -1,0 +1,410 @@
+#!/usr/bin/env python3
+"""bench.py -- MPI_Pack/MPI_Unpack throughput of the B200 datatype engine.
+
+Workload (BASELINE.json configs[1], "cfg2"): a 3D MPI_Type_create_subarray
+of a 1 MiB object in a 1024^3-byte allocation, contiguous-dim extent E0 swept
+over 1..512 B (E1, E2 per SURVEY.md §8a). One STEP = for every E0: pack K
+objects (incount = K, objects one extent = 1 GiB apart) and unpack them back,
+through the product's C-ABI on device-resident buffers. The L2 is flushed
+(a 512 MiB write) before every kernel and only the kernels are timed, with
+CUDA events on the launching stream.
+
+  value      = algorithmic bytes (2 x incount x size per pack or unpack:
+               described bytes read + packed bytes written) / kernel time
+  e2e        = the same metric through the same C-ABI with the packed
+               message in pinned HOST memory: unpack reads it over PCIe,
+               pack writes it back (the paper's one-shot method); host<->
+               device traffic is inside the timed region
+  roofline   = dominant kernel vs MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline = the reference's own pack/unpack (oracle/_ref, compiled from
+               the untouched reference headers) on this host, bounded sample
+
+--impl reference times the reference CPU executor on the same workload
+(bounded: one object per E0 per step) with all host threads.
+Multi-GPU: pack/unpack does not shard ("replicas only"): each rank
+runs the same workload on its own GPU; value sums over ranks, time is the
+max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+E0S = [1, 2, 4, 8, 16, 32, 64, 128, 256, 512]
+METRIC = "MPI_Pack/Unpack GB/s (3D subarray, 1 MiB object, E0 sweep 1-512 B)"
+UNIT = "GB/s"
+FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback, only if MEASURED_PEAKS.json is absent
+
+
+def cfg2_dims(e0):
+    e2 = 2 ** math.ceil(math.log2((1 << 20) // e0) / 2)
+    e1 = (1 << 20) // (e0 * e2)
+    return e0, e1, e2
+
+
+def cfg2_prog(e0):
+    e0, e1, e2 = cfg2_dims(e0)
+    return [4, 3, 0, 1024, 1024, 1024, e0, e1, e2, 0, 0, 0, 0, 0]
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", FALLBACK_HBM)), "measured"
+    return FALLBACK_HBM, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ distributed
+def dist_setup(n):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, local, world
+
+
+def barrier_max(torch, world, value):
+    if world == 1:
+        return value
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier_sum(torch, world, value):
+    if world == 1:
+        return value
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ reference CPU
+def reference_engine():
+    from oracle.pyoracle import reference, oracle
+    r = reference()
+    if r is not None:
+        return r, "reference"
+    return oracle(), "port"
+
+
+def cpu_sample(threads, budget_s, reps_min=1):
+    """Times the reference CPU pack+unpack of one cfg2 object per E0 (commit
+    excluded). Returns (GB/s, seconds, reps, kind)."""
+    import numpy as np
+    eng, kind = reference_engine()
+    buf = np.zeros(1 << 30, np.uint8)  # the 1024^3 allocation
+    buf[::4093] = 7
+    total_bytes, total_t, reps = 0, 0.0, 0
+    handles = [(e0, eng.handle(cfg2_prog(e0))) for e0 in E0S]
+    packed = np.zeros(1 << 20, np.uint8)
+    t_start = time.perf_counter()
+    while reps < reps_min or (time.perf_counter() - t_start) < budget_s:
+        for e0, h in handles:
+            t0 = time.perf_counter()
+            if kind == "reference":
+                st, _ = eng.pack_h(h, buf.ctypes.data, buf.nbytes, 1, packed.ctypes.data, packed.nbytes, 0, threads)
+                st2, _ = eng.unpack_h(h, packed.ctypes.data, packed.nbytes, 0, 1, buf.ctypes.data, buf.nbytes, threads)
+            else:
+                st, _ = eng.pack_h(h, buf.ctypes.data, buf.nbytes, 1, packed.ctypes.data, packed.nbytes, 0)
+                st2, _ = eng.unpack_h(h, packed.ctypes.data, packed.nbytes, 0, 1, buf.ctypes.data, buf.nbytes)
+            total_t += time.perf_counter() - t0
+            assert st == 0 and st2 == 0
+            total_bytes += 4 * (1 << 20)
+        reps += 1
+    return total_bytes / total_t / 1e9, total_t, reps, kind
+
+
+def run_reference(args):
+    rank, local, world = dist_setup(args.gpus)
+    if rank != 0:
+        return 0
+    threads = 0  # PackOptions{.threads = 0}: hardware concurrency
+    ncores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_sample(threads, 0.0)
+    t_total, b_total = 0.0, 0
+    for _ in range(args.steps):
+        gbs, t, reps, kind = cpu_sample(threads, 0.0)
+        t_total += t
+        b_total += gbs * t * 1e9
+    value = b_total / t_total / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t_total / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": "cfg2 3D subarray pack+unpack, 1 MiB object in 1024^3 B, "
+                               "E0 in 1..512 (bounded CPU sample: 1 object per E0 per step)",
+                   "threads": "hardware_concurrency (PackOptions.threads=0)"},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": ncores, "kind": kind,
+                         "sample": "1 cfg2 object per E0 (10 pack + 10 unpack) per step"},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ ours
+def run_ours(args):
+    import numpy as np
+    import torch
+    import ctypes as C
+
+    import paper_2012_14363_b200 as sp
+    from paper_2012_14363_b200 import _capi
+
+    rank, local, world = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    K = args.incount
+    lib = _capi.lib
+    stream = torch.cuda.current_stream()
+    sh = C.c_void_p(stream.cuda_stream)
+
+    # one 1024^3 allocation per object: objects one extent (1 GiB) apart
+    src = torch.empty((K << 30), dtype=torch.uint8, device="cuda")
+    src[::4099] = 3  # touch; content is irrelevant to timing (parity is in tests/)
+    packed = torch.zeros(K << 20, dtype=torch.uint8, device="cuda")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    types = []
+    for e0 in E0S:
+        d = sp.from_program(cfg2_prog(e0))
+        ct = sp.commit_type(d)
+        types.append((e0, d, ct))
+
+    pos = C.c_int64(0)
+
+    def call(pack, ct, count, s_ptr, s_len, d_ptr, d_len):
+        pos.value = 0
+        if pack:
+            st = lib.sp_pack(s_ptr, s_len, ct.handle, count, d_ptr, d_len, C.byref(pos), sh)
+        else:
+            st = lib.sp_unpack(s_ptr, s_len, C.byref(pos), ct.handle, count, d_ptr, d_len, sh)
+        if st:
+            raise RuntimeError(lib.sp_last_error().decode())
+
+    def one_step(record):
+        """pack + unpack of K objects for every E0; returns per-kernel ms"""
+        evs = []
+        for e0, d, ct in types:
+            for pack in (True, False):
+                flush.zero_()
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                if pack:
+                    call(True, ct, K, src.data_ptr(), src.numel(), packed.data_ptr(), packed.numel())
+                else:
+                    call(False, ct, K, packed.data_ptr(), packed.numel(), src.data_ptr(), src.numel())
+                b.record(stream)
+                li = sp.last_launch()
+                evs.append((e0, pack, a, b, li))
+        return evs
+
+    for _ in range(args.warmup):
+        one_step(False)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    launches0 = sp.kernel_launch_count()
+    per = {}  # (e0, pack) -> list of ms
+    kinfo = {}
+    with ClockSampler(local) as clk:
+        all_evs = []
+        for _ in range(args.steps):
+            all_evs.extend(one_step(True))
+        torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    launches = sp.kernel_launch_count() - launches0
+    for e0, pack, a, b, li in all_evs:
+        per.setdefault((e0, pack), []).append(a.elapsed_time(b))
+        kinfo[(e0, pack)] = li
+    step_ms = sum(sum(v) for v in per.values()) / args.steps
+    step_ms = barrier_max(torch, world, step_ms)
+    bytes_per_kernel = 2 * K * (1 << 20)
+    bytes_per_step = bytes_per_kernel * 2 * len(E0S)
+    value = barrier_sum(torch, world, bytes_per_step) / (step_ms * 1e-3) / 1e9
+    hbm, hbm_kind = peaks()
+
+    sweep = []
+    dominant = None
+    for e0 in E0S:
+        row = {"E0": e0, "dims": list(cfg2_dims(e0)), "sector_cap": round(2 * e0 / (32 + e0), 3) if e0 < 32 else 1.0}
+        for pack in (True, False):
+            ms = statistics.mean(per[(e0, pack)])
+            gbs = bytes_per_kernel / (ms * 1e-3) / 1e9
+            tag = "pack" if pack else "unpack"
+            li = kinfo[(e0, pack)]
+            row[f"{tag}_us"] = round(ms * 1e3, 2)
+            row[f"{tag}_GBps"] = round(gbs, 1)
+            row[f"{tag}_frac"] = round(gbs / hbm, 4)
+            row[f"{tag}_kernel"] = f"{li.kernel.name}/w{li.word}"
+            if dominant is None or ms > dominant[0]:
+                dominant = (ms, e0, tag, gbs, li)
+        sweep.append(row)
+
+    # e2e: packed message in pinned host memory, through the same C-ABI
+    Ke = min(K, args.e2e_incount)
+    host_msg = torch.empty(Ke << 20, dtype=torch.uint8).pin_memory()
+    host_msg.fill_(5)
+    e2e_t = 0.0
+    for it in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for e0, d, ct in types:
+            call(False, ct, Ke, host_msg.data_ptr(), host_msg.numel(), src.data_ptr(), src.numel())
+            call(True, ct, Ke, src.data_ptr(), src.numel(), host_msg.data_ptr(), host_msg.numel())
+        b.record(stream)
+        torch.cuda.synchronize()
+        if it >= args.warmup:
+            e2e_t += a.elapsed_time(b)
+    e2e_ms = barrier_max(torch, world, e2e_t / args.steps)
+    e2e_bytes = 2 * Ke * (1 << 20) * 2 * len(E0S)
+    e2e_val = barrier_sum(torch, world, e2e_bytes) / (e2e_ms * 1e-3) / 1e9
+
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return 0
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        gbs, t, reps, kind = cpu_sample(1, args.cpu_seconds)
+        cpu = {"value": round(gbs, 4), "unit": UNIT, "cores": 1, "kind": kind,
+               "sample": f"{reps} x (pack+unpack of 1 cfg2 object per E0), {t:.1f} s CPU, "
+                         "PackOptions.threads=1 (the reference's fastest setting)"}
+    ms, e0, tag, gbs, li = dominant
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tfile):
+        with open(tfile) as f:
+            traffic = json.load(f).get(f"cfg2_E0_{e0}_{tag}_K{K}")
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic",
+        "config": {"workload": f"cfg2: MPI_Type_create_subarray 3D, 1 MiB object in 1024^3 B, "
+                               f"E0 sweep {E0S[0]}-{E0S[-1]} B, pack+unpack, incount={K} per call",
+                   "incount": K, "l2": "flushed (512 MiB write) before every timed kernel",
+                   "parallelism": f"replicas x{world}"},
+        "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(gbs / hbm, 4), "traffic": traffic,
+                     "kernel": f"{tag} E0={e0} {li.kernel.name}/w{li.word}",
+                     "peak_source": hbm_kind,
+                     "algorithmic_bytes_per_launch": bytes_per_kernel},
+        "sweep": sweep,
+        "e2e": {"value": round(e2e_val, 2), "unit": UNIT, "h2d_bytes_per_step": Ke * (1 << 20) * len(E0S),
+                "d2h_bytes_per_step": Ke * (1 << 20) * len(E0S),
+                "how": f"sp_unpack from pinned host + sp_pack to pinned host, incount={Ke}, all E0"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--incount", type=int, default=32)
+    ap.add_argument("--e2e-incount", type=int, default=8)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

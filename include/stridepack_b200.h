@@ -1,0 +1,166 @@
+/*
+ * stridepack_b200.h -- C-ABI of the B200-native derived-datatype engine
+ * (libstridepack_b200.so). Plain pointers and sizes only; no CUDA or torch
+ * types cross this boundary (streams are passed as `void *` and interpreted
+ * as cudaStream_t, NULL = the legacy default stream).
+ *
+ * Each entry point replaces one entry of the reference engine's C++ API
+ * ("stridepack", /root/reference/proj/include/stridepack/); the cited
+ * file:line is the interface it stands in for. The reference reports errors
+ * as C++ exceptions (errors.hpp:8-47); here every call returns an sp_status
+ * whose values map 1:1 onto those exception types, and never throws.
+ *
+ * Threading: type construction, commit and queries are thread-safe
+ * (commit.hpp:81-99). sp_pack/sp_unpack may run concurrently on distinct
+ * destination buffers. Kernels are enqueued on the caller's
+ * stream on the CURRENT CUDA device; calls on device or pinned host memory
+ * return without synchronising. Pageable host buffers are staged through the
+ * device and synchronise the stream before returning.
+ */
+#ifndef STRIDEPACK_B200_H
+#define STRIDEPACK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: errors.hpp:8-47 ---------------------------------- */
+typedef int sp_status;
+enum {
+  SP_OK = 0,
+  SP_ERR_INVALID_ARGUMENT = 1,   /* InvalidArgument   errors.hpp:13 */
+  SP_ERR_UNSUPPORTED_ORDER = 2,  /* UnsupportedOrder  errors.hpp:18 */
+  SP_ERR_INVALID_LAYOUT = 3,     /* InvalidLayout     errors.hpp:23 */
+  SP_ERR_BUFFER_TOO_SMALL = 4,   /* BufferTooSmall    errors.hpp:27 */
+  SP_ERR_OVERLAPPING_LAYOUT = 5, /* OverlappingLayout errors.hpp:32 */
+  SP_ERR_UNSUPPORTED = 6,        /* Unsupported       errors.hpp:37 */
+  SP_ERR_EMPTY_PROFILE = 7,      /* EmptyProfile      errors.hpp:41 */
+  SP_ERR_PARSE = 8,              /* ParseError        errors.hpp:45 */
+  SP_ERR_INTERNAL = 9,
+  SP_ERR_INVALID_HANDLE = 11,
+  SP_ERR_CUDA = 12,              /* a CUDA runtime call failed */
+  SP_ERR_NO_DEVICE = 13          /* no usable CUDA device: the GPU path is
+                                    the only execution path, there is no
+                                    host fallback */
+};
+
+const char *sp_status_string(sp_status s);
+/* message of the last failing call on this thread ("" if none) */
+const char *sp_last_error(void);
+
+/* ---- datatype construction: type_def.hpp:125-195 -------------------- */
+typedef uint64_t sp_type; /* opaque handle; 0 is never valid */
+
+enum { SP_BYTE = 0, SP_INT = 1, SP_FLOAT = 2, SP_DOUBLE = 3 }; /* NamedKind type_def.hpp:15 */
+enum { SP_ORDER_C = 0, SP_ORDER_FORTRAN = 1 };                 /* ArrayOrder type_def.hpp:47 */
+
+/* make_named                 type_def.hpp:125 */
+sp_status sp_type_named(int kind, sp_type *out);
+/* make_contiguous            type_def.hpp:129 */
+sp_status sp_type_contiguous(int64_t count, sp_type inner, sp_type *out);
+/* make_vector  (stride in inner extents)   type_def.hpp:137 */
+sp_status sp_type_vector(int64_t count, int64_t blocklength, int64_t stride,
+                         sp_type inner, sp_type *out);
+/* make_hvector (stride in bytes)           type_def.hpp:149 */
+sp_status sp_type_hvector(int64_t count, int64_t blocklength,
+                          int64_t stride_bytes, sp_type inner, sp_type *out);
+/* make_subarray: dim 0 innermost, C order only (type_def.hpp:161-195) */
+sp_status sp_type_subarray(int64_t ndims, const int64_t *sizes,
+                           const int64_t *subsizes, const int64_t *offsets,
+                           sp_type inner, int order, sp_type *out);
+/* releases the handle; definitions that wrap it keep their own reference */
+sp_status sp_type_free(sp_type t);
+/* type_size                  type_def.hpp:198 */
+sp_status sp_type_size(sp_type t, int64_t *size);
+/* type_extent                type_def.hpp:221 */
+sp_status sp_type_extent(sp_type t, int64_t *extent);
+
+/* ---- commit: commit.hpp:51 (commit_type) / :87 (TypeRegistry::commit) -
+ * Canonicalises the definition (translate -> fold/elide/flatten/sort to a
+ * fixpoint -> StridedBlock -> plan), decides overlap exactly, and records
+ * the execution plan. Idempotent. O(definition tree), not O(size). */
+sp_status sp_type_commit(sp_type t);
+
+enum { SP_FORM_STRIDED = 0, SP_FORM_EMPTY = 1, SP_FORM_UNSUPPORTED = 2 }; /* commit.hpp:21 */
+enum { SP_STRATEGY_GRIDZ = 0, SP_STRATEGY_ITERATE = 1 };                   /* plan.hpp:13 */
+
+/* CommittedType (commit.hpp:30-43) + PackPlan (plan.hpp:27-44) */
+typedef struct {
+  int64_t form;
+  int64_t size;        /* described bytes per object */
+  int64_t extent;      /* placement span for consecutive objects */
+  int64_t span;        /* one past the last described byte */
+  int64_t overlapping; /* some byte described twice */
+  int64_t ndims;       /* StridedBlock dims (0 unless form == STRIDED) */
+  int64_t start;       /* StridedBlock start */
+  int64_t word;        /* PackPlan.word (reference select_word_size) */
+  int64_t block[3], grid[3], strategy; /* PackPlan block/grid/count strategy */
+  int64_t n_fallback_runs; /* definition-order runs (Unsupported form) */
+  int64_t simplify_rounds; /* fixpoint rounds (canon.hpp:117), -1 if n/a */
+} sp_type_info;
+
+/* Fills info and, when cap >= ndims, the StridedBlock counts/strides
+ * (strided_block.hpp:17-46). Requires a committed type. */
+sp_status sp_type_query(sp_type t, sp_type_info *info, int64_t *counts,
+                        int64_t *strides, int64_t cap);
+
+/* ---- pack / unpack: pack.hpp:99 / pack.hpp:143 ---------------------- *
+ * pack: gathers `incount` objects laid out at src + j*extent into
+ * dst + *position in canonical order (object-major, dimension 1 fastest,
+ * exactly the reference executor's byte order) and advances *position by
+ * incount*size. Error precedence follows pack.hpp:102-126:
+ * INVALID_ARGUMENT (incount < 1, position < 0), BUFFER_TOO_SMALL (dst),
+ * EMPTY no-op, BUFFER_TOO_SMALL (src), UNSUPPORTED (fallback disabled).
+ * src_bytes/dst_bytes are the caller's buffer sizes (UINT64_MAX = unknown).
+ * unpack follows pack.hpp:146-159: INVALID_ARGUMENT, OVERLAPPING_LAYOUT,
+ * BUFFER_TOO_SMALL (src), EMPTY no-op, BUFFER_TOO_SMALL (dst). Bytes of dst
+ * outside the layout are never written. */
+sp_status sp_pack(const void *src, uint64_t src_bytes, sp_type t,
+                  int64_t incount, void *dst, uint64_t dst_bytes,
+                  int64_t *position, void *stream);
+sp_status sp_unpack(const void *src, uint64_t src_bytes, int64_t *position,
+                    sp_type t, int64_t outcount, void *dst, uint64_t dst_bytes,
+                    void *stream);
+
+/* Options mirror PackOptions (pack.hpp:15-18) plus test/bench knobs. */
+enum {
+  SP_KERNEL_AUTO = 0,
+  SP_KERNEL_WORDS = 1,    /* generic N-D word kernel */
+  SP_KERNEL_SMALLROW = 2, /* rows of 1/2/4/8 B gathered into 16 B stores */
+  SP_KERNEL_BLOCKLIST = 3,/* device block-list (definition-order runs) */
+  SP_KERNEL_TMA = 4,      /* tensor-map box staged through shared memory */
+  SP_KERNEL_WORDS64 = 5   /* generic kernel with 64-bit indexing (chosen
+                             automatically beyond 2^32 words or rows) */
+};
+typedef struct {
+  int allow_fallback; /* PackOptions.allow_fallback (default 1) */
+  int kernel;         /* SP_KERNEL_* (0 = auto) */
+  int force_word;     /* 0 = auto, else 1/2/4/8/16 (must be legal) */
+} sp_pack_options;
+sp_status sp_pack_ex(const void *src, uint64_t src_bytes, sp_type t,
+                     int64_t incount, void *dst, uint64_t dst_bytes,
+                     int64_t *position, void *stream,
+                     const sp_pack_options *opt);
+sp_status sp_unpack_ex(const void *src, uint64_t src_bytes, int64_t *position,
+                       sp_type t, int64_t outcount, void *dst,
+                       uint64_t dst_bytes, void *stream,
+                       const sp_pack_options *opt);
+
+/* What the last pack or unpack call on this thread launched. */
+typedef struct {
+  int64_t kernel;      /* SP_KERNEL_* actually used, 0 = no launch (empty) */
+  int64_t word;        /* word size of the launch */
+  int64_t launches;    /* kernels enqueued by that call */
+  int64_t grid, block; /* launch shape of the main kernel */
+  int64_t staged;      /* 1 if pageable host memory was staged */
+} sp_launch_info;
+sp_status sp_last_launch(sp_launch_info *out);
+/* total kernels this library enqueued in this process */
+int64_t sp_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STRIDEPACK_B200_H */

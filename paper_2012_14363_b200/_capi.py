@@ -1,0 +1,79 @@
+"""ctypes binding of include/stridepack_b200.h (libstridepack_b200.so).
+
+The shared library is built in-tree by ``__graft_entry__.build()``
+(paper_2012_14363_b200/csrc/Makefile). Importing this module without it
+fails loudly: there is no Python or CPU fallback for the datatype engine.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "libstridepack_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(the B200 engine has no fallback implementation)")
+
+lib = C.CDLL(LIB_PATH)
+
+i64 = C.c_int64
+u64 = C.c_uint64
+i64p = C.POINTER(C.c_int64)
+sp_type = C.c_uint64
+
+
+class TypeInfo(C.Structure):
+    _fields_ = [("form", i64), ("size", i64), ("extent", i64), ("span", i64),
+                ("overlapping", i64), ("ndims", i64), ("start", i64), ("word", i64),
+                ("block", i64 * 3), ("grid", i64 * 3), ("strategy", i64),
+                ("n_fallback_runs", i64), ("simplify_rounds", i64)]
+
+
+class PackOptions(C.Structure):
+    _fields_ = [("allow_fallback", C.c_int), ("kernel", C.c_int), ("force_word", C.c_int)]
+
+
+class LaunchInfo(C.Structure):
+    _fields_ = [("kernel", i64), ("word", i64), ("launches", i64), ("grid", i64),
+                ("block", i64), ("staged", i64)]
+
+
+def _sig(name, res, *args):
+    f = getattr(lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+_sig("sp_status_string", C.c_char_p, C.c_int)
+_sig("sp_last_error", C.c_char_p)
+_sig("sp_type_named", C.c_int, C.c_int, C.POINTER(sp_type))
+_sig("sp_type_contiguous", C.c_int, i64, sp_type, C.POINTER(sp_type))
+_sig("sp_type_vector", C.c_int, i64, i64, i64, sp_type, C.POINTER(sp_type))
+_sig("sp_type_hvector", C.c_int, i64, i64, i64, sp_type, C.POINTER(sp_type))
+_sig("sp_type_subarray", C.c_int, i64, i64p, i64p, i64p, sp_type, C.c_int, C.POINTER(sp_type))
+_sig("sp_type_free", C.c_int, sp_type)
+_sig("sp_type_size", C.c_int, sp_type, i64p)
+_sig("sp_type_extent", C.c_int, sp_type, i64p)
+_sig("sp_type_commit", C.c_int, sp_type)
+_sig("sp_type_query", C.c_int, sp_type, C.POINTER(TypeInfo), i64p, i64p, i64)
+_sig("sp_pack", C.c_int, C.c_void_p, u64, sp_type, i64, C.c_void_p, u64, i64p, C.c_void_p)
+_sig("sp_unpack", C.c_int, C.c_void_p, u64, i64p, sp_type, i64, C.c_void_p, u64, C.c_void_p)
+_sig("sp_pack_ex", C.c_int, C.c_void_p, u64, sp_type, i64, C.c_void_p, u64, i64p, C.c_void_p,
+     C.POINTER(PackOptions))
+_sig("sp_unpack_ex", C.c_int, C.c_void_p, u64, i64p, sp_type, i64, C.c_void_p, u64, C.c_void_p,
+     C.POINTER(PackOptions))
+_sig("sp_last_launch", C.c_int, C.POINTER(LaunchInfo))
+_sig("sp_kernel_launch_count", i64)
+
+
+def exported_symbols():
+    """Every function include/stridepack_b200.h declares (for ABI tests)."""
+    import re
+    hdr = os.path.join(os.path.dirname(PKG_DIR), "include", "stridepack_b200.h")
+    src = open(hdr).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(sp_[a-z0-9_]+)\s*\(", src)))

@@ -1,0 +1,183 @@
+// capi.cpp -- extern "C" entry points of libstridepack_b200.so.
+// Every call converts internal errors (spb::Error) into an sp_status and a
+// thread-local message; nothing throws across the ABI.
+#include <cstring>
+#include <exception>
+#include <new>
+#include <string>
+
+#include "core.hpp"
+
+namespace {
+
+thread_local std::string t_err;
+
+template <class F> sp_status guard(F &&f) {
+  try {
+    t_err.clear();
+    f();
+    return SP_OK;
+  } catch (const spb::Error &e) {
+    t_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc &) {
+    t_err = "out of host memory";
+    return SP_ERR_INTERNAL;
+  } catch (const std::exception &e) {
+    t_err = e.what();
+    return SP_ERR_INTERNAL;
+  }
+}
+
+spb::DefPtr def_of(sp_type h) { return spb::registry().get(h).def; }
+
+sp_status add(spb::DefPtr d, sp_type *out) {
+  if (!out) spb::fail(SP_ERR_INVALID_ARGUMENT, "null output handle");
+  *out = spb::registry().add(std::move(d));
+  return SP_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+const char *sp_status_string(sp_status s) {
+  switch (s) {
+  case SP_OK: return "ok";
+  case SP_ERR_INVALID_ARGUMENT: return "InvalidArgument";
+  case SP_ERR_UNSUPPORTED_ORDER: return "UnsupportedOrder";
+  case SP_ERR_INVALID_LAYOUT: return "InvalidLayout";
+  case SP_ERR_BUFFER_TOO_SMALL: return "BufferTooSmall";
+  case SP_ERR_OVERLAPPING_LAYOUT: return "OverlappingLayout";
+  case SP_ERR_UNSUPPORTED: return "Unsupported";
+  case SP_ERR_EMPTY_PROFILE: return "EmptyProfile";
+  case SP_ERR_PARSE: return "ParseError";
+  case SP_ERR_INTERNAL: return "InternalError";
+  case SP_ERR_INVALID_HANDLE: return "InvalidHandle";
+  case SP_ERR_CUDA: return "CudaError";
+  case SP_ERR_NO_DEVICE: return "NoDevice";
+  default: return "unknown";
+  }
+}
+
+const char *sp_last_error(void) { return t_err.c_str(); }
+
+sp_status sp_type_named(int kind, sp_type *out) {
+  return guard([&] { add(spb::make_named(kind), out); });
+}
+
+sp_status sp_type_contiguous(int64_t count, sp_type inner, sp_type *out) {
+  return guard([&] { add(spb::make_contiguous(count, def_of(inner)), out); });
+}
+
+sp_status sp_type_vector(int64_t count, int64_t blocklength, int64_t stride, sp_type inner, sp_type *out) {
+  return guard([&] { add(spb::make_vector(count, blocklength, stride, def_of(inner)), out); });
+}
+
+sp_status sp_type_hvector(int64_t count, int64_t blocklength, int64_t stride_bytes, sp_type inner,
+                          sp_type *out) {
+  return guard([&] { add(spb::make_hvector(count, blocklength, stride_bytes, def_of(inner)), out); });
+}
+
+sp_status sp_type_subarray(int64_t ndims, const int64_t *sizes, const int64_t *subsizes,
+                           const int64_t *offsets, sp_type inner, int order, sp_type *out) {
+  return guard([&] { add(spb::make_subarray(ndims, sizes, subsizes, offsets, def_of(inner), order), out); });
+}
+
+sp_status sp_type_free(sp_type t) {
+  return guard([&] { spb::registry().remove(t); });
+}
+
+sp_status sp_type_size(sp_type t, int64_t *size) {
+  return guard([&] {
+    if (!size) spb::fail(SP_ERR_INVALID_ARGUMENT, "null output");
+    *size = def_of(t)->size;
+  });
+}
+
+sp_status sp_type_extent(sp_type t, int64_t *extent) {
+  return guard([&] {
+    if (!extent) spb::fail(SP_ERR_INVALID_ARGUMENT, "null output");
+    *extent = def_of(t)->extent;
+  });
+}
+
+sp_status sp_type_commit(sp_type t) {
+  return guard([&] { spb::registry().commit(t); });
+}
+
+sp_status sp_type_query(sp_type t, sp_type_info *info, int64_t *counts, int64_t *strides, int64_t cap) {
+  return guard([&] {
+    if (!info) spb::fail(SP_ERR_INVALID_ARGUMENT, "null info");
+    const spb::Entry e = spb::registry().get(t);
+    if (!e.committed) spb::fail(SP_ERR_INVALID_ARGUMENT, "type is not committed");
+    const spb::Committed &c = *e.committed;
+    std::memset(info, 0, sizeof(*info));
+    info->form = c.form;
+    info->size = c.size;
+    info->extent = c.extent;
+    info->span = c.span;
+    info->overlapping = c.overlapping;
+    info->simplify_rounds = c.simplify_rounds;
+    info->n_fallback_runs = c.n_def_runs;
+    if (c.form == SP_FORM_STRIDED) {
+      info->ndims = c.sb.ndims();
+      info->start = c.sb.start;
+      info->word = c.plan.word;
+      for (int d = 0; d < 3; ++d) {
+        info->block[d] = c.plan.block[d];
+        info->grid[d] = c.plan.grid[d];
+      }
+      info->strategy = c.plan.strategy;
+      if (counts && strides && cap >= info->ndims) {
+        for (int d = 0; d < c.sb.ndims(); ++d) {
+          counts[d] = c.sb.counts[d];
+          strides[d] = c.sb.strides[d];
+        }
+      }
+    }
+  });
+}
+
+static sp_status pack_impl(bool pack, const void *src, uint64_t src_bytes, sp_type t, int64_t count, void *dst,
+                           uint64_t dst_bytes, int64_t *position, void *stream, const sp_pack_options *opt) {
+  return guard([&] {
+    if (!position) spb::fail(SP_ERR_INVALID_ARGUMENT, "null position");
+    const spb::Entry e = spb::registry().get(t);
+    if (!e.committed) spb::fail(SP_ERR_INVALID_ARGUMENT, "type is not committed");
+    spb::PackArgs a{};
+    a.ct = e.committed.get();
+    a.src = src;
+    a.src_bytes = src_bytes;
+    a.dst = dst;
+    a.dst_bytes = dst_bytes;
+    a.count = count;
+    a.position = *position;
+    a.stream = stream;
+    a.opt = opt ? *opt : sp_pack_options{1, SP_KERNEL_AUTO, 0};
+    a.pack = pack;
+    *position = spb::execute(a);
+  });
+}
+
+sp_status sp_pack(const void *src, uint64_t src_bytes, sp_type t, int64_t incount, void *dst, uint64_t dst_bytes,
+                  int64_t *position, void *stream) {
+  return pack_impl(true, src, src_bytes, t, incount, dst, dst_bytes, position, stream, nullptr);
+}
+
+sp_status sp_unpack(const void *src, uint64_t src_bytes, int64_t *position, sp_type t, int64_t outcount, void *dst,
+                    uint64_t dst_bytes, void *stream) {
+  return pack_impl(false, src, src_bytes, t, outcount, dst, dst_bytes, position, stream, nullptr);
+}
+
+sp_status sp_pack_ex(const void *src, uint64_t src_bytes, sp_type t, int64_t incount, void *dst, uint64_t dst_bytes,
+                     int64_t *position, void *stream, const sp_pack_options *opt) {
+  return pack_impl(true, src, src_bytes, t, incount, dst, dst_bytes, position, stream, opt);
+}
+
+sp_status sp_unpack_ex(const void *src, uint64_t src_bytes, int64_t *position, sp_type t, int64_t outcount,
+                       void *dst, uint64_t dst_bytes, void *stream, const sp_pack_options *opt) {
+  return pack_impl(false, src, src_bytes, t, outcount, dst, dst_bytes, position, stream, opt);
+}
+
+} // extern "C"

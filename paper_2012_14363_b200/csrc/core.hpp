@@ -1,0 +1,147 @@
+// core.hpp -- host-side datatype engine (internal).
+//
+// The B200 engine keeps the reference's semantics (canonical StridedBlock,
+// reference PackPlan, pack byte order, error precedence) but not its
+// structure: definitions carry size/extent/span computed once at
+// construction (O(1) per level), the IR chain is a flat vector rewritten in
+// place, and overlap is decided exactly from the StridedBlock lattice instead
+// of enumerating and sorting every byte run (commit.hpp:57 in the reference
+// is O(size log size); here commit is O(tree) + a bounded search).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <shared_mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "stridepack_b200.h"
+
+namespace spb {
+
+// ---------------------------------------------------------------- errors
+struct Error {
+  sp_status code;
+  std::string msg;
+};
+[[noreturn]] void fail(sp_status code, std::string msg);
+
+// ---------------------------------------------------------------- types
+enum class Kind : uint8_t { Named, Contiguous, Vector, Hvector, Subarray };
+
+// One definition level (type_def.hpp:52-123). Immutable once built.
+struct TypeDef {
+  Kind kind = Kind::Named;
+  int named = 0;            // SP_BYTE..SP_DOUBLE
+  int64_t count = 0;        // contiguous/vector/hvector count
+  int64_t blocklength = 0;  // vector/hvector
+  int64_t stride = 0;       // vector: inner extents; hvector: bytes
+  std::vector<int64_t> sizes, subsizes, offsets; // subarray, dim 0 innermost
+  std::shared_ptr<const TypeDef> inner;
+  // derived once (type_def.hpp:198-250 + block_list span)
+  int64_t size = 0, extent = 0, span = 0;
+  int depth = 1;
+};
+using DefPtr = std::shared_ptr<const TypeDef>;
+
+DefPtr make_named(int kind);
+DefPtr make_contiguous(int64_t count, DefPtr inner);
+DefPtr make_vector(int64_t count, int64_t bl, int64_t stride, DefPtr inner);
+DefPtr make_hvector(int64_t count, int64_t bl, int64_t stride_b, DefPtr inner);
+DefPtr make_subarray(int64_t ndims, const int64_t *sizes,
+                     const int64_t *subsizes, const int64_t *offsets,
+                     DefPtr inner, int order);
+
+// ---------------------------------------------------------------- canon
+// Canonical strided form (strided_block.hpp:17-46): counts[0] bytes at
+// stride 1, counts[i>0] repetitions at strides[i] (non-decreasing).
+struct StridedBlock {
+  int64_t start = 0;
+  std::vector<int64_t> counts, strides;
+  int ndims() const { return static_cast<int>(counts.size()); }
+};
+
+// The reference's descriptive plan (plan.hpp:27-44), kept for parity.
+struct RefPlan {
+  int64_t word = 1;
+  int64_t block[3] = {1, 1, 1};
+  int64_t grid[3] = {1, 1, 1};
+  int strategy = SP_STRATEGY_GRIDZ;
+};
+
+struct Run {
+  int64_t off, len;
+};
+
+// Device copy of the definition-order run table for the block-list kernel.
+struct DeviceRuns {
+  int device = -1;
+  int64_t *d_src = nullptr;   // run source offsets (within one object)
+  int64_t *d_dst = nullptr;   // exclusive prefix sum of lengths
+  int64_t *d_len = nullptr;
+  int64_t n = 0;
+};
+
+struct Committed {
+  int form = SP_FORM_EMPTY;
+  int64_t size = 0, extent = 0, span = 0;
+  bool overlapping = false;
+  StridedBlock sb;        // valid when form == STRIDED
+  RefPlan plan;           // valid when form == STRIDED
+  int64_t simplify_rounds = -1;
+  int64_t n_def_runs = 0; // reference fallback_runs.size() (Unsupported)
+  std::vector<Run> runs;  // definition-order runs, adjacent runs coalesced
+                          // (Unsupported form only; multiplicity preserved)
+  mutable std::mutex dev_mu;
+  mutable DeviceRuns dev; // lazily uploaded block list
+  ~Committed();
+};
+using CommitPtr = std::shared_ptr<const Committed>;
+
+// translate + simplify + lower + plan + exact overlap (commit.hpp:51-79)
+CommitPtr commit_def(const TypeDef &def);
+
+// exposed for tests via the C-ABI: exact injectivity of a strided block
+bool strided_overlaps(const StridedBlock &sb);
+
+// ---------------------------------------------------------------- registry
+struct Entry {
+  DefPtr def;
+  CommitPtr committed; // null until sp_type_commit
+};
+
+class Registry {
+public:
+  sp_type add(DefPtr def);
+  Entry get(sp_type h) const;  // copy of the entry, fails on bad handle
+  CommitPtr commit(sp_type h);
+  void remove(sp_type h);
+
+private:
+  mutable std::shared_mutex mu_;
+  std::unordered_map<sp_type, Entry> map_;
+  sp_type next_ = 1;
+};
+Registry &registry();
+
+// ---------------------------------------------------------------- execution
+struct PackArgs {
+  const Committed *ct;
+  const void *src;
+  uint64_t src_bytes;
+  void *dst;
+  uint64_t dst_bytes;
+  int64_t count;    // incount / outcount
+  int64_t position; // byte offset into the packed buffer
+  void *stream;
+  sp_pack_options opt;
+  bool pack;        // true: gather (pack), false: scatter (unpack)
+};
+// validated launch (pack.cu); returns new position
+int64_t execute(const PackArgs &a);
+
+void set_last_launch(const sp_launch_info &li);
+
+} // namespace spb

@@ -1,0 +1,729 @@
+// pack.cu -- sm_100a pack/unpack kernels and their launcher.
+//
+// The reference executes a committed StridedBlock on the host
+// (pack.hpp:47-60 walk_words: object-major, dimension 1 fastest, one
+// memcpy of `word` bytes at a time). On B200 the same byte order is produced
+// by kernels that see the object as ROWS of c0 = counts[0] bytes:
+//
+//   packed[pos + R*c0 + b] = strided[start + sum_k i_k * str_k + b]
+//
+// where R enumerates the row multi-index (i_0 fastest) and the object count
+// is just one more row dimension with stride = extent. Row dimensions that
+// are contiguous in row order are merged on the host, so a kernel only ever
+// walks the irreducible geometry.
+//
+// Kernels:
+//   k_words<W,PACK>    one W-byte word per work item; consecutive lanes own
+//                      consecutive packed words, so the packed side is fully
+//                      coalesced and the strided side is coalesced within a
+//                      row. Index math is fast-divmod (mul-hi), no division.
+//   k_smallrow<C0,PACK> rows of 1/2/4/8 bytes: each lane assembles 16/C0
+//                      rows into one 16-byte packed word (one STG.128 per
+//                      lane, or one LDG.128 for unpack) and walks the rows by
+//                      carry-increment instead of re-dividing.
+//   k_blocklist<PACK>  definition-order run table on the device, for forms
+//                      without a strided canon (zero-stride "Unsupported"
+//                      types) or with more row dims than a kernel carries.
+// W is the largest power of two <= 16 dividing the row length, every row
+// stride, and BOTH buffer addresses (the reference's select_word_size,
+// plan.hpp:47-64, plus the address alignment a GPU load needs).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <string>
+
+#include "core.hpp"
+
+namespace spb {
+
+static std::atomic<int64_t> g_launches{0};
+static thread_local sp_launch_info t_last{};
+
+void set_last_launch(const sp_launch_info &li) { t_last = li; }
+
+static void cuda_check(cudaError_t e, const char *what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(SP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+// ------------------------------------------------------------ fast divmod
+// Granlund-Montgomery round-up division for runtime-invariant divisors.
+struct FastDiv {
+  uint32_t d = 1, m = 1, s1 = 0, s2 = 0;
+};
+
+static FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  int l = 0;
+  while ((uint64_t{1} << l) < d) ++l;
+  f.m = static_cast<uint32_t>(((uint64_t{1} << 32) * ((uint64_t{1} << l) - d)) / d + 1);
+  f.s1 = l > 0 ? 1 : 0;
+  f.s2 = l > 0 ? l - 1 : 0;
+  return f;
+}
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f) {
+  const uint32_t t = __umulhi(f.m, n);
+  return (t + ((n - t) >> f.s1)) >> f.s2;
+}
+
+// ------------------------------------------------------------ geometry
+constexpr int KMAX = 12; // row dims a kernel carries (incl. the object dim)
+
+struct Geom {
+  int nd;             // row dims
+  uint32_t wpr;       // words per row (c0 / W)
+  FastDiv wdiv;       // divides by wpr
+  uint32_t cnt[KMAX]; // row-dim counts, dim 0 fastest
+  FastDiv div[KMAX];
+  int64_t str[KMAX];  // row-dim byte strides on the strided side
+  int64_t back[KMAX]; // cnt[k]*str[k], for carry-increment walks
+  uint64_t total;     // work items (words, or 16-B chunks for smallrow)
+  uint64_t rows;      // total rows
+  // smallrow only: packed-side 16-byte grid
+  uint64_t head;      // bytes before the first 16-B aligned packed address
+};
+
+// strided-side byte offset of row r (r < rows)
+__device__ __forceinline__ int64_t row_offset(uint32_t r, const Geom &g) {
+  int64_t off = 0;
+#pragma unroll 1
+  for (int k = 0; k < g.nd - 1; ++k) {
+    const uint32_t q = fdiv(r, g.div[k]);
+    off += static_cast<int64_t>(r - q * g.cnt[k]) * g.str[k];
+    r = q;
+  }
+  if (g.nd > 0) off += static_cast<int64_t>(r) * g.str[g.nd - 1];
+  return off;
+}
+
+template <int W> struct Word;
+template <> struct Word<1> { using T = uint8_t; };
+template <> struct Word<2> { using T = uint16_t; };
+template <> struct Word<4> { using T = uint32_t; };
+template <> struct Word<8> { using T = uint2; };
+template <> struct Word<16> { using T = uint4; };
+
+// streaming loads/stores: every byte is touched once, keep it out of L1
+template <class T> __device__ __forceinline__ T ld_stream(const T *p) { return __ldcs(p); }
+template <> __device__ __forceinline__ uint8_t ld_stream(const uint8_t *p) {
+  return static_cast<uint8_t>(__ldcs(reinterpret_cast<const char *>(p)));
+}
+template <> __device__ __forceinline__ uint16_t ld_stream(const uint16_t *p) {
+  return static_cast<uint16_t>(__ldcs(reinterpret_cast<const unsigned short *>(p)));
+}
+template <class T> __device__ __forceinline__ void st_stream(T *p, T v) { __stcs(p, v); }
+template <> __device__ __forceinline__ void st_stream(uint8_t *p, uint8_t v) {
+  __stcs(reinterpret_cast<char *>(p), static_cast<char>(v));
+}
+template <> __device__ __forceinline__ void st_stream(uint16_t *p, uint16_t v) {
+  __stcs(reinterpret_cast<unsigned short *>(p), static_cast<unsigned short>(v));
+}
+
+// ------------------------------------------------------------ k_words
+// strided: base of the strided side (already offset by start)
+// packed:  base of the packed side (already offset by position)
+template <int W, bool PACK, int U>
+__global__ void __launch_bounds__(256) k_words(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
+                                               const Geom g) {
+  using T = typename Word<W>::T;
+  const uint32_t total = static_cast<uint32_t>(g.total);
+  const uint32_t step = gridDim.x * blockDim.x * U;
+  for (uint32_t base = blockIdx.x * blockDim.x * U + threadIdx.x; base < total; base += step) {
+    T v[U];
+    int64_t soff[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t q = base + u * blockDim.x;
+      if (q < total) {
+        const uint32_t row = fdiv(q, g.wdiv);
+        const uint32_t col = q - row * g.wpr;
+        soff[u] = row_offset(row, g) + static_cast<int64_t>(col) * W;
+        if (PACK) {
+          v[u] = ld_stream(reinterpret_cast<const T *>(in + soff[u]));
+        } else {
+          v[u] = ld_stream(reinterpret_cast<const T *>(in) + q);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t q = base + u * blockDim.x;
+      if (q < total) {
+        if (PACK) {
+          st_stream(reinterpret_cast<T *>(out) + q, v[u]);
+        } else {
+          st_stream(reinterpret_cast<T *>(out + soff[u]), v[u]);
+        }
+      }
+    }
+  }
+}
+
+// 64-bit fallback for > 4 Gi words or > 4 Gi rows (plain division; rare)
+template <int W, bool PACK>
+__global__ void __launch_bounds__(256) k_words64(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
+                                                 const Geom g, const uint64_t *cnt64) {
+  using T = typename Word<W>::T;
+  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < g.total; q += step) {
+    uint64_t row = q / g.wpr;
+    const uint64_t col = q - row * g.wpr;
+    int64_t off = static_cast<int64_t>(col) * W;
+    for (int k = 0; k < g.nd; ++k) {
+      const uint64_t c = cnt64[k];
+      const uint64_t i = (k == g.nd - 1) ? row : row % c;
+      off += static_cast<int64_t>(i) * g.str[k];
+      row = (k == g.nd - 1) ? 0 : row / c;
+    }
+    if (PACK) {
+      st_stream(reinterpret_cast<T *>(out) + q, ld_stream(reinterpret_cast<const T *>(in + off)));
+    } else {
+      st_stream(reinterpret_cast<T *>(out + off), ld_stream(reinterpret_cast<const T *>(in) + q));
+    }
+  }
+}
+
+// ------------------------------------------------------------ k_smallrow
+// Packed side seen as 16-byte aligned chunks; chunk t covers packed bytes
+// [16t - head, 16t - head + 16). Rows are C0 bytes and C0-aligned on both
+// sides, so a row never straddles a chunk. Interior chunks move with one
+// 16-byte access on the packed side; the (at most two) edge chunks fall back
+// to per-row C0-byte accesses.
+template <int C0, bool PACK>
+__global__ void __launch_bounds__(256) k_smallrow(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
+                                                  const Geom g) {
+  using T = typename Word<C0>::T;
+  constexpr int R = 16 / C0;
+  const uint32_t nchunks = static_cast<uint32_t>(g.total);
+  const uint32_t rows = static_cast<uint32_t>(g.rows);
+  const uint32_t head_rows = static_cast<uint32_t>(g.head / C0);
+  const uint32_t step = gridDim.x * blockDim.x;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nchunks; t += step) {
+    // rows [r0, r1) live in this chunk
+    const int64_t first = static_cast<int64_t>(t) * R - head_rows;
+    const uint32_t r0 = first < 0 ? 0u : static_cast<uint32_t>(first);
+    const int64_t lastrow = first + R < static_cast<int64_t>(rows) ? first + R : static_cast<int64_t>(rows);
+    const uint32_t r1 = static_cast<uint32_t>(lastrow);
+    if (r0 >= r1) continue;
+    // decompose r0 once, then carry-increment
+    uint32_t idx[KMAX];
+    int64_t off = 0;
+    {
+      uint32_t r = r0;
+      for (int k = 0; k < g.nd - 1; ++k) {
+        const uint32_t q = fdiv(r, g.div[k]);
+        idx[k] = r - q * g.cnt[k];
+        off += static_cast<int64_t>(idx[k]) * g.str[k];
+        r = q;
+      }
+      if (g.nd > 0) {
+        idx[g.nd - 1] = r;
+        off += static_cast<int64_t>(r) * g.str[g.nd - 1];
+      }
+    }
+    auto advance = [&]() {
+      for (int k = 0; k < g.nd; ++k) {
+        off += g.str[k];
+        if (++idx[k] < g.cnt[k] || k == g.nd - 1) return;
+        idx[k] = 0;
+        off -= g.back[k];
+      }
+    };
+    const bool full = (first >= 0) && (r1 - r0 == R);
+    if (full) {
+      union {
+        uint4 v;
+        T e[R];
+      } buf;
+      if (PACK) {
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          buf.e[j] = ld_stream(reinterpret_cast<const T *>(in + off));
+          if (j + 1 < R) advance();
+        }
+        st_stream(reinterpret_cast<uint4 *>(out + static_cast<int64_t>(r0) * C0), buf.v);
+      } else {
+        buf.v = ld_stream(reinterpret_cast<const uint4 *>(in + static_cast<int64_t>(r0) * C0));
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          st_stream(reinterpret_cast<T *>(out + off), buf.e[j]);
+          if (j + 1 < R) advance();
+        }
+      }
+    } else {
+      for (uint32_t r = r0; r < r1; ++r) {
+        if (PACK) {
+          st_stream(reinterpret_cast<T *>(out + static_cast<int64_t>(r) * C0),
+                    ld_stream(reinterpret_cast<const T *>(in + off)));
+        } else {
+          st_stream(reinterpret_cast<T *>(out + off),
+                    ld_stream(reinterpret_cast<const T *>(in + static_cast<int64_t>(r) * C0)));
+        }
+        if (r + 1 < r1) advance();
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ k_blocklist
+// One thread per (object, run): byte loop over the run. Used only for
+// definition-order gathers (Unsupported forms, pack.hpp:123-135) and for
+// strided forms with more row dimensions than KMAX.
+template <bool PACK>
+__global__ void __launch_bounds__(256) k_blocklist(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
+                                                   const int64_t *__restrict__ rsrc,
+                                                   const int64_t *__restrict__ rdst,
+                                                   const int64_t *__restrict__ rlen, int64_t nruns,
+                                                   int64_t nobj, int64_t extent, int64_t size) {
+  const int64_t total = nruns * nobj;
+  const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += step) {
+    const int64_t j = t / nruns, k = t - j * nruns;
+    const int64_t so = j * extent + rsrc[k], po = j * size + rdst[k], n = rlen[k];
+    for (int64_t b = 0; b < n; ++b) {
+      if (PACK) {
+        out[po + b] = in[so + b];
+      } else {
+        out[so + b] = in[po + b];
+      }
+    }
+  }
+}
+
+// ============================================================ host side
+
+Committed::~Committed() {
+  if (dev.d_src) {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (dev.device >= 0) cudaSetDevice(dev.device);
+    cudaFree(dev.d_src);
+    cudaFree(dev.d_dst);
+    cudaFree(dev.d_len);
+    if (cur >= 0) cudaSetDevice(cur);
+  }
+}
+
+namespace {
+
+struct RowDims {
+  int64_t c0 = 0;
+  std::vector<int64_t> cnt, str; // dim 0 fastest
+};
+
+// Row geometry of `count` objects; contiguous-in-row-order dims merged.
+RowDims row_dims(const Committed &ct, int64_t count) {
+  RowDims r;
+  const StridedBlock &sb = ct.sb;
+  r.c0 = sb.counts[0];
+  std::vector<std::pair<int64_t, int64_t>> dims;
+  for (int d = 1; d < sb.ndims(); ++d) dims.emplace_back(sb.counts[d], sb.strides[d]);
+  dims.emplace_back(count, ct.extent);
+  for (auto &[c, s] : dims) {
+    if (c == 1) continue;
+    if (r.cnt.empty() && s == r.c0) { // rows abut: one longer row
+      r.c0 *= c;
+      continue;
+    }
+    if (!r.cnt.empty() && s == r.cnt.back() * r.str.back()) {
+      r.cnt.back() *= c;
+      continue;
+    }
+    r.cnt.push_back(c);
+    r.str.push_back(s);
+  }
+  return r;
+}
+
+int pow2_align(uint64_t v) {
+  int w = 16;
+  while (w > 1 && (v % static_cast<uint64_t>(w))) w >>= 1;
+  return w;
+}
+
+enum class MemKind { Device, Pinned, Pageable };
+
+struct Resolved {
+  MemKind kind;
+  uint8_t *dptr; // device-accessible address (for Device/Pinned)
+};
+
+Resolved resolve(const void *p) {
+  cudaPointerAttributes at{};
+  const cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return {MemKind::Pageable, nullptr};
+  }
+  switch (at.type) {
+  case cudaMemoryTypeDevice:
+  case cudaMemoryTypeManaged:
+    return {MemKind::Device, static_cast<uint8_t *>(const_cast<void *>(p))};
+  case cudaMemoryTypeHost:
+    return {MemKind::Pinned, static_cast<uint8_t *>(at.devicePointer)};
+  default:
+    return {MemKind::Pageable, nullptr};
+  }
+}
+
+int sm_count() {
+  static thread_local int dev = -1, sms = 148;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != dev) {
+    dev = cur;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+unsigned grid_for(uint64_t items, int per_thread) {
+  const uint64_t blocks = (items + 256ull * per_thread - 1) / (256ull * per_thread);
+  const uint64_t cap = static_cast<uint64_t>(sm_count()) * 8; // 8 x 256 = 2048 threads/SM
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min(blocks, cap)));
+}
+
+template <int W, bool PACK>
+void launch_words(const uint8_t *in, uint8_t *out, const Geom &g, cudaStream_t s, sp_launch_info &li) {
+  const bool big = g.total >= static_cast<uint64_t>(sm_count()) * 2048 * 4;
+  unsigned grid = grid_for(g.total, big ? 4 : 1);
+  if (big) {
+    k_words<W, PACK, 4><<<grid, 256, 0, s>>>(in, out, g);
+  } else {
+    k_words<W, PACK, 1><<<grid, 256, 0, s>>>(in, out, g);
+  }
+  li.grid = grid;
+  li.block = 256;
+}
+
+template <bool PACK>
+void dispatch_words(int w, const uint8_t *in, uint8_t *out, const Geom &g, cudaStream_t s, sp_launch_info &li) {
+  switch (w) {
+  case 16: launch_words<16, PACK>(in, out, g, s, li); break;
+  case 8: launch_words<8, PACK>(in, out, g, s, li); break;
+  case 4: launch_words<4, PACK>(in, out, g, s, li); break;
+  case 2: launch_words<2, PACK>(in, out, g, s, li); break;
+  default: launch_words<1, PACK>(in, out, g, s, li); break;
+  }
+}
+
+template <bool PACK>
+void dispatch_smallrow(int c0, const uint8_t *in, uint8_t *out, const Geom &g, cudaStream_t s,
+                       sp_launch_info &li) {
+  const unsigned grid = grid_for(g.total, 1);
+  switch (c0) {
+  case 1: k_smallrow<1, PACK><<<grid, 256, 0, s>>>(in, out, g); break;
+  case 2: k_smallrow<2, PACK><<<grid, 256, 0, s>>>(in, out, g); break;
+  case 4: k_smallrow<4, PACK><<<grid, 256, 0, s>>>(in, out, g); break;
+  default: k_smallrow<8, PACK><<<grid, 256, 0, s>>>(in, out, g); break;
+  }
+  li.grid = grid;
+  li.block = 256;
+}
+
+template <bool PACK>
+void dispatch_words64(int w, const uint8_t *in, uint8_t *out, const Geom &g, const uint64_t *cnt64,
+                      cudaStream_t s, sp_launch_info &li) {
+  const unsigned grid = grid_for(g.total, 1);
+  switch (w) {
+  case 16: k_words64<16, PACK><<<grid, 256, 0, s>>>(in, out, g, cnt64); break;
+  case 8: k_words64<8, PACK><<<grid, 256, 0, s>>>(in, out, g, cnt64); break;
+  case 4: k_words64<4, PACK><<<grid, 256, 0, s>>>(in, out, g, cnt64); break;
+  case 2: k_words64<2, PACK><<<grid, 256, 0, s>>>(in, out, g, cnt64); break;
+  default: k_words64<1, PACK><<<grid, 256, 0, s>>>(in, out, g, cnt64); break;
+  }
+  li.grid = grid;
+  li.block = 256;
+}
+
+// upload the run table of a committed type to the current device (cached)
+const DeviceRuns &device_runs(const Committed &ct, const std::vector<Run> &runs) {
+  std::lock_guard<std::mutex> lk(ct.dev_mu);
+  int cur = 0;
+  cuda_check(cudaGetDevice(&cur), "cudaGetDevice");
+  if (ct.dev.d_src && ct.dev.device == cur) return ct.dev;
+  if (ct.dev.d_src) {
+    cudaFree(ct.dev.d_src);
+    cudaFree(ct.dev.d_dst);
+    cudaFree(ct.dev.d_len);
+    ct.dev = DeviceRuns{};
+  }
+  const size_t n = runs.size();
+  std::vector<int64_t> hs(n), hd(n), hl(n);
+  int64_t acc = 0;
+  for (size_t k = 0; k < n; ++k) {
+    hs[k] = runs[k].off;
+    hd[k] = acc;
+    hl[k] = runs[k].len;
+    acc += runs[k].len;
+  }
+  DeviceRuns d;
+  d.device = cur;
+  d.n = static_cast<int64_t>(n);
+  const size_t bytes = std::max<size_t>(n, 1) * sizeof(int64_t);
+  cuda_check(cudaMalloc(&d.d_src, bytes), "cudaMalloc(runs)");
+  cuda_check(cudaMalloc(&d.d_dst, bytes), "cudaMalloc(runs)");
+  cuda_check(cudaMalloc(&d.d_len, bytes), "cudaMalloc(runs)");
+  cuda_check(cudaMemcpy(d.d_src, hs.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice), "upload runs");
+  cuda_check(cudaMemcpy(d.d_dst, hd.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice), "upload runs");
+  cuda_check(cudaMemcpy(d.d_len, hl.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice), "upload runs");
+  ct.dev = d;
+  return ct.dev;
+}
+
+// runs of a strided form, for row geometries too deep for the kernels
+std::vector<Run> strided_runs(const StridedBlock &sb) {
+  std::vector<Run> out;
+  std::vector<int64_t> idx(sb.ndims(), 0);
+  for (;;) {
+    int64_t off = sb.start;
+    for (int d = 1; d < sb.ndims(); ++d) off += idx[d] * sb.strides[d];
+    out.push_back({off, sb.counts[0]});
+    int d = 1;
+    while (d < sb.ndims() && ++idx[d] == sb.counts[d]) idx[d++] = 0;
+    if (d >= sb.ndims()) break;
+  }
+  return out;
+}
+
+// Launch on device-accessible pointers. strided: object base (no start);
+// packed: packed buffer base + position.
+void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8_t *strided_out,
+            const uint8_t *packed_in, uint8_t *packed_out, bool pack, cudaStream_t s,
+            const sp_pack_options &opt, sp_launch_info &li) {
+  const uint8_t *in = pack ? strided_in : packed_in;
+  uint8_t *out = pack ? packed_out : strided_out;
+  const uint64_t strided_addr = reinterpret_cast<uint64_t>(pack ? strided_in : strided_out);
+  const uint64_t packed_addr = reinterpret_cast<uint64_t>(pack ? packed_out : packed_in);
+
+  bool blocklist = ct.form != SP_FORM_STRIDED || opt.kernel == SP_KERNEL_BLOCKLIST;
+  RowDims rd;
+  if (!blocklist) {
+    rd = row_dims(ct, count);
+    if (static_cast<int>(rd.cnt.size()) > KMAX) blocklist = true;
+  }
+  if (blocklist) {
+    std::vector<Run> tmp;
+    const std::vector<Run> *runs = &ct.runs;
+    if (ct.form == SP_FORM_STRIDED) {
+      tmp = strided_runs(ct.sb);
+      runs = &tmp;
+    }
+    const DeviceRuns &dr = device_runs(ct, *runs);
+    const unsigned grid = grid_for(static_cast<uint64_t>(dr.n * count), 1);
+    if (pack) {
+      k_blocklist<true><<<grid, 256, 0, s>>>(in, out, dr.d_src, dr.d_dst, dr.d_len, dr.n, count, ct.extent,
+                                             ct.size);
+    } else {
+      k_blocklist<false><<<grid, 256, 0, s>>>(in, out, dr.d_src, dr.d_dst, dr.d_len, dr.n, count,
+                                              ct.extent, ct.size);
+    }
+    cuda_check(cudaGetLastError(), "k_blocklist launch");
+    li.kernel = SP_KERNEL_BLOCKLIST;
+    li.word = 1;
+    li.launches = 1;
+    li.grid = grid;
+    li.block = 256;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return;
+  }
+
+  // alignment-derived word
+  uint64_t g_or = static_cast<uint64_t>(rd.c0) | (strided_addr + ct.sb.start) | packed_addr;
+  for (int64_t st : rd.str) g_or |= static_cast<uint64_t>(st);
+  int w = pow2_align(g_or);
+  if (opt.force_word) {
+    if (opt.force_word > w || (opt.force_word & (opt.force_word - 1)))
+      fail(SP_ERR_INVALID_ARGUMENT, "force_word is not legal for these buffers");
+    w = opt.force_word;
+  }
+  // strided side offset by the StridedBlock start
+  const uint8_t *sin = pack ? in + ct.sb.start : in;
+  uint8_t *sout = pack ? out : out + ct.sb.start;
+
+  uint64_t rows = 1;
+  for (int64_t c : rd.cnt) rows *= static_cast<uint64_t>(c);
+  const uint64_t total_bytes = rows * static_cast<uint64_t>(rd.c0);
+
+  Geom g{};
+  g.nd = static_cast<int>(rd.cnt.size());
+  bool fits32 = rows < (1ull << 32) && total_bytes / static_cast<uint64_t>(w) < (1ull << 32);
+  for (int k = 0; k < g.nd; ++k) {
+    fits32 = fits32 && rd.cnt[k] < (int64_t{1} << 32);
+    g.str[k] = rd.str[k];
+    g.back[k] = rd.cnt[k] * rd.str[k];
+  }
+  g.rows = rows;
+
+  const bool smallrow_ok = (rd.c0 == 1 || rd.c0 == 2 || rd.c0 == 4 || rd.c0 == 8) && w >= rd.c0 && fits32;
+  int kernel = opt.kernel;
+  if (kernel == SP_KERNEL_AUTO) kernel = smallrow_ok && !opt.force_word ? SP_KERNEL_SMALLROW : SP_KERNEL_WORDS;
+  if (!fits32 || kernel == SP_KERNEL_WORDS64) {
+    fits32 = false;
+    kernel = SP_KERNEL_WORDS64;
+  }
+  if (kernel == SP_KERNEL_SMALLROW && !smallrow_ok) fail(SP_ERR_INVALID_ARGUMENT, "smallrow kernel not applicable");
+  if (kernel == SP_KERNEL_TMA) fail(SP_ERR_UNSUPPORTED, "TMA kernel not built in this configuration");
+
+  if (fits32) {
+    for (int k = 0; k < g.nd; ++k) {
+      g.cnt[k] = static_cast<uint32_t>(rd.cnt[k]);
+      g.div[k] = make_fastdiv(g.cnt[k]);
+    }
+  }
+  if (kernel == SP_KERNEL_SMALLROW) {
+    // packed side on the 16-byte grid: chunk t spans packed offsets
+    // [16t - head, 16t - head + 16), head = packed address mod 16
+    g.head = packed_addr & 15;
+    g.total = (total_bytes + g.head + 15) / 16;
+    if (pack) {
+      dispatch_smallrow<true>(static_cast<int>(rd.c0), sin, out, g, s, li);
+    } else {
+      dispatch_smallrow<false>(static_cast<int>(rd.c0), in, sout, g, s, li);
+    }
+    li.word = rd.c0;
+  } else if (fits32) {
+    g.wpr = static_cast<uint32_t>(rd.c0 / w);
+    g.wdiv = make_fastdiv(g.wpr);
+    g.total = total_bytes / static_cast<uint64_t>(w);
+    if (pack) {
+      dispatch_words<true>(w, sin, out, g, s, li);
+    } else {
+      dispatch_words<false>(w, in, sout, g, s, li);
+    }
+    li.word = w;
+  } else {
+    g.wpr = static_cast<uint32_t>(std::min<int64_t>(rd.c0 / w, 0xffffffff));
+    if (rd.c0 / w >= (int64_t{1} << 32)) fail(SP_ERR_UNSUPPORTED, "row longer than 64 GiB words");
+    g.total = total_bytes / static_cast<uint64_t>(w);
+    uint64_t *cnt64 = nullptr;
+    cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&cnt64), KMAX * sizeof(uint64_t), s), "cudaMallocAsync");
+    uint64_t hc[KMAX] = {0};
+    for (int k = 0; k < g.nd; ++k) hc[k] = static_cast<uint64_t>(rd.cnt[k]);
+    cuda_check(cudaMemcpyAsync(cnt64, hc, sizeof(hc), cudaMemcpyHostToDevice, s), "cudaMemcpyAsync");
+    if (pack) {
+      dispatch_words64<true>(w, sin, out, g, cnt64, s, li);
+    } else {
+      dispatch_words64<false>(w, in, sout, g, cnt64, s, li);
+    }
+    cuda_check(cudaFreeAsync(cnt64, s), "cudaFreeAsync");
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize"); // hc lifetime
+    li.word = w;
+  }
+  cuda_check(cudaGetLastError(), "pack kernel launch");
+  li.kernel = kernel;
+  li.launches = 1;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void require_device() {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    fail(SP_ERR_NO_DEVICE, "no CUDA device: the B200 kernels are the only execution path");
+  }
+}
+
+} // namespace
+
+// Validation order follows pack.hpp:102-126 / :146-159 exactly.
+int64_t execute(const PackArgs &a) {
+  const Committed &ct = *a.ct;
+  sp_launch_info li{};
+  if (a.pack) {
+    if (a.count < 1 || a.position < 0) fail(SP_ERR_INVALID_ARGUMENT, "pack: incount must be positive, position >= 0");
+    if (static_cast<uint64_t>(a.position + a.count * ct.size) > a.dst_bytes)
+      fail(SP_ERR_BUFFER_TOO_SMALL, "pack: destination too small");
+    if (ct.form == SP_FORM_EMPTY) {
+      set_last_launch(li);
+      return a.position;
+    }
+    if (static_cast<uint64_t>((a.count - 1) * ct.extent + ct.span) > a.src_bytes)
+      fail(SP_ERR_BUFFER_TOO_SMALL, "pack: source too small");
+    if (ct.form == SP_FORM_UNSUPPORTED && !a.opt.allow_fallback)
+      fail(SP_ERR_UNSUPPORTED, "pack: type has no strided form");
+  } else {
+    if (a.count < 1 || a.position < 0) fail(SP_ERR_INVALID_ARGUMENT, "unpack: outcount must be positive, position >= 0");
+    if (ct.overlapping) fail(SP_ERR_OVERLAPPING_LAYOUT, "unpack: layout describes overlapping bytes");
+    if (static_cast<uint64_t>(a.position + a.count * ct.size) > a.src_bytes)
+      fail(SP_ERR_BUFFER_TOO_SMALL, "unpack: source too small");
+    if (ct.form == SP_FORM_EMPTY) {
+      set_last_launch(li);
+      return a.position;
+    }
+    if (static_cast<uint64_t>((a.count - 1) * ct.extent + ct.span) > a.dst_bytes)
+      fail(SP_ERR_BUFFER_TOO_SMALL, "unpack: destination too small");
+    if (ct.form == SP_FORM_UNSUPPORTED && !a.opt.allow_fallback)
+      fail(SP_ERR_UNSUPPORTED, "unpack: type has no strided form");
+  }
+  require_device();
+  cudaStream_t s = static_cast<cudaStream_t>(a.stream);
+  const int64_t strided_len = (a.count - 1) * ct.extent + ct.span;
+  const int64_t packed_len = a.count * ct.size;
+
+  const void *strided_user = a.pack ? a.src : a.dst;
+  const Resolved rs = resolve(strided_user);
+  const Resolved rp = a.pack ? resolve(static_cast<uint8_t *>(a.dst) + a.position)
+                             : resolve(static_cast<const uint8_t *>(a.src) + a.position);
+  uint8_t *strided_dev = rs.dptr;
+  uint8_t *packed_dev = rp.dptr; // already at position
+  uint8_t *scratch_s = nullptr, *scratch_p = nullptr;
+  bool staged = false;
+  if (rs.kind == MemKind::Pageable) {
+    staged = true;
+    cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&scratch_s), static_cast<size_t>(strided_len), s),
+               "cudaMallocAsync(stage)");
+    // pack reads the span; unpack must preserve bytes outside the layout
+    cuda_check(cudaMemcpyAsync(scratch_s, strided_user, static_cast<size_t>(strided_len), cudaMemcpyHostToDevice, s),
+               "stage strided H2D");
+    strided_dev = scratch_s;
+  }
+  if (rp.kind == MemKind::Pageable) {
+    staged = true;
+    cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&scratch_p), static_cast<size_t>(packed_len), s),
+               "cudaMallocAsync(stage)");
+    if (!a.pack)
+      cuda_check(cudaMemcpyAsync(scratch_p, static_cast<const uint8_t *>(a.src) + a.position,
+                                 static_cast<size_t>(packed_len), cudaMemcpyHostToDevice, s),
+                 "stage packed H2D");
+    packed_dev = scratch_p;
+  }
+  if (a.pack) {
+    launch(ct, a.count, strided_dev, nullptr, nullptr, packed_dev, true, s, a.opt, li);
+  } else {
+    launch(ct, a.count, nullptr, strided_dev, packed_dev, nullptr, false, s, a.opt, li);
+  }
+  if (staged) {
+    if (a.pack && scratch_p)
+      cuda_check(cudaMemcpyAsync(static_cast<uint8_t *>(a.dst) + a.position, scratch_p,
+                                 static_cast<size_t>(packed_len), cudaMemcpyDeviceToHost, s),
+                 "stage packed D2H");
+    if (!a.pack && scratch_s)
+      cuda_check(cudaMemcpyAsync(a.dst, scratch_s, static_cast<size_t>(strided_len), cudaMemcpyDeviceToHost, s),
+                 "stage strided D2H");
+    if (scratch_s) cuda_check(cudaFreeAsync(scratch_s, s), "cudaFreeAsync");
+    if (scratch_p) cuda_check(cudaFreeAsync(scratch_p, s), "cudaFreeAsync");
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(stage)");
+  }
+  li.staged = staged;
+  set_last_launch(li);
+  return a.position + packed_len;
+}
+
+} // namespace spb
+
+extern "C" sp_status sp_last_launch(sp_launch_info *out) {
+  if (!out) return SP_ERR_INVALID_ARGUMENT;
+  *out = spb::t_last;
+  return SP_OK;
+}
+
+extern "C" int64_t sp_kernel_launch_count(void) { return spb::g_launches.load(); }
