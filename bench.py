@@ -245,6 +245,15 @@ def run_ours(args):
     src[::4099] = 3  # touch; content is irrelevant to timing (parity is in tests/)
     packed = torch.zeros(K << 20, dtype=torch.uint8, device="cuda")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    flush_sink = torch.empty(1, dtype=torch.int64, device="cuda")
+
+    def flush_l2(i):
+        # write 512 MiB (> 126 MB L2), then read it back: the dirty lines are
+        # written back during the read, outside the timed window, so the
+        # timed kernel starts on a cold, clean L2
+        flush.fill_(i & 0xFF)
+        torch.sum(flush.view(torch.int64), dim=0, out=flush_sink)
+
     types = []
     for e0 in E0S:
         d = sp.from_program(cfg2_prog(e0))
@@ -267,7 +276,7 @@ def run_ours(args):
         evs = []
         for e0, d, ct in types:
             for pack in (True, False):
-                flush.zero_()
+                flush_l2(len(evs))
                 a = torch.cuda.Event(enable_timing=True)
                 b = torch.cuda.Event(enable_timing=True)
                 a.record(stream)
@@ -309,7 +318,12 @@ def run_ours(args):
     sweep = []
     dominant = None
     for e0 in E0S:
-        row = {"E0": e0, "dims": list(cfg2_dims(e0)), "sector_cap": round(2 * e0 / (32 + e0), 3) if e0 < 32 else 1.0}
+        # caps: 32-B-sector model and the measured B200 DRAM
+        # access granularity for isolated rows (128 B per touched line,
+        # profiles/r01_dram_granularity.md)
+        row = {"E0": e0, "dims": list(cfg2_dims(e0)),
+               "sector_cap": round(2 * e0 / (32 + e0), 3) if e0 < 32 else 1.0,
+               "line_cap": round(2 * e0 / (128 + e0), 3) if e0 < 128 else 1.0}
         for pack in (True, False):
             ms = statistics.mean(per[(e0, pack)])
             gbs = bytes_per_kernel / (ms * 1e-3) / 1e9
@@ -368,7 +382,7 @@ def run_ours(args):
         "data": "synthetic",
         "config": {"workload": f"cfg2: MPI_Type_create_subarray 3D, 1 MiB object in 1024^3 B, "
                                f"E0 sweep {E0S[0]}-{E0S[-1]} B, pack+unpack, incount={K} per call",
-                   "incount": K, "l2": "flushed (512 MiB write) before every timed kernel",
+                   "incount": K, "l2": "flushed before every timed kernel (512 MiB write, then read back so the timed kernel sees a cold clean L2)",
                    "parallelism": f"replicas x{world}"},
         "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(gbs / hbm, 4), "traffic": traffic,
@@ -396,7 +410,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--incount", type=int, default=32)
+    ap.add_argument("--incount", type=int, default=64)
     ap.add_argument("--e2e-incount", type=int, default=8)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
