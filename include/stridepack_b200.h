@@ -160,6 +160,53 @@ sp_status sp_last_launch(sp_launch_info *out);
 /* total kernels this library enqueued in this process */
 int64_t sp_kernel_launch_count(void);
 
+/* ---- send-method model: perf_model.hpp / profile_io.hpp ------------- *
+ * A MachineProfile (perf_model.hpp:36-45) holds four transfer curves
+ * (bytes -> seconds) and four pack surfaces ((object, block) -> seconds).
+ * The model (paper Eqs. 1-3) is
+ *   device  = gpu_pack + gpu_gpu + gpu_unpack
+ *   oneshot = host_pack + cpu_cpu + host_unpack
+ *   staged  = gpu_pack + d2h + cpu_cpu + h2d + gpu_unpack
+ * with log-log interpolation clamped at the sampled range. */
+typedef struct sp_profile_s *sp_profile;
+typedef struct sp_model_cache_s *sp_model_cache;
+enum { SP_CURVE_CPU_CPU = 0, SP_CURVE_GPU_GPU = 1, SP_CURVE_D2H = 2, SP_CURVE_H2D = 3 };
+enum { SP_SURF_GPU_PACK = 0, SP_SURF_GPU_UNPACK = 1, SP_SURF_HOST_PACK = 2, SP_SURF_HOST_UNPACK = 3 };
+enum { SP_METHOD_ONESHOT = 0, SP_METHOD_DEVICE = 1, SP_METHOD_STAGED = 2 }; /* MethodChoice perf_model.hpp:46 */
+
+sp_status sp_profile_create(sp_profile *out);
+/* load_profile           profile_io.hpp:88 (text) / :166 (file) */
+sp_status sp_profile_parse(const char *text, sp_profile *out);
+sp_status sp_profile_load(const char *path, sp_profile *out);
+/* save_profile           profile_io.hpp:174; *len = text length; buf may be
+ * NULL to query the size (cap must exceed *len) */
+sp_status sp_profile_save(sp_profile p, const char *header, char *buf,
+                          int64_t cap, int64_t *len);
+sp_status sp_profile_free(sp_profile p);
+sp_status sp_profile_set_curve(sp_profile p, int curve, const double *size,
+                               const double *time, int64_t n);
+/* time is row-major [nobj][nblk] */
+sp_status sp_profile_set_surface(sp_profile p, int surf, const double *object,
+                                 int64_t nobj, const double *block,
+                                 int64_t nblk, const double *time);
+/* interp_1d              perf_model.hpp:113 */
+sp_status sp_interp_1d(sp_profile p, int curve, double size, double *t);
+/* interp_2d              perf_model.hpp:125 */
+sp_status sp_interp_2d(sp_profile p, int surf, double object, double block,
+                       double *t);
+/* t_device/t_oneshot/t_staged  perf_model.hpp:139-159 (NULL outputs ok) */
+sp_status sp_model_times(sp_profile p, int64_t object_size, int64_t block_size,
+                         double *t_device, double *t_oneshot, double *t_staged);
+/* choose_method          perf_model.hpp:163 */
+sp_status sp_choose_method(sp_profile p, int64_t object_size,
+                           int64_t block_size, int *method);
+/* ModelCache             perf_model.hpp:184-229 (the profile must outlive
+ * nothing: the cache keeps its own reference) */
+sp_status sp_model_cache_create(sp_profile p, sp_model_cache *out);
+sp_status sp_model_cache_choose(sp_model_cache c, int64_t object_size,
+                                int64_t block_size, int *method);
+sp_status sp_model_cache_free(sp_model_cache c);
+
 #ifdef __cplusplus
 }
 #endif

@@ -77,3 +77,22 @@ def exported_symbols():
     src = open(hdr).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(sp_[a-z0-9_]+)\s*\(", src)))
+
+# ---- model (perf_model.hpp / profile_io.hpp)
+dbl = C.c_double
+dblp = C.POINTER(C.c_double)
+vp = C.c_void_p
+_sig("sp_profile_create", C.c_int, C.POINTER(vp))
+_sig("sp_profile_parse", C.c_int, C.c_char_p, C.POINTER(vp))
+_sig("sp_profile_load", C.c_int, C.c_char_p, C.POINTER(vp))
+_sig("sp_profile_save", C.c_int, vp, C.c_char_p, C.c_char_p, i64, i64p)
+_sig("sp_profile_free", C.c_int, vp)
+_sig("sp_profile_set_curve", C.c_int, vp, C.c_int, dblp, dblp, i64)
+_sig("sp_profile_set_surface", C.c_int, vp, C.c_int, dblp, i64, dblp, i64, dblp)
+_sig("sp_interp_1d", C.c_int, vp, C.c_int, dbl, dblp)
+_sig("sp_interp_2d", C.c_int, vp, C.c_int, dbl, dbl, dblp)
+_sig("sp_model_times", C.c_int, vp, i64, i64, dblp, dblp, dblp)
+_sig("sp_choose_method", C.c_int, vp, i64, i64, C.POINTER(C.c_int))
+_sig("sp_model_cache_create", C.c_int, vp, C.POINTER(vp))
+_sig("sp_model_cache_choose", C.c_int, vp, i64, i64, C.POINTER(C.c_int))
+_sig("sp_model_cache_free", C.c_int, vp)

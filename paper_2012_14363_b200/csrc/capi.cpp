@@ -39,6 +39,10 @@ sp_status add(spb::DefPtr d, sp_type *out) {
 
 } // namespace
 
+namespace spb {
+void set_last_error(const std::string &msg) { t_err = msg; }
+} // namespace spb
+
 extern "C" {
 
 const char *sp_status_string(sp_status s) {

@@ -27,6 +27,8 @@ struct Error {
   std::string msg;
 };
 [[noreturn]] void fail(sp_status code, std::string msg);
+// message returned by sp_last_error() on this thread
+void set_last_error(const std::string &msg);
 
 // ---------------------------------------------------------------- types
 enum class Kind : uint8_t { Named, Contiguous, Vector, Hvector, Subarray };

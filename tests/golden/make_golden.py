@@ -19,7 +19,7 @@ reference tree does not exist):
 """
 from __future__ import annotations
 
-import ctypes as C
+import ctypes as C  # noqa: F401
 import hashlib
 import json
 import os
@@ -105,7 +105,8 @@ def main():
         json.dump(digests, f, separators=(",", ":"))
     print(f"corpus: {len(corpus)} defs, pack digests: {len(digests)}")
     try:
-        import make_golden_model  # noqa: F401  (model + halo fixtures, if present)
+        sys.path.insert(0, HERE)
+        import make_golden_model
         make_golden_model.main(R)
     except ImportError:
         pass

@@ -1,0 +1,207 @@
+"""Send-method model (M1) and profile I/O (M2): the product's C++ model against
+the reference's golden outputs (tests/golden/model_golden.json) and the
+Python restatement (oracle/model.py), plus the KATs of
+proj/tests/test_perfmodel.cpp and acceptance.cpp criteria 5, 6 and 8. CPU only.
+"""
+import os
+import subprocess
+import threading
+
+import numpy as np
+import pytest
+
+from oracle import model as om
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = os.path.join(HERE, "golden")
+
+
+@pytest.fixture(scope="module")
+def M():
+    import paper_2012_14363_b200.model as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def text():
+    return open(os.path.join(GOLD, "default.profile")).read()
+
+
+@pytest.fixture(scope="module")
+def prof(M, text):
+    return M.load_profile(text)
+
+
+@pytest.fixture(scope="module")
+def gold():
+    import json
+    return json.load(open(os.path.join(GOLD, "model_golden.json")))
+
+
+def test_oracle_model_matches_reference_golden(text, gold):
+    p = om.parse(text)
+    for q in gold["base"]:
+        if q["status"]:
+            with pytest.raises(om.InvalidArgument):
+                om.choose(p, q["o"], q["b"])
+            continue
+        assert om.choose(p, q["o"], q["b"]) == q["method"]
+        assert om.times(p, q["o"], q["b"]) == (q["t_device"], q["t_oneshot"], q["t_staged"])
+    for k, rows in gold["scaled"].items():
+        ps = om.scaled(p, float(k))
+        for q in rows:
+            if not q["status"]:
+                assert om.choose(ps, q["o"], q["b"]) == q["method"]
+
+
+def test_product_model_bit_exact_vs_reference(M, prof, gold):
+    for q in gold["base"]:
+        mq = M.ModelQuery(q["o"], q["b"])
+        if q["status"]:
+            from paper_2012_14363_b200 import InvalidArgument
+            with pytest.raises(InvalidArgument):
+                M.choose_method(prof, mq)
+            continue
+        assert int(M.choose_method(prof, mq)) == q["method"]
+        assert M.model_times(prof, mq) == (q["t_device"], q["t_oneshot"], q["t_staged"])
+
+
+def test_profile_round_trip_byte_identical(M, text):
+    """save(load(x)) reproduces the reference's own save_profile output"""
+    p = M.load_profile(text)
+    header = ("proj/data/default.profile as re-emitted by the reference's save_profile\n"
+              "(synthetic Summit-shaped fixture, see the reference header)")
+    assert M.save_profile(p, header) == text
+    q = M.load_profile(M.save_profile(p, "round trip"))
+    assert M.save_profile(q) == M.save_profile(p)
+
+
+def zero_pack_profile(M):
+    """test_perfmodel.cpp:16-36"""
+    p = M.MachineProfile()
+    p.set_curve("cpu_cpu", [64, 1 << 22], [1.3e-6, 400e-6])
+    p.set_curve("gpu_gpu", [64, 1 << 22], [6.0e-6, 500e-6])
+    p.set_curve("d2h", [64, 1 << 22], [7.0e-6, 200e-6])
+    p.set_curve("h2d", [64, 1 << 22], [7.0e-6, 200e-6])
+    for s in ("gpu_pack", "gpu_unpack", "host_pack", "host_unpack"):
+        p.set_surface(s, [64, 1 << 22], [8, 4096], [[0, 0], [0, 0]])
+    return p
+
+
+def test_interp_kats(M):
+    """test_perfmodel.cpp:42-77"""
+    from paper_2012_14363_b200 import EmptyProfile
+    p = M.MachineProfile()
+    p.set_curve("cpu_cpu", [1024, 4096], [1e-6, 4e-6])
+    assert M.interp_1d(p, "cpu_cpu", 1024) == 1e-6
+    assert M.interp_1d(p, "cpu_cpu", 4096) == 4e-6
+    assert M.interp_1d(p, "cpu_cpu", 2048) == pytest.approx(2e-6, rel=1e-12)
+    assert M.interp_1d(p, "cpu_cpu", 10) == 1e-6
+    assert M.interp_1d(p, "cpu_cpu", 1 << 20) == 4e-6
+    with pytest.raises(EmptyProfile):
+        M.interp_1d(p, "gpu_gpu", 64)
+    p.set_curve("d2h", [64, 128, 512], [1e-6, 3e-6, 9e-6])
+    assert M.interp_1d(p, "d2h", 128) == 3e-6
+    p.set_surface("gpu_pack", [1, 4], [1, 4], [[1e-6, 4e-6], [4e-6, 16e-6]])
+    assert M.interp_2d(p, "gpu_pack", 1, 1) == 1e-6
+    assert M.interp_2d(p, "gpu_pack", 4, 4) == 16e-6
+    assert M.interp_2d(p, "gpu_pack", 2, 2) == pytest.approx(4e-6, rel=1e-12)
+    assert M.interp_2d(p, "gpu_pack", 1, 2) == pytest.approx(2e-6, rel=1e-12)
+    assert M.interp_2d(p, "gpu_pack", 2, 4) == pytest.approx(8e-6, rel=1e-12)
+    p.set_surface("host_pack", [64, 1 << 22], [8, 4096], [[3e-6, 3e-6], [3e-6, 3e-6]])
+    assert M.interp_2d(p, "host_pack", 512, 64) == 3e-6
+    with pytest.raises(EmptyProfile):
+        M.interp_2d(p, "host_unpack", 64, 8)
+
+
+def test_zero_pack_reduces_to_transfers(M):
+    """test_perfmodel.cpp:80-101"""
+    p = zero_pack_profile(M)
+    for size in (64, 1024, 1 << 20):
+        q = M.ModelQuery(size, 8)
+        assert M.t_device(p, q) == pytest.approx(M.interp_1d(p, "gpu_gpu", size))
+        assert M.t_oneshot(p, q) == pytest.approx(M.interp_1d(p, "cpu_cpu", size))
+    for size in (64, 4096, 1 << 18, 1 << 22):
+        assert M.choose_method(p, M.ModelQuery(size, 8)) == M.MethodChoice.OneShot
+
+
+def test_default_profile_qualitative(M, prof):
+    """test_perfmodel.cpp:103-150, acceptance.cpp criteria 5-6"""
+    for blk in (8, 64, 256):
+        assert M.choose_method(prof, M.ModelQuery(512, blk)) == M.MethodChoice.OneShot
+    assert M.choose_method(prof, M.ModelQuery(4 << 20, 16)) == M.MethodChoice.Device
+    small_oneshot = any(all(M.choose_method(prof, M.ModelQuery(o, min(b, o))) == M.MethodChoice.OneShot
+                            for b in (8, 16, 32, 64)) for o in (64, 128, 256, 512, 1024))
+    assert small_oneshot
+    for blk in (8, 128, 2048):
+        prev = (0, 0, 0)
+        size = 4096
+        while size <= 16 << 20:
+            t = M.model_times(prof, M.ModelQuery(size, blk))
+            assert all(a >= b for a, b in zip(t, prev))
+            prev = t
+            size *= 2
+
+
+def test_query_validation(M):
+    from paper_2012_14363_b200 import InvalidArgument
+    p = zero_pack_profile(M)
+    for o, b in ((0, 1), (64, 0), (64, 128)):
+        with pytest.raises(InvalidArgument):
+            M.choose_method(p, M.ModelQuery(o, b))
+
+
+def test_cache_agrees_and_is_thread_safe(M, prof):
+    """test_perfmodel.cpp:152-208, acceptance.cpp criterion 8 (agreement)"""
+    cache = M.ModelCache(prof)
+    rng = np.random.default_rng(8)
+    for _ in range(2000):
+        o = int(1 + rng.integers(0, 1 << 22))
+        b = int(1 + rng.integers(0, o))
+        assert cache.choose(M.ModelQuery(o, b)) == M.choose_method(prof, M.ModelQuery(o, b))
+    rng = np.random.default_rng(15)
+    for _ in range(3000):
+        q = M.ModelQuery(1024 + int(rng.integers(0, 64)), 1 + int(rng.integers(0, 64)))
+        assert cache.choose(q) == M.choose_method(prof, q)
+    bad = []
+
+    def worker(t):
+        r = np.random.default_rng(100 + t)
+        for _ in range(1000):
+            o = 64 << int(r.integers(0, 16))
+            q = M.ModelQuery(o, min(8 << int(r.integers(0, 8)), o))
+            if cache.choose(q) != M.choose_method(prof, q):
+                bad.append(q)
+
+    ths = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    assert not bad
+
+
+def test_parse_rejects_malformed(M):
+    """test_perfmodel.cpp:225-236"""
+    from paper_2012_14363_b200 import ParseError
+    for bad in ["curve bogus\n1 2\n", "curve cpu_cpu\n64 1e-6\n32 2e-6\n",
+                "surface gpu_pack\n64 8 1e-6\n128 16 1e-6\n64 16 1e-6\n", "64 1e-6\n"]:
+        with pytest.raises(ParseError):
+            M.load_profile(bad)
+    M.load_profile("# comment only\ncurve cpu_cpu\n64 1.5e-6 # eol\n")
+
+
+def test_warm_cache_speedup_native(tmp_path):
+    """acceptance.cpp criterion 8: warm lookups >= 10x faster than cold
+    recomputation, timed natively (tests/native/model_cache_bench.cpp)."""
+    root = os.path.dirname(HERE)
+    exe = tmp_path / "model_cache_bench"
+    subprocess.run(["/usr/bin/g++", "-std=c++17", "-O2", os.path.join(HERE, "native", "model_cache_bench.cpp"),
+                    "-I", os.path.join(root, "include"), "-L", os.path.join(root, "paper_2012_14363_b200"),
+                    "-lstridepack_b200", "-Wl,-rpath," + os.path.join(root, "paper_2012_14363_b200"),
+                    "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe), os.path.join(GOLD, "default.profile")], capture_output=True, text=True,
+                         check=True).stdout
+    cold, warm, agree = out.split()
+    assert agree == "1"
+    assert float(warm) * 10 <= float(cold), out
