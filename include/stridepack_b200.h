@@ -131,8 +131,9 @@ enum {
   SP_KERNEL_SMALLROW = 2, /* rows of 1/2/4/8 B gathered into 16 B stores */
   SP_KERNEL_BLOCKLIST = 3,/* device block-list (definition-order runs) */
   SP_KERNEL_TMA = 4,      /* tensor-map box staged through shared memory */
-  SP_KERNEL_WORDS64 = 5   /* generic kernel with 64-bit indexing (chosen
+  SP_KERNEL_WORDS64 = 5,  /* generic kernel with 64-bit indexing (chosen
                              automatically beyond 2^32 words or rows) */
+  SP_KERNEL_BATCH = 6     /* many jobs in one launch (sp_batch_*) */
 };
 typedef struct {
   int allow_fallback; /* PackOptions.allow_fallback (default 1) */
@@ -159,6 +160,31 @@ typedef struct {
 sp_status sp_last_launch(sp_launch_info *out);
 /* total kernels this library enqueued in this process */
 int64_t sp_kernel_launch_count(void);
+
+/* ---- batches: many pack (or unpack) jobs in ONE kernel launch -------- *
+ * Replaces a loop of pack() calls over one buffer (halo.hpp:227-235: 26
+ * region packs into one send buffer) with a persistent plan. Each job has
+ * the arguments of sp_pack (unpack == 0) or sp_unpack (unpack == 1) and is
+ * validated at creation in the same precedence; the plan binds the
+ * pointers, which must be device memory, pinned host memory or peer-GPU
+ * memory mapped through CUDA IPC (pack-to-peer). Empty types are skipped;
+ * forms without a strided canon are rejected (SP_ERR_UNSUPPORTED). */
+typedef struct {
+  const void *src;
+  uint64_t src_bytes;
+  sp_type type;
+  int64_t count;
+  void *dst;
+  uint64_t dst_bytes;
+  int64_t position; /* offset into the packed buffer (dst for pack, src for unpack) */
+} sp_batch_job;
+typedef struct sp_batch_s *sp_batch;
+sp_status sp_batch_create(const sp_batch_job *jobs, int64_t n, int unpack,
+                          sp_batch *out);
+sp_status sp_batch_execute(sp_batch b, void *stream);
+/* packed bytes one execution moves */
+sp_status sp_batch_bytes(sp_batch b, int64_t *bytes);
+sp_status sp_batch_free(sp_batch b);
 
 /* ---- send-method model: perf_model.hpp / profile_io.hpp ------------- *
  * A MachineProfile (perf_model.hpp:36-45) holds four transfer curves
@@ -206,6 +232,50 @@ sp_status sp_model_cache_create(sp_profile p, sp_model_cache *out);
 sp_status sp_model_cache_choose(sp_model_cache c, int64_t object_size,
                                 int64_t block_size, int *method);
 sp_status sp_model_cache_free(sp_model_cache c);
+
+/* ---- 3D halo exchange: halo.hpp ------------------------------------- *
+ * HaloConfig (halo.hpp:25-30): periodic rank grid, interior cells per rank
+ * per axis, stencil radius, payload bytes per cell. */
+typedef struct {
+  int64_t ranks[3];
+  int64_t interior[3];
+  int64_t radius;
+  int64_t element_bytes;
+} sp_halo_config;
+
+/* build_halo_types (halo.hpp:98-130): the 26 (send, recv) byte-normalised
+ * subarray types over the padded allocation, committed, in direction order
+ * z, y, x in {-1,0,1}. dir[k*3 + a] is the direction on axis a (x,y,z);
+ * cells[k] the grid points per region. Handles are owned by the caller. */
+sp_status sp_halo_types(const sp_halo_config *cfg, sp_type send[26],
+                        sp_type recv[26], int dir[78], int64_t cells[26]);
+/* rank index of the neighbour of `rank` in direction dir (periodic) */
+sp_status sp_halo_neighbor(const sp_halo_config *cfg, int64_t rank,
+                           const int dir[3], int64_t *neighbor);
+/* fill_cell pattern (halo.hpp:152-164) into rank's padded allocation
+ * (device memory): interior from the global pattern, ghosts 0xee */
+sp_status sp_halo_fill(const sp_halo_config *cfg, int64_t rank, void *alloc,
+                       void *stream);
+/* exact check of every padded cell against the wrapped global pattern
+ * (halo.hpp:264-285); synchronises `stream`; *mismatched = bad cells */
+sp_status sp_halo_verify(const sp_halo_config *cfg, int64_t rank,
+                         const void *alloc, void *stream, int64_t *mismatched);
+
+enum { SP_HALO_FUSED = 0, /* pack-to-peer: one batch stores every segment
+                             into the receiver's buffer */
+       SP_HALO_COPY = 1   /* pack, per-segment copies, unpack (the
+                             reference's three phases) */ };
+/* ExchangeReport (halo.hpp:132-138) + measured device times */
+typedef struct {
+  double pack_seconds, alltoallv_seconds, unpack_seconds; /* modeled */
+  int64_t verified, bytes_moved, mismatched_cells;
+  double measured_pack_seconds, measured_exchange_seconds,
+      measured_unpack_seconds; /* CUDA-event averages over iters */
+} sp_halo_report;
+/* run_exchange (halo.hpp:172): every rank of the grid on the CURRENT
+ * device; profile may be NULL (no modeled times). */
+sp_status sp_halo_run(const sp_halo_config *cfg, sp_profile profile,
+                      int method, int iters, sp_halo_report *out);
 
 #ifdef __cplusplus
 }

@@ -96,3 +96,34 @@ _sig("sp_choose_method", C.c_int, vp, i64, i64, C.POINTER(C.c_int))
 _sig("sp_model_cache_create", C.c_int, vp, C.POINTER(vp))
 _sig("sp_model_cache_choose", C.c_int, vp, i64, i64, C.POINTER(C.c_int))
 _sig("sp_model_cache_free", C.c_int, vp)
+
+# ---- batches
+class BatchJob(C.Structure):
+    _fields_ = [("src", C.c_void_p), ("src_bytes", u64), ("type", sp_type), ("count", i64),
+                ("dst", C.c_void_p), ("dst_bytes", u64), ("position", i64)]
+
+
+_sig("sp_batch_create", C.c_int, C.POINTER(BatchJob), i64, C.c_int, C.POINTER(vp))
+_sig("sp_batch_execute", C.c_int, vp, vp)
+_sig("sp_batch_bytes", C.c_int, vp, i64p)
+_sig("sp_batch_free", C.c_int, vp)
+
+
+# ---- halo
+class HaloConfig(C.Structure):
+    _fields_ = [("ranks", i64 * 3), ("interior", i64 * 3), ("radius", i64), ("element_bytes", i64)]
+
+
+class HaloReport(C.Structure):
+    _fields_ = [("pack_seconds", dbl), ("alltoallv_seconds", dbl), ("unpack_seconds", dbl),
+                ("verified", i64), ("bytes_moved", i64), ("mismatched_cells", i64),
+                ("measured_pack_seconds", dbl), ("measured_exchange_seconds", dbl),
+                ("measured_unpack_seconds", dbl)]
+
+
+_sig("sp_halo_types", C.c_int, C.POINTER(HaloConfig), C.POINTER(sp_type), C.POINTER(sp_type),
+     C.POINTER(C.c_int), i64p)
+_sig("sp_halo_neighbor", C.c_int, C.POINTER(HaloConfig), i64, C.POINTER(C.c_int), i64p)
+_sig("sp_halo_fill", C.c_int, C.POINTER(HaloConfig), i64, vp, vp)
+_sig("sp_halo_verify", C.c_int, C.POINTER(HaloConfig), i64, vp, vp, i64p)
+_sig("sp_halo_run", C.c_int, C.POINTER(HaloConfig), vp, C.c_int, C.c_int, C.POINTER(HaloReport))

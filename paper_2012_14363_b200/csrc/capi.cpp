@@ -4,7 +4,9 @@
 #include <cstring>
 #include <exception>
 #include <new>
+#include <memory>
 #include <string>
+#include <vector>
 
 #include "core.hpp"
 
@@ -182,6 +184,52 @@ sp_status sp_pack_ex(const void *src, uint64_t src_bytes, sp_type t, int64_t inc
 sp_status sp_unpack_ex(const void *src, uint64_t src_bytes, int64_t *position, sp_type t, int64_t outcount,
                        void *dst, uint64_t dst_bytes, void *stream, const sp_pack_options *opt) {
   return pack_impl(false, src, src_bytes, t, outcount, dst, dst_bytes, position, stream, opt);
+}
+
+} // extern "C"
+
+struct sp_batch_s {
+  spb::Batch *b = nullptr;
+  std::vector<spb::CommitPtr> keep; // committed types outlive the plan
+  ~sp_batch_s() { spb::batch_destroy(b); }
+};
+
+extern "C" {
+
+sp_status sp_batch_create(const sp_batch_job *jobs, int64_t n, int unpack, sp_batch *out) {
+  return guard([&] {
+    if (!out || (n > 0 && !jobs) || n < 0) spb::fail(SP_ERR_INVALID_ARGUMENT, "bad batch arguments");
+    auto h = std::make_unique<sp_batch_s>();
+    std::vector<spb::BatchSpec> specs;
+    for (int64_t i = 0; i < n; ++i) {
+      const spb::Entry e = spb::registry().get(jobs[i].type);
+      if (!e.committed) spb::fail(SP_ERR_INVALID_ARGUMENT, "type is not committed");
+      h->keep.push_back(e.committed);
+      specs.push_back({e.committed.get(), jobs[i].src, jobs[i].src_bytes, jobs[i].count, jobs[i].dst,
+                       jobs[i].dst_bytes, jobs[i].position});
+    }
+    h->b = spb::batch_create(specs, unpack != 0);
+    *out = h.release();
+  });
+}
+
+sp_status sp_batch_execute(sp_batch b, void *stream) {
+  return guard([&] {
+    if (!b) spb::fail(SP_ERR_INVALID_ARGUMENT, "null batch");
+    spb::batch_execute(*b->b, stream);
+  });
+}
+
+sp_status sp_batch_bytes(sp_batch b, int64_t *bytes) {
+  return guard([&] {
+    if (!b || !bytes) spb::fail(SP_ERR_INVALID_ARGUMENT, "null argument");
+    *bytes = spb::batch_bytes(*b->b);
+  });
+}
+
+sp_status sp_batch_free(sp_batch b) {
+  delete b;
+  return SP_OK;
 }
 
 } // extern "C"

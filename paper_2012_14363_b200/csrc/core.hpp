@@ -145,5 +145,23 @@ struct PackArgs {
 int64_t execute(const PackArgs &a);
 
 void set_last_launch(const sp_launch_info &li);
+void cuda_check(int err, const char *what);  // cudaError_t as int
+void require_device();
+
+// persistent multi-job launches (pack.cu)
+struct BatchSpec {
+  const Committed *ct;
+  const void *src;
+  uint64_t src_bytes;
+  int64_t count;
+  void *dst;
+  uint64_t dst_bytes;
+  int64_t position;
+};
+struct Batch;
+Batch *batch_create(const std::vector<BatchSpec> &specs, bool unpack);
+void batch_execute(const Batch &b, void *stream);
+void batch_destroy(Batch *b);
+int64_t batch_bytes(const Batch &b);
 
 } // namespace spb

@@ -275,9 +275,6 @@ struct ModelCache {
 // ============================================================ C-ABI
 using spb::Profile;
 
-struct sp_profile_s {
-  std::shared_ptr<Profile> p;
-};
 struct sp_model_cache_s {
   spb::ModelCache c;
 };

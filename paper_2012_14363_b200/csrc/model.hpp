@@ -31,3 +31,7 @@ Profile parse_profile(const std::string &text);
 std::string format_profile(const Profile &p, const std::string &header);
 
 } // namespace spb
+
+struct sp_profile_s {     // the C-ABI handle
+  std::shared_ptr<spb::Profile> p;
+};

@@ -43,10 +43,20 @@ static thread_local sp_launch_info t_last{};
 
 void set_last_launch(const sp_launch_info &li) { t_last = li; }
 
-static void cuda_check(cudaError_t e, const char *what) {
+void cuda_check(int err, const char *what) {
+  const cudaError_t e = static_cast<cudaError_t>(err);
   if (e != cudaSuccess) {
     cudaGetLastError();
     fail(SP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+void require_device() {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    fail(SP_ERR_NO_DEVICE, "no CUDA device: the B200 kernels are the only execution path");
   }
 }
 
@@ -623,16 +633,206 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
-void require_device() {
-  int n = 0;
-  const cudaError_t e = cudaGetDeviceCount(&n);
-  if (e != cudaSuccess || n == 0) {
-    cudaGetLastError();
-    fail(SP_ERR_NO_DEVICE, "no CUDA device: the B200 kernels are the only execution path");
+} // namespace
+
+// ============================================================ batches
+// A persistent list of (type, buffers) jobs executed by ONE launch: every
+// 1024-word chunk of every job is a unit of work, blocks walk the chunks
+// grid-stride and look their job up by binary search, so small regions
+// (halo corners, edges) share the grid with large ones (faces) instead of
+// costing a launch each. Destinations may be peer-GPU memory mapped over
+// NVLink (CUDA IPC), which turns the batch into a fused pack-to-peer.
+constexpr uint32_t kBatchChunk = 256 * 4;
+
+struct BatchJob {
+  Geom g;
+  const uint8_t *in;
+  uint8_t *out;
+  int w;
+  int pack;
+};
+
+template <int W, bool PACK>
+__device__ __noinline__ void batch_chunk(const BatchJob &j, uint32_t base) {
+  using T = typename Word<W>::T;
+  const uint32_t total = static_cast<uint32_t>(j.g.total);
+  T v[4];
+  int64_t soff[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t q = base + u * 256;
+    if (q < total) {
+      const uint32_t row = fdiv(q, j.g.wdiv);
+      soff[u] = row_offset(row, j.g) + static_cast<int64_t>(q - row * j.g.wpr) * W;
+      v[u] = PACK ? ld_stream(reinterpret_cast<const T *>(j.in + soff[u])) : ld_stream(reinterpret_cast<const T *>(j.in) + q);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t q = base + u * 256;
+    if (q < total) {
+      if (PACK) {
+        st_stream(reinterpret_cast<T *>(j.out) + q, v[u]);
+      } else {
+        st_stream(reinterpret_cast<T *>(j.out + soff[u]), v[u]);
+      }
+    }
   }
 }
 
+__global__ void __launch_bounds__(256, 4) k_batch(const BatchJob *__restrict__ jobs,
+                                               const uint32_t *__restrict__ chunk0, int njobs,
+                                               uint32_t nchunks) {
+  __shared__ BatchJob sj;
+  int loaded = -1;
+  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    int lo = 0, hi = njobs - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (chunk0[mid] <= c) {
+        lo = mid;
+      } else {
+        hi = mid - 1;
+      }
+    }
+    if (lo != loaded) {
+      __syncthreads();
+      const uint32_t *s = reinterpret_cast<const uint32_t *>(jobs + lo);
+      uint32_t *d = reinterpret_cast<uint32_t *>(&sj);
+      for (uint32_t i = threadIdx.x; i < sizeof(BatchJob) / 4; i += blockDim.x) d[i] = s[i];
+      __syncthreads();
+      loaded = lo;
+    }
+    const uint32_t base = (c - chunk0[lo]) * kBatchChunk + threadIdx.x;
+    switch (sj.w * 2 + sj.pack) {
+    case 33: batch_chunk<16, true>(sj, base); break;
+    case 32: batch_chunk<16, false>(sj, base); break;
+    case 17: batch_chunk<8, true>(sj, base); break;
+    case 16: batch_chunk<8, false>(sj, base); break;
+    case 9: batch_chunk<4, true>(sj, base); break;
+    case 8: batch_chunk<4, false>(sj, base); break;
+    case 5: batch_chunk<2, true>(sj, base); break;
+    case 4: batch_chunk<2, false>(sj, base); break;
+    case 3: batch_chunk<1, true>(sj, base); break;
+    default: batch_chunk<1, false>(sj, base); break;
+    }
+  }
+}
+
+struct Batch {
+  int device = -1;
+  BatchJob *d_jobs = nullptr;
+  uint32_t *d_chunk0 = nullptr;
+  int njobs = 0;
+  uint32_t nchunks = 0;
+  int64_t bytes = 0; // packed bytes moved per execution
+  ~Batch() {
+    if (d_jobs) {
+      cudaFree(d_jobs);
+      cudaFree(d_chunk0);
+    }
+  }
+};
+
+namespace {
+
+// word-kernel job for one (type, count, buffers): row geometry + the
+// alignment-derived word, on device-accessible pointers
+BatchJob plan_job(const Committed &ct, int64_t count, const uint8_t *strided, const uint8_t *packed, bool pack) {
+  if (ct.form != SP_FORM_STRIDED) fail(SP_ERR_UNSUPPORTED, "batch: only strided forms can be batched");
+  const RowDims rd = row_dims(ct, count);
+  if (static_cast<int>(rd.cnt.size()) > KMAX) fail(SP_ERR_UNSUPPORTED, "batch: too many row dimensions");
+  uint64_t g_or = static_cast<uint64_t>(rd.c0) | (reinterpret_cast<uint64_t>(strided) + ct.sb.start) |
+                  reinterpret_cast<uint64_t>(packed);
+  for (int64_t st : rd.str) g_or |= static_cast<uint64_t>(st);
+  const int w = pow2_align(g_or);
+  uint64_t rows = 1;
+  for (int64_t c : rd.cnt) rows *= static_cast<uint64_t>(c);
+  const uint64_t words = rows * static_cast<uint64_t>(rd.c0) / static_cast<uint64_t>(w);
+  if (words >= (1ull << 32) || rows >= (1ull << 32) || rd.c0 / w >= (int64_t{1} << 32))
+    fail(SP_ERR_UNSUPPORTED, "batch: job larger than 2^32 words");
+  BatchJob j{};
+  j.g.nd = static_cast<int>(rd.cnt.size());
+  for (int k = 0; k < j.g.nd; ++k) {
+    j.g.cnt[k] = static_cast<uint32_t>(rd.cnt[k]);
+    j.g.div[k] = make_fastdiv(j.g.cnt[k]);
+    j.g.str[k] = rd.str[k];
+    j.g.back[k] = rd.cnt[k] * rd.str[k];
+  }
+  j.g.wpr = static_cast<uint32_t>(rd.c0 / w);
+  j.g.wdiv = make_fastdiv(j.g.wpr);
+  j.g.total = words;
+  j.g.rows = rows;
+  j.w = w;
+  j.pack = pack;
+  j.in = pack ? strided + ct.sb.start : packed;
+  j.out = pack ? const_cast<uint8_t *>(packed) : const_cast<uint8_t *>(strided) + ct.sb.start;
+  return j;
+}
+
 } // namespace
+
+Batch *batch_create(const std::vector<BatchSpec> &specs, bool unpack) {
+  require_device();
+  std::vector<BatchJob> jobs;
+  std::vector<uint32_t> chunk0;
+  uint64_t chunks = 0;
+  int64_t bytes = 0;
+  for (const BatchSpec &s : specs) {
+    const Committed &ct = *s.ct;
+    // argument checks in the reference's precedence (pack.hpp:102-126 / :146-159)
+    if (s.count < 1 || s.position < 0) fail(SP_ERR_INVALID_ARGUMENT, "batch: count must be positive, position >= 0");
+    if (unpack && ct.overlapping) fail(SP_ERR_OVERLAPPING_LAYOUT, "batch: unpack layout describes overlapping bytes");
+    const uint64_t packed_need = static_cast<uint64_t>(s.position + s.count * ct.size);
+    if (packed_need > (unpack ? s.src_bytes : s.dst_bytes)) fail(SP_ERR_BUFFER_TOO_SMALL, "batch: packed buffer too small");
+    if (ct.form == SP_FORM_EMPTY) continue;
+    const uint64_t strided_need = static_cast<uint64_t>((s.count - 1) * ct.extent + ct.span);
+    if (strided_need > (unpack ? s.dst_bytes : s.src_bytes)) fail(SP_ERR_BUFFER_TOO_SMALL, "batch: strided buffer too small");
+    const void *strided = unpack ? s.dst : s.src;
+    const void *packed = unpack ? s.src : s.dst;
+    const Resolved rs = resolve(strided), rp = resolve(packed);
+    if (rs.kind == MemKind::Pageable || rp.kind == MemKind::Pageable)
+      fail(SP_ERR_INVALID_ARGUMENT, "batch: buffers must be device, pinned or peer-mapped memory");
+    BatchJob j = plan_job(ct, s.count, rs.dptr, rp.dptr + s.position, !unpack);
+    chunk0.push_back(static_cast<uint32_t>(chunks));
+    chunks += (j.g.total + kBatchChunk - 1) / kBatchChunk;
+    if (chunks >= (1ull << 32)) fail(SP_ERR_UNSUPPORTED, "batch: too much work for one launch");
+    bytes += s.count * ct.size;
+    jobs.push_back(j);
+  }
+  auto b = std::make_unique<Batch>();
+  cuda_check(cudaGetDevice(&b->device), "cudaGetDevice");
+  b->njobs = static_cast<int>(jobs.size());
+  b->nchunks = static_cast<uint32_t>(chunks);
+  b->bytes = bytes;
+  if (!jobs.empty()) {
+    cuda_check(cudaMalloc(&b->d_jobs, jobs.size() * sizeof(BatchJob)), "cudaMalloc(batch)");
+    cuda_check(cudaMalloc(&b->d_chunk0, chunk0.size() * sizeof(uint32_t)), "cudaMalloc(batch)");
+    cuda_check(cudaMemcpy(b->d_jobs, jobs.data(), jobs.size() * sizeof(BatchJob), cudaMemcpyHostToDevice), "upload batch");
+    cuda_check(cudaMemcpy(b->d_chunk0, chunk0.data(), chunk0.size() * sizeof(uint32_t), cudaMemcpyHostToDevice),
+               "upload batch");
+  }
+  return b.release();
+}
+
+void batch_execute(const Batch &b, void *stream) {
+  sp_launch_info li{};
+  if (b.njobs > 0) {
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(b.nchunks, static_cast<uint64_t>(sm_count()) * 8));
+    k_batch<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(b.d_jobs, b.d_chunk0, b.njobs, b.nchunks);
+    cuda_check(cudaGetLastError(), "k_batch launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    li.kernel = SP_KERNEL_BATCH;
+    li.launches = 1;
+    li.grid = grid;
+    li.block = 256;
+  }
+  set_last_launch(li);
+}
+
+void batch_destroy(Batch *b) { delete b; }
+
+int64_t batch_bytes(const Batch &b) { return b.bytes; }
 
 // Validation order follows pack.hpp:102-126 / :146-159 exactly.
 int64_t execute(const PackArgs &a) {

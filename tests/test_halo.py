@@ -1,0 +1,165 @@
+"""3D halo exchange (H1): region geometry against the reference's own halo
+types (tests/golden/halo_golden.json), the KATs of proj/tests/test_halo.cpp,
+and on the GPU the full exchange (fused pack-to-peer batches and the copy
+baseline) verified cell-for-cell with the reference's fill_cell pattern and
+its modeled phase times reproduced exactly."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def H():
+    import paper_2012_14363_b200.halo as h
+    return h
+
+
+@pytest.fixture(scope="module")
+def hgold():
+    return json.load(open(os.path.join(GOLD, "halo_golden.json")))
+
+
+def test_region_types_match_reference(sp, H, orc, hgold):
+    for g in hgold["types"]:
+        cfg = H.HaloConfig(interior=tuple(g["interior"]), radius=g["radius"], element_bytes=g["elem"])
+        regs = H.build_halo_types(cfg)
+        assert len(regs) == 26
+        for mine, ref in zip(regs, g["regions"]):
+            assert list(mine.dir) == ref["dir"] and mine.gridpoints == ref["cells"]
+            for ct, prog in ((mine.send, ref["send"]), (mine.recv, ref["recv"])):
+                want = orc.commit(prog)
+                assert (ct.size, ct.extent, ct.span, ct.overlapping) == (want.size, want.extent, want.span,
+                                                                          want.overlapping)
+                assert ct.canon == sp.StridedBlock(want.start, tuple(want.counts), tuple(want.strides))
+
+
+def test_face_edge_corner_geometry(H):
+    """test_halo.cpp:11-44"""
+    cfg = H.HaloConfig(interior=(16, 16, 16), radius=3, element_bytes=64)
+    regs = H.build_halo_types(cfg)
+    faces = edges = corners = recv_cells = 0
+    for r in regs:
+        axes = sum(abs(x) for x in r.dir)
+        want = {1: 3 * 16 * 16, 2: 3 * 3 * 16, 3: 27}[axes]
+        assert r.gridpoints == want
+        assert r.send.size == want * 64 and r.recv.size == want * 64
+        faces += axes == 1
+        edges += axes == 2
+        corners += axes == 3
+        recv_cells += r.gridpoints
+    assert (faces, edges, corners) == (6, 12, 8)
+    assert recv_cells == 22 ** 3 - 16 ** 3
+    small = H.build_halo_types(H.HaloConfig(interior=(2, 2, 2), radius=1, element_bytes=8))
+    assert all(r.gridpoints == 1 for r in small if sum(abs(x) for x in r.dir) == 3)
+
+
+def test_config_validation(sp, H):
+    """test_halo.cpp:58-68"""
+    with pytest.raises(sp.InvalidArgument):
+        H.build_halo_types(H.HaloConfig(interior=(4, 4, 4), radius=3))
+    with pytest.raises(sp.InvalidArgument):
+        H.build_halo_types(H.HaloConfig(interior=(4, 4, 4), radius=0))
+    H.build_halo_types(H.HaloConfig(interior=(4, 4, 4), radius=2))
+    with pytest.raises(sp.InvalidArgument):
+        H.neighbor(H.HaloConfig(ranks=(0, 1, 1), interior=(4, 4, 4), radius=2), 0, (1, 0, 0))
+
+
+def test_neighbor_mapping(H):
+    cfg = H.HaloConfig(ranks=(3, 1, 2), interior=(4, 6, 8), radius=2)
+    # rank = (z*R1 + y)*R0 + x, periodic
+    assert H.neighbor(cfg, 0, (-1, 0, 0)) == 2
+    assert H.neighbor(cfg, 0, (0, 0, 1)) == 3
+    assert H.neighbor(cfg, 5, (1, 1, 1)) == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("method", [0, 1])
+def test_exchange_matches_reference_reports(H, cuda, hgold, method):
+    """run_exchange: every ghost cell exact; bytes moved and the modeled
+    phase times equal the reference's ExchangeReport (halo.hpp:287-320)."""
+    import paper_2012_14363_b200.model as M
+    prof = M.load_profile_file(os.path.join(GOLD, "default.profile"))
+    for r in hgold["reports"]:
+        cfg = H.HaloConfig(tuple(r["ranks"]), tuple(r["interior"]), r["radius"], r["elem"])
+        rep = H.run_exchange(cfg, prof, method=method, iters=2)
+        assert rep.verified and rep.mismatched_cells == 0, r
+        assert rep.bytes_moved == r["bytes"]
+        assert (rep.pack_seconds, rep.alltoallv_seconds, rep.unpack_seconds) == (r["pack"], r["alltoallv"],
+                                                                                 r["unpack"])
+        assert rep.measured_pack_seconds > 0 and rep.measured_unpack_seconds > 0
+
+
+@pytest.mark.gpu
+def test_randomized_desk_scale_exchanges(H, cuda):
+    """test_halo.cpp:108-125"""
+    rng = np.random.default_rng(314)
+    for _ in range(6):
+        radius = 1 + int(rng.integers(0, 2))
+        ranks = tuple(1 + int(rng.integers(0, 3)) for _ in range(3))
+        interior = tuple(2 * radius + int(rng.integers(0, 8)) for _ in range(3))
+        elem = [1, 4, 8, 64][int(rng.integers(0, 4))]
+        for method in (0, 1):
+            rep = H.run_exchange(H.HaloConfig(ranks, interior, radius, elem), None, method=method)
+            assert rep.verified, (ranks, interior, radius, elem, method)
+
+
+@pytest.mark.gpu
+def test_verify_detects_unexchanged_ghosts(H, cuda):
+    torch = cuda
+    cfg = H.HaloConfig((1, 1, 1), (6, 6, 6), 1, 8)
+    alloc = torch.empty(8 ** 3 * 8, dtype=torch.uint8, device="cuda")
+    H.fill(cfg, 0, alloc)
+    assert H.verify(cfg, 0, alloc) == 8 ** 3 - 6 ** 3  # every ghost cell is still 0xee
+    host = alloc.cpu().numpy().reshape(8, 8, 8, 8)
+    assert (host[0, 0, 0] == 0xEE).all() and not (host[1, 1, 1] == 0xEE).all()
+
+
+@pytest.mark.gpu
+def test_batch_parity_vs_oracle(sp, orc, cuda, corpus):
+    """many (type, buffer) jobs in one launch == per-job oracle packs"""
+    torch = cuda
+    from paper_2012_14363_b200.halo import Batch
+    rng = np.random.default_rng(9)
+    picks = [e for e in corpus if e["ref"]["status"] == 0 and e["ref"]["form"] == 0
+             and 0 < e["ref"]["size"] <= (1 << 14)][:120]
+    jobs, wants, srcs = [], [], []
+    total = sum(e["ref"]["size"] * 2 for e in picks) + 16 * len(picks)
+    packed = torch.zeros(total, dtype=torch.uint8, device="cuda")
+    pos = 0
+    for e in picks:
+        ct = sp.commit_type(sp.from_program(e["prog"]))
+        inc = 1 + int(rng.integers(0, 2))
+        span = (inc - 1) * ct.extent + ct.span
+        host = rng.integers(0, 256, span, dtype=np.uint8)
+        src = torch.from_numpy(host).cuda()
+        srcs.append(src)
+        want = np.zeros(inc * ct.size, np.uint8)
+        assert orc.pack(e["prog"], host, inc, want, 0)[0] == 0
+        jobs.append((src, ct, inc, packed, pos))
+        wants.append((pos, want, e["prog"], inc, span, ct))
+        pos += inc * ct.size + int(rng.integers(0, 3))
+    b = Batch(jobs)
+    assert b.bytes == sum(len(w[1]) for w in wants)
+    b.execute()
+    torch.cuda.synchronize()
+    got = packed.cpu().numpy()
+    for p, want, prog, inc, span, ct in wants:
+        assert np.array_equal(got[p:p + len(want)], want), prog
+    # unpack batch back into sentinel-filled buffers
+    outs, ujobs = [], []
+    for (p, want, prog, inc, span, ct) in wants:
+        if ct.overlapping:
+            continue
+        o = torch.full((span,), 0x3C, dtype=torch.uint8, device="cuda")
+        outs.append((o, p, want, prog, inc, span))
+        ujobs.append((packed, ct, inc, o, p))
+    Batch(ujobs, unpack=True).execute()
+    torch.cuda.synchronize()
+    for o, p, want, prog, inc, span in outs:
+        exp = np.full(span, 0x3C, np.uint8)
+        assert orc.unpack(prog, want, 0, inc, exp)[0] == 0
+        assert np.array_equal(o.cpu().numpy(), exp), prog
