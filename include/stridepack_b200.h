@@ -277,6 +277,48 @@ typedef struct {
 sp_status sp_halo_run(const sp_halo_config *cfg, sp_profile profile,
                       int method, int iters, sp_halo_report *out);
 
+/* ---- node-local runtime (the "system MPI" this image lacks) ---------- *
+ * One process per GPU. A POSIX shared-memory segment named after `job`
+ * carries bootstrap, barriers and control mailboxes; CUDA IPC maps peer
+ * device memory (kernels store into a peer's HBM over NVLink); each rank
+ * owns a device receive window and a shared pinned host region.
+ * device < 0 initialises the control plane only (no CUDA calls). */
+sp_status sp_rt_init(int rank, int size, const char *job, int device,
+                     int64_t window_bytes, int64_t host_bytes);
+sp_status sp_rt_finalize(void);
+sp_status sp_rt_rank(int *rank);
+sp_status sp_rt_size(int *size);
+sp_status sp_rt_barrier(void);
+/* small control payloads (<= 16 bytes) between ranks, matched by tag */
+sp_status sp_rt_host_send(int dst, int tag, const void *data, int64_t bytes);
+sp_status sp_rt_host_recv(int src, int tag, void *data, int64_t cap,
+                          int64_t *bytes);
+/* collective: peers[r] = rank r's `local` device pointer mapped here */
+sp_status sp_rt_exchange_ptr(void *local, void **peers);
+/* the send-method model used by sp_rt_send when method < 0 */
+sp_status sp_rt_set_profile(sp_profile p);
+sp_status sp_rt_choose(sp_type t, int64_t count, int *method);
+/* MPI_Send / MPI_Recv of `count` objects of a committed type between two
+ * ranks: rendezvous, then DEVICE (pack kernel stores into the receiver's
+ * HBM window through IPC), ONESHOT (pack kernel stores into the receiver's
+ * pinned host region) or STAGED (device pack, D2H, H2D, unpack); method < 0
+ * = model-selected (Eqs. 1-3). source/tag < 0 match any. status = {source,
+ * tag, bytes, method}. Blocking; the buffers must be device-accessible. */
+sp_status sp_rt_send(const void *buf, uint64_t buf_bytes, int64_t count,
+                     sp_type t, int dest, int tag, int method,
+                     int *used_method);
+sp_status sp_rt_recv(void *buf, uint64_t buf_bytes, int64_t count, sp_type t,
+                     int source, int tag, int64_t status[4]);
+
+/* distributed halo exchange: one rank per process (grid size == runtime
+ * size); `alloc` is this rank's padded allocation on its device. */
+typedef struct sp_halo_plan_s *sp_halo_plan;
+sp_status sp_halo_plan_create(const sp_halo_config *cfg, void *alloc,
+                              int method, sp_halo_plan *out);
+/* collective; times = {pack, exchange, unpack, iteration} seconds */
+sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]);
+sp_status sp_halo_plan_free(sp_halo_plan p);
+
 #ifdef __cplusplus
 }
 #endif

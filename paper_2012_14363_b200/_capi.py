@@ -127,3 +127,20 @@ _sig("sp_halo_neighbor", C.c_int, C.POINTER(HaloConfig), i64, C.POINTER(C.c_int)
 _sig("sp_halo_fill", C.c_int, C.POINTER(HaloConfig), i64, vp, vp)
 _sig("sp_halo_verify", C.c_int, C.POINTER(HaloConfig), i64, vp, vp, i64p)
 _sig("sp_halo_run", C.c_int, C.POINTER(HaloConfig), vp, C.c_int, C.c_int, C.POINTER(HaloReport))
+
+# ---- runtime
+_sig("sp_rt_init", C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_int, i64, i64)
+_sig("sp_rt_finalize", C.c_int)
+_sig("sp_rt_rank", C.c_int, C.POINTER(C.c_int))
+_sig("sp_rt_size", C.c_int, C.POINTER(C.c_int))
+_sig("sp_rt_barrier", C.c_int)
+_sig("sp_rt_host_send", C.c_int, C.c_int, C.c_int, vp, i64)
+_sig("sp_rt_host_recv", C.c_int, C.c_int, C.c_int, vp, i64, i64p)
+_sig("sp_rt_exchange_ptr", C.c_int, vp, C.POINTER(vp))
+_sig("sp_rt_set_profile", C.c_int, vp)
+_sig("sp_rt_choose", C.c_int, sp_type, i64, C.POINTER(C.c_int))
+_sig("sp_rt_send", C.c_int, vp, u64, i64, sp_type, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int))
+_sig("sp_rt_recv", C.c_int, vp, u64, i64, sp_type, C.c_int, C.c_int, i64p)
+_sig("sp_halo_plan_create", C.c_int, C.POINTER(HaloConfig), vp, C.c_int, C.POINTER(vp))
+_sig("sp_halo_plan_exchange", C.c_int, vp, dblp)
+_sig("sp_halo_plan_free", C.c_int, vp)

@@ -1,0 +1,241 @@
+// capi_rt.cpp -- C-ABI of the node-local runtime, point-to-point messages
+// and the multi-process halo exchange.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "guard.hpp"
+#include "halo.hpp"
+#include "rt.hpp"
+
+using namespace spb;
+
+namespace {
+CommitPtr committed_of(sp_type t) {
+  const Entry e = registry().get(t);
+  if (!e.committed) fail(SP_ERR_INVALID_ARGUMENT, "type is not committed");
+  return e.committed;
+}
+} // namespace
+
+// One rank's share of a distributed halo exchange: its padded allocation,
+// a receive buffer every neighbour writes into through CUDA IPC, and two
+// persistent batch launches (26 packs, 26 unpacks).
+struct sp_halo_plan_s {
+  HaloCfg cfg{};
+  int method = SP_HALO_FUSED;
+  int rank = 0;
+  uint8_t *alloc = nullptr;
+  uint8_t *recv = nullptr, *send = nullptr;
+  int64_t seg_total = 0;
+  std::vector<int64_t> seg_off;
+  std::vector<CommitPtr> keep;
+  Batch *pack = nullptr, *unpack = nullptr;
+  std::vector<uint8_t *> peer_send; // COPY method: where to pull segments from
+  std::vector<int64_t> copy_src_rank;
+  cudaEvent_t ev[4] = {};
+  ~sp_halo_plan_s() {
+    batch_destroy(pack);
+    batch_destroy(unpack);
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    if (recv) cudaFree(recv);
+    if (send) cudaFree(send);
+  }
+};
+
+extern "C" {
+
+sp_status sp_rt_init(int rank, int size, const char *job, int device, int64_t window_bytes, int64_t host_bytes) {
+  return guarded([&] { rt_init(rank, size, job, device, window_bytes, host_bytes); });
+}
+
+sp_status sp_rt_finalize(void) {
+  return guarded([&] { rt_finalize(); });
+}
+
+sp_status sp_rt_rank(int *rank) {
+  return guarded([&] {
+    need(rank);
+    *rank = rt_rank();
+  });
+}
+
+sp_status sp_rt_size(int *size) {
+  return guarded([&] {
+    need(size);
+    *size = rt_size();
+  });
+}
+
+sp_status sp_rt_barrier(void) {
+  return guarded([&] { rt_barrier(); });
+}
+
+sp_status sp_rt_host_send(int dst, int tag, const void *data, int64_t bytes) {
+  return guarded([&] { rt_host_send(dst, tag, data, bytes); });
+}
+
+sp_status sp_rt_host_recv(int src, int tag, void *data, int64_t cap, int64_t *bytes) {
+  return guarded([&] {
+    const int64_t n = rt_host_recv(src, tag, data, cap);
+    if (bytes) *bytes = n;
+  });
+}
+
+sp_status sp_rt_set_profile(sp_profile p) {
+  return guarded([&] { rt_set_profile(p); });
+}
+
+sp_status sp_rt_exchange_ptr(void *local, void **peers) {
+  return guarded([&] {
+    need(peers);
+    std::vector<uint8_t *> out;
+    rt_exchange_ptr(local, out);
+    for (size_t r = 0; r < out.size(); ++r) peers[r] = out[r];
+  });
+}
+
+sp_status sp_rt_choose(sp_type t, int64_t count, int *method) {
+  return guarded([&] {
+    need(method);
+    *method = rt_choose(*committed_of(t), count);
+  });
+}
+
+sp_status sp_rt_send(const void *buf, uint64_t buf_bytes, int64_t count, sp_type t, int dest, int tag, int method,
+                     int *used_method) {
+  return guarded([&] {
+    if (count < 0) fail(SP_ERR_INVALID_ARGUMENT, "send: negative count");
+    RtTrace tr{};
+    rt_send(buf, buf_bytes, count, *committed_of(t), dest, tag, method, &tr);
+    if (used_method) *used_method = tr.method;
+  });
+}
+
+sp_status sp_rt_recv(void *buf, uint64_t buf_bytes, int64_t count, sp_type t, int source, int tag,
+                     int64_t status[4]) {
+  return guarded([&] {
+    if (count < 0) fail(SP_ERR_INVALID_ARGUMENT, "recv: negative count");
+    RtStatus st{};
+    rt_recv(buf, buf_bytes, count, *committed_of(t), source, tag, &st);
+    if (status) {
+      status[0] = st.source;
+      status[1] = st.tag;
+      status[2] = st.bytes;
+      status[3] = st.method;
+    }
+  });
+}
+
+sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int method, sp_halo_plan *out) {
+  return guarded([&] {
+    need(cfgp);
+    need(alloc);
+    need(out);
+    if (method != SP_HALO_FUSED && method != SP_HALO_COPY) fail(SP_ERR_INVALID_ARGUMENT, "unknown halo method");
+    HaloCfg c{};
+    for (int a = 0; a < 3; ++a) {
+      c.ranks[a] = cfgp->ranks[a];
+      c.interior[a] = cfgp->interior[a];
+    }
+    c.radius = cfgp->radius;
+    c.elem = cfgp->element_bytes;
+    halo_validate(c);
+    if (c.ranks[0] * c.ranks[1] * c.ranks[2] != rt_size())
+      fail(SP_ERR_INVALID_ARGUMENT, "halo rank grid does not match the runtime size");
+    require_device();
+    auto p = std::make_unique<sp_halo_plan_s>();
+    p->cfg = c;
+    p->method = method;
+    p->rank = rt_rank();
+    p->alloc = static_cast<uint8_t *>(alloc);
+    const auto regions = halo_regions(c);
+    const int64_t pad = (c.interior[0] + 2 * c.radius) * (c.interior[1] + 2 * c.radius) *
+                        (c.interior[2] + 2 * c.radius) * c.elem;
+    std::vector<CommitPtr> sct, rct;
+    p->seg_off.assign(27, 0);
+    for (int k = 0; k < 26; ++k) {
+      sct.push_back(commit_def(*regions[k].send));
+      rct.push_back(commit_def(*regions[k].recv));
+      p->seg_off[k + 1] = p->seg_off[k] + sct[k]->size;
+    }
+    p->keep = sct;
+    p->keep.insert(p->keep.end(), rct.begin(), rct.end());
+    p->seg_total = p->seg_off[26];
+    cuda_check(cudaMalloc(&p->recv, static_cast<size_t>(p->seg_total)), "cudaMalloc(halo recv)");
+    if (method == SP_HALO_COPY) cuda_check(cudaMalloc(&p->send, static_cast<size_t>(p->seg_total)), "cudaMalloc");
+    std::vector<uint8_t *> peer_recv;
+    rt_exchange_ptr(p->recv, peer_recv);
+    if (method == SP_HALO_COPY) rt_exchange_ptr(p->send, p->peer_send);
+    std::vector<BatchSpec> packs, unpacks;
+    for (int j = 0; j < 26; ++j) {
+      if (method == SP_HALO_FUSED) {
+        // segment j of this rank is segment 25-j of the rank at +d_j,
+        // written straight into that rank's HBM (halo.hpp:237-254)
+        const int64_t to = halo_rank_of(c, p->rank, regions[j].dir);
+        packs.push_back({sct[j].get(), alloc, static_cast<uint64_t>(pad), 1, peer_recv[to],
+                         static_cast<uint64_t>(p->seg_total), p->seg_off[25 - j]});
+      } else {
+        packs.push_back({sct[j].get(), alloc, static_cast<uint64_t>(pad), 1, p->send,
+                         static_cast<uint64_t>(p->seg_total), p->seg_off[j]});
+        p->copy_src_rank.push_back(halo_rank_of(c, p->rank, regions[j].dir));
+      }
+      unpacks.push_back({rct[j].get(), p->recv, static_cast<uint64_t>(p->seg_total), 1, alloc,
+                         static_cast<uint64_t>(pad), p->seg_off[j]});
+    }
+    p->pack = batch_create(packs, false);
+    p->unpack = batch_create(unpacks, true);
+    for (auto &e : p->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    *out = p.release();
+  });
+}
+
+// collective; times[0..3] = pack, exchange, unpack, whole iteration (s),
+// measured with CUDA events on this rank's stream
+sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
+  return guarded([&] {
+    need(p);
+    cudaStream_t s = static_cast<cudaStream_t>(rt_stream());
+    rt_barrier(); // every neighbour has consumed the previous iteration
+    cuda_check(cudaEventRecord(p->ev[0], s), "cudaEventRecord");
+    batch_execute(*p->pack, s);
+    cuda_check(cudaEventRecord(p->ev[1], s), "cudaEventRecord");
+    if (p->method == SP_HALO_COPY) {
+      cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+      rt_barrier(); // all send buffers packed
+      for (int k = 0; k < 26; ++k) {
+        const int64_t from = p->copy_src_rank[k];
+        cuda_check(cudaMemcpyAsync(p->recv + p->seg_off[k], p->peer_send[from] + p->seg_off[25 - k],
+                                   static_cast<size_t>(p->seg_off[k + 1] - p->seg_off[k]), cudaMemcpyDefault, s),
+                   "segment copy");
+      }
+    }
+    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    rt_barrier(); // every segment addressed to this rank has landed
+    cuda_check(cudaEventRecord(p->ev[2], s), "cudaEventRecord");
+    batch_execute(*p->unpack, s);
+    cuda_check(cudaEventRecord(p->ev[3], s), "cudaEventRecord");
+    cuda_check(cudaEventSynchronize(p->ev[3]), "cudaEventSynchronize");
+    if (times) {
+      float a = 0, b = 0, d = 0, t = 0;
+      cudaEventElapsedTime(&a, p->ev[0], p->ev[1]);
+      cudaEventElapsedTime(&b, p->ev[1], p->ev[2]);
+      cudaEventElapsedTime(&d, p->ev[2], p->ev[3]);
+      cudaEventElapsedTime(&t, p->ev[0], p->ev[3]);
+      times[0] = a * 1e-3;
+      times[1] = b * 1e-3;
+      times[2] = d * 1e-3;
+      times[3] = t * 1e-3;
+    }
+  });
+}
+
+sp_status sp_halo_plan_free(sp_halo_plan p) {
+  delete p;
+  return SP_OK;
+}
+
+} // extern "C"

@@ -1,0 +1,35 @@
+// rt.hpp -- node-local multi-process runtime (internal).
+#pragma once
+
+#include <vector>
+
+#include "core.hpp"
+#include "model.hpp"
+
+namespace spb {
+
+struct RtTrace {
+  int method;
+  int64_t bytes;
+};
+struct RtStatus {
+  int source, tag, method;
+  int64_t bytes;
+};
+
+void rt_init(int rank, int size, const char *name, int device, int64_t window_bytes, int64_t host_bytes);
+void rt_finalize();
+int rt_rank();
+int rt_size();
+void rt_barrier();
+void rt_host_send(int dst, int tag, const void *data, int64_t bytes);
+int64_t rt_host_recv(int src, int tag, void *data, int64_t cap);
+void rt_exchange_ptr(void *local, std::vector<uint8_t *> &out);
+void rt_send(const void *buf, uint64_t buf_bytes, int64_t count, const Committed &ct, int dest, int tag, int method,
+             RtTrace *trace);
+void rt_recv(void *buf, uint64_t buf_bytes, int64_t count, const Committed &ct, int source, int tag, RtStatus *st);
+void rt_set_profile(sp_profile_s *p);
+int rt_choose(const Committed &ct, int64_t count);
+void *rt_stream();
+
+} // namespace spb

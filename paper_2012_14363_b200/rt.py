@@ -1,0 +1,108 @@
+"""Node-local multi-process runtime (one process per GPU): bootstrap,
+barriers, IPC pointer exchange, datatype Send/Recv with the three transfer
+methods of the paper (device / one-shot / staged) selected by the model,
+and the distributed halo-exchange plan. Backs the MPI surface (libtempi)."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import _buffer, _check, _capi
+from ._capi import lib
+
+DEVICE, ONESHOT, STAGED = 1, 0, 2
+AUTO = -1
+
+
+def init(rank: int, size: int, job: str, device: int = -1, window_bytes: int = 256 << 20,
+         host_bytes: int = 256 << 20):
+    _check(lib.sp_rt_init(rank, size, job.encode(), device, window_bytes if device >= 0 else 0,
+                          host_bytes if device >= 0 else 0))
+
+
+def finalize():
+    _check(lib.sp_rt_finalize())
+
+
+def rank() -> int:
+    v = C.c_int()
+    _check(lib.sp_rt_rank(C.byref(v)))
+    return v.value
+
+
+def size() -> int:
+    v = C.c_int()
+    _check(lib.sp_rt_size(C.byref(v)))
+    return v.value
+
+
+def barrier():
+    _check(lib.sp_rt_barrier())
+
+
+def host_send(dst: int, tag: int, payload: bytes):
+    buf = C.create_string_buffer(payload, len(payload))
+    _check(lib.sp_rt_host_send(dst, tag, buf, len(payload)))
+
+
+def host_recv(src: int, tag: int) -> bytes:
+    buf = C.create_string_buffer(16)
+    n = C.c_int64()
+    _check(lib.sp_rt_host_recv(src, tag, buf, 16, C.byref(n)))
+    return buf.raw[:n.value]
+
+
+def exchange_ptr(tensor_or_ptr):
+    n = size()
+    peers = (C.c_void_p * n)()
+    ptr = tensor_or_ptr if isinstance(tensor_or_ptr, int) else tensor_or_ptr.data_ptr()
+    _check(lib.sp_rt_exchange_ptr(ptr, peers))
+    return [p or 0 for p in peers]
+
+
+def set_profile(profile):
+    _check(lib.sp_rt_set_profile(profile.handle if profile is not None else None))
+
+
+def choose(ct, count: int) -> int:
+    m = C.c_int()
+    _check(lib.sp_rt_choose(ct.handle, count, C.byref(m)))
+    return m.value
+
+
+def send(buf, count: int, ct, dest: int, tag: int = 0, method: int = AUTO) -> int:
+    a, n, _ = _buffer(buf, False)
+    used = C.c_int()
+    _check(lib.sp_rt_send(a, n, count, ct.handle, dest, tag, method, C.byref(used)))
+    return used.value
+
+
+def recv(buf, count: int, ct, source: int = -1, tag: int = -1):
+    a, n, _ = _buffer(buf, True)
+    st = (C.c_int64 * 4)()
+    _check(lib.sp_rt_recv(a, n, count, ct.handle, source, tag, st))
+    return {"source": st[0], "tag": st[1], "bytes": st[2], "method": st[3]}
+
+
+class HaloPlan:
+    def __init__(self, cfg, alloc, method: int = 0):
+        a, n, _ = _buffer(alloc, True)
+        h = C.c_void_p()
+        _check(lib.sp_halo_plan_create(C.byref(cfg.c()), a, method, C.byref(h)))
+        self.handle = h.value
+
+    def exchange(self):
+        t = (C.c_double * 4)()
+        _check(lib.sp_halo_plan_exchange(self.handle, t))
+        return {"pack": t[0], "exchange": t[1], "unpack": t[2], "iteration": t[3]}
+
+    def free(self):
+        if self.handle:
+            lib.sp_halo_plan_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

@@ -1,0 +1,142 @@
+"""The node-local runtime under the MPI surface, exercised with real
+processes. CPU: bootstrap, barriers and control messages (world 2 and 3).
+GPU (two processes sharing cuda:0 through CUDA IPC, the same code path as
+two NVLink peers): datatype Send/Recv with every transfer method, bit-exact
+against the oracle, and the distributed halo exchange verified cell by
+cell."""
+import multiprocessing as mp
+import os
+import sys
+import traceback
+import uuid
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _spawn(target, world, *args, timeout=240):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    job = uuid.uuid4().hex[:12]
+    ps = [ctx.Process(target=_entry, args=(target, r, world, job, q) + args) for r in range(world)]
+    for p in ps:
+        p.start()
+    results = {}
+    try:
+        for _ in range(world):
+            r, ok, payload = q.get(timeout=timeout)
+            results[r] = (ok, payload)
+    finally:
+        for p in ps:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    for r in range(world):
+        ok, payload = results[r]
+        assert ok, f"rank {r}: {payload}"
+    return {r: results[r][1] for r in range(world)}
+
+
+def _entry(target, rank, world, job, q, *args):
+    sys.path.insert(0, ROOT)
+    try:
+        q.put((rank, True, target(rank, world, job, *args)))
+    except Exception:
+        q.put((rank, False, traceback.format_exc()))
+
+
+# ------------------------------------------------------------ CPU control plane
+def _control(rank, world, job):
+    import paper_2012_14363_b200.rt as rt
+    rt.init(rank, world, job, device=-1)
+    assert rt.rank() == rank and rt.size() == world
+    for _ in range(200):
+        rt.barrier()
+    # ring of control messages, two laps, tags kept apart
+    right, left = (rank + 1) % world, (rank - 1) % world
+    rt.host_send(right, 7, f"r{rank}".encode())
+    rt.host_send(right, 9, b"tag9")
+    got9 = rt.host_recv(left, 9)
+    got7 = rt.host_recv(left, 7)
+    assert got7 == f"r{left}".encode() and got9 == b"tag9"
+    rt.finalize()
+    return "ok"
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_runtime_control_plane(world):
+    assert set(_spawn(_control, world).values()) == {"ok"}
+
+
+# ------------------------------------------------------------ GPU data plane
+def _sendrecv(rank, world, job):
+    import torch
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.rt as rt
+    import paper_2012_14363_b200.model as M
+    from oracle.pyoracle import oracle
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=64 << 20, host_bytes=64 << 20)
+    rt.set_profile(M.load_profile_file(os.path.join(ROOT, "tests", "golden", "default.profile")))
+    # cfg4-shaped object: subarray block E0=64 at 1 KiB pitch, 3D
+    prog = [4, 3, 0, 128, 64, 16, 64, 32, 8, 16, 8, 4, 0, 0]
+    ct = sp.commit_type(sp.from_program(prog))
+    out = []
+    for i, method in enumerate([rt.DEVICE, rt.ONESHOT, rt.STAGED, rt.AUTO]):
+        count = 1 + i % 2
+        span = (count - 1) * ct.extent + ct.span
+        rng = np.random.default_rng(100 + i)
+        host = rng.integers(0, 256, span, dtype=np.uint8)
+        if rank == 0:
+            used = rt.send(torch.from_numpy(host).cuda(), count, ct, 1, tag=i, method=method)
+            out.append(used)
+        else:
+            dst = torch.full((span,), 0x11, dtype=torch.uint8, device="cuda")
+            st = rt.recv(dst, count, ct, source=0, tag=i)
+            packed = np.zeros(count * ct.size, np.uint8)
+            assert oracle().pack(prog, host, count, packed, 0)[0] == 0
+            want = np.full(span, 0x11, np.uint8)
+            assert oracle().unpack(prog, packed, 0, count, want)[0] == 0
+            assert np.array_equal(dst.cpu().numpy(), want), (method, st)
+            assert st["bytes"] == count * ct.size and st["source"] == 0 and st["tag"] == i
+            out.append(st["method"])
+    rt.finalize()
+    return out
+
+
+@pytest.mark.gpu
+def test_sendrecv_every_method_two_processes(cuda):
+    res = _spawn(_sendrecv, 2)
+    assert res[0][:3] == [1, 0, 2] and res[1][:3] == [1, 0, 2]
+    assert res[0][3] == res[1][3]  # the model's choice, seen identically on both sides
+
+
+def _halo(rank, world, job, ranks, method):
+    import torch
+    import paper_2012_14363_b200.halo as H
+    import paper_2012_14363_b200.rt as rt
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=1 << 20, host_bytes=1 << 20)
+    cfg = H.HaloConfig(ranks, (12, 10, 8), 2, 16)
+    pad = 16 * 14 * 12 * 16
+    alloc = torch.empty(pad, dtype=torch.uint8, device="cuda")
+    H.fill(cfg, rank, alloc)
+    plan = rt.HaloPlan(cfg, alloc, method)
+    for _ in range(3):
+        t = plan.exchange()
+    bad = H.verify(cfg, rank, alloc)
+    plan.free()
+    rt.finalize()
+    return bad, t
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ranks,method", [((2, 1, 1), 0), ((2, 1, 1), 1), ((1, 3, 1), 0)])
+def test_distributed_halo_exchange(cuda, ranks, method):
+    world = ranks[0] * ranks[1] * ranks[2]
+    res = _spawn(_halo, world, ranks, method)
+    for r, (bad, t) in res.items():
+        assert bad == 0, (r, bad)
+        assert t["pack"] > 0 and t["iteration"] >= t["pack"]
