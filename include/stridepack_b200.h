@@ -310,6 +310,21 @@ sp_status sp_rt_send(const void *buf, uint64_t buf_bytes, int64_t count,
 sp_status sp_rt_recv(void *buf, uint64_t buf_bytes, int64_t count, sp_type t,
                      int source, int tag, int64_t status[4]);
 
+/* MPI_Neighbor_alltoallv over a distributed graph (collective over every
+ * runtime rank): block i (sendcounts[i] objects of sendtype at
+ * sdispls[i]*extent) goes to dests[i]; block j from sources[j] lands at
+ * rdispls[j]*extent(recvtype). ONE batch launch per rank packs every block
+ * with sendtype straight into the receiving rank's buffer through CUDA IPC.
+ * recvtype must be dense bytes (MPI_PACKED/MPI_BYTE-like). The k-th edge to
+ * a rank matches that rank's k-th edge from this one. */
+sp_status sp_rt_neighbor_alltoallv(const void *sendbuf,
+                                   const int64_t *sendcounts,
+                                   const int64_t *sdispls, int64_t outdegree,
+                                   const int *dests, sp_type sendtype,
+                                   void *recvbuf, const int64_t *recvcounts,
+                                   const int64_t *rdispls, int64_t indegree,
+                                   const int *sources, sp_type recvtype);
+
 /* distributed halo exchange: one rank per process (grid size == runtime
  * size); `alloc` is this rank's padded allocation on its device. */
 typedef struct sp_halo_plan_s *sp_halo_plan;

@@ -130,6 +130,22 @@ sp_status sp_rt_recv(void *buf, uint64_t buf_bytes, int64_t count, sp_type t, in
   });
 }
 
+sp_status sp_rt_neighbor_alltoallv(const void *sendbuf, const int64_t *sendcounts, const int64_t *sdispls,
+                                   int64_t outdegree, const int *dests, sp_type sendtype, void *recvbuf,
+                                   const int64_t *recvcounts, const int64_t *rdispls, int64_t indegree,
+                                   const int *sources, sp_type recvtype) {
+  return guarded([&] {
+    if (outdegree < 0 || indegree < 0) fail(SP_ERR_INVALID_ARGUMENT, "negative degree");
+    if ((outdegree && (!sendcounts || !sdispls || !dests)) || (indegree && (!recvcounts || !rdispls || !sources)))
+      fail(SP_ERR_INVALID_ARGUMENT, "null neighbour arrays");
+    std::vector<int64_t> sc(sendcounts, sendcounts + outdegree), sd(sdispls, sdispls + outdegree);
+    std::vector<int64_t> rc(recvcounts, recvcounts + indegree), rd(rdispls, rdispls + indegree);
+    std::vector<int> ds(dests, dests + outdegree), ss(sources, sources + indegree);
+    rt_neighbor_alltoallv(static_cast<const uint8_t *>(sendbuf), sc, sd, *committed_of(sendtype),
+                          static_cast<uint8_t *>(recvbuf), rc, rd, *committed_of(recvtype), ss, ds);
+  });
+}
+
 sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int method, sp_halo_plan *out) {
   return guarded([&] {
     need(cfgp);

@@ -35,6 +35,7 @@ namespace {
 constexpr uint64_t kMagic = 0x5350423230305254ull; // "SPB200RT"
 constexpr int kMaxRanks = 64;
 constexpr int kRing = 32;
+constexpr int kMaxEdges = 256;
 
 struct Msg {
   uint32_t kind;
@@ -63,6 +64,9 @@ struct Slot {
   cudaIpcMemHandle_t xh;      // publication area of sp_rt_exchange_ptr
   int64_t xoff;
   int64_t xbytes;
+  int32_t nedges;             // neighbour-exchange in-edges: (src, offset, bytes)
+  int32_t pad2;
+  int64_t edges[kMaxEdges][3];
 };
 
 struct Shm {
@@ -499,5 +503,87 @@ int rt_choose(const Committed &ct, int64_t count) {
 }
 
 void *rt_stream() { return rt().stream; }
+
+// ------------------------------------------------------------ neighbour exchange
+// MPI_Neighbor_alltoallv over a distributed graph: every rank publishes its
+// receive buffer (CUDA IPC) and the (source, offset, bytes) of each in-edge;
+// each rank then runs ONE batch launch that packs every out-edge block with
+// the send type straight into the matching receiver's buffer (the k-th edge
+// to a rank matches that rank's k-th edge from us, MPI-3.1 §7.6), and a
+// barrier publishes completion. Batches are cached per call signature, so
+// an iterative halo loop re-launches a persistent plan.
+namespace {
+struct NbrCacheEntry {
+  std::string key;
+  Batch *batch;
+};
+std::deque<NbrCacheEntry> g_nbr_cache;
+} // namespace
+
+void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &send_counts,
+                           const std::vector<int64_t> &send_displs, const Committed &st, uint8_t *recvbuf,
+                           const std::vector<int64_t> &recv_counts, const std::vector<int64_t> &recv_displs,
+                           const Committed &rtp, const std::vector<int> &sources, const std::vector<int> &dests) {
+  Runtime &R = rt();
+  if (static_cast<int>(sources.size()) > kMaxEdges) fail(SP_ERR_UNSUPPORTED, "neighbour exchange: indegree > 256");
+  const bool dense_recv = rtp.form == SP_FORM_STRIDED && rtp.sb.ndims() == 1 && rtp.sb.start == 0 &&
+                          rtp.extent == rtp.size;
+  if (!dense_recv && rtp.form != SP_FORM_EMPTY)
+    fail(SP_ERR_UNSUPPORTED, "neighbour exchange: receive type must be contiguous bytes (e.g. MPI_PACKED)");
+  Slot &me = R.shm->slots[R.rank];
+  if (recvbuf) {
+    ipc_handle_of(recvbuf, &me.xh, &me.xoff);
+    me.xbytes = 1;
+  } else {
+    me.xbytes = 0;
+  }
+  me.nedges = static_cast<int32_t>(sources.size());
+  for (size_t j = 0; j < sources.size(); ++j) {
+    me.edges[j][0] = sources[j];
+    me.edges[j][1] = recv_displs[j] * rtp.extent;
+    me.edges[j][2] = recv_counts[j] * rtp.size;
+  }
+  rt_barrier(); // layouts published, every receive buffer is owned by the call
+  std::string key(reinterpret_cast<const char *>(&sendbuf), sizeof(sendbuf));
+  std::vector<BatchSpec> jobs;
+  std::vector<int> seen(R.size, 0);
+  for (size_t i = 0; i < dests.size(); ++i) {
+    const int d = dests[i];
+    const int occ = seen[d]++;
+    const Slot &peer = R.shm->slots[d];
+    int hit = -1;
+    for (int j = 0, k = 0; j < peer.nedges; ++j)
+      if (peer.edges[j][0] == R.rank && k++ == occ) {
+        hit = j;
+        break;
+      }
+    if (hit < 0) fail(SP_ERR_INVALID_ARGUMENT, "neighbour exchange: destination does not list this rank as source");
+    const int64_t bytes = send_counts[i] * st.size;
+    if (bytes > peer.edges[hit][2]) fail(SP_ERR_BUFFER_TOO_SMALL, "neighbour exchange: message truncated");
+    if (bytes == 0) continue;
+    uint8_t *base = d == R.rank ? recvbuf : open_ipc(peer.xh) + peer.xoff;
+    jobs.push_back({&st, sendbuf + send_displs[i] * st.extent, UINT64_MAX, send_counts[i], base, UINT64_MAX,
+                    peer.edges[hit][1]});
+    const int64_t sig[4] = {reinterpret_cast<int64_t>(base), peer.edges[hit][1], send_counts[i], send_displs[i]};
+    key.append(reinterpret_cast<const char *>(sig), sizeof(sig));
+  }
+  key.append(reinterpret_cast<const char *>(&st), sizeof(void *));
+  Batch *b = nullptr;
+  for (auto &e : g_nbr_cache)
+    if (e.key == key) b = e.batch;
+  if (!b && !jobs.empty()) {
+    b = batch_create(jobs, false);
+    g_nbr_cache.push_back({key, b});
+    if (g_nbr_cache.size() > 16) {
+      batch_destroy(g_nbr_cache.front().batch);
+      g_nbr_cache.pop_front();
+    }
+  }
+  if (b) {
+    batch_execute(*b, R.stream);
+    cuda_check(cudaStreamSynchronize(R.stream), "cudaStreamSynchronize(neighbor)");
+  }
+  rt_barrier(); // every block addressed to this rank has landed
+}
 
 } // namespace spb

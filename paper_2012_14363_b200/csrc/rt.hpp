@@ -31,5 +31,9 @@ void rt_recv(void *buf, uint64_t buf_bytes, int64_t count, const Committed &ct, 
 void rt_set_profile(sp_profile_s *p);
 int rt_choose(const Committed &ct, int64_t count);
 void *rt_stream();
+void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &send_counts,
+                           const std::vector<int64_t> &send_displs, const Committed &st, uint8_t *recvbuf,
+                           const std::vector<int64_t> &recv_counts, const std::vector<int64_t> &recv_displs,
+                           const Committed &rtp, const std::vector<int> &sources, const std::vector<int> &dests);
 
 } // namespace spb

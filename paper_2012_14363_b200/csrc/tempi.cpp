@@ -1,0 +1,589 @@
+// tempi.cpp -- the MPI surface (libtempi_b200.so), include/mpi.h.
+//
+// TEMPI's interposer exports MPI_* and forwards what it does not accelerate
+// to the system MPI through PMPI_* (PAPER.md:781-796). Here MPI_* is the
+// accelerated layer (datatypes canonicalised at MPI_Type_commit, sm_100a
+// pack/unpack kernels, model-selected transfers, fused pack-to-peer
+// neighbour exchange) and PMPI_* the base layer over the node-local runtime
+// (rt.cpp), since the image ships no MPI library.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <unistd.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "mpi.h"
+#include "stridepack_b200.h"
+
+namespace {
+
+struct Comm {
+  int kind = 0; // 0 world/self, 1 dist graph, 2 cartesian
+  std::vector<int> sources, dests;
+  std::vector<int> dims, periods;
+};
+
+struct State {
+  bool initialized = false, finalized = false;
+  int rank = 0, size = 1, device = -1;
+  std::unordered_map<int, sp_type> types; // MPI handle -> engine handle
+  int next_type = 100;
+  std::unordered_map<int, Comm> comms;
+  int next_comm = 100;
+  int forced_method = -1;
+  sp_profile profile = nullptr;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+};
+
+State &S() {
+  static State s;
+  return s;
+}
+
+int to_mpi(sp_status st) {
+  switch (st) {
+  case SP_OK: return MPI_SUCCESS;
+  case SP_ERR_INVALID_ARGUMENT: return MPI_ERR_ARG;
+  case SP_ERR_UNSUPPORTED_ORDER: return MPI_ERR_ARG;
+  case SP_ERR_INVALID_LAYOUT: return MPI_ERR_TYPE;
+  case SP_ERR_BUFFER_TOO_SMALL: return MPI_ERR_TRUNCATE;
+  case SP_ERR_OVERLAPPING_LAYOUT: return MPI_ERR_TYPE;
+  case SP_ERR_UNSUPPORTED: return MPI_ERR_UNSUPPORTED_OPERATION;
+  case SP_ERR_INVALID_HANDLE: return MPI_ERR_TYPE;
+  default: return MPI_ERR_INTERN;
+  }
+}
+
+#define TRY(expr)                                                                                                \
+  do {                                                                                                           \
+    const sp_status _st = (expr);                                                                                \
+    if (_st != SP_OK) {                                                                                          \
+      if (std::getenv("TEMPI_VERBOSE")) std::fprintf(stderr, "tempi: %s: %s\n", #expr, sp_last_error());        \
+      return to_mpi(_st);                                                                                        \
+    }                                                                                                            \
+  } while (0)
+
+int env_int(const char *a, const char *b, const char *c, int dflt) {
+  for (const char *k : {a, b, c}) {
+    if (!k) continue;
+    if (const char *v = std::getenv(k)) return std::atoi(v);
+  }
+  return dflt;
+}
+
+// engine handle of an MPI datatype
+bool lookup(MPI_Datatype t, sp_type *out) {
+  auto it = S().types.find(t);
+  if (it == S().types.end()) return false;
+  *out = it->second;
+  return true;
+}
+
+#define TYPE(t, var)                                                                                             \
+  sp_type var;                                                                                                   \
+  if (!lookup((t), &var)) return MPI_ERR_TYPE
+
+int new_type(sp_type h, MPI_Datatype *out) {
+  if (!out) return MPI_ERR_ARG;
+  std::lock_guard<std::mutex> lk(S().mu);
+  const int id = S().next_type++;
+  S().types[id] = h;
+  *out = id;
+  return MPI_SUCCESS;
+}
+
+const Comm *comm_of(MPI_Comm c) {
+  if (c == MPI_COMM_WORLD || c == MPI_COMM_SELF) {
+    static Comm world;
+    return &world;
+  }
+  auto it = S().comms.find(c);
+  return it == S().comms.end() ? nullptr : &it->second;
+}
+
+std::string default_profile_path() {
+  Dl_info info{};
+  if (dladdr(reinterpret_cast<void *>(&default_profile_path), &info) && info.dli_fname) {
+    std::string p(info.dli_fname);
+    const auto slash = p.rfind('/');
+    if (slash != std::string::npos) return p.substr(0, slash) + "/../profiles/b200.profile";
+  }
+  return "";
+}
+
+} // namespace
+
+extern "C" {
+
+// ============================================================ runtime
+int PMPI_Init(int *, char ***) {
+  State &s = S();
+  if (s.initialized) return MPI_ERR_OTHER;
+  s.rank = env_int("TEMPI_RANK", "RANK", "OMPI_COMM_WORLD_RANK", 0);
+  s.size = env_int("TEMPI_SIZE", "WORLD_SIZE", "OMPI_COMM_WORLD_SIZE", 1);
+  const int local = env_int("TEMPI_LOCAL_RANK", "LOCAL_RANK", "OMPI_COMM_WORLD_LOCAL_RANK", s.rank);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess) {
+    cudaGetLastError();
+    ndev = 0;
+  }
+  s.device = ndev > 0 ? env_int("TEMPI_DEVICE", nullptr, nullptr, local % ndev) : -1;
+  std::string job;
+  if (const char *j = std::getenv("TEMPI_JOB")) {
+    job = j;
+  } else if (const char *j2 = std::getenv("TORCHELASTIC_RUN_ID")) {
+    job = std::string(j2) + "_" + (std::getenv("MASTER_PORT") ? std::getenv("MASTER_PORT") : "0");
+  } else if (const char *p = std::getenv("MASTER_PORT")) {
+    job = std::string("port") + p;
+  } else {
+    job = "single" + std::to_string(getpid());
+  }
+  const int64_t window = static_cast<int64_t>(env_int("TEMPI_WINDOW_MB", nullptr, nullptr, 256)) << 20;
+  const int64_t host = static_cast<int64_t>(env_int("TEMPI_HOST_MB", nullptr, nullptr, 256)) << 20;
+  TRY(sp_rt_init(s.rank, s.size, job.c_str(), s.device, window, host));
+  // predefined types
+  const std::pair<int, int> named[] = {{MPI_BYTE, SP_BYTE},   {MPI_CHAR, SP_BYTE},  {MPI_INT, SP_INT},
+                                       {MPI_FLOAT, SP_FLOAT}, {MPI_DOUBLE, SP_DOUBLE},
+                                       {MPI_PACKED, SP_BYTE}, {MPI_UNSIGNED_CHAR, SP_BYTE}};
+  for (auto [m, k] : named) {
+    sp_type h = 0;
+    TRY(sp_type_named(k, &h));
+    TRY(sp_type_commit(h));
+    s.types[m] = h;
+  }
+  if (s.device >= 0) {
+    cudaSetDevice(s.device);
+    cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
+  }
+  std::string prof = std::getenv("TEMPI_PROFILE") ? std::getenv("TEMPI_PROFILE") : default_profile_path();
+  if (!prof.empty() && sp_profile_load(prof.c_str(), &s.profile) == SP_OK) sp_rt_set_profile(s.profile);
+  if (const char *m = std::getenv("TEMPI_METHOD")) s.forced_method = std::atoi(m);
+  s.initialized = true;
+  return MPI_SUCCESS;
+}
+
+int MPI_Init(int *argc, char ***argv) { return PMPI_Init(argc, argv); }
+
+int MPI_Init_thread(int *argc, char ***argv, int, int *provided) {
+  if (provided) *provided = MPI_THREAD_SERIALIZED;
+  return PMPI_Init(argc, argv);
+}
+
+int MPI_Initialized(int *flag) {
+  if (flag) *flag = S().initialized;
+  return MPI_SUCCESS;
+}
+
+int PMPI_Finalize(void) {
+  State &s = S();
+  if (!s.initialized || s.finalized) return MPI_ERR_OTHER;
+  TRY(sp_rt_finalize());
+  if (s.stream) cudaStreamDestroy(s.stream);
+  if (s.profile) sp_profile_free(s.profile);
+  s.finalized = true;
+  return MPI_SUCCESS;
+}
+
+int MPI_Finalize(void) { return PMPI_Finalize(); }
+
+int MPI_Finalized(int *flag) {
+  if (flag) *flag = S().finalized;
+  return MPI_SUCCESS;
+}
+
+int PMPI_Comm_rank(MPI_Comm comm, int *rank) {
+  if (!comm_of(comm) || !rank) return MPI_ERR_COMM;
+  *rank = comm == MPI_COMM_SELF ? 0 : S().rank;
+  return MPI_SUCCESS;
+}
+int MPI_Comm_rank(MPI_Comm comm, int *rank) { return PMPI_Comm_rank(comm, rank); }
+
+int PMPI_Comm_size(MPI_Comm comm, int *size) {
+  if (!comm_of(comm) || !size) return MPI_ERR_COMM;
+  *size = comm == MPI_COMM_SELF ? 1 : S().size;
+  return MPI_SUCCESS;
+}
+int MPI_Comm_size(MPI_Comm comm, int *size) { return PMPI_Comm_size(comm, size); }
+
+int PMPI_Barrier(MPI_Comm comm) {
+  if (!comm_of(comm)) return MPI_ERR_COMM;
+  if (comm == MPI_COMM_SELF) return MPI_SUCCESS;
+  TRY(sp_rt_barrier());
+  return MPI_SUCCESS;
+}
+int MPI_Barrier(MPI_Comm comm) { return PMPI_Barrier(comm); }
+
+int MPI_Abort(MPI_Comm, int errorcode) {
+  std::fprintf(stderr, "MPI_Abort(%d) on rank %d\n", errorcode, S().rank);
+  std::_Exit(errorcode ? errorcode : 1);
+}
+
+double MPI_Wtime(void) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+int MPI_Error_string(int code, char *string, int *len) {
+  if (!string || !len) return MPI_ERR_ARG;
+  const char *m = code == MPI_SUCCESS ? "success" : code == MPI_ERR_TRUNCATE ? "message truncated"
+                  : code == MPI_ERR_TYPE ? "invalid datatype" : code == MPI_ERR_ARG ? "invalid argument"
+                  : code == MPI_ERR_UNSUPPORTED_OPERATION ? "unsupported operation" : "error";
+  std::snprintf(string, MPI_MAX_ERROR_STRING, "%s", m);
+  *len = static_cast<int>(std::strlen(string));
+  return MPI_SUCCESS;
+}
+
+int MPI_Get_count(const MPI_Status *status, MPI_Datatype datatype, int *count) {
+  TYPE(datatype, h);
+  int64_t size = 0;
+  TRY(sp_type_size(h, &size));
+  if (!status || !count) return MPI_ERR_ARG;
+  *count = size ? (status->bytes % size ? MPI_UNDEFINED : static_cast<int>(status->bytes / size)) : 0;
+  return MPI_SUCCESS;
+}
+
+// ============================================================ datatypes
+int MPI_Type_contiguous(int count, MPI_Datatype oldtype, MPI_Datatype *newtype) {
+  TYPE(oldtype, in);
+  sp_type h;
+  TRY(sp_type_contiguous(count, in, &h));
+  return new_type(h, newtype);
+}
+
+int MPI_Type_vector(int count, int blocklength, int stride, MPI_Datatype oldtype, MPI_Datatype *newtype) {
+  TYPE(oldtype, in);
+  sp_type h;
+  TRY(sp_type_vector(count, blocklength, stride, in, &h));
+  return new_type(h, newtype);
+}
+
+int MPI_Type_create_hvector(int count, int blocklength, MPI_Aint stride, MPI_Datatype oldtype,
+                            MPI_Datatype *newtype) {
+  TYPE(oldtype, in);
+  sp_type h;
+  TRY(sp_type_hvector(count, blocklength, stride, in, &h));
+  return new_type(h, newtype);
+}
+
+// MPI_ORDER_C lists the slowest dimension first; the engine (like the
+// reference, type_def.hpp:75) keeps dimension 0 innermost, so C order is
+// reversed and Fortran order passed through.
+int MPI_Type_create_subarray(int ndims, const int sizes[], const int subsizes[], const int starts[], int order,
+                             MPI_Datatype oldtype, MPI_Datatype *newtype) {
+  TYPE(oldtype, in);
+  if (ndims < 1 || !sizes || !subsizes || !starts) return MPI_ERR_ARG;
+  if (order != MPI_ORDER_C && order != MPI_ORDER_FORTRAN) return MPI_ERR_ARG;
+  std::vector<int64_t> sz(ndims), sub(ndims), off(ndims);
+  for (int i = 0; i < ndims; ++i) {
+    const int j = order == MPI_ORDER_C ? ndims - 1 - i : i;
+    sz[i] = sizes[j];
+    sub[i] = subsizes[j];
+    off[i] = starts[j];
+    if (off[i] + sub[i] > sz[i]) return MPI_ERR_ARG; // MPI forbids the oversized case
+  }
+  sp_type h;
+  TRY(sp_type_subarray(ndims, sz.data(), sub.data(), off.data(), in, SP_ORDER_C, &h));
+  return new_type(h, newtype);
+}
+
+int PMPI_Type_commit(MPI_Datatype *datatype) {
+  if (!datatype) return MPI_ERR_ARG;
+  TYPE(*datatype, h);
+  TRY(sp_type_commit(h));
+  return MPI_SUCCESS;
+}
+int MPI_Type_commit(MPI_Datatype *datatype) { return PMPI_Type_commit(datatype); }
+
+int MPI_Type_free(MPI_Datatype *datatype) {
+  if (!datatype || *datatype < 100) return MPI_ERR_TYPE;
+  TYPE(*datatype, h);
+  TRY(sp_type_free(h));
+  std::lock_guard<std::mutex> lk(S().mu);
+  S().types.erase(*datatype);
+  *datatype = MPI_DATATYPE_NULL;
+  return MPI_SUCCESS;
+}
+
+int MPI_Type_size(MPI_Datatype datatype, int *size) {
+  TYPE(datatype, h);
+  if (!size) return MPI_ERR_ARG;
+  int64_t s = 0;
+  TRY(sp_type_size(h, &s));
+  *size = static_cast<int>(s);
+  return MPI_SUCCESS;
+}
+
+int MPI_Type_get_extent(MPI_Datatype datatype, MPI_Aint *lb, MPI_Aint *extent) {
+  TYPE(datatype, h);
+  if (!lb || !extent) return MPI_ERR_ARG;
+  int64_t e = 0;
+  TRY(sp_type_extent(h, &e));
+  *lb = 0;
+  *extent = e;
+  return MPI_SUCCESS;
+}
+
+// ============================================================ packing
+int PMPI_Pack(const void *inbuf, int incount, MPI_Datatype datatype, void *outbuf, int outsize, int *position,
+              MPI_Comm comm) {
+  if (!comm_of(comm)) return MPI_ERR_COMM;
+  if (!position || outsize < 0) return MPI_ERR_ARG;
+  if (incount < 0) return MPI_ERR_COUNT;
+  if (incount == 0) return MPI_SUCCESS; // MPI allows it; the engine (like pack.hpp:102) does not
+  TYPE(datatype, h);
+  int64_t pos = *position;
+  TRY(sp_pack(inbuf, UINT64_MAX, h, incount, outbuf, static_cast<uint64_t>(outsize), &pos, S().stream));
+  if (S().stream && cudaStreamSynchronize(S().stream) != cudaSuccess) return MPI_ERR_INTERN;
+  *position = static_cast<int>(pos);
+  return MPI_SUCCESS;
+}
+int MPI_Pack(const void *inbuf, int incount, MPI_Datatype datatype, void *outbuf, int outsize, int *position,
+             MPI_Comm comm) {
+  return PMPI_Pack(inbuf, incount, datatype, outbuf, outsize, position, comm);
+}
+
+int PMPI_Unpack(const void *inbuf, int insize, int *position, void *outbuf, int outcount, MPI_Datatype datatype,
+                MPI_Comm comm) {
+  if (!comm_of(comm)) return MPI_ERR_COMM;
+  if (!position || insize < 0) return MPI_ERR_ARG;
+  if (outcount < 0) return MPI_ERR_COUNT;
+  if (outcount == 0) return MPI_SUCCESS;
+  TYPE(datatype, h);
+  int64_t pos = *position;
+  TRY(sp_unpack(inbuf, static_cast<uint64_t>(insize), &pos, h, outcount, outbuf, UINT64_MAX, S().stream));
+  if (S().stream && cudaStreamSynchronize(S().stream) != cudaSuccess) return MPI_ERR_INTERN;
+  *position = static_cast<int>(pos);
+  return MPI_SUCCESS;
+}
+int MPI_Unpack(const void *inbuf, int insize, int *position, void *outbuf, int outcount, MPI_Datatype datatype,
+               MPI_Comm comm) {
+  return PMPI_Unpack(inbuf, insize, position, outbuf, outcount, datatype, comm);
+}
+
+int MPI_Pack_size(int incount, MPI_Datatype datatype, MPI_Comm comm, int *size) {
+  if (!comm_of(comm)) return MPI_ERR_COMM;
+  TYPE(datatype, h);
+  if (!size || incount < 0) return MPI_ERR_ARG;
+  int64_t s = 0;
+  TRY(sp_type_size(h, &s));
+  *size = static_cast<int>(s * incount);
+  return MPI_SUCCESS;
+}
+
+// ============================================================ point to point
+static int send_impl(const void *buf, int count, MPI_Datatype datatype, int dest, int tag, MPI_Comm comm,
+                     int method) {
+  if (!comm_of(comm)) return MPI_ERR_COMM;
+  if (dest == MPI_PROC_NULL) return MPI_SUCCESS;
+  if (dest < 0 || dest >= S().size) return MPI_ERR_RANK;
+  if (tag < 0) return MPI_ERR_TAG;
+  if (count < 0) return MPI_ERR_COUNT;
+  TYPE(datatype, h);
+  TRY(sp_rt_send(buf, UINT64_MAX, count, h, dest, tag, method, nullptr));
+  return MPI_SUCCESS;
+}
+
+int PMPI_Send(const void *buf, int count, MPI_Datatype datatype, int dest, int tag, MPI_Comm comm) {
+  return send_impl(buf, count, datatype, dest, tag, comm, SP_METHOD_DEVICE);
+}
+
+// the interposed send: the model picks device / one-shot / staged per
+// message unless TEMPI_METHOD forces one
+int MPI_Send(const void *buf, int count, MPI_Datatype datatype, int dest, int tag, MPI_Comm comm) {
+  return send_impl(buf, count, datatype, dest, tag, comm, S().forced_method);
+}
+
+int PMPI_Recv(void *buf, int count, MPI_Datatype datatype, int source, int tag, MPI_Comm comm,
+              MPI_Status *status) {
+  if (!comm_of(comm)) return MPI_ERR_COMM;
+  if (source == MPI_PROC_NULL) {
+    if (status) *status = MPI_Status{MPI_PROC_NULL, MPI_ANY_TAG, MPI_SUCCESS, 0, 0};
+    return MPI_SUCCESS;
+  }
+  if (count < 0) return MPI_ERR_COUNT;
+  TYPE(datatype, h);
+  int64_t st[4] = {0, 0, 0, 0};
+  TRY(sp_rt_recv(buf, UINT64_MAX, count, h, source, tag, st));
+  if (status) *status = MPI_Status{static_cast<int>(st[0]), static_cast<int>(st[1]), MPI_SUCCESS,
+                                   static_cast<int>(st[3]), st[2]};
+  return MPI_SUCCESS;
+}
+int MPI_Recv(void *buf, int count, MPI_Datatype datatype, int source, int tag, MPI_Comm comm, MPI_Status *status) {
+  return PMPI_Recv(buf, count, datatype, source, tag, comm, status);
+}
+
+// ============================================================ topologies
+int MPI_Dist_graph_create_adjacent(MPI_Comm comm_old, int indegree, const int sources[], const int *,
+                                   int outdegree, const int destinations[], const int *, int, int,
+                                   MPI_Comm *comm_dist_graph) {
+  if (!comm_of(comm_old) || !comm_dist_graph) return MPI_ERR_COMM;
+  if (indegree < 0 || outdegree < 0) return MPI_ERR_ARG;
+  Comm c;
+  c.kind = 1;
+  c.sources.assign(sources, sources + indegree);
+  c.dests.assign(destinations, destinations + outdegree);
+  for (int r : c.sources)
+    if ((r < 0 || r >= S().size) && r != MPI_PROC_NULL) return MPI_ERR_RANK;
+  for (int r : c.dests)
+    if ((r < 0 || r >= S().size) && r != MPI_PROC_NULL) return MPI_ERR_RANK;
+  std::lock_guard<std::mutex> lk(S().mu);
+  const int id = S().next_comm++;
+  S().comms[id] = std::move(c);
+  *comm_dist_graph = id;
+  return MPI_SUCCESS;
+}
+
+int MPI_Dist_graph_neighbors_count(MPI_Comm comm, int *indegree, int *outdegree, int *weighted) {
+  const Comm *c = comm_of(comm);
+  if (!c || !indegree || !outdegree) return MPI_ERR_COMM;
+  *indegree = static_cast<int>(c->sources.size());
+  *outdegree = static_cast<int>(c->dests.size());
+  if (weighted) *weighted = 0;
+  return MPI_SUCCESS;
+}
+
+int MPI_Dist_graph_neighbors(MPI_Comm comm, int maxin, int sources[], int *, int maxout, int destinations[],
+                             int *) {
+  const Comm *c = comm_of(comm);
+  if (!c) return MPI_ERR_COMM;
+  for (int i = 0; i < maxin && i < static_cast<int>(c->sources.size()); ++i) sources[i] = c->sources[i];
+  for (int i = 0; i < maxout && i < static_cast<int>(c->dests.size()); ++i) destinations[i] = c->dests[i];
+  return MPI_SUCCESS;
+}
+
+int MPI_Cart_create(MPI_Comm comm_old, int ndims, const int dims[], const int periods[], int, MPI_Comm *comm_cart) {
+  if (!comm_of(comm_old) || !comm_cart) return MPI_ERR_COMM;
+  int n = 1;
+  for (int i = 0; i < ndims; ++i) n *= dims[i];
+  if (n != S().size) return MPI_ERR_ARG;
+  Comm c;
+  c.kind = 2;
+  c.dims.assign(dims, dims + ndims);
+  c.periods.assign(periods, periods + ndims);
+  std::lock_guard<std::mutex> lk(S().mu);
+  const int id = S().next_comm++;
+  S().comms[id] = c;
+  *comm_cart = id;
+  // neighbour order of a Cartesian topology: per dimension, -1 then +1
+  auto &cc = S().comms[id];
+  for (int d = 0; d < ndims; ++d) {
+    int src = 0, dst = 0;
+    MPI_Cart_shift(id, d, 1, &src, &dst);
+    cc.sources.push_back(src);
+    cc.sources.push_back(dst);
+    cc.dests.push_back(src);
+    cc.dests.push_back(dst);
+  }
+  return MPI_SUCCESS;
+}
+
+int MPI_Cart_coords(MPI_Comm comm, int rank, int maxdims, int coords[]) {
+  const Comm *c = comm_of(comm);
+  if (!c || c->kind != 2) return MPI_ERR_COMM;
+  const int nd = static_cast<int>(c->dims.size());
+  for (int d = nd - 1; d >= 0; --d) { // row-major: last dimension fastest
+    if (d < maxdims) coords[d] = rank % c->dims[d];
+    rank /= c->dims[d];
+  }
+  return MPI_SUCCESS;
+}
+
+int MPI_Cart_rank(MPI_Comm comm, const int coords[], int *rank) {
+  const Comm *c = comm_of(comm);
+  if (!c || c->kind != 2 || !rank) return MPI_ERR_COMM;
+  int r = 0;
+  for (size_t d = 0; d < c->dims.size(); ++d) {
+    int x = coords[d];
+    if (c->periods[d]) {
+      x = ((x % c->dims[d]) + c->dims[d]) % c->dims[d];
+    } else if (x < 0 || x >= c->dims[d]) {
+      *rank = MPI_PROC_NULL;
+      return MPI_SUCCESS;
+    }
+    r = r * c->dims[d] + x;
+  }
+  *rank = r;
+  return MPI_SUCCESS;
+}
+
+int MPI_Cart_shift(MPI_Comm comm, int direction, int disp, int *rank_source, int *rank_dest) {
+  const Comm *c = comm_of(comm);
+  if (!c || c->kind != 2 || direction < 0 || direction >= static_cast<int>(c->dims.size())) return MPI_ERR_COMM;
+  std::vector<int> co(c->dims.size());
+  MPI_Cart_coords(comm, S().rank, static_cast<int>(co.size()), co.data());
+  co[direction] -= disp;
+  MPI_Cart_rank(comm, co.data(), rank_source);
+  co[direction] += 2 * disp;
+  MPI_Cart_rank(comm, co.data(), rank_dest);
+  return MPI_SUCCESS;
+}
+
+int MPI_Comm_free(MPI_Comm *comm) {
+  if (!comm || *comm < 100) return MPI_ERR_COMM;
+  std::lock_guard<std::mutex> lk(S().mu);
+  S().comms.erase(*comm);
+  *comm = MPI_COMM_NULL;
+  return MPI_SUCCESS;
+}
+
+// ============================================================ neighbour exchange
+int PMPI_Neighbor_alltoallv(const void *sendbuf, const int sendcounts[], const int sdispls[], MPI_Datatype sendtype,
+                            void *recvbuf, const int recvcounts[], const int rdispls[], MPI_Datatype recvtype,
+                            MPI_Comm comm) {
+  const Comm *c = comm_of(comm);
+  if (!c || c->kind == 0) return MPI_ERR_COMM;
+  TYPE(sendtype, hs);
+  TYPE(recvtype, hr);
+  // drop MPI_PROC_NULL edges (non-periodic Cartesian borders)
+  std::vector<int> src, dst;
+  std::vector<int64_t> scount, sdisp, rcount, rdisp;
+  for (size_t i = 0; i < c->dests.size(); ++i)
+    if (c->dests[i] != MPI_PROC_NULL) {
+      dst.push_back(c->dests[i]);
+      scount.push_back(sendcounts[i]);
+      sdisp.push_back(sdispls[i]);
+    }
+  for (size_t j = 0; j < c->sources.size(); ++j)
+    if (c->sources[j] != MPI_PROC_NULL) {
+      src.push_back(c->sources[j]);
+      rcount.push_back(recvcounts[j]);
+      rdisp.push_back(rdispls[j]);
+    }
+  TRY(sp_rt_neighbor_alltoallv(sendbuf, scount.data(), sdisp.data(), static_cast<int64_t>(dst.size()), dst.data(),
+                               hs, recvbuf, rcount.data(), rdisp.data(), static_cast<int64_t>(src.size()),
+                               src.data(), hr));
+  return MPI_SUCCESS;
+}
+
+int MPI_Neighbor_alltoallv(const void *sendbuf, const int sendcounts[], const int sdispls[], MPI_Datatype sendtype,
+                           void *recvbuf, const int recvcounts[], const int rdispls[], MPI_Datatype recvtype,
+                           MPI_Comm comm) {
+  return PMPI_Neighbor_alltoallv(sendbuf, sendcounts, sdispls, sendtype, recvbuf, recvcounts, rdispls, recvtype,
+                                 comm);
+}
+
+// ============================================================ TEMPI controls
+int TEMPI_Set_method(int method) {
+  if (method < -1 || method > 2) return MPI_ERR_ARG;
+  S().forced_method = method;
+  return MPI_SUCCESS;
+}
+
+int TEMPI_Load_profile(const char *path) {
+  sp_profile p = nullptr;
+  TRY(sp_profile_load(path, &p));
+  TRY(sp_rt_set_profile(p));
+  if (S().profile) sp_profile_free(S().profile);
+  S().profile = p;
+  return MPI_SUCCESS;
+}
+
+} // extern "C"

@@ -1,0 +1,42 @@
+#!/usr/bin/env python3
+"""tempirun -- launch N ranks of an MPI program linked against libtempi_b200.
+
+    python tools/tempirun.py -n 4 ./my_mpi_program args...
+
+Sets TEMPI_RANK / TEMPI_SIZE / TEMPI_LOCAL_RANK / TEMPI_JOB for each process
+(rank r uses GPU r % device_count unless TEMPI_DEVICE is set), waits for all
+of them and exits with the first nonzero status. torchrun works too: the
+library reads RANK / WORLD_SIZE / LOCAL_RANK / TORCHELASTIC_RUN_ID.
+"""
+import argparse
+import os
+import subprocess
+import sys
+import uuid
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("-n", "--np", type=int, default=1)
+    ap.add_argument("--timeout", type=float, default=600)
+    ap.add_argument("cmd", nargs=argparse.REMAINDER)
+    a = ap.parse_args()
+    job = "run" + uuid.uuid4().hex[:10]
+    procs = []
+    for r in range(a.np):
+        env = dict(os.environ, TEMPI_RANK=str(r), TEMPI_SIZE=str(a.np), TEMPI_LOCAL_RANK=str(r), TEMPI_JOB=job)
+        procs.append(subprocess.Popen(a.cmd, env=env))
+    rc = 0
+    try:
+        for p in procs:
+            p.wait(timeout=a.timeout)
+            rc = rc or p.returncode
+    except subprocess.TimeoutExpired:
+        for p in procs:
+            p.kill()
+        rc = 124
+    sys.exit(rc)
+
+
+if __name__ == "__main__":
+    main()
