@@ -15,6 +15,7 @@ def header_symbols(name):
     src = open(os.path.join(ROOT, "include", name)).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     src = re.sub(r"//[^\n]*", "", src)
+    src = re.sub(r"^\s*#[^\n]*", "", src, flags=re.M)
     return sorted(set(re.findall(r"\b((?:sp|MPI|PMPI)_[A-Za-z0-9_]+)\s*\(", src)))
 
 
