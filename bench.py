@@ -131,11 +131,16 @@ def dist_setup(n):
     return rank, local, world
 
 
+def reduce_device():
+    import torch.distributed as dist
+    return "cpu" if dist.is_initialized() and dist.get_backend() == "gloo" else "cuda"
+
+
 def barrier_max(torch, world, value):
     if world == 1:
         return value
     import torch.distributed as dist
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    t = torch.tensor([value], dtype=torch.float64, device=reduce_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -144,7 +149,7 @@ def barrier_sum(torch, world, value):
     if world == 1:
         return value
     import torch.distributed as dist
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    t = torch.tensor([value], dtype=torch.float64, device=reduce_device())
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
@@ -153,6 +158,16 @@ def barrier(world):
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
+
+
+def shared_job_name(world, rank):
+    """one name for the engine's node-local runtime, agreed by all ranks"""
+    import uuid
+    name = ["bench" + uuid.uuid4().hex[:10]]
+    if world > 1:
+        import torch.distributed as dist
+        dist.broadcast_object_list(name, src=0)
+    return name[0]
 
 
 # ------------------------------------------------------------------ reference CPU
@@ -231,10 +246,16 @@ def run_ours(args):
     from paper_2012_14363_b200 import _capi
 
     rank, local, world = dist_setup(args.gpus)
+    # BENCH_DEVICE / BENCH_BACKEND=gloo let several ranks share one GPU in
+    # tests (NCCL refuses duplicate devices); the driver uses the defaults
+    local = int(os.environ.get("BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("BENCH_BACKEND", "nccl") == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     K = args.incount
     lib = _capi.lib
     stream = torch.cuda.current_stream()
@@ -358,6 +379,17 @@ def run_ours(args):
     e2e_bytes = 2 * Ke * (1 << 20) * 2 * len(E0S)
     e2e_val = barrier_sum(torch, world, e2e_bytes) / (e2e_ms * 1e-3) / 1e9
 
+    # multi-GPU rows: halo exchange (config 5) and model-selected send (config 4)
+    del src, packed, flush, host_msg
+    torch.cuda.empty_cache()
+    halo = send = None
+    if not args.no_halo:
+        from tools.bench_parts import halo_section, send_section
+        job = shared_job_name(world, rank)
+        halo = halo_section(torch, rank, world, local, job)
+        if world >= 2:
+            send = send_section(torch, rank, world, local, job)
+
     if rank != 0:
         if world > 1:
             import torch.distributed as dist
@@ -396,6 +428,8 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
+        "halo": halo,
+        "send": send,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -414,6 +448,7 @@ def main():
     ap.add_argument("--e2e-incount", type=int, default=8)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-halo", action="store_true", help="skip the halo / send sections")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

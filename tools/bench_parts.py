@@ -1,0 +1,177 @@
+"""Multi-GPU sections of bench.py (imported by it; also runnable alone).
+
+halo_section : the 3D 26-neighbour halo exchange (BASELINE config 5: radius
+               2, 256^3 points/rank, 32 B/point) on a rank grid of the
+               world size, through the engine's fused pack-to-peer plan
+               (one batch launch per rank stores every segment into the
+               neighbour's HBM over CUDA IPC / NVLink), verified cell by
+               cell, and -- when torch.distributed is up -- the NCCL
+               baseline (batch pack, 26 ncclSend/ncclRecv in one group,
+               batch unpack). Device-timed with CUDA events, max over ranks.
+send_section : BASELINE config 4, a non-contiguous 3D object sent rank 0 ->
+               rank 1 (half ping-pong), 1 KiB-64 MiB, every
+               fixed method and the model's choice.
+"""
+from __future__ import annotations
+
+import math
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+GRIDS = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2), 3: (3, 1, 1), 6: (3, 2, 1)}
+NVLINK_GBPS = 900.0          # per direction per GPU, nominal
+NVLINK_MEASURED_GBPS = 770.0  # peer copy per direction (B200_PROFILING.md)
+
+
+def remote_bytes(cfg, regions, rank):
+    """bytes this rank sends to OTHER ranks (NVLink traffic)"""
+    import paper_2012_14363_b200.halo as H
+    return sum(r.send.size for r in regions if H.neighbor(cfg, rank, r.dir) != rank)
+
+
+def _reduce(torch, world, v, op):
+    if world == 1:
+        return v
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cpu" if dist.get_backend() == "gloo" else "cuda")
+    dist.all_reduce(t, op=op)
+    return float(t.item())
+
+
+def halo_section(torch, rank, world, local, job, iters=20, warmup=5, nccl=True):
+    import paper_2012_14363_b200.halo as H
+    import paper_2012_14363_b200.rt as rt
+    import torch.distributed as dist
+    grid = GRIDS.get(world)
+    if grid is None:
+        return {"skipped": f"no 3D grid for {world} ranks"}
+    cfg = H.HaloConfig(grid, (256, 256, 256), 2, 32)
+    regions = H.build_halo_types(cfg)
+    pad = 260 ** 3 * 32
+    seg = [0]
+    for r in regions:
+        seg.append(seg[-1] + r.send.size)
+    rt.init(rank, world, job, device=local, window_bytes=1 << 20, host_bytes=1 << 20)
+    alloc = torch.empty(pad, dtype=torch.uint8, device="cuda")
+    H.fill(cfg, rank, alloc)
+    torch.cuda.synchronize()
+    plan = rt.HaloPlan(cfg, alloc, H.FUSED)
+    for _ in range(warmup):
+        plan.exchange()
+    ts = [plan.exchange() for _ in range(iters)]
+    bad = H.verify(cfg, rank, alloc)
+    plan.free()
+    MAX = dist.ReduceOp.MAX if world > 1 else None
+    phase = {k: _reduce(torch, world, statistics.median(t[k] for t in ts), MAX) for k in ts[0]}
+    bad = _reduce(torch, world, float(bad), MAX)
+    rbytes = remote_bytes(cfg, regions, rank)
+    out = {"grid": list(grid), "interior": 256, "radius": 2, "element_bytes": 32,
+           "bytes_per_rank": seg[-1], "remote_bytes_per_rank": rbytes, "verified": bad == 0,
+           "fused_us": {k: round(v * 1e6, 2) for k, v in phase.items()},
+           "fused_hbm_GBps_per_rank": round(4 * seg[-1] / phase["iteration"] / 1e9, 1),
+           "nvlink_bound_us": round(rbytes / (NVLINK_MEASURED_GBPS * 1e9) * 1e6, 2)}
+    if nccl and world > 1 and dist.is_initialized() and dist.get_backend() == "nccl":
+        out["nccl"] = _nccl_halo(torch, cfg, regions, seg, alloc, rank, world, iters, warmup)
+    rt.finalize()
+    return out
+
+
+def _nccl_halo(torch, cfg, regions, seg, alloc, rank, world, iters, warmup):
+    """baseline: batch pack -> 26 NCCL send/recv in one group -> batch unpack"""
+    import paper_2012_14363_b200.halo as H
+    import torch.distributed as dist
+    H.fill(cfg, rank, alloc)
+    sbuf = torch.empty(seg[-1], dtype=torch.uint8, device="cuda")
+    rbuf = torch.empty(seg[-1], dtype=torch.uint8, device="cuda")
+    pack = H.Batch([(alloc, r.send, 1, sbuf, seg[j]) for j, r in enumerate(regions)])
+    unpack = H.Batch([(rbuf, r.recv, 1, alloc, seg[k]) for k, r in enumerate(regions)], unpack=True)
+    ops = []
+    for j, r in enumerate(regions):
+        ops.append(dist.P2POp(dist.isend, sbuf[seg[j]:seg[j + 1]], H.neighbor(cfg, rank, r.dir)))
+    for k in range(25, -1, -1):  # the i-th recv from a peer matches its i-th send
+        peer = H.neighbor(cfg, rank, regions[k].dir)
+        ops.append(dist.P2POp(dist.irecv, rbuf[seg[k]:seg[k + 1]], peer))
+    s = torch.cuda.current_stream()
+    times = []
+    for it in range(warmup + iters):
+        dist.barrier()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record(s)
+        pack.execute(s)
+        ev[1].record(s)
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        ev[2].record(s)
+        unpack.execute(s)
+        ev[3].record(s)
+        torch.cuda.synchronize()
+        if it >= warmup:
+            times.append([ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]),
+                          ev[0].elapsed_time(ev[3])])
+    bad = H.verify(cfg, rank, alloc)
+    MAX = dist.ReduceOp.MAX
+    med = [_reduce(torch, world, statistics.median(t[i] for t in times), MAX) for i in range(4)]
+    return {"verified": _reduce(torch, world, float(bad), MAX) == 0,
+            "us": {"pack": round(med[0] * 1e3, 2), "exchange": round(med[1] * 1e3, 2),
+                   "unpack": round(med[2] * 1e3, 2), "iteration": round(med[3] * 1e3, 2)}}
+
+
+def cfg4_prog(e0, n):
+    """3D subarray with E0-byte blocks, n bytes total (BASELINE config 4):
+    E1*E2 = n/E0 split as powers of two, sizes {max(2E0,64), 2E1, E2}."""
+    rows = n // e0
+    e2 = 2 ** (int(math.log2(rows)) // 2)
+    e1 = rows // e2
+    sizes = [max(2 * e0, 64), 2 * e1, e2]
+    return [4, 3, 0] + sizes + [e0, e1, e2] + [0, 0, 0] + [0, 0]
+
+
+def send_section(torch, rank, world, local, job, reps=10, warmup=3):
+    """rank 0 -> rank 1, every method + model; other ranks idle"""
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.model as M
+    import paper_2012_14363_b200.rt as rt
+    if world < 2:
+        return {"skipped": "needs 2 ranks"}
+    rt.init(rank, world, job + "s", device=local, window_bytes=72 << 20, host_bytes=72 << 20)
+    prof_path = os.path.join(ROOT, "profiles", "b200.profile")
+    if os.path.exists(prof_path):
+        rt.set_profile(M.load_profile_file(prof_path))
+    rows = []
+    import time
+    for e0 in (8, 64, 512):
+        for n in [1 << k for k in range(10, 27, 4)]:
+            if n < e0 * 4:
+                continue
+            ct = sp.commit_type(sp.from_program(cfg4_prog(e0, n)))
+            buf = torch.zeros(ct.span, dtype=torch.uint8, device="cuda")
+            row = {"E0": e0, "bytes": ct.size}
+            for name, m in (("device", rt.DEVICE), ("oneshot", rt.ONESHOT), ("staged", rt.STAGED),
+                            ("model", rt.AUTO)):
+                ts, used = [], None
+                for it in range(warmup + reps):
+                    rt.barrier()
+                    t0 = time.perf_counter()
+                    if rank == 0:
+                        used = rt.send(buf, 1, ct, 1, tag=it, method=m)
+                        rt.recv(buf, 1, ct, source=1, tag=it)
+                    elif rank == 1:
+                        st = rt.recv(buf, 1, ct, source=0, tag=it)
+                        used = st["method"]
+                        rt.send(buf, 1, ct, 0, tag=it, method=m)
+                    if it >= warmup:
+                        ts.append((time.perf_counter() - t0) / 2)
+                if rank <= 1:
+                    row[name + "_us"] = round(statistics.median(ts) * 1e6, 2)
+                    row[name + "_GBps"] = round(ct.size / statistics.median(ts) / 1e9, 2)
+                    if name == "model":
+                        row["model_choice"] = {0: "oneshot", 1: "device", 2: "staged"}[used]
+            rows.append(row)
+    rt.finalize()
+    return {"pair": [0, 1], "timing": "half ping-pong wall time (host-synchronous MPI_Send/Recv semantics)",
+            "nvlink_peak_GBps": NVLINK_MEASURED_GBPS, "rows": rows}
