@@ -6,6 +6,7 @@
 // ties, the line-oriented text format); the profile this engine ships is
 // MEASURED on B200 by tools/measure (profiles/b200.profile).
 #include <array>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -234,38 +235,55 @@ std::string format_profile(const Profile &p, const std::string &header) {
 // ------------------------------------------------------------ cache
 // Memoised choose_method keyed on (object, block). 32 shards, each a hash
 // map under its own reader/writer lock; a miss computes outside the lock.
+// Lock-free on the hit path: a direct-mapped table of 2^16 slots, each two
+// atomic words (object size; block size << 3 | method << 1 | valid). A
+// reader loads tag, object, tag again and accepts only an unchanged, valid
+// tag whose object and block match -- a concurrent writer can only cause a
+// miss, and a miss recomputes choose_method, so answers are always exact.
+// Colliding queries overwrite each other (it is a cache of a pure function).
 struct ModelCache {
-  explicit ModelCache(std::shared_ptr<const Profile> p) : prof(std::move(p)) {}
-  struct Key {
-    int64_t o, b;
-    bool operator==(const Key &k) const { return o == k.o && b == k.b; }
+  explicit ModelCache(std::shared_ptr<const Profile> p) : prof(std::move(p)), sets(new Set[kSets]) {}
+  static constexpr size_t kSets = size_t{1} << 14; // x 4 ways = 64 Ki entries, 1 MiB
+  struct Slot {
+    std::atomic<uint64_t> tag{0};
+    std::atomic<uint64_t> obj{0};
   };
-  struct KeyHash {
-    size_t operator()(const Key &k) const {
-      uint64_t h = static_cast<uint64_t>(k.o) * 0xd6e8feb86659fd93ull ^ static_cast<uint64_t>(k.b);
-      h ^= h >> 31;
-      h *= 0x9e3779b97f4a7c15ull;
-      return static_cast<size_t>(h ^ (h >> 29));
-    }
-  };
-  struct Shard {
-    std::shared_mutex mu;
-    std::unordered_map<Key, int, KeyHash> map;
+  struct alignas(64) Set {
+    Slot way[4];
   };
   std::shared_ptr<const Profile> prof;
-  Shard shards[32];
+  std::unique_ptr<Set[]> sets;
+
+  static uint64_t hash(int64_t o, int64_t b) {
+    uint64_t h = static_cast<uint64_t>(o) * 0xd6e8feb86659fd93ull ^ static_cast<uint64_t>(b);
+    h ^= h >> 31;
+    h *= 0x9e3779b97f4a7c15ull;
+    return h ^ (h >> 29);
+  }
 
   int choose(int64_t o, int64_t b) {
-    const Key k{o, b};
-    Shard &s = shards[KeyHash{}(k) >> 59];
-    {
-      std::shared_lock lk(s.mu);
-      auto it = s.map.find(k);
-      if (it != s.map.end()) return it->second;
+    const uint64_t h = hash(o, b);
+    Set &set = sets[h & (kSets - 1)];
+    for (Slot &s : set.way) {
+      const uint64_t t1 = s.tag.load(std::memory_order_acquire);
+      const uint64_t ob = s.obj.load(std::memory_order_acquire);
+      const uint64_t t2 = s.tag.load(std::memory_order_acquire);
+      if (t1 == t2 && (t1 & 1) && ob == static_cast<uint64_t>(o) && (t1 >> 3) == static_cast<uint64_t>(b))
+        return static_cast<int>((t1 >> 1) & 3);
     }
     const int m = choose_method(*prof, o, b);
-    std::unique_lock lk(s.mu);
-    s.map.emplace(k, m);
+    if (b >= 0 && b < (int64_t{1} << 60)) { // publish: invalidate, write, validate
+      Slot *victim = &set.way[(h >> 40) & 3];
+      for (Slot &s : set.way)
+        if (!(s.tag.load(std::memory_order_relaxed) & 1)) {
+          victim = &s;
+          break;
+        }
+      victim->tag.store(0, std::memory_order_release);
+      victim->obj.store(static_cast<uint64_t>(o), std::memory_order_release);
+      victim->tag.store(static_cast<uint64_t>(b) << 3 | static_cast<uint64_t>(m) << 1 | 1,
+                        std::memory_order_release);
+    }
     return m;
   }
 };

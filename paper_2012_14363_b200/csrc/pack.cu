@@ -35,6 +35,7 @@
 #include <string>
 
 #include "core.hpp"
+#include "tma.hpp"
 
 namespace spb {
 
@@ -580,7 +581,42 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
     kernel = SP_KERNEL_WORDS64;
   }
   if (kernel == SP_KERNEL_SMALLROW && !smallrow_ok) fail(SP_ERR_INVALID_ARGUMENT, "smallrow kernel not applicable");
-  if (kernel == SP_KERNEL_TMA) fail(SP_ERR_UNSUPPORTED, "TMA kernel not built in this configuration");
+  // unpack of long rows: the TMA store path measured 5-9% ahead of the
+  // LDG/STG kernel at c0 >= 128 (profiles/r01_tma_vs_words.txt); pack ties
+  if (kernel == SP_KERNEL_WORDS && opt.kernel == SP_KERNEL_AUTO && !pack && !opt.force_word && rd.c0 >= 128 &&
+      g.nd <= 4) {
+    TmaGeometry probe{};
+    probe.c0 = rd.c0;
+    probe.nd = g.nd;
+    for (int k = 0; k < g.nd; ++k) {
+      probe.cnt[k] = rd.cnt[k];
+      probe.str[k] = rd.str[k];
+    }
+    probe.strided_addr = strided_addr + ct.sb.start;
+    probe.packed_addr = packed_addr;
+    if (tma_applicable(probe)) kernel = SP_KERNEL_TMA;
+  }
+  if (kernel == SP_KERNEL_TMA) {
+    TmaGeometry tg{};
+    tg.c0 = rd.c0;
+    tg.nd = g.nd;
+    if (tg.nd > 4) fail(SP_ERR_INVALID_ARGUMENT, "TMA path: more than 4 row dimensions");
+    for (int k = 0; k < tg.nd; ++k) {
+      tg.cnt[k] = rd.cnt[k];
+      tg.str[k] = rd.str[k];
+    }
+    tg.strided_addr = strided_addr + ct.sb.start;
+    tg.packed_addr = packed_addr;
+    int64_t grid = 0;
+    tma_launch(tg, pack ? sin : sout, pack ? out : const_cast<uint8_t *>(in), pack, s, &grid);
+    li.kernel = SP_KERNEL_TMA;
+    li.word = 16;
+    li.launches = 1;
+    li.grid = grid;
+    li.block = 32;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return;
+  }
 
   if (fits32) {
     for (int k = 0; k < g.nd; ++k) {
@@ -642,7 +678,7 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
 // (halo corners, edges) share the grid with large ones (faces) instead of
 // costing a launch each. Destinations may be peer-GPU memory mapped over
 // NVLink (CUDA IPC), which turns the batch into a fused pack-to-peer.
-constexpr uint32_t kBatchChunk = 256 * 4;
+constexpr uint32_t kBatchChunk = 256 * 2; // words per chunk: two per thread
 
 struct BatchJob {
   Geom g;
@@ -652,37 +688,11 @@ struct BatchJob {
   int pack;
 };
 
+// one launch per (word size, direction) group; all jobs of a group share W
 template <int W, bool PACK>
-__device__ __noinline__ void batch_chunk(const BatchJob &j, uint32_t base) {
+__global__ void __launch_bounds__(256) k_batch(const BatchJob *__restrict__ jobs,
+                                               const uint32_t *__restrict__ chunk0, int njobs, uint32_t nchunks) {
   using T = typename Word<W>::T;
-  const uint32_t total = static_cast<uint32_t>(j.g.total);
-  T v[4];
-  int64_t soff[4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const uint32_t q = base + u * 256;
-    if (q < total) {
-      const uint32_t row = fdiv(q, j.g.wdiv);
-      soff[u] = row_offset(row, j.g) + static_cast<int64_t>(q - row * j.g.wpr) * W;
-      v[u] = PACK ? ld_stream(reinterpret_cast<const T *>(j.in + soff[u])) : ld_stream(reinterpret_cast<const T *>(j.in) + q);
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const uint32_t q = base + u * 256;
-    if (q < total) {
-      if (PACK) {
-        st_stream(reinterpret_cast<T *>(j.out) + q, v[u]);
-      } else {
-        st_stream(reinterpret_cast<T *>(j.out + soff[u]), v[u]);
-      }
-    }
-  }
-}
-
-__global__ void __launch_bounds__(256, 4) k_batch(const BatchJob *__restrict__ jobs,
-                                               const uint32_t *__restrict__ chunk0, int njobs,
-                                               uint32_t nchunks) {
   __shared__ BatchJob sj;
   int loaded = -1;
   for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
@@ -697,39 +707,56 @@ __global__ void __launch_bounds__(256, 4) k_batch(const BatchJob *__restrict__ j
     }
     if (lo != loaded) {
       __syncthreads();
-      const uint32_t *s = reinterpret_cast<const uint32_t *>(jobs + lo);
-      uint32_t *d = reinterpret_cast<uint32_t *>(&sj);
-      for (uint32_t i = threadIdx.x; i < sizeof(BatchJob) / 4; i += blockDim.x) d[i] = s[i];
+      const uint32_t *src = reinterpret_cast<const uint32_t *>(jobs + lo);
+      uint32_t *dst = reinterpret_cast<uint32_t *>(&sj);
+      for (uint32_t i = threadIdx.x; i < sizeof(BatchJob) / 4; i += blockDim.x) dst[i] = src[i];
       __syncthreads();
       loaded = lo;
     }
+    const uint32_t total = static_cast<uint32_t>(sj.g.total);
     const uint32_t base = (c - chunk0[lo]) * kBatchChunk + threadIdx.x;
-    switch (sj.w * 2 + sj.pack) {
-    case 33: batch_chunk<16, true>(sj, base); break;
-    case 32: batch_chunk<16, false>(sj, base); break;
-    case 17: batch_chunk<8, true>(sj, base); break;
-    case 16: batch_chunk<8, false>(sj, base); break;
-    case 9: batch_chunk<4, true>(sj, base); break;
-    case 8: batch_chunk<4, false>(sj, base); break;
-    case 5: batch_chunk<2, true>(sj, base); break;
-    case 4: batch_chunk<2, false>(sj, base); break;
-    case 3: batch_chunk<1, true>(sj, base); break;
-    default: batch_chunk<1, false>(sj, base); break;
+    T v[2];
+    int64_t soff[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint32_t q = base + u * 256;
+      if (q < total) {
+        const uint32_t row = fdiv(q, sj.g.wdiv);
+        soff[u] = row_offset(row, sj.g) + static_cast<int64_t>(q - row * sj.g.wpr) * W;
+        v[u] = PACK ? ld_stream(reinterpret_cast<const T *>(sj.in + soff[u]))
+                    : ld_stream(reinterpret_cast<const T *>(sj.in) + q);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint32_t q = base + u * 256;
+      if (q < total) {
+        if (PACK) {
+          st_stream(reinterpret_cast<T *>(sj.out) + q, v[u]);
+        } else {
+          st_stream(reinterpret_cast<T *>(sj.out + soff[u]), v[u]);
+        }
+      }
     }
   }
 }
 
-struct Batch {
-  int device = -1;
+struct BatchGroup {
+  int w = 0, pack = 0;
   BatchJob *d_jobs = nullptr;
   uint32_t *d_chunk0 = nullptr;
   int njobs = 0;
   uint32_t nchunks = 0;
+};
+
+struct Batch {
+  int device = -1;
+  std::vector<BatchGroup> groups;
   int64_t bytes = 0; // packed bytes moved per execution
   ~Batch() {
-    if (d_jobs) {
-      cudaFree(d_jobs);
-      cudaFree(d_chunk0);
+    for (auto &g : groups) {
+      cudaFree(g.d_jobs);
+      cudaFree(g.d_chunk0);
     }
   }
 };
@@ -774,9 +801,7 @@ BatchJob plan_job(const Committed &ct, int64_t count, const uint8_t *strided, co
 
 Batch *batch_create(const std::vector<BatchSpec> &specs, bool unpack) {
   require_device();
-  std::vector<BatchJob> jobs;
-  std::vector<uint32_t> chunk0;
-  uint64_t chunks = 0;
+  std::vector<BatchJob> by_w[5]; // W = 1, 2, 4, 8, 16
   int64_t bytes = 0;
   for (const BatchSpec &s : specs) {
     const Committed &ct = *s.ct;
@@ -794,22 +819,34 @@ Batch *batch_create(const std::vector<BatchSpec> &specs, bool unpack) {
     if (rs.kind == MemKind::Pageable || rp.kind == MemKind::Pageable)
       fail(SP_ERR_INVALID_ARGUMENT, "batch: buffers must be device, pinned or peer-mapped memory");
     BatchJob j = plan_job(ct, s.count, rs.dptr, rp.dptr + s.position, !unpack);
-    chunk0.push_back(static_cast<uint32_t>(chunks));
-    chunks += (j.g.total + kBatchChunk - 1) / kBatchChunk;
-    if (chunks >= (1ull << 32)) fail(SP_ERR_UNSUPPORTED, "batch: too much work for one launch");
+    by_w[__builtin_ctz(static_cast<unsigned>(j.w))].push_back(j);
     bytes += s.count * ct.size;
-    jobs.push_back(j);
   }
   auto b = std::make_unique<Batch>();
   cuda_check(cudaGetDevice(&b->device), "cudaGetDevice");
-  b->njobs = static_cast<int>(jobs.size());
-  b->nchunks = static_cast<uint32_t>(chunks);
   b->bytes = bytes;
-  if (!jobs.empty()) {
-    cuda_check(cudaMalloc(&b->d_jobs, jobs.size() * sizeof(BatchJob)), "cudaMalloc(batch)");
-    cuda_check(cudaMalloc(&b->d_chunk0, chunk0.size() * sizeof(uint32_t)), "cudaMalloc(batch)");
-    cuda_check(cudaMemcpy(b->d_jobs, jobs.data(), jobs.size() * sizeof(BatchJob), cudaMemcpyHostToDevice), "upload batch");
-    cuda_check(cudaMemcpy(b->d_chunk0, chunk0.data(), chunk0.size() * sizeof(uint32_t), cudaMemcpyHostToDevice),
+  for (int wi = 4; wi >= 0; --wi) {
+    const auto &jobs = by_w[wi];
+    if (jobs.empty()) continue;
+    BatchGroup g;
+    g.w = 1 << wi;
+    g.pack = !unpack;
+    std::vector<uint32_t> chunk0;
+    uint64_t chunks = 0;
+    for (const BatchJob &j : jobs) {
+      chunk0.push_back(static_cast<uint32_t>(chunks));
+      chunks += (j.g.total + kBatchChunk - 1) / kBatchChunk;
+      if (chunks >= (1ull << 32)) fail(SP_ERR_UNSUPPORTED, "batch: too much work for one launch");
+    }
+    g.njobs = static_cast<int>(jobs.size());
+    g.nchunks = static_cast<uint32_t>(chunks);
+    b->groups.push_back(g);
+    BatchGroup &G = b->groups.back();
+    cuda_check(cudaMalloc(&G.d_jobs, jobs.size() * sizeof(BatchJob)), "cudaMalloc(batch)");
+    cuda_check(cudaMalloc(&G.d_chunk0, chunk0.size() * sizeof(uint32_t)), "cudaMalloc(batch)");
+    cuda_check(cudaMemcpy(G.d_jobs, jobs.data(), jobs.size() * sizeof(BatchJob), cudaMemcpyHostToDevice),
+               "upload batch");
+    cuda_check(cudaMemcpy(G.d_chunk0, chunk0.data(), chunk0.size() * sizeof(uint32_t), cudaMemcpyHostToDevice),
                "upload batch");
   }
   return b.release();
@@ -817,13 +854,25 @@ Batch *batch_create(const std::vector<BatchSpec> &specs, bool unpack) {
 
 void batch_execute(const Batch &b, void *stream) {
   sp_launch_info li{};
-  if (b.njobs > 0) {
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(b.nchunks, static_cast<uint64_t>(sm_count()) * 8));
-    k_batch<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(b.d_jobs, b.d_chunk0, b.njobs, b.nchunks);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (const BatchGroup &g : b.groups) {
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(g.nchunks, static_cast<uint64_t>(sm_count()) * 8));
+    switch (g.w * 2 + g.pack) {
+    case 33: k_batch<16, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
+    case 32: k_batch<16, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
+    case 17: k_batch<8, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
+    case 16: k_batch<8, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
+    case 9: k_batch<4, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
+    case 8: k_batch<4, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
+    case 5: k_batch<2, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
+    case 4: k_batch<2, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
+    case 3: k_batch<1, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
+    default: k_batch<1, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
+    }
     cuda_check(cudaGetLastError(), "k_batch launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
     li.kernel = SP_KERNEL_BATCH;
-    li.launches = 1;
+    li.launches += 1;
     li.grid = grid;
     li.block = 256;
   }

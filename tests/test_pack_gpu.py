@@ -367,3 +367,80 @@ def test_cfg2_sweep_full_size(sp, orc, cuda, e0):
     assert torch.equal(again, dst)
     assert int((back != 0).sum()) <= ct.size
     assert int(back.to(torch.int64).sum()) == int(dst.to(torch.int64).sum())
+
+
+# ------------------------------------------------------------ TMA path
+def test_tma_path_parity(sp, orc, cuda, corpus):
+    """the TMA-tiled kernels (tensor-map box staged through shared memory)
+    produce the oracle's bytes wherever they apply; rows clipped at tile
+    edges are never written on unpack"""
+    torch = cuda
+    rng = np.random.default_rng(404)
+    n = 0
+    for e in corpus:
+        r = e["ref"]
+        if r["status"] or r["form"] != 0 or r["size"] > (1 << 15) or r["overlapping"]:
+            continue
+        prog = e["prog"]
+        ct = sp.commit_type(sp.from_program(prog))
+        inc = 1 + int(rng.integers(0, 2))
+        span = (inc - 1) * ct.extent + ct.span
+        host = rng.integers(0, 256, span, dtype=np.uint8)
+        src = dev(torch, host)
+        dst = torch.zeros(inc * ct.size, dtype=torch.uint8, device="cuda")
+        try:
+            sp.pack(src, ct, inc, dst, 0, kernel=sp.Kernel.TMA)
+        except sp.InvalidArgument:
+            continue
+        assert sp.last_launch().kernel == sp.Kernel.TMA
+        want = np.zeros(inc * ct.size, np.uint8)
+        orc.pack(prog, host, inc, want, 0)
+        assert np.array_equal(dst.cpu().numpy(), want), prog
+        back = torch.full((span,), 0x6B, dtype=torch.uint8, device="cuda")
+        sp.unpack(dst, 0, ct, inc, back, kernel=sp.Kernel.TMA)
+        exp = np.full(span, 0x6B, np.uint8)
+        orc.unpack(prog, want, 0, inc, exp)
+        assert np.array_equal(back.cpu().numpy(), exp), prog
+        n += 1
+    # hand-built shapes that exercise partial tiles, 4 row dims and counts
+    b = sp.make_named(sp.NamedKind.Byte)
+    shapes = [sp.make_hvector(300, 1, 64, sp.make_contiguous(48, b)),
+              sp.make_hvector(3, 1, 16384, sp.make_hvector(257, 1, 32, sp.make_contiguous(16, b))),
+              sp.make_hvector(2, 1, 1 << 16, sp.make_hvector(3, 1, 8192, sp.make_hvector(5, 1, 512,
+                                                                                      sp.make_contiguous(256, b))))]
+    for d in shapes:
+        ct = sp.commit_type(d)
+        for inc in (1, 3):
+            span = (inc - 1) * ct.extent + ct.span
+            host = rng.integers(0, 256, span, dtype=np.uint8)
+            dst = torch.zeros(inc * ct.size, dtype=torch.uint8, device="cuda")
+            sp.pack(dev(torch, host), ct, inc, dst, 0, kernel=sp.Kernel.TMA)
+            ref = torch.zeros_like(dst)
+            sp.pack(dev(torch, host), ct, inc, ref, 0, kernel=sp.Kernel.Words)
+            assert torch.equal(dst, ref)
+            back = torch.full((span,), 7, dtype=torch.uint8, device="cuda")
+            sp.unpack(dst, 0, ct, inc, back, kernel=sp.Kernel.TMA)
+            ref2 = torch.full((span,), 7, dtype=torch.uint8, device="cuda")
+            sp.unpack(dst, 0, ct, inc, ref2, kernel=sp.Kernel.Words)
+            assert torch.equal(back, ref2)
+            n += 1
+    assert n > 20
+
+
+@pytest.mark.parametrize("e0", [16, 32, 64, 128, 256, 512])
+def test_tma_cfg2_full_size(sp, cuda, e0):
+    torch = cuda
+    prog, _ = cfg2_prog(e0)
+    ct = sp.commit_type(sp.from_program(prog))
+    g = torch.Generator(device="cuda").manual_seed(e0 + 1)
+    src = torch.randint(0, 256, (ct.span,), dtype=torch.uint8, device="cuda", generator=g)
+    a = torch.zeros(ct.size, dtype=torch.uint8, device="cuda")
+    bb = torch.zeros(ct.size, dtype=torch.uint8, device="cuda")
+    sp.pack(src, ct, 1, a, 0, kernel=sp.Kernel.TMA)
+    sp.pack(src, ct, 1, bb, 0, kernel=sp.Kernel.Words)
+    assert torch.equal(a, bb)
+    out1 = torch.zeros(ct.span, dtype=torch.uint8, device="cuda")
+    out2 = torch.zeros(ct.span, dtype=torch.uint8, device="cuda")
+    sp.unpack(a, 0, ct, 1, out1, kernel=sp.Kernel.TMA)
+    sp.unpack(a, 0, ct, 1, out2, kernel=sp.Kernel.Words)
+    assert torch.equal(out1, out2)
