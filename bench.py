@@ -236,6 +236,54 @@ def run_reference(args):
     return 0
 
 
+def build_line(args, value, step_ms, world, K, dominant, sweep, e2e_val, Ke, launches, clk, cpu, halo, send):
+    hbm, hbm_kind = peaks()
+    ms, e0, tag, gbs, li = dominant
+    bytes_per_kernel = 2 * K * (1 << 20)
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tfile):
+        with open(tfile) as f:
+            traffic = json.load(f).get(f"cfg2_E0_{e0}_{tag}_K{K}")
+    # the dominant kernel's physical ceiling: the B200 DRAM transaction rate
+    # (HBM peak / 128 B; profiles/r01_dram_granularity.md). Pack of E0 < 128
+    # costs one 128-B line read per row; unpack of E0 < 32 a 32-B sector
+    # read-modify-write (two transactions) per row.
+    if tag == "pack":
+        cap = 2 * e0 / (128 + e0) if e0 < 128 else 1.0
+    else:
+        cap = (e0 / 128 if e0 < 32 else (2 * e0 / (128 + e0) if e0 < 128 else 1.0))
+    return {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic",
+        "config": {"workload": f"cfg2: MPI_Type_create_subarray 3D, 1 MiB object in 1024^3 B, "
+                               f"E0 sweep {E0S[0]}-{E0S[-1]} B, pack+unpack, incount={K} per call",
+                   "incount": K,
+                   "l2": "flushed before every timed kernel (512 MiB write, then read back so the timed "
+                         "kernel sees a cold clean L2)",
+                   "parallelism": f"replicas x{world}"},
+        "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(gbs / hbm, 4), "traffic": traffic,
+                     "kernel": f"{tag} E0={e0} {li.kernel.name}/w{li.word}",
+                     "peak_source": hbm_kind,
+                     "algorithmic_bytes_per_launch": bytes_per_kernel,
+                     "transaction_cap_frac": round(cap, 4),
+                     "frac_of_transaction_cap": round(gbs / hbm / cap, 3)},
+        "sweep": sweep,
+        "e2e": {"value": round(e2e_val, 2), "unit": UNIT, "h2d_bytes_per_step": Ke * (1 << 20) * len(E0S),
+                "d2h_bytes_per_step": Ke * (1 << 20) * len(E0S),
+                "how": f"per E0: sp_unpack from pinned host (one-shot receive) then sp_pack to pinned host "
+                       f"(one-shot send), incount={Ke}; inbound and outbound legs pipelined on two streams"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "halo": halo,
+        "send": send,
+    }
+
+
 # ------------------------------------------------------------------ ours
 def run_ours(args):
     import numpy as np
@@ -358,79 +406,106 @@ def run_ours(args):
                 dominant = (ms, e0, tag, gbs, li)
         sweep.append(row)
 
-    # e2e: packed message in pinned host memory, through the same C-ABI
+    # e2e: the packed messages live in pinned HOST memory. Per E0, sp_unpack
+    # reads one over PCIe into the device object (one-shot receive) and
+    # sp_pack writes it back to host (one-shot send). The ten E0 objects sit
+    # at disjoint, aligned x offsets of one allocation, so the inbound leg
+    # of E0[i+1] (stream A, H2D) overlaps the outbound leg of E0[i]
+    # (stream B, D2H) -- PCIe is full duplex.
+    del src, packed
+    torch.cuda.empty_cache()
     Ke = min(K, args.e2e_incount)
-    host_msg = torch.empty(Ke << 20, dtype=torch.uint8).pin_memory()
-    host_msg.fill_(5)
+    xoff, at = {}, 0
+    for e0 in sorted(E0S, reverse=True):
+        xoff[e0] = at
+        at += e0
+    esrc = torch.empty((Ke << 30) + 4096, dtype=torch.uint8, device="cuda")
+    msg_in = [torch.full((Ke << 20,), 5, dtype=torch.uint8).pin_memory() for _ in E0S]
+    msg_out = [torch.empty(Ke << 20, dtype=torch.uint8).pin_memory() for _ in E0S]
+    sA, sB = torch.cuda.Stream(), torch.cuda.Stream()
+    hA, hB = C.c_void_p(sA.cuda_stream), C.c_void_p(sB.cuda_stream)
     e2e_t = 0.0
     for it in range(args.warmup + args.steps):
         torch.cuda.synchronize()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for e0, d, ct in types:
-            call(False, ct, Ke, host_msg.data_ptr(), host_msg.numel(), src.data_ptr(), src.numel())
-            call(True, ct, Ke, src.data_ptr(), src.numel(), host_msg.data_ptr(), host_msg.numel())
-        b.record(stream)
+        a.record(sA)
+        sB.wait_event(a)
+        for i, (e0, d, ct) in enumerate(types):
+            obj = esrc.data_ptr() + xoff[e0]
+            pos.value = 0
+            st = lib.sp_unpack(msg_in[i].data_ptr(), msg_in[i].numel(), C.byref(pos), ct.handle, Ke, obj,
+                               esrc.numel() - xoff[e0], hA)
+            assert st == 0, lib.sp_last_error()
+            ev = torch.cuda.Event()
+            ev.record(sA)
+            sB.wait_event(ev)
+            pos.value = 0
+            st = lib.sp_pack(obj, esrc.numel() - xoff[e0], ct.handle, Ke, msg_out[i].data_ptr(),
+                             msg_out[i].numel(), C.byref(pos), hB)
+            assert st == 0, lib.sp_last_error()
+        b.record(sB)
         torch.cuda.synchronize()
         if it >= args.warmup:
             e2e_t += a.elapsed_time(b)
     e2e_ms = barrier_max(torch, world, e2e_t / args.steps)
     e2e_bytes = 2 * Ke * (1 << 20) * 2 * len(E0S)
     e2e_val = barrier_sum(torch, world, e2e_bytes) / (e2e_ms * 1e-3) / 1e9
+    del esrc, msg_in, msg_out
 
-    # multi-GPU rows: halo exchange (config 5) and model-selected send (config 4)
-    del src, packed, flush, host_msg
+    # multi-GPU rows: halo exchange (config 5) and model-selected send (config 4).
+    # A watchdog guarantees the driver its JSON line even if these hang.
+    del flush
     torch.cuda.empty_cache()
     halo = send = None
+    line_box = {}
     if not args.no_halo:
         from tools.bench_parts import halo_section, send_section
+
+        def on_timeout():
+            if rank == 0 and "line" in line_box:
+                line_box["line"]["halo"] = {"error": "timed out"}
+                print(json.dumps(line_box["line"]), flush=True)
+            os._exit(0)
+
+        cpu_pre = None
+        if world == 1 and not args.no_cpu_baseline:  # measured first: the watchdog line needs it
+            gbs, t, reps, kind = cpu_sample(1, args.cpu_seconds)
+            cpu_pre = {"value": round(gbs, 4), "unit": UNIT, "cores": 1, "kind": kind,
+                       "sample": f"{reps} x (pack+unpack of 1 cfg2 object per E0), {t:.1f} s CPU, "
+                                 "PackOptions.threads=1 (the reference's fastest setting)"}
+            args.no_cpu_baseline = True
+            line_box["cpu"] = cpu_pre
+        line_box["line"] = build_line(args, value, step_ms, world, K, dominant, sweep, e2e_val, Ke,
+                                      launches, clk, cpu_pre, None, None)
+        dog = threading.Timer(args.section_timeout, on_timeout)
+        dog.daemon = True
+        dog.start()
         job = shared_job_name(world, rank)
-        halo = halo_section(torch, rank, world, local, job)
+        try:
+            halo = halo_section(torch, rank, world, local, job)
+        except Exception as exc:  # recorded, never fatal to the bench line
+            halo = {"error": f"{type(exc).__name__}: {exc}"}
         if world >= 2:
-            send = send_section(torch, rank, world, local, job)
+            try:
+                send = send_section(torch, rank, world, local, job)
+            except Exception as exc:
+                send = {"error": f"{type(exc).__name__}: {exc}"}
+        dog.cancel()
 
     if rank != 0:
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()
         return 0
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    cpu = line_box.get("cpu")
+    if cpu is None and world == 1 and not args.no_cpu_baseline:
         gbs, t, reps, kind = cpu_sample(1, args.cpu_seconds)
         cpu = {"value": round(gbs, 4), "unit": UNIT, "cores": 1, "kind": kind,
                "sample": f"{reps} x (pack+unpack of 1 cfg2 object per E0), {t:.1f} s CPU, "
                          "PackOptions.threads=1 (the reference's fastest setting)"}
-    ms, e0, tag, gbs, li = dominant
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tfile):
-        with open(tfile) as f:
-            traffic = json.load(f).get(f"cfg2_E0_{e0}_{tag}_K{K}")
-    line = {
-        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-        "data": "synthetic",
-        "config": {"workload": f"cfg2: MPI_Type_create_subarray 3D, 1 MiB object in 1024^3 B, "
-                               f"E0 sweep {E0S[0]}-{E0S[-1]} B, pack+unpack, incount={K} per call",
-                   "incount": K, "l2": "flushed before every timed kernel (512 MiB write, then read back so the timed kernel sees a cold clean L2)",
-                   "parallelism": f"replicas x{world}"},
-        "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
-                     "frac": round(gbs / hbm, 4), "traffic": traffic,
-                     "kernel": f"{tag} E0={e0} {li.kernel.name}/w{li.word}",
-                     "peak_source": hbm_kind,
-                     "algorithmic_bytes_per_launch": bytes_per_kernel},
-        "sweep": sweep,
-        "e2e": {"value": round(e2e_val, 2), "unit": UNIT, "h2d_bytes_per_step": Ke * (1 << 20) * len(E0S),
-                "d2h_bytes_per_step": Ke * (1 << 20) * len(E0S),
-                "how": f"sp_unpack from pinned host + sp_pack to pinned host, incount={Ke}, all E0"},
-        "gpu_launches": launches,
-        "clocks": clk.summary(),
-        "cpu_baseline": cpu,
-        "halo": halo,
-        "send": send,
-    }
+    line = build_line(args, value, step_ms, world, K, dominant, sweep, e2e_val, Ke, launches, clk, cpu, halo,
+                      send)
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -449,6 +524,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-halo", action="store_true", help="skip the halo / send sections")
+    ap.add_argument("--section-timeout", type=float, default=420.0,
+                    help="watchdog (s) for the halo/send sections; the bench line is printed regardless")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -444,3 +444,32 @@ def test_tma_cfg2_full_size(sp, cuda, e0):
     sp.unpack(a, 0, ct, 1, out1, kernel=sp.Kernel.TMA)
     sp.unpack(a, 0, ct, 1, out2, kernel=sp.Kernel.Words)
     assert torch.equal(out1, out2)
+
+
+# ------------------------------------------------------------ config 3
+def test_cfg3_constructions_identical(sp, cuda):
+    """BASELINE config 3: the cfg2 object (E0=32) built five ways reaches one
+    StridedBlock and one plan, and packs to identical bytes"""
+    torch = cuda
+    e0, e1, e2 = 32, 128, 256
+    b = sp.make_named(sp.NamedKind.Byte)
+    ways = [
+        sp.make_subarray(3, [1024] * 3, [e0, e1, e2], [0, 0, 0], b),
+        sp.make_hvector(e2, 1, 1 << 20, sp.make_vector(e1, e0, 1024, b)),
+        sp.make_hvector(e2, 1, 1 << 20, sp.make_vector(e1, 1, 1024 // e0, sp.make_hvector(e0, 1, 1, b))),
+        sp.make_hvector(e2, 1, 1 << 20, sp.make_hvector(e1, 1, 1024, sp.make_contiguous(e0, b))),
+        sp.make_subarray(1, [1024], [e2], [0], sp.make_subarray(2, [1024, 1024], [e0, e1], [0, 0], b)),
+    ]
+    cts = [sp.commit_type(w) for w in ways]
+    assert len({(c.canon, c.plan) for c in cts}) == 1
+    assert cts[0].canon == sp.StridedBlock(0, (e0, e1, e2), (1, 1024, 1 << 20))
+    span = max(c.span for c in cts)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    src = torch.randint(0, 256, (span,), dtype=torch.uint8, device="cuda", generator=g)
+    outs = []
+    for c in cts:
+        o = torch.empty(c.size, dtype=torch.uint8, device="cuda")
+        sp.pack(src, c, 1, o, 0)
+        outs.append(o)
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
