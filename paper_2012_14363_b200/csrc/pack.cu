@@ -395,9 +395,18 @@ int sm_count() {
   return sms;
 }
 
+// Kernels that read or write pinned host memory are PCIe-bound (~55 GB/s
+// per direction): a few CTAs keep enough bytes in flight, and leaving the
+// other SMs free lets an inbound and an outbound transfer run concurrently
+// (PCIe is full duplex). Set by execute() for the duration of one launch.
+thread_local unsigned t_host_grid_cap = 0;
+constexpr unsigned kHostGridCap = 48;
+constexpr int64_t kDmaStageMin = int64_t{1} << 20; // pinned packed messages >= 1 MiB move by DMA
+
 unsigned grid_for(uint64_t items, int per_thread) {
   const uint64_t blocks = (items + 256ull * per_thread - 1) / (256ull * per_thread);
-  const uint64_t cap = static_cast<uint64_t>(sm_count()) * 8; // 8 x 256 = 2048 threads/SM
+  uint64_t cap = static_cast<uint64_t>(sm_count()) * 8; // 8 x 256 = 2048 threads/SM
+  if (t_host_grid_cap) cap = std::min<uint64_t>(cap, t_host_grid_cap);
   return static_cast<unsigned>(std::max<uint64_t>(1, std::min(blocks, cap)));
 }
 
@@ -584,7 +593,7 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
   // unpack of long rows: the TMA store path measured 5-9% ahead of the
   // LDG/STG kernel at c0 >= 128 (profiles/r01_tma_vs_words.txt); pack ties
   if (kernel == SP_KERNEL_WORDS && opt.kernel == SP_KERNEL_AUTO && !pack && !opt.force_word && rd.c0 >= 128 &&
-      g.nd <= 4) {
+      g.nd <= 4 && t_host_grid_cap == 0 /* device memory on both sides */) {
     TmaGeometry probe{};
     probe.c0 = rd.c0;
     probe.nd = g.nd;
@@ -924,10 +933,30 @@ int64_t execute(const PackArgs &a) {
                              : resolve(static_cast<const uint8_t *>(a.src) + a.position);
   uint8_t *strided_dev = rs.dptr;
   uint8_t *packed_dev = rp.dptr; // already at position
+  // A large packed message in pinned host memory moves by DMA: the copy
+  // engine streams it over PCIe while the kernel runs on device memory with
+  // the whole GPU (zero-copy kernels would hold SMs hostage to PCIe latency,
+  // and two streams could not overlap inbound and outbound traffic). Small
+  // messages keep the zero-copy one-shot path (lowest latency).
+  const bool dma_packed = rp.kind == MemKind::Pinned && packed_len >= kDmaStageMin;
+  struct CapGuard {
+    explicit CapGuard(bool on) { t_host_grid_cap = on ? kHostGridCap : 0; }
+    ~CapGuard() { t_host_grid_cap = 0; }
+  } cap_guard(rs.kind == MemKind::Pinned || (rp.kind == MemKind::Pinned && !dma_packed));
   uint8_t *scratch_s = nullptr, *scratch_p = nullptr;
-  bool staged = false;
-  if (rs.kind == MemKind::Pageable) {
+  bool staged = false, must_sync = false;
+  if (dma_packed) {
     staged = true;
+    cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&scratch_p), static_cast<size_t>(packed_len), s),
+               "cudaMallocAsync(dma)");
+    if (!a.pack)
+      cuda_check(cudaMemcpyAsync(scratch_p, static_cast<const uint8_t *>(a.src) + a.position,
+                                 static_cast<size_t>(packed_len), cudaMemcpyHostToDevice, s),
+                 "dma packed H2D");
+    packed_dev = scratch_p;
+  }
+  if (rs.kind == MemKind::Pageable) {
+    staged = must_sync = true;
     cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&scratch_s), static_cast<size_t>(strided_len), s),
                "cudaMallocAsync(stage)");
     // pack reads the span; unpack must preserve bytes outside the layout
@@ -936,7 +965,7 @@ int64_t execute(const PackArgs &a) {
     strided_dev = scratch_s;
   }
   if (rp.kind == MemKind::Pageable) {
-    staged = true;
+    staged = must_sync = true;
     cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&scratch_p), static_cast<size_t>(packed_len), s),
                "cudaMallocAsync(stage)");
     if (!a.pack)
@@ -960,7 +989,9 @@ int64_t execute(const PackArgs &a) {
                  "stage strided D2H");
     if (scratch_s) cuda_check(cudaFreeAsync(scratch_s, s), "cudaFreeAsync");
     if (scratch_p) cuda_check(cudaFreeAsync(scratch_p, s), "cudaFreeAsync");
-    cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(stage)");
+    // pageable memory is only safe once the copies completed; pinned DMA
+    // staging stays stream-ordered like every other call
+    if (must_sync) cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(stage)");
   }
   li.staged = staged;
   set_last_launch(li);

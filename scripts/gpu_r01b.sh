@@ -1,0 +1,7 @@
+TAG=r01b
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -4 | tee gpurun_out/pytest_$TAG.log
+timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; tail -2 gpurun_out/bench_$TAG.err
+python -c "import json;d=json.load(open('gpurun_out/bench_$TAG.json'));print(d['value'],d['e2e'],d['roofline'],d['halo'],d['cpu_baseline'],d['clocks'])"
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:k_ --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline --e2e-incount 1 --no-halo > /dev/null 2>&1
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 2>/dev/null | tail -1 > gpurun_out/bench_ref_$TAG.json; cat gpurun_out/bench_ref_$TAG.json
+nproc; lscpu | grep "Model name"
