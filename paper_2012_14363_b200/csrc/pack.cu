@@ -32,6 +32,8 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "core.hpp"
@@ -402,6 +404,31 @@ int sm_count() {
 thread_local unsigned t_host_grid_cap = 0;
 constexpr unsigned kHostGridCap = 48;
 constexpr int64_t kDmaStageMin = int64_t{1} << 20; // pinned packed messages >= 1 MiB move by DMA
+
+// Persistent per-(device, stream) staging buffers for DMA'd messages. Work
+// on one stream is ordered, so reuse by the next call on that stream is
+// safe; a pool allocation freed on one stream and reused on another would
+// make the stream-ordered allocator insert a cross-stream dependency and
+// serialise the inbound and outbound legs of a pipelined exchange.
+uint8_t *stage_buffer(cudaStream_t s, size_t bytes) {
+  struct Stage {
+    uint8_t *p = nullptr;
+    size_t n = 0;
+  };
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, Stage> stages;
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(mu);
+  Stage &st = stages[{dev, s}];
+  if (st.n < bytes) {
+    if (st.p) cuda_check(cudaFreeAsync(st.p, s), "cudaFreeAsync(stage)");
+    const size_t n = std::max(bytes, st.n * 2);
+    cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&st.p), n, s), "cudaMallocAsync(stage)");
+    st.n = n;
+  }
+  return st.p;
+}
 
 unsigned grid_for(uint64_t items, int per_thread) {
   const uint64_t blocks = (items + 256ull * per_thread - 1) / (256ull * per_thread);
@@ -945,10 +972,10 @@ int64_t execute(const PackArgs &a) {
   } cap_guard(rs.kind == MemKind::Pinned || (rp.kind == MemKind::Pinned && !dma_packed));
   uint8_t *scratch_s = nullptr, *scratch_p = nullptr;
   bool staged = false, must_sync = false;
+  uint8_t *dma_stage = nullptr;
   if (dma_packed) {
     staged = true;
-    cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&scratch_p), static_cast<size_t>(packed_len), s),
-               "cudaMallocAsync(dma)");
+    dma_stage = scratch_p = stage_buffer(s, static_cast<size_t>(packed_len));
     if (!a.pack)
       cuda_check(cudaMemcpyAsync(scratch_p, static_cast<const uint8_t *>(a.src) + a.position,
                                  static_cast<size_t>(packed_len), cudaMemcpyHostToDevice, s),
@@ -988,7 +1015,7 @@ int64_t execute(const PackArgs &a) {
       cuda_check(cudaMemcpyAsync(a.dst, scratch_s, static_cast<size_t>(strided_len), cudaMemcpyDeviceToHost, s),
                  "stage strided D2H");
     if (scratch_s) cuda_check(cudaFreeAsync(scratch_s, s), "cudaFreeAsync");
-    if (scratch_p) cuda_check(cudaFreeAsync(scratch_p, s), "cudaFreeAsync");
+    if (scratch_p && scratch_p != dma_stage) cuda_check(cudaFreeAsync(scratch_p, s), "cudaFreeAsync");
     // pageable memory is only safe once the copies completed; pinned DMA
     // staging stays stream-ordered like every other call
     if (must_sync) cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize(stage)");
