@@ -263,8 +263,13 @@ sp_status sp_halo_verify(const sp_halo_config *cfg, int64_t rank,
 
 enum { SP_HALO_FUSED = 0, /* pack-to-peer: one batch stores every segment
                              into the receiver's buffer */
-       SP_HALO_COPY = 1   /* pack, per-segment copies, unpack (the
-                             reference's three phases) */ };
+       SP_HALO_COPY = 1,  /* pack, per-segment copies, unpack (the
+                             reference's three phases) */
+       SP_HALO_FUSED_ASYNC = 2 /* distributed plans only: pack-to-peer with
+                             device-side completion flags (stream memory
+                             operations on IPC-mapped peer memory); the
+                             iteration is ordered on the GPU, no host
+                             barrier between pack and unpack */ };
 /* ExchangeReport (halo.hpp:132-138) + measured device times */
 typedef struct {
   double pack_seconds, alltoallv_seconds, unpack_seconds; /* modeled */

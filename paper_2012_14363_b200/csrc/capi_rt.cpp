@@ -36,6 +36,13 @@ struct sp_halo_plan_s {
   std::vector<uint8_t *> peer_send; // COPY method: where to pull segments from
   std::vector<int64_t> copy_src_rank;
   cudaEvent_t ev[4] = {};
+  // SP_HALO_FUSED_ASYNC: per-peer completion flags in device memory,
+  // flags[READY + src] (data of iteration n has landed) and flags[FREE + dst]
+  // (the receiver consumed iteration n); peers' arrays are IPC-mapped
+  uint64_t *flags = nullptr;
+  std::vector<uint8_t *> peer_flags;
+  std::vector<int> out_peers, in_peers; // distinct neighbours
+  uint64_t iter = 0;
   ~sp_halo_plan_s() {
     batch_destroy(pack);
     batch_destroy(unpack);
@@ -43,8 +50,43 @@ struct sp_halo_plan_s {
       if (e) cudaEventDestroy(e);
     if (recv) cudaFree(recv);
     if (send) cudaFree(send);
+    if (flags) cudaFree(flags);
   }
 };
+
+namespace {
+
+// stream memory operations (driver API, resolved at run time)
+using WaitFn = int (*)(cudaStream_t, uint64_t, uint64_t, unsigned);
+using WriteFn = int (*)(cudaStream_t, uint64_t, uint64_t, unsigned);
+struct MemOps {
+  WaitFn wait = nullptr;
+  WriteFn write = nullptr;
+  unsigned wait_flags = 0; // GEQ (+ FLUSH of remote writes when supported)
+};
+const MemOps &memops() {
+  static MemOps m = [] {
+    MemOps o;
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &p, cudaEnableDefault, &q) == cudaSuccess && p)
+      o.wait = reinterpret_cast<WaitFn>(p);
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &p, cudaEnableDefault, &q) == cudaSuccess && p)
+      o.write = reinterpret_cast<WriteFn>(p);
+    cudaGetLastError();
+    int dev = 0, flush = 0;
+    cudaGetDevice(&dev);
+    // CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES = 98 -> CU_STREAM_WAIT_VALUE_FLUSH (1 << 30)
+    if (cudaDeviceGetAttribute(&flush, static_cast<cudaDeviceAttr>(98), dev) == cudaSuccess && flush)
+      o.wait_flags = 1u << 30;
+    cudaGetLastError();
+    return o;
+  }();
+  return m;
+}
+constexpr int kReady = 0, kFree = 1; // flags[kind * size + peer]
+
+} // namespace
 
 extern "C" {
 
@@ -151,7 +193,10 @@ sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int metho
     need(cfgp);
     need(alloc);
     need(out);
-    if (method != SP_HALO_FUSED && method != SP_HALO_COPY) fail(SP_ERR_INVALID_ARGUMENT, "unknown halo method");
+    if (method != SP_HALO_FUSED && method != SP_HALO_COPY && method != SP_HALO_FUSED_ASYNC)
+      fail(SP_ERR_INVALID_ARGUMENT, "unknown halo method");
+    if (method == SP_HALO_FUSED_ASYNC && (!memops().wait || !memops().write))
+      fail(SP_ERR_UNSUPPORTED, "stream memory operations unavailable");
     HaloCfg c{};
     for (int a = 0; a < 3; ++a) {
       c.ranks[a] = cfgp->ranks[a];
@@ -188,7 +233,7 @@ sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int metho
     if (method == SP_HALO_COPY) rt_exchange_ptr(p->send, p->peer_send);
     std::vector<BatchSpec> packs, unpacks;
     for (int j = 0; j < 26; ++j) {
-      if (method == SP_HALO_FUSED) {
+      if (method != SP_HALO_COPY) {
         // segment j of this rank is segment 25-j of the rank at +d_j,
         // written straight into that rank's HBM (halo.hpp:237-254)
         const int64_t to = halo_rank_of(c, p->rank, regions[j].dir);
@@ -205,6 +250,26 @@ sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int metho
     p->pack = batch_create(packs, false);
     p->unpack = batch_create(unpacks, true);
     for (auto &e : p->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    if (method == SP_HALO_FUSED_ASYNC) {
+      const int n = rt_size();
+      cuda_check(cudaMalloc(&p->flags, 2 * n * sizeof(uint64_t)), "cudaMalloc(flags)");
+      cuda_check(cudaMemset(p->flags, 0, 2 * n * sizeof(uint64_t)), "cudaMemset(flags)");
+      cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+      rt_exchange_ptr(p->flags, p->peer_flags);
+      std::vector<char> seen_out(n, 0), seen_in(n, 0);
+      for (int j = 0; j < 26; ++j) {
+        const int64_t nb = halo_rank_of(c, p->rank, regions[j].dir);
+        if (!seen_out[nb]) {
+          seen_out[nb] = 1;
+          p->out_peers.push_back(static_cast<int>(nb));
+        }
+        const int64_t from = halo_rank_of(c, p->rank, {-regions[j].dir[0], -regions[j].dir[1], -regions[j].dir[2]});
+        if (!seen_in[from]) {
+          seen_in[from] = 1;
+          p->in_peers.push_back(static_cast<int>(from));
+        }
+      }
+    }
     *out = p.release();
   });
 }
@@ -215,6 +280,33 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
   return guarded([&] {
     need(p);
     cudaStream_t s = static_cast<cudaStream_t>(rt_stream());
+    if (p->method == SP_HALO_FUSED_ASYNC) {
+      // device-ordered iteration: no host barrier, no host round trip.
+      // wait FREE (receiver consumed n-1) -> pack into peers -> signal
+      // READY=n to each receiver -> wait READY=n from each sender ->
+      // unpack -> signal FREE=n back to each sender.
+      const MemOps &m = memops();
+      const int n = rt_size(), me = p->rank;
+      const uint64_t it = ++p->iter;
+      auto at = [&](uint8_t *base, int kind, int peer) {
+        return reinterpret_cast<uint64_t>(base) + static_cast<uint64_t>(kind * n + peer) * sizeof(uint64_t);
+      };
+      uint8_t *mine = reinterpret_cast<uint8_t *>(p->flags);
+      cuda_check(cudaEventRecord(p->ev[0], s), "cudaEventRecord");
+      for (int q : p->out_peers)
+        if (m.wait(s, at(mine, kFree, q), it - 1, m.wait_flags)) fail(SP_ERR_CUDA, "cuStreamWaitValue64(free)");
+      batch_execute(*p->pack, s);
+      cuda_check(cudaEventRecord(p->ev[1], s), "cudaEventRecord");
+      for (int q : p->out_peers)
+        if (m.write(s, at(p->peer_flags[q], kReady, me), it, 0)) fail(SP_ERR_CUDA, "cuStreamWriteValue64(ready)");
+      for (int q : p->in_peers)
+        if (m.wait(s, at(mine, kReady, q), it, m.wait_flags)) fail(SP_ERR_CUDA, "cuStreamWaitValue64(ready)");
+      cuda_check(cudaEventRecord(p->ev[2], s), "cudaEventRecord");
+      batch_execute(*p->unpack, s);
+      cuda_check(cudaEventRecord(p->ev[3], s), "cudaEventRecord");
+      for (int q : p->in_peers)
+        if (m.write(s, at(p->peer_flags[q], kFree, me), it, 0)) fail(SP_ERR_CUDA, "cuStreamWriteValue64(free)");
+    } else {
     rt_barrier(); // every neighbour has consumed the previous iteration
     cuda_check(cudaEventRecord(p->ev[0], s), "cudaEventRecord");
     batch_execute(*p->pack, s);
@@ -234,6 +326,7 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
     cuda_check(cudaEventRecord(p->ev[2], s), "cudaEventRecord");
     batch_execute(*p->unpack, s);
     cuda_check(cudaEventRecord(p->ev[3], s), "cudaEventRecord");
+    }
     cuda_check(cudaEventSynchronize(p->ev[3]), "cudaEventSynchronize");
     if (times) {
       float a = 0, b = 0, d = 0, t = 0;

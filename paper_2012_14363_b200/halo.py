@@ -13,7 +13,7 @@ from typing import List, Optional, Sequence
 from . import TypeDef, _buffer, _capi, _check, _stream, commit_type
 from ._capi import lib
 
-FUSED, COPY = 0, 1
+FUSED, COPY, FUSED_ASYNC = 0, 1, 2
 
 
 @dataclass

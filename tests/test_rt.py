@@ -133,7 +133,8 @@ def _halo(rank, world, job, ranks, method):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("ranks,method", [((2, 1, 1), 0), ((2, 1, 1), 1), ((1, 3, 1), 0)])
+@pytest.mark.parametrize("ranks,method", [((2, 1, 1), 0), ((2, 1, 1), 1), ((1, 3, 1), 0), ((1, 1, 1), 2),
+                                          ((2, 1, 1), 2), ((2, 2, 1), 2)])
 def test_distributed_halo_exchange(cuda, ranks, method):
     world = ranks[0] * ranks[1] * ranks[2]
     res = _spawn(_halo, world, ranks, method)
