@@ -43,6 +43,8 @@ struct sp_halo_plan_s {
   std::vector<uint8_t *> peer_flags;
   std::vector<int> out_peers, in_peers; // distinct neighbours
   uint64_t iter = 0;
+  unsigned *done = nullptr; // block-completion counters of the pack / unpack launches
+  bool remote_peers = true; // some neighbour's memory is on another GPU
   ~sp_halo_plan_s() {
     batch_destroy(pack);
     batch_destroy(unpack);
@@ -51,39 +53,12 @@ struct sp_halo_plan_s {
     if (recv) cudaFree(recv);
     if (send) cudaFree(send);
     if (flags) cudaFree(flags);
+    if (done) cudaFree(done);
   }
 };
 
 namespace {
 
-// stream memory operations (driver API, resolved at run time)
-using WaitFn = int (*)(cudaStream_t, uint64_t, uint64_t, unsigned);
-using WriteFn = int (*)(cudaStream_t, uint64_t, uint64_t, unsigned);
-struct MemOps {
-  WaitFn wait = nullptr;
-  WriteFn write = nullptr;
-  unsigned wait_flags = 0; // GEQ (+ FLUSH of remote writes when supported)
-};
-const MemOps &memops() {
-  static MemOps m = [] {
-    MemOps o;
-    void *p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &p, cudaEnableDefault, &q) == cudaSuccess && p)
-      o.wait = reinterpret_cast<WaitFn>(p);
-    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &p, cudaEnableDefault, &q) == cudaSuccess && p)
-      o.write = reinterpret_cast<WriteFn>(p);
-    cudaGetLastError();
-    int dev = 0, flush = 0;
-    cudaGetDevice(&dev);
-    // CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES = 98 -> CU_STREAM_WAIT_VALUE_FLUSH (1 << 30)
-    if (cudaDeviceGetAttribute(&flush, static_cast<cudaDeviceAttr>(98), dev) == cudaSuccess && flush)
-      o.wait_flags = 1u << 30;
-    cudaGetLastError();
-    return o;
-  }();
-  return m;
-}
 constexpr int kReady = 0, kFree = 1; // flags[kind * size + peer]
 
 } // namespace
@@ -195,8 +170,6 @@ sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int metho
     need(out);
     if (method != SP_HALO_FUSED && method != SP_HALO_COPY && method != SP_HALO_FUSED_ASYNC)
       fail(SP_ERR_INVALID_ARGUMENT, "unknown halo method");
-    if (method == SP_HALO_FUSED_ASYNC && (!memops().wait || !memops().write))
-      fail(SP_ERR_UNSUPPORTED, "stream memory operations unavailable");
     HaloCfg c{};
     for (int a = 0; a < 3; ++a) {
       c.ranks[a] = cfgp->ranks[a];
@@ -254,8 +227,18 @@ sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int metho
       const int n = rt_size();
       cuda_check(cudaMalloc(&p->flags, 2 * n * sizeof(uint64_t)), "cudaMalloc(flags)");
       cuda_check(cudaMemset(p->flags, 0, 2 * n * sizeof(uint64_t)), "cudaMemset(flags)");
+      cuda_check(cudaMalloc(&p->done, 2 * sizeof(unsigned)), "cudaMalloc(done)");
+      cuda_check(cudaMemset(p->done, 0, 2 * sizeof(unsigned)), "cudaMemset(done)");
       cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
       rt_exchange_ptr(p->flags, p->peer_flags);
+      int mydev = 0;
+      cuda_check(cudaGetDevice(&mydev), "cudaGetDevice");
+      p->remote_peers = false;
+      for (uint8_t *pf : p->peer_flags) {
+        cudaPointerAttributes at{};
+        if (pf && cudaPointerGetAttributes(&at, pf) == cudaSuccess && at.device != mydev) p->remote_peers = true;
+      }
+      cudaGetLastError();
       std::vector<char> seen_out(n, 0), seen_in(n, 0);
       for (int j = 0; j < 26; ++j) {
         const int64_t nb = halo_rank_of(c, p->rank, regions[j].dir);
@@ -281,31 +264,40 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
     need(p);
     cudaStream_t s = static_cast<cudaStream_t>(rt_stream());
     if (p->method == SP_HALO_FUSED_ASYNC) {
-      // device-ordered iteration: no host barrier, no host round trip.
-      // wait FREE (receiver consumed n-1) -> pack into peers -> signal
-      // READY=n to each receiver -> wait READY=n from each sender ->
-      // unpack -> signal FREE=n back to each sender.
-      const MemOps &m = memops();
+      // device-ordered iteration, signalled from inside the kernels: the
+      // pack batch waits (in every block) until each receiver has consumed
+      // iteration n-1, stores the segments into the receivers' HBM, and its
+      // last block release-stores READY=n into each receiver's flags; the
+      // unpack batch waits for READY=n from each sender and releases FREE=n
+      // back. No host barrier, no stream memory op, no host round trip.
       const int n = rt_size(), me = p->rank;
       const uint64_t it = ++p->iter;
       auto at = [&](uint8_t *base, int kind, int peer) {
-        return reinterpret_cast<uint64_t>(base) + static_cast<uint64_t>(kind * n + peer) * sizeof(uint64_t);
+        return reinterpret_cast<uint64_t *>(base + static_cast<size_t>(kind * n + peer) * sizeof(uint64_t));
       };
       uint8_t *mine = reinterpret_cast<uint8_t *>(p->flags);
+      BatchSignal ps, us;
+      for (int q : p->out_peers) {
+        ps.wait.push_back(at(mine, kFree, q));
+        ps.signal.push_back(at(p->peer_flags[q], kReady, me));
+      }
+      ps.wait_value = it - 1;
+      ps.signal_value = it;
+      ps.done = p->done;
+      for (int q : p->in_peers) {
+        us.wait.push_back(at(mine, kReady, q));
+        us.signal.push_back(at(p->peer_flags[q], kFree, me));
+      }
+      us.wait_value = it;
+      us.signal_value = it;
+      us.done = p->done + 1;
+      ps.sys_scope = us.sys_scope = p->remote_peers;
       cuda_check(cudaEventRecord(p->ev[0], s), "cudaEventRecord");
-      for (int q : p->out_peers)
-        if (m.wait(s, at(mine, kFree, q), it - 1, m.wait_flags)) fail(SP_ERR_CUDA, "cuStreamWaitValue64(free)");
-      batch_execute(*p->pack, s);
+      batch_execute_signaled(*p->pack, s, ps);
       cuda_check(cudaEventRecord(p->ev[1], s), "cudaEventRecord");
-      for (int q : p->out_peers)
-        if (m.write(s, at(p->peer_flags[q], kReady, me), it, 0)) fail(SP_ERR_CUDA, "cuStreamWriteValue64(ready)");
-      for (int q : p->in_peers)
-        if (m.wait(s, at(mine, kReady, q), it, m.wait_flags)) fail(SP_ERR_CUDA, "cuStreamWaitValue64(ready)");
       cuda_check(cudaEventRecord(p->ev[2], s), "cudaEventRecord");
-      batch_execute(*p->unpack, s);
+      batch_execute_signaled(*p->unpack, s, us);
       cuda_check(cudaEventRecord(p->ev[3], s), "cudaEventRecord");
-      for (int q : p->in_peers)
-        if (m.write(s, at(p->peer_flags[q], kFree, me), it, 0)) fail(SP_ERR_CUDA, "cuStreamWriteValue64(free)");
     } else {
     rt_barrier(); // every neighbour has consumed the previous iteration
     cuda_check(cudaEventRecord(p->ev[0], s), "cudaEventRecord");

@@ -162,6 +162,16 @@ struct Batch;
 Batch *batch_create(const std::vector<BatchSpec> &specs, bool unpack);
 void batch_execute(const Batch &b, void *stream);
 void batch_destroy(Batch *b);
+// in-kernel completion protocol for distributed exchanges (pack.cu)
+struct BatchSignal {
+  std::vector<const uint64_t *> wait; // local flags, each must reach wait_value
+  uint64_t wait_value = 0;
+  std::vector<uint64_t *> signal;     // (peer) flags set to signal_value at the end
+  uint64_t signal_value = 0;
+  unsigned *done = nullptr;           // device counter, zero-initialised, one per stream
+  bool sys_scope = true;              // a destination is on another GPU
+};
+void batch_execute_signaled(const Batch &b, void *stream, const BatchSignal &sig);
 int64_t batch_bytes(const Batch &b);
 
 } // namespace spb

@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -725,12 +726,43 @@ struct BatchJob {
 };
 
 // one launch per (word size, direction) group; all jobs of a group share W
+// Optional in-kernel completion protocol (distributed halo): every block
+// first waits until each `wait` flag (local memory, written by peers over
+// NVLink) reaches wait_value; after the last chunk, the LAST block to finish
+// publishes signal_value to each `signal` flag (peer memory) with a
+// system-scope release store, after system-scope fences by every thread.
+constexpr int kMaxSig = 32;
+struct BatchSig {
+  const unsigned long long *wait[kMaxSig];
+  unsigned long long *signal[kMaxSig];
+  unsigned long long wait_value, signal_value;
+  unsigned *done; // block-completion counter of this launch (device memory)
+  int n_wait, n_signal;
+  int sys_scope;  // some destination lives on another GPU: system-scope fences
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 template <int W, bool PACK>
 __global__ void __launch_bounds__(256) k_batch(const BatchJob *__restrict__ jobs,
-                                               const uint32_t *__restrict__ chunk0, int njobs, uint32_t nchunks) {
+                                               const uint32_t *__restrict__ chunk0, int njobs, uint32_t nchunks,
+                                               const BatchSig sig) {
   using T = typename Word<W>::T;
   __shared__ BatchJob sj;
   int loaded = -1;
+  if (sig.n_wait) {
+    if (threadIdx.x < static_cast<unsigned>(sig.n_wait))
+      while (ld_acquire_sys(sig.wait[threadIdx.x]) < sig.wait_value) __nanosleep(100);
+    __syncthreads();
+  }
   for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
     int lo = 0, hi = njobs - 1;
     while (lo < hi) {
@@ -773,6 +805,26 @@ __global__ void __launch_bounds__(256) k_batch(const BatchJob *__restrict__ jobs
           st_stream(reinterpret_cast<T *>(sj.out + soff[u]), v[u]);
         }
       }
+    }
+  }
+  if (sig.n_signal) {
+    // bar.sync orders every thread's stores before thread 0 (CTA scope);
+    // thread 0's system-scope fence is cumulative over them
+    __syncthreads();
+    // every block releases its stores before counting itself done: at GPU
+    // scope when all destinations are on this device, at system scope when
+    // some were written over NVLink into a peer GPU
+    if (threadIdx.x == 0) {
+      if (sig.sys_scope) {
+        __threadfence_system();
+      } else {
+        __threadfence();
+      }
+    }
+    if (threadIdx.x == 0 && atomicAdd(sig.done, 1u) == gridDim.x - 1) {
+      __threadfence_system();
+      for (int i = 0; i < sig.n_signal; ++i) st_release_sys(sig.signal[i], sig.signal_value);
+      atomicExch(sig.done, 0u); // ready for the next launch on this stream
     }
   }
 }
@@ -888,22 +940,41 @@ Batch *batch_create(const std::vector<BatchSpec> &specs, bool unpack) {
   return b.release();
 }
 
-void batch_execute(const Batch &b, void *stream) {
+namespace {
+void batch_launch(const Batch &b, void *stream, const BatchSignal *bs) {
   sp_launch_info li{};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  for (const BatchGroup &g : b.groups) {
+  for (size_t gi = 0; gi < b.groups.size(); ++gi) {
+    const BatchGroup &g = b.groups[gi];
+    BatchSig sig{};
+    if (bs) { // wait in the first kernel, signal from the last
+      if (bs->wait.size() > static_cast<size_t>(kMaxSig) || bs->signal.size() > static_cast<size_t>(kMaxSig))
+        fail(SP_ERR_UNSUPPORTED, "batch signalling: more than 32 peers");
+      if (gi == 0) {
+        sig.n_wait = static_cast<int>(bs->wait.size());
+        for (int i = 0; i < sig.n_wait; ++i) sig.wait[i] = reinterpret_cast<const unsigned long long *>(bs->wait[i]);
+        sig.wait_value = bs->wait_value;
+      }
+      if (gi + 1 == b.groups.size()) {
+        sig.n_signal = static_cast<int>(bs->signal.size());
+        for (int i = 0; i < sig.n_signal; ++i) sig.signal[i] = reinterpret_cast<unsigned long long *>(bs->signal[i]);
+        sig.signal_value = bs->signal_value;
+        sig.done = bs->done;
+        sig.sys_scope = bs->sys_scope ? 1 : 0;
+      }
+    }
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(g.nchunks, static_cast<uint64_t>(sm_count()) * 8));
     switch (g.w * 2 + g.pack) {
-    case 33: k_batch<16, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
-    case 32: k_batch<16, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
-    case 17: k_batch<8, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
-    case 16: k_batch<8, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
-    case 9: k_batch<4, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
-    case 8: k_batch<4, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
-    case 5: k_batch<2, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
-    case 4: k_batch<2, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
-    case 3: k_batch<1, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
-    default: k_batch<1, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks); break;
+    case 33: k_batch<16, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
+    case 32: k_batch<16, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
+    case 17: k_batch<8, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
+    case 16: k_batch<8, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
+    case 9: k_batch<4, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
+    case 8: k_batch<4, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
+    case 5: k_batch<2, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
+    case 4: k_batch<2, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
+    case 3: k_batch<1, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
+    default: k_batch<1, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
     }
     cuda_check(cudaGetLastError(), "k_batch launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -913,6 +984,14 @@ void batch_execute(const Batch &b, void *stream) {
     li.block = 256;
   }
   set_last_launch(li);
+}
+} // namespace
+
+void batch_execute(const Batch &b, void *stream) { batch_launch(b, stream, nullptr); }
+
+void batch_execute_signaled(const Batch &b, void *stream, const BatchSignal &sig) {
+  if (b.groups.empty()) fail(SP_ERR_UNSUPPORTED, "batch signalling needs at least one non-empty job");
+  batch_launch(b, stream, &sig);
 }
 
 void batch_destroy(Batch *b) { delete b; }
