@@ -68,22 +68,62 @@ def peaks():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+    """SM clock and throttle reasons sampled DURING the timed region
+    (B200_PROFILING.md's clocks line). The timed region is tens of ms, shorter
+    than nvidia-smi's sampling period, so the same NVML counters nvidia-smi
+    reads are polled from a thread every 2 ms; nvidia-smi -lms is the
+    fallback when NVML is unavailable."""
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
         self.proc = None
         self.lines = []
+        self.nvml = []  # (sm_mhz, max_mhz, reason_bits)
+        self.source = None
+        self._stop = threading.Event()
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            uuid = "GPU-" + str(torch.cuda.get_device_properties(self.index).uuid)
+            return pynvml, pynvml.nvmlDeviceGetHandleByUUID(uuid)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _poll(self, pynvml, h):
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while True:
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.nvml.append((sm, mx, bits))
+            except Exception:
+                pass
+            if self._stop.wait(0.002):
+                break
 
     def __enter__(self):
+        try:
+            pynvml, h = self._nvml_handle()
+            self.source = "nvml-2ms"
+            self.t = threading.Thread(target=self._poll, args=(pynvml, h), daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            pass
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.source = "nvidia-smi-100ms"
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except (OSError, FileNotFoundError):
@@ -95,15 +135,24 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self._stop.set()
         if self.proc is not None:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        elif self.source:
+            self.t.join(timeout=5)
 
     def summary(self):
         sm, mx, reasons = [], None, set()
+        for s_, m_, bits in self.nvml:
+            sm.append(float(s_))
+            mx = float(m_)
+            for n, bit in self.REASONS.items():
+                if bits & bit:
+                    reasons.add(n)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -120,7 +169,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": self.source}
 
 
 # ------------------------------------------------------------------ distributed
@@ -315,7 +364,7 @@ def run_ours(args):
     src[::4099] = 3  # touch; content is irrelevant to timing (parity is in tests/)
     packed = torch.zeros(K << 20, dtype=torch.uint8, device="cuda")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-    flush_sink = torch.empty(1, dtype=torch.int64, device="cuda")
+    flush_sink = torch.empty((), dtype=torch.int64, device="cuda")
 
     def flush_l2(i):
         # write 512 MiB (> 126 MB L2), then read it back: the dirty lines are

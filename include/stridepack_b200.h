@@ -133,7 +133,9 @@ enum {
   SP_KERNEL_TMA = 4,      /* tensor-map box staged through shared memory */
   SP_KERNEL_WORDS64 = 5,  /* generic kernel with 64-bit indexing (chosen
                              automatically beyond 2^32 words or rows) */
-  SP_KERNEL_BATCH = 6     /* many jobs in one launch (sp_batch_*) */
+  SP_KERNEL_BATCH = 6,    /* many jobs in one launch (sp_batch_*) */
+  SP_KERNEL_SHIFT = 7     /* misaligned rows >= 16 B: aligned 16-B packed
+                             chunks assembled by funnel shifts */
 };
 typedef struct {
   int allow_fallback; /* PackOptions.allow_fallback (default 1) */

@@ -133,6 +133,8 @@ class Kernel(enum.IntEnum):
     BlockList = 3
     TMA = 4
     Words64 = 5
+    Batch = 6
+    Shift = 7
 
 
 # ------------------------------------------------------------------ types

@@ -285,6 +285,136 @@ __global__ void __launch_bounds__(256) k_smallrow(const uint8_t *__restrict__ in
   }
 }
 
+// ------------------------------------------------------------ k_shift
+// Rows (c0 >= 16 B) whose strided-side addresses or strides are not word
+// aligned (e.g. a subarray starting at byte 3) would force W = 1 in k_words.
+// The shift kernels keep 16-B accesses by aligning the work to the 16-B grid
+// of the side that is WRITTEN and funnel-shifting what is read:
+//   k_shift_pack   : lane = one aligned 16-B packed chunk (touches <= 2 rows,
+//                    since c0 >= 16), built from the aligned source blocks
+//                    that hold its bytes -> one STG.128;
+//   k_shift_unpack : lane = one aligned 16-B block of a destination row
+//                    (ceil(c0/16)+1 slots per row, empty ones skip), read
+//                    from the packed blocks that hold its bytes -> one
+//                    STG.128 inside the row, masked u32/u8 stores at its ends.
+// Only aligned blocks that contain described bytes are loaded or stored, so
+// no access leaves the blocks the layout touches.
+// Auto-selection, from scripts/shift_bench.py on B200 (profiles/r01_shift_bench.json):
+//   pack  : 4.0-5.1 TB/s against 1.26 (W=1) and 3.6-4.4 (W=4, c0 % 16 == 0);
+//           at W=4 with c0 % 16 != 0 the word kernel stays ahead;
+//   unpack: 1.6-2.5 TB/s against 1.33 (W=1) for c0 >= 128; shorter rows lose
+//           to W=1 because the row-end partial blocks become per-lane
+//           scattered sub-word stores.
+static bool shift_wins(bool pack, int w, int64_t c0) {
+  if (pack) return w <= 2 || (w == 4 && c0 % 16 == 0);
+  return w <= 2 && c0 >= 128;
+}
+
+// the 16 bytes starting at (window), of which only [lo, hi) are meaningful;
+// aligned 16-B blocks not intersecting [lo, hi) are never read
+__device__ __forceinline__ uint4 load_window(const uint8_t *window, const uint8_t *lo, const uint8_t *hi) {
+  const uintptr_t w = reinterpret_cast<uintptr_t>(window);
+  const uintptr_t b0 = w & ~uintptr_t{15}, b1 = b0 + 16;
+  const uintptr_t l = reinterpret_cast<uintptr_t>(lo), h = reinterpret_cast<uintptr_t>(hi);
+  uint4 x0 = make_uint4(0, 0, 0, 0), x1 = make_uint4(0, 0, 0, 0);
+  if (l < b0 + 16 && h > b0) x0 = ld_stream(reinterpret_cast<const uint4 *>(b0));
+  const unsigned d = static_cast<unsigned>(w & 15);
+  if (d && l < b1 + 16 && h > b1) x1 = ld_stream(reinterpret_cast<const uint4 *>(b1));
+  const uint32_t W[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+  const unsigned q = d >> 2, sh = (d & 3) * 8;
+  uint32_t v[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) { // v[k] = W[k + q], selects instead of local memory
+    const uint32_t a = k + 0 < 8 ? W[k] : 0, b = k + 1 < 8 ? W[k + 1] : 0;
+    const uint32_t c = k + 2 < 8 ? W[k + 2] : 0, e = k + 3 < 8 ? W[k + 3] : 0;
+    v[k] = q == 0 ? a : q == 1 ? b : q == 2 ? c : e;
+  }
+  return make_uint4(__funnelshift_r(v[0], v[1], sh), __funnelshift_r(v[1], v[2], sh),
+                    __funnelshift_r(v[2], v[3], sh), __funnelshift_r(v[3], v[4], sh));
+}
+
+__device__ __forceinline__ uint4 merge_bytes(uint4 a, uint4 b, unsigned n) { // bytes [0,n) of a, rest of b
+  uint32_t r[4];
+  const uint32_t A[4] = {a.x, a.y, a.z, a.w}, B[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int lo = static_cast<int>(n) - 4 * k; // bytes of word k taken from a
+    const uint32_t m = lo >= 4 ? 0xffffffffu : lo <= 0 ? 0u : (0xffffffffu >> (32 - 8 * lo));
+    r[k] = (A[k] & m) | (B[k] & ~m);
+  }
+  return make_uint4(r[0], r[1], r[2], r[3]);
+}
+
+// bytes [lo, hi) of the aligned 16-B block at blk: whole u32 words where
+// covered, single bytes at the two ends
+__device__ __forceinline__ void store_masked(uint8_t *blk, uint4 z, unsigned lo, unsigned hi) {
+  const uint32_t Z[4] = {z.x, z.y, z.z, z.w};
+#pragma unroll
+  for (unsigned i = 0; i < 4; ++i) {
+    if (lo <= 4 * i && 4 * i + 4 <= hi) {
+      st_stream(reinterpret_cast<uint32_t *>(blk) + i, Z[i]);
+    } else {
+#pragma unroll
+      for (unsigned b = 0; b < 4; ++b) {
+        const unsigned k = 4 * i + b;
+        if (lo <= k && k < hi) st_stream(blk + k, static_cast<uint8_t>(Z[i] >> (8 * b)));
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_shift_pack(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
+                                                    const Geom g, uint32_t c0, FastDiv c0div) {
+  const uint32_t nchunks = static_cast<uint32_t>(g.total);
+  const uint64_t T = g.rows * c0;
+  const uint32_t step = gridDim.x * blockDim.x;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nchunks; t += step) {
+    const int64_t lo = static_cast<int64_t>(t) * 16 - static_cast<int64_t>(g.head);
+    if (lo >= 0 && static_cast<uint64_t>(lo) + 16 <= T) {
+      const uint32_t p = static_cast<uint32_t>(lo);
+      const uint32_t r = fdiv(p, c0div), col = p - r * c0;
+      const unsigned n1 = min(16u, c0 - col);
+      const uint8_t *a = in + row_offset(r, g) + col;
+      uint4 v = load_window(a, a, a + n1);
+      if (n1 < 16) { // the chunk continues at the start of row r + 1
+        const uint8_t *b = in + row_offset(r + 1, g);
+        v = merge_bytes(v, load_window(b - n1, b, b + (16 - n1)), n1);
+      }
+      st_stream(reinterpret_cast<uint4 *>(out + p), v);
+    } else { // first / last chunk: byte by byte over its valid range
+      const int64_t b0 = lo < 0 ? 0 : lo;
+      const int64_t b1 = static_cast<int64_t>(T) < lo + 16 ? static_cast<int64_t>(T) : lo + 16;
+      for (int64_t p = b0; p < b1; ++p) {
+        const uint32_t pp = static_cast<uint32_t>(p);
+        const uint32_t r = fdiv(pp, c0div), col = pp - r * c0;
+        out[p] = in[row_offset(r, g) + col];
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_shift_unpack(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
+                                                      const Geom g, uint32_t c0, uint32_t slots, FastDiv sdiv) {
+  const uint32_t nitems = static_cast<uint32_t>(g.total);
+  const uint32_t step = gridDim.x * blockDim.x;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nitems; t += step) {
+    const uint32_t r = fdiv(t, sdiv), j = t - r * slots;
+    const uintptr_t A = reinterpret_cast<uintptr_t>(out + row_offset(r, g)); // row start
+    const uintptr_t B = (A & ~uintptr_t{15}) + 16 * uintptr_t{j};           // this lane's block
+    const uintptr_t vlo = B > A ? B : A, vhi = B + 16 < A + c0 ? B + 16 : A + c0;
+    if (vlo >= vhi) continue;
+    const uint8_t *P = in + static_cast<uint64_t>(r) * c0; // packed row start
+    const uint4 z = load_window(P + static_cast<intptr_t>(B - A), P + (vlo - A), P + (vhi - A));
+    uint8_t *blk = reinterpret_cast<uint8_t *>(B);
+    const unsigned lo = static_cast<unsigned>(vlo - B), hi = static_cast<unsigned>(vhi - B);
+    if (lo == 0 && hi == 16) {
+      st_stream(reinterpret_cast<uint4 *>(blk), z);
+    } else {
+      store_masked(blk, z, lo, hi);
+    }
+  }
+}
+
 // ------------------------------------------------------------ k_blocklist
 // One thread per (object, run): byte loop over the run. Used only for
 // definition-order gathers (Unsupported forms, pack.hpp:123-135) and for
@@ -618,6 +748,13 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
     kernel = SP_KERNEL_WORDS64;
   }
   if (kernel == SP_KERNEL_SMALLROW && !smallrow_ok) fail(SP_ERR_INVALID_ARGUMENT, "smallrow kernel not applicable");
+  // misaligned long rows: the word would be < kShiftBelow only because of
+  // addresses / strides, the shift kernel keeps 16-B packed-side accesses
+  const bool shift_ok = rd.c0 >= 16 && fits32 && total_bytes < (1ull << 32);
+  if (kernel == SP_KERNEL_WORDS && opt.kernel == SP_KERNEL_AUTO && !opt.force_word && shift_ok &&
+      shift_wins(pack, w, rd.c0))
+    kernel = SP_KERNEL_SHIFT;
+  if (kernel == SP_KERNEL_SHIFT && !shift_ok) fail(SP_ERR_INVALID_ARGUMENT, "shift kernel not applicable");
   // unpack of long rows: the TMA store path measured 5-9% ahead of the
   // LDG/STG kernel at c0 >= 128 (profiles/r01_tma_vs_words.txt); pack ties
   if (kernel == SP_KERNEL_WORDS && opt.kernel == SP_KERNEL_AUTO && !pack && !opt.force_word && rd.c0 >= 128 &&
@@ -672,6 +809,23 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
       dispatch_smallrow<false>(static_cast<int>(rd.c0), in, sout, g, s, li);
     }
     li.word = rd.c0;
+  } else if (kernel == SP_KERNEL_SHIFT) {
+    unsigned grid = 0;
+    if (pack) { // aligned 16-B packed chunks
+      g.head = packed_addr & 15;
+      g.total = (total_bytes + g.head + 15) / 16;
+      grid = grid_for(g.total, 1);
+      k_shift_pack<<<grid, 256, 0, s>>>(sin, out, g, static_cast<uint32_t>(rd.c0),
+                                        make_fastdiv(static_cast<uint32_t>(rd.c0)));
+    } else { // aligned 16-B destination blocks, ceil(c0/16)+1 slots per row
+      const uint32_t slots = static_cast<uint32_t>((rd.c0 + 15) / 16 + 1);
+      g.total = rows * slots;
+      grid = grid_for(g.total, 1);
+      k_shift_unpack<<<grid, 256, 0, s>>>(in, sout, g, static_cast<uint32_t>(rd.c0), slots, make_fastdiv(slots));
+    }
+    li.grid = grid;
+    li.block = 256;
+    li.word = 16;
   } else if (fits32) {
     g.wpr = static_cast<uint32_t>(rd.c0 / w);
     g.wdiv = make_fastdiv(g.wpr);

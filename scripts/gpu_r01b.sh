@@ -1,4 +1,4 @@
-TAG=r01b
+TAG=${1:-r01b}
 timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -4 | tee gpurun_out/pytest_$TAG.log
 timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; tail -2 gpurun_out/bench_$TAG.err
 python -c "import json;d=json.load(open('gpurun_out/bench_$TAG.json'));print(d['value'],d['e2e'],d['roofline'],d['halo'],d['cpu_baseline'],d['clocks'])"

@@ -176,10 +176,12 @@ def test_reference_golden_digests(sp, cuda, pack_digests):
 
 
 # ------------------------------------------------------------ randomized parity
-KERNELS = ["auto", "words", "words_w1", "blocklist", "words64"]
+KERNELS = ["auto", "words", "words_w1", "blocklist", "words64", "shift"]
 
 
 def _opts(sp, ct, which):
+    if which == "shift":
+        return dict(kernel=sp.Kernel.Shift)
     if which == "words":
         return dict(kernel=sp.Kernel.Words)
     if which == "words_w1":
@@ -206,6 +208,8 @@ def test_corpus_parity_all_kernels(sp, orc, cuda, corpus, which):
         prog = e["prog"]
         ct = sp.commit_type(sp.from_program(prog))
         if which == "words64" and ct.form != sp.CanonForm.Strided:
+            continue
+        if which == "shift" and (ct.form != sp.CanonForm.Strided or ct.canon.counts[0] < 16):
             continue
         inc = 1 + int(rng.integers(0, 3))
         pos = int(rng.integers(0, 19))
@@ -235,7 +239,49 @@ def test_corpus_parity_all_kernels(sp, orc, cuda, corpus, which):
             assert np.array_equal(ob[sshift:sshift + span], exp), prog
             assert (ob[:sshift] == 0x5A).all() and (ob[sshift + span:] == 0x5A).all()
         checked += 1
-    assert checked > 500
+    assert checked > (150 if which == "shift" else 500)
+
+
+@pytest.mark.parametrize("c0", [16, 17, 31, 33, 100, 255, 4099])
+def test_shift_kernel_misaligned_rows(sp, orc, cuda, c0):
+    """rows >= 16 B whose strided-side addresses are not word aligned (byte
+    offsets into a subarray) run the funnel-shift kernel: exact for every
+    strided / packed misalignment pair, sentinels intact on both sides"""
+    torch = cuda
+    rows = 37
+    pitch = c0 + 5
+    prog = [3, rows, 1, pitch, 1, c0, 0, 0]  # hvector(rows,1,pitch,contiguous(c0,BYTE))
+    ct = sp.commit_type(sp.from_program(prog))
+    rng = np.random.default_rng(c0)
+    host = rng.integers(0, 256, ct.span, dtype=np.uint8)
+    want = np.zeros(ct.size, np.uint8)
+    assert orc.pack(prog, host, 1, want, 0)[0] == 0
+    for sshift in (0, 1, 3, 8, 13):
+        sbuf = torch.zeros(ct.span + 32, dtype=torch.uint8, device="cuda")
+        sbuf[sshift:sshift + ct.span] = dev(torch, host)
+        for dshift in (0, 5, 15):
+            dbuf = torch.full((ct.size + 32,), 0xEE, dtype=torch.uint8, device="cuda")
+            sp.pack(sbuf[sshift:sshift + ct.span], ct, 1, dbuf[dshift:dshift + ct.size], 0)
+            li = sp.last_launch()
+            assert li.kernel == sp.Kernel.Shift, li
+            got = dbuf.cpu().numpy()
+            assert np.array_equal(got[dshift:dshift + ct.size], want), (sshift, dshift)
+            assert (got[:dshift] == 0xEE).all() and (got[dshift + ct.size:] == 0xEE).all()
+            obuf = torch.full((ct.span + 32,), 0x5A, dtype=torch.uint8, device="cuda")
+            sp.unpack(dbuf[dshift:dshift + ct.size], 0, ct, 1, obuf[sshift:sshift + ct.span],
+                      kernel=sp.Kernel.Shift)
+            assert sp.last_launch().kernel == sp.Kernel.Shift
+            exp = np.full(ct.span, 0x5A, np.uint8)
+            assert orc.unpack(prog, want, 0, 1, exp)[0] == 0
+            ob = obuf.cpu().numpy()
+            assert np.array_equal(ob[sshift:sshift + ct.span], exp), (sshift, dshift)
+            assert (ob[:sshift] == 0x5A).all() and (ob[sshift + ct.span:] == 0x5A).all()
+            # automatic choice: shift for unpack of long misaligned rows only
+            obuf.fill_(0x5A)
+            sp.unpack(dbuf[dshift:dshift + ct.size], 0, ct, 1, obuf[sshift:sshift + ct.span])
+            auto = sp.last_launch().kernel
+            assert auto == (sp.Kernel.Shift if c0 >= 128 else sp.Kernel.Words), (c0, auto)
+            assert np.array_equal(obuf.cpu().numpy()[sshift:sshift + ct.span], exp)
 
 
 def test_smallrow_kernel_selected_and_exact(sp, orc, cuda):
