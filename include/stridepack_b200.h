@@ -76,6 +76,18 @@ sp_status sp_type_free(sp_type t);
 sp_status sp_type_size(sp_type t, int64_t *size);
 /* type_extent                type_def.hpp:221 */
 sp_status sp_type_extent(sp_type t, int64_t *extent);
+/* flatten_oracle (block_list.hpp:123-126; CLI `flatten`, cli.hpp:98-108):
+ * the definition's byte runs, sorted, abutting/overlapping runs merged
+ * (normalize_blocks, block_list.hpp:44-61). *n = run count; the arrays are
+ * filled when cap >= *n; *overlap = 1 if some byte is described twice. */
+sp_status sp_type_flatten(sp_type t, int64_t *offsets, int64_t *lengths,
+                          int64_t cap, int64_t *n, int *overlap);
+/* parse_type_file (typefile.hpp:131-258): parses a type-description text
+ * and returns a NEW uncommitted handle for the committed statement's type;
+ * `name` (if cap > 0) receives its name. Diagnostics are SP_ERR_PARSE with
+ * "line N: ..." messages (sp_last_error). */
+sp_status sp_typefile_parse(const char *text, sp_type *out, char *name,
+                            int64_t name_cap);
 
 /* ---- commit: commit.hpp:51 (commit_type) / :87 (TypeRegistry::commit) -
  * Canonicalises the definition (translate -> fold/elide/flatten/sort to a
@@ -184,7 +196,29 @@ typedef struct sp_batch_s *sp_batch;
 sp_status sp_batch_create(const sp_batch_job *jobs, int64_t n, int unpack,
                           sp_batch *out);
 sp_status sp_batch_execute(sp_batch b, void *stream);
-/* packed bytes one execution moves */
+/* Typed copies in ONE launch (no packed intermediate): byte k of `count`
+ * objects of `src_type` at src (pack order) is stored at byte k of
+ * `dst_count` objects of `dst_type` at dst (unpack order) -- the pack of
+ * pack.hpp:99 fused with the unpack of pack.hpp:143 that MPI_Sendrecv with
+ * two datatypes, a self-send, or MPI_Neighbor_alltoallw would run. Both
+ * sides must describe the same byte count (SP_ERR_INVALID_ARGUMENT), the
+ * destination must not overlap itself (SP_ERR_OVERLAPPING_LAYOUT), the
+ * buffers must cover (count-1)*extent+span (SP_ERR_BUFFER_TOO_SMALL), and
+ * both types need a strided form (SP_ERR_UNSUPPORTED). dst may be peer-GPU
+ * memory mapped through CUDA IPC (copy-to-peer over NVLink). */
+typedef struct {
+  const void *src;
+  uint64_t src_bytes;
+  sp_type src_type;
+  int64_t src_count;
+  void *dst;
+  uint64_t dst_bytes;
+  sp_type dst_type;
+  int64_t dst_count;
+} sp_copy_job;
+sp_status sp_copy_batch_create(const sp_copy_job *jobs, int64_t n,
+                               sp_batch *out);
+/* payload bytes one execution moves */
 sp_status sp_batch_bytes(sp_batch b, int64_t *bytes);
 sp_status sp_batch_free(sp_batch b);
 
@@ -267,11 +301,15 @@ enum { SP_HALO_FUSED = 0, /* pack-to-peer: one batch stores every segment
                              into the receiver's buffer */
        SP_HALO_COPY = 1,  /* pack, per-segment copies, unpack (the
                              reference's three phases) */
-       SP_HALO_FUSED_ASYNC = 2 /* distributed plans only: pack-to-peer with
-                             device-side completion flags (stream memory
-                             operations on IPC-mapped peer memory); the
-                             iteration is ordered on the GPU, no host
-                             barrier between pack and unpack */ };
+       SP_HALO_FUSED_ASYNC = 2, /* distributed plans only: pack-to-peer with
+                             in-kernel completion flags (acquire/release on
+                             IPC-mapped peer memory); the iteration is
+                             ordered on the GPU, no host barrier between
+                             pack and unpack */
+       SP_HALO_DIRECT = 3 /* ghost writes: one typed-copy launch moves every
+                             send region straight into the receiving rank's
+                             ghost cells (no packed segment, no unpack); in
+                             distributed plans ordered by in-kernel flags */ };
 /* ExchangeReport (halo.hpp:132-138) + measured device times */
 typedef struct {
   double pack_seconds, alltoallv_seconds, unpack_seconds; /* modeled */

@@ -213,6 +213,52 @@ def make_subarray(ndims: int, sizes: Sequence[int], subsizes: Sequence[int],
                 desc=f"subarray({ndims},{lst(sizes)},{lst(subsizes)},{lst(offsets)},{inner})")
 
 
+@dataclass(frozen=True)
+class Block:                       # block_list.hpp:13-18
+    offset: int
+    length: int
+
+
+@dataclass(frozen=True)
+class BlockList:                   # block_list.hpp:20-40
+    blocks: tuple
+    overlap: bool
+
+    def total_length(self) -> int:
+        return sum(b.length for b in self.blocks)
+
+    def span(self) -> int:
+        return self.blocks[-1].offset + self.blocks[-1].length if self.blocks else 0
+
+
+def flatten(d: TypeDef) -> BlockList:
+    """The definition's normalized byte runs (flatten_oracle,
+    block_list.hpp:123-126; the CLI's `flatten`)."""
+    n = C.c_int64()
+    ov = C.c_int()
+    _check(lib.sp_type_flatten(d.handle, None, None, 0, C.byref(n), C.byref(ov)))
+    off = (C.c_int64 * max(n.value, 1))()
+    ln = (C.c_int64 * max(n.value, 1))()
+    _check(lib.sp_type_flatten(d.handle, off, ln, n.value, C.byref(n), C.byref(ov)))
+    return BlockList(tuple(Block(off[i], ln[i]) for i in range(n.value)), bool(ov.value))
+
+
+@dataclass(frozen=True)
+class TypeFileResult:              # typefile.hpp:27-30
+    name: str
+    def_: TypeDef
+
+
+def parse_type_file(text: str) -> TypeFileResult:
+    """typefile.hpp:131-258: `type <name> = <ctor>(...)` lines and one final
+    `commit <name>`; errors raise ParseError("line N: ...")."""
+    h = _capi.sp_type()
+    name = C.create_string_buffer(256)
+    _check(lib.sp_typefile_parse(text.encode(), C.byref(h), name, 256))
+    nm = name.value.decode()
+    return TypeFileResult(nm, TypeDef(h.value, f"typefile:{nm}"))
+
+
 def type_size(d: TypeDef) -> int:
     return d.size()
 

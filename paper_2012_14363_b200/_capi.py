@@ -60,6 +60,8 @@ _sig("sp_type_size", C.c_int, sp_type, i64p)
 _sig("sp_type_extent", C.c_int, sp_type, i64p)
 _sig("sp_type_commit", C.c_int, sp_type)
 _sig("sp_type_query", C.c_int, sp_type, C.POINTER(TypeInfo), i64p, i64p, i64)
+_sig("sp_type_flatten", C.c_int, sp_type, i64p, i64p, i64, i64p, C.POINTER(C.c_int))
+_sig("sp_typefile_parse", C.c_int, C.c_char_p, C.POINTER(sp_type), C.c_char_p, i64)
 _sig("sp_pack", C.c_int, C.c_void_p, u64, sp_type, i64, C.c_void_p, u64, i64p, C.c_void_p)
 _sig("sp_unpack", C.c_int, C.c_void_p, u64, i64p, sp_type, i64, C.c_void_p, u64, C.c_void_p)
 _sig("sp_pack_ex", C.c_int, C.c_void_p, u64, sp_type, i64, C.c_void_p, u64, i64p, C.c_void_p,
@@ -104,6 +106,14 @@ class BatchJob(C.Structure):
 
 
 _sig("sp_batch_create", C.c_int, C.POINTER(BatchJob), i64, C.c_int, C.POINTER(vp))
+
+
+class CopyJob(C.Structure):
+    _fields_ = [("src", C.c_void_p), ("src_bytes", u64), ("src_type", sp_type), ("src_count", i64),
+                ("dst", C.c_void_p), ("dst_bytes", u64), ("dst_type", sp_type), ("dst_count", i64)]
+
+
+_sig("sp_copy_batch_create", C.c_int, C.POINTER(CopyJob), i64, C.POINTER(vp))
 _sig("sp_batch_execute", C.c_int, vp, vp)
 _sig("sp_batch_bytes", C.c_int, vp, i64p)
 _sig("sp_batch_free", C.c_int, vp)

@@ -108,6 +108,22 @@ sp_status sp_type_extent(sp_type t, int64_t *extent) {
   });
 }
 
+sp_status sp_type_flatten(sp_type t, int64_t *offsets, int64_t *lengths, int64_t cap, int64_t *n, int *overlap) {
+  return guard([&] {
+    if (!n) spb::fail(SP_ERR_INVALID_ARGUMENT, "null output");
+    bool ov = false;
+    const std::vector<spb::Run> runs = spb::flatten_def(*def_of(t), ov);
+    *n = static_cast<int64_t>(runs.size());
+    if (overlap) *overlap = ov ? 1 : 0;
+    if (offsets && lengths && cap >= *n) {
+      for (size_t i = 0; i < runs.size(); ++i) {
+        offsets[i] = runs[i].off;
+        lengths[i] = runs[i].len;
+      }
+    }
+  });
+}
+
 sp_status sp_type_commit(sp_type t) {
   return guard([&] { spb::registry().commit(t); });
 }
@@ -209,6 +225,24 @@ sp_status sp_batch_create(const sp_batch_job *jobs, int64_t n, int unpack, sp_ba
                        jobs[i].dst_bytes, jobs[i].position});
     }
     h->b = spb::batch_create(specs, unpack != 0);
+    *out = h.release();
+  });
+}
+
+sp_status sp_copy_batch_create(const sp_copy_job *jobs, int64_t n, sp_batch *out) {
+  return guard([&] {
+    if (!out || (n > 0 && !jobs) || n < 0) spb::fail(SP_ERR_INVALID_ARGUMENT, "bad batch arguments");
+    auto h = std::make_unique<sp_batch_s>();
+    std::vector<spb::CopySpec> specs;
+    for (int64_t i = 0; i < n; ++i) {
+      const spb::Entry es = spb::registry().get(jobs[i].src_type), ed = spb::registry().get(jobs[i].dst_type);
+      if (!es.committed || !ed.committed) spb::fail(SP_ERR_INVALID_ARGUMENT, "type is not committed");
+      h->keep.push_back(es.committed);
+      h->keep.push_back(ed.committed);
+      specs.push_back({es.committed.get(), jobs[i].src, jobs[i].src_bytes, jobs[i].src_count, ed.committed.get(),
+                       jobs[i].dst, jobs[i].dst_bytes, jobs[i].dst_count});
+    }
+    h->b = spb::copy_batch_create(specs);
     *out = h.release();
   });
 }

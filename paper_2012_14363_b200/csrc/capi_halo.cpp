@@ -77,7 +77,8 @@ sp_status sp_halo_verify(const sp_halo_config *cfg, int64_t rank, const void *al
 sp_status sp_halo_run(const sp_halo_config *cfg, sp_profile profile, int method, int iters, sp_halo_report *out) {
   return guarded([&] {
     need(out);
-    if (method != SP_HALO_FUSED && method != SP_HALO_COPY) fail(SP_ERR_INVALID_ARGUMENT, "unknown halo method");
+    if (method != SP_HALO_FUSED && method != SP_HALO_COPY && method != SP_HALO_DIRECT)
+      fail(SP_ERR_INVALID_ARGUMENT, "unknown halo method");
     if (iters < 1) fail(SP_ERR_INVALID_ARGUMENT, "iters must be positive");
     const HaloReport r = halo_run(cfg_of(cfg), profile ? profile->p.get() : nullptr, method, iters);
     out->pack_seconds = r.model_pack_s;

@@ -168,7 +168,8 @@ sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int metho
     need(cfgp);
     need(alloc);
     need(out);
-    if (method != SP_HALO_FUSED && method != SP_HALO_COPY && method != SP_HALO_FUSED_ASYNC)
+    if (method != SP_HALO_FUSED && method != SP_HALO_COPY && method != SP_HALO_FUSED_ASYNC &&
+        method != SP_HALO_DIRECT)
       fail(SP_ERR_INVALID_ARGUMENT, "unknown halo method");
     HaloCfg c{};
     for (int a = 0; a < 3; ++a) {
@@ -199,12 +200,25 @@ sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int metho
     p->keep = sct;
     p->keep.insert(p->keep.end(), rct.begin(), rct.end());
     p->seg_total = p->seg_off[26];
+    std::vector<BatchSpec> packs, unpacks;
+    if (method == SP_HALO_DIRECT) {
+      // ghost writes: region j of this rank lands in region 25-j of the
+      // padded allocation of the rank at +d_j, through its IPC mapping
+      std::vector<uint8_t *> peer_alloc;
+      rt_exchange_ptr(alloc, peer_alloc);
+      std::vector<CopySpec> copies;
+      for (int j = 0; j < 26; ++j) {
+        const int64_t to = halo_rank_of(c, p->rank, regions[j].dir);
+        copies.push_back({sct[j].get(), alloc, static_cast<uint64_t>(pad), 1, rct[25 - j].get(), peer_alloc[to],
+                          static_cast<uint64_t>(pad), 1});
+      }
+      p->pack = copy_batch_create(copies);
+    } else {
     cuda_check(cudaMalloc(&p->recv, static_cast<size_t>(p->seg_total)), "cudaMalloc(halo recv)");
     if (method == SP_HALO_COPY) cuda_check(cudaMalloc(&p->send, static_cast<size_t>(p->seg_total)), "cudaMalloc");
     std::vector<uint8_t *> peer_recv;
     rt_exchange_ptr(p->recv, peer_recv);
     if (method == SP_HALO_COPY) rt_exchange_ptr(p->send, p->peer_send);
-    std::vector<BatchSpec> packs, unpacks;
     for (int j = 0; j < 26; ++j) {
       if (method != SP_HALO_COPY) {
         // segment j of this rank is segment 25-j of the rank at +d_j,
@@ -222,8 +236,9 @@ sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int metho
     }
     p->pack = batch_create(packs, false);
     p->unpack = batch_create(unpacks, true);
+    }
     for (auto &e : p->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
-    if (method == SP_HALO_FUSED_ASYNC) {
+    if (method == SP_HALO_FUSED_ASYNC || method == SP_HALO_DIRECT) {
       const int n = rt_size();
       cuda_check(cudaMalloc(&p->flags, 2 * n * sizeof(uint64_t)), "cudaMalloc(flags)");
       cuda_check(cudaMemset(p->flags, 0, 2 * n * sizeof(uint64_t)), "cudaMemset(flags)");
@@ -263,7 +278,43 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
   return guarded([&] {
     need(p);
     cudaStream_t s = static_cast<cudaStream_t>(rt_stream());
-    if (p->method == SP_HALO_FUSED_ASYNC) {
+    if (p->method == SP_HALO_DIRECT) {
+      // one copy launch per iteration: block 0 first tells this rank's
+      // senders that the ghosts of iteration n-1 are consumed (FREE=n-1;
+      // everything earlier on the stream has completed), every block waits
+      // for FREE=n-1 from its receivers, the regions are stored into the
+      // receivers' ghost cells over NVLink, and the last block publishes
+      // READY=n to each receiver; a one-warp kernel then waits for READY=n
+      // from this rank's senders, so later work on the stream sees whole
+      // ghost shells.
+      const int n = rt_size(), me = p->rank;
+      const uint64_t it = ++p->iter;
+      auto at = [&](uint8_t *base, int kind, int peer) {
+        return reinterpret_cast<uint64_t *>(base + static_cast<size_t>(kind * n + peer) * sizeof(uint64_t));
+      };
+      uint8_t *mine = reinterpret_cast<uint8_t *>(p->flags);
+      BatchSignal ks;
+      std::vector<const uint64_t *> ready;
+      for (int q : p->in_peers) {
+        ks.pre.push_back(at(p->peer_flags[q], kFree, me));
+        ready.push_back(at(mine, kReady, q));
+      }
+      ks.pre_value = it - 1;
+      for (int q : p->out_peers) {
+        ks.wait.push_back(at(mine, kFree, q));
+        ks.signal.push_back(at(p->peer_flags[q], kReady, me));
+      }
+      ks.wait_value = it - 1;
+      ks.signal_value = it;
+      ks.done = p->done;
+      ks.sys_scope = p->remote_peers;
+      cuda_check(cudaEventRecord(p->ev[0], s), "cudaEventRecord");
+      batch_execute_signaled(*p->pack, s, ks);
+      cuda_check(cudaEventRecord(p->ev[1], s), "cudaEventRecord");
+      cuda_check(cudaEventRecord(p->ev[2], s), "cudaEventRecord");
+      flags_wait(ready, it, s);
+      cuda_check(cudaEventRecord(p->ev[3], s), "cudaEventRecord");
+    } else if (p->method == SP_HALO_FUSED_ASYNC) {
       // device-ordered iteration, signalled from inside the kernels: the
       // pack batch waits (in every block) until each receiver has consumed
       // iteration n-1, stores the segments into the receivers' HBM, and its

@@ -105,6 +105,12 @@ using CommitPtr = std::shared_ptr<const Committed>;
 // translate + simplify + lower + plan + exact overlap (commit.hpp:51-79)
 CommitPtr commit_def(const TypeDef &def);
 
+// the definition's normalized run list (block_list.hpp:44-61 over :67-121)
+std::vector<Run> flatten_def(const TypeDef &def, bool &overlap);
+
+// type-file front end (typefile.hpp:17-260); name = the committed name
+DefPtr parse_type_file(const std::string &text, std::string &name);
+
 // exposed for tests via the C-ABI: exact injectivity of a strided block
 bool strided_overlaps(const StridedBlock &sb);
 
@@ -160,6 +166,19 @@ struct BatchSpec {
 };
 struct Batch;
 Batch *batch_create(const std::vector<BatchSpec> &specs, bool unpack);
+// typed copies: byte k of (sct, scount) at src lands on byte k of
+// (dct, dcount) at dst; scount*sct.size must equal dcount*dct.size
+struct CopySpec {
+  const Committed *sct;
+  const void *src;
+  uint64_t src_bytes;
+  int64_t scount;
+  const Committed *dct;
+  void *dst;
+  uint64_t dst_bytes;
+  int64_t dcount;
+};
+Batch *copy_batch_create(const std::vector<CopySpec> &specs);
 void batch_execute(const Batch &b, void *stream);
 void batch_destroy(Batch *b);
 // in-kernel completion protocol for distributed exchanges (pack.cu)
@@ -170,7 +189,11 @@ struct BatchSignal {
   uint64_t signal_value = 0;
   unsigned *done = nullptr;           // device counter, zero-initialised, one per stream
   bool sys_scope = true;              // a destination is on another GPU
+  std::vector<uint64_t *> pre;        // (peer) flags set to pre_value BEFORE the wait
+  uint64_t pre_value = 0;
 };
+// one-warp kernel: waits until every flag reaches value (acquire, system scope)
+void flags_wait(const std::vector<const uint64_t *> &wait, uint64_t value, void *stream);
 void batch_execute_signaled(const Batch &b, void *stream, const BatchSignal &sig);
 int64_t batch_bytes(const Batch &b);
 

@@ -200,6 +200,9 @@ int64_t halo_verify(const HaloCfg &c, int64_t rank, const void *alloc, void *str
 // Every rank of the grid lives on the current device (the reference's
 // run_exchange, halo.hpp:172-322, simulates them in host memory).
 HaloReport halo_run(const HaloCfg &c, const Profile *prof, int method, int iters) {
+  if (method != SP_HALO_FUSED && method != SP_HALO_COPY && method != SP_HALO_DIRECT)
+    fail(SP_ERR_INVALID_ARGUMENT, "halo: unknown method for a one-process exchange");
+  halo_validate(c); // configuration errors first, as run_exchange does (halo.hpp:172-175)
   require_device();
   auto regions = halo_regions(c);
   const int64_t nranks = c.ranks[0] * c.ranks[1] * c.ranks[2];
@@ -239,7 +242,21 @@ HaloReport halo_run(const HaloCfg &c, const Profile *prof, int method, int iters
                          static_cast<uint64_t>(pad), seg_off[j]});
     }
   }
-  std::unique_ptr<Batch, void (*)(Batch *)> pb(batch_create(packs, false), batch_destroy);
+  // DIRECT: rank s copies its region j straight into region 25-j of the
+  // receiver's padded allocation (the ghost cells), no packed segment
+  std::vector<CopySpec> copies;
+  if (method == SP_HALO_DIRECT) {
+    packs.clear();
+    unpacks.clear();
+    for (int64_t rk = 0; rk < nranks; ++rk)
+      for (size_t j = 0; j < 26; ++j) {
+        const int64_t to = halo_rank_of(c, rk, regions[j].dir);
+        copies.push_back({send_ct[j].get(), alloc[rk], static_cast<uint64_t>(pad), 1, recv_ct[25 - j].get(), alloc[to],
+                          static_cast<uint64_t>(pad), 1});
+      }
+  }
+  std::unique_ptr<Batch, void (*)(Batch *)> pb(
+      method == SP_HALO_DIRECT ? copy_batch_create(copies) : batch_create(packs, false), batch_destroy);
   std::unique_ptr<Batch, void (*)(Batch *)> ub(batch_create(unpacks, true), batch_destroy);
   cudaEvent_t ev[4];
   for (auto &e : ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
@@ -259,7 +276,7 @@ HaloReport halo_run(const HaloCfg &c, const Profile *prof, int method, int iters
         }
     }
     cuda_check(cudaEventRecord(ev[2], s), "cudaEventRecord");
-    batch_execute(*ub, s);
+    if (method != SP_HALO_DIRECT) batch_execute(*ub, s);
     cuda_check(cudaEventRecord(ev[3], s), "cudaEventRecord");
     cuda_check(cudaEventSynchronize(ev[3]), "cudaEventSynchronize");
     float a, b, d;

@@ -863,28 +863,40 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
 } // namespace
 
 // ============================================================ batches
-// A persistent list of (type, buffers) jobs executed by ONE launch: every
-// 1024-word chunk of every job is a unit of work, blocks walk the chunks
-// grid-stride and look their job up by binary search, so small regions
-// (halo corners, edges) share the grid with large ones (faces) instead of
-// costing a launch each. Destinations may be peer-GPU memory mapped over
-// NVLink (CUDA IPC), which turns the batch into a fused pack-to-peer.
-constexpr uint32_t kBatchChunk = 256 * 2; // words per chunk: two per thread
+// A persistent list of jobs executed by ONE launch per word size. A job is
+//   PACK   (type, count, strided src) -> packed dst
+//   UNPACK packed src -> (type, count, strided dst)
+//   COPY   (type S, count, strided src) -> (type D, count', strided dst),
+//          byte k of S's pack order lands on byte k of D's: a typed copy
+//          with no packed intermediate (halo ghost writes, alltoallw).
+// Destinations may be peer-GPU memory mapped over NVLink (CUDA IPC), which
+// turns the batch into a fused pack-to-peer / copy-to-peer.
+//
+// Work distribution: the words of all jobs form one index space, split into
+// equal contiguous ranges, one per CTA of a single resident wave (grid =
+// SMs x resident CTAs per SM). Each thread moves U words per round with all
+// U loads issued before the first store, so a CTA's whole range is usually
+// one or two DRAM round trips and no CTA waits on a straggler chunk. Within
+// a round a thread finds its job by walking forward from the CTA's first
+// job (ranges rarely cross a job boundary); the job descriptors are read
+// through the read-only path and stay L1-resident.
+constexpr int kBatchU = 4;
+enum : int { kModeUnpack = 0, kModePack = 1, kModeCopy = 2 };
 
 struct BatchJob {
-  Geom g;
-  const uint8_t *in;
-  uint8_t *out;
-  int w;
-  int pack;
+  Geom gs;           // strided-side geometry of the source (PACK, COPY)
+  Geom gd;           // strided-side geometry of the destination (UNPACK, COPY)
+  const uint8_t *in; // source base (strided sources already at start)
+  uint8_t *out;      // destination base
+  uint64_t begin;    // first word of this job in the launch's index space
+  int same;          // COPY with gd == gs: destination offset = source offset
 };
 
-// one launch per (word size, direction) group; all jobs of a group share W
 // Optional in-kernel completion protocol (distributed halo): every block
 // first waits until each `wait` flag (local memory, written by peers over
-// NVLink) reaches wait_value; after the last chunk, the LAST block to finish
+// NVLink) reaches wait_value; after the last word, the LAST block to finish
 // publishes signal_value to each `signal` flag (peer memory) with a
-// system-scope release store, after system-scope fences by every thread.
+// system-scope release store, after fences by every block.
 constexpr int kMaxSig = 32;
 struct BatchSig {
   const unsigned long long *wait[kMaxSig];
@@ -893,6 +905,11 @@ struct BatchSig {
   unsigned *done; // block-completion counter of this launch (device memory)
   int n_wait, n_signal;
   int sys_scope;  // some destination lives on another GPU: system-scope fences
+  // published by block 0 BEFORE waiting (consumer-side "ready" flags: the
+  // stream order guarantees everything before this launch has completed)
+  unsigned long long *pre[kMaxSig];
+  unsigned long long pre_value;
+  int n_pre;
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
@@ -905,69 +922,77 @@ __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned l
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-template <int W, bool PACK>
-__global__ void __launch_bounds__(256) k_batch(const BatchJob *__restrict__ jobs,
-                                               const uint32_t *__restrict__ chunk0, int njobs, uint32_t nchunks,
-                                               const BatchSig sig) {
+// byte offset of word q on a strided side
+template <int W> __device__ __forceinline__ int64_t word_offset(uint32_t q, const Geom &g) {
+  const uint32_t row = fdiv(q, g.wdiv);
+  return row_offset(row, g) + static_cast<int64_t>(q - row * g.wpr) * W;
+}
+
+template <int W, int MODE>
+__global__ void __launch_bounds__(256) k_batch(const BatchJob *__restrict__ jobs, int njobs, uint32_t total,
+                                               uint32_t per_block, const BatchSig sig) {
   using T = typename Word<W>::T;
-  __shared__ BatchJob sj;
-  int loaded = -1;
+  if (sig.n_pre && blockIdx.x == 0 && threadIdx.x < static_cast<unsigned>(sig.n_pre))
+    st_release_sys(sig.pre[threadIdx.x], sig.pre_value);
   if (sig.n_wait) {
     if (threadIdx.x < static_cast<unsigned>(sig.n_wait))
-      while (ld_acquire_sys(sig.wait[threadIdx.x]) < sig.wait_value) __nanosleep(100);
+      while (ld_acquire_sys(sig.wait[threadIdx.x]) < sig.wait_value) __nanosleep(64);
     __syncthreads();
   }
-  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    int lo = 0, hi = njobs - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (chunk0[mid] <= c) {
-        lo = mid;
+  const uint32_t lo = blockIdx.x * per_block;
+  const uint32_t hi = min(total, lo + per_block);
+  // first job of this block's range: last job with begin <= lo
+  int j0 = 0;
+  {
+    int a = 0, b = njobs - 1;
+    while (a < b) {
+      const int m = (a + b + 1) >> 1;
+      if (jobs[m].begin <= lo) {
+        a = m;
       } else {
-        hi = mid - 1;
+        b = m - 1;
       }
     }
-    if (lo != loaded) {
-      __syncthreads();
-      const uint32_t *src = reinterpret_cast<const uint32_t *>(jobs + lo);
-      uint32_t *dst = reinterpret_cast<uint32_t *>(&sj);
-      for (uint32_t i = threadIdx.x; i < sizeof(BatchJob) / 4; i += blockDim.x) dst[i] = src[i];
-      __syncthreads();
-      loaded = lo;
-    }
-    const uint32_t total = static_cast<uint32_t>(sj.g.total);
-    const uint32_t base = (c - chunk0[lo]) * kBatchChunk + threadIdx.x;
-    T v[2];
-    int64_t soff[2];
+    j0 = a;
+  }
+  for (uint32_t base = lo + threadIdx.x; base < hi; base += 256 * kBatchU) {
+    T v[kBatchU];
+    int64_t doff[kBatchU];
+    int jw[kBatchU];
+    int j = j0;
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < kBatchU; ++u) {
       const uint32_t q = base + u * 256;
-      if (q < total) {
-        const uint32_t row = fdiv(q, sj.g.wdiv);
-        soff[u] = row_offset(row, sj.g) + static_cast<int64_t>(q - row * sj.g.wpr) * W;
-        v[u] = PACK ? ld_stream(reinterpret_cast<const T *>(sj.in + soff[u]))
-                    : ld_stream(reinterpret_cast<const T *>(sj.in) + q);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const uint32_t q = base + u * 256;
-      if (q < total) {
-        if (PACK) {
-          st_stream(reinterpret_cast<T *>(sj.out) + q, v[u]);
+      jw[u] = -1;
+      if (q < hi) {
+        while (j + 1 < njobs && jobs[j + 1].begin <= q) ++j;
+        const BatchJob &J = jobs[j];
+        const uint32_t ql = q - static_cast<uint32_t>(J.begin);
+        jw[u] = j;
+        if (MODE == kModeUnpack) {
+          v[u] = ld_stream(reinterpret_cast<const T *>(J.in) + ql);
+          doff[u] = word_offset<W>(ql, J.gd);
         } else {
-          st_stream(reinterpret_cast<T *>(sj.out + soff[u]), v[u]);
+          const int64_t so = word_offset<W>(ql, J.gs);
+          v[u] = ld_stream(reinterpret_cast<const T *>(J.in + so));
+          if (MODE == kModePack) {
+            doff[u] = static_cast<int64_t>(ql) * W;
+          } else {
+            doff[u] = J.same ? so : word_offset<W>(ql, J.gd);
+          }
         }
       }
     }
+#pragma unroll
+    for (int u = 0; u < kBatchU; ++u)
+      if (jw[u] >= 0) st_stream(reinterpret_cast<T *>(jobs[jw[u]].out + doff[u]), v[u]);
   }
   if (sig.n_signal) {
     // bar.sync orders every thread's stores before thread 0 (CTA scope);
-    // thread 0's system-scope fence is cumulative over them
+    // thread 0's fence is cumulative over them: GPU scope when every
+    // destination is on this device, system scope when some were written
+    // over NVLink into a peer GPU
     __syncthreads();
-    // every block releases its stores before counting itself done: at GPU
-    // scope when all destinations are on this device, at system scope when
-    // some were written over NVLink into a peer GPU
     if (threadIdx.x == 0) {
       if (sig.sys_scope) {
         __threadfence_system();
@@ -984,59 +1009,85 @@ __global__ void __launch_bounds__(256) k_batch(const BatchJob *__restrict__ jobs
 }
 
 struct BatchGroup {
-  int w = 0, pack = 0;
+  int w = 0, mode = 0;
   BatchJob *d_jobs = nullptr;
-  uint32_t *d_chunk0 = nullptr;
   int njobs = 0;
-  uint32_t nchunks = 0;
+  uint32_t total = 0; // words
 };
 
 struct Batch {
   int device = -1;
   std::vector<BatchGroup> groups;
-  int64_t bytes = 0; // packed bytes moved per execution
+  int64_t bytes = 0; // payload bytes moved per execution
   ~Batch() {
-    for (auto &g : groups) {
-      cudaFree(g.d_jobs);
-      cudaFree(g.d_chunk0);
-    }
+    for (auto &g : groups) cudaFree(g.d_jobs);
   }
 };
 
 namespace {
 
-// word-kernel job for one (type, count, buffers): row geometry + the
-// alignment-derived word, on device-accessible pointers
-BatchJob plan_job(const Committed &ct, int64_t count, const uint8_t *strided, const uint8_t *packed, bool pack) {
-  if (ct.form != SP_FORM_STRIDED) fail(SP_ERR_UNSUPPORTED, "batch: only strided forms can be batched");
-  const RowDims rd = row_dims(ct, count);
+Geom batch_geom(const RowDims &rd, int w) {
   if (static_cast<int>(rd.cnt.size()) > KMAX) fail(SP_ERR_UNSUPPORTED, "batch: too many row dimensions");
-  uint64_t g_or = static_cast<uint64_t>(rd.c0) | (reinterpret_cast<uint64_t>(strided) + ct.sb.start) |
-                  reinterpret_cast<uint64_t>(packed);
-  for (int64_t st : rd.str) g_or |= static_cast<uint64_t>(st);
-  const int w = pow2_align(g_or);
   uint64_t rows = 1;
   for (int64_t c : rd.cnt) rows *= static_cast<uint64_t>(c);
   const uint64_t words = rows * static_cast<uint64_t>(rd.c0) / static_cast<uint64_t>(w);
   if (words >= (1ull << 32) || rows >= (1ull << 32) || rd.c0 / w >= (int64_t{1} << 32))
     fail(SP_ERR_UNSUPPORTED, "batch: job larger than 2^32 words");
-  BatchJob j{};
-  j.g.nd = static_cast<int>(rd.cnt.size());
-  for (int k = 0; k < j.g.nd; ++k) {
-    j.g.cnt[k] = static_cast<uint32_t>(rd.cnt[k]);
-    j.g.div[k] = make_fastdiv(j.g.cnt[k]);
-    j.g.str[k] = rd.str[k];
-    j.g.back[k] = rd.cnt[k] * rd.str[k];
+  Geom g{};
+  g.nd = static_cast<int>(rd.cnt.size());
+  for (int k = 0; k < g.nd; ++k) {
+    g.cnt[k] = static_cast<uint32_t>(rd.cnt[k]);
+    g.div[k] = make_fastdiv(g.cnt[k]);
+    g.str[k] = rd.str[k];
+    g.back[k] = rd.cnt[k] * rd.str[k];
   }
-  j.g.wpr = static_cast<uint32_t>(rd.c0 / w);
-  j.g.wdiv = make_fastdiv(j.g.wpr);
-  j.g.total = words;
-  j.g.rows = rows;
-  j.w = w;
-  j.pack = pack;
-  j.in = pack ? strided + ct.sb.start : packed;
-  j.out = pack ? const_cast<uint8_t *>(packed) : const_cast<uint8_t *>(strided) + ct.sb.start;
-  return j;
+  g.wpr = static_cast<uint32_t>(rd.c0 / w);
+  g.wdiv = make_fastdiv(g.wpr);
+  g.total = words;
+  g.rows = rows;
+  return g;
+}
+
+uint64_t align_bits(const RowDims &rd, uint64_t base) {
+  uint64_t g_or = static_cast<uint64_t>(rd.c0) | base;
+  for (int64_t st : rd.str) g_or |= static_cast<uint64_t>(st);
+  return g_or;
+}
+
+bool same_geom(const RowDims &a, const RowDims &b) { return a.c0 == b.c0 && a.cnt == b.cnt && a.str == b.str; }
+
+// device-accessible address of a batch buffer (device, pinned or peer-mapped)
+const uint8_t *batch_ptr(const void *p) {
+  const Resolved r = resolve(p);
+  if (r.kind == MemKind::Pageable)
+    fail(SP_ERR_INVALID_ARGUMENT, "batch: buffers must be device, pinned or peer-mapped memory");
+  return r.dptr;
+}
+
+Batch *build_batch(std::vector<BatchJob> (&by_w)[5], int mode, int64_t bytes) {
+  auto b = std::make_unique<Batch>();
+  cuda_check(cudaGetDevice(&b->device), "cudaGetDevice");
+  b->bytes = bytes;
+  for (int wi = 4; wi >= 0; --wi) {
+    auto &jobs = by_w[wi];
+    if (jobs.empty()) continue;
+    BatchGroup g;
+    g.w = 1 << wi;
+    g.mode = mode;
+    uint64_t words = 0;
+    for (BatchJob &j : jobs) {
+      j.begin = words;
+      words += mode == kModeUnpack ? j.gd.total : j.gs.total;
+      if (words >= (1ull << 32)) fail(SP_ERR_UNSUPPORTED, "batch: too much work for one launch");
+    }
+    g.njobs = static_cast<int>(jobs.size());
+    g.total = static_cast<uint32_t>(words);
+    cuda_check(cudaMalloc(&g.d_jobs, jobs.size() * sizeof(BatchJob)), "cudaMalloc(batch)");
+    b->groups.push_back(g);
+    cuda_check(cudaMemcpy(g.d_jobs, jobs.data(), jobs.size() * sizeof(BatchJob), cudaMemcpyHostToDevice),
+               "upload batch");
+  }
+  return b.release();
 }
 
 } // namespace
@@ -1055,56 +1106,99 @@ Batch *batch_create(const std::vector<BatchSpec> &specs, bool unpack) {
     if (ct.form == SP_FORM_EMPTY) continue;
     const uint64_t strided_need = static_cast<uint64_t>((s.count - 1) * ct.extent + ct.span);
     if (strided_need > (unpack ? s.dst_bytes : s.src_bytes)) fail(SP_ERR_BUFFER_TOO_SMALL, "batch: strided buffer too small");
-    const void *strided = unpack ? s.dst : s.src;
-    const void *packed = unpack ? s.src : s.dst;
-    const Resolved rs = resolve(strided), rp = resolve(packed);
-    if (rs.kind == MemKind::Pageable || rp.kind == MemKind::Pageable)
-      fail(SP_ERR_INVALID_ARGUMENT, "batch: buffers must be device, pinned or peer-mapped memory");
-    BatchJob j = plan_job(ct, s.count, rs.dptr, rp.dptr + s.position, !unpack);
-    by_w[__builtin_ctz(static_cast<unsigned>(j.w))].push_back(j);
+    if (ct.form != SP_FORM_STRIDED) fail(SP_ERR_UNSUPPORTED, "batch: only strided forms can be batched");
+    const uint8_t *strided = batch_ptr(unpack ? s.dst : s.src) + ct.sb.start;
+    const uint8_t *packed = batch_ptr(unpack ? s.src : s.dst) + s.position;
+    const RowDims rd = row_dims(ct, s.count);
+    const int w = pow2_align(align_bits(rd, reinterpret_cast<uint64_t>(strided)) | reinterpret_cast<uint64_t>(packed));
+    BatchJob j{};
+    const Geom g = batch_geom(rd, w);
+    if (unpack) {
+      j.gd = g;
+    } else {
+      j.gs = g;
+    }
+    j.in = unpack ? packed : strided;
+    j.out = const_cast<uint8_t *>(unpack ? strided : packed);
+    by_w[__builtin_ctz(static_cast<unsigned>(w))].push_back(j);
     bytes += s.count * ct.size;
   }
-  auto b = std::make_unique<Batch>();
-  cuda_check(cudaGetDevice(&b->device), "cudaGetDevice");
-  b->bytes = bytes;
-  for (int wi = 4; wi >= 0; --wi) {
-    const auto &jobs = by_w[wi];
-    if (jobs.empty()) continue;
-    BatchGroup g;
-    g.w = 1 << wi;
-    g.pack = !unpack;
-    std::vector<uint32_t> chunk0;
-    uint64_t chunks = 0;
-    for (const BatchJob &j : jobs) {
-      chunk0.push_back(static_cast<uint32_t>(chunks));
-      chunks += (j.g.total + kBatchChunk - 1) / kBatchChunk;
-      if (chunks >= (1ull << 32)) fail(SP_ERR_UNSUPPORTED, "batch: too much work for one launch");
-    }
-    g.njobs = static_cast<int>(jobs.size());
-    g.nchunks = static_cast<uint32_t>(chunks);
-    b->groups.push_back(g);
-    BatchGroup &G = b->groups.back();
-    cuda_check(cudaMalloc(&G.d_jobs, jobs.size() * sizeof(BatchJob)), "cudaMalloc(batch)");
-    cuda_check(cudaMalloc(&G.d_chunk0, chunk0.size() * sizeof(uint32_t)), "cudaMalloc(batch)");
-    cuda_check(cudaMemcpy(G.d_jobs, jobs.data(), jobs.size() * sizeof(BatchJob), cudaMemcpyHostToDevice),
-               "upload batch");
-    cuda_check(cudaMemcpy(G.d_chunk0, chunk0.data(), chunk0.size() * sizeof(uint32_t), cudaMemcpyHostToDevice),
-               "upload batch");
+  return build_batch(by_w, unpack ? kModeUnpack : kModePack, bytes);
+}
+
+Batch *copy_batch_create(const std::vector<CopySpec> &specs) {
+  require_device();
+  std::vector<BatchJob> by_w[5];
+  int64_t bytes = 0;
+  for (const CopySpec &s : specs) {
+    const Committed &sc = *s.sct, &dc = *s.dct;
+    if (s.scount < 0 || s.dcount < 0) fail(SP_ERR_INVALID_ARGUMENT, "copy: counts must be >= 0");
+    if (s.scount * sc.size != s.dcount * dc.size)
+      fail(SP_ERR_INVALID_ARGUMENT, "copy: source and destination describe different byte counts");
+    if (dc.overlapping) fail(SP_ERR_OVERLAPPING_LAYOUT, "copy: destination layout describes overlapping bytes");
+    if (s.scount * sc.size == 0) continue;
+    if (static_cast<uint64_t>((s.scount - 1) * sc.extent + sc.span) > s.src_bytes)
+      fail(SP_ERR_BUFFER_TOO_SMALL, "copy: source too small");
+    if (static_cast<uint64_t>((s.dcount - 1) * dc.extent + dc.span) > s.dst_bytes)
+      fail(SP_ERR_BUFFER_TOO_SMALL, "copy: destination too small");
+    if (sc.form != SP_FORM_STRIDED || dc.form != SP_FORM_STRIDED)
+      fail(SP_ERR_UNSUPPORTED, "copy: only strided forms can be batched");
+    const uint8_t *src = batch_ptr(s.src) + sc.sb.start;
+    const uint8_t *dst = batch_ptr(s.dst) + dc.sb.start;
+    const RowDims rs = row_dims(sc, s.scount), rd = row_dims(dc, s.dcount);
+    const int w = pow2_align(align_bits(rs, reinterpret_cast<uint64_t>(src)) |
+                             align_bits(rd, reinterpret_cast<uint64_t>(dst)));
+    BatchJob j{};
+    j.gs = batch_geom(rs, w);
+    j.gd = batch_geom(rd, w);
+    j.same = same_geom(rs, rd) ? 1 : 0;
+    j.in = src;
+    j.out = const_cast<uint8_t *>(dst);
+    by_w[__builtin_ctz(static_cast<unsigned>(w))].push_back(j);
+    bytes += s.scount * sc.size;
   }
-  return b.release();
+  return build_batch(by_w, kModeCopy, bytes);
 }
 
 namespace {
+
+template <int W, int MODE> void launch_batch(const BatchGroup &g, const BatchSig &sig, cudaStream_t s, unsigned &grid) {
+  static thread_local int occ_dev = -1, occ = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (occ_dev != dev) {
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_batch<W, MODE>, 256, 0), "occupancy");
+    occ = std::max(occ, 1);
+    occ_dev = dev;
+  }
+  const uint64_t want = (static_cast<uint64_t>(g.total) + 256ull * kBatchU - 1) / (256ull * kBatchU);
+  grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sm_count()) * occ)));
+  const uint32_t per = static_cast<uint32_t>((static_cast<uint64_t>(g.total) + grid - 1) / grid);
+  k_batch<W, MODE><<<grid, 256, 0, s>>>(g.d_jobs, g.njobs, g.total, per, sig);
+}
+
+template <int W> void launch_batch_w(const BatchGroup &g, const BatchSig &sig, cudaStream_t s, unsigned &grid) {
+  switch (g.mode) {
+  case kModePack: launch_batch<W, kModePack>(g, sig, s, grid); break;
+  case kModeUnpack: launch_batch<W, kModeUnpack>(g, sig, s, grid); break;
+  default: launch_batch<W, kModeCopy>(g, sig, s, grid); break;
+  }
+}
+
 void batch_launch(const Batch &b, void *stream, const BatchSignal *bs) {
   sp_launch_info li{};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (size_t gi = 0; gi < b.groups.size(); ++gi) {
     const BatchGroup &g = b.groups[gi];
     BatchSig sig{};
-    if (bs) { // wait in the first kernel, signal from the last
-      if (bs->wait.size() > static_cast<size_t>(kMaxSig) || bs->signal.size() > static_cast<size_t>(kMaxSig))
+    if (bs) { // pre-signal and wait in the first kernel, signal from the last
+      if (bs->wait.size() > static_cast<size_t>(kMaxSig) || bs->signal.size() > static_cast<size_t>(kMaxSig) ||
+          bs->pre.size() > static_cast<size_t>(kMaxSig))
         fail(SP_ERR_UNSUPPORTED, "batch signalling: more than 32 peers");
       if (gi == 0) {
+        sig.n_pre = static_cast<int>(bs->pre.size());
+        for (int i = 0; i < sig.n_pre; ++i) sig.pre[i] = reinterpret_cast<unsigned long long *>(bs->pre[i]);
+        sig.pre_value = bs->pre_value;
         sig.n_wait = static_cast<int>(bs->wait.size());
         for (int i = 0; i < sig.n_wait; ++i) sig.wait[i] = reinterpret_cast<const unsigned long long *>(bs->wait[i]);
         sig.wait_value = bs->wait_value;
@@ -1117,18 +1211,13 @@ void batch_launch(const Batch &b, void *stream, const BatchSignal *bs) {
         sig.sys_scope = bs->sys_scope ? 1 : 0;
       }
     }
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(g.nchunks, static_cast<uint64_t>(sm_count()) * 8));
-    switch (g.w * 2 + g.pack) {
-    case 33: k_batch<16, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
-    case 32: k_batch<16, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
-    case 17: k_batch<8, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
-    case 16: k_batch<8, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
-    case 9: k_batch<4, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
-    case 8: k_batch<4, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
-    case 5: k_batch<2, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
-    case 4: k_batch<2, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
-    case 3: k_batch<1, true><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
-    default: k_batch<1, false><<<grid, 256, 0, s>>>(g.d_jobs, g.d_chunk0, g.njobs, g.nchunks, sig); break;
+    unsigned grid = 0;
+    switch (g.w) {
+    case 16: launch_batch_w<16>(g, sig, s, grid); break;
+    case 8: launch_batch_w<8>(g, sig, s, grid); break;
+    case 4: launch_batch_w<4>(g, sig, s, grid); break;
+    case 2: launch_batch_w<2>(g, sig, s, grid); break;
+    default: launch_batch_w<1>(g, sig, s, grid); break;
     }
     cuda_check(cudaGetLastError(), "k_batch launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -1141,6 +1230,24 @@ void batch_launch(const Batch &b, void *stream, const BatchSignal *bs) {
 }
 } // namespace
 
+// one warp: lane i spins until wait[i] >= value (acquire, system scope)
+__global__ void k_flag_wait(const BatchSig sig) {
+  if (threadIdx.x < static_cast<unsigned>(sig.n_wait))
+    while (ld_acquire_sys(sig.wait[threadIdx.x]) < sig.wait_value) __nanosleep(64);
+}
+
+void flags_wait(const std::vector<const uint64_t *> &wait, uint64_t value, void *stream) {
+  if (wait.empty()) return;
+  if (wait.size() > static_cast<size_t>(kMaxSig)) fail(SP_ERR_UNSUPPORTED, "flag wait: more than 32 peers");
+  BatchSig sig{};
+  sig.n_wait = static_cast<int>(wait.size());
+  for (int i = 0; i < sig.n_wait; ++i) sig.wait[i] = reinterpret_cast<const unsigned long long *>(wait[i]);
+  sig.wait_value = value;
+  k_flag_wait<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(sig);
+  cuda_check(cudaGetLastError(), "k_flag_wait launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
 void batch_execute(const Batch &b, void *stream) { batch_launch(b, stream, nullptr); }
 
 void batch_execute_signaled(const Batch &b, void *stream, const BatchSignal &sig) {
@@ -1152,33 +1259,36 @@ void batch_destroy(Batch *b) { delete b; }
 
 int64_t batch_bytes(const Batch &b) { return b.bytes; }
 
+// check_user_buffer (pack.hpp:85-91), same message
+static void need_bytes(uint64_t have, int64_t need, const char *what) {
+  if (static_cast<uint64_t>(need) > have)
+    fail(SP_ERR_BUFFER_TOO_SMALL, std::string(what) + ": need " + std::to_string(need) + " bytes, have " +
+                                      std::to_string(have));
+}
+
 // Validation order follows pack.hpp:102-126 / :146-159 exactly.
 int64_t execute(const PackArgs &a) {
   const Committed &ct = *a.ct;
   sp_launch_info li{};
   if (a.pack) {
     if (a.count < 1 || a.position < 0) fail(SP_ERR_INVALID_ARGUMENT, "pack: incount must be positive, position >= 0");
-    if (static_cast<uint64_t>(a.position + a.count * ct.size) > a.dst_bytes)
-      fail(SP_ERR_BUFFER_TOO_SMALL, "pack: destination too small");
+    need_bytes(a.dst_bytes, a.position + a.count * ct.size, "pack: destination");
     if (ct.form == SP_FORM_EMPTY) {
       set_last_launch(li);
       return a.position;
     }
-    if (static_cast<uint64_t>((a.count - 1) * ct.extent + ct.span) > a.src_bytes)
-      fail(SP_ERR_BUFFER_TOO_SMALL, "pack: source too small");
+    need_bytes(a.src_bytes, (a.count - 1) * ct.extent + ct.span, "pack: source");
     if (ct.form == SP_FORM_UNSUPPORTED && !a.opt.allow_fallback)
       fail(SP_ERR_UNSUPPORTED, "pack: type has no strided form");
   } else {
     if (a.count < 1 || a.position < 0) fail(SP_ERR_INVALID_ARGUMENT, "unpack: outcount must be positive, position >= 0");
     if (ct.overlapping) fail(SP_ERR_OVERLAPPING_LAYOUT, "unpack: layout describes overlapping bytes");
-    if (static_cast<uint64_t>(a.position + a.count * ct.size) > a.src_bytes)
-      fail(SP_ERR_BUFFER_TOO_SMALL, "unpack: source too small");
+    need_bytes(a.src_bytes, a.position + a.count * ct.size, "unpack: source");
     if (ct.form == SP_FORM_EMPTY) {
       set_last_launch(li);
       return a.position;
     }
-    if (static_cast<uint64_t>((a.count - 1) * ct.extent + ct.span) > a.dst_bytes)
-      fail(SP_ERR_BUFFER_TOO_SMALL, "unpack: destination too small");
+    need_bytes(a.dst_bytes, (a.count - 1) * ct.extent + ct.span, "unpack: destination");
     if (ct.form == SP_FORM_UNSUPPORTED && !a.opt.allow_fallback)
       fail(SP_ERR_UNSUPPORTED, "unpack: type has no strided form");
   }

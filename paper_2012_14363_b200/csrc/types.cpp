@@ -397,6 +397,26 @@ static std::vector<Run> def_runs(const TypeDef &d) {
   return out;
 }
 
+// normalize_blocks (block_list.hpp:44-61): sorted by (offset, length),
+// abutting or overlapping runs merged; overlap records bytes described twice
+std::vector<Run> flatten_def(const TypeDef &def, bool &overlap) {
+  std::vector<Run> runs = def_runs(def);
+  std::sort(runs.begin(), runs.end(),
+            [](const Run &a, const Run &b) { return a.off != b.off ? a.off < b.off : a.len < b.len; });
+  std::vector<Run> out;
+  overlap = false;
+  for (const Run &r : runs) {
+    if (!out.empty() && r.off <= out.back().off + out.back().len) {
+      Run &cur = out.back();
+      if (r.off < cur.off + cur.len) overlap = true;
+      cur.len = std::max(cur.len, r.off + r.len - cur.off);
+    } else {
+      out.push_back(r);
+    }
+  }
+  return out;
+}
+
 static int64_t leaf_bytes(const TypeDef &d) {
   const TypeDef *p = &d;
   while (p->kind != Kind::Named) p = p->inner.get();

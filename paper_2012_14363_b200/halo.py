@@ -13,7 +13,7 @@ from typing import List, Optional, Sequence
 from . import TypeDef, _buffer, _capi, _check, _stream, commit_type
 from ._capi import lib
 
-FUSED, COPY, FUSED_ASYNC = 0, 1, 2
+FUSED, COPY, FUSED_ASYNC, DIRECT = 0, 1, 2, 3
 
 
 @dataclass
@@ -114,6 +114,24 @@ class Batch:
         h = C.c_void_p()
         _check(lib.sp_batch_create(arr, len(jobs), int(unpack), C.byref(h)))
         self.handle = h.value
+
+    @classmethod
+    def copies(cls, jobs):
+        """Typed copies in one launch (sp_copy_batch_create): jobs are
+        (src, src_ct, src_count, dst, dst_ct, dst_count); byte k of the
+        source's pack order lands on byte k of the destination's."""
+        self = cls.__new__(cls)
+        arr = (_capi.CopyJob * max(len(jobs), 1))()
+        self._keep = []
+        for i, (src, sct, sn_, dst, dct, dn_) in enumerate(jobs):
+            sa, sn, _ = _buffer(src, False)
+            da, dn, _ = _buffer(dst, True)
+            arr[i] = _capi.CopyJob(sa, sn, sct.handle, sn_, da, dn, dct.handle, dn_)
+            self._keep += [sct, dct]
+        h = C.c_void_p()
+        _check(lib.sp_copy_batch_create(arr, len(jobs), C.byref(h)))
+        self.handle = h.value
+        return self
 
     def __del__(self):
         try:

@@ -127,6 +127,12 @@ def _halo(rank, world, job, ranks, method):
     for _ in range(3):
         t = plan.exchange()
     bad = H.verify(cfg, rank, alloc)
+    # reset the ghosts: a fourth iteration must rewrite all of them
+    H.fill(cfg, rank, alloc)
+    torch.cuda.synchronize()
+    rt.barrier()
+    plan.exchange()
+    bad += H.verify(cfg, rank, alloc)
     plan.free()
     rt.finalize()
     return bad, t
@@ -134,7 +140,8 @@ def _halo(rank, world, job, ranks, method):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("ranks,method", [((2, 1, 1), 0), ((2, 1, 1), 1), ((1, 3, 1), 0), ((1, 1, 1), 2),
-                                          ((2, 1, 1), 2), ((2, 2, 1), 2)])
+                                          ((2, 1, 1), 2), ((2, 2, 1), 2), ((1, 1, 1), 3), ((2, 1, 1), 3),
+                                          ((1, 3, 1), 3), ((2, 2, 1), 3)])
 def test_distributed_halo_exchange(cuda, ranks, method):
     world = ranks[0] * ranks[1] * ranks[2]
     res = _spawn(_halo, world, ranks, method)

@@ -74,12 +74,17 @@ def halo_section(torch, rank, world, local, job, iters=20, warmup=5, nccl=True):
         ph = {k: _reduce(torch, world, statistics.median(t[k] for t in ts), MAX) for k in ts[0]}
         return ph, _reduce(torch, world, float(bad), MAX)
 
+    phase_direct, bad_direct = run(H.DIRECT)  # ghost writes: one typed-copy launch, no packed segments
     phase, bad = run(H.FUSED_ASYNC)      # device-ordered: completion flags, no host barrier
     phase_sync, bad_sync = run(H.FUSED)  # host-barrier variant, for comparison
-    bad = max(bad, bad_sync)
+    bad = max(bad, bad_sync, bad_direct)
     rbytes = remote_bytes(cfg, regions, rank)
     out = {"grid": list(grid), "interior": 256, "radius": 2, "element_bytes": 32,
            "bytes_per_rank": seg[-1], "remote_bytes_per_rank": rbytes, "verified": bad == 0,
+           "direct_us": {"copy": round(phase_direct["pack"] * 1e6, 2),
+                         "wait": round(phase_direct["unpack"] * 1e6, 2),
+                         "iteration": round(phase_direct["iteration"] * 1e6, 2)},
+           "direct_hbm_GBps_per_rank": round(2 * seg[-1] / phase_direct["iteration"] / 1e9, 1),
            "fused_us": {k: round(v * 1e6, 2) for k, v in phase.items()},
            "fused_hostsync_us": {k: round(v * 1e6, 2) for k, v in phase_sync.items()},
            "fused_hbm_GBps_per_rank": round(4 * seg[-1] / phase["iteration"] / 1e9, 1),
