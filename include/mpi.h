@@ -25,6 +25,7 @@ extern "C" {
 
 typedef int MPI_Datatype;
 typedef int MPI_Comm;
+typedef int MPI_Request;
 typedef int64_t MPI_Aint;
 typedef int64_t MPI_Count;
 
@@ -68,6 +69,8 @@ typedef struct {
 #define MPI_PROC_NULL (-2)
 #define MPI_UNDEFINED (-32766)
 #define MPI_STATUS_IGNORE ((MPI_Status *)0)
+#define MPI_STATUSES_IGNORE ((MPI_Status *)0)
+#define MPI_REQUEST_NULL ((MPI_Request)0)
 #define MPI_UNWEIGHTED ((int *)0)
 #define MPI_INFO_NULL 0
 #define MPI_ORDER_C 56
@@ -115,6 +118,19 @@ int MPI_Pack_size(int incount, MPI_Datatype datatype, MPI_Comm comm, int *size);
 int MPI_Send(const void *buf, int count, MPI_Datatype datatype, int dest, int tag, MPI_Comm comm);
 int MPI_Recv(void *buf, int count, MPI_Datatype datatype, int source, int tag, MPI_Comm comm,
              MPI_Status *status);
+/* non-blocking point to point: requests progressed by every MPI call;
+ * messages above two chunks (TEMPI_CHUNK, default 4 MiB) are pipelined
+ * chunk by chunk, device-to-device messages run as one fused copy kernel */
+int MPI_Isend(const void *buf, int count, MPI_Datatype datatype, int dest, int tag, MPI_Comm comm,
+              MPI_Request *request);
+int MPI_Irecv(void *buf, int count, MPI_Datatype datatype, int source, int tag, MPI_Comm comm,
+              MPI_Request *request);
+int MPI_Wait(MPI_Request *request, MPI_Status *status);
+int MPI_Waitall(int count, MPI_Request requests[], MPI_Status statuses[]);
+int MPI_Test(MPI_Request *request, int *flag, MPI_Status *status);
+int MPI_Sendrecv(const void *sendbuf, int sendcount, MPI_Datatype sendtype, int dest, int sendtag, void *recvbuf,
+                 int recvcount, MPI_Datatype recvtype, int source, int recvtag, MPI_Comm comm,
+                 MPI_Status *status);
 
 /* topologies + neighbourhood exchange (accelerated: fused pack-to-peer) */
 int MPI_Dist_graph_create_adjacent(MPI_Comm comm_old, int indegree, const int sources[],
@@ -147,12 +163,19 @@ int PMPI_Unpack(const void *inbuf, int insize, int *position, void *outbuf, int 
 int PMPI_Send(const void *buf, int count, MPI_Datatype datatype, int dest, int tag, MPI_Comm comm);
 int PMPI_Recv(void *buf, int count, MPI_Datatype datatype, int source, int tag, MPI_Comm comm,
               MPI_Status *status);
+int PMPI_Isend(const void *buf, int count, MPI_Datatype datatype, int dest, int tag, MPI_Comm comm,
+               MPI_Request *request);
+int PMPI_Irecv(void *buf, int count, MPI_Datatype datatype, int source, int tag, MPI_Comm comm,
+               MPI_Request *request);
+int PMPI_Wait(MPI_Request *request, MPI_Status *status);
 int PMPI_Neighbor_alltoallv(const void *sendbuf, const int sendcounts[], const int sdispls[],
                             MPI_Datatype sendtype, void *recvbuf, const int recvcounts[], const int rdispls[],
                             MPI_Datatype recvtype, MPI_Comm comm);
 
-/* TEMPI-specific controls (not MPI): force a transfer method for MPI_Send
- * (-1 = model-selected, the default), load a machine profile. */
+/* TEMPI-specific controls (not MPI): force a transfer method for MPI_Send /
+ * MPI_Isend (-1 = model-selected, the default; 0 one-shot, 1 device, 2
+ * staged, 3 direct = fused copy into the receiver's device buffer), load a
+ * machine profile. */
 int TEMPI_Set_method(int method);
 int TEMPI_Load_profile(const char *path);
 

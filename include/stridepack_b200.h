@@ -234,7 +234,10 @@ typedef struct sp_profile_s *sp_profile;
 typedef struct sp_model_cache_s *sp_model_cache;
 enum { SP_CURVE_CPU_CPU = 0, SP_CURVE_GPU_GPU = 1, SP_CURVE_D2H = 2, SP_CURVE_H2D = 3 };
 enum { SP_SURF_GPU_PACK = 0, SP_SURF_GPU_UNPACK = 1, SP_SURF_HOST_PACK = 2, SP_SURF_HOST_UNPACK = 3 };
-enum { SP_METHOD_ONESHOT = 0, SP_METHOD_DEVICE = 1, SP_METHOD_STAGED = 2 }; /* MethodChoice perf_model.hpp:46 */
+enum { SP_METHOD_ONESHOT = 0, SP_METHOD_DEVICE = 1, SP_METHOD_STAGED = 2, /* MethodChoice perf_model.hpp:46 */
+       SP_METHOD_DIRECT = 3 /* runtime only (sp_rt_*): the device path with the
+                               pack, NVLink transfer and unpack fused into one
+                               typed-copy kernel into the receiver's buffer */ };
 
 sp_status sp_profile_create(sp_profile *out);
 /* load_profile           profile_io.hpp:88 (text) / :166 (file) */
@@ -345,15 +348,36 @@ sp_status sp_rt_set_profile(sp_profile p);
 sp_status sp_rt_choose(sp_type t, int64_t count, int *method);
 /* MPI_Send / MPI_Recv of `count` objects of a committed type between two
  * ranks: rendezvous, then DEVICE (pack kernel stores into the receiver's
- * HBM window through IPC), ONESHOT (pack kernel stores into the receiver's
- * pinned host region) or STAGED (device pack, D2H, H2D, unpack); method < 0
- * = model-selected (Eqs. 1-3). source/tag < 0 match any. status = {source,
- * tag, bytes, method}. Blocking; the buffers must be device-accessible. */
+ * HBM window through IPC, the receiver unpacks), ONESHOT (pack kernel
+ * stores into the receiver's pinned host region) or STAGED (device pack,
+ * D2H, H2D, unpack); DIRECT = the device path where the receiver, when its
+ * buffer is device memory, publishes buffer + canonical geometry and the
+ * sender runs one typed-copy kernel into it (falls back to DEVICE
+ * otherwise). method < 0 = model-selected (Eqs. 1-3; a DEVICE choice runs as
+ * DIRECT). Messages above two chunks (sp_rt_set_chunk, default 4 MiB) are
+ * pipelined chunk by chunk. source/tag < 0 match any. status = {source,
+ * tag, bytes, method used}. Blocking; the buffers must be device-accessible
+ * (or pinned / pageable host memory, staged by the engine). */
 sp_status sp_rt_send(const void *buf, uint64_t buf_bytes, int64_t count,
                      sp_type t, int dest, int tag, int method,
                      int *used_method);
 sp_status sp_rt_recv(void *buf, uint64_t buf_bytes, int64_t count, sp_type t,
                      int source, int tag, int64_t status[4]);
+/* MPI_Isend / MPI_Irecv / MPI_Test / MPI_Wait: the same protocol as
+ * non-blocking requests. Every runtime call (and sp_rt_barrier) progresses
+ * all pending requests. sp_rt_test sets *done and, once done, fills status
+ * and frees the request; sp_rt_wait blocks until done. The error of a
+ * failed request (e.g. truncation) is returned by test/wait. */
+typedef uint64_t sp_request;
+sp_status sp_rt_isend(const void *buf, uint64_t buf_bytes, int64_t count,
+                      sp_type t, int dest, int tag, int method,
+                      sp_request *req);
+sp_status sp_rt_irecv(void *buf, uint64_t buf_bytes, int64_t count, sp_type t,
+                      int source, int tag, sp_request *req);
+sp_status sp_rt_test(sp_request req, int *done, int64_t status[4]);
+sp_status sp_rt_wait(sp_request req, int64_t status[4]);
+/* packed bytes per pipelined chunk (multiple of 16; TEMPI_CHUNK env) */
+sp_status sp_rt_set_chunk(int64_t bytes);
 
 /* MPI_Neighbor_alltoallv over a distributed graph (collective over every
  * runtime rank): block i (sendcounts[i] objects of sendtype at

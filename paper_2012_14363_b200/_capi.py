@@ -151,6 +151,11 @@ _sig("sp_rt_set_profile", C.c_int, vp)
 _sig("sp_rt_choose", C.c_int, sp_type, i64, C.POINTER(C.c_int))
 _sig("sp_rt_send", C.c_int, vp, u64, i64, sp_type, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int))
 _sig("sp_rt_recv", C.c_int, vp, u64, i64, sp_type, C.c_int, C.c_int, i64p)
+_sig("sp_rt_isend", C.c_int, vp, u64, i64, sp_type, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint64))
+_sig("sp_rt_irecv", C.c_int, vp, u64, i64, sp_type, C.c_int, C.c_int, C.POINTER(C.c_uint64))
+_sig("sp_rt_test", C.c_int, C.c_uint64, C.POINTER(C.c_int), i64p)
+_sig("sp_rt_wait", C.c_int, C.c_uint64, i64p)
+_sig("sp_rt_set_chunk", C.c_int, i64)
 _sig("sp_halo_plan_create", C.c_int, C.POINTER(HaloConfig), vp, C.c_int, C.POINTER(vp))
 _sig("sp_halo_plan_exchange", C.c_int, vp, dblp)
 _sig("sp_halo_plan_free", C.c_int, vp)

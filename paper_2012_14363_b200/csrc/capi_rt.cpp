@@ -127,7 +127,7 @@ sp_status sp_rt_send(const void *buf, uint64_t buf_bytes, int64_t count, sp_type
   return guarded([&] {
     if (count < 0) fail(SP_ERR_INVALID_ARGUMENT, "send: negative count");
     RtTrace tr{};
-    rt_send(buf, buf_bytes, count, *committed_of(t), dest, tag, method, &tr);
+    rt_send(buf, buf_bytes, count, committed_of(t), dest, tag, method, &tr);
     if (used_method) *used_method = tr.method;
   });
 }
@@ -137,7 +137,7 @@ sp_status sp_rt_recv(void *buf, uint64_t buf_bytes, int64_t count, sp_type t, in
   return guarded([&] {
     if (count < 0) fail(SP_ERR_INVALID_ARGUMENT, "recv: negative count");
     RtStatus st{};
-    rt_recv(buf, buf_bytes, count, *committed_of(t), source, tag, &st);
+    rt_recv(buf, buf_bytes, count, committed_of(t), source, tag, &st);
     if (status) {
       status[0] = st.source;
       status[1] = st.tag;
@@ -145,6 +145,58 @@ sp_status sp_rt_recv(void *buf, uint64_t buf_bytes, int64_t count, sp_type t, in
       status[3] = st.method;
     }
   });
+}
+
+namespace {
+void fill_status(const RtStatus &st, int64_t status[4]) {
+  if (!status) return;
+  status[0] = st.source;
+  status[1] = st.tag;
+  status[2] = st.bytes;
+  status[3] = st.method;
+}
+} // namespace
+
+sp_status sp_rt_isend(const void *buf, uint64_t buf_bytes, int64_t count, sp_type t, int dest, int tag, int method,
+                      sp_request *req) {
+  return guarded([&] {
+    need(req);
+    if (count < 0) fail(SP_ERR_INVALID_ARGUMENT, "send: negative count");
+    *req = rt_isend(buf, buf_bytes, count, committed_of(t), dest, tag, method);
+  });
+}
+
+sp_status sp_rt_irecv(void *buf, uint64_t buf_bytes, int64_t count, sp_type t, int source, int tag,
+                      sp_request *req) {
+  return guarded([&] {
+    need(req);
+    if (count < 0) fail(SP_ERR_INVALID_ARGUMENT, "recv: negative count");
+    *req = rt_irecv(buf, buf_bytes, count, committed_of(t), source, tag);
+  });
+}
+
+sp_status sp_rt_test(sp_request req, int *done, int64_t status[4]) {
+  return guarded([&] {
+    need(done);
+    RtStatus st{};
+    *done = 0;
+    if (rt_test(req, &st)) {
+      *done = 1;
+      fill_status(st, status);
+    }
+  });
+}
+
+sp_status sp_rt_wait(sp_request req, int64_t status[4]) {
+  return guarded([&] {
+    RtStatus st{};
+    rt_wait(req, &st);
+    fill_status(st, status);
+  });
+}
+
+sp_status sp_rt_set_chunk(int64_t bytes) {
+  return guarded([&] { rt_set_chunk(bytes); });
 }
 
 sp_status sp_rt_neighbor_alltoallv(const void *sendbuf, const int64_t *sendcounts, const int64_t *sdispls,

@@ -179,6 +179,12 @@ struct CopySpec {
   int64_t dcount;
 };
 Batch *copy_batch_create(const std::vector<CopySpec> &specs);
+// single-job launches over the packed-byte range [lo, hi) of one message
+// (chunks of a pipelined message; lo and interior hi multiples of 16):
+// no descriptor upload, the job travels as a kernel parameter
+bool range_capable(const Committed &ct, int64_t count, const void *strided, const void *packed);
+void range_execute(const BatchSpec &spec, bool unpack, uint64_t lo, uint64_t hi, void *stream);
+void copy_execute(const CopySpec &spec, uint64_t lo, uint64_t hi, void *stream);
 void batch_execute(const Batch &b, void *stream);
 void batch_destroy(Batch *b);
 // in-kernel completion protocol for distributed exchanges (pack.cu)

@@ -881,6 +881,7 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
 // job (ranges rarely cross a job boundary); the job descriptors are read
 // through the read-only path and stay L1-resident.
 constexpr int kBatchU = 4;
+constexpr int kJobSlots = 4; // job descriptors a CTA stages in shared memory
 enum : int { kModeUnpack = 0, kModePack = 1, kModeCopy = 2 };
 
 struct BatchJob {
@@ -889,6 +890,8 @@ struct BatchJob {
   const uint8_t *in; // source base (strided sources already at start)
   uint8_t *out;      // destination base
   uint64_t begin;    // first word of this job in the launch's index space
+  uint32_t q0;       // first word of the job's own stream this launch moves
+                     // (non-zero for one chunk of a pipelined message)
   int same;          // COPY with gd == gs: destination offset = source offset
 };
 
@@ -929,8 +932,8 @@ template <int W> __device__ __forceinline__ int64_t word_offset(uint32_t q, cons
 }
 
 template <int W, int MODE>
-__global__ void __launch_bounds__(256) k_batch(const BatchJob *__restrict__ jobs, int njobs, uint32_t total,
-                                               uint32_t per_block, const BatchSig sig) {
+__device__ __forceinline__ void batch_body(const BatchJob *__restrict__ jobs, int njobs, uint32_t total,
+                                           uint32_t per_block, const BatchSig &sig) {
   using T = typename Word<W>::T;
   if (sig.n_pre && blockIdx.x == 0 && threadIdx.x < static_cast<unsigned>(sig.n_pre))
     st_release_sys(sig.pre[threadIdx.x], sig.pre_value);
@@ -941,33 +944,49 @@ __global__ void __launch_bounds__(256) k_batch(const BatchJob *__restrict__ jobs
   }
   const uint32_t lo = blockIdx.x * per_block;
   const uint32_t hi = min(total, lo + per_block);
-  // first job of this block's range: last job with begin <= lo
-  int j0 = 0;
-  {
+  // jobs of this block's range: [j0, j1]; up to kJobSlots of them are
+  // staged in shared memory so the per-word index math reads on-chip
+  // descriptors (a range spanning more, e.g. many halo corners, reads the
+  // descriptors from global memory through L1)
+  __shared__ BatchJob sjob[kJobSlots];
+  auto last_le = [&](uint32_t q) {
     int a = 0, b = njobs - 1;
     while (a < b) {
       const int m = (a + b + 1) >> 1;
-      if (jobs[m].begin <= lo) {
+      if (jobs[m].begin <= q) {
         a = m;
       } else {
         b = m - 1;
       }
     }
-    j0 = a;
+    return a;
+  };
+  const int j0 = lo < hi ? last_le(lo) : 0;
+  const int j1 = lo < hi ? last_le(hi - 1) : 0;
+  const int nj = j1 - j0 + 1;
+  const bool staged = nj <= kJobSlots;
+  if (staged) {
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(jobs + j0);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(sjob);
+    const uint32_t words = static_cast<uint32_t>(nj * sizeof(BatchJob) / 4);
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
   }
+  __syncthreads();
+  const BatchJob *JB = staged ? sjob : jobs + j0;
+  const int nlocal = staged ? nj : njobs - j0;
   for (uint32_t base = lo + threadIdx.x; base < hi; base += 256 * kBatchU) {
     T v[kBatchU];
     int64_t doff[kBatchU];
     int jw[kBatchU];
-    int j = j0;
+    int j = 0;
 #pragma unroll
     for (int u = 0; u < kBatchU; ++u) {
       const uint32_t q = base + u * 256;
       jw[u] = -1;
       if (q < hi) {
-        while (j + 1 < njobs && jobs[j + 1].begin <= q) ++j;
-        const BatchJob &J = jobs[j];
-        const uint32_t ql = q - static_cast<uint32_t>(J.begin);
+        while (j + 1 < nlocal && JB[j + 1].begin <= q) ++j;
+        const BatchJob &J = JB[j];
+        const uint32_t ql = q - static_cast<uint32_t>(J.begin) + J.q0;
         jw[u] = j;
         if (MODE == kModeUnpack) {
           v[u] = ld_stream(reinterpret_cast<const T *>(J.in) + ql);
@@ -985,7 +1004,7 @@ __global__ void __launch_bounds__(256) k_batch(const BatchJob *__restrict__ jobs
     }
 #pragma unroll
     for (int u = 0; u < kBatchU; ++u)
-      if (jw[u] >= 0) st_stream(reinterpret_cast<T *>(jobs[jw[u]].out + doff[u]), v[u]);
+      if (jw[u] >= 0) st_stream(reinterpret_cast<T *>(JB[jw[u]].out + doff[u]), v[u]);
   }
   if (sig.n_signal) {
     // bar.sync orders every thread's stores before thread 0 (CTA scope);
@@ -1006,6 +1025,21 @@ __global__ void __launch_bounds__(256) k_batch(const BatchJob *__restrict__ jobs
       atomicExch(sig.done, 0u); // ready for the next launch on this stream
     }
   }
+}
+
+template <int W, int MODE>
+__global__ void __launch_bounds__(256) k_batch(const BatchJob *__restrict__ jobs, int njobs, uint32_t total,
+                                               uint32_t per_block, const BatchSig sig) {
+  batch_body<W, MODE>(jobs, njobs, total, per_block, sig);
+}
+
+// one job passed by value (param space): a single message or message chunk
+// launches without uploading a descriptor
+template <int W, int MODE>
+__global__ void __launch_bounds__(256) k_job(const __grid_constant__ BatchJob job, uint32_t total,
+                                             uint32_t per_block) {
+  const BatchSig none{};
+  batch_body<W, MODE>(&job, 1, total, per_block, none);
 }
 
 struct BatchGroup {
@@ -1092,36 +1126,77 @@ Batch *build_batch(std::vector<BatchJob> (&by_w)[5], int mode, int64_t bytes) {
 
 } // namespace
 
+namespace {
+
+// validated job of one (type, count, buffers) pack or unpack; `align` is
+// OR-ed into the word-size choice (chunk boundaries of a pipelined message).
+// Returns false for an Empty form (nothing to move).
+bool make_pack_job(const BatchSpec &s, bool unpack, uint64_t align, BatchJob &j, int &w) {
+  const Committed &ct = *s.ct;
+  // argument checks in the reference's precedence (pack.hpp:102-126 / :146-159)
+  if (s.count < 1 || s.position < 0) fail(SP_ERR_INVALID_ARGUMENT, "batch: count must be positive, position >= 0");
+  if (unpack && ct.overlapping) fail(SP_ERR_OVERLAPPING_LAYOUT, "batch: unpack layout describes overlapping bytes");
+  const uint64_t packed_need = static_cast<uint64_t>(s.position + s.count * ct.size);
+  if (packed_need > (unpack ? s.src_bytes : s.dst_bytes)) fail(SP_ERR_BUFFER_TOO_SMALL, "batch: packed buffer too small");
+  if (ct.form == SP_FORM_EMPTY) return false;
+  const uint64_t strided_need = static_cast<uint64_t>((s.count - 1) * ct.extent + ct.span);
+  if (strided_need > (unpack ? s.dst_bytes : s.src_bytes)) fail(SP_ERR_BUFFER_TOO_SMALL, "batch: strided buffer too small");
+  if (ct.form != SP_FORM_STRIDED) fail(SP_ERR_UNSUPPORTED, "batch: only strided forms can be batched");
+  const uint8_t *strided = batch_ptr(unpack ? s.dst : s.src) + ct.sb.start;
+  const uint8_t *packed = batch_ptr(unpack ? s.src : s.dst) + s.position;
+  const RowDims rd = row_dims(ct, s.count);
+  w = pow2_align(align_bits(rd, reinterpret_cast<uint64_t>(strided)) | reinterpret_cast<uint64_t>(packed) | align);
+  j = BatchJob{};
+  const Geom g = batch_geom(rd, w);
+  if (unpack) {
+    j.gd = g;
+  } else {
+    j.gs = g;
+  }
+  j.in = unpack ? packed : strided;
+  j.out = const_cast<uint8_t *>(unpack ? strided : packed);
+  return true;
+}
+
+bool make_copy_job(const CopySpec &s, uint64_t align, BatchJob &j, int &w) {
+  const Committed &sc = *s.sct, &dc = *s.dct;
+  if (s.scount < 0 || s.dcount < 0) fail(SP_ERR_INVALID_ARGUMENT, "copy: counts must be >= 0");
+  if (s.scount * sc.size != s.dcount * dc.size)
+    fail(SP_ERR_INVALID_ARGUMENT, "copy: source and destination describe different byte counts");
+  if (dc.overlapping) fail(SP_ERR_OVERLAPPING_LAYOUT, "copy: destination layout describes overlapping bytes");
+  if (s.scount * sc.size == 0) return false;
+  if (static_cast<uint64_t>((s.scount - 1) * sc.extent + sc.span) > s.src_bytes)
+    fail(SP_ERR_BUFFER_TOO_SMALL, "copy: source too small");
+  if (static_cast<uint64_t>((s.dcount - 1) * dc.extent + dc.span) > s.dst_bytes)
+    fail(SP_ERR_BUFFER_TOO_SMALL, "copy: destination too small");
+  if (sc.form != SP_FORM_STRIDED || dc.form != SP_FORM_STRIDED)
+    fail(SP_ERR_UNSUPPORTED, "copy: only strided forms can be batched");
+  const uint8_t *src = batch_ptr(s.src) + sc.sb.start;
+  const uint8_t *dst = batch_ptr(s.dst) + dc.sb.start;
+  const RowDims rs = row_dims(sc, s.scount), rd = row_dims(dc, s.dcount);
+  w = pow2_align(align_bits(rs, reinterpret_cast<uint64_t>(src)) | align_bits(rd, reinterpret_cast<uint64_t>(dst)) |
+                 align);
+  j = BatchJob{};
+  j.gs = batch_geom(rs, w);
+  j.gd = batch_geom(rd, w);
+  j.same = same_geom(rs, rd) ? 1 : 0;
+  j.in = src;
+  j.out = const_cast<uint8_t *>(dst);
+  return true;
+}
+
+} // namespace
+
 Batch *batch_create(const std::vector<BatchSpec> &specs, bool unpack) {
   require_device();
   std::vector<BatchJob> by_w[5]; // W = 1, 2, 4, 8, 16
   int64_t bytes = 0;
   for (const BatchSpec &s : specs) {
-    const Committed &ct = *s.ct;
-    // argument checks in the reference's precedence (pack.hpp:102-126 / :146-159)
-    if (s.count < 1 || s.position < 0) fail(SP_ERR_INVALID_ARGUMENT, "batch: count must be positive, position >= 0");
-    if (unpack && ct.overlapping) fail(SP_ERR_OVERLAPPING_LAYOUT, "batch: unpack layout describes overlapping bytes");
-    const uint64_t packed_need = static_cast<uint64_t>(s.position + s.count * ct.size);
-    if (packed_need > (unpack ? s.src_bytes : s.dst_bytes)) fail(SP_ERR_BUFFER_TOO_SMALL, "batch: packed buffer too small");
-    if (ct.form == SP_FORM_EMPTY) continue;
-    const uint64_t strided_need = static_cast<uint64_t>((s.count - 1) * ct.extent + ct.span);
-    if (strided_need > (unpack ? s.dst_bytes : s.src_bytes)) fail(SP_ERR_BUFFER_TOO_SMALL, "batch: strided buffer too small");
-    if (ct.form != SP_FORM_STRIDED) fail(SP_ERR_UNSUPPORTED, "batch: only strided forms can be batched");
-    const uint8_t *strided = batch_ptr(unpack ? s.dst : s.src) + ct.sb.start;
-    const uint8_t *packed = batch_ptr(unpack ? s.src : s.dst) + s.position;
-    const RowDims rd = row_dims(ct, s.count);
-    const int w = pow2_align(align_bits(rd, reinterpret_cast<uint64_t>(strided)) | reinterpret_cast<uint64_t>(packed));
-    BatchJob j{};
-    const Geom g = batch_geom(rd, w);
-    if (unpack) {
-      j.gd = g;
-    } else {
-      j.gs = g;
-    }
-    j.in = unpack ? packed : strided;
-    j.out = const_cast<uint8_t *>(unpack ? strided : packed);
+    BatchJob j;
+    int w = 1;
+    if (!make_pack_job(s, unpack, 0, j, w)) continue;
     by_w[__builtin_ctz(static_cast<unsigned>(w))].push_back(j);
-    bytes += s.count * ct.size;
+    bytes += s.count * s.ct->size;
   }
   return build_batch(by_w, unpack ? kModeUnpack : kModePack, bytes);
 }
@@ -1131,31 +1206,11 @@ Batch *copy_batch_create(const std::vector<CopySpec> &specs) {
   std::vector<BatchJob> by_w[5];
   int64_t bytes = 0;
   for (const CopySpec &s : specs) {
-    const Committed &sc = *s.sct, &dc = *s.dct;
-    if (s.scount < 0 || s.dcount < 0) fail(SP_ERR_INVALID_ARGUMENT, "copy: counts must be >= 0");
-    if (s.scount * sc.size != s.dcount * dc.size)
-      fail(SP_ERR_INVALID_ARGUMENT, "copy: source and destination describe different byte counts");
-    if (dc.overlapping) fail(SP_ERR_OVERLAPPING_LAYOUT, "copy: destination layout describes overlapping bytes");
-    if (s.scount * sc.size == 0) continue;
-    if (static_cast<uint64_t>((s.scount - 1) * sc.extent + sc.span) > s.src_bytes)
-      fail(SP_ERR_BUFFER_TOO_SMALL, "copy: source too small");
-    if (static_cast<uint64_t>((s.dcount - 1) * dc.extent + dc.span) > s.dst_bytes)
-      fail(SP_ERR_BUFFER_TOO_SMALL, "copy: destination too small");
-    if (sc.form != SP_FORM_STRIDED || dc.form != SP_FORM_STRIDED)
-      fail(SP_ERR_UNSUPPORTED, "copy: only strided forms can be batched");
-    const uint8_t *src = batch_ptr(s.src) + sc.sb.start;
-    const uint8_t *dst = batch_ptr(s.dst) + dc.sb.start;
-    const RowDims rs = row_dims(sc, s.scount), rd = row_dims(dc, s.dcount);
-    const int w = pow2_align(align_bits(rs, reinterpret_cast<uint64_t>(src)) |
-                             align_bits(rd, reinterpret_cast<uint64_t>(dst)));
-    BatchJob j{};
-    j.gs = batch_geom(rs, w);
-    j.gd = batch_geom(rd, w);
-    j.same = same_geom(rs, rd) ? 1 : 0;
-    j.in = src;
-    j.out = const_cast<uint8_t *>(dst);
+    BatchJob j;
+    int w = 1;
+    if (!make_copy_job(s, 0, j, w)) continue;
     by_w[__builtin_ctz(static_cast<unsigned>(w))].push_back(j);
-    bytes += s.scount * sc.size;
+    bytes += s.scount * s.sct->size;
   }
   return build_batch(by_w, kModeCopy, bytes);
 }
@@ -1246,6 +1301,90 @@ void flags_wait(const std::vector<const uint64_t *> &wait, uint64_t value, void 
   k_flag_wait<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(sig);
   cuda_check(cudaGetLastError(), "k_flag_wait launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+namespace {
+
+template <int W, int MODE> void launch_job(const BatchJob &j, uint32_t words, cudaStream_t s) {
+  static thread_local int occ_dev = -1, occ = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (occ_dev != dev) {
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_job<W, MODE>, 256, 0), "occupancy");
+    occ = std::max(occ, 1);
+    occ_dev = dev;
+  }
+  const uint64_t want = (static_cast<uint64_t>(words) + 256ull * kBatchU - 1) / (256ull * kBatchU);
+  uint64_t cap = static_cast<uint64_t>(sm_count()) * occ;
+  if (t_host_grid_cap) cap = std::min<uint64_t>(cap, t_host_grid_cap);
+  const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, cap)));
+  const uint32_t per = static_cast<uint32_t>((static_cast<uint64_t>(words) + grid - 1) / grid);
+  k_job<W, MODE><<<grid, 256, 0, s>>>(j, words, per);
+  cuda_check(cudaGetLastError(), "k_job launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  sp_launch_info li{};
+  li.kernel = SP_KERNEL_BATCH;
+  li.word = W;
+  li.launches = 1;
+  li.grid = grid;
+  li.block = 256;
+  set_last_launch(li);
+}
+
+template <int MODE> void launch_job_w(int w, const BatchJob &j, uint32_t words, cudaStream_t s) {
+  switch (w) {
+  case 16: launch_job<16, MODE>(j, words, s); break;
+  case 8: launch_job<8, MODE>(j, words, s); break;
+  case 4: launch_job<4, MODE>(j, words, s); break;
+  case 2: launch_job<2, MODE>(j, words, s); break;
+  default: launch_job<1, MODE>(j, words, s); break;
+  }
+}
+
+// words [lo/w, hi/w) of a job's stream in one launch
+void launch_range(int mode, int w, BatchJob j, uint64_t total_bytes, uint64_t lo, uint64_t hi, cudaStream_t s) {
+  if (hi > total_bytes || lo > hi) fail(SP_ERR_INVALID_ARGUMENT, "range outside the message");
+  if (lo == hi) return;
+  if ((hi - lo) / w >= (1ull << 32) || hi / w >= (1ull << 32)) fail(SP_ERR_UNSUPPORTED, "range larger than 2^32 words");
+  j.begin = 0;
+  j.q0 = static_cast<uint32_t>(lo / w);
+  const uint32_t words = static_cast<uint32_t>((hi - lo) / w);
+  switch (mode) {
+  case kModePack: launch_job_w<kModePack>(w, j, words, s); break;
+  case kModeUnpack: launch_job_w<kModeUnpack>(w, j, words, s); break;
+  default: launch_job_w<kModeCopy>(w, j, words, s); break;
+  }
+}
+
+// chunk boundaries strictly inside the message carry alignment; the end of
+// the message is a whole number of words by construction
+uint64_t range_align(uint64_t lo, uint64_t hi, uint64_t total) { return lo | (hi == total ? 0 : hi); }
+
+} // namespace
+
+bool range_capable(const Committed &ct, int64_t count, const void *strided, const void *packed) {
+  if (ct.form != SP_FORM_STRIDED || count < 1) return false;
+  if (static_cast<int>(row_dims(ct, count).cnt.size()) > KMAX) return false;
+  const Resolved a = resolve(strided), b = resolve(packed);
+  return a.kind != MemKind::Pageable && b.kind != MemKind::Pageable;
+}
+
+void range_execute(const BatchSpec &spec, bool unpack, uint64_t lo, uint64_t hi, void *stream) {
+  require_device();
+  const uint64_t total = static_cast<uint64_t>(spec.count * spec.ct->size);
+  BatchJob j;
+  int w = 1;
+  if (!make_pack_job(spec, unpack, range_align(lo, hi, total), j, w)) return;
+  launch_range(unpack ? kModeUnpack : kModePack, w, j, total, lo, hi, static_cast<cudaStream_t>(stream));
+}
+
+void copy_execute(const CopySpec &spec, uint64_t lo, uint64_t hi, void *stream) {
+  require_device();
+  const uint64_t total = static_cast<uint64_t>(spec.scount * spec.sct->size);
+  BatchJob j;
+  int w = 1;
+  if (!make_copy_job(spec, range_align(lo, hi, total), j, w)) return;
+  launch_range(kModeCopy, w, j, total, lo, hi, static_cast<cudaStream_t>(stream));
 }
 
 void batch_execute(const Batch &b, void *stream) { batch_launch(b, stream, nullptr); }

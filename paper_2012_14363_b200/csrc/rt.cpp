@@ -16,6 +16,7 @@
 #include <unistd.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -29,6 +30,9 @@
 #include "rt.hpp"
 
 namespace spb {
+
+void engine_init(int64_t window_bytes, int64_t host_bytes);
+void engine_fini();
 
 namespace {
 
@@ -53,6 +57,21 @@ struct Mailbox { // single producer (src) / single consumer (dst)
   Msg ring[kRing];
 };
 
+// a receiver's published destination for a DIRECT message: its buffer (IPC
+// handle + offset, raw pointer for self-sends) and its type's canonical
+// StridedBlock, from which the sender rebuilds the destination geometry
+constexpr int kDescs = 32;
+constexpr int kDescDims = 12;
+struct Desc {
+  int32_t ndims;
+  int32_t pad;
+  int64_t start, size, extent, span, count;
+  int64_t counts[kDescDims], strides[kDescDims];
+  cudaIpcMemHandle_t h;
+  int64_t off;
+  uint64_t raw;
+};
+
 struct Slot {
   std::atomic<uint32_t> ready;
   int32_t pid;
@@ -67,6 +86,7 @@ struct Slot {
   int32_t nedges;             // neighbour-exchange in-edges: (src, offset, bytes)
   int32_t pad2;
   int64_t edges[kMaxEdges][3];
+  Desc desc[kDescs];          // DIRECT destinations granted by this rank
 };
 
 struct Shm {
@@ -106,7 +126,8 @@ struct Runtime {
   std::vector<uint8_t *> peer_host;
   std::map<std::string, uint8_t *> ipc_cache; // handle bytes -> mapped base
   std::deque<Msg> unexpected;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;  // sends, batches, halo plans
+  cudaStream_t rstream = nullptr; // receives (unpack of arriving chunks)
   std::unique_ptr<sp_model_cache_s, sp_status (*)(sp_model_cache_s *)> cache{nullptr, sp_model_cache_free};
   sp_profile_s *profile = nullptr;
   std::mutex mu; // the runtime serialises its own calls (MPI_THREAD_SERIALIZED)
@@ -145,12 +166,19 @@ void *map_shm(const std::string &nm, size_t bytes, bool create) {
   return p;
 }
 
+void drain();
+
 void post(int dst, const Msg &m) {
   Runtime &R = rt();
   Mailbox &b = R.shm->box[dst][R.rank];
   const uint64_t t = b.tail.load(std::memory_order_relaxed);
   unsigned spins = 0;
-  while (t - b.head.load(std::memory_order_acquire) >= kRing) pause_briefly(spins);
+  // a full ring: keep draining our own mailboxes so two ranks posting to
+  // each other cannot wait on each other
+  while (t - b.head.load(std::memory_order_acquire) >= kRing) {
+    drain();
+    pause_briefly(spins);
+  }
   b.ring[t % kRing] = m;
   b.tail.store(t + 1, std::memory_order_release);
 }
@@ -272,6 +300,7 @@ void rt_init(int rank, int size, const char *name, int device, int64_t window_by
   if (device >= 0) {
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
     cuda_check(cudaStreamCreateWithFlags(&G.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaStreamCreateWithFlags(&G.rstream, cudaStreamNonBlocking), "cudaStreamCreate");
     if (window_bytes > 0) {
       cuda_check(cudaMalloc(&G.window, static_cast<size_t>(window_bytes)), "cudaMalloc(window)");
       cuda_check(cudaIpcGetMemHandle(&me.window, G.window), "cudaIpcGetMemHandle(window)");
@@ -289,6 +318,7 @@ void rt_init(int rank, int size, const char *name, int device, int64_t window_by
   }
   me.window_bytes = G.window_bytes;
   me.host_bytes = G.host_bytes;
+  engine_init(G.window_bytes, G.host_bytes);
   me.ready.store(1, std::memory_order_release);
   rt_barrier();
 }
@@ -310,7 +340,9 @@ void rt_finalize() {
     munmap(R.host, static_cast<size_t>(R.host_bytes));
     shm_unlink(host_name(R.name, R.rank).c_str());
   }
+  engine_fini();
   if (R.stream) cudaStreamDestroy(R.stream);
+  if (R.rstream) cudaStreamDestroy(R.rstream);
   const bool last = R.rank == 0;
   const std::string nm = R.name;
   munmap(R.shm, R.shm_bytes);
@@ -331,7 +363,10 @@ void rt_barrier() {
     R.shm->generation.store(gen + 1, std::memory_order_release);
   } else {
     unsigned spins = 0;
-    while (R.shm->generation.load(std::memory_order_acquire) == gen) pause_briefly(spins);
+    while (R.shm->generation.load(std::memory_order_acquire) == gen) {
+      rt_progress(); // pending non-blocking messages keep moving
+      pause_briefly(spins);
+    }
   }
 }
 
@@ -373,111 +408,601 @@ void rt_exchange_ptr(void *local, std::vector<uint8_t *> &out) {
 }
 
 // ------------------------------------------------------------ point to point
-// Rendezvous: the sender announces (RTS), the receiver grants its window
-// (CTS) once a matching receive is posted, the sender packs straight into
-// the granted memory and signals completion (FIN), the receiver unpacks.
+// Non-blocking rendezvous with a progress engine (MPI_Isend / MPI_Irecv;
+// the blocking calls are isend/irecv + wait). Per message:
+//   sender   RTS(method, bytes, direct-capable)          -> receiver
+//   receiver CTS(method', offset of its grant)           -> sender
+//   sender   CHUNK(k of n, packed bytes [lo, hi)) ...    -> receiver
+// Transfer methods (the model picks the first three):
 //   DEVICE : pack kernel -> receiver's device window through CUDA IPC
-//            (NVLink); receiver unpacks from its own HBM
+//            (NVLink); the receiver unpacks from its own HBM
 //   ONESHOT: pack kernel -> receiver's shared pinned host region (mapped);
-//            receiver's unpack kernel reads host memory directly
-//   STAGED : pack kernel -> local device scratch -> D2H copy into the
-//            receiver's host region; receiver copies H2D, then unpacks
-void rt_send(const void *buf, uint64_t buf_bytes, int64_t count, const Committed &ct, int dest, int tag,
-             int method, RtTrace *trace) {
-  Runtime &R = rt();
-  if (dest < 0 || dest >= R.size) fail(SP_ERR_INVALID_ARGUMENT, "send: bad destination rank");
-  if (tag < 0) fail(SP_ERR_INVALID_ARGUMENT, "send: negative tag");
-  const int64_t bytes = count * ct.size;
-  if (method < 0) method = rt_choose(ct, count);
-  if (method == SP_METHOD_DEVICE && bytes > R.shm->slots[dest].window_bytes)
-    fail(SP_ERR_UNSUPPORTED, "send: message larger than the receive window");
-  if (method != SP_METHOD_DEVICE && bytes > R.shm->slots[dest].host_bytes)
-    fail(SP_ERR_UNSUPPORTED, "send: message larger than the receiver's host region");
-  post(dest, Msg{kRTS, R.rank, tag, method, bytes, 0, 0});
-  wait_msg(kCTS, dest, tag);
-  if (bytes > 0) {
-    int64_t pos = 0;
-    PackArgs a{};
-    a.ct = &ct;
-    a.src = buf;
-    a.src_bytes = buf_bytes;
-    a.count = count;
-    a.stream = R.stream;
-    a.opt = sp_pack_options{1, SP_KERNEL_AUTO, 0};
-    a.pack = true;
-    if (method == SP_METHOD_DEVICE) {
-      a.dst = peer_window(dest);
-      a.dst_bytes = static_cast<uint64_t>(bytes);
-      execute(a);
-    } else if (method == SP_METHOD_ONESHOT) {
-      a.dst = peer_host(dest);
-      a.dst_bytes = static_cast<uint64_t>(bytes);
-      execute(a);
-    } else {
-      uint8_t *scratch = nullptr;
-      cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&scratch), static_cast<size_t>(bytes), R.stream),
-                 "cudaMallocAsync");
-      a.dst = scratch;
-      a.dst_bytes = static_cast<uint64_t>(bytes);
-      execute(a);
-      cuda_check(cudaMemcpyAsync(peer_host(dest), scratch, static_cast<size_t>(bytes), cudaMemcpyDeviceToHost,
-                                 R.stream),
-                 "staged D2H");
-      cuda_check(cudaFreeAsync(scratch, R.stream), "cudaFreeAsync");
-    }
-    (void)pos;
-    cuda_check(cudaStreamSynchronize(R.stream), "cudaStreamSynchronize(send)");
+//            the receiver's unpack kernel reads host memory directly
+//   STAGED : pack kernel -> local device scratch -> D2H into the receiver's
+//            host region; the receiver copies H2D, then unpacks
+//   DIRECT : the receiver upgrades a DEVICE message whose destination is
+//            device memory: it publishes its buffer (IPC) and the canonical
+//            geometry of its type, and the sender runs ONE typed-copy kernel
+//            that stores every byte at its final strided address in the
+//            receiver's HBM -- pack, NVLink transfer and unpack fused, no
+//            window, no unpack launch.
+// Messages above two chunks (TEMPI_CHUNK / sp_rt_set_chunk, default 4 MiB)
+// move in chunks of the packed stream: the sender reports each chunk as its
+// event completes, and the receiver unpacks (STAGED: copies in and unpacks)
+// chunk k while the sender is still producing chunk k+1, so packing, the
+// link and unpacking overlap. Grants are carved out of the receiver's window
+// / host region by a first-fit allocator, so several messages can be in
+// flight to one rank.
+namespace {
+
+constexpr uint32_t kCHUNK = 5;
+constexpr int64_t kGrantAlign = 256;
+
+struct RangeAlloc {
+  std::map<int64_t, int64_t> free_; // offset -> length
+  void reset(int64_t cap) {
+    free_.clear();
+    if (cap > 0) free_[0] = cap;
   }
-  post(dest, Msg{kFIN, R.rank, tag, method, bytes, 0, 0});
-  if (trace) {
-    trace->method = method;
-    trace->bytes = bytes;
+  int64_t take(int64_t n) {
+    n = std::max<int64_t>(kGrantAlign, (n + kGrantAlign - 1) / kGrantAlign * kGrantAlign);
+    for (auto it = free_.begin(); it != free_.end(); ++it) {
+      if (it->second < n) continue;
+      const int64_t off = it->first, len = it->second;
+      free_.erase(it);
+      if (len > n) free_[off + n] = len - n;
+      return off;
+    }
+    return -1;
+  }
+  void give(int64_t off, int64_t n) {
+    n = std::max<int64_t>(kGrantAlign, (n + kGrantAlign - 1) / kGrantAlign * kGrantAlign);
+    auto it = free_.emplace(off, n).first;
+    auto nx = std::next(it);
+    if (nx != free_.end() && it->first + it->second == nx->first) {
+      it->second += nx->second;
+      free_.erase(nx);
+    }
+    if (it != free_.begin()) {
+      auto pv = std::prev(it);
+      if (pv->first + pv->second == it->first) {
+        pv->second += it->second;
+        free_.erase(it);
+      }
+    }
+  }
+};
+
+enum class St { Start, WaitCts, Streaming, WaitRts, Matched, Receiving, Draining, Done };
+
+struct Req {
+  uint64_t id = 0;
+  bool send = false;
+  St st = St::Start;
+  const void *sbuf = nullptr;
+  void *rbuf = nullptr;
+  uint64_t buf_bytes = 0;
+  int64_t count = 0;
+  CommitPtr ct;
+  int peer = -1, tag = 0, method = 0;
+  int64_t bytes = 0;
+  // sender
+  uint64_t rreq = 0;
+  int64_t grant = 0;
+  int nchunks = 0, reported = 0;
+  std::vector<std::pair<int64_t, int64_t>> chunks;
+  std::vector<cudaEvent_t> evs;
+  uint8_t *scratch = nullptr;
+  // receiver
+  int src_want = -1, tag_want = -1;
+  uint64_t sreq = 0;
+  int region = 0; // 1 window, 2 host region, 3 descriptor
+  int got = 0, expect = -1;
+  bool ranged = false;
+  uint8_t *rbuf_stage = nullptr;
+  cudaEvent_t last = nullptr;
+  RtStatus status{};
+  // completion
+  sp_status err = SP_OK;
+  std::string msg;
+};
+
+struct Engine {
+  uint64_t next_id = 1;
+  std::deque<std::unique_ptr<Req>> active;      // posting order
+  std::map<uint64_t, std::unique_ptr<Req>> done; // completed, not yet waited
+  std::vector<cudaEvent_t> pool;
+  RangeAlloc win, host;
+  uint32_t desc_used = 0; // bitmap of this rank's published descriptors
+  int64_t chunk = int64_t{4} << 20;
+  bool in_progress = false;
+};
+Engine *g_eng = nullptr;
+
+Engine &eng() {
+  if (!g_eng) fail(SP_ERR_INVALID_ARGUMENT, "runtime not initialised (sp_rt_init)");
+  return *g_eng;
+}
+
+cudaEvent_t get_event() {
+  Engine &E = eng();
+  if (!E.pool.empty()) {
+    cudaEvent_t e = E.pool.back();
+    E.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+  return e;
+}
+
+void put_event(cudaEvent_t e) {
+  if (e) eng().pool.push_back(e);
+}
+
+bool event_done(cudaEvent_t e) {
+  const cudaError_t q = cudaEventQuery(e);
+  if (q == cudaSuccess) return true;
+  if (q == cudaErrorNotReady) return false;
+  cuda_check(q, "cudaEventQuery");
+  return false;
+}
+
+// first message of `kind` from `src` addressed to request `id`
+bool take(uint32_t kind, int src, uint64_t id, Msg &out) {
+  Runtime &R = rt();
+  for (auto it = R.unexpected.begin(); it != R.unexpected.end(); ++it)
+    if (it->kind == kind && it->src == src && static_cast<uint64_t>(it->aux) == id) {
+      out = *it;
+      R.unexpected.erase(it);
+      return true;
+    }
+  return false;
+}
+
+std::vector<std::pair<int64_t, int64_t>> chunk_plan(int64_t bytes) {
+  const int64_t c = eng().chunk;
+  std::vector<std::pair<int64_t, int64_t>> out;
+  if (bytes <= 2 * c) {
+    out.emplace_back(0, bytes);
+    return out;
+  }
+  for (int64_t lo = 0; lo < bytes; lo += c) out.emplace_back(lo, std::min(bytes, lo + c));
+  return out;
+}
+
+void committed_from(const Desc &d, Committed &c) {
+  c.form = SP_FORM_STRIDED;
+  c.size = d.size;
+  c.extent = d.extent;
+  c.span = d.span;
+  c.overlapping = false;
+  c.sb.start = d.start;
+  c.sb.counts.assign(d.counts, d.counts + d.ndims);
+  c.sb.strides.assign(d.strides, d.strides + d.ndims);
+}
+
+bool describable(const Committed &ct) {
+  return ct.form == SP_FORM_STRIDED && !ct.overlapping && ct.sb.ndims() <= kDescDims;
+}
+
+// ---- sender
+void send_stream(Req &q) {
+  Runtime &R = rt();
+  const cudaStream_t s = R.stream;
+  if (q.bytes == 0) {
+    q.chunks.assign(1, {0, 0});
+  } else if (q.method == SP_METHOD_DIRECT) {
+    const Desc &d = R.shm->slots[q.peer].desc[q.grant];
+    Committed dst;
+    committed_from(d, dst);
+    uint8_t *base = q.peer == R.rank ? reinterpret_cast<uint8_t *>(d.raw) : open_ipc(d.h) + d.off;
+    const CopySpec spec{q.ct.get(), q.sbuf, q.buf_bytes, q.count, &dst, base, UINT64_MAX, d.count};
+    copy_execute(spec, 0, static_cast<uint64_t>(q.bytes), s);
+    q.chunks.assign(1, {0, q.bytes});
+  } else {
+    uint8_t *dst = nullptr;
+    if (q.method == SP_METHOD_DEVICE) {
+      dst = peer_window(q.peer) + q.grant;
+    } else if (q.method == SP_METHOD_ONESHOT) {
+      dst = peer_host(q.peer) + q.grant;
+    } else {
+      cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&q.scratch), static_cast<size_t>(q.bytes), s),
+                 "cudaMallocAsync(staged)");
+      dst = q.scratch;
+    }
+    const bool ranged = range_capable(*q.ct, q.count, q.sbuf, dst);
+    q.chunks = ranged ? chunk_plan(q.bytes) : std::vector<std::pair<int64_t, int64_t>>{{0, q.bytes}};
+    const BatchSpec spec{q.ct.get(), q.sbuf, q.buf_bytes, q.count, dst, static_cast<uint64_t>(q.bytes), 0};
+    for (auto [lo, hi] : q.chunks) {
+      if (ranged) {
+        range_execute(spec, false, static_cast<uint64_t>(lo), static_cast<uint64_t>(hi), s);
+      } else {
+        PackArgs a{};
+        a.ct = q.ct.get();
+        a.src = q.sbuf;
+        a.src_bytes = q.buf_bytes;
+        a.count = q.count;
+        a.dst = dst;
+        a.dst_bytes = static_cast<uint64_t>(q.bytes);
+        a.stream = s;
+        a.opt = sp_pack_options{1, SP_KERNEL_AUTO, 0};
+        a.pack = true;
+        execute(a);
+      }
+      if (q.method == SP_METHOD_STAGED)
+        cuda_check(cudaMemcpyAsync(peer_host(q.peer) + q.grant + lo, q.scratch + lo, static_cast<size_t>(hi - lo),
+                                   cudaMemcpyDeviceToHost, s),
+                   "staged D2H");
+      cudaEvent_t e = get_event();
+      cuda_check(cudaEventRecord(e, s), "cudaEventRecord");
+      q.evs.push_back(e);
+    }
+    if (q.scratch) {
+      cuda_check(cudaFreeAsync(q.scratch, s), "cudaFreeAsync(staged)");
+      q.scratch = nullptr;
+    }
+  }
+  if (q.evs.empty()) { // nothing was launched (empty message) or DIRECT
+    cudaEvent_t e = get_event();
+    cuda_check(cudaEventRecord(e, s), "cudaEventRecord");
+    q.evs.push_back(e);
+  }
+  q.nchunks = static_cast<int>(q.chunks.size());
+}
+
+bool step_send(Req &q) {
+  Runtime &R = rt();
+  switch (q.st) {
+  case St::Start: {
+    // DIRECT travels as a DEVICE request the receiver may upgrade; the
+    // sender can run the copy kernel when its source is device-accessible
+    const bool direct_ok = q.bytes > 0 && q.method == SP_METHOD_DIRECT && range_capable(*q.ct, q.count, q.sbuf, q.sbuf);
+    if (q.method == SP_METHOD_DIRECT) q.method = SP_METHOD_DEVICE;
+    post(q.peer, Msg{kRTS, R.rank, q.tag, q.method, q.bytes, direct_ok ? 1 : 0, static_cast<int64_t>(q.id)});
+    q.st = St::WaitCts;
+    return true;
+  }
+  case St::WaitCts: {
+    Msg m;
+    if (!take(kCTS, q.peer, q.id, m)) return false;
+    q.method = m.method;
+    q.grant = m.offset;
+    q.rreq = static_cast<uint64_t>(m.tag);
+    q.bytes = m.bytes; // 0 when the receiver refused the message (truncation)
+    send_stream(q);
+    q.st = St::Streaming;
+    return true;
+  }
+  case St::Streaming: {
+    bool moved = false;
+    while (q.reported < static_cast<int>(q.evs.size()) && event_done(q.evs[q.reported])) {
+      const int k = q.reported;
+      const auto [lo, hi] = k < static_cast<int>(q.chunks.size()) ? q.chunks[k] : std::pair<int64_t, int64_t>{0, 0};
+      post(q.peer, Msg{kCHUNK, R.rank, k, q.nchunks, hi, lo, static_cast<int64_t>(q.rreq)});
+      ++q.reported;
+      moved = true;
+    }
+    if (q.reported == static_cast<int>(q.evs.size())) {
+      for (auto e : q.evs) put_event(e);
+      q.evs.clear();
+      q.st = St::Done;
+    }
+    return moved;
+  }
+  default:
+    return false;
   }
 }
 
-void rt_recv(void *buf, uint64_t buf_bytes, int64_t count, const Committed &ct, int source, int tag, RtStatus *st) {
+// ---- receiver
+bool step_recv(Req &q) {
   Runtime &R = rt();
-  const Msg rts = wait_msg(kRTS, source, tag);
-  const int64_t bytes = count * ct.size;
-  if (rts.bytes > bytes) fail(SP_ERR_BUFFER_TOO_SMALL, "recv: message truncated (MPI_ERR_TRUNCATE)");
-  post(rts.src, Msg{kCTS, R.rank, rts.tag, rts.method, rts.bytes, 0, 0});
-  wait_msg(kFIN, rts.src, rts.tag);
-  if (rts.bytes > 0) {
-    if (ct.size == 0 || rts.bytes % ct.size) fail(SP_ERR_INVALID_ARGUMENT, "recv: message is not whole objects");
-    const int64_t n = rts.bytes / ct.size;
-    int64_t pos = 0;
-    PackArgs a{};
-    a.ct = &ct;
-    a.dst = buf;
-    a.dst_bytes = buf_bytes;
-    a.count = n;
-    a.position = pos;
-    a.stream = R.stream;
-    a.opt = sp_pack_options{1, SP_KERNEL_AUTO, 0};
-    a.pack = false;
-    uint8_t *scratch = nullptr;
-    if (rts.method == SP_METHOD_DEVICE) {
-      a.src = R.window;
-    } else if (rts.method == SP_METHOD_ONESHOT) {
-      a.src = R.host;
-    } else {
-      cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&scratch), static_cast<size_t>(rts.bytes), R.stream),
-                 "cudaMallocAsync");
-      cuda_check(cudaMemcpyAsync(scratch, R.host, static_cast<size_t>(rts.bytes), cudaMemcpyHostToDevice, R.stream),
-                 "staged H2D");
-      a.src = scratch;
+  Engine &E = eng();
+  const cudaStream_t s = R.rstream;
+  switch (q.st) {
+  case St::WaitRts: {
+    for (auto it = R.unexpected.begin(); it != R.unexpected.end(); ++it) {
+      if (it->kind != kRTS || (q.src_want >= 0 && it->src != q.src_want) || (q.tag_want >= 0 && it->tag != q.tag_want))
+        continue;
+      const Msg m = *it;
+      R.unexpected.erase(it);
+      q.peer = m.src;
+      q.tag = m.tag;
+      q.method = m.method;
+      q.bytes = m.bytes;
+      q.sreq = static_cast<uint64_t>(m.aux);
+      q.status = RtStatus{m.src, m.tag, m.method, m.bytes};
+      if (m.bytes > q.count * q.ct->size) {
+        q.err = SP_ERR_BUFFER_TOO_SMALL;
+        q.msg = "recv: message truncated (MPI_ERR_TRUNCATE)";
+      } else if (m.bytes > 0 && (q.ct->size == 0 || m.bytes % q.ct->size)) {
+        q.err = SP_ERR_INVALID_ARGUMENT;
+        q.msg = "recv: message is not whole objects";
+      }
+      // DIRECT upgrade: the sender can run the copy kernel, the destination
+      // is device memory and the type has a publishable canonical form
+      if (!q.err && m.offset == 1 && m.method == SP_METHOD_DEVICE && describable(*q.ct) &&
+          range_capable(*q.ct, m.bytes / q.ct->size, q.rbuf, q.rbuf)) {
+        cudaPointerAttributes at{};
+        const bool dev = cudaPointerGetAttributes(&at, q.rbuf) == cudaSuccess && at.type == cudaMemoryTypeDevice;
+        cudaGetLastError();
+        if (dev && E.desc_used != ~0u) q.method = SP_METHOD_DIRECT;
+      }
+      q.st = St::Matched;
+      return true;
     }
-    a.src_bytes = static_cast<uint64_t>(rts.bytes);
-    execute(a);
-    if (scratch) cuda_check(cudaFreeAsync(scratch, R.stream), "cudaFreeAsync");
-    cuda_check(cudaStreamSynchronize(R.stream), "cudaStreamSynchronize(recv)");
+    return false;
   }
+  case St::Matched: {
+    if (q.err) { // release the sender without a transfer; the error surfaces at wait
+      post(q.peer, Msg{kCTS, R.rank, static_cast<int32_t>(q.id), SP_METHOD_DEVICE, 0, 0, static_cast<int64_t>(q.sreq)});
+      q.bytes = 0;
+      q.st = St::Receiving;
+      return true;
+    }
+    int64_t grant = 0;
+    if (q.bytes == 0) {
+      q.region = 0;
+    } else if (q.method == SP_METHOD_DIRECT) {
+      int slot = 0;
+      while (E.desc_used & (1u << slot)) ++slot;
+      Desc &d = R.shm->slots[R.rank].desc[slot];
+      const Committed &c = *q.ct;
+      d.ndims = c.sb.ndims();
+      d.start = c.sb.start;
+      for (int i = 0; i < d.ndims; ++i) {
+        d.counts[i] = c.sb.counts[i];
+        d.strides[i] = c.sb.strides[i];
+      }
+      d.size = c.size;
+      d.extent = c.extent;
+      d.span = c.span;
+      d.count = q.bytes / c.size;
+      d.raw = reinterpret_cast<uint64_t>(q.rbuf);
+      ipc_handle_of(q.rbuf, &d.h, &d.off);
+      E.desc_used |= 1u << slot;
+      q.region = 3;
+      grant = slot;
+    } else if (q.method == SP_METHOD_DEVICE) {
+      if (q.bytes > R.window_bytes) {
+        q.err = SP_ERR_UNSUPPORTED;
+        q.msg = "recv: message larger than the receive window and not deliverable directly";
+        return true; // Matched again: refuses with a zero-byte grant
+      }
+      grant = E.win.take(q.bytes);
+      if (grant < 0) return false; // window busy: grant later
+      q.region = 1;
+    } else {
+      grant = E.host.take(q.bytes);
+      if (grant < 0) return false;
+      q.region = 2;
+    }
+    q.grant = grant;
+    if (q.method == SP_METHOD_STAGED && q.bytes > 0)
+      cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&q.rbuf_stage), static_cast<size_t>(q.bytes), s),
+                 "cudaMallocAsync(staged)");
+    const uint8_t *packed = q.method == SP_METHOD_DEVICE   ? R.window + grant
+                            : q.method == SP_METHOD_STAGED ? q.rbuf_stage
+                                                           : R.host + grant;
+    q.ranged = q.bytes > 0 && q.method != SP_METHOD_DIRECT && range_capable(*q.ct, q.bytes / q.ct->size, q.rbuf, packed);
+    post(q.peer, Msg{kCTS, R.rank, static_cast<int32_t>(q.id), q.method, q.bytes, grant, static_cast<int64_t>(q.sreq)});
+    q.st = St::Receiving;
+    return true;
+  }
+  case St::Receiving: {
+    bool moved = false;
+    Msg m;
+    while (take(kCHUNK, q.peer, q.id, m)) {
+      moved = true;
+      q.expect = m.method;
+      ++q.got;
+      const int64_t lo = m.offset, hi = m.bytes;
+      if (q.bytes == 0 || q.method == SP_METHOD_DIRECT) continue;
+      const int64_t n = q.bytes / q.ct->size;
+      const uint8_t *src = q.method == SP_METHOD_DEVICE ? R.window + q.grant
+                           : q.method == SP_METHOD_STAGED ? q.rbuf_stage
+                                                          : R.host + q.grant;
+      if (q.method == SP_METHOD_STAGED)
+        cuda_check(cudaMemcpyAsync(q.rbuf_stage + lo, R.host + q.grant + lo, static_cast<size_t>(hi - lo),
+                                   cudaMemcpyHostToDevice, s),
+                   "staged H2D");
+      if (q.ranged) {
+        const BatchSpec spec{q.ct.get(), src, static_cast<uint64_t>(q.bytes), n, q.rbuf, q.buf_bytes, 0};
+        range_execute(spec, true, static_cast<uint64_t>(lo), static_cast<uint64_t>(hi), s);
+      } else if (q.got == q.expect) {
+        PackArgs a{};
+        a.ct = q.ct.get();
+        a.src = src;
+        a.src_bytes = static_cast<uint64_t>(q.bytes);
+        a.dst = q.rbuf;
+        a.dst_bytes = q.buf_bytes;
+        a.count = n;
+        a.stream = s;
+        a.opt = sp_pack_options{1, SP_KERNEL_AUTO, 0};
+        a.pack = false;
+        execute(a);
+      }
+    }
+    if (q.expect >= 0 && q.got == q.expect) {
+      if (q.rbuf_stage) {
+        cuda_check(cudaFreeAsync(q.rbuf_stage, s), "cudaFreeAsync(staged)");
+        q.rbuf_stage = nullptr;
+      }
+      q.last = get_event();
+      cuda_check(cudaEventRecord(q.last, s), "cudaEventRecord");
+      q.st = St::Draining;
+      moved = true;
+    }
+    return moved;
+  }
+  case St::Draining: {
+    if (!event_done(q.last)) return false;
+    put_event(q.last);
+    q.last = nullptr;
+    if (q.region == 1) E.win.give(q.grant, q.bytes);
+    if (q.region == 2) E.host.give(q.grant, q.bytes);
+    if (q.region == 3) E.desc_used &= ~(1u << q.grant);
+    q.region = 0;
+    q.st = St::Done;
+    return true;
+  }
+  default:
+    return false;
+  }
+}
+
+} // namespace
+
+// one pass over every active request; requests that finish move to `done`
+void rt_progress() {
+  Engine &E = eng();
+  if (E.in_progress) return;
+  E.in_progress = true;
+  struct Reset {
+    bool &f;
+    ~Reset() { f = false; }
+  } reset{E.in_progress};
+  drain();
+  bool moved = true;
+  while (moved) {
+    moved = false;
+    for (auto it = E.active.begin(); it != E.active.end();) {
+      Req &q = **it;
+      try {
+        moved = (q.send ? step_send(q) : step_recv(q)) || moved;
+      } catch (const Error &e) {
+        q.err = e.code;
+        q.msg = e.msg;
+        q.st = St::Done;
+      }
+      if (q.st == St::Done) {
+        E.done[q.id] = std::move(*it);
+        it = E.active.erase(it);
+        moved = true;
+      } else {
+        ++it;
+      }
+    }
+    if (moved) drain();
+  }
+}
+
+void engine_init(int64_t window_bytes, int64_t host_bytes) {
+  delete g_eng;
+  g_eng = new Engine;
+  g_eng->win.reset(window_bytes);
+  g_eng->host.reset(host_bytes);
+  if (const char *c = std::getenv("TEMPI_CHUNK")) {
+    const int64_t v = std::atoll(c);
+    if (v >= 16 && v % 16 == 0) g_eng->chunk = v;
+  }
+}
+
+void engine_fini() {
+  if (!g_eng) return;
+  for (cudaEvent_t e : g_eng->pool) cudaEventDestroy(e);
+  delete g_eng;
+  g_eng = nullptr;
+}
+
+uint64_t rt_isend(const void *buf, uint64_t buf_bytes, int64_t count, CommitPtr ct, int dest, int tag, int method) {
+  Runtime &R = rt();
+  Engine &E = eng();
+  if (dest < 0 || dest >= R.size) fail(SP_ERR_INVALID_ARGUMENT, "send: bad destination rank");
+  if (tag < 0) fail(SP_ERR_INVALID_ARGUMENT, "send: negative tag");
+  const int64_t bytes = count * ct->size;
+  if (method < 0) {
+    method = rt_choose(*ct, count);
+    if (method == SP_METHOD_DEVICE) method = SP_METHOD_DIRECT; // fused when the receiver can take it
+  }
+  if (method != SP_METHOD_DEVICE && method != SP_METHOD_ONESHOT && method != SP_METHOD_STAGED &&
+      method != SP_METHOD_DIRECT)
+    fail(SP_ERR_INVALID_ARGUMENT, "send: unknown method");
+  if (method == SP_METHOD_DEVICE && bytes > R.shm->slots[dest].window_bytes)
+    fail(SP_ERR_UNSUPPORTED, "send: message larger than the receive window");
+  if (method != SP_METHOD_DEVICE && method != SP_METHOD_DIRECT && bytes > R.shm->slots[dest].host_bytes)
+    fail(SP_ERR_UNSUPPORTED, "send: message larger than the receiver's host region");
+  auto q = std::make_unique<Req>();
+  q->id = E.next_id++;
+  q->send = true;
+  q->sbuf = buf;
+  q->buf_bytes = buf_bytes;
+  q->count = count;
+  q->ct = std::move(ct);
+  q->peer = dest;
+  q->tag = tag;
+  q->method = method;
+  q->bytes = bytes;
+  q->st = St::Start;
+  const uint64_t id = q->id;
+  E.active.push_back(std::move(q));
+  rt_progress();
+  return id;
+}
+
+uint64_t rt_irecv(void *buf, uint64_t buf_bytes, int64_t count, CommitPtr ct, int source, int tag) {
+  Runtime &R = rt();
+  Engine &E = eng();
+  if (source >= R.size) fail(SP_ERR_INVALID_ARGUMENT, "recv: bad source rank");
+  auto q = std::make_unique<Req>();
+  q->id = E.next_id++;
+  q->rbuf = buf;
+  q->buf_bytes = buf_bytes;
+  q->count = count;
+  q->ct = std::move(ct);
+  q->src_want = source;
+  q->tag_want = tag;
+  q->st = St::WaitRts;
+  const uint64_t id = q->id;
+  E.active.push_back(std::move(q));
+  rt_progress();
+  return id;
+}
+
+// completes (and frees) request `id` if it has finished; rethrows its error
+bool rt_test(uint64_t id, RtStatus *st) {
+  Engine &E = eng();
+  rt_progress();
+  auto it = E.done.find(id);
+  if (it == E.done.end()) {
+    bool known = false;
+    for (auto &q : E.active) known = known || q->id == id;
+    if (!known) fail(SP_ERR_INVALID_HANDLE, "unknown request");
+    return false;
+  }
+  std::unique_ptr<Req> q = std::move(it->second);
+  E.done.erase(it);
   if (st) {
-    st->source = rts.src;
-    st->tag = rts.tag;
-    st->bytes = rts.bytes;
-    st->method = rts.method;
+    *st = q->send ? RtStatus{q->peer, q->tag, q->method, q->bytes} : q->status;
+    if (!q->send) st->method = q->method;
   }
+  if (q->err) fail(q->err, q->msg);
+  return true;
+}
+
+void rt_wait(uint64_t id, RtStatus *st) {
+  unsigned spins = 0;
+  while (!rt_test(id, st)) pause_briefly(spins);
+}
+
+void rt_set_chunk(int64_t bytes) {
+  if (bytes < 16 || bytes % 16) fail(SP_ERR_INVALID_ARGUMENT, "chunk size must be a positive multiple of 16");
+  eng().chunk = bytes;
+}
+
+void rt_send(const void *buf, uint64_t buf_bytes, int64_t count, CommitPtr ct, int dest, int tag, int method,
+             RtTrace *trace) {
+  RtStatus st{};
+  rt_wait(rt_isend(buf, buf_bytes, count, std::move(ct), dest, tag, method), &st);
+  if (trace) {
+    trace->method = st.method;
+    trace->bytes = st.bytes;
+  }
+}
+
+void rt_recv(void *buf, uint64_t buf_bytes, int64_t count, CommitPtr ct, int source, int tag, RtStatus *st) {
+  rt_wait(rt_irecv(buf, buf_bytes, count, std::move(ct), source, tag), st);
 }
 
 void rt_set_profile(sp_profile_s *p) {

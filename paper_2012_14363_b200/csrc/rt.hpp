@@ -25,9 +25,16 @@ void rt_barrier();
 void rt_host_send(int dst, int tag, const void *data, int64_t bytes);
 int64_t rt_host_recv(int src, int tag, void *data, int64_t cap);
 void rt_exchange_ptr(void *local, std::vector<uint8_t *> &out);
-void rt_send(const void *buf, uint64_t buf_bytes, int64_t count, const Committed &ct, int dest, int tag, int method,
+void rt_send(const void *buf, uint64_t buf_bytes, int64_t count, CommitPtr ct, int dest, int tag, int method,
              RtTrace *trace);
-void rt_recv(void *buf, uint64_t buf_bytes, int64_t count, const Committed &ct, int source, int tag, RtStatus *st);
+void rt_recv(void *buf, uint64_t buf_bytes, int64_t count, CommitPtr ct, int source, int tag, RtStatus *st);
+// non-blocking point to point: request ids, progressed by every runtime call
+uint64_t rt_isend(const void *buf, uint64_t buf_bytes, int64_t count, CommitPtr ct, int dest, int tag, int method);
+uint64_t rt_irecv(void *buf, uint64_t buf_bytes, int64_t count, CommitPtr ct, int source, int tag);
+bool rt_test(uint64_t req, RtStatus *st); // true (and the request is freed) once complete
+void rt_wait(uint64_t req, RtStatus *st);
+void rt_progress();
+void rt_set_chunk(int64_t bytes);
 void rt_set_profile(sp_profile_s *p);
 int rt_choose(const Committed &ct, int64_t count);
 void *rt_stream();

@@ -39,6 +39,8 @@ struct State {
   std::unordered_map<int, Comm> comms;
   int next_comm = 100;
   int forced_method = -1;
+  std::unordered_map<int, sp_request> requests; // MPI_Request -> engine request
+  int next_request = 1;
   sp_profile profile = nullptr;
   cudaStream_t stream = nullptr;
   std::mutex mu;
@@ -420,6 +422,122 @@ int MPI_Recv(void *buf, int count, MPI_Datatype datatype, int source, int tag, M
   return PMPI_Recv(buf, count, datatype, source, tag, comm, status);
 }
 
+// ------------------------------------------------------------ non-blocking
+static int isend_impl(const void *buf, int count, MPI_Datatype datatype, int dest, int tag, MPI_Comm comm,
+                      int method, MPI_Request *request) {
+  if (!request) return MPI_ERR_ARG;
+  *request = MPI_REQUEST_NULL;
+  if (!comm_of(comm)) return MPI_ERR_COMM;
+  if (dest == MPI_PROC_NULL) return MPI_SUCCESS;
+  if (dest < 0 || dest >= S().size) return MPI_ERR_RANK;
+  if (tag < 0) return MPI_ERR_TAG;
+  if (count < 0) return MPI_ERR_COUNT;
+  TYPE(datatype, h);
+  sp_request r = 0;
+  TRY(sp_rt_isend(buf, UINT64_MAX, count, h, dest, tag, method, &r));
+  std::lock_guard<std::mutex> lk(S().mu);
+  const int id = S().next_request++;
+  S().requests[id] = r;
+  *request = id;
+  return MPI_SUCCESS;
+}
+
+int PMPI_Isend(const void *buf, int count, MPI_Datatype datatype, int dest, int tag, MPI_Comm comm,
+               MPI_Request *request) {
+  return isend_impl(buf, count, datatype, dest, tag, comm, SP_METHOD_DEVICE, request);
+}
+
+int MPI_Isend(const void *buf, int count, MPI_Datatype datatype, int dest, int tag, MPI_Comm comm,
+              MPI_Request *request) {
+  return isend_impl(buf, count, datatype, dest, tag, comm, S().forced_method, request);
+}
+
+int PMPI_Irecv(void *buf, int count, MPI_Datatype datatype, int source, int tag, MPI_Comm comm,
+               MPI_Request *request) {
+  if (!request) return MPI_ERR_ARG;
+  *request = MPI_REQUEST_NULL;
+  if (!comm_of(comm)) return MPI_ERR_COMM;
+  if (source == MPI_PROC_NULL) return MPI_SUCCESS;
+  if (count < 0) return MPI_ERR_COUNT;
+  TYPE(datatype, h);
+  sp_request r = 0;
+  TRY(sp_rt_irecv(buf, UINT64_MAX, count, h, source, tag, &r));
+  std::lock_guard<std::mutex> lk(S().mu);
+  const int id = S().next_request++;
+  S().requests[id] = r;
+  *request = id;
+  return MPI_SUCCESS;
+}
+
+int MPI_Irecv(void *buf, int count, MPI_Datatype datatype, int source, int tag, MPI_Comm comm,
+              MPI_Request *request) {
+  return PMPI_Irecv(buf, count, datatype, source, tag, comm, request);
+}
+
+static int complete(MPI_Request *request, MPI_Status *status, bool block, int *flag) {
+  if (!request) return MPI_ERR_ARG;
+  if (*request == MPI_REQUEST_NULL) { // null or PROC_NULL request: empty status
+    if (status) *status = MPI_Status{MPI_ANY_SOURCE, MPI_ANY_TAG, MPI_SUCCESS, 0, 0};
+    if (flag) *flag = 1;
+    return MPI_SUCCESS;
+  }
+  sp_request r = 0;
+  {
+    std::lock_guard<std::mutex> lk(S().mu);
+    auto it = S().requests.find(*request);
+    if (it == S().requests.end()) return MPI_ERR_ARG;
+    r = it->second;
+  }
+  int64_t st[4] = {0, 0, 0, 0};
+  int done = 1;
+  sp_status rc = block ? sp_rt_wait(r, st) : sp_rt_test(r, &done, st);
+  if (flag) *flag = done;
+  if (!done && rc == SP_OK) return MPI_SUCCESS;
+  {
+    std::lock_guard<std::mutex> lk(S().mu);
+    S().requests.erase(*request);
+  }
+  *request = MPI_REQUEST_NULL;
+  TRY(rc);
+  if (status) *status = MPI_Status{static_cast<int>(st[0]), static_cast<int>(st[1]), MPI_SUCCESS,
+                                   static_cast<int>(st[3]), st[2]};
+  return MPI_SUCCESS;
+}
+
+int PMPI_Wait(MPI_Request *request, MPI_Status *status) { return complete(request, status, true, nullptr); }
+int MPI_Wait(MPI_Request *request, MPI_Status *status) { return PMPI_Wait(request, status); }
+
+int MPI_Test(MPI_Request *request, int *flag, MPI_Status *status) {
+  if (!flag) return MPI_ERR_ARG;
+  return complete(request, status, false, flag);
+}
+
+int MPI_Waitall(int count, MPI_Request requests[], MPI_Status statuses[]) {
+  if (count < 0 || (count && !requests)) return MPI_ERR_ARG;
+  int first_err = MPI_SUCCESS;
+  for (int i = 0; i < count; ++i) {
+    const int rc = complete(&requests[i], statuses ? &statuses[i] : nullptr, true, nullptr);
+    if (rc != MPI_SUCCESS && first_err == MPI_SUCCESS) first_err = rc;
+  }
+  return first_err;
+}
+
+int MPI_Sendrecv(const void *sendbuf, int sendcount, MPI_Datatype sendtype, int dest, int sendtag, void *recvbuf,
+                 int recvcount, MPI_Datatype recvtype, int source, int recvtag, MPI_Comm comm,
+                 MPI_Status *status) {
+  MPI_Request r[2] = {MPI_REQUEST_NULL, MPI_REQUEST_NULL};
+  int rc = MPI_Irecv(recvbuf, recvcount, recvtype, source, recvtag, comm, &r[0]);
+  if (rc != MPI_SUCCESS) return rc;
+  rc = MPI_Isend(sendbuf, sendcount, sendtype, dest, sendtag, comm, &r[1]);
+  if (rc != MPI_SUCCESS) {
+    MPI_Wait(&r[0], MPI_STATUS_IGNORE);
+    return rc;
+  }
+  const int rc1 = MPI_Wait(&r[1], MPI_STATUS_IGNORE);
+  const int rc0 = MPI_Wait(&r[0], status);
+  return rc0 != MPI_SUCCESS ? rc0 : rc1;
+}
+
 // ============================================================ topologies
 int MPI_Dist_graph_create_adjacent(MPI_Comm comm_old, int indegree, const int sources[], const int *,
                                    int outdegree, const int destinations[], const int *, int, int,
@@ -572,7 +690,7 @@ int MPI_Neighbor_alltoallv(const void *sendbuf, const int sendcounts[], const in
 
 // ============================================================ TEMPI controls
 int TEMPI_Set_method(int method) {
-  if (method < -1 || method > 2) return MPI_ERR_ARG;
+  if (method < -1 || method > 3) return MPI_ERR_ARG;
   S().forced_method = method;
   return MPI_SUCCESS;
 }

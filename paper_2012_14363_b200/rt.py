@@ -10,7 +10,7 @@ import os
 from . import _buffer, _check, _capi
 from ._capi import lib
 
-DEVICE, ONESHOT, STAGED = 1, 0, 2
+DEVICE, ONESHOT, STAGED, DIRECT = 1, 0, 2, 3
 AUTO = -1
 
 
@@ -82,6 +82,58 @@ def recv(buf, count: int, ct, source: int = -1, tag: int = -1):
     st = (C.c_int64 * 4)()
     _check(lib.sp_rt_recv(a, n, count, ct.handle, source, tag, st))
     return {"source": st[0], "tag": st[1], "bytes": st[2], "method": st[3]}
+
+
+def _status(st):
+    return {"source": st[0], "tag": st[1], "bytes": st[2], "method": st[3]}
+
+
+class Request:
+    """MPI_Request of sp_rt_isend / sp_rt_irecv; keeps its buffer alive."""
+
+    def __init__(self, handle: int, keep):
+        self.handle = handle
+        self._keep = keep
+        self.status = None
+
+    def test(self) -> bool:
+        if self.status is not None:
+            return True
+        done = C.c_int()
+        st = (C.c_int64 * 4)()
+        _check(lib.sp_rt_test(self.handle, C.byref(done), st))
+        if done.value:
+            self.status = _status(st)
+        return bool(done.value)
+
+    def wait(self):
+        if self.status is None:
+            st = (C.c_int64 * 4)()
+            _check(lib.sp_rt_wait(self.handle, st))
+            self.status = _status(st)
+        return self.status
+
+
+def isend(buf, count: int, ct, dest: int, tag: int = 0, method: int = AUTO) -> Request:
+    a, n, _ = _buffer(buf, False)
+    h = C.c_uint64()
+    _check(lib.sp_rt_isend(a, n, count, ct.handle, dest, tag, method, C.byref(h)))
+    return Request(h.value, (buf, ct))
+
+
+def irecv(buf, count: int, ct, source: int = -1, tag: int = -1) -> Request:
+    a, n, _ = _buffer(buf, True)
+    h = C.c_uint64()
+    _check(lib.sp_rt_irecv(a, n, count, ct.handle, source, tag, C.byref(h)))
+    return Request(h.value, (buf, ct))
+
+
+def waitall(reqs):
+    return [r.wait() for r in reqs]
+
+
+def set_chunk(nbytes: int):
+    _check(lib.sp_rt_set_chunk(nbytes))
 
 
 class HaloPlan:

@@ -49,7 +49,7 @@ int main(int argc, char **argv) {
   }
   /* Send/Recv, every method, ring of two */
   if (size >= 2) {
-    for (int m = -1; m <= 2; ++m) {
+    for (int m = -1; m <= 3; ++m) {
       CHECK(TEMPI_Set_method(m) == MPI_SUCCESS);
       if (rank == 0) {
         for (long i = 0; i < N; ++i) h[i] = pat(i, m + 2);

@@ -52,6 +52,17 @@ def test_mpi_pack_and_sendrecv(cuda, tmp_path, np_):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("np_", [1, 2, 3])
+def test_mpi_nonblocking_ring(cuda, tmp_path, np_):
+    """MPI_Isend/Irecv/Test/Waitall/Sendrecv, every method, chunked messages"""
+    os.environ["TEMPI_CHUNK"] = str(64 << 10)  # pipeline the 600-960 KiB messages in 64 KiB chunks
+    try:
+        assert "OK" in run(np_, build(tmp_path, "mpi_isend"))
+    finally:
+        del os.environ["TEMPI_CHUNK"]
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("grid", [(1, 1, 1), (2, 1, 1), (2, 2, 1), (2, 2, 2)])
 def test_mpi_halo_exchange(cuda, tmp_path, grid):
     exe = build(tmp_path, "mpi_halo")

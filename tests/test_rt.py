@@ -113,6 +113,126 @@ def test_sendrecv_every_method_two_processes(cuda):
     assert res[0][3] == res[1][3]  # the model's choice, seen identically on both sides
 
 
+def _nonblocking(rank, world, job):
+    """rank 0 posts every message before rank 1 posts a single receive
+    (receives posted in reverse tag order): forced methods, DIRECT, chunked
+    pipelining with a 64 KiB chunk, multi-object counts, a pageable host
+    source, a zero-byte message, and a truncated receive"""
+    import torch
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.rt as rt
+    from oracle.pyoracle import oracle
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=16 << 20, host_bytes=16 << 20)
+    rt.set_chunk(64 << 10)
+    progs = [[4, 3, 0, 128, 64, 16, 64, 32, 8, 16, 8, 4, 0, 0],        # 3D subarray, 16 KiB
+             [4, 3, 0, 512, 96, 40, 96, 80, 36, 3, 5, 2, 0, 0],        # 276 KiB, odd start
+             [2, 4096, 1, 9, 0, 3],                                   # 32 KiB vector of doubles
+             [3, 700, 3, 1000, 0, 0]]                                 # hvector of 3-byte blocks
+    plan = [(0, rt.DEVICE, 1), (1, rt.DEVICE, 2), (1, rt.STAGED, 1), (1, rt.ONESHOT, 2), (1, rt.DIRECT, 1),
+            (0, rt.DIRECT, 3), (2, rt.AUTO, 2), (3, rt.STAGED, 4), (3, rt.DIRECT, 2), (2, rt.ONESHOT, 1)]
+    types = [sp.commit_type(sp.from_program(p)) for p in progs]
+    orc = oracle()
+    used = []
+    if rank == 0:
+        reqs = []
+        for tag, (ti, method, count) in enumerate(plan):
+            ct = types[ti]
+            span = (count - 1) * ct.extent + ct.span
+            host = np.random.default_rng(tag).integers(0, 256, span, dtype=np.uint8)
+            src = torch.from_numpy(host) if tag == 9 else torch.from_numpy(host).cuda()  # tag 9: pageable
+            reqs.append(rt.isend(src, count, ct, 1, tag=tag, method=method))
+        zero = rt.isend(torch.zeros(16, dtype=torch.uint8, device="cuda"), 0, types[0], 1, tag=50)
+        trunc = rt.isend(torch.zeros(types[2].span * 2, dtype=torch.uint8, device="cuda"), 2, types[2], 1, tag=60)
+        used = [r["method"] for r in rt.waitall(reqs)]
+        zero.wait()
+        trunc.wait()
+    else:
+        reqs = {}
+        bufs = {}
+        for tag in reversed(range(len(plan))):
+            ti, method, count = plan[tag]
+            ct = types[ti]
+            span = (count - 1) * ct.extent + ct.span
+            bufs[tag] = torch.full((span,), 0x77, dtype=torch.uint8, device="cuda")
+            reqs[tag] = rt.irecv(bufs[tag], count, ct, source=0, tag=tag)
+        for tag in range(len(plan)):
+            ti, method, count = plan[tag]
+            st = reqs[tag].wait()
+            ct = types[ti]
+            span = (count - 1) * ct.extent + ct.span
+            host = np.random.default_rng(tag).integers(0, 256, span, dtype=np.uint8)
+            packed = np.zeros(count * ct.size, np.uint8)
+            assert orc.pack(progs[ti], host, count, packed, 0)[0] == 0
+            want = np.full(span, 0x77, np.uint8)
+            assert orc.unpack(progs[ti], packed, 0, count, want)[0] == 0
+            assert np.array_equal(bufs[tag].cpu().numpy(), want), (tag, st)
+            assert st["bytes"] == count * ct.size and st["tag"] == tag
+            used.append(st["method"])
+        z = rt.irecv(torch.zeros(16, dtype=torch.uint8, device="cuda"), 1, types[0], source=0, tag=50)
+        assert z.wait()["bytes"] == 0
+        t = rt.irecv(torch.zeros(types[2].span, dtype=torch.uint8, device="cuda"), 1, types[2], source=0, tag=60)
+        try:
+            t.wait()
+            raise AssertionError("truncation not reported")
+        except sp.BufferTooSmall:
+            pass
+    rt.finalize()
+    return used
+
+
+@pytest.mark.gpu
+def test_nonblocking_pipelined_and_direct(cuda):
+    res = _spawn(_nonblocking, 2)
+    # both sides agree on the method each message used
+    assert res[0] == res[1]
+    m = res[0]
+    assert m[0] == 1 and m[1] == 1 and m[2] == 2 and m[3] == 0  # forced DEVICE / STAGED / ONESHOT
+    assert m[4] == 3 and m[5] == 3 and m[8] == 3               # DIRECT into device buffers
+    assert m[9] == 0
+
+
+def _ring(rank, world, job):
+    """every rank sends to its right and receives from its left at once"""
+    import torch
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.rt as rt
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=8 << 20, host_bytes=8 << 20)
+    rt.set_chunk(32 << 10)
+    ct = sp.commit_type(sp.from_program([4, 3, 0, 256, 64, 32, 128, 40, 20, 64, 8, 6, 0, 0]))
+    right, left = (rank + 1) % world, (rank - 1) % world
+    ok = True
+    for it, method in enumerate([rt.DEVICE, rt.DIRECT, rt.STAGED, rt.ONESHOT, rt.AUTO]):
+        src = torch.full((ct.span,), rank * 16 + it, dtype=torch.uint8, device="cuda")
+        dst = torch.zeros(ct.span, dtype=torch.uint8, device="cuda")
+        torch.cuda.synchronize()  # MPI semantics: buffers are ready when the call is made
+        r = rt.irecv(dst, 1, ct, source=left, tag=it)
+        s = rt.isend(src, 1, ct, right, tag=it, method=method)
+        s.wait()
+        r.wait()
+        want = torch.zeros(ct.span, dtype=torch.uint8, device="cuda")
+        full = torch.full((ct.span,), left * 16 + it, dtype=torch.uint8, device="cuda")
+        sp.unpack(*_packed(sp, ct, full), 0, ct, 1, want)
+        ok = ok and bool(torch.equal(dst, want))
+        assert ok, (it, method)
+    rt.finalize()
+    return ok
+
+
+def _packed(sp, ct, full):
+    import torch
+    p = torch.empty(ct.size, dtype=torch.uint8, device="cuda")
+    sp.pack(full, ct, 1, p, 0)
+    torch.cuda.synchronize()
+    return (p,)
+
+
+@pytest.mark.gpu
+def test_nonblocking_ring_three_processes(cuda):
+    assert all(_spawn(_ring, 3).values())
+
+
 def _halo(rank, world, job, ranks, method):
     import torch
     import paper_2012_14363_b200.halo as H

@@ -62,13 +62,28 @@ def halo_section(torch, rank, world, local, job, iters=20, warmup=5, nccl=True):
     torch.cuda.synchronize()
     MAX = dist.ReduceOp.MAX if world > 1 else None
 
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    sink = torch.empty(1, dtype=torch.int64, device="cuda")
+
+    def cold(i):
+        # 512 MiB written then read back: every timed exchange starts on a
+        # cold, clean L2 (the halo's 51 MB would otherwise stay L2-resident
+        # between iterations, which a stencil sweep in between would not allow)
+        flush.fill_(i & 0xFF)
+        torch.sum(flush.view(torch.int64), dim=0, out=sink[0])
+        torch.cuda.synchronize()
+
     def run(method):
         H.fill(cfg, rank, alloc)
         torch.cuda.synchronize()
         plan = rt.HaloPlan(cfg, alloc, method)
-        for _ in range(warmup):
+        for i in range(warmup):
+            cold(i)
             plan.exchange()
-        ts = [plan.exchange() for _ in range(iters)]
+        ts = []
+        for i in range(iters):
+            cold(i)
+            ts.append(plan.exchange())
         bad = H.verify(cfg, rank, alloc)
         plan.free()
         ph = {k: _reduce(torch, world, statistics.median(t[k] for t in ts), MAX) for k in ts[0]}
@@ -80,6 +95,7 @@ def halo_section(torch, rank, world, local, job, iters=20, warmup=5, nccl=True):
     bad = max(bad, bad_sync, bad_direct)
     rbytes = remote_bytes(cfg, regions, rank)
     out = {"grid": list(grid), "interior": 256, "radius": 2, "element_bytes": 32,
+           "l2": "flushed (512 MiB write + read) before every exchange",
            "bytes_per_rank": seg[-1], "remote_bytes_per_rank": rbytes, "verified": bad == 0,
            "direct_us": {"copy": round(phase_direct["pack"] * 1e6, 2),
                          "wait": round(phase_direct["unpack"] * 1e6, 2),
@@ -90,12 +106,12 @@ def halo_section(torch, rank, world, local, job, iters=20, warmup=5, nccl=True):
            "fused_hbm_GBps_per_rank": round(4 * seg[-1] / phase["iteration"] / 1e9, 1),
            "nvlink_bound_us": round(rbytes / (NVLINK_MEASURED_GBPS * 1e9) * 1e6, 2)}
     if nccl and world > 1 and dist.is_initialized() and dist.get_backend() == "nccl":
-        out["nccl"] = _nccl_halo(torch, cfg, regions, seg, alloc, rank, world, iters, warmup)
+        out["nccl"] = _nccl_halo(torch, cfg, regions, seg, alloc, rank, world, iters, warmup, cold)
     rt.finalize()
     return out
 
 
-def _nccl_halo(torch, cfg, regions, seg, alloc, rank, world, iters, warmup):
+def _nccl_halo(torch, cfg, regions, seg, alloc, rank, world, iters, warmup, cold):
     """baseline: batch pack -> 26 NCCL send/recv in one group -> batch unpack"""
     import paper_2012_14363_b200.halo as H
     import torch.distributed as dist
@@ -113,6 +129,7 @@ def _nccl_halo(torch, cfg, regions, seg, alloc, rank, world, iters, warmup):
     s = torch.cuda.current_stream()
     times = []
     for it in range(warmup + iters):
+        cold(it)
         dist.barrier()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         ev[0].record(s)
@@ -166,7 +183,7 @@ def send_section(torch, rank, world, local, job, reps=10, warmup=3):
             buf = torch.zeros(ct.span, dtype=torch.uint8, device="cuda")
             row = {"E0": e0, "bytes": ct.size}
             for name, m in (("device", rt.DEVICE), ("oneshot", rt.ONESHOT), ("staged", rt.STAGED),
-                            ("model", rt.AUTO)):
+                            ("direct", rt.DIRECT), ("model", rt.AUTO)):
                 ts, used = [], None
                 for it in range(warmup + reps):
                     rt.barrier()
@@ -184,7 +201,7 @@ def send_section(torch, rank, world, local, job, reps=10, warmup=3):
                     row[name + "_us"] = round(statistics.median(ts) * 1e6, 2)
                     row[name + "_GBps"] = round(ct.size / statistics.median(ts) / 1e9, 2)
                     if name == "model":
-                        row["model_choice"] = {0: "oneshot", 1: "device", 2: "staged"}[used]
+                        row["model_choice"] = {0: "oneshot", 1: "device", 2: "staged", 3: "direct"}[used]
             rows.append(row)
     rt.finalize()
     return {"pair": [0, 1], "timing": "half ping-pong wall time (host-synchronous MPI_Send/Recv semantics)",
