@@ -149,6 +149,13 @@ int MPI_Neighbor_alltoallv(const void *sendbuf, const int sendcounts[], const in
                            MPI_Datatype sendtype, void *recvbuf, const int recvcounts[], const int rdispls[],
                            MPI_Datatype recvtype, MPI_Comm comm);
 
+/* per-neighbour datatypes on both sides, byte displacements (accelerated:
+ * one typed-copy launch per rank stores every block at its final strided
+ * place in the receiver's buffer over NVLink) */
+int MPI_Neighbor_alltoallw(const void *sendbuf, const int sendcounts[], const MPI_Aint sdispls[],
+                           const MPI_Datatype sendtypes[], void *recvbuf, const int recvcounts[],
+                           const MPI_Aint rdispls[], const MPI_Datatype recvtypes[], MPI_Comm comm);
+
 /* profiling interface: the base implementations under the interposer */
 int PMPI_Init(int *argc, char ***argv);
 int PMPI_Finalize(void);
@@ -171,6 +178,9 @@ int PMPI_Wait(MPI_Request *request, MPI_Status *status);
 int PMPI_Neighbor_alltoallv(const void *sendbuf, const int sendcounts[], const int sdispls[],
                             MPI_Datatype sendtype, void *recvbuf, const int recvcounts[], const int rdispls[],
                             MPI_Datatype recvtype, MPI_Comm comm);
+int PMPI_Neighbor_alltoallw(const void *sendbuf, const int sendcounts[], const MPI_Aint sdispls[],
+                            const MPI_Datatype sendtypes[], void *recvbuf, const int recvcounts[],
+                            const MPI_Aint rdispls[], const MPI_Datatype recvtypes[], MPI_Comm comm);
 
 /* TEMPI-specific controls (not MPI): force a transfer method for MPI_Send /
  * MPI_Isend (-1 = model-selected, the default; 0 one-shot, 1 device, 2

@@ -393,6 +393,23 @@ sp_status sp_rt_neighbor_alltoallv(const void *sendbuf,
                                    void *recvbuf, const int64_t *recvcounts,
                                    const int64_t *rdispls, int64_t indegree,
                                    const int *sources, sp_type recvtype);
+/* MPI_Neighbor_alltoallw (collective): per-edge datatypes on both sides and
+ * BYTE displacements. Each rank publishes, per in-edge, its receive buffer
+ * and the canonical geometry of recvtypes[j]; block i (sendcounts[i]
+ * objects of sendtypes[i] at sendbuf + sdispls[i]) is then stored by ONE
+ * typed-copy launch per rank straight to its strided place in the
+ * receiver's buffer (recvbuf + rdispls[j], recvtypes[j]) -- no packed
+ * intermediate, no unpack. Send and receive of an edge must describe the
+ * same byte count; receive types need a strided non-overlapping form. */
+sp_status sp_rt_neighbor_alltoallw(const void *sendbuf,
+                                   const int64_t *sendcounts,
+                                   const int64_t *sdispls,
+                                   const sp_type *sendtypes, int64_t outdegree,
+                                   const int *dests, void *recvbuf,
+                                   const int64_t *recvcounts,
+                                   const int64_t *rdispls,
+                                   const sp_type *recvtypes, int64_t indegree,
+                                   const int *sources);
 
 /* distributed halo exchange: one rank per process (grid size == runtime
  * size); `alloc` is this rank's padded allocation on its device. */

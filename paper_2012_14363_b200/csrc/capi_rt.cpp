@@ -215,6 +215,26 @@ sp_status sp_rt_neighbor_alltoallv(const void *sendbuf, const int64_t *sendcount
   });
 }
 
+sp_status sp_rt_neighbor_alltoallw(const void *sendbuf, const int64_t *sendcounts, const int64_t *sdispls,
+                                   const sp_type *sendtypes, int64_t outdegree, const int *dests, void *recvbuf,
+                                   const int64_t *recvcounts, const int64_t *rdispls, const sp_type *recvtypes,
+                                   int64_t indegree, const int *sources) {
+  return guarded([&] {
+    if (outdegree < 0 || indegree < 0) fail(SP_ERR_INVALID_ARGUMENT, "negative degree");
+    if ((outdegree && (!sendcounts || !sdispls || !sendtypes || !dests)) ||
+        (indegree && (!recvcounts || !rdispls || !recvtypes || !sources)))
+      fail(SP_ERR_INVALID_ARGUMENT, "null neighbour arrays");
+    std::vector<int64_t> sc(sendcounts, sendcounts + outdegree), sd(sdispls, sdispls + outdegree);
+    std::vector<int64_t> rc(recvcounts, recvcounts + indegree), rd(rdispls, rdispls + indegree);
+    std::vector<int> ds(dests, dests + outdegree), ss(sources, sources + indegree);
+    std::vector<CommitPtr> st, rtp;
+    for (int64_t i = 0; i < outdegree; ++i) st.push_back(committed_of(sendtypes[i]));
+    for (int64_t j = 0; j < indegree; ++j) rtp.push_back(committed_of(recvtypes[j]));
+    rt_neighbor_alltoallw(static_cast<const uint8_t *>(sendbuf), sc, sd, st, static_cast<uint8_t *>(recvbuf), rc, rd,
+                          rtp, ss, ds);
+  });
+}
+
 sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int method, sp_halo_plan *out) {
   return guarded([&] {
     need(cfgp);

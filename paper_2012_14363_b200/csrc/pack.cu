@@ -931,49 +931,94 @@ template <int W> __device__ __forceinline__ int64_t word_offset(uint32_t q, cons
   return row_offset(row, g) + static_cast<int64_t>(q - row * g.wpr) * W;
 }
 
+// Geometry of up to 3 row dims held in registers: the common case (halo
+// regions, cfg1-cfg4 objects) computes every word offset from registers,
+// so a thread's U loads issue back to back instead of each waiting on
+// descriptor reads.
+constexpr int kRegDims = 3;
+struct RegGeom {
+  uint32_t wpr, c0, c1;
+  FastDiv wdiv, d0, d1;
+  int64_t s0, s1, s2;
+  int nd;
+};
+
+__device__ __forceinline__ RegGeom reg_geom(const Geom &g) {
+  RegGeom r;
+  r.nd = g.nd;
+  r.wpr = g.wpr;
+  r.wdiv = g.wdiv;
+  r.c0 = g.cnt[0];
+  r.c1 = g.cnt[1];
+  r.d0 = g.div[0];
+  r.d1 = g.div[1];
+  r.s0 = g.str[0];
+  r.s1 = g.str[1];
+  r.s2 = g.str[2];
+  return r;
+}
+
+template <int W> __device__ __forceinline__ int64_t reg_offset(uint32_t q, const RegGeom &r) {
+  const uint32_t row = fdiv(q, r.wdiv);
+  int64_t off = static_cast<int64_t>(q - row * r.wpr) * W;
+  if (r.nd <= 1) return r.nd == 1 ? off + static_cast<int64_t>(row) * r.s0 : off;
+  const uint32_t q1 = fdiv(row, r.d0);
+  off += static_cast<int64_t>(row - q1 * r.c0) * r.s0;
+  if (r.nd == 2) return off + static_cast<int64_t>(q1) * r.s1;
+  const uint32_t q2 = fdiv(q1, r.d1);
+  return off + static_cast<int64_t>(q1 - q2 * r.c1) * r.s1 + static_cast<int64_t>(q2) * r.s2;
+}
+
+template <int MODE> __device__ __forceinline__ bool reg_ok(const BatchJob &J) {
+  const bool src_ok = MODE == kModeUnpack || J.gs.nd <= kRegDims;
+  const bool dst_ok = MODE == kModePack || (MODE == kModeCopy && J.same) || J.gd.nd <= kRegDims;
+  return src_ok && dst_ok;
+}
+
+// words [lo, hi) of the launch, all inside job J (offsets from registers)
 template <int W, int MODE>
-__device__ __forceinline__ void batch_body(const BatchJob *__restrict__ jobs, int njobs, uint32_t total,
-                                           uint32_t per_block, const BatchSig &sig) {
+__device__ __forceinline__ void move_single(const BatchJob &J, uint32_t lo, uint32_t hi) {
   using T = typename Word<W>::T;
-  if (sig.n_pre && blockIdx.x == 0 && threadIdx.x < static_cast<unsigned>(sig.n_pre))
-    st_release_sys(sig.pre[threadIdx.x], sig.pre_value);
-  if (sig.n_wait) {
-    if (threadIdx.x < static_cast<unsigned>(sig.n_wait))
-      while (ld_acquire_sys(sig.wait[threadIdx.x]) < sig.wait_value) __nanosleep(64);
-    __syncthreads();
-  }
-  const uint32_t lo = blockIdx.x * per_block;
-  const uint32_t hi = min(total, lo + per_block);
-  // jobs of this block's range: [j0, j1]; up to kJobSlots of them are
-  // staged in shared memory so the per-word index math reads on-chip
-  // descriptors (a range spanning more, e.g. many halo corners, reads the
-  // descriptors from global memory through L1)
-  __shared__ BatchJob sjob[kJobSlots];
-  auto last_le = [&](uint32_t q) {
-    int a = 0, b = njobs - 1;
-    while (a < b) {
-      const int m = (a + b + 1) >> 1;
-      if (jobs[m].begin <= q) {
-        a = m;
-      } else {
-        b = m - 1;
+  RegGeom gs{}, gd{};
+  if (MODE != kModeUnpack) gs = reg_geom(J.gs);
+  const bool same = MODE == kModeCopy && J.same;
+  if (MODE == kModeUnpack || (MODE == kModeCopy && !same)) gd = reg_geom(J.gd);
+  const uint8_t *in = J.in;
+  uint8_t *out = J.out;
+  const uint32_t shift = J.q0 - static_cast<uint32_t>(J.begin);
+  for (uint32_t base = lo + threadIdx.x; base < hi; base += 256 * kBatchU) {
+    T v[kBatchU];
+    int64_t doff[kBatchU];
+#pragma unroll
+    for (int u = 0; u < kBatchU; ++u) {
+      const uint32_t q = base + u * 256;
+      if (q < hi) {
+        const uint32_t ql = q + shift;
+        if (MODE == kModeUnpack) {
+          v[u] = ld_stream(reinterpret_cast<const T *>(in) + ql);
+          doff[u] = reg_offset<W>(ql, gd);
+        } else {
+          const int64_t so = reg_offset<W>(ql, gs);
+          v[u] = ld_stream(reinterpret_cast<const T *>(in + so));
+          if (MODE == kModePack) {
+            doff[u] = static_cast<int64_t>(ql) * W;
+          } else {
+            doff[u] = same ? so : reg_offset<W>(ql, gd);
+          }
+        }
       }
     }
-    return a;
-  };
-  const int j0 = lo < hi ? last_le(lo) : 0;
-  const int j1 = lo < hi ? last_le(hi - 1) : 0;
-  const int nj = j1 - j0 + 1;
-  const bool staged = nj <= kJobSlots;
-  if (staged) {
-    const uint32_t *src = reinterpret_cast<const uint32_t *>(jobs + j0);
-    uint32_t *dst = reinterpret_cast<uint32_t *>(sjob);
-    const uint32_t words = static_cast<uint32_t>(nj * sizeof(BatchJob) / 4);
-    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+#pragma unroll
+    for (int u = 0; u < kBatchU; ++u)
+      if (base + u * 256 < hi) st_stream(reinterpret_cast<T *>(out + doff[u]), v[u]);
   }
-  __syncthreads();
-  const BatchJob *JB = staged ? sjob : jobs + j0;
-  const int nlocal = staged ? nj : njobs - j0;
+}
+
+// words [lo, hi) spanning several jobs, or deeper geometry: descriptors
+// read per word (JB: nlocal jobs starting at the one holding lo)
+template <int W, int MODE>
+__device__ __forceinline__ void move_multi(const BatchJob *JB, int nlocal, uint32_t lo, uint32_t hi) {
+  using T = typename Word<W>::T;
   for (uint32_t base = lo + threadIdx.x; base < hi; base += 256 * kBatchU) {
     T v[kBatchU];
     int64_t doff[kBatchU];
@@ -1006,6 +1051,19 @@ __device__ __forceinline__ void batch_body(const BatchJob *__restrict__ jobs, in
     for (int u = 0; u < kBatchU; ++u)
       if (jw[u] >= 0) st_stream(reinterpret_cast<T *>(JB[jw[u]].out + doff[u]), v[u]);
   }
+}
+
+__device__ __forceinline__ void batch_prologue(const BatchSig &sig) {
+  if (sig.n_pre && blockIdx.x == 0 && threadIdx.x < static_cast<unsigned>(sig.n_pre))
+    st_release_sys(sig.pre[threadIdx.x], sig.pre_value);
+  if (sig.n_wait) {
+    if (threadIdx.x < static_cast<unsigned>(sig.n_wait))
+      while (ld_acquire_sys(sig.wait[threadIdx.x]) < sig.wait_value) __nanosleep(64);
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void batch_epilogue(const BatchSig &sig) {
   if (sig.n_signal) {
     // bar.sync orders every thread's stores before thread 0 (CTA scope);
     // thread 0's fence is cumulative over them: GPU scope when every
@@ -1030,7 +1088,44 @@ __device__ __forceinline__ void batch_body(const BatchJob *__restrict__ jobs, in
 template <int W, int MODE>
 __global__ void __launch_bounds__(256) k_batch(const BatchJob *__restrict__ jobs, int njobs, uint32_t total,
                                                uint32_t per_block, const BatchSig sig) {
-  batch_body<W, MODE>(jobs, njobs, total, per_block, sig);
+  batch_prologue(sig);
+  const uint32_t lo = blockIdx.x * per_block;
+  const uint32_t hi = min(total, lo + per_block);
+  // jobs of this block's range: [j0, j1]; up to kJobSlots of them are
+  // staged in shared memory (a range spanning more, e.g. many halo corners,
+  // reads the descriptors from global memory through L1)
+  __shared__ BatchJob sjob[kJobSlots];
+  auto last_le = [&](uint32_t q) {
+    int a = 0, b = njobs - 1;
+    while (a < b) {
+      const int m = (a + b + 1) >> 1;
+      if (jobs[m].begin <= q) {
+        a = m;
+      } else {
+        b = m - 1;
+      }
+    }
+    return a;
+  };
+  const int j0 = lo < hi ? last_le(lo) : 0;
+  const int j1 = lo < hi ? last_le(hi - 1) : 0;
+  const int nj = j1 - j0 + 1;
+  const bool staged = nj <= kJobSlots;
+  if (staged) {
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(jobs + j0);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(sjob);
+    const uint32_t words = static_cast<uint32_t>(nj * sizeof(BatchJob) / 4);
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  if (lo < hi) {
+    if (nj == 1 && reg_ok<MODE>(sjob[0])) {
+      move_single<W, MODE>(sjob[0], lo, hi);
+    } else {
+      move_multi<W, MODE>(staged ? sjob : jobs + j0, staged ? nj : njobs - j0, lo, hi);
+    }
+  }
+  batch_epilogue(sig);
 }
 
 // one job passed by value (param space): a single message or message chunk
@@ -1038,8 +1133,14 @@ __global__ void __launch_bounds__(256) k_batch(const BatchJob *__restrict__ jobs
 template <int W, int MODE>
 __global__ void __launch_bounds__(256) k_job(const __grid_constant__ BatchJob job, uint32_t total,
                                              uint32_t per_block) {
-  const BatchSig none{};
-  batch_body<W, MODE>(&job, 1, total, per_block, none);
+  const uint32_t lo = blockIdx.x * per_block;
+  const uint32_t hi = min(total, lo + per_block);
+  if (lo >= hi) return;
+  if (reg_ok<MODE>(job)) {
+    move_single<W, MODE>(job, lo, hi);
+  } else {
+    move_multi<W, MODE>(&job, 1, lo, hi);
+  }
 }
 
 struct BatchGroup {

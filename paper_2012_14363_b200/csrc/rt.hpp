@@ -43,4 +43,10 @@ void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &s
                            const std::vector<int64_t> &recv_counts, const std::vector<int64_t> &recv_displs,
                            const Committed &rtp, const std::vector<int> &sources, const std::vector<int> &dests);
 
+void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &send_counts,
+                           const std::vector<int64_t> &send_displs, const std::vector<CommitPtr> &send_types,
+                           uint8_t *recvbuf, const std::vector<int64_t> &recv_counts,
+                           const std::vector<int64_t> &recv_displs, const std::vector<CommitPtr> &recv_types,
+                           const std::vector<int> &sources, const std::vector<int> &dests);
+
 } // namespace spb

@@ -688,6 +688,43 @@ int MPI_Neighbor_alltoallv(const void *sendbuf, const int sendcounts[], const in
                                  comm);
 }
 
+int PMPI_Neighbor_alltoallw(const void *sendbuf, const int sendcounts[], const MPI_Aint sdispls[],
+                            const MPI_Datatype sendtypes[], void *recvbuf, const int recvcounts[],
+                            const MPI_Aint rdispls[], const MPI_Datatype recvtypes[], MPI_Comm comm) {
+  const Comm *c = comm_of(comm);
+  if (!c || c->kind == 0) return MPI_ERR_COMM;
+  std::vector<int> src, dst;
+  std::vector<int64_t> scount, sdisp, rcount, rdisp;
+  std::vector<sp_type> st, rt;
+  for (size_t i = 0; i < c->dests.size(); ++i)
+    if (c->dests[i] != MPI_PROC_NULL) {
+      TYPE(sendtypes[i], h);
+      dst.push_back(c->dests[i]);
+      scount.push_back(sendcounts[i]);
+      sdisp.push_back(sdispls[i]);
+      st.push_back(h);
+    }
+  for (size_t j = 0; j < c->sources.size(); ++j)
+    if (c->sources[j] != MPI_PROC_NULL) {
+      TYPE(recvtypes[j], h);
+      src.push_back(c->sources[j]);
+      rcount.push_back(recvcounts[j]);
+      rdisp.push_back(rdispls[j]);
+      rt.push_back(h);
+    }
+  TRY(sp_rt_neighbor_alltoallw(sendbuf, scount.data(), sdisp.data(), st.data(), static_cast<int64_t>(dst.size()),
+                               dst.data(), recvbuf, rcount.data(), rdisp.data(), rt.data(),
+                               static_cast<int64_t>(src.size()), src.data()));
+  return MPI_SUCCESS;
+}
+
+int MPI_Neighbor_alltoallw(const void *sendbuf, const int sendcounts[], const MPI_Aint sdispls[],
+                           const MPI_Datatype sendtypes[], void *recvbuf, const int recvcounts[],
+                           const MPI_Aint rdispls[], const MPI_Datatype recvtypes[], MPI_Comm comm) {
+  return PMPI_Neighbor_alltoallw(sendbuf, sendcounts, sdispls, sendtypes, recvbuf, recvcounts, rdispls, recvtypes,
+                                 comm);
+}
+
 // ============================================================ TEMPI controls
 int TEMPI_Set_method(int method) {
   if (method < -1 || method > 3) return MPI_ERR_ARG;

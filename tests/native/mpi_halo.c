@@ -3,7 +3,11 @@
  * region into one device buffer, MPI_Neighbor_alltoallv over a distributed
  * graph of the 26 neighbours, MPI_Unpack into the ghost shell. Verified
  * with the reference's fill_cell pattern (sp_halo_fill / sp_halo_verify).
- * usage: mpi_halo RX RY RZ N RADIUS ELEM ITERS   (RX*RY*RZ == ranks)
+ * With MODE = 1 the exchange is ONE MPI_Neighbor_alltoallw call on the
+ * padded allocation itself: send types = the interior regions, receive
+ * types = the ghost regions, byte displacements 0 (ghost writes, no packed
+ * buffers).
+ * usage: mpi_halo RX RY RZ N RADIUS ELEM ITERS [MODE]  (RX*RY*RZ == ranks)
  * prints per-phase wall times of the last iteration and "OK". */
 #include <stdio.h>
 #include <stdlib.h>
@@ -25,7 +29,9 @@ int main(int argc, char **argv) {
   MPI_Comm_rank(MPI_COMM_WORLD, &rank);
   MPI_Comm_size(MPI_COMM_WORLD, &size);
   const int R[3] = {atoi(argv[1]), atoi(argv[2]), atoi(argv[3])};
-  const int n = atoi(argv[4]), r = atoi(argv[5]), e = atoi(argv[6]), iters = atoi(argv[7]);
+  const int n = atoi(argv[4]), r = atoi(argv[5]), e = atoi(argv[6]);
+  int iters = atoi(argv[7]);
+  const int mode = argc > 8 ? atoi(argv[8]) : 0;
   CHECK(R[0] * R[1] * R[2] == size);
   const int p = n + 2 * r;
   const long alloc_bytes = (long)p * p * p * e;
@@ -72,6 +78,25 @@ int main(int argc, char **argv) {
   CHECK(sp_halo_fill(&cfg, rank, alloc, NULL) == SP_OK);
   cudaDeviceSynchronize();
   double tp = 0, tx = 0, tu = 0;
+  if (mode == 1) {
+    /* edge i brings the neighbour's region i into my ghost region 25-i */
+    int ones[26];
+    MPI_Aint zeros[26];
+    MPI_Datatype rtypes[26];
+    for (int i = 0; i < 26; ++i) {
+      ones[i] = 1;
+      zeros[i] = 0;
+      rtypes[i] = recv_t[25 - i];
+    }
+    for (int it = 0; it < iters; ++it) {
+      if (it + 1 == iters) CHECK(sp_halo_fill(&cfg, rank, alloc, NULL) == SP_OK && cudaDeviceSynchronize() == cudaSuccess);
+      MPI_Barrier(MPI_COMM_WORLD);
+      const double t0 = MPI_Wtime();
+      CHECK(MPI_Neighbor_alltoallw(alloc, ones, zeros, send_t, alloc, ones, zeros, rtypes, g) == MPI_SUCCESS);
+      tx = MPI_Wtime() - t0;
+    }
+    iters = 0;
+  }
   for (int it = 0; it < iters; ++it) {
     MPI_Barrier(MPI_COMM_WORLD);
     const double t0 = MPI_Wtime();
