@@ -343,6 +343,9 @@ sp_status sp_rt_host_recv(int src, int tag, void *data, int64_t cap,
                           int64_t *bytes);
 /* collective: peers[r] = rank r's `local` device pointer mapped here */
 sp_status sp_rt_exchange_ptr(void *local, void **peers);
+/* the runtime's stream (cudaStream_t) on which sends, batches and halo
+ * plans are enqueued; work the caller orders before them goes here */
+sp_status sp_rt_stream(void **stream);
 /* the send-method model used by sp_rt_send when method < 0 */
 sp_status sp_rt_set_profile(sp_profile p);
 sp_status sp_rt_choose(sp_type t, int64_t count, int *method);

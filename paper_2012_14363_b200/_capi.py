@@ -147,6 +147,7 @@ _sig("sp_rt_barrier", C.c_int)
 _sig("sp_rt_host_send", C.c_int, C.c_int, C.c_int, vp, i64)
 _sig("sp_rt_host_recv", C.c_int, C.c_int, C.c_int, vp, i64, i64p)
 _sig("sp_rt_exchange_ptr", C.c_int, vp, C.POINTER(vp))
+_sig("sp_rt_stream", C.c_int, C.POINTER(vp))
 _sig("sp_rt_set_profile", C.c_int, vp)
 _sig("sp_rt_choose", C.c_int, sp_type, i64, C.POINTER(C.c_int))
 _sig("sp_rt_send", C.c_int, vp, u64, i64, sp_type, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int))

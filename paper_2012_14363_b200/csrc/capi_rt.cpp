@@ -2,6 +2,7 @@
 // and the multi-process halo exchange.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -104,6 +105,13 @@ sp_status sp_rt_host_recv(int src, int tag, void *data, int64_t cap, int64_t *by
 
 sp_status sp_rt_set_profile(sp_profile p) {
   return guarded([&] { rt_set_profile(p); });
+}
+
+sp_status sp_rt_stream(void **stream) {
+  return guarded([&] {
+    need(stream);
+    *stream = rt_stream();
+  });
 }
 
 sp_status sp_rt_exchange_ptr(void *local, void **peers) {
@@ -356,9 +364,9 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
       // everything earlier on the stream has completed), every block waits
       // for FREE=n-1 from its receivers, the regions are stored into the
       // receivers' ghost cells over NVLink, and the last block publishes
-      // READY=n to each receiver; a one-warp kernel then waits for READY=n
-      // from this rank's senders, so later work on the stream sees whole
-      // ghost shells.
+      // READY=n to each receiver and then waits for READY=n from this
+      // rank's senders, so later work on the stream sees whole ghost
+      // shells.
       const int n = rt_size(), me = p->rank;
       const uint64_t it = ++p->iter;
       auto at = [&](uint8_t *base, int kind, int peer) {
@@ -380,11 +388,22 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
       ks.signal_value = it;
       ks.done = p->done;
       ks.sys_scope = p->remote_peers;
+      // the last block, after publishing READY=n, waits for READY=n from
+      // this rank's senders: the launch completes only when the ghost shell
+      // is whole, so no separate wait kernel
+      ks.post = ready;
+      ks.post_value = it;
+      if (const char *x = std::getenv("SPB_HALO_EXPERIMENT")) { // timing study only (breaks ordering)
+        const int bits = std::atoi(x);
+        if (bits & 1) ks.wait.clear();
+        if (bits & 2) ks.pre.clear();
+        if (bits & 4) ks.post.clear();
+        if (bits & 8) ks.signal.clear();
+      }
       cuda_check(cudaEventRecord(p->ev[0], s), "cudaEventRecord");
       batch_execute_signaled(*p->pack, s, ks);
       cuda_check(cudaEventRecord(p->ev[1], s), "cudaEventRecord");
       cuda_check(cudaEventRecord(p->ev[2], s), "cudaEventRecord");
-      flags_wait(ready, it, s);
       cuda_check(cudaEventRecord(p->ev[3], s), "cudaEventRecord");
     } else if (p->method == SP_HALO_FUSED_ASYNC) {
       // device-ordered iteration, signalled from inside the kernels: the

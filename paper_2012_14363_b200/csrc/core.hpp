@@ -197,6 +197,8 @@ struct BatchSignal {
   bool sys_scope = true;              // a destination is on another GPU
   std::vector<uint64_t *> pre;        // (peer) flags set to pre_value BEFORE the wait
   uint64_t pre_value = 0;
+  std::vector<const uint64_t *> post; // local flags the last block waits for after signalling
+  uint64_t post_value = 0;
 };
 // one-warp kernel: waits until every flag reaches value (acquire, system scope)
 void flags_wait(const std::vector<const uint64_t *> &wait, uint64_t value, void *stream);

@@ -880,8 +880,8 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
 // a round a thread finds its job by walking forward from the CTA's first
 // job (ranges rarely cross a job boundary); the job descriptors are read
 // through the read-only path and stay L1-resident.
-constexpr int kBatchU = 4;
-constexpr int kJobSlots = 4; // job descriptors a CTA stages in shared memory
+constexpr int kBatchU = 2;                            // words in flight per thread
+constexpr uint32_t kBatchChunk = 256 * kBatchU;       // words per unit of work
 enum : int { kModeUnpack = 0, kModePack = 1, kModeCopy = 2 };
 
 struct BatchJob {
@@ -913,6 +913,11 @@ struct BatchSig {
   unsigned long long *pre[kMaxSig];
   unsigned long long pre_value;
   int n_pre;
+  // waited for by the LAST block after it signalled (completion of the
+  // peers' writes into this rank's memory folded into the same launch)
+  const unsigned long long *post[kMaxSig];
+  unsigned long long post_value;
+  int n_post;
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
@@ -931,126 +936,35 @@ template <int W> __device__ __forceinline__ int64_t word_offset(uint32_t q, cons
   return row_offset(row, g) + static_cast<int64_t>(q - row * g.wpr) * W;
 }
 
-// Geometry of up to 3 row dims held in registers: the common case (halo
-// regions, cfg1-cfg4 objects) computes every word offset from registers,
-// so a thread's U loads issue back to back instead of each waiting on
-// descriptor reads.
-constexpr int kRegDims = 3;
-struct RegGeom {
-  uint32_t wpr, c0, c1;
-  FastDiv wdiv, d0, d1;
-  int64_t s0, s1, s2;
-  int nd;
-};
-
-__device__ __forceinline__ RegGeom reg_geom(const Geom &g) {
-  RegGeom r;
-  r.nd = g.nd;
-  r.wpr = g.wpr;
-  r.wdiv = g.wdiv;
-  r.c0 = g.cnt[0];
-  r.c1 = g.cnt[1];
-  r.d0 = g.div[0];
-  r.d1 = g.div[1];
-  r.s0 = g.str[0];
-  r.s1 = g.str[1];
-  r.s2 = g.str[2];
-  return r;
-}
-
-template <int W> __device__ __forceinline__ int64_t reg_offset(uint32_t q, const RegGeom &r) {
-  const uint32_t row = fdiv(q, r.wdiv);
-  int64_t off = static_cast<int64_t>(q - row * r.wpr) * W;
-  if (r.nd <= 1) return r.nd == 1 ? off + static_cast<int64_t>(row) * r.s0 : off;
-  const uint32_t q1 = fdiv(row, r.d0);
-  off += static_cast<int64_t>(row - q1 * r.c0) * r.s0;
-  if (r.nd == 2) return off + static_cast<int64_t>(q1) * r.s1;
-  const uint32_t q2 = fdiv(q1, r.d1);
-  return off + static_cast<int64_t>(q1 - q2 * r.c1) * r.s1 + static_cast<int64_t>(q2) * r.s2;
-}
-
-template <int MODE> __device__ __forceinline__ bool reg_ok(const BatchJob &J) {
-  const bool src_ok = MODE == kModeUnpack || J.gs.nd <= kRegDims;
-  const bool dst_ok = MODE == kModePack || (MODE == kModeCopy && J.same) || J.gd.nd <= kRegDims;
-  return src_ok && dst_ok;
-}
-
-// words [lo, hi) of the launch, all inside job J (offsets from registers)
-template <int W, int MODE>
-__device__ __forceinline__ void move_single(const BatchJob &J, uint32_t lo, uint32_t hi) {
+// words of chunk `c` (job-local) of job J: U per thread, all U loads issued
+// before the first store; geometry read from J (shared or param memory)
+template <int W, int MODE> __device__ __forceinline__ void move_chunk(const BatchJob &J, uint32_t c, uint32_t words) {
   using T = typename Word<W>::T;
-  RegGeom gs{}, gd{};
-  if (MODE != kModeUnpack) gs = reg_geom(J.gs);
-  const bool same = MODE == kModeCopy && J.same;
-  if (MODE == kModeUnpack || (MODE == kModeCopy && !same)) gd = reg_geom(J.gd);
-  const uint8_t *in = J.in;
-  uint8_t *out = J.out;
-  const uint32_t shift = J.q0 - static_cast<uint32_t>(J.begin);
-  for (uint32_t base = lo + threadIdx.x; base < hi; base += 256 * kBatchU) {
-    T v[kBatchU];
-    int64_t doff[kBatchU];
+  const uint32_t base = c * kBatchChunk + threadIdx.x;
+  T v[kBatchU];
+  int64_t doff[kBatchU];
 #pragma unroll
-    for (int u = 0; u < kBatchU; ++u) {
-      const uint32_t q = base + u * 256;
-      if (q < hi) {
-        const uint32_t ql = q + shift;
-        if (MODE == kModeUnpack) {
-          v[u] = ld_stream(reinterpret_cast<const T *>(in) + ql);
-          doff[u] = reg_offset<W>(ql, gd);
+  for (int u = 0; u < kBatchU; ++u) {
+    const uint32_t q = base + u * 256;
+    if (q < words) {
+      const uint32_t ql = q + J.q0;
+      if (MODE == kModeUnpack) {
+        v[u] = ld_stream(reinterpret_cast<const T *>(J.in) + ql);
+        doff[u] = word_offset<W>(ql, J.gd);
+      } else {
+        const int64_t so = word_offset<W>(ql, J.gs);
+        v[u] = ld_stream(reinterpret_cast<const T *>(J.in + so));
+        if (MODE == kModePack) {
+          doff[u] = static_cast<int64_t>(ql) * W;
         } else {
-          const int64_t so = reg_offset<W>(ql, gs);
-          v[u] = ld_stream(reinterpret_cast<const T *>(in + so));
-          if (MODE == kModePack) {
-            doff[u] = static_cast<int64_t>(ql) * W;
-          } else {
-            doff[u] = same ? so : reg_offset<W>(ql, gd);
-          }
+          doff[u] = J.same ? so : word_offset<W>(ql, J.gd);
         }
       }
     }
-#pragma unroll
-    for (int u = 0; u < kBatchU; ++u)
-      if (base + u * 256 < hi) st_stream(reinterpret_cast<T *>(out + doff[u]), v[u]);
   }
-}
-
-// words [lo, hi) spanning several jobs, or deeper geometry: descriptors
-// read per word (JB: nlocal jobs starting at the one holding lo)
-template <int W, int MODE>
-__device__ __forceinline__ void move_multi(const BatchJob *JB, int nlocal, uint32_t lo, uint32_t hi) {
-  using T = typename Word<W>::T;
-  for (uint32_t base = lo + threadIdx.x; base < hi; base += 256 * kBatchU) {
-    T v[kBatchU];
-    int64_t doff[kBatchU];
-    int jw[kBatchU];
-    int j = 0;
 #pragma unroll
-    for (int u = 0; u < kBatchU; ++u) {
-      const uint32_t q = base + u * 256;
-      jw[u] = -1;
-      if (q < hi) {
-        while (j + 1 < nlocal && JB[j + 1].begin <= q) ++j;
-        const BatchJob &J = JB[j];
-        const uint32_t ql = q - static_cast<uint32_t>(J.begin) + J.q0;
-        jw[u] = j;
-        if (MODE == kModeUnpack) {
-          v[u] = ld_stream(reinterpret_cast<const T *>(J.in) + ql);
-          doff[u] = word_offset<W>(ql, J.gd);
-        } else {
-          const int64_t so = word_offset<W>(ql, J.gs);
-          v[u] = ld_stream(reinterpret_cast<const T *>(J.in + so));
-          if (MODE == kModePack) {
-            doff[u] = static_cast<int64_t>(ql) * W;
-          } else {
-            doff[u] = J.same ? so : word_offset<W>(ql, J.gd);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kBatchU; ++u)
-      if (jw[u] >= 0) st_stream(reinterpret_cast<T *>(JB[jw[u]].out + doff[u]), v[u]);
-  }
+  for (int u = 0; u < kBatchU; ++u)
+    if (base + u * 256 < words) st_stream(reinterpret_cast<T *>(J.out + doff[u]), v[u]);
 }
 
 __device__ __forceinline__ void batch_prologue(const BatchSig &sig) {
@@ -1077,77 +991,162 @@ __device__ __forceinline__ void batch_epilogue(const BatchSig &sig) {
         __threadfence();
       }
     }
-    if (threadIdx.x == 0 && atomicAdd(sig.done, 1u) == gridDim.x - 1) {
-      __threadfence_system();
-      for (int i = 0; i < sig.n_signal; ++i) st_release_sys(sig.signal[i], sig.signal_value);
-      atomicExch(sig.done, 0u); // ready for the next launch on this stream
+    __shared__ int last;
+    if (threadIdx.x == 0) last = atomicAdd(sig.done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last) {
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int i = 0; i < sig.n_signal; ++i) st_release_sys(sig.signal[i], sig.signal_value);
+        atomicExch(sig.done, 0u); // ready for the next launch on this stream
+      }
+      // every other block of this launch has finished, so waiting here
+      // cannot starve them; the peers publish before they wait, so the
+      // ranks' last blocks cannot wait on each other in a cycle
+      if (threadIdx.x < static_cast<unsigned>(sig.n_post))
+        while (ld_acquire_sys(sig.post[threadIdx.x]) < sig.post_value) __nanosleep(32);
     }
   }
 }
 
+__device__ __forceinline__ uint32_t job_words(const BatchJob &J, int mode) {
+  return static_cast<uint32_t>(mode == kModeUnpack ? J.gd.total : J.gs.total);
+}
+
+// Every chunk (kBatchChunk words of one job) is a unit of work; CTAs walk
+// the chunks grid-stride, so each CTA sees chunks of every job (the slow
+// 64-B-row regions of a halo spread over the whole grid) and the grid stays
+// one resident wave at full occupancy. The chunk's job is found by binary
+// search on the jobs' first-chunk indices and staged in shared memory.
 template <int W, int MODE>
-__global__ void __launch_bounds__(256) k_batch(const BatchJob *__restrict__ jobs, int njobs, uint32_t total,
-                                               uint32_t per_block, const BatchSig sig) {
+__global__ void __launch_bounds__(256) k_batch(const BatchJob *__restrict__ jobs, int njobs, uint32_t nchunks,
+                                               const BatchSig sig) {
   batch_prologue(sig);
-  const uint32_t lo = blockIdx.x * per_block;
-  const uint32_t hi = min(total, lo + per_block);
-  // jobs of this block's range: [j0, j1]; up to kJobSlots of them are
-  // staged in shared memory (a range spanning more, e.g. many halo corners,
-  // reads the descriptors from global memory through L1)
-  __shared__ BatchJob sjob[kJobSlots];
-  auto last_le = [&](uint32_t q) {
+  __shared__ BatchJob sj;
+  int loaded = -1;
+  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
     int a = 0, b = njobs - 1;
     while (a < b) {
       const int m = (a + b + 1) >> 1;
-      if (jobs[m].begin <= q) {
+      if (jobs[m].begin <= c) {
         a = m;
       } else {
         b = m - 1;
       }
     }
-    return a;
-  };
-  const int j0 = lo < hi ? last_le(lo) : 0;
-  const int j1 = lo < hi ? last_le(hi - 1) : 0;
-  const int nj = j1 - j0 + 1;
-  const bool staged = nj <= kJobSlots;
-  if (staged) {
-    const uint32_t *src = reinterpret_cast<const uint32_t *>(jobs + j0);
-    uint32_t *dst = reinterpret_cast<uint32_t *>(sjob);
-    const uint32_t words = static_cast<uint32_t>(nj * sizeof(BatchJob) / 4);
-    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
-  }
-  __syncthreads();
-  if (lo < hi) {
-    if (nj == 1 && reg_ok<MODE>(sjob[0])) {
-      move_single<W, MODE>(sjob[0], lo, hi);
-    } else {
-      move_multi<W, MODE>(staged ? sjob : jobs + j0, staged ? nj : njobs - j0, lo, hi);
+    if (a != loaded) {
+      __syncthreads();
+      const uint32_t *src = reinterpret_cast<const uint32_t *>(jobs + a);
+      uint32_t *dst = reinterpret_cast<uint32_t *>(&sj);
+      for (uint32_t i = threadIdx.x; i < sizeof(BatchJob) / 4; i += blockDim.x) dst[i] = src[i];
+      __syncthreads();
+      loaded = a;
     }
+    move_chunk<W, MODE>(sj, c - static_cast<uint32_t>(sj.begin), job_words(sj, MODE) - sj.q0);
   }
   batch_epilogue(sig);
 }
 
 // one job passed by value (param space): a single message or message chunk
-// launches without uploading a descriptor
+// launches without uploading a descriptor; `words` from q0 on
 template <int W, int MODE>
-__global__ void __launch_bounds__(256) k_job(const __grid_constant__ BatchJob job, uint32_t total,
-                                             uint32_t per_block) {
-  const uint32_t lo = blockIdx.x * per_block;
-  const uint32_t hi = min(total, lo + per_block);
-  if (lo >= hi) return;
-  if (reg_ok<MODE>(job)) {
-    move_single<W, MODE>(job, lo, hi);
-  } else {
-    move_multi<W, MODE>(&job, 1, lo, hi);
+__global__ void __launch_bounds__(256) k_job(const __grid_constant__ BatchJob job, uint32_t words) {
+  const uint32_t nchunks = (words + kBatchChunk - 1) / kBatchChunk;
+  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) move_chunk<W, MODE>(job, c, words);
+}
+
+// ---- compact job tables in kernel-parameter space
+// A batch of up to kParamJobs jobs whose geometries have at most 3 row dims
+// (every halo region, every cfg1-cfg4 object) travels by value: the
+// chunk -> job search and every descriptor read hit the constant cache, so
+// a chunk starts with no dependent global load and no barrier, and word
+// offsets are computed from registers.
+constexpr int kParamJobs = 32;
+struct CGeom {
+  uint32_t wpr, c0, c1;
+  int32_t nd;
+  FastDiv wdiv, d0, d1;
+  int64_t s0, s1, s2;
+  uint32_t total; // words of the job's stream
+  uint32_t pad;
+};
+struct CJob {
+  const uint8_t *in;
+  uint8_t *out;
+  CGeom gs, gd;
+  uint32_t begin; // first chunk
+  uint32_t q0;
+  int32_t same;
+  int32_t pad;
+};
+struct CTable {
+  CJob jobs[kParamJobs];
+  int32_t njobs;
+  uint32_t nchunks;
+};
+
+template <int W> __device__ __forceinline__ int64_t c_offset(uint32_t q, const CGeom &r) {
+  const uint32_t row = fdiv(q, r.wdiv);
+  int64_t off = static_cast<int64_t>(q - row * r.wpr) * W;
+  if (r.nd <= 1) return r.nd == 1 ? off + static_cast<int64_t>(row) * r.s0 : off;
+  const uint32_t q1 = fdiv(row, r.d0);
+  off += static_cast<int64_t>(row - q1 * r.c0) * r.s0;
+  if (r.nd == 2) return off + static_cast<int64_t>(q1) * r.s1;
+  const uint32_t q2 = fdiv(q1, r.d1);
+  return off + static_cast<int64_t>(q1 - q2 * r.c1) * r.s1 + static_cast<int64_t>(q2) * r.s2;
+}
+
+template <int W, int MODE>
+__global__ void __launch_bounds__(256) k_batchp(const __grid_constant__ CTable t, const BatchSig sig) {
+  using T = typename Word<W>::T;
+  batch_prologue(sig);
+  for (uint32_t c = blockIdx.x; c < t.nchunks; c += gridDim.x) {
+    int a = 0, b = t.njobs - 1;
+    while (a < b) {
+      const int m = (a + b + 1) >> 1;
+      if (t.jobs[m].begin <= c) {
+        a = m;
+      } else {
+        b = m - 1;
+      }
+    }
+    const CJob &J = t.jobs[a];
+    const uint32_t words = (MODE == kModeUnpack ? J.gd.total : J.gs.total) - J.q0;
+    const uint32_t base = (c - J.begin) * kBatchChunk + threadIdx.x;
+    T v[kBatchU];
+    int64_t doff[kBatchU];
+#pragma unroll
+    for (int u = 0; u < kBatchU; ++u) {
+      const uint32_t q = base + u * 256;
+      if (q < words) {
+        const uint32_t ql = q + J.q0;
+        if (MODE == kModeUnpack) {
+          v[u] = ld_stream(reinterpret_cast<const T *>(J.in) + ql);
+          doff[u] = c_offset<W>(ql, J.gd);
+        } else {
+          const int64_t so = c_offset<W>(ql, J.gs);
+          v[u] = ld_stream(reinterpret_cast<const T *>(J.in + so));
+          if (MODE == kModePack) {
+            doff[u] = static_cast<int64_t>(ql) * W;
+          } else {
+            doff[u] = J.same ? so : c_offset<W>(ql, J.gd);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kBatchU; ++u)
+      if (base + u * 256 < words) st_stream(reinterpret_cast<T *>(J.out + doff[u]), v[u]);
   }
+  batch_epilogue(sig);
 }
 
 struct BatchGroup {
   int w = 0, mode = 0;
   BatchJob *d_jobs = nullptr;
   int njobs = 0;
-  uint32_t total = 0; // words
+  uint32_t nchunks = 0;
+  std::shared_ptr<CTable> table; // set when the jobs fit kernel-parameter space
 };
 
 struct Batch {
@@ -1209,14 +1208,51 @@ Batch *build_batch(std::vector<BatchJob> (&by_w)[5], int mode, int64_t bytes) {
     BatchGroup g;
     g.w = 1 << wi;
     g.mode = mode;
-    uint64_t words = 0;
+    uint64_t chunks = 0;
     for (BatchJob &j : jobs) {
-      j.begin = words;
-      words += mode == kModeUnpack ? j.gd.total : j.gs.total;
-      if (words >= (1ull << 32)) fail(SP_ERR_UNSUPPORTED, "batch: too much work for one launch");
+      j.begin = chunks; // first chunk of the job
+      chunks += ((mode == kModeUnpack ? j.gd.total : j.gs.total) + kBatchChunk - 1) / kBatchChunk;
+      if (chunks >= (1ull << 32)) fail(SP_ERR_UNSUPPORTED, "batch: too much work for one launch");
     }
     g.njobs = static_cast<int>(jobs.size());
-    g.total = static_cast<uint32_t>(words);
+    g.nchunks = static_cast<uint32_t>(chunks);
+    bool compact = jobs.size() <= static_cast<size_t>(kParamJobs);
+    for (const BatchJob &j : jobs) {
+      const bool needs_s = mode != kModeUnpack, needs_d = mode == kModeUnpack || (mode == kModeCopy && !j.same);
+      compact = compact && (!needs_s || j.gs.nd <= 3) && (!needs_d || j.gd.nd <= 3);
+    }
+    if (compact) {
+      auto t = std::make_shared<CTable>();
+      std::memset(t.get(), 0, sizeof(CTable));
+      auto cg = [](const Geom &g) {
+        CGeom c{};
+        c.nd = g.nd;
+        c.wpr = g.wpr;
+        c.wdiv = g.wdiv;
+        c.c0 = g.cnt[0];
+        c.c1 = g.cnt[1];
+        c.d0 = g.div[0];
+        c.d1 = g.div[1];
+        c.s0 = g.str[0];
+        c.s1 = g.str[1];
+        c.s2 = g.str[2];
+        c.total = static_cast<uint32_t>(g.total);
+        return c;
+      };
+      for (size_t i = 0; i < jobs.size(); ++i) {
+        CJob &c = t->jobs[i];
+        c.in = jobs[i].in;
+        c.out = jobs[i].out;
+        c.gs = cg(jobs[i].gs);
+        c.gd = cg(jobs[i].gd);
+        c.begin = static_cast<uint32_t>(jobs[i].begin);
+        c.q0 = jobs[i].q0;
+        c.same = jobs[i].same;
+      }
+      t->njobs = g.njobs;
+      t->nchunks = g.nchunks;
+      g.table = t;
+    }
     cuda_check(cudaMalloc(&g.d_jobs, jobs.size() * sizeof(BatchJob)), "cudaMalloc(batch)");
     b->groups.push_back(g);
     cuda_check(cudaMemcpy(g.d_jobs, jobs.data(), jobs.size() * sizeof(BatchJob), cudaMemcpyHostToDevice),
@@ -1327,10 +1363,13 @@ template <int W, int MODE> void launch_batch(const BatchGroup &g, const BatchSig
     occ = std::max(occ, 1);
     occ_dev = dev;
   }
-  const uint64_t want = (static_cast<uint64_t>(g.total) + 256ull * kBatchU - 1) / (256ull * kBatchU);
-  grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sm_count()) * occ)));
-  const uint32_t per = static_cast<uint32_t>((static_cast<uint64_t>(g.total) + grid - 1) / grid);
-  k_batch<W, MODE><<<grid, 256, 0, s>>>(g.d_jobs, g.njobs, g.total, per, sig);
+  grid = static_cast<unsigned>(
+      std::max<uint64_t>(1, std::min<uint64_t>(g.nchunks, static_cast<uint64_t>(sm_count()) * occ)));
+  if (g.table) {
+    k_batchp<W, MODE><<<grid, 256, 0, s>>>(*g.table, sig);
+  } else {
+    k_batch<W, MODE><<<grid, 256, 0, s>>>(g.d_jobs, g.njobs, g.nchunks, sig);
+  }
 }
 
 template <int W> void launch_batch_w(const BatchGroup &g, const BatchSig &sig, cudaStream_t s, unsigned &grid) {
@@ -1365,6 +1404,10 @@ void batch_launch(const Batch &b, void *stream, const BatchSignal *bs) {
         sig.signal_value = bs->signal_value;
         sig.done = bs->done;
         sig.sys_scope = bs->sys_scope ? 1 : 0;
+        if (bs->post.size() > static_cast<size_t>(kMaxSig)) fail(SP_ERR_UNSUPPORTED, "batch signalling: more than 32 peers");
+        sig.n_post = static_cast<int>(bs->post.size());
+        for (int i = 0; i < sig.n_post; ++i) sig.post[i] = reinterpret_cast<const unsigned long long *>(bs->post[i]);
+        sig.post_value = bs->post_value;
       }
     }
     unsigned grid = 0;
@@ -1415,12 +1458,11 @@ template <int W, int MODE> void launch_job(const BatchJob &j, uint32_t words, cu
     occ = std::max(occ, 1);
     occ_dev = dev;
   }
-  const uint64_t want = (static_cast<uint64_t>(words) + 256ull * kBatchU - 1) / (256ull * kBatchU);
+  const uint64_t want = (static_cast<uint64_t>(words) + kBatchChunk - 1) / kBatchChunk;
   uint64_t cap = static_cast<uint64_t>(sm_count()) * occ;
   if (t_host_grid_cap) cap = std::min<uint64_t>(cap, t_host_grid_cap);
   const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, cap)));
-  const uint32_t per = static_cast<uint32_t>((static_cast<uint64_t>(words) + grid - 1) / grid);
-  k_job<W, MODE><<<grid, 256, 0, s>>>(j, words, per);
+  k_job<W, MODE><<<grid, 256, 0, s>>>(j, words);
   cuda_check(cudaGetLastError(), "k_job launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
   sp_launch_info li{};

@@ -60,6 +60,13 @@ def exchange_ptr(tensor_or_ptr):
     return [p or 0 for p in peers]
 
 
+def stream() -> int:
+    """cudaStream_t of the runtime (sends, batches, halo plans)"""
+    v = C.c_void_p()
+    _check(lib.sp_rt_stream(C.byref(v)))
+    return v.value or 0
+
+
 def set_profile(profile):
     _check(lib.sp_rt_set_profile(profile.handle if profile is not None else None))
 

@@ -28,8 +28,8 @@ def timed(fn):
     ts = []
     for i in range(reps):
         flush.fill_(i & 0xFF)
-        torch.sum(flush.view(torch.int64), dim=0, out=sink[0])
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.sum(flush.view(torch.int64), dim=0, out=sink[0])  # same stream, not waited for:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)  # no host latency timed
         a.record(s)
         fn()
         b.record(s)
