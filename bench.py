@@ -285,7 +285,8 @@ def run_reference(args):
     return 0
 
 
-def build_line(args, value, step_ms, world, K, dominant, sweep, e2e_val, Ke, launches, clk, cpu, halo, send):
+def build_line(args, value, step_ms, world, K, dominant, sweep, e2e_val, Ke, launches, clk, cpu, halo, send,
+               pcie_ms=None):
     hbm, hbm_kind = peaks()
     ms, e0, tag, gbs, li = dominant
     bytes_per_kernel = 2 * K * (1 << 20)
@@ -325,8 +326,11 @@ def build_line(args, value, step_ms, world, K, dominant, sweep, e2e_val, Ke, lau
                 "d2h_bytes_per_step": Ke * (1 << 20) * len(E0S),
                 "how": f"sp_unpack from / sp_pack to PINNED HOST message buffers through the C-ABI "
                        f"(the engine stages each message over PCIe: H2D + unpack kernel, pack kernel + "
-                       f"D2H); {Ke} objects per E0 as one-object messages interleaved across E0 and dealt "
-                       f"round-robin to 4 streams so transfers and kernels of different messages overlap"},
+                       f"D2H); incount={Ke} per E0 message, one stream per E0 so transfers and kernels of "
+                       f"different messages overlap",
+                "pcie_bound_ms": round(pcie_ms, 3) if pcie_ms else None,
+                "pcie_bound_note": "the same H2D and D2H bytes as plain pinned copies on two streams at once; "
+                                   "e2e ms / this = how far the leg is from the link"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
@@ -461,15 +465,16 @@ def run_ours(args):
     # goes through the public C-ABI with those host pointers: sp_unpack
     # moves a message over PCIe into the device object (the engine's DMA
     # staging: H2D into a per-stream stage buffer, then the kernel) and
-    # sp_pack sends it back (kernel, then D2H). Each E0's Ke objects are
-    # separate one-object messages, interleaved across E0 and dealt
-    # round-robin to NS streams, so PCIe in, kernels and PCIe out of
-    # different messages overlap (PCIe is full duplex) and no stream waits
-    # on another; the long small-E0 kernels no longer stall the pipeline.
+    # sp_pack sends it back (kernel, then D2H). Each E0's message (Ke
+    # objects) has its own stream, so PCIe in, kernels and PCIe out of
+    # different messages overlap (PCIe is full duplex). scripts/e2e_exp.py
+    # measured the alternatives on B200: one-object messages interleaved
+    # over 4-8 streams 2.80 ms, per-E0 messages on 4 streams 2.79 ms, on 10
+    # streams 2.44 ms -- the leg is PCIe-bound (see pcie_bound_ms).
     del src, packed
     torch.cuda.empty_cache()
     Ke = min(K, args.e2e_incount)
-    NS = 4
+    NS = len(E0S)
     xoff, at = {}, 0
     for e0 in sorted(E0S, reverse=True):
         xoff[e0] = at
@@ -479,12 +484,10 @@ def run_ours(args):
     msg_out = [torch.empty(Ke << 20, dtype=torch.uint8).pin_memory() for _ in E0S]
     streams = [torch.cuda.Stream() for _ in range(NS)]
     handles = [C.c_void_p(st.cuda_stream) for st in streams]
-    items = []  # (type, strided object address, packed message offset, E0 index)
-    order = sorted(range(len(types)), key=lambda i: -types[i][0])
-    for j in range(Ke):
-        for i in order:
-            e0, d, ct = types[i]
-            items.append((ct, esrc.data_ptr() + (j << 30) + xoff[e0], j << 20, i))
+    items = []  # (type, strided object address, E0 index)
+    for i in sorted(range(len(types)), key=lambda i: -types[i][0]):
+        e0, d, ct = types[i]
+        items.append((ct, esrc.data_ptr() + xoff[e0], i))
     e2e_t = 0.0
     for it in range(args.warmup + args.steps):
         torch.cuda.synchronize()
@@ -493,15 +496,15 @@ def run_ours(args):
         a.record(streams[0])
         for st in streams[1:]:
             st.wait_event(a)
-        for n, (ct, obj, off, i) in enumerate(items):
+        for n, (ct, obj, i) in enumerate(items):
             h = handles[n % NS]
-            pos.value = off
-            st = lib.sp_unpack(msg_in[i].data_ptr(), msg_in[i].numel(), C.byref(pos), ct.handle, 1, obj,
-                               esrc.numel(), h)
+            pos.value = 0
+            st = lib.sp_unpack(msg_in[i].data_ptr(), msg_in[i].numel(), C.byref(pos), ct.handle, Ke, obj,
+                               esrc.numel() - (obj - esrc.data_ptr()), h)
             assert st == 0, lib.sp_last_error()
-            pos.value = off
-            st = lib.sp_pack(obj, esrc.numel(), ct.handle, 1, msg_out[i].data_ptr(), msg_out[i].numel(),
-                             C.byref(pos), h)
+            pos.value = 0
+            st = lib.sp_pack(obj, esrc.numel() - (obj - esrc.data_ptr()), ct.handle, Ke, msg_out[i].data_ptr(),
+                             msg_out[i].numel(), C.byref(pos), h)
             assert st == 0, lib.sp_last_error()
         for st in streams[1:]:
             ev = torch.cuda.Event()
@@ -511,6 +514,32 @@ def run_ours(args):
         torch.cuda.synchronize()
         if it >= args.warmup:
             e2e_t += a.elapsed_time(b)
+    # PCIe bound of the leg: the same bytes in both directions at once,
+    # plain pinned copies on two streams (no kernels)
+    dev_buf = torch.empty(2 * (Ke << 20) * len(E0S), dtype=torch.uint8, device="cuda")
+    hin = torch.cat(msg_in).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    half = hin.numel()
+    pcie = []
+    for it in range(4):
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(streams[0])
+        streams[1].wait_event(a)
+        with torch.cuda.stream(streams[0]):
+            dev_buf[:half].copy_(hin, non_blocking=True)
+        with torch.cuda.stream(streams[1]):
+            hout.copy_(dev_buf[half:], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(streams[1])
+        streams[0].wait_event(ev)
+        b.record(streams[0])
+        torch.cuda.synchronize()
+        if it:
+            pcie.append(a.elapsed_time(b))
+    pcie_ms = min(pcie)
+    del dev_buf, hin, hout
     e2e_ms = barrier_max(torch, world, e2e_t / args.steps)
     e2e_bytes = 2 * Ke * (1 << 20) * 2 * len(E0S)
     e2e_val = barrier_sum(torch, world, e2e_bytes) / (e2e_ms * 1e-3) / 1e9
@@ -523,7 +552,7 @@ def run_ours(args):
     halo = send = None
     line_box = {}
     if not args.no_halo:
-        from tools.bench_parts import halo_section, send_section
+        from tools.bench_parts import halo_section, send_section, send_self_section
 
         def on_timeout():
             if rank == 0 and "line" in line_box:
@@ -540,7 +569,7 @@ def run_ours(args):
             args.no_cpu_baseline = True
             line_box["cpu"] = cpu_pre
         line_box["line"] = build_line(args, value, step_ms, world, K, dominant, sweep, e2e_val, Ke,
-                                      launches, clk, cpu_pre, None, None)
+                                      launches, clk, cpu_pre, None, None, pcie_ms)
         dog = threading.Timer(args.section_timeout, on_timeout)
         dog.daemon = True
         dog.start()
@@ -549,11 +578,13 @@ def run_ours(args):
             halo = halo_section(torch, rank, world, local, job)
         except Exception as exc:  # recorded, never fatal to the bench line
             halo = {"error": f"{type(exc).__name__}: {exc}"}
-        if world >= 2:
-            try:
+        try:
+            if world >= 2:
                 send = send_section(torch, rank, world, local, job)
-            except Exception as exc:
-                send = {"error": f"{type(exc).__name__}: {exc}"}
+            else:
+                send = send_self_section(torch, rank, local, job)
+        except Exception as exc:
+            send = {"error": f"{type(exc).__name__}: {exc}"}
         dog.cancel()
 
     if rank != 0:
@@ -568,7 +599,7 @@ def run_ours(args):
                "sample": f"{reps} x (pack+unpack of 1 cfg2 object per E0), {t:.1f} s CPU, "
                          "PackOptions.threads=1 (the reference's fastest setting)"}
     line = build_line(args, value, step_ms, world, K, dominant, sweep, e2e_val, Ke, launches, clk, cpu, halo,
-                      send)
+                      send, pcie_ms)
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -393,13 +393,6 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
       // is whole, so no separate wait kernel
       ks.post = ready;
       ks.post_value = it;
-      if (const char *x = std::getenv("SPB_HALO_EXPERIMENT")) { // timing study only (breaks ordering)
-        const int bits = std::atoi(x);
-        if (bits & 1) ks.wait.clear();
-        if (bits & 2) ks.pre.clear();
-        if (bits & 4) ks.post.clear();
-        if (bits & 8) ks.signal.clear();
-      }
       cuda_check(cudaEventRecord(p->ev[0], s), "cudaEventRecord");
       batch_execute_signaled(*p->pack, s, ks);
       cuda_check(cudaEventRecord(p->ev[1], s), "cudaEventRecord");

@@ -212,6 +212,59 @@ def send_section(torch, rank, world, local, job, reps=10, warmup=3):
             "nvlink_peak_GBps": NVLINK_MEASURED_GBPS, "rows": rows}
 
 
+def send_self_section(torch, rank, local, job, reps=7, warmup=2):
+    """Config 4's code path on ONE GPU: rank 0 sends to itself (MPI_Isend +
+    MPI_Irecv + MPI_Wait x2) with every method, 1 KiB - 64 MiB, E0 in
+    {8, 64, 512}. No NVLink is involved: this measures the protocol, the
+    kernels and the HBM traffic of each method (DEVICE = pack to the window +
+    unpack, DIRECT = one typed copy, ONE-SHOT / STAGED over PCIe). Wall time
+    per message, device buffers, L2 flushed before every message."""
+    import time
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.model as M
+    import paper_2012_14363_b200.rt as rt
+    if rank != 0:
+        return None
+    rt.init(0, 1, job + "self", device=local, window_bytes=72 << 20, host_bytes=72 << 20)
+    prof_path = os.path.join(ROOT, "profiles", "b200.profile")
+    if os.path.exists(prof_path):
+        rt.set_profile(M.load_profile_file(prof_path))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    rows = []
+    names = {0: "oneshot", 1: "device", 2: "staged", 3: "direct"}
+    for e0 in (8, 64, 512):
+        for n in [1 << k for k in range(10, 27, 4)]:
+            if n < e0 * 4:
+                continue
+            ct = sp.commit_type(sp.from_program(cfg4_prog(e0, n)))
+            src = torch.ones(ct.span, dtype=torch.uint8, device="cuda")
+            dst = torch.zeros(ct.span, dtype=torch.uint8, device="cuda")
+            row = {"E0": e0, "bytes": ct.size}
+            for name, m in (("device", rt.DEVICE), ("direct", rt.DIRECT), ("oneshot", rt.ONESHOT),
+                            ("staged", rt.STAGED), ("model", rt.AUTO)):
+                ts, used = [], None
+                for it in range(warmup + reps):
+                    flush.fill_(it & 0xFF)
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    r = rt.irecv(dst, 1, ct, source=0, tag=it)
+                    q = rt.isend(src, 1, ct, 0, tag=it, method=m)
+                    q.wait()
+                    used = r.wait()["method"]
+                    if it >= warmup:
+                        ts.append(time.perf_counter() - t0)
+                t = statistics.median(ts)
+                row[name + "_us"] = round(t * 1e6, 2)
+                row[name + "_GBps"] = round(ct.size / t / 1e9, 2)
+                if name == "model":
+                    row["model_choice"] = names[used]
+            rows.append(row)
+    rt.finalize()
+    return {"pair": [0, 0], "timing": "wall time of Isend+Irecv+Wait to self, median; device buffers; "
+                                      "one GPU (no NVLink): protocol + kernels + HBM/PCIe traffic per method",
+            "rows": rows}
+
+
 if __name__ == "__main__":  # one-rank halo section alone: python tools/bench_parts.py
     import json
     import uuid
