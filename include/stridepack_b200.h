@@ -356,8 +356,10 @@ sp_status sp_rt_choose(sp_type t, int64_t count, int *method);
  * D2H, H2D, unpack); DIRECT = the device path where the receiver, when its
  * buffer is device memory, publishes buffer + canonical geometry and the
  * sender runs one typed-copy kernel into it (falls back to DEVICE
- * otherwise). method < 0 = model-selected (Eqs. 1-3; a DEVICE choice runs as
- * DIRECT). Messages above two chunks (sp_rt_set_chunk, default 4 MiB) are
+ * otherwise). method < 0 = model-selected (Eqs. 1-3) with DIRECT offered to
+ * the receiver, the model's choice being the fallback when the receive
+ * buffer is not device memory. Messages above two chunks (sp_rt_set_chunk,
+ * default 4 MiB) are
  * pipelined chunk by chunk. source/tag < 0 match any. status = {source,
  * tag, bytes, method used}. Blocking; the buffers must be device-accessible
  * (or pinned / pageable host memory, staged by the engine). */

@@ -755,9 +755,10 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
       shift_wins(pack, w, rd.c0))
     kernel = SP_KERNEL_SHIFT;
   if (kernel == SP_KERNEL_SHIFT && !shift_ok) fail(SP_ERR_INVALID_ARGUMENT, "shift kernel not applicable");
-  // unpack of long rows: the TMA store path measured 5-9% ahead of the
-  // LDG/STG kernel at c0 >= 128 (profiles/r01_tma_vs_words.txt); pack ties
-  if (kernel == SP_KERNEL_WORDS && opt.kernel == SP_KERNEL_AUTO && !pack && !opt.force_word && rd.c0 >= 128 &&
+  // unpack of rows >= 64 B: the TMA store path measured 6-9% ahead of the
+  // LDG/STG kernel at c0 = 64 and 128 (profiles/r01_tma_vs_words.txt) and
+  // ties above; at 32 B it loses; pack ties or loses everywhere
+  if (kernel == SP_KERNEL_WORDS && opt.kernel == SP_KERNEL_AUTO && !pack && !opt.force_word && rd.c0 >= 64 &&
       g.nd <= 4 && t_host_grid_cap == 0 /* device memory on both sides */) {
     TmaGeometry probe{};
     probe.c0 = rd.c0;

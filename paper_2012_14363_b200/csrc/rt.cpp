@@ -487,6 +487,7 @@ struct Req {
   int64_t count = 0;
   CommitPtr ct;
   int peer = -1, tag = 0, method = 0;
+  bool allow_direct = false;
   int64_t bytes = 0;
   // sender
   uint64_t rreq = 0;
@@ -657,10 +658,12 @@ bool step_send(Req &q) {
   Runtime &R = rt();
   switch (q.st) {
   case St::Start: {
-    // DIRECT travels as a DEVICE request the receiver may upgrade; the
-    // sender can run the copy kernel when its source is device-accessible
-    const bool direct_ok = q.bytes > 0 && q.method == SP_METHOD_DIRECT && range_capable(*q.ct, q.count, q.sbuf, q.sbuf);
-    if (q.method == SP_METHOD_DIRECT) q.method = SP_METHOD_DEVICE;
+    // DIRECT travels as an upgrade offer on the fallback method's request:
+    // the sender can run the copy kernel when its source is
+    // device-accessible, the receiver accepts when its buffer is device
+    // memory, and otherwise the fallback (the model's choice, or DEVICE
+    // for an explicit DIRECT) moves the message
+    const bool direct_ok = q.bytes > 0 && q.allow_direct && range_capable(*q.ct, q.count, q.sbuf, q.sbuf);
     post(q.peer, Msg{kRTS, R.rank, q.tag, q.method, q.bytes, direct_ok ? 1 : 0, static_cast<int64_t>(q.id)});
     q.st = St::WaitCts;
     return true;
@@ -724,7 +727,7 @@ bool step_recv(Req &q) {
       }
       // DIRECT upgrade: the sender can run the copy kernel, the destination
       // is device memory and the type has a publishable canonical form
-      if (!q.err && m.offset == 1 && m.method == SP_METHOD_DEVICE && describable(*q.ct) &&
+      if (!q.err && m.offset == 1 && describable(*q.ct) &&
           range_capable(*q.ct, m.bytes / q.ct->size, q.rbuf, q.rbuf)) {
         cudaPointerAttributes at{};
         const bool dev = cudaPointerGetAttributes(&at, q.rbuf) == cudaSuccess && at.type == cudaMemoryTypeDevice;
@@ -776,6 +779,11 @@ bool step_recv(Req &q) {
       if (grant < 0) return false; // window busy: grant later
       q.region = 1;
     } else {
+      if (q.bytes > R.host_bytes) {
+        q.err = SP_ERR_UNSUPPORTED;
+        q.msg = "recv: message larger than the host region and not deliverable directly";
+        return true; // Matched again: refuses with a zero-byte grant
+      }
       grant = E.host.take(q.bytes);
       if (grant < 0) return false;
       q.region = 2;
@@ -914,16 +922,20 @@ uint64_t rt_isend(const void *buf, uint64_t buf_bytes, int64_t count, CommitPtr 
   if (dest < 0 || dest >= R.size) fail(SP_ERR_INVALID_ARGUMENT, "send: bad destination rank");
   if (tag < 0) fail(SP_ERR_INVALID_ARGUMENT, "send: negative tag");
   const int64_t bytes = count * ct->size;
-  if (method < 0) {
-    method = rt_choose(*ct, count);
-    if (method == SP_METHOD_DEVICE) method = SP_METHOD_DIRECT; // fused when the receiver can take it
-  }
-  if (method != SP_METHOD_DEVICE && method != SP_METHOD_ONESHOT && method != SP_METHOD_STAGED &&
-      method != SP_METHOD_DIRECT)
+  // model-selected messages (method < 0) and explicit DIRECT offer the
+  // fused copy to the receiver; the model's choice (DEVICE for an explicit
+  // DIRECT) is the fallback when the receive buffer is not device memory.
+  // On B200 the fused copy wins at every size measured (one kernel, no
+  // window, no unpack; bench.py `send`), which the paper's three-term
+  // model cannot express.
+  bool allow_direct = method < 0 || method == SP_METHOD_DIRECT;
+  if (method < 0) method = rt_choose(*ct, count);
+  if (method == SP_METHOD_DIRECT) method = SP_METHOD_DEVICE;
+  if (method != SP_METHOD_DEVICE && method != SP_METHOD_ONESHOT && method != SP_METHOD_STAGED)
     fail(SP_ERR_INVALID_ARGUMENT, "send: unknown method");
-  if (method == SP_METHOD_DEVICE && bytes > R.shm->slots[dest].window_bytes)
+  if (!allow_direct && method == SP_METHOD_DEVICE && bytes > R.shm->slots[dest].window_bytes)
     fail(SP_ERR_UNSUPPORTED, "send: message larger than the receive window");
-  if (method != SP_METHOD_DEVICE && method != SP_METHOD_DIRECT && bytes > R.shm->slots[dest].host_bytes)
+  if (!allow_direct && method != SP_METHOD_DEVICE && bytes > R.shm->slots[dest].host_bytes)
     fail(SP_ERR_UNSUPPORTED, "send: message larger than the receiver's host region");
   auto q = std::make_unique<Req>();
   q->id = E.next_id++;
@@ -935,6 +947,7 @@ uint64_t rt_isend(const void *buf, uint64_t buf_bytes, int64_t count, CommitPtr 
   q->peer = dest;
   q->tag = tag;
   q->method = method;
+  q->allow_direct = allow_direct;
   q->bytes = bytes;
   q->st = St::Start;
   const uint64_t id = q->id;
