@@ -1,3 +1,4 @@
+# ncu evidence: bench launch list + full captures of the halo batch kernels (copied to profiles/ by hand)
 set -o pipefail
 mkdir -p gpurun_out
 timeout 900 python bench.py 2>gpurun_out/bench.err | tee gpurun_out/bench.json

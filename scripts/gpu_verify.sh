@@ -1,3 +1,4 @@
+# round-end style verification on one B200: GPU tests, smoke, bench, reference arm
 # Full verification on one B200: GPU tests, smoke, default bench, reference arm.
 set -o pipefail
 mkdir -p gpurun_out

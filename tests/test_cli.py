@@ -327,3 +327,36 @@ def test_profile_gen_emits_loadable_profile(tf, cuda, sp):  # test_cli.cpp:275-2
     assert run("profile-gen", "--out", out)[0] == 0  # overwrite
     M.load_profile_file(out)
     assert p is not None
+
+
+def test_flatten_matches_oracle_on_corpus(sp, orc, corpus):
+    """sp_type_flatten (the CLI's `flatten`) == the oracle's normalized block
+    list (block_list.hpp:44-61 over :67-121) on reference-corpus definitions
+    small enough to enumerate"""
+    n = 0
+    for e in corpus:
+        r = e["ref"]
+        if r["status"] != 0 or r["size"] > (1 << 16):
+            continue
+        st, blocks, overlap = orc.flatten(e["prog"])
+        assert st == 0
+        got = sp.flatten(sp.from_program(e["prog"]))
+        assert [(b.offset, b.length) for b in got.blocks] == blocks, e["prog"]
+        assert got.overlap == overlap
+        n += 1
+    assert n > 300
+
+
+def test_flatten_matches_live_reference(sp, ref):
+    """against the reference compiled in place, on a fresh corpus"""
+    progs = ref.corpus(0xF1A7, 200, 0)
+    n = 0
+    for prog in progs:
+        st, blocks, overlap = ref.flatten(prog)
+        if st != 0 or sum(l for _, l in blocks) > (1 << 16):
+            continue
+        got = sp.flatten(sp.from_program(prog))
+        assert [(b.offset, b.length) for b in got.blocks] == blocks, prog
+        assert got.overlap == overlap
+        n += 1
+    assert n > 50
