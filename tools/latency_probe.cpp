@@ -1,0 +1,93 @@
+// tools/latency_probe.cpp -- host-side cost of the pieces of a small
+// message on this node (median of 2000 calls each): the CUDA runtime calls
+// the engine makes per message, an sp_pack of a small type, and a complete
+// self-send (sp_rt_isend + sp_rt_irecv + waits) for each method.
+//   latency_probe            (one B200; prints one line per probe)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <vector>
+
+#include "stridepack_b200.h"
+
+template <class F> static double med_us(F &&f, int reps = 2000) {
+  for (int i = 0; i < 50; ++i) f();
+  std::vector<double> t;
+  for (int i = 0; i < reps; ++i) {
+    const auto a = std::chrono::steady_clock::now();
+    f();
+    t.push_back(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - a).count());
+  }
+  std::sort(t.begin(), t.end());
+  return t[t.size() / 2];
+}
+
+__global__ void k_empty() {}
+
+#define CK(x)                                                                                                  \
+  do {                                                                                                         \
+    if ((x) != 0) {                                                                                            \
+      std::printf("%s failed: %s\n", #x, sp_last_error());                                                     \
+      return 1;                                                                                                \
+    }                                                                                                          \
+  } while (0)
+
+int main() {
+  cudaSetDevice(0);
+  cudaStream_t s;
+  cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  uint8_t *d = nullptr, *d2 = nullptr;
+  cudaMalloc(&d, 1 << 20);
+  cudaMalloc(&d2, 1 << 20);
+  cudaPointerAttributes at{};
+  std::printf("cudaPointerGetAttributes   %8.2f us\n", med_us([&] { cudaPointerGetAttributes(&at, d + 64); }));
+  cudaIpcMemHandle_t h;
+  std::printf("cudaIpcGetMemHandle        %8.2f us\n", med_us([&] { cudaIpcGetMemHandle(&h, d); }));
+  cudaEvent_t ev;
+  cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  std::printf("launch empty + sync        %8.2f us\n", med_us([&] {
+                k_empty<<<1, 32, 0, s>>>();
+                cudaStreamSynchronize(s);
+              }));
+  std::printf("launch + event poll        %8.2f us\n", med_us([&] {
+                k_empty<<<1, 32, 0, s>>>();
+                cudaEventRecord(ev, s);
+                while (cudaEventQuery(ev) == cudaErrorNotReady) {
+                }
+              }));
+  sp_type byte, row, t;
+  CK(sp_type_named(SP_BYTE, &byte));
+  CK(sp_type_contiguous(64, byte, &row));
+  CK(sp_type_hvector(16, 1, 1024, row, &t)); // 1 KiB of 64-B rows
+  CK(sp_type_commit(t));
+  int64_t pos = 0;
+  std::printf("sp_pack 1 KiB (enqueue)    %8.2f us\n", med_us([&] {
+                pos = 0;
+                sp_pack(d, 1 << 20, t, 1, d2, 1 << 20, &pos, s);
+              }));
+  cudaStreamSynchronize(s);
+  std::printf("sp_pack 1 KiB + sync       %8.2f us\n", med_us([&] {
+                pos = 0;
+                sp_pack(d, 1 << 20, t, 1, d2, 1 << 20, &pos, s);
+                cudaStreamSynchronize(s);
+              }));
+  CK(sp_rt_init(0, 1, "latprobe", 0, 8 << 20, 8 << 20));
+  for (int m : {SP_METHOD_DIRECT, SP_METHOD_DEVICE, SP_METHOD_ONESHOT, SP_METHOD_STAGED}) {
+    int tag = 0;
+    const double us = med_us(
+        [&] {
+          sp_request r, q;
+          sp_rt_irecv(d2, 1 << 20, 1, t, 0, tag, &r);
+          sp_rt_isend(d, 1 << 20, 1, t, 0, tag, m, &q);
+          sp_rt_wait(q, nullptr);
+          sp_rt_wait(r, nullptr);
+          ++tag;
+        },
+        500);
+    std::printf("self send 1 KiB method %d   %8.2f us\n", m, us);
+  }
+  CK(sp_rt_finalize());
+  return 0;
+}
