@@ -979,7 +979,7 @@ __device__ __forceinline__ void batch_prologue(const BatchSig &sig) {
 }
 
 __device__ __forceinline__ void batch_epilogue(const BatchSig &sig) {
-  if (sig.n_signal) {
+  if (sig.n_signal || sig.n_post) {
     // bar.sync orders every thread's stores before thread 0 (CTA scope);
     // thread 0's fence is cumulative over them: GPU scope when every
     // destination is on this device, system scope when some were written

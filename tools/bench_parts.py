@@ -28,6 +28,16 @@ NVLINK_GBPS = 900.0          # per direction per GPU, nominal
 NVLINK_MEASURED_GBPS = 770.0  # peer copy per direction (B200_PROFILING.md)
 
 
+def _hbm_peak():
+    """measured HBM copy bandwidth (MEASURED_PEAKS.json), else the recipe's fallback"""
+    import json
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f).get("hbm_gbs", 6650.0))
+    return 6650.0
+
+
 def remote_bytes(cfg, regions, rank):
     """bytes this rank sends to OTHER ranks (NVLink traffic)"""
     import paper_2012_14363_b200.halo as H
@@ -101,10 +111,13 @@ def halo_section(torch, rank, world, local, job, iters=20, warmup=5, nccl=True):
     out = {"grid": list(grid), "interior": 256, "radius": 2, "element_bytes": 32,
            "l2": "flushed (512 MiB write + read, enqueued on the plan's stream) before every exchange",
            "bytes_per_rank": seg[-1], "remote_bytes_per_rank": rbytes, "verified": bad == 0,
-           "direct_us": {"copy": round(phase_direct["pack"] * 1e6, 2),
-                         "wait": round(phase_direct["unpack"] * 1e6, 2),
-                         "iteration": round(phase_direct["iteration"] * 1e6, 2)},
+           "direct_us": {"iteration": round(phase_direct["iteration"] * 1e6, 2),
+                         "how": "one typed-copy launch per rank writes every ghost region in place "
+                                "(in-kernel completion flags to remote neighbours)"},
            "direct_hbm_GBps_per_rank": round(2 * seg[-1] / phase_direct["iteration"] / 1e9, 1),
+           "direct_hbm_frac": round(2 * seg[-1] / phase_direct["iteration"] / 1e9 / _hbm_peak(), 3),
+           "direct_frac_of_nvlink_bound": (round(rbytes / (NVLINK_MEASURED_GBPS * 1e9) / phase_direct["iteration"], 3)
+                                           if rbytes else None),
            "fused_us": {k: round(v * 1e6, 2) for k, v in phase.items()},
            "fused_hostsync_us": {k: round(v * 1e6, 2) for k, v in phase_sync.items()},
            "fused_hbm_GBps_per_rank": round(4 * seg[-1] / phase["iteration"] / 1e9, 1),
