@@ -216,6 +216,10 @@ typedef struct {
   sp_type dst_type;
   int64_t dst_count;
 } sp_copy_job;
+/* one typed copy, one launch, no descriptor upload (the job travels as a
+ * kernel parameter): MPI_Sendrecv of two datatypes within one process, or
+ * a send to self. Buffers: device, pinned or peer-mapped memory. */
+sp_status sp_copy(const sp_copy_job *job, void *stream);
 sp_status sp_copy_batch_create(const sp_copy_job *jobs, int64_t n,
                                sp_batch *out);
 /* payload bytes one execution moves */

@@ -446,6 +446,20 @@ def unpack(src, position: int, ct: CommittedType, outcount: int, dst, *,
     return pos.value
 
 
+def copy(src, src_ct: CommittedType, src_count: int, dst, dst_ct: CommittedType, dst_count: int, *,
+         stream=None, sync: bool = False) -> None:
+    """Typed copy (sp_copy): byte k of src_count objects of src_ct in pack
+    order lands on byte k of dst_count objects of dst_ct in unpack order --
+    pack.hpp:99 fused with pack.hpp:143, one kernel, no packed buffer."""
+    sa, sn, sc = _buffer(src, False)
+    da, dn, dc = _buffer(dst, True)
+    job = _capi.CopyJob(sa, sn, src_ct.handle, src_count, da, dn, dst_ct.handle, dst_count)
+    s = _stream(stream, sc or dc)
+    _check(lib.sp_copy(C.byref(job), s))
+    if sync:
+        _sync(s)
+
+
 def _sync(stream_handle: int):
     import torch
     if stream_handle:

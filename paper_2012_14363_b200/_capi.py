@@ -114,6 +114,7 @@ class CopyJob(C.Structure):
 
 
 _sig("sp_copy_batch_create", C.c_int, C.POINTER(CopyJob), i64, C.POINTER(vp))
+_sig("sp_copy", C.c_int, C.POINTER(CopyJob), vp)
 _sig("sp_batch_execute", C.c_int, vp, vp)
 _sig("sp_batch_bytes", C.c_int, vp, i64p)
 _sig("sp_batch_free", C.c_int, vp)

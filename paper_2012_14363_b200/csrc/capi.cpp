@@ -229,6 +229,17 @@ sp_status sp_batch_create(const sp_batch_job *jobs, int64_t n, int unpack, sp_ba
   });
 }
 
+sp_status sp_copy(const sp_copy_job *job, void *stream) {
+  return guard([&] {
+    if (!job) spb::fail(SP_ERR_INVALID_ARGUMENT, "null job");
+    const spb::Entry es = spb::registry().get(job->src_type), ed = spb::registry().get(job->dst_type);
+    if (!es.committed || !ed.committed) spb::fail(SP_ERR_INVALID_ARGUMENT, "type is not committed");
+    const spb::CopySpec spec{es.committed.get(), job->src, job->src_bytes, job->src_count, ed.committed.get(),
+                             job->dst, job->dst_bytes, job->dst_count};
+    spb::copy_execute(spec, 0, static_cast<uint64_t>(job->src_count * es.committed->size), stream);
+  });
+}
+
 sp_status sp_copy_batch_create(const sp_copy_job *jobs, int64_t n, sp_batch *out) {
   return guard([&] {
     if (!out || (n > 0 && !jobs) || n < 0) spb::fail(SP_ERR_INVALID_ARGUMENT, "bad batch arguments");

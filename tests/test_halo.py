@@ -234,6 +234,13 @@ def test_copy_batch_counts_and_errors(sp, orc, cuda):
     exp = np.zeros(dst.numel(), np.uint8)
     assert orc.unpack(pb, packed, 0, 4, exp)[0] == 0
     assert np.array_equal(dst.cpu().numpy(), exp)
+    # the same copy as a single by-value launch (sp_copy)
+    dst.zero_()
+    sp.copy(src, a, 4, dst, b, 4, sync=True)
+    assert np.array_equal(dst.cpu().numpy(), exp)
+    assert sp.last_launch().kernel == sp.Kernel.Batch
+    with pytest.raises(sp.InvalidArgument):
+        sp.copy(src, a, 4, dst, b, 3)
     with pytest.raises(sp.InvalidArgument):
         Batch.copies([(src, a, 4, dst, b, 3)])
     ov = sp.commit_type(sp.make_hvector(2, 1, 2, sp.make_contiguous(4, sp.make_named(sp.NamedKind.Byte))))
