@@ -394,7 +394,11 @@ sp_status sp_rt_set_chunk(int64_t bytes);
  * rdispls[j]*extent(recvtype). ONE batch launch per rank packs every block
  * with sendtype straight into the receiving rank's buffer through CUDA IPC.
  * recvtype must be dense bytes (MPI_PACKED/MPI_BYTE-like). The k-th edge to
- * a rank matches that rank's k-th edge from this one. */
+ * a rank matches that rank's k-th edge from this one. No host barrier: a
+ * rank announces each call to its in-neighbours through shared memory,
+ * waits only for its out-neighbours' announcements, and the data kernel
+ * publishes per-pair READY counters to the receivers and waits (last CTA)
+ * for its senders', so the call returns when its own blocks have landed. */
 sp_status sp_rt_neighbor_alltoallv(const void *sendbuf,
                                    const int64_t *sendcounts,
                                    const int64_t *sdispls, int64_t outdegree,

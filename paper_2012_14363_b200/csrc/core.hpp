@@ -199,7 +199,10 @@ struct BatchSignal {
   uint64_t pre_value = 0;
   std::vector<const uint64_t *> post; // local flags the last block waits for after signalling
   uint64_t post_value = 0;
+  std::vector<uint64_t> signal_values, post_values; // per-target values (else the scalars)
 };
+// one-warp kernel: release-stores the signals, then waits for the post flags
+void flags_signal_wait(const BatchSignal &sig, void *stream);
 // one-warp kernel: waits until every flag reaches value (acquire, system scope)
 void flags_wait(const std::vector<const uint64_t *> &wait, uint64_t value, void *stream);
 void batch_execute_signaled(const Batch &b, void *stream, const BatchSignal &sig);

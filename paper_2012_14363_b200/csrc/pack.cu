@@ -919,6 +919,10 @@ struct BatchSig {
   const unsigned long long *post[kMaxSig];
   unsigned long long post_value;
   int n_post;
+  // per-target values (neighbour collectives count calls per peer pair);
+  // used instead of signal_value / post_value when per_target is set
+  unsigned long long signal_vals[kMaxSig], post_vals[kMaxSig];
+  int per_target;
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
@@ -998,14 +1002,17 @@ __device__ __forceinline__ void batch_epilogue(const BatchSig &sig) {
     if (last) {
       if (threadIdx.x == 0) {
         __threadfence_system();
-        for (int i = 0; i < sig.n_signal; ++i) st_release_sys(sig.signal[i], sig.signal_value);
+        for (int i = 0; i < sig.n_signal; ++i)
+          st_release_sys(sig.signal[i], sig.per_target ? sig.signal_vals[i] : sig.signal_value);
         atomicExch(sig.done, 0u); // ready for the next launch on this stream
       }
       // every other block of this launch has finished, so waiting here
       // cannot starve them; the peers publish before they wait, so the
       // ranks' last blocks cannot wait on each other in a cycle
       if (threadIdx.x < static_cast<unsigned>(sig.n_post))
-        while (ld_acquire_sys(sig.post[threadIdx.x]) < sig.post_value) __nanosleep(32);
+        while (ld_acquire_sys(sig.post[threadIdx.x]) <
+               (sig.per_target ? sig.post_vals[threadIdx.x] : sig.post_value))
+          __nanosleep(32);
     }
   }
 }
@@ -1409,6 +1416,13 @@ void batch_launch(const Batch &b, void *stream, const BatchSignal *bs) {
         sig.n_post = static_cast<int>(bs->post.size());
         for (int i = 0; i < sig.n_post; ++i) sig.post[i] = reinterpret_cast<const unsigned long long *>(bs->post[i]);
         sig.post_value = bs->post_value;
+        if (!bs->signal_values.empty() || !bs->post_values.empty()) {
+          if (bs->signal_values.size() != bs->signal.size() || bs->post_values.size() != bs->post.size())
+            fail(SP_ERR_INTERNAL, "batch signalling: per-target values do not match the targets");
+          sig.per_target = 1;
+          for (int i = 0; i < sig.n_signal; ++i) sig.signal_vals[i] = bs->signal_values[i];
+          for (int i = 0; i < sig.n_post; ++i) sig.post_vals[i] = bs->post_values[i];
+        }
       }
     }
     unsigned grid = 0;
@@ -1529,6 +1543,40 @@ void copy_execute(const CopySpec &spec, uint64_t lo, uint64_t hi, void *stream) 
   int w = 1;
   if (!make_copy_job(spec, range_align(lo, hi, total), j, w)) return;
   launch_range(kModeCopy, w, j, total, lo, hi, static_cast<cudaStream_t>(stream));
+}
+
+// one warp: release-store each signal, then wait for each post flag; the
+// completion protocol of a neighbour call that moves no bytes
+__global__ void k_flag_signal_wait(const BatchSig sig) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int i = 0; i < sig.n_signal; ++i)
+      st_release_sys(sig.signal[i], sig.per_target ? sig.signal_vals[i] : sig.signal_value);
+  }
+  if (threadIdx.x < static_cast<unsigned>(sig.n_post))
+    while (ld_acquire_sys(sig.post[threadIdx.x]) < (sig.per_target ? sig.post_vals[threadIdx.x] : sig.post_value))
+      __nanosleep(32);
+}
+
+void flags_signal_wait(const BatchSignal &bs, void *stream) {
+  if (bs.signal.size() > static_cast<size_t>(kMaxSig) || bs.post.size() > static_cast<size_t>(kMaxSig))
+    fail(SP_ERR_UNSUPPORTED, "flag signalling: more than 32 peers");
+  if (bs.signal.empty() && bs.post.empty()) return;
+  BatchSig sig{};
+  sig.n_signal = static_cast<int>(bs.signal.size());
+  sig.n_post = static_cast<int>(bs.post.size());
+  for (int i = 0; i < sig.n_signal; ++i) sig.signal[i] = reinterpret_cast<unsigned long long *>(bs.signal[i]);
+  for (int i = 0; i < sig.n_post; ++i) sig.post[i] = reinterpret_cast<const unsigned long long *>(bs.post[i]);
+  sig.signal_value = bs.signal_value;
+  sig.post_value = bs.post_value;
+  if (!bs.signal_values.empty() || !bs.post_values.empty()) {
+    sig.per_target = 1;
+    for (int i = 0; i < sig.n_signal; ++i) sig.signal_vals[i] = bs.signal_values[i];
+    for (int i = 0; i < sig.n_post; ++i) sig.post_vals[i] = bs.post_values[i];
+  }
+  k_flag_signal_wait<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(sig);
+  cuda_check(cudaGetLastError(), "k_flag_signal_wait launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void batch_execute(const Batch &b, void *stream) { batch_launch(b, stream, nullptr); }

@@ -89,6 +89,9 @@ struct Slot {
   int64_t edges[kMaxEdges][3];
   Desc desc[kDescs];          // DIRECT destinations granted by this rank
   Desc wdesc[kMaxWEdges];     // MPI_Neighbor_alltoallw in-edge destinations
+  // neighbour collectives: pair_entered[s] = how many calls with s as a
+  // source this rank has entered (its layout for that call is published)
+  std::atomic<uint64_t> pair_entered[kMaxRanks];
 };
 
 struct Shm {
@@ -130,6 +133,13 @@ struct Runtime {
   std::deque<Msg> unexpected;
   cudaStream_t stream = nullptr;  // sends, batches, halo plans
   cudaStream_t rstream = nullptr; // receives (unpack of arriving chunks)
+  // neighbour collectives: per-source READY counters written by the
+  // senders' kernels (IPC-mapped), calls per peer pair, a block counter
+  uint64_t *nbr_flags = nullptr;
+  std::vector<uint8_t *> peer_nbr_flags;
+  std::vector<uint64_t> pair_sent, pair_recv;
+  unsigned *nbr_done = nullptr;
+  bool nbr_remote = false;
   std::unique_ptr<sp_model_cache_s, sp_status (*)(sp_model_cache_s *)> cache{nullptr, sp_model_cache_free};
   sp_profile_s *profile = nullptr;
   std::mutex mu; // the runtime serialises its own calls (MPI_THREAD_SERIALIZED)
@@ -321,8 +331,26 @@ void rt_init(int rank, int size, const char *name, int device, int64_t window_by
   me.window_bytes = G.window_bytes;
   me.host_bytes = G.host_bytes;
   engine_init(G.window_bytes, G.host_bytes);
+  G.pair_sent.assign(size, 0);
+  G.pair_recv.assign(size, 0);
+  if (device >= 0) {
+    cuda_check(cudaMalloc(&G.nbr_flags, kMaxRanks * sizeof(uint64_t)), "cudaMalloc(nbr flags)");
+    cuda_check(cudaMemset(G.nbr_flags, 0, kMaxRanks * sizeof(uint64_t)), "cudaMemset(nbr flags)");
+    cuda_check(cudaMalloc(&G.nbr_done, sizeof(unsigned)), "cudaMalloc(nbr done)");
+    cuda_check(cudaMemset(G.nbr_done, 0, sizeof(unsigned)), "cudaMemset(nbr done)");
+    cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+  }
   me.ready.store(1, std::memory_order_release);
   rt_barrier();
+  rt_exchange_ptr(G.nbr_flags, G.peer_nbr_flags);
+  if (device >= 0)
+    for (int r = 0; r < size; ++r) {
+      cudaPointerAttributes at{};
+      if (G.peer_nbr_flags[r] && cudaPointerGetAttributes(&at, G.peer_nbr_flags[r]) == cudaSuccess &&
+          at.device != device)
+        G.nbr_remote = true;
+    }
+  cudaGetLastError();
 }
 
 void rt_finalize() {
@@ -337,6 +365,8 @@ void rt_finalize() {
     }
   rt_barrier();
   if (R.window) cudaFree(R.window);
+  if (R.nbr_flags) cudaFree(R.nbr_flags);
+  if (R.nbr_done) cudaFree(R.nbr_done);
   if (R.host) {
     cudaHostUnregister(R.host);
     munmap(R.host, static_cast<size_t>(R.host_bytes));
@@ -732,7 +762,7 @@ bool step_recv(Req &q) {
         cudaPointerAttributes at{};
         const bool dev = cudaPointerGetAttributes(&at, q.rbuf) == cudaSuccess && at.type == cudaMemoryTypeDevice;
         cudaGetLastError();
-        if (dev && E.desc_used != ~0u) q.method = SP_METHOD_DIRECT;
+        if (dev) q.method = SP_METHOD_DIRECT; // a descriptor slot is taken at the grant
       }
       q.st = St::Matched;
       return true;
@@ -749,6 +779,11 @@ bool step_recv(Req &q) {
     int64_t grant = 0;
     if (q.bytes == 0) {
       q.region = 0;
+    } else if (q.method == SP_METHOD_DIRECT && E.desc_used == ~0u) {
+      // every descriptor slot is held by a DIRECT message still in flight:
+      // this one moves by the sender's fallback method instead
+      q.method = q.status.method;
+      return true; // Matched again with the fallback
     } else if (q.method == SP_METHOD_DIRECT) {
       int slot = 0;
       while (E.desc_used & (1u << slot)) ++slot;
@@ -1060,6 +1095,68 @@ struct NbrCacheEntry {
 std::deque<NbrCacheEntry> g_nbr_cache;
 } // namespace
 
+// batch-cache key part of a committed type: its geometry
+void append_type_key(std::string &key, const Committed &c) {
+  const int64_t head[5] = {c.form, c.size, c.extent, c.span, c.sb.start};
+  key.append(reinterpret_cast<const char *>(head), sizeof(head));
+  key.append(reinterpret_cast<const char *>(c.sb.counts.data()), c.sb.counts.size() * sizeof(int64_t));
+  key.append(reinterpret_cast<const char *>(c.sb.strides.data()), c.sb.strides.size() * sizeof(int64_t));
+}
+
+// Entering a neighbour collective without a barrier (call after this rank's
+// layout is published): for every distinct in-neighbour s, count the call
+// and announce it (slot.pair_entered[s]); for every distinct out-neighbour
+// d, count the call and wait until d has entered it -- d's receive buffer
+// then belongs to the call and its layout is readable. The returned signal
+// set makes the data kernel publish READY to each out-neighbour (value =
+// calls on that pair) and wait, in its last block, for READY from each
+// in-neighbour, so the call is complete when the kernel is: no host
+// barrier before or after. Edges to self need no flags (stream order).
+BatchSignal nbr_enter(const std::vector<int> &sources, const std::vector<int> &dests) {
+  Runtime &R = rt();
+  BatchSignal bs;
+  std::vector<char> seen_s(R.size, 0), seen_d(R.size, 0);
+  for (int s : sources) {
+    if (s == R.rank || seen_s[s]) continue;
+    seen_s[s] = 1;
+    const uint64_t n = ++R.pair_recv[s];
+    bs.post.push_back(R.nbr_flags + s);
+    bs.post_values.push_back(n);
+  }
+  std::atomic_thread_fence(std::memory_order_release); // layout before the announcement
+  for (int s = 0; s < R.size; ++s)
+    if (seen_s[s]) R.shm->slots[R.rank].pair_entered[s].store(R.pair_recv[s], std::memory_order_release);
+  std::vector<int> outs;
+  for (int d : dests) {
+    if (d == R.rank || seen_d[d]) continue;
+    seen_d[d] = 1;
+    const uint64_t n = ++R.pair_sent[d];
+    bs.signal.push_back(reinterpret_cast<uint64_t *>(R.peer_nbr_flags[d]) + R.rank);
+    bs.signal_values.push_back(n);
+    outs.push_back(d);
+  }
+  for (int d : outs) {
+    unsigned spins = 0;
+    while (R.shm->slots[d].pair_entered[R.rank].load(std::memory_order_acquire) < R.pair_sent[d]) {
+      rt_progress();
+      pause_briefly(spins);
+    }
+  }
+  bs.done = R.nbr_done;
+  bs.sys_scope = R.nbr_remote;
+  return bs;
+}
+
+void nbr_run(Batch *b, const BatchSignal &bs) {
+  Runtime &R = rt();
+  if (b) {
+    batch_execute_signaled(*b, R.stream, bs);
+  } else {
+    flags_signal_wait(bs, R.stream);
+  }
+  cuda_check(cudaStreamSynchronize(R.stream), "cudaStreamSynchronize(neighbor)");
+}
+
 void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &send_counts,
                            const std::vector<int64_t> &send_displs, const Committed &st, uint8_t *recvbuf,
                            const std::vector<int64_t> &recv_counts, const std::vector<int64_t> &recv_displs,
@@ -1083,7 +1180,7 @@ void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &s
     me.edges[j][1] = recv_displs[j] * rtp.extent;
     me.edges[j][2] = recv_counts[j] * rtp.size;
   }
-  rt_barrier(); // layouts published, every receive buffer is owned by the call
+  const BatchSignal bs = nbr_enter(sources, dests); // replaces a barrier
   std::string key(reinterpret_cast<const char *>(&sendbuf), sizeof(sendbuf));
   std::vector<BatchSpec> jobs;
   std::vector<int> seen(R.size, 0);
@@ -1107,7 +1204,7 @@ void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &s
     const int64_t sig[4] = {reinterpret_cast<int64_t>(base), peer.edges[hit][1], send_counts[i], send_displs[i]};
     key.append(reinterpret_cast<const char *>(sig), sizeof(sig));
   }
-  key.append(reinterpret_cast<const char *>(&st), sizeof(void *));
+  append_type_key(key, st); // geometry, not the address: a freed type's address can be reused
   Batch *b = nullptr;
   for (auto &e : g_nbr_cache)
     if (e.key == key) b = e.batch;
@@ -1119,11 +1216,7 @@ void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &s
       g_nbr_cache.pop_front();
     }
   }
-  if (b) {
-    batch_execute(*b, R.stream);
-    cuda_check(cudaStreamSynchronize(R.stream), "cudaStreamSynchronize(neighbor)");
-  }
-  rt_barrier(); // every block addressed to this rank has landed
+  nbr_run(b, bs); // returns when every block addressed to this rank has landed
 }
 
 // MPI_Neighbor_alltoallw with per-edge datatypes on BOTH sides: each rank
@@ -1183,7 +1276,7 @@ void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &s
   } else {
     me.xbytes = 0;
   }
-  rt_barrier(); // layouts published, every receive buffer is owned by the call
+  const BatchSignal bs = nbr_enter(sources, dests); // replaces a barrier
   std::string key(reinterpret_cast<const char *>(&sendbuf), sizeof(sendbuf));
   std::vector<CopySpec> jobs;
   std::vector<std::unique_ptr<Committed>> dst_types;
@@ -1210,9 +1303,9 @@ void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &s
     committed_from(wd, *dc);
     uint8_t *base = (d == R.rank ? recvbuf : open_ipc(peer.xh) + peer.xoff) + peer.edges[hit][1];
     jobs.push_back({&st, sendbuf + send_displs[i], UINT64_MAX, send_counts[i], dc.get(), base, UINT64_MAX, wd.count});
-    const int64_t sig[6] = {reinterpret_cast<int64_t>(base), send_counts[i], send_displs[i], wd.count, wd.start,
-                            reinterpret_cast<int64_t>(&st)};
+    const int64_t sig[5] = {reinterpret_cast<int64_t>(base), send_counts[i], send_displs[i], wd.count, wd.start};
     key.append(reinterpret_cast<const char *>(sig), sizeof(sig));
+    append_type_key(key, st);
     key.append(reinterpret_cast<const char *>(wd.counts), sizeof(int64_t) * wd.ndims);
     key.append(reinterpret_cast<const char *>(wd.strides), sizeof(int64_t) * wd.ndims);
     dst_types.push_back(std::move(dc));
@@ -1228,11 +1321,7 @@ void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &s
       g_nbrw_cache.pop_front();
     }
   }
-  if (b) {
-    batch_execute(*b, R.stream);
-    cuda_check(cudaStreamSynchronize(R.stream), "cudaStreamSynchronize(neighbor)");
-  }
-  rt_barrier(); // every block addressed to this rank has landed
+  nbr_run(b, bs); // returns when every block addressed to this rank has landed
 }
 
 } // namespace spb
