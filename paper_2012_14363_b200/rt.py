@@ -139,6 +139,37 @@ def waitall(reqs):
     return [r.wait() for r in reqs]
 
 
+class NeighborW:
+    """MPI_Neighbor_alltoallw argument set (built once, called many times):
+    sends = [(dest, count, type, byte displacement)], recvs = [(source,
+    count, type, byte displacement)]. A call is collective: one typed-copy
+    launch per rank, no host barrier."""
+
+    def __init__(self, sends, recvs):
+        no, ni = len(sends), len(recvs)
+        self._keep = [t for _, _, t, _ in sends] + [t for _, _, t, _ in recvs]
+        self.no, self.ni = no, ni
+        self.sc = (C.c_int64 * max(no, 1))(*[c for _, c, _, _ in sends])
+        self.sd = (C.c_int64 * max(no, 1))(*[d for _, _, _, d in sends])
+        self.st = (_capi.sp_type * max(no, 1))(*[t.handle for _, _, t, _ in sends])
+        self.dst = (C.c_int * max(no, 1))(*[r for r, _, _, _ in sends])
+        self.rc = (C.c_int64 * max(ni, 1))(*[c for _, c, _, _ in recvs])
+        self.rd = (C.c_int64 * max(ni, 1))(*[d for _, _, _, d in recvs])
+        self.rt = (_capi.sp_type * max(ni, 1))(*[t.handle for _, _, t, _ in recvs])
+        self.src = (C.c_int * max(ni, 1))(*[r for r, _, _, _ in recvs])
+
+    def __call__(self, sendbuf, recvbuf):
+        sa = sendbuf if isinstance(sendbuf, int) else sendbuf.data_ptr()
+        ra = recvbuf if isinstance(recvbuf, int) else recvbuf.data_ptr()
+        _check(lib.sp_rt_neighbor_alltoallw(sa, self.sc, self.sd, self.st, self.no, self.dst, ra, self.rc, self.rd,
+                                            self.rt, self.ni, self.src))
+
+
+def neighbor_alltoallw(sendbuf, sends, recvbuf, recvs):
+    """one-shot form of NeighborW"""
+    NeighborW(sends, recvs)(sendbuf, recvbuf)
+
+
 def set_chunk(nbytes: int):
     _check(lib.sp_rt_set_chunk(nbytes))
 

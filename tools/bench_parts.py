@@ -122,6 +122,27 @@ def halo_section(torch, rank, world, local, job, iters=20, warmup=5, nccl=True):
            "fused_hostsync_us": {k: round(v * 1e6, 2) for k, v in phase_sync.items()},
            "fused_hbm_GBps_per_rank": round(4 * seg[-1] / phase["iteration"] / 1e9, 1),
            "nvlink_bound_us": round(rbytes / (NVLINK_MEASURED_GBPS * 1e9) * 1e6, 2)}
+    # the same exchange through the MPI-level call (MPI_Neighbor_alltoallw
+    # with the 26 region types): one typed-copy launch per rank plus the
+    # per-call entry protocol and a stream synchronisation; wall time
+    import time
+    H.fill(cfg, rank, alloc)
+    torch.cuda.synchronize()
+    sends = [(H.neighbor(cfg, rank, r.dir), 1, r.send, 0) for r in regions]
+    recvs = [(H.neighbor(cfg, rank, tuple(-x for x in r.dir)), 1, regions[25 - j].recv, 0)
+             for j, r in enumerate(regions)]
+    nw = rt.NeighborW(sends, recvs)
+    ws = []
+    for i in range(warmup + iters):
+        cold(i)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        nw(alloc, alloc)
+        if i >= warmup:
+            ws.append(time.perf_counter() - t0)
+    bad_w = H.verify(cfg, rank, alloc)
+    out["mpi_alltoallw_us"] = round(_reduce(torch, world, statistics.median(ws), MAX) * 1e6, 2)
+    out["verified"] = out["verified"] and _reduce(torch, world, float(bad_w), MAX) == 0
     if nccl and world > 1 and dist.is_initialized() and dist.get_backend() == "nccl":
         out["nccl"] = _nccl_halo(torch, cfg, regions, seg, alloc, rank, world, iters, warmup, cold)
     rt.finalize()
