@@ -15,6 +15,7 @@
 #include <time.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
@@ -92,6 +93,7 @@ struct Slot {
   // neighbour collectives: pair_entered[s] = how many calls with s as a
   // source this rank has entered (its layout for that call is published)
   std::atomic<uint64_t> pair_entered[kMaxRanks];
+  std::atomic<uint64_t> layout_ver; // bumped whenever the published neighbour layout changes
 };
 
 struct Shm {
@@ -140,6 +142,7 @@ struct Runtime {
   std::vector<uint64_t> pair_sent, pair_recv;
   unsigned *nbr_done = nullptr;
   bool nbr_remote = false;
+  std::string nbr_layout; // bytes of the last published neighbour layout
   std::unique_ptr<sp_model_cache_s, sp_status (*)(sp_model_cache_s *)> cache{nullptr, sp_model_cache_free};
   sp_profile_s *profile = nullptr;
   std::mutex mu; // the runtime serialises its own calls (MPI_THREAD_SERIALIZED)
@@ -1095,6 +1098,78 @@ struct NbrCacheEntry {
 std::deque<NbrCacheEntry> g_nbr_cache;
 } // namespace
 
+// Publishes this rank's receive layout for a neighbour call (IPC handle of
+// the receive buffer, in-edges, and for alltoallw the receive geometries)
+// and bumps layout_ver when it differs from the previous call's.
+void nbr_publish(uint8_t *recvbuf, const std::vector<int> &sources, const std::vector<int64_t> &disp_bytes,
+                 const std::vector<int64_t> &bytes, const std::vector<const Desc *> *wdesc) {
+  Runtime &R = rt();
+  Slot &me = R.shm->slots[R.rank];
+  cudaIpcMemHandle_t h{};
+  int64_t off = 0;
+  const bool any = recvbuf != nullptr && std::any_of(bytes.begin(), bytes.end(), [](int64_t b) { return b > 0; });
+  if (any) ipc_handle_of(recvbuf, &h, &off);
+  std::string lay(reinterpret_cast<const char *>(&h), sizeof(h));
+  lay.append(reinterpret_cast<const char *>(&off), sizeof(off));
+  lay.push_back(any ? 1 : 0);
+  for (size_t j = 0; j < sources.size(); ++j) {
+    const int64_t e[3] = {sources[j], disp_bytes[j], bytes[j]};
+    lay.append(reinterpret_cast<const char *>(e), sizeof(e));
+    if (wdesc && (*wdesc)[j]) lay.append(reinterpret_cast<const char *>((*wdesc)[j]), sizeof(Desc));
+  }
+  if (lay == R.nbr_layout) return; // unchanged: peers keep their cached plans
+  me.xh = h;
+  me.xoff = off;
+  me.xbytes = any ? 1 : 0;
+  me.nedges = static_cast<int32_t>(sources.size());
+  for (size_t j = 0; j < sources.size(); ++j) {
+    me.edges[j][0] = sources[j];
+    me.edges[j][1] = disp_bytes[j];
+    me.edges[j][2] = bytes[j];
+    if (wdesc && (*wdesc)[j]) me.wdesc[j] = *(*wdesc)[j];
+  }
+  R.nbr_layout = std::move(lay);
+  me.layout_ver.fetch_add(1, std::memory_order_release);
+}
+
+// Last call of each neighbour collective: when a call repeats it (same
+// arguments, every out-neighbour's layout version unchanged) the cached
+// batch is relaunched without rebuilding jobs or cache keys.
+struct NbrLast {
+  std::string sig;
+  std::vector<std::pair<int, uint64_t>> peer_ver;
+  Batch *batch = nullptr;
+  bool valid = false;
+};
+
+NbrLast g_last_v, g_last_w;
+
+bool nbr_last_hit(const NbrLast &last, const std::string &sig) {
+  if (!last.valid || last.sig != sig) return false;
+  Runtime &R = rt();
+  for (auto [d, v] : last.peer_ver)
+    if (R.shm->slots[d].layout_ver.load(std::memory_order_acquire) != v) return false;
+  return true;
+}
+
+void nbr_last_set(NbrLast &last, std::string sig, const std::vector<int> &dests, Batch *b) {
+  Runtime &R = rt();
+  last.sig = std::move(sig);
+  last.peer_ver.clear();
+  std::vector<char> seen(R.size, 0);
+  for (int d : dests)
+    if (!seen[d]) {
+      seen[d] = 1;
+      last.peer_ver.emplace_back(d, R.shm->slots[d].layout_ver.load(std::memory_order_acquire));
+    }
+  last.batch = b;
+  last.valid = true;
+}
+
+template <class T> void append_bytes(std::string &s, const std::vector<T> &v) {
+  s.append(reinterpret_cast<const char *>(v.data()), v.size() * sizeof(T));
+}
+
 // batch-cache key part of a committed type: its geometry
 void append_type_key(std::string &key, const Committed &c) {
   const int64_t head[5] = {c.form, c.size, c.extent, c.span, c.sb.start};
@@ -1167,20 +1242,25 @@ void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &s
                           rtp.extent == rtp.size;
   if (!dense_recv && rtp.form != SP_FORM_EMPTY)
     fail(SP_ERR_UNSUPPORTED, "neighbour exchange: receive type must be contiguous bytes (e.g. MPI_PACKED)");
-  Slot &me = R.shm->slots[R.rank];
-  if (recvbuf) {
-    ipc_handle_of(recvbuf, &me.xh, &me.xoff);
-    me.xbytes = 1;
-  } else {
-    me.xbytes = 0;
-  }
-  me.nedges = static_cast<int32_t>(sources.size());
-  for (size_t j = 0; j < sources.size(); ++j) {
-    me.edges[j][0] = sources[j];
-    me.edges[j][1] = recv_displs[j] * rtp.extent;
-    me.edges[j][2] = recv_counts[j] * rtp.size;
+  {
+    std::vector<int64_t> disp(sources.size()), bytes(sources.size());
+    for (size_t j = 0; j < sources.size(); ++j) {
+      disp[j] = recv_displs[j] * rtp.extent;
+      bytes[j] = recv_counts[j] * rtp.size;
+    }
+    nbr_publish(recvbuf, sources, disp, bytes, nullptr);
   }
   const BatchSignal bs = nbr_enter(sources, dests); // replaces a barrier
+  std::string sig(reinterpret_cast<const char *>(&sendbuf), sizeof(sendbuf));
+  sig.append(reinterpret_cast<const char *>(&recvbuf), sizeof(recvbuf));
+  append_bytes(sig, send_counts);
+  append_bytes(sig, send_displs);
+  append_bytes(sig, dests);
+  append_type_key(sig, st);
+  if (nbr_last_hit(g_last_v, sig)) {
+    nbr_run(g_last_v.batch, bs);
+    return;
+  }
   std::string key(reinterpret_cast<const char *>(&sendbuf), sizeof(sendbuf));
   std::vector<BatchSpec> jobs;
   std::vector<int> seen(R.size, 0);
@@ -1212,10 +1292,12 @@ void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &s
     b = batch_create(jobs, false);
     g_nbr_cache.push_back({key, b});
     if (g_nbr_cache.size() > 16) {
+      if (g_last_v.batch == g_nbr_cache.front().batch) g_last_v.valid = false;
       batch_destroy(g_nbr_cache.front().batch);
       g_nbr_cache.pop_front();
     }
   }
+  nbr_last_set(g_last_v, std::move(sig), dests, b);
   nbr_run(b, bs); // returns when every block addressed to this rank has landed
 }
 
@@ -1254,29 +1336,33 @@ void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &s
                            const std::vector<int> &sources, const std::vector<int> &dests) {
   Runtime &R = rt();
   if (static_cast<int>(sources.size()) > kMaxWEdges) fail(SP_ERR_UNSUPPORTED, "neighbour alltoallw: indegree > 64");
-  Slot &me = R.shm->slots[R.rank];
-  bool any_recv = false;
-  me.nedges = static_cast<int32_t>(sources.size());
-  for (size_t j = 0; j < sources.size(); ++j) {
-    const Committed &rt_ = *recv_types[j];
-    const int64_t bytes = recv_counts[j] * rt_.size;
-    if (bytes > 0 && !describable(rt_))
-      fail(SP_ERR_UNSUPPORTED, "neighbour alltoallw: receive types need a strided, non-overlapping canonical form");
-    me.edges[j][0] = sources[j];
-    me.edges[j][1] = recv_displs[j];
-    me.edges[j][2] = bytes;
-    if (bytes > 0) {
-      desc_of(rt_, recv_counts[j], me.wdesc[j]);
-      any_recv = true;
+  {
+    std::vector<Desc> descs(sources.size(), Desc{});
+    std::vector<const Desc *> dp(sources.size(), nullptr);
+    std::vector<int64_t> bytes(sources.size());
+    for (size_t j = 0; j < sources.size(); ++j) {
+      const Committed &rt_ = *recv_types[j];
+      bytes[j] = recv_counts[j] * rt_.size;
+      if (bytes[j] > 0 && !describable(rt_))
+        fail(SP_ERR_UNSUPPORTED, "neighbour alltoallw: receive types need a strided, non-overlapping canonical form");
+      if (bytes[j] > 0) {
+        desc_of(rt_, recv_counts[j], descs[j]);
+        dp[j] = &descs[j];
+      }
     }
-  }
-  if (any_recv) {
-    ipc_handle_of(recvbuf, &me.xh, &me.xoff);
-    me.xbytes = 1;
-  } else {
-    me.xbytes = 0;
+    nbr_publish(recvbuf, sources, recv_displs, bytes, &dp);
   }
   const BatchSignal bs = nbr_enter(sources, dests); // replaces a barrier
+  std::string sig(reinterpret_cast<const char *>(&sendbuf), sizeof(sendbuf));
+  sig.append(reinterpret_cast<const char *>(&recvbuf), sizeof(recvbuf));
+  append_bytes(sig, send_counts);
+  append_bytes(sig, send_displs);
+  append_bytes(sig, dests);
+  for (const CommitPtr &t : send_types) append_type_key(sig, *t);
+  if (nbr_last_hit(g_last_w, sig)) {
+    nbr_run(g_last_w.batch, bs);
+    return;
+  }
   std::string key(reinterpret_cast<const char *>(&sendbuf), sizeof(sendbuf));
   std::vector<CopySpec> jobs;
   std::vector<std::unique_ptr<Committed>> dst_types;
@@ -1317,10 +1403,12 @@ void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &s
     b = copy_batch_create(jobs);
     g_nbrw_cache.push_back({key, b});
     if (g_nbrw_cache.size() > 16) {
+      if (g_last_w.batch == g_nbrw_cache.front().batch) g_last_w.valid = false;
       batch_destroy(g_nbrw_cache.front().batch);
       g_nbrw_cache.pop_front();
     }
   }
+  nbr_last_set(g_last_w, std::move(sig), dests, b);
   nbr_run(b, bs); // returns when every block addressed to this rank has landed
 }
 

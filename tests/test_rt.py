@@ -233,6 +233,47 @@ def test_nonblocking_ring_three_processes(cuda):
     assert all(_spawn(_ring, 3).values())
 
 
+def _nbrw(rank, world, job):
+    """MPI_Neighbor_alltoallw on a ring of 3: repeated calls (the cached fast
+    path), then the receiver switches buffers and types between calls -- the
+    senders must see the new layouts (layout versions) and stay exact"""
+    import torch
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.rt as rt
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=1 << 20, host_bytes=1 << 20)
+    right, left = (rank + 1) % world, (rank - 1) % world
+    B = sp.make_named(sp.NamedKind.Byte)
+    # a 3-D 64x32x16 block of bytes; send the interior box, receive into two layouts
+    box = sp.commit_type(sp.make_subarray(3, [64, 32, 16], [16, 8, 4], [8, 4, 2], B))
+    dst_a = sp.commit_type(sp.make_subarray(3, [64, 32, 16], [16, 8, 4], [40, 20, 10], B))
+    dst_b = sp.commit_type(sp.make_hvector(32, 1, 96, sp.make_contiguous(16, B)))  # 512 B, other shape
+    n = 64 * 32 * 16
+    src = torch.arange(n, dtype=torch.int64, device="cuda").mul_(7).add_(rank).to(torch.uint8)
+    ok = True
+    for it in range(4):
+        rdt = dst_a if it < 2 else dst_b
+        recv = torch.full((n + (4096 if it == 3 else 0),), 0xAB, dtype=torch.uint8, device="cuda")  # new buffer
+        torch.cuda.synchronize()
+        rt.NeighborW([(right, 1, box, 0)], [(left, 1, rdt, 0)])(src, recv)
+        # expected: the left neighbour's box bytes, unpacked with rdt
+        lsrc = torch.arange(n, dtype=torch.int64, device="cuda").mul_(7).add_(left).to(torch.uint8)
+        packed = torch.empty(box.size, dtype=torch.uint8, device="cuda")
+        sp.pack(lsrc, box, 1, packed, 0)
+        want = torch.full_like(recv, 0xAB)
+        sp.unpack(packed, 0, rdt, 1, want)
+        torch.cuda.synchronize()
+        ok = ok and bool(torch.equal(recv, want))
+        assert ok, (rank, it)
+    rt.finalize()
+    return ok
+
+
+@pytest.mark.gpu
+def test_neighbor_alltoallw_layout_changes(cuda):
+    assert all(_spawn(_nbrw, 3).values())
+
+
 def _halo(rank, world, job, ranks, method):
     import torch
     import paper_2012_14363_b200.halo as H
