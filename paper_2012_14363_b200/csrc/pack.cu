@@ -881,7 +881,7 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
 // a round a thread finds its job by walking forward from the CTA's first
 // job (ranges rarely cross a job boundary); the job descriptors are read
 // through the read-only path and stay L1-resident.
-constexpr int kBatchU = 2;                            // words in flight per thread
+constexpr int kBatchU = 4;                            // words in flight per thread
 constexpr uint32_t kBatchChunk = 256 * kBatchU;       // words per unit of work
 enum : int { kModeUnpack = 0, kModePack = 1, kModeCopy = 2 };
 
