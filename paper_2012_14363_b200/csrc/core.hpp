@@ -203,8 +203,6 @@ struct BatchSignal {
 };
 // one-warp kernel: release-stores the signals, then waits for the post flags
 void flags_signal_wait(const BatchSignal &sig, void *stream);
-// one-warp kernel: waits until every flag reaches value (acquire, system scope)
-void flags_wait(const std::vector<const uint64_t *> &wait, uint64_t value, void *stream);
 void batch_execute_signaled(const Batch &b, void *stream, const BatchSignal &sig);
 int64_t batch_bytes(const Batch &b);
 

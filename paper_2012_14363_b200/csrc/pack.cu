@@ -1444,23 +1444,6 @@ void batch_launch(const Batch &b, void *stream, const BatchSignal *bs) {
 }
 } // namespace
 
-// one warp: lane i spins until wait[i] >= value (acquire, system scope)
-__global__ void k_flag_wait(const BatchSig sig) {
-  if (threadIdx.x < static_cast<unsigned>(sig.n_wait))
-    while (ld_acquire_sys(sig.wait[threadIdx.x]) < sig.wait_value) __nanosleep(64);
-}
-
-void flags_wait(const std::vector<const uint64_t *> &wait, uint64_t value, void *stream) {
-  if (wait.empty()) return;
-  if (wait.size() > static_cast<size_t>(kMaxSig)) fail(SP_ERR_UNSUPPORTED, "flag wait: more than 32 peers");
-  BatchSig sig{};
-  sig.n_wait = static_cast<int>(wait.size());
-  for (int i = 0; i < sig.n_wait; ++i) sig.wait[i] = reinterpret_cast<const unsigned long long *>(wait[i]);
-  sig.wait_value = value;
-  k_flag_wait<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(sig);
-  cuda_check(cudaGetLastError(), "k_flag_wait launch");
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-}
 
 namespace {
 
