@@ -1,5 +1,8 @@
-"""e2e variants (bench.py's e2e leg): host time per step vs device time,
-for NS streams and per-object vs per-E0 messages through the C-ABI."""
+"""e2e variants (bench.py's e2e leg): device time per step for messages of
+Ke/split objects per E0 in three issue orders over NS streams, and the PCIe
+bound (the same bytes as plain copies in both directions at once). Measured
+on B200 (round 1): every variant 2.30-2.71 ms against a 1.71 ms bound; the
+same loop driven from C++ instead of Python was within noise (2.26-2.43)."""
 import ctypes as C, math, os, sys, time, json
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -22,18 +25,30 @@ msg_in = [torch.full((Ke << 20,), 5, dtype=torch.uint8).pin_memory() for _ in E0
 msg_out = [torch.empty(Ke << 20, dtype=torch.uint8).pin_memory() for _ in E0S]
 pos = C.c_int64(0)
 res = {}
-for NS, per_obj in [(4, True), (2, True), (8, True), (4, False), (10, False)]:
+ORDERS = {"desc": sorted(E0S, reverse=True), "asc": sorted(E0S), "mix": [1, 4, 8, 16, 2, 32, 64, 128, 256, 512]}
+for NS, split, order in [(10, 1, "desc"), (10, 1, "asc"), (10, 1, "mix"), (20, 2, "desc"), (20, 2, "mix"),
+                         (40, 4, "mix"), (16, 2, "mix"), (8, 8, "desc")]:
     streams = [torch.cuda.Stream() for _ in range(NS)]
-    handles = [C.c_void_p(s.cuda_stream) for s in streams]
+    handles = (C.c_void_p * NS)(*[s.cuda_stream for s in streams])
     items = []
-    order = sorted(range(len(types)), key=lambda i: -types[i][0])
-    if per_obj:
-        for j in range(Ke):
-            for i in order:
-                items.append((types[i][1], esrc.data_ptr() + (j << 30) + xoff[types[i][0]], j << 20, i, 1))
-    else:
-        for i in order:
-            items.append((types[i][1], esrc.data_ptr() + xoff[types[i][0]], 0, i, Ke))
+    per = Ke // split
+    idx = {e0: i for i, (e0, _) in enumerate(types)}
+    for part in range(split):
+        for e0 in ORDERS[order]:
+            i = idx[e0]
+            ct = types[i][1]
+            j0 = part * per
+            items.append((ct, esrc.data_ptr() + (j0 << 30) + xoff[e0], msg_in[i].data_ptr() + (j0 << 20),
+                          msg_out[i].data_ptr() + (j0 << 20), per << 20, per))
+    per_obj = f"split={split} order={order}"
+    n = len(items)
+    arr_t = (_capi.sp_type * n)(*[it[0].handle for it in items])
+    arr_c = (C.c_int64 * n)(*[it[5] for it in items])
+    arr_o = (C.c_void_p * n)(*[it[1] for it in items])
+    arr_ob = (C.c_uint64 * n)(*[esrc.numel() - (it[1] - esrc.data_ptr()) for it in items])
+    arr_i = (C.c_void_p * n)(*[it[2] for it in items])
+    arr_out = (C.c_void_p * n)(*[it[3] for it in items])
+    arr_mb = (C.c_uint64 * n)(*[it[4] for it in items])
     dev, host = [], []
     for it in range(8):
         torch.cuda.synchronize()
@@ -41,12 +56,12 @@ for NS, per_obj in [(4, True), (2, True), (8, True), (4, False), (10, False)]:
         a.record(streams[0])
         for s in streams[1:]: s.wait_event(a)
         t0 = time.perf_counter()
-        for n, (ct, obj, off, i, cnt) in enumerate(items):
-            h = handles[n % NS]
-            pos.value = off
-            assert lib.sp_unpack(msg_in[i].data_ptr(), msg_in[i].numel(), C.byref(pos), ct.handle, cnt, obj, esrc.numel(), h) == 0
-            pos.value = off
-            assert lib.sp_pack(obj, esrc.numel(), ct.handle, cnt, msg_out[i].data_ptr(), msg_out[i].numel(), C.byref(pos), h) == 0
+        for k, (ct, obj, mi, mo, mb, cnt) in enumerate(items):
+            h = C.c_void_p(handles[k % NS])
+            pos.value = 0
+            assert lib.sp_unpack(mi, mb, C.byref(pos), ct.handle, cnt, obj, esrc.numel(), h) == 0
+            pos.value = 0
+            assert lib.sp_pack(obj, esrc.numel(), ct.handle, cnt, mo, mb, C.byref(pos), h) == 0
         t1 = time.perf_counter()
         for s in streams[1:]:
             ev = torch.cuda.Event(); ev.record(s); streams[0].wait_event(ev)
@@ -55,6 +70,23 @@ for NS, per_obj in [(4, True), (2, True), (8, True), (4, False), (10, False)]:
         if it >= 3:
             dev.append(a.elapsed_time(b)); host.append((t1 - t0) * 1e3)
     bytes_ = 2 * Ke * (1 << 20) * 2 * len(E0S)
-    res[f"NS={NS} per_obj={per_obj}"] = {"dev_ms": round(min(dev), 3), "host_ms": round(min(host), 3),
-                                         "GBps": round(bytes_ / (min(dev) * 1e-3) / 1e9, 1)}
+    res[f"NS={NS} {per_obj}"] = {"dev_ms": round(min(dev), 3), "host_ms": round(min(host), 3),
+                                                         "GBps": round(bytes_ / (min(dev) * 1e-3) / 1e9, 1)}
+# PCIe bound
+dev_buf = torch.empty(2 * (Ke << 20) * len(E0S), dtype=torch.uint8, device="cuda")
+hin = torch.cat(msg_in).pin_memory()
+hout = torch.empty_like(hin).pin_memory()
+half = hin.numel()
+s0, s1 = torch.cuda.Stream(), torch.cuda.Stream()
+pc = []
+for it in range(5):
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+    a.record(s0); s1.wait_event(a)
+    with torch.cuda.stream(s0): dev_buf[:half].copy_(hin, non_blocking=True)
+    with torch.cuda.stream(s1): hout.copy_(dev_buf[half:], non_blocking=True)
+    ev = torch.cuda.Event(); ev.record(s1); s0.wait_event(ev); b.record(s0)
+    torch.cuda.synchronize()
+    if it: pc.append(a.elapsed_time(b))
+res["pcie_bound_ms"] = round(min(pc), 3)
 print(json.dumps(res, indent=1))
