@@ -471,6 +471,7 @@ void rt_exchange_ptr(void *local, std::vector<uint8_t *> &out) {
 namespace {
 
 constexpr uint32_t kCHUNK = 5;
+constexpr int64_t kDirectRemoteMinRow = 64; // bytes per destination row for DIRECT across GPUs
 constexpr int64_t kGrantAlign = 256;
 
 struct RangeAlloc {
@@ -765,7 +766,13 @@ bool step_recv(Req &q) {
         cudaPointerAttributes at{};
         const bool dev = cudaPointerGetAttributes(&at, q.rbuf) == cudaSuccess && at.type == cudaMemoryTypeDevice;
         cudaGetLastError();
-        if (dev) q.method = SP_METHOD_DIRECT; // a descriptor slot is taken at the grant
+        // over NVLink the fused copy stores each destination row as its own
+        // remote write: short rows would cost a link transaction per few
+        // bytes, where the fallback ships packed full lines and unpacks
+        // locally -- accept DIRECT from another GPU only for rows >= 64 B
+        const bool remote = R.shm->slots[m.src].device != R.device;
+        const bool rows_ok = !remote || q.ct->sb.counts[0] >= kDirectRemoteMinRow;
+        if (dev && rows_ok) q.method = SP_METHOD_DIRECT; // a descriptor slot is taken at the grant
       }
       q.st = St::Matched;
       return true;
