@@ -286,7 +286,7 @@ def run_reference(args):
 
 
 def build_line(args, value, step_ms, world, K, dominant, sweep, e2e_val, Ke, launches, clk, cpu, halo, send,
-               pcie_ms=None):
+               pcie_ms=None, single=None):
     hbm, hbm_kind = peaks()
     ms, e0, tag, gbs, li = dominant
     bytes_per_kernel = 2 * K * (1 << 20)
@@ -322,6 +322,7 @@ def build_line(args, value, step_ms, world, K, dominant, sweep, e2e_val, Ke, lau
                      "transaction_cap_frac": round(cap, 4),
                      "frac_of_transaction_cap": round(gbs / hbm / cap, 3)},
         "sweep": sweep,
+        "single_object": single,
         "e2e": {"value": round(e2e_val, 2), "unit": UNIT, "h2d_bytes_per_step": Ke * (1 << 20) * len(E0S),
                 "d2h_bytes_per_step": Ke * (1 << 20) * len(E0S),
                 "how": f"sp_unpack from / sp_pack to PINNED HOST message buffers through the C-ABI "
@@ -461,6 +462,33 @@ def run_ours(args):
                 dominant = (ms, e0, tag, gbs, li)
         sweep.append(row)
 
+    # single objects (outside the timed region): one 1 MiB object per call,
+    # the unit the paper reports per pack (cfg1 = vector(131072,1,64,DOUBLE)
+    # and every cfg2 E0), cold L2, kernel time by events
+    single = []
+    for name, prog in [("cfg1", [2, 131072, 1, 64, 0, 3])] + [(f"cfg2 E0={e0}", cfg2_prog(e0)) for e0 in E0S]:
+        ct1 = sp.commit_type(sp.from_program(prog))
+        r = {"object": name, "bytes": ct1.size}
+        for pack in (True, False):
+            ts = []
+            for i in range(5):
+                flush_l2(i)
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                if pack:
+                    call(True, ct1, 1, src.data_ptr(), src.numel(), packed.data_ptr(), packed.numel())
+                else:
+                    call(False, ct1, 1, packed.data_ptr(), packed.numel(), src.data_ptr(), src.numel())
+                b.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            us = min(ts) * 1e3
+            tag = "pack" if pack else "unpack"
+            r[f"{tag}_us"] = round(us, 2)
+            r[f"{tag}_GBps"] = round(2 * ct1.size / us / 1e3, 1)
+        single.append(r)
+
     # e2e: the packed messages live in pinned HOST memory and every call
     # goes through the public C-ABI with those host pointers: sp_unpack
     # moves a message over PCIe into the device object (the engine's DMA
@@ -569,7 +597,7 @@ def run_ours(args):
             args.no_cpu_baseline = True
             line_box["cpu"] = cpu_pre
         line_box["line"] = build_line(args, value, step_ms, world, K, dominant, sweep, e2e_val, Ke,
-                                      launches, clk, cpu_pre, None, None, pcie_ms)
+                                      launches, clk, cpu_pre, None, None, pcie_ms, single)
         dog = threading.Timer(args.section_timeout, on_timeout)
         dog.daemon = True
         dog.start()
@@ -599,7 +627,7 @@ def run_ours(args):
                "sample": f"{reps} x (pack+unpack of 1 cfg2 object per E0), {t:.1f} s CPU, "
                          "PackOptions.threads=1 (the reference's fastest setting)"}
     line = build_line(args, value, step_ms, world, K, dominant, sweep, e2e_val, Ke, launches, clk, cpu, halo,
-                      send, pcie_ms)
+                      send, pcie_ms, single)
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
