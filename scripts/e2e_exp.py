@@ -26,21 +26,41 @@ msg_out = [torch.empty(Ke << 20, dtype=torch.uint8).pin_memory() for _ in E0S]
 pos = C.c_int64(0)
 res = {}
 ORDERS = {"desc": sorted(E0S, reverse=True), "asc": sorted(E0S), "mix": [1, 4, 8, 16, 2, 32, 64, 128, 256, 512]}
-for NS, split, order in [(10, 1, "desc"), (10, 1, "asc"), (10, 1, "mix"), (20, 2, "desc"), (20, 2, "mix"),
-                         (40, 4, "mix"), (16, 2, "mix"), (8, 8, "desc")]:
+idx = {e0: i for i, (e0, _) in enumerate(types)}
+
+
+def pieces(splits):
+    """messages as (e0, first object, objects), the slow small-E0 objects
+    split finer and dealt between the fast ones"""
+    fast = [(e0, j, Ke // splits.get(e0, 1)) for e0 in sorted(E0S, reverse=True)
+            for j in range(0, Ke, Ke // splits.get(e0, 1)) if splits.get(e0, 1) == 1]
+    slow = [(e0, j, Ke // splits[e0]) for e0 in sorted(E0S) if splits.get(e0, 1) > 1
+            for j in range(0, Ke, Ke // splits[e0])]
+    out = []
+    while fast or slow:
+        if fast:
+            out.append(fast.pop(0))
+        for _ in range(max(1, len(slow) // max(1, len(fast) + 1))):
+            if slow:
+                out.append(slow.pop(0))
+    return out
+
+
+VARIANTS = [(10, "per-E0 desc", [(e0, 0, Ke) for e0 in ORDERS["desc"]]),
+            (16, "split E0<=4 x8", pieces({1: 8, 2: 8, 4: 8})),
+            (16, "split E0<=8 x4", pieces({1: 4, 2: 4, 4: 4, 8: 4})),
+            (24, "split E0<=16 x8", pieces({1: 8, 2: 8, 4: 8, 8: 8, 16: 8})),
+            (8, "split E0<=4 x8 NS8", pieces({1: 8, 2: 8, 4: 8}))]
+for NS, label, msgs in VARIANTS:
     streams = [torch.cuda.Stream() for _ in range(NS)]
     handles = (C.c_void_p * NS)(*[s.cuda_stream for s in streams])
     items = []
-    per = Ke // split
-    idx = {e0: i for i, (e0, _) in enumerate(types)}
-    for part in range(split):
-        for e0 in ORDERS[order]:
-            i = idx[e0]
-            ct = types[i][1]
-            j0 = part * per
-            items.append((ct, esrc.data_ptr() + (j0 << 30) + xoff[e0], msg_in[i].data_ptr() + (j0 << 20),
-                          msg_out[i].data_ptr() + (j0 << 20), per << 20, per))
-    per_obj = f"split={split} order={order}"
+    for e0, j0, per in msgs:
+        i = idx[e0]
+        ct = types[i][1]
+        items.append((ct, esrc.data_ptr() + (j0 << 30) + xoff[e0], msg_in[i].data_ptr() + (j0 << 20),
+                      msg_out[i].data_ptr() + (j0 << 20), per << 20, per))
+    per_obj = label
     n = len(items)
     arr_t = (_capi.sp_type * n)(*[it[0].handle for it in items])
     arr_c = (C.c_int64 * n)(*[it[5] for it in items])
