@@ -305,6 +305,10 @@ __global__ void __launch_bounds__(256) k_smallrow(const uint8_t *__restrict__ in
 //   unpack: 1.6-2.5 TB/s against 1.33 (W=1) for c0 >= 128; shorter rows lose
 //           to W=1 because the row-end partial blocks become per-lane
 //           scattered sub-word stores.
+// below this the LDG/STG kernel wins the TMA unpack (1 MiB single objects:
+// 6.1 vs 8.1 us, bench.py single_object); the sweep's 64 MiB calls keep TMA
+constexpr uint64_t kTmaMinBytes = uint64_t{8} << 20;
+
 static bool shift_wins(bool pack, int w, int64_t c0) {
   if (pack) return w <= 2 || (w == 4 && c0 % 16 == 0);
   return w <= 2 && c0 >= 128;
@@ -759,7 +763,8 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
   // LDG/STG kernel at c0 = 64 and 128 (profiles/r01_tma_vs_words.txt) and
   // ties above; at 32 B it loses; pack ties or loses everywhere
   if (kernel == SP_KERNEL_WORDS && opt.kernel == SP_KERNEL_AUTO && !pack && !opt.force_word && rd.c0 >= 64 &&
-      g.nd <= 4 && t_host_grid_cap == 0 /* device memory on both sides */) {
+      g.nd <= 4 && t_host_grid_cap == 0 /* device memory on both sides */ &&
+      total_bytes >= kTmaMinBytes /* the TMA ring's pipeline fill costs ~2 us on a 1 MiB object */) {
     TmaGeometry probe{};
     probe.c0 = rd.c0;
     probe.nd = g.nd;

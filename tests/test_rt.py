@@ -192,6 +192,41 @@ def test_nonblocking_pipelined_and_direct(cuda):
     assert m[9] == 0
 
 
+def _window_pressure(rank, world, job):
+    """24 DEVICE and 8 STAGED messages of 256 KiB in flight at once into a
+    1 MiB window / host region: grants wait for space and the receiver still
+    matches in posting order"""
+    import torch
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.rt as rt
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=1 << 20, host_bytes=1 << 20)
+    ct = sp.commit_type(sp.make_hvector(1024, 1, 512, sp.make_contiguous(256, sp.make_named(sp.NamedKind.Byte))))
+    n = 32
+    ok = True
+    if rank == 0:
+        srcs = [torch.full((1024 * 512,), k, dtype=torch.uint8, device="cuda") for k in range(n)]
+        torch.cuda.synchronize()
+        reqs = [rt.isend(srcs[k], 1, ct, 1, tag=7, method=rt.DEVICE if k % 4 else rt.STAGED) for k in range(n)]
+        rt.waitall(reqs)
+    else:
+        dsts = [torch.zeros(1024 * 512, dtype=torch.uint8, device="cuda") for _ in range(n)]
+        torch.cuda.synchronize()
+        reqs = [rt.irecv(dsts[k], 1, ct, source=0, tag=7) for k in range(n)]
+        sts = rt.waitall(reqs)
+        for k in range(n):
+            v = dsts[k].view(1024, 512)[:, :256]
+            ok = ok and bool((v == k).all()) and bool((dsts[k].view(1024, 512)[:, 256:] == 0).all())
+            ok = ok and sts[k]["bytes"] == ct.size and sts[k]["method"] == (1 if k % 4 else 2)
+    rt.finalize()
+    return ok
+
+
+@pytest.mark.gpu
+def test_many_messages_window_pressure(cuda):
+    assert all(_spawn(_window_pressure, 2).values())
+
+
 def _ring(rank, world, job):
     """every rank sends to its right and receives from its left at once"""
     import torch
