@@ -243,6 +243,44 @@ def flatten(d: TypeDef) -> BlockList:
     return BlockList(tuple(Block(off[i], ln[i]) for i in range(n.value)), bool(ov.value))
 
 
+# the reference's name for the same list (block_list.hpp:123-126)
+flatten_oracle = flatten
+
+
+def normalize_blocks(runs) -> BlockList:
+    """block_list.hpp:44-61: drop empty runs, sort by (offset, length),
+    merge abutting / overlapping runs; overlap = some byte described twice.
+    runs: iterable of (offset, length) or Block."""
+    rs = sorted(((r.offset, r.length) if isinstance(r, Block) else (int(r[0]), int(r[1])))
+                for r in runs)
+    out, overlap = [], False
+    for off, ln in rs:
+        if ln == 0:
+            continue
+        if out and off <= out[-1][0] + out[-1][1]:
+            if off < out[-1][0] + out[-1][1]:
+                overlap = True
+            end = max(out[-1][0] + out[-1][1], off + ln)
+            out[-1] = (out[-1][0], end - out[-1][0])
+        else:
+            out.append((off, ln))
+    return BlockList(tuple(Block(o, l) for o, l in out), overlap)
+
+
+def enumerate_blocks(sb: "StridedBlock") -> BlockList:
+    """block_list.hpp:129-159: the normalized runs a StridedBlock describes
+    (counts[0] bytes per run, dimension 1 fastest)."""
+    if any(c < 1 for c in sb.counts):
+        return BlockList((), False)
+    import itertools
+    runs = []
+    dims = [range(c) for c in sb.counts[1:]]
+    for idx in itertools.product(*reversed(dims)):
+        off = sb.start + sum(i * st for i, st in zip(reversed(idx), sb.strides[1:]))
+        runs.append((off, sb.counts[0]))
+    return normalize_blocks(runs)
+
+
 @dataclass(frozen=True)
 class TypeFileResult:              # typefile.hpp:27-30
     name: str

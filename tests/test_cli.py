@@ -360,3 +360,23 @@ def test_flatten_matches_live_reference(sp, ref):
         assert got.overlap == overlap
         n += 1
     assert n > 50
+
+
+def test_enumerate_and_normalize_match_flatten(sp, corpus):
+    """block_list.hpp: enumerate_blocks(canonical form) == flatten(definition)
+    for strided definitions (translate + canonicalisation preserve the byte
+    set), and normalize_blocks of the definition's runs is idempotent"""
+    n = 0
+    for e in corpus:
+        r = e["ref"]
+        if r["status"] != 0 or r["form"] != 0 or r["size"] > (1 << 14) or r["overlapping"]:
+            continue
+        d = sp.from_program(e["prog"])
+        ct = sp.commit_type(d)
+        got = sp.flatten_oracle(d)
+        assert sp.enumerate_blocks(ct.canon) == got, e["prog"]
+        assert sp.normalize_blocks(got.blocks) == got
+        n += 1
+    assert n > 100
+    assert sp.normalize_blocks([(8, 4), (0, 4), (2, 4), (12, 0)]) == sp.BlockList(
+        (sp.Block(0, 6), sp.Block(8, 4)), True)
