@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libstridepack_b200.so")
+# SPB_LIB selects another build of the same library (e.g. the ASan/UBSan
+# build of `make -C paper_2012_14363_b200/csrc asan`); default: in-tree
+LIB_PATH = os.environ.get("SPB_LIB") or os.path.join(PKG_DIR, "libstridepack_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
