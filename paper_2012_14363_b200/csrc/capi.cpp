@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "core.hpp"
+#include "trace.hpp"
 
 namespace {
 
@@ -125,6 +126,7 @@ sp_status sp_type_flatten(sp_type t, int64_t *offsets, int64_t *lengths, int64_t
 }
 
 sp_status sp_type_commit(sp_type t) {
+  SPB_TRACE("sp_type_commit");
   return guard([&] { spb::registry().commit(t); });
 }
 
@@ -163,6 +165,7 @@ sp_status sp_type_query(sp_type t, sp_type_info *info, int64_t *counts, int64_t 
 
 static sp_status pack_impl(bool pack, const void *src, uint64_t src_bytes, sp_type t, int64_t count, void *dst,
                            uint64_t dst_bytes, int64_t *position, void *stream, const sp_pack_options *opt) {
+  SPB_TRACE(pack ? "sp_pack" : "sp_unpack");
   return guard([&] {
     if (!position) spb::fail(SP_ERR_INVALID_ARGUMENT, "null position");
     const spb::Entry e = spb::registry().get(t);
@@ -230,6 +233,7 @@ sp_status sp_batch_create(const sp_batch_job *jobs, int64_t n, int unpack, sp_ba
 }
 
 sp_status sp_copy(const sp_copy_job *job, void *stream) {
+  SPB_TRACE("sp_copy");
   return guard([&] {
     if (!job) spb::fail(SP_ERR_INVALID_ARGUMENT, "null job");
     const spb::Entry es = spb::registry().get(job->src_type), ed = spb::registry().get(job->dst_type);
@@ -259,6 +263,7 @@ sp_status sp_copy_batch_create(const sp_copy_job *jobs, int64_t n, sp_batch *out
 }
 
 sp_status sp_batch_execute(sp_batch b, void *stream) {
+  SPB_TRACE("sp_batch_execute");
   return guard([&] {
     if (!b) spb::fail(SP_ERR_INVALID_ARGUMENT, "null batch");
     spb::batch_execute(*b->b, stream);

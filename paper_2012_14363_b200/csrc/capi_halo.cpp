@@ -3,6 +3,7 @@
 
 #include "guard.hpp"
 #include "halo.hpp"
+#include "trace.hpp"
 
 using namespace spb;
 
@@ -75,6 +76,7 @@ sp_status sp_halo_verify(const sp_halo_config *cfg, int64_t rank, const void *al
 }
 
 sp_status sp_halo_run(const sp_halo_config *cfg, sp_profile profile, int method, int iters, sp_halo_report *out) {
+  SPB_TRACE("sp_halo_run");
   return guarded([&] {
     need(out);
     if (method != SP_HALO_FUSED && method != SP_HALO_COPY && method != SP_HALO_DIRECT)

@@ -10,6 +10,7 @@
 #include "guard.hpp"
 #include "halo.hpp"
 #include "rt.hpp"
+#include "trace.hpp"
 
 using namespace spb;
 
@@ -132,6 +133,7 @@ sp_status sp_rt_choose(sp_type t, int64_t count, int *method) {
 
 sp_status sp_rt_send(const void *buf, uint64_t buf_bytes, int64_t count, sp_type t, int dest, int tag, int method,
                      int *used_method) {
+  SPB_TRACE("sp_rt_send");
   return guarded([&] {
     if (count < 0) fail(SP_ERR_INVALID_ARGUMENT, "send: negative count");
     RtTrace tr{};
@@ -142,6 +144,7 @@ sp_status sp_rt_send(const void *buf, uint64_t buf_bytes, int64_t count, sp_type
 
 sp_status sp_rt_recv(void *buf, uint64_t buf_bytes, int64_t count, sp_type t, int source, int tag,
                      int64_t status[4]) {
+  SPB_TRACE("sp_rt_recv");
   return guarded([&] {
     if (count < 0) fail(SP_ERR_INVALID_ARGUMENT, "recv: negative count");
     RtStatus st{};
@@ -167,6 +170,7 @@ void fill_status(const RtStatus &st, int64_t status[4]) {
 
 sp_status sp_rt_isend(const void *buf, uint64_t buf_bytes, int64_t count, sp_type t, int dest, int tag, int method,
                       sp_request *req) {
+  SPB_TRACE("sp_rt_isend");
   return guarded([&] {
     need(req);
     if (count < 0) fail(SP_ERR_INVALID_ARGUMENT, "send: negative count");
@@ -176,6 +180,7 @@ sp_status sp_rt_isend(const void *buf, uint64_t buf_bytes, int64_t count, sp_typ
 
 sp_status sp_rt_irecv(void *buf, uint64_t buf_bytes, int64_t count, sp_type t, int source, int tag,
                       sp_request *req) {
+  SPB_TRACE("sp_rt_irecv");
   return guarded([&] {
     need(req);
     if (count < 0) fail(SP_ERR_INVALID_ARGUMENT, "recv: negative count");
@@ -196,6 +201,7 @@ sp_status sp_rt_test(sp_request req, int *done, int64_t status[4]) {
 }
 
 sp_status sp_rt_wait(sp_request req, int64_t status[4]) {
+  SPB_TRACE("sp_rt_wait");
   return guarded([&] {
     RtStatus st{};
     rt_wait(req, &st);
@@ -211,6 +217,7 @@ sp_status sp_rt_neighbor_alltoallv(const void *sendbuf, const int64_t *sendcount
                                    int64_t outdegree, const int *dests, sp_type sendtype, void *recvbuf,
                                    const int64_t *recvcounts, const int64_t *rdispls, int64_t indegree,
                                    const int *sources, sp_type recvtype) {
+  SPB_TRACE("sp_rt_neighbor_alltoallv");
   return guarded([&] {
     if (outdegree < 0 || indegree < 0) fail(SP_ERR_INVALID_ARGUMENT, "negative degree");
     if ((outdegree && (!sendcounts || !sdispls || !dests)) || (indegree && (!recvcounts || !rdispls || !sources)))
@@ -227,6 +234,7 @@ sp_status sp_rt_neighbor_alltoallw(const void *sendbuf, const int64_t *sendcount
                                    const sp_type *sendtypes, int64_t outdegree, const int *dests, void *recvbuf,
                                    const int64_t *recvcounts, const int64_t *rdispls, const sp_type *recvtypes,
                                    int64_t indegree, const int *sources) {
+  SPB_TRACE("sp_rt_neighbor_alltoallw");
   return guarded([&] {
     if (outdegree < 0 || indegree < 0) fail(SP_ERR_INVALID_ARGUMENT, "negative degree");
     if ((outdegree && (!sendcounts || !sdispls || !sendtypes || !dests)) ||
@@ -361,6 +369,7 @@ sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int metho
 // collective; times[0..3] = pack, exchange, unpack, whole iteration (s),
 // measured with CUDA events on this rank's stream
 sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
+  SPB_TRACE("sp_halo_plan_exchange");
   return guarded([&] {
     need(p);
     cudaStream_t s = static_cast<cudaStream_t>(rt_stream());
