@@ -393,8 +393,10 @@ sp_status sp_rt_set_chunk(int64_t bytes);
  * sdispls[i]*extent) goes to dests[i]; block j from sources[j] lands at
  * rdispls[j]*extent(recvtype). ONE batch launch per rank packs every block
  * with sendtype straight into the receiving rank's buffer through CUDA IPC.
- * recvtype must be dense bytes (MPI_PACKED/MPI_BYTE-like). The k-th edge to
- * a rank matches that rank's k-th edge from this one. No host barrier: a
+ * With a dense-bytes recvtype (MPI_PACKED/MPI_BYTE-like) the blocks are
+ * packed into the receivers' buffers; with a strided recvtype each block is
+ * a typed copy straight to its strided place (the alltoallw path). The k-th
+ * edge to a rank matches that rank's k-th edge from this one. No host barrier: a
  * rank announces each call to its in-neighbours through shared memory,
  * waits only for its out-neighbours' announcements, and the data kernel
  * publishes per-pair READY counters to the receivers and waits (last CTA)

@@ -160,6 +160,8 @@ _sig("sp_rt_irecv", C.c_int, vp, u64, i64, sp_type, C.c_int, C.c_int, C.POINTER(
 _sig("sp_rt_test", C.c_int, C.c_uint64, C.POINTER(C.c_int), i64p)
 _sig("sp_rt_wait", C.c_int, C.c_uint64, i64p)
 _sig("sp_rt_set_chunk", C.c_int, i64)
+_sig("sp_rt_neighbor_alltoallv", C.c_int, vp, i64p, i64p, i64, C.POINTER(C.c_int), sp_type, vp, i64p, i64p, i64,
+     C.POINTER(C.c_int), sp_type)
 _sig("sp_rt_neighbor_alltoallw", C.c_int, vp, i64p, i64p, C.POINTER(sp_type), i64, C.POINTER(C.c_int), vp, i64p,
      i64p, C.POINTER(sp_type), i64, C.POINTER(C.c_int))
 _sig("sp_halo_plan_create", C.c_int, C.POINTER(HaloConfig), vp, C.c_int, C.POINTER(vp))

@@ -225,8 +225,22 @@ sp_status sp_rt_neighbor_alltoallv(const void *sendbuf, const int64_t *sendcount
     std::vector<int64_t> sc(sendcounts, sendcounts + outdegree), sd(sdispls, sdispls + outdegree);
     std::vector<int64_t> rc(recvcounts, recvcounts + indegree), rd(rdispls, rdispls + indegree);
     std::vector<int> ds(dests, dests + outdegree), ss(sources, sources + indegree);
-    rt_neighbor_alltoallv(static_cast<const uint8_t *>(sendbuf), sc, sd, *committed_of(sendtype),
-                          static_cast<uint8_t *>(recvbuf), rc, rd, *committed_of(recvtype), ss, ds);
+    const CommitPtr st = committed_of(sendtype), rtp = committed_of(recvtype);
+    const bool dense_recv = rtp->form == SP_FORM_EMPTY ||
+                            (rtp->form == SP_FORM_STRIDED && rtp->sb.ndims() == 1 && rtp->sb.start == 0 &&
+                             rtp->extent == rtp->size);
+    if (dense_recv) { // packed receive buffer: pack-to-peer batch
+      rt_neighbor_alltoallv(static_cast<const uint8_t *>(sendbuf), sc, sd, *st, static_cast<uint8_t *>(recvbuf), rc,
+                            rd, *rtp, ss, ds);
+      return;
+    }
+    // a strided receive type: the alltoallw path with that type on every
+    // edge (displacements in extents become bytes) -- typed copies straight
+    // into the receivers' strided buffers
+    for (auto &d : sd) d *= st->extent;
+    for (auto &d : rd) d *= rtp->extent;
+    rt_neighbor_alltoallw(static_cast<const uint8_t *>(sendbuf), sc, sd, std::vector<CommitPtr>(sc.size(), st),
+                          static_cast<uint8_t *>(recvbuf), rc, rd, std::vector<CommitPtr>(rc.size(), rtp), ss, ds);
   });
 }
 

@@ -165,6 +165,21 @@ class NeighborW:
                                             self.rt, self.ni, self.src))
 
 
+def neighbor_alltoallv(sendbuf, sendtype, sends, recvbuf, recvtype, recvs):
+    """MPI_Neighbor_alltoallv (collective): sends = [(dest, count,
+    displacement in sendtype extents)], recvs = [(source, count,
+    displacement in recvtype extents)]"""
+    sa = sendbuf if isinstance(sendbuf, int) else sendbuf.data_ptr()
+    ra = recvbuf if isinstance(recvbuf, int) else recvbuf.data_ptr()
+    no, ni = len(sends), len(recvs)
+    I64o, I64i = C.c_int64 * max(no, 1), C.c_int64 * max(ni, 1)
+    Io, Ii = C.c_int * max(no, 1), C.c_int * max(ni, 1)
+    _check(lib.sp_rt_neighbor_alltoallv(
+        sa, I64o(*[c for _, c, _ in sends]), I64o(*[d for _, _, d in sends]), no, Io(*[r for r, _, _ in sends]),
+        sendtype.handle, ra, I64i(*[c for _, c, _ in recvs]), I64i(*[d for _, _, d in recvs]), ni,
+        Ii(*[r for r, _, _ in recvs]), recvtype.handle))
+
+
 def neighbor_alltoallw(sendbuf, sends, recvbuf, recvs):
     """one-shot form of NeighborW"""
     NeighborW(sends, recvs)(sendbuf, recvbuf)

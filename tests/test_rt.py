@@ -309,6 +309,46 @@ def test_neighbor_alltoallw_layout_changes(cuda):
     assert all(_spawn(_nbrw, 3).values())
 
 
+def _nbrv(rank, world, job):
+    """MPI_Neighbor_alltoallv on a ring of 3 with a packed (bytes) and a
+    strided receive type, 2 objects per edge, displacements in extents"""
+    import torch
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.rt as rt
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=1 << 20, host_bytes=1 << 20)
+    right, left = (rank + 1) % world, (rank - 1) % world
+    B = sp.make_named(sp.NamedKind.Byte)
+    st = sp.commit_type(sp.make_vector(8, 24, 64, B))               # 192 B per object, extent 472
+    dense = sp.commit_type(sp.make_contiguous(192, B))
+    strided = sp.commit_type(sp.make_hvector(12, 16, 40, B))        # 192 B, extent 456
+    src = torch.arange(4096, dtype=torch.int64, device="cuda").mul_(13).add_(rank * 7).to(torch.uint8)
+    lsrc = torch.arange(4096, dtype=torch.int64, device="cuda").mul_(13).add_(left * 7).to(torch.uint8)
+    rsrc = torch.arange(4096, dtype=torch.int64, device="cuda").mul_(13).add_(right * 7).to(torch.uint8)
+    ok = True
+    for rt_type in (dense, strided):
+        for it in range(2):
+            recv = torch.full((8192,), 0xEE, dtype=torch.uint8, device="cuda")
+            torch.cuda.synchronize()
+            # 2 objects to the right at displacement 1, 2 objects to the left at displacement 4
+            rt.neighbor_alltoallv(src, st, [(right, 2, 1), (left, 2, 4)], recv, rt_type, [(left, 2, 0), (right, 2, 6)])
+            want = torch.full_like(recv, 0xEE)
+            pk = torch.empty(2 * 192, dtype=torch.uint8, device="cuda")
+            for peer_src, sdisp, rdisp in ((lsrc, 1, 0), (rsrc, 4, 6)):
+                sp.pack(peer_src[sdisp * st.extent:], st, 2, pk, 0)
+                sp.unpack(pk, 0, rt_type, 2, want[rdisp * rt_type.extent:])
+            torch.cuda.synchronize()
+            ok = ok and bool(torch.equal(recv, want))
+            assert ok, (rank, rt_type is strided, it)
+    rt.finalize()
+    return ok
+
+
+@pytest.mark.gpu
+def test_neighbor_alltoallv_packed_and_strided_receive(cuda):
+    assert all(_spawn(_nbrv, 3).values())
+
+
 def _halo(rank, world, job, ranks, method):
     import torch
     import paper_2012_14363_b200.halo as H
