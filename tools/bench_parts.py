@@ -240,6 +240,8 @@ def send_section(torch, rank, world, local, job, reps=10, warmup=3):
                     row[name + "_GBps"] = round(ct.size / statistics.median(ts) / 1e9, 2)
                     if name == "model":
                         row["model_choice"] = {0: "oneshot", 1: "device", 2: "staged", 3: "direct"}[used]
+                        row["model_frac_of_nvlink"] = round(ct.size / statistics.median(ts) / 1e9 /
+                                                            NVLINK_MEASURED_GBPS, 3)
             rows.append(row)
     rt.finalize()
     return {"pair": [0, 1], "timing": "half ping-pong wall time (host-synchronous MPI_Send/Recv semantics)",
