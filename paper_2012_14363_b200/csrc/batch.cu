@@ -1,0 +1,728 @@
+// batch.cu -- many-job launches (pack, unpack, typed copy), single-job
+// ranged launches (pipelined message chunks, sp_copy) and the in-kernel
+// completion protocol of the distributed halo and neighbour collectives.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "core.hpp"
+#include "kernels.cuh"
+
+namespace spb {
+
+// ============================================================ batches
+// A persistent list of jobs executed by ONE launch per word size. A job is
+//   PACK   (type, count, strided src) -> packed dst
+//   UNPACK packed src -> (type, count, strided dst)
+//   COPY   (type S, count, strided src) -> (type D, count', strided dst),
+//          byte k of S's pack order lands on byte k of D's: a typed copy
+//          with no packed intermediate (halo ghost writes, alltoallw).
+// Destinations may be peer-GPU memory mapped over NVLink (CUDA IPC), which
+// turns the batch into a fused pack-to-peer / copy-to-peer.
+//
+// Work distribution: the words of all jobs form one index space, split into
+// equal contiguous ranges, one per CTA of a single resident wave (grid =
+// SMs x resident CTAs per SM). Each thread moves U words per round with all
+// U loads issued before the first store, so a CTA's whole range is usually
+// one or two DRAM round trips and no CTA waits on a straggler chunk. Within
+// a round a thread finds its job by walking forward from the CTA's first
+// job (ranges rarely cross a job boundary); the job descriptors are read
+// through the read-only path and stay L1-resident.
+constexpr int kBatchU = 4;                            // words in flight per thread
+constexpr uint32_t kBatchChunk = 256 * kBatchU;       // words per unit of work
+enum : int { kModeUnpack = 0, kModePack = 1, kModeCopy = 2 };
+
+struct BatchJob {
+  Geom gs;           // strided-side geometry of the source (PACK, COPY)
+  Geom gd;           // strided-side geometry of the destination (UNPACK, COPY)
+  const uint8_t *in; // source base (strided sources already at start)
+  uint8_t *out;      // destination base
+  uint64_t begin;    // first word of this job in the launch's index space
+  uint32_t q0;       // first word of the job's own stream this launch moves
+                     // (non-zero for one chunk of a pipelined message)
+  int same;          // COPY with gd == gs: destination offset = source offset
+};
+
+// Optional in-kernel completion protocol (distributed halo): every block
+// first waits until each `wait` flag (local memory, written by peers over
+// NVLink) reaches wait_value; after the last word, the LAST block to finish
+// publishes signal_value to each `signal` flag (peer memory) with a
+// system-scope release store, after fences by every block.
+constexpr int kMaxSig = 32;
+struct BatchSig {
+  const unsigned long long *wait[kMaxSig];
+  unsigned long long *signal[kMaxSig];
+  unsigned long long wait_value, signal_value;
+  unsigned *done; // block-completion counter of this launch (device memory)
+  int n_wait, n_signal;
+  int sys_scope;  // some destination lives on another GPU: system-scope fences
+  // published by block 0 BEFORE waiting (consumer-side "ready" flags: the
+  // stream order guarantees everything before this launch has completed)
+  unsigned long long *pre[kMaxSig];
+  unsigned long long pre_value;
+  int n_pre;
+  // waited for by the LAST block after it signalled (completion of the
+  // peers' writes into this rank's memory folded into the same launch)
+  const unsigned long long *post[kMaxSig];
+  unsigned long long post_value;
+  int n_post;
+  // per-target values (neighbour collectives count calls per peer pair);
+  // used instead of signal_value / post_value when per_target is set
+  unsigned long long signal_vals[kMaxSig], post_vals[kMaxSig];
+  int per_target;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// byte offset of word q on a strided side
+template <int W> __device__ __forceinline__ int64_t word_offset(uint32_t q, const Geom &g) {
+  const uint32_t row = fdiv(q, g.wdiv);
+  return row_offset(row, g) + static_cast<int64_t>(q - row * g.wpr) * W;
+}
+
+// words of chunk `c` (job-local) of job J: U per thread, all U loads issued
+// before the first store; geometry read from J (shared or param memory)
+template <int W, int MODE> __device__ __forceinline__ void move_chunk(const BatchJob &J, uint32_t c, uint32_t words) {
+  using T = typename Word<W>::T;
+  const uint32_t base = c * kBatchChunk + threadIdx.x;
+  T v[kBatchU];
+  int64_t doff[kBatchU];
+#pragma unroll
+  for (int u = 0; u < kBatchU; ++u) {
+    const uint32_t q = base + u * 256;
+    if (q < words) {
+      const uint32_t ql = q + J.q0;
+      if (MODE == kModeUnpack) {
+        v[u] = ld_stream(reinterpret_cast<const T *>(J.in) + ql);
+        doff[u] = word_offset<W>(ql, J.gd);
+      } else {
+        const int64_t so = word_offset<W>(ql, J.gs);
+        v[u] = ld_stream(reinterpret_cast<const T *>(J.in + so));
+        if (MODE == kModePack) {
+          doff[u] = static_cast<int64_t>(ql) * W;
+        } else {
+          doff[u] = J.same ? so : word_offset<W>(ql, J.gd);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kBatchU; ++u)
+    if (base + u * 256 < words) st_stream(reinterpret_cast<T *>(J.out + doff[u]), v[u]);
+}
+
+__device__ __forceinline__ void batch_prologue(const BatchSig &sig) {
+  if (sig.n_pre && blockIdx.x == 0 && threadIdx.x < static_cast<unsigned>(sig.n_pre))
+    st_release_sys(sig.pre[threadIdx.x], sig.pre_value);
+  if (sig.n_wait) {
+    if (threadIdx.x < static_cast<unsigned>(sig.n_wait))
+      while (ld_acquire_sys(sig.wait[threadIdx.x]) < sig.wait_value) __nanosleep(64);
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void batch_epilogue(const BatchSig &sig) {
+  if (sig.n_signal || sig.n_post) {
+    // bar.sync orders every thread's stores before thread 0 (CTA scope);
+    // thread 0's fence is cumulative over them: GPU scope when every
+    // destination is on this device, system scope when some were written
+    // over NVLink into a peer GPU
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (sig.sys_scope) {
+        __threadfence_system();
+      } else {
+        __threadfence();
+      }
+    }
+    __shared__ int last;
+    if (threadIdx.x == 0) last = atomicAdd(sig.done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last) {
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int i = 0; i < sig.n_signal; ++i)
+          st_release_sys(sig.signal[i], sig.per_target ? sig.signal_vals[i] : sig.signal_value);
+        atomicExch(sig.done, 0u); // ready for the next launch on this stream
+      }
+      // every other block of this launch has finished, so waiting here
+      // cannot starve them; the peers publish before they wait, so the
+      // ranks' last blocks cannot wait on each other in a cycle
+      if (threadIdx.x < static_cast<unsigned>(sig.n_post))
+        while (ld_acquire_sys(sig.post[threadIdx.x]) <
+               (sig.per_target ? sig.post_vals[threadIdx.x] : sig.post_value))
+          __nanosleep(32);
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t job_words(const BatchJob &J, int mode) {
+  return static_cast<uint32_t>(mode == kModeUnpack ? J.gd.total : J.gs.total);
+}
+
+// Every chunk (kBatchChunk words of one job) is a unit of work; CTAs walk
+// the chunks grid-stride, so each CTA sees chunks of every job (the slow
+// 64-B-row regions of a halo spread over the whole grid) and the grid stays
+// one resident wave at full occupancy. The chunk's job is found by binary
+// search on the jobs' first-chunk indices and staged in shared memory.
+template <int W, int MODE>
+__global__ void __launch_bounds__(256) k_batch(const BatchJob *__restrict__ jobs, int njobs, uint32_t nchunks,
+                                               const BatchSig sig) {
+  batch_prologue(sig);
+  __shared__ BatchJob sj;
+  int loaded = -1;
+  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    int a = 0, b = njobs - 1;
+    while (a < b) {
+      const int m = (a + b + 1) >> 1;
+      if (jobs[m].begin <= c) {
+        a = m;
+      } else {
+        b = m - 1;
+      }
+    }
+    if (a != loaded) {
+      __syncthreads();
+      const uint32_t *src = reinterpret_cast<const uint32_t *>(jobs + a);
+      uint32_t *dst = reinterpret_cast<uint32_t *>(&sj);
+      for (uint32_t i = threadIdx.x; i < sizeof(BatchJob) / 4; i += blockDim.x) dst[i] = src[i];
+      __syncthreads();
+      loaded = a;
+    }
+    move_chunk<W, MODE>(sj, c - static_cast<uint32_t>(sj.begin), job_words(sj, MODE) - sj.q0);
+  }
+  batch_epilogue(sig);
+}
+
+// one job passed by value (param space): a single message or message chunk
+// launches without uploading a descriptor; `words` from q0 on
+template <int W, int MODE>
+__global__ void __launch_bounds__(256) k_job(const __grid_constant__ BatchJob job, uint32_t words) {
+  const uint32_t nchunks = (words + kBatchChunk - 1) / kBatchChunk;
+  for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) move_chunk<W, MODE>(job, c, words);
+}
+
+// ---- compact job tables in kernel-parameter space
+// A batch of up to kParamJobs jobs whose geometries have at most 3 row dims
+// (every halo region, every cfg1-cfg4 object) travels by value: the
+// chunk -> job search and every descriptor read hit the constant cache, so
+// a chunk starts with no dependent global load and no barrier, and word
+// offsets are computed from registers.
+constexpr int kParamJobs = 32;
+struct CGeom {
+  uint32_t wpr, c0, c1;
+  int32_t nd;
+  FastDiv wdiv, d0, d1;
+  int64_t s0, s1, s2;
+  uint32_t total; // words of the job's stream
+  uint32_t pad;
+};
+struct CJob {
+  const uint8_t *in;
+  uint8_t *out;
+  CGeom gs, gd;
+  uint32_t begin; // first chunk
+  uint32_t q0;
+  int32_t same;
+  int32_t pad;
+};
+struct CTable {
+  CJob jobs[kParamJobs];
+  int32_t njobs;
+  uint32_t nchunks;
+};
+
+template <int W> __device__ __forceinline__ int64_t c_offset(uint32_t q, const CGeom &r) {
+  const uint32_t row = fdiv(q, r.wdiv);
+  int64_t off = static_cast<int64_t>(q - row * r.wpr) * W;
+  if (r.nd <= 1) return r.nd == 1 ? off + static_cast<int64_t>(row) * r.s0 : off;
+  const uint32_t q1 = fdiv(row, r.d0);
+  off += static_cast<int64_t>(row - q1 * r.c0) * r.s0;
+  if (r.nd == 2) return off + static_cast<int64_t>(q1) * r.s1;
+  const uint32_t q2 = fdiv(q1, r.d1);
+  return off + static_cast<int64_t>(q1 - q2 * r.c1) * r.s1 + static_cast<int64_t>(q2) * r.s2;
+}
+
+template <int W, int MODE>
+__global__ void __launch_bounds__(256) k_batchp(const __grid_constant__ CTable t, const BatchSig sig) {
+  using T = typename Word<W>::T;
+  batch_prologue(sig);
+  for (uint32_t c = blockIdx.x; c < t.nchunks; c += gridDim.x) {
+    int a = 0, b = t.njobs - 1;
+    while (a < b) {
+      const int m = (a + b + 1) >> 1;
+      if (t.jobs[m].begin <= c) {
+        a = m;
+      } else {
+        b = m - 1;
+      }
+    }
+    const CJob &J = t.jobs[a];
+    const uint32_t words = (MODE == kModeUnpack ? J.gd.total : J.gs.total) - J.q0;
+    const uint32_t base = (c - J.begin) * kBatchChunk + threadIdx.x;
+    T v[kBatchU];
+    int64_t doff[kBatchU];
+#pragma unroll
+    for (int u = 0; u < kBatchU; ++u) {
+      const uint32_t q = base + u * 256;
+      if (q < words) {
+        const uint32_t ql = q + J.q0;
+        if (MODE == kModeUnpack) {
+          v[u] = ld_stream(reinterpret_cast<const T *>(J.in) + ql);
+          doff[u] = c_offset<W>(ql, J.gd);
+        } else {
+          const int64_t so = c_offset<W>(ql, J.gs);
+          v[u] = ld_stream(reinterpret_cast<const T *>(J.in + so));
+          if (MODE == kModePack) {
+            doff[u] = static_cast<int64_t>(ql) * W;
+          } else {
+            doff[u] = J.same ? so : c_offset<W>(ql, J.gd);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kBatchU; ++u)
+      if (base + u * 256 < words) st_stream(reinterpret_cast<T *>(J.out + doff[u]), v[u]);
+  }
+  batch_epilogue(sig);
+}
+
+struct BatchGroup {
+  int w = 0, mode = 0;
+  BatchJob *d_jobs = nullptr;
+  int njobs = 0;
+  uint32_t nchunks = 0;
+  std::shared_ptr<CTable> table; // set when the jobs fit kernel-parameter space
+};
+
+struct Batch {
+  int device = -1;
+  std::vector<BatchGroup> groups;
+  int64_t bytes = 0; // payload bytes moved per execution
+  ~Batch() {
+    for (auto &g : groups) cudaFree(g.d_jobs);
+  }
+};
+
+namespace {
+
+Geom batch_geom(const RowDims &rd, int w) {
+  if (static_cast<int>(rd.cnt.size()) > KMAX) fail(SP_ERR_UNSUPPORTED, "batch: too many row dimensions");
+  uint64_t rows = 1;
+  for (int64_t c : rd.cnt) rows *= static_cast<uint64_t>(c);
+  const uint64_t words = rows * static_cast<uint64_t>(rd.c0) / static_cast<uint64_t>(w);
+  if (words >= (1ull << 32) || rows >= (1ull << 32) || rd.c0 / w >= (int64_t{1} << 32))
+    fail(SP_ERR_UNSUPPORTED, "batch: job larger than 2^32 words");
+  Geom g{};
+  g.nd = static_cast<int>(rd.cnt.size());
+  for (int k = 0; k < g.nd; ++k) {
+    g.cnt[k] = static_cast<uint32_t>(rd.cnt[k]);
+    g.div[k] = make_fastdiv(g.cnt[k]);
+    g.str[k] = rd.str[k];
+    g.back[k] = rd.cnt[k] * rd.str[k];
+  }
+  g.wpr = static_cast<uint32_t>(rd.c0 / w);
+  g.wdiv = make_fastdiv(g.wpr);
+  g.total = words;
+  g.rows = rows;
+  return g;
+}
+
+uint64_t align_bits(const RowDims &rd, uint64_t base) {
+  uint64_t g_or = static_cast<uint64_t>(rd.c0) | base;
+  for (int64_t st : rd.str) g_or |= static_cast<uint64_t>(st);
+  return g_or;
+}
+
+bool same_geom(const RowDims &a, const RowDims &b) { return a.c0 == b.c0 && a.cnt == b.cnt && a.str == b.str; }
+
+// device-accessible address of a batch buffer (device, pinned or peer-mapped)
+const uint8_t *batch_ptr(const void *p) {
+  const Resolved r = resolve(p);
+  if (r.kind == MemKind::Pageable)
+    fail(SP_ERR_INVALID_ARGUMENT, "batch: buffers must be device, pinned or peer-mapped memory");
+  return r.dptr;
+}
+
+Batch *build_batch(std::vector<BatchJob> (&by_w)[5], int mode, int64_t bytes) {
+  auto b = std::make_unique<Batch>();
+  cuda_check(cudaGetDevice(&b->device), "cudaGetDevice");
+  b->bytes = bytes;
+  for (int wi = 4; wi >= 0; --wi) {
+    auto &jobs = by_w[wi];
+    if (jobs.empty()) continue;
+    BatchGroup g;
+    g.w = 1 << wi;
+    g.mode = mode;
+    uint64_t chunks = 0;
+    for (BatchJob &j : jobs) {
+      j.begin = chunks; // first chunk of the job
+      chunks += ((mode == kModeUnpack ? j.gd.total : j.gs.total) + kBatchChunk - 1) / kBatchChunk;
+      if (chunks >= (1ull << 32)) fail(SP_ERR_UNSUPPORTED, "batch: too much work for one launch");
+    }
+    g.njobs = static_cast<int>(jobs.size());
+    g.nchunks = static_cast<uint32_t>(chunks);
+    bool compact = jobs.size() <= static_cast<size_t>(kParamJobs);
+    for (const BatchJob &j : jobs) {
+      const bool needs_s = mode != kModeUnpack, needs_d = mode == kModeUnpack || (mode == kModeCopy && !j.same);
+      compact = compact && (!needs_s || j.gs.nd <= 3) && (!needs_d || j.gd.nd <= 3);
+    }
+    if (compact) {
+      auto t = std::make_shared<CTable>();
+      std::memset(t.get(), 0, sizeof(CTable));
+      auto cg = [](const Geom &g) {
+        CGeom c{};
+        c.nd = g.nd;
+        c.wpr = g.wpr;
+        c.wdiv = g.wdiv;
+        c.c0 = g.cnt[0];
+        c.c1 = g.cnt[1];
+        c.d0 = g.div[0];
+        c.d1 = g.div[1];
+        c.s0 = g.str[0];
+        c.s1 = g.str[1];
+        c.s2 = g.str[2];
+        c.total = static_cast<uint32_t>(g.total);
+        return c;
+      };
+      for (size_t i = 0; i < jobs.size(); ++i) {
+        CJob &c = t->jobs[i];
+        c.in = jobs[i].in;
+        c.out = jobs[i].out;
+        c.gs = cg(jobs[i].gs);
+        c.gd = cg(jobs[i].gd);
+        c.begin = static_cast<uint32_t>(jobs[i].begin);
+        c.q0 = jobs[i].q0;
+        c.same = jobs[i].same;
+      }
+      t->njobs = g.njobs;
+      t->nchunks = g.nchunks;
+      g.table = t;
+    }
+    cuda_check(cudaMalloc(&g.d_jobs, jobs.size() * sizeof(BatchJob)), "cudaMalloc(batch)");
+    b->groups.push_back(g);
+    cuda_check(cudaMemcpy(g.d_jobs, jobs.data(), jobs.size() * sizeof(BatchJob), cudaMemcpyHostToDevice),
+               "upload batch");
+  }
+  return b.release();
+}
+
+} // namespace
+
+namespace {
+
+// validated job of one (type, count, buffers) pack or unpack; `align` is
+// OR-ed into the word-size choice (chunk boundaries of a pipelined message).
+// Returns false for an Empty form (nothing to move).
+bool make_pack_job(const BatchSpec &s, bool unpack, uint64_t align, BatchJob &j, int &w) {
+  const Committed &ct = *s.ct;
+  // argument checks in the reference's precedence (pack.hpp:102-126 / :146-159)
+  if (s.count < 1 || s.position < 0) fail(SP_ERR_INVALID_ARGUMENT, "batch: count must be positive, position >= 0");
+  if (unpack && ct.overlapping) fail(SP_ERR_OVERLAPPING_LAYOUT, "batch: unpack layout describes overlapping bytes");
+  const uint64_t packed_need = static_cast<uint64_t>(s.position + s.count * ct.size);
+  if (packed_need > (unpack ? s.src_bytes : s.dst_bytes)) fail(SP_ERR_BUFFER_TOO_SMALL, "batch: packed buffer too small");
+  if (ct.form == SP_FORM_EMPTY) return false;
+  const uint64_t strided_need = static_cast<uint64_t>((s.count - 1) * ct.extent + ct.span);
+  if (strided_need > (unpack ? s.dst_bytes : s.src_bytes)) fail(SP_ERR_BUFFER_TOO_SMALL, "batch: strided buffer too small");
+  if (ct.form != SP_FORM_STRIDED) fail(SP_ERR_UNSUPPORTED, "batch: only strided forms can be batched");
+  const uint8_t *strided = batch_ptr(unpack ? s.dst : s.src) + ct.sb.start;
+  const uint8_t *packed = batch_ptr(unpack ? s.src : s.dst) + s.position;
+  const RowDims rd = row_dims(ct, s.count);
+  w = pow2_align(align_bits(rd, reinterpret_cast<uint64_t>(strided)) | reinterpret_cast<uint64_t>(packed) | align);
+  j = BatchJob{};
+  const Geom g = batch_geom(rd, w);
+  if (unpack) {
+    j.gd = g;
+  } else {
+    j.gs = g;
+  }
+  j.in = unpack ? packed : strided;
+  j.out = const_cast<uint8_t *>(unpack ? strided : packed);
+  return true;
+}
+
+bool make_copy_job(const CopySpec &s, uint64_t align, BatchJob &j, int &w) {
+  const Committed &sc = *s.sct, &dc = *s.dct;
+  if (s.scount < 0 || s.dcount < 0) fail(SP_ERR_INVALID_ARGUMENT, "copy: counts must be >= 0");
+  if (s.scount * sc.size != s.dcount * dc.size)
+    fail(SP_ERR_INVALID_ARGUMENT, "copy: source and destination describe different byte counts");
+  if (dc.overlapping) fail(SP_ERR_OVERLAPPING_LAYOUT, "copy: destination layout describes overlapping bytes");
+  if (s.scount * sc.size == 0) return false;
+  if (static_cast<uint64_t>((s.scount - 1) * sc.extent + sc.span) > s.src_bytes)
+    fail(SP_ERR_BUFFER_TOO_SMALL, "copy: source too small");
+  if (static_cast<uint64_t>((s.dcount - 1) * dc.extent + dc.span) > s.dst_bytes)
+    fail(SP_ERR_BUFFER_TOO_SMALL, "copy: destination too small");
+  if (sc.form != SP_FORM_STRIDED || dc.form != SP_FORM_STRIDED)
+    fail(SP_ERR_UNSUPPORTED, "copy: only strided forms can be batched");
+  const uint8_t *src = batch_ptr(s.src) + sc.sb.start;
+  const uint8_t *dst = batch_ptr(s.dst) + dc.sb.start;
+  const RowDims rs = row_dims(sc, s.scount), rd = row_dims(dc, s.dcount);
+  w = pow2_align(align_bits(rs, reinterpret_cast<uint64_t>(src)) | align_bits(rd, reinterpret_cast<uint64_t>(dst)) |
+                 align);
+  j = BatchJob{};
+  j.gs = batch_geom(rs, w);
+  j.gd = batch_geom(rd, w);
+  j.same = same_geom(rs, rd) ? 1 : 0;
+  j.in = src;
+  j.out = const_cast<uint8_t *>(dst);
+  return true;
+}
+
+} // namespace
+
+Batch *batch_create(const std::vector<BatchSpec> &specs, bool unpack) {
+  require_device();
+  std::vector<BatchJob> by_w[5]; // W = 1, 2, 4, 8, 16
+  int64_t bytes = 0;
+  for (const BatchSpec &s : specs) {
+    BatchJob j;
+    int w = 1;
+    if (!make_pack_job(s, unpack, 0, j, w)) continue;
+    by_w[__builtin_ctz(static_cast<unsigned>(w))].push_back(j);
+    bytes += s.count * s.ct->size;
+  }
+  return build_batch(by_w, unpack ? kModeUnpack : kModePack, bytes);
+}
+
+Batch *copy_batch_create(const std::vector<CopySpec> &specs) {
+  require_device();
+  std::vector<BatchJob> by_w[5];
+  int64_t bytes = 0;
+  for (const CopySpec &s : specs) {
+    BatchJob j;
+    int w = 1;
+    if (!make_copy_job(s, 0, j, w)) continue;
+    by_w[__builtin_ctz(static_cast<unsigned>(w))].push_back(j);
+    bytes += s.scount * s.sct->size;
+  }
+  return build_batch(by_w, kModeCopy, bytes);
+}
+
+namespace {
+
+template <int W, int MODE> void launch_batch(const BatchGroup &g, const BatchSig &sig, cudaStream_t s, unsigned &grid) {
+  static thread_local int occ_dev = -1, occ = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (occ_dev != dev) {
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_batch<W, MODE>, 256, 0), "occupancy");
+    occ = std::max(occ, 1);
+    occ_dev = dev;
+  }
+  grid = static_cast<unsigned>(
+      std::max<uint64_t>(1, std::min<uint64_t>(g.nchunks, static_cast<uint64_t>(sm_count()) * occ)));
+  if (g.table) {
+    k_batchp<W, MODE><<<grid, 256, 0, s>>>(*g.table, sig);
+  } else {
+    k_batch<W, MODE><<<grid, 256, 0, s>>>(g.d_jobs, g.njobs, g.nchunks, sig);
+  }
+}
+
+template <int W> void launch_batch_w(const BatchGroup &g, const BatchSig &sig, cudaStream_t s, unsigned &grid) {
+  switch (g.mode) {
+  case kModePack: launch_batch<W, kModePack>(g, sig, s, grid); break;
+  case kModeUnpack: launch_batch<W, kModeUnpack>(g, sig, s, grid); break;
+  default: launch_batch<W, kModeCopy>(g, sig, s, grid); break;
+  }
+}
+
+void batch_launch(const Batch &b, void *stream, const BatchSignal *bs) {
+  sp_launch_info li{};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (size_t gi = 0; gi < b.groups.size(); ++gi) {
+    const BatchGroup &g = b.groups[gi];
+    BatchSig sig{};
+    if (bs) { // pre-signal and wait in the first kernel, signal from the last
+      if (bs->wait.size() > static_cast<size_t>(kMaxSig) || bs->signal.size() > static_cast<size_t>(kMaxSig) ||
+          bs->pre.size() > static_cast<size_t>(kMaxSig))
+        fail(SP_ERR_UNSUPPORTED, "batch signalling: more than 32 peers");
+      if (gi == 0) {
+        sig.n_pre = static_cast<int>(bs->pre.size());
+        for (int i = 0; i < sig.n_pre; ++i) sig.pre[i] = reinterpret_cast<unsigned long long *>(bs->pre[i]);
+        sig.pre_value = bs->pre_value;
+        sig.n_wait = static_cast<int>(bs->wait.size());
+        for (int i = 0; i < sig.n_wait; ++i) sig.wait[i] = reinterpret_cast<const unsigned long long *>(bs->wait[i]);
+        sig.wait_value = bs->wait_value;
+      }
+      if (gi + 1 == b.groups.size()) {
+        sig.n_signal = static_cast<int>(bs->signal.size());
+        for (int i = 0; i < sig.n_signal; ++i) sig.signal[i] = reinterpret_cast<unsigned long long *>(bs->signal[i]);
+        sig.signal_value = bs->signal_value;
+        sig.done = bs->done;
+        sig.sys_scope = bs->sys_scope ? 1 : 0;
+        if (bs->post.size() > static_cast<size_t>(kMaxSig)) fail(SP_ERR_UNSUPPORTED, "batch signalling: more than 32 peers");
+        sig.n_post = static_cast<int>(bs->post.size());
+        for (int i = 0; i < sig.n_post; ++i) sig.post[i] = reinterpret_cast<const unsigned long long *>(bs->post[i]);
+        sig.post_value = bs->post_value;
+        if (!bs->signal_values.empty() || !bs->post_values.empty()) {
+          if (bs->signal_values.size() != bs->signal.size() || bs->post_values.size() != bs->post.size())
+            fail(SP_ERR_INTERNAL, "batch signalling: per-target values do not match the targets");
+          sig.per_target = 1;
+          for (int i = 0; i < sig.n_signal; ++i) sig.signal_vals[i] = bs->signal_values[i];
+          for (int i = 0; i < sig.n_post; ++i) sig.post_vals[i] = bs->post_values[i];
+        }
+      }
+    }
+    unsigned grid = 0;
+    switch (g.w) {
+    case 16: launch_batch_w<16>(g, sig, s, grid); break;
+    case 8: launch_batch_w<8>(g, sig, s, grid); break;
+    case 4: launch_batch_w<4>(g, sig, s, grid); break;
+    case 2: launch_batch_w<2>(g, sig, s, grid); break;
+    default: launch_batch_w<1>(g, sig, s, grid); break;
+    }
+    cuda_check(cudaGetLastError(), "k_batch launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    li.kernel = SP_KERNEL_BATCH;
+    li.launches += 1;
+    li.grid = grid;
+    li.block = 256;
+  }
+  set_last_launch(li);
+}
+} // namespace
+
+
+namespace {
+
+template <int W, int MODE> void launch_job(const BatchJob &j, uint32_t words, cudaStream_t s) {
+  static thread_local int occ_dev = -1, occ = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (occ_dev != dev) {
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_job<W, MODE>, 256, 0), "occupancy");
+    occ = std::max(occ, 1);
+    occ_dev = dev;
+  }
+  const uint64_t want = (static_cast<uint64_t>(words) + kBatchChunk - 1) / kBatchChunk;
+  uint64_t cap = static_cast<uint64_t>(sm_count()) * occ;
+  if (t_host_grid_cap) cap = std::min<uint64_t>(cap, t_host_grid_cap);
+  const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, cap)));
+  k_job<W, MODE><<<grid, 256, 0, s>>>(j, words);
+  cuda_check(cudaGetLastError(), "k_job launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  sp_launch_info li{};
+  li.kernel = SP_KERNEL_BATCH;
+  li.word = W;
+  li.launches = 1;
+  li.grid = grid;
+  li.block = 256;
+  set_last_launch(li);
+}
+
+template <int MODE> void launch_job_w(int w, const BatchJob &j, uint32_t words, cudaStream_t s) {
+  switch (w) {
+  case 16: launch_job<16, MODE>(j, words, s); break;
+  case 8: launch_job<8, MODE>(j, words, s); break;
+  case 4: launch_job<4, MODE>(j, words, s); break;
+  case 2: launch_job<2, MODE>(j, words, s); break;
+  default: launch_job<1, MODE>(j, words, s); break;
+  }
+}
+
+// words [lo/w, hi/w) of a job's stream in one launch
+void launch_range(int mode, int w, BatchJob j, uint64_t total_bytes, uint64_t lo, uint64_t hi, cudaStream_t s) {
+  if (hi > total_bytes || lo > hi) fail(SP_ERR_INVALID_ARGUMENT, "range outside the message");
+  if (lo == hi) return;
+  if ((hi - lo) / w >= (1ull << 32) || hi / w >= (1ull << 32)) fail(SP_ERR_UNSUPPORTED, "range larger than 2^32 words");
+  j.begin = 0;
+  j.q0 = static_cast<uint32_t>(lo / w);
+  const uint32_t words = static_cast<uint32_t>((hi - lo) / w);
+  switch (mode) {
+  case kModePack: launch_job_w<kModePack>(w, j, words, s); break;
+  case kModeUnpack: launch_job_w<kModeUnpack>(w, j, words, s); break;
+  default: launch_job_w<kModeCopy>(w, j, words, s); break;
+  }
+}
+
+// chunk boundaries strictly inside the message carry alignment; the end of
+// the message is a whole number of words by construction
+uint64_t range_align(uint64_t lo, uint64_t hi, uint64_t total) { return lo | (hi == total ? 0 : hi); }
+
+} // namespace
+
+bool range_capable(const Committed &ct, int64_t count, const void *strided, const void *packed) {
+  if (ct.form != SP_FORM_STRIDED || count < 1) return false;
+  if (static_cast<int>(row_dims(ct, count).cnt.size()) > KMAX) return false;
+  const Resolved a = resolve(strided), b = resolve(packed);
+  return a.kind != MemKind::Pageable && b.kind != MemKind::Pageable;
+}
+
+void range_execute(const BatchSpec &spec, bool unpack, uint64_t lo, uint64_t hi, void *stream) {
+  require_device();
+  const uint64_t total = static_cast<uint64_t>(spec.count * spec.ct->size);
+  BatchJob j;
+  int w = 1;
+  if (!make_pack_job(spec, unpack, range_align(lo, hi, total), j, w)) return;
+  launch_range(unpack ? kModeUnpack : kModePack, w, j, total, lo, hi, static_cast<cudaStream_t>(stream));
+}
+
+void copy_execute(const CopySpec &spec, uint64_t lo, uint64_t hi, void *stream) {
+  require_device();
+  const uint64_t total = static_cast<uint64_t>(spec.scount * spec.sct->size);
+  BatchJob j;
+  int w = 1;
+  if (!make_copy_job(spec, range_align(lo, hi, total), j, w)) return;
+  launch_range(kModeCopy, w, j, total, lo, hi, static_cast<cudaStream_t>(stream));
+}
+
+// one warp: release-store each signal, then wait for each post flag; the
+// completion protocol of a neighbour call that moves no bytes
+__global__ void k_flag_signal_wait(const BatchSig sig) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int i = 0; i < sig.n_signal; ++i)
+      st_release_sys(sig.signal[i], sig.per_target ? sig.signal_vals[i] : sig.signal_value);
+  }
+  if (threadIdx.x < static_cast<unsigned>(sig.n_post))
+    while (ld_acquire_sys(sig.post[threadIdx.x]) < (sig.per_target ? sig.post_vals[threadIdx.x] : sig.post_value))
+      __nanosleep(32);
+}
+
+void flags_signal_wait(const BatchSignal &bs, void *stream) {
+  if (bs.signal.size() > static_cast<size_t>(kMaxSig) || bs.post.size() > static_cast<size_t>(kMaxSig))
+    fail(SP_ERR_UNSUPPORTED, "flag signalling: more than 32 peers");
+  if (bs.signal.empty() && bs.post.empty()) return;
+  BatchSig sig{};
+  sig.n_signal = static_cast<int>(bs.signal.size());
+  sig.n_post = static_cast<int>(bs.post.size());
+  for (int i = 0; i < sig.n_signal; ++i) sig.signal[i] = reinterpret_cast<unsigned long long *>(bs.signal[i]);
+  for (int i = 0; i < sig.n_post; ++i) sig.post[i] = reinterpret_cast<const unsigned long long *>(bs.post[i]);
+  sig.signal_value = bs.signal_value;
+  sig.post_value = bs.post_value;
+  if (!bs.signal_values.empty() || !bs.post_values.empty()) {
+    sig.per_target = 1;
+    for (int i = 0; i < sig.n_signal; ++i) sig.signal_vals[i] = bs.signal_values[i];
+    for (int i = 0; i < sig.n_post; ++i) sig.post_vals[i] = bs.post_values[i];
+  }
+  k_flag_signal_wait<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(sig);
+  cuda_check(cudaGetLastError(), "k_flag_signal_wait launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void batch_execute(const Batch &b, void *stream) { batch_launch(b, stream, nullptr); }
+
+void batch_execute_signaled(const Batch &b, void *stream, const BatchSignal &sig) {
+  if (b.groups.empty()) fail(SP_ERR_UNSUPPORTED, "batch signalling needs at least one non-empty job");
+  batch_launch(b, stream, &sig);
+}
+
+void batch_destroy(Batch *b) { delete b; }
+
+int64_t batch_bytes(const Batch &b) { return b.bytes; }
+
+} // namespace spb
