@@ -42,6 +42,20 @@ __global__ void scatter(const uint4 *__restrict__ packed, uint8_t *__restrict__ 
   }
 }
 
+// the E0 = 1 PACK pattern: 16 one-byte loads at 1 KiB pitch -> one 16-B store
+__global__ void gather(const uint8_t *__restrict__ in, uint4 *__restrict__ packed, uint64_t pitch, uint32_t nchunks) {
+  const uint32_t step = gridDim.x * blockDim.x;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nchunks; t += step) {
+    uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint8_t b = uint8_t(__ldcs(reinterpret_cast<const char *>(in + (uint64_t(t) * 16 + j) * pitch)));
+      w[j >> 2] |= uint32_t(b) << ((j & 3) * 8);
+    }
+    __stcs(packed + t, make_uint4(w[0], w[1], w[2], w[3]));
+  }
+}
+
 template <int M, int F> float run(const uint4 *pk, uint8_t *out, uint64_t pitch, uint32_t nchunks, uint8_t *flush) {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
@@ -76,5 +90,22 @@ int main() {
   printf("M1 st   %.1f GB/s\n", bytes / run<1, 1>(pk, out, pitch, nchunks, flush) / 1e6);
   printf("M2 stcs %.1f GB/s\n", bytes / run<2, 0>(pk, out, pitch, nchunks, flush) / 1e6);
   printf("M2 st   %.1f GB/s\n", bytes / run<2, 1>(pk, out, pitch, nchunks, flush) / 1e6);
+  {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float best = 1e30f;
+    for (int r = 0; r < 4; ++r) {
+      cudaMemset(flush, r, 512u << 20);
+      cudaEventRecord(a);
+      gather<<<148 * 8, 256>>>(out, pk, pitch, nchunks);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      if (ms < best) best = ms;
+    }
+    printf("gather (pack pattern) %.1f GB/s\n", bytes / best / 1e6);
+  }
   return 0;
 }
