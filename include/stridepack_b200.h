@@ -46,6 +46,11 @@ enum {
                                     host fallback */
 };
 
+/* version of this C-ABI: bumped when a declaration changes incompatibly
+ * (SP_ABI_VERSION at compile time, sp_abi_version() at run time) */
+#define SP_ABI_VERSION 2
+int sp_abi_version(void);
+
 const char *sp_status_string(sp_status s);
 /* message of the last failing call on this thread ("" if none) */
 const char *sp_last_error(void);

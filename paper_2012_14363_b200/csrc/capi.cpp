@@ -48,6 +48,8 @@ void set_last_error(const std::string &msg) { t_err = msg; }
 
 extern "C" {
 
+int sp_abi_version(void) { return SP_ABI_VERSION; }
+
 const char *sp_status_string(sp_status s) {
   switch (s) {
   case SP_OK: return "ok";

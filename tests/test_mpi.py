@@ -17,11 +17,23 @@ NATIVE = os.path.join(ROOT, "tests", "native")
 
 def build(tmp_path, name):
     exe = str(tmp_path / name)
-    subprocess.run(["/usr/bin/gcc", "-O2", "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include",
+    subprocess.run(["/usr/bin/gcc", "-O2", "-Wall", "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include",
                     os.path.join(NATIVE, name + ".c"), "-o", exe, "-L" + PKG, "-ltempi_b200",
                     "-lstridepack_b200", "-L/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath," + PKG],
                    check=True)
     return exe
+
+
+@pytest.mark.gpu
+def test_capi_from_c(cuda, tmp_path):
+    """the engine's C-ABI driven from plain C: pack, unpack, typed copy, errors"""
+    p = subprocess.run([build(tmp_path, "capi_pack")], capture_output=True, text=True, timeout=120)
+    assert p.returncode == 0 and "OK" in p.stdout, p.stdout + p.stderr
+
+
+def test_capi_c_program_compiles(tmp_path):
+    """CPU: the C program builds against include/stridepack_b200.h"""
+    assert os.path.exists(build(tmp_path, "capi_pack"))
 
 
 def run(np_, *cmd, timeout=300):
