@@ -73,6 +73,21 @@ int main() {
                 sp_pack(d, 1 << 20, t, 1, d2, 1 << 20, &pos, s);
                 cudaStreamSynchronize(s);
               }));
+  // enqueue cost of batch launches: the job table travels as a kernel
+  // parameter (k_batchp), ~224 B per job
+  for (int nj : {1, 8, 26}) {
+    std::vector<sp_copy_job> jobs;
+    for (int i = 0; i < nj; ++i) jobs.push_back(sp_copy_job{d, uint64_t{1} << 20, t, 1, d2 + 1024 * i, (uint64_t{1} << 20) - 1024 * uint64_t(i), t, 1});
+    sp_batch b = nullptr;
+    CK(sp_copy_batch_create(jobs.data(), nj, &b));
+    std::printf("copy batch %2d jobs enqueue %8.2f us\n", nj, med_us([&] { sp_batch_execute(b, s); }));
+    cudaStreamSynchronize(s);
+    std::printf("copy batch %2d jobs + sync %8.2f us\n", nj, med_us([&] {
+                  sp_batch_execute(b, s);
+                  cudaStreamSynchronize(s);
+                }));
+    sp_batch_free(b);
+  }
   CK(sp_rt_init(0, 1, "latprobe", 0, 8 << 20, 8 << 20));
   for (int m : {SP_METHOD_DIRECT, SP_METHOD_DEVICE, SP_METHOD_ONESHOT, SP_METHOD_STAGED}) {
     int tag = 0;
