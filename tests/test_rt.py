@@ -349,6 +349,39 @@ def test_neighbor_alltoallv_packed_and_strided_receive(cuda):
     assert all(_spawn(_nbrv, 3).values())
 
 
+def _halo_soak(rank, world, job, ranks, method, iters):
+    """many back-to-back iterations with no barrier between them (the
+    in-kernel flags alone order the ranks against each other), three rounds
+    of fresh plans on reset ghosts, every cell verified after each round"""
+    import torch
+    import paper_2012_14363_b200.halo as H
+    import paper_2012_14363_b200.rt as rt
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=1 << 20, host_bytes=1 << 20)
+    cfg = H.HaloConfig(ranks, (10, 12, 8), 2, 8)
+    alloc = torch.empty(14 * 16 * 12 * 8, dtype=torch.uint8, device="cuda")
+    bad = 0
+    for rnd in range(3):
+        H.fill(cfg, rank, alloc)
+        torch.cuda.synchronize()
+        rt.barrier()
+        plan = rt.HaloPlan(cfg, alloc, method)
+        for _ in range(iters):
+            plan.exchange()
+        bad += H.verify(cfg, rank, alloc)
+        plan.free()
+    rt.finalize()
+    return bad
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ranks,method", [((2, 1, 1), 3), ((1, 3, 1), 3), ((2, 1, 1), 2), ((2, 2, 1), 3)])
+def test_distributed_halo_soak(cuda, ranks, method):
+    world = ranks[0] * ranks[1] * ranks[2]
+    res = _spawn(_halo_soak, world, ranks, method, 25, timeout=400)
+    assert all(v == 0 for v in res.values()), res
+
+
 def _halo(rank, world, job, ranks, method):
     import torch
     import paper_2012_14363_b200.halo as H
