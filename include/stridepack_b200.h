@@ -436,7 +436,11 @@ sp_status sp_rt_neighbor_alltoallw(const void *sendbuf,
 typedef struct sp_halo_plan_s *sp_halo_plan;
 sp_status sp_halo_plan_create(const sp_halo_config *cfg, void *alloc,
                               int method, sp_halo_plan *out);
-/* collective; times = {pack, exchange, unpack, iteration} seconds */
+/* collective; times = {pack, exchange, unpack, iteration} seconds (the call
+ * then waits for the iteration). With times == NULL the device-ordered
+ * methods (DIRECT, FUSED_ASYNC) only enqueue on the runtime stream
+ * (sp_rt_stream): iterations pipeline on the GPU and work the caller
+ * enqueues on that stream sees complete ghost shells. */
 sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]);
 sp_status sp_halo_plan_free(sp_halo_plan p);
 

@@ -196,7 +196,12 @@ class HaloPlan:
         _check(lib.sp_halo_plan_create(C.byref(cfg.c()), a, method, C.byref(h)))
         self.handle = h.value
 
-    def exchange(self):
+    def exchange(self, timed: bool = True):
+        """one iteration; timed=False only enqueues (DIRECT / FUSED_ASYNC)
+        on the runtime stream, so iterations pipeline on the GPU"""
+        if not timed:
+            _check(lib.sp_halo_plan_exchange(self.handle, None))
+            return None
         t = (C.c_double * 4)()
         _check(lib.sp_halo_plan_exchange(self.handle, t))
         return {"pack": t[0], "exchange": t[1], "unpack": t[2], "iteration": t[3]}
