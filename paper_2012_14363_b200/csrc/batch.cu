@@ -25,14 +25,16 @@ namespace spb {
 // Destinations may be peer-GPU memory mapped over NVLink (CUDA IPC), which
 // turns the batch into a fused pack-to-peer / copy-to-peer.
 //
-// Work distribution: the words of all jobs form one index space, split into
-// equal contiguous ranges, one per CTA of a single resident wave (grid =
-// SMs x resident CTAs per SM). Each thread moves U words per round with all
-// U loads issued before the first store, so a CTA's whole range is usually
-// one or two DRAM round trips and no CTA waits on a straggler chunk. Within
-// a round a thread finds its job by walking forward from the CTA's first
-// job (ranges rarely cross a job boundary); the job descriptors are read
-// through the read-only path and stay L1-resident.
+// Work distribution: every job is cut into chunks of kBatchChunk words (the
+// last one partial), and the chunks of all jobs form one index space that
+// the CTAs of a single resident wave walk grid-stride. A thread moves U
+// words of its chunk with all U loads issued before the first store. The
+// chunk's job is found by binary search on the jobs' first-chunk indices:
+// up to kParamJobs jobs with <= 3 row dims travel in kernel-parameter space
+// (k_batchp, constant-cache reads), larger batches stage the chunk's job in
+// shared memory (k_batch). Measured alternatives (balanced contiguous
+// ranges, dynamic chunk tickets, launch-order interleaving, job orderings,
+// U = 2 / 8, 8 CTAs/SM with spills) are in profiles/r01_halo_batch.md.
 constexpr int kBatchU = 4;                            // words in flight per thread
 constexpr uint32_t kBatchChunk = 256 * kBatchU;       // words per unit of work
 enum : int { kModeUnpack = 0, kModePack = 1, kModeCopy = 2 };
