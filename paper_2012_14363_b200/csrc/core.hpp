@@ -9,6 +9,7 @@
 // is O(size log size); here commit is O(tree) + a bounded search).
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <memory>
 #include <mutex>
@@ -124,13 +125,18 @@ class Registry {
 public:
   sp_type add(DefPtr def);
   Entry get(sp_type h) const;  // copy of the entry, fails on bad handle
+  CommitPtr committed(sp_type h) const; // the commit record, fails when absent
   CommitPtr commit(sp_type h);
   void remove(sp_type h);
+  // bumped by every remove(): callers that cache handle -> record lookups
+  // across calls revalidate when it moves (handles are never reused)
+  uint64_t generation() const { return gen_.load(std::memory_order_acquire); }
 
 private:
   mutable std::shared_mutex mu_;
   std::unordered_map<sp_type, Entry> map_;
   sp_type next_ = 1;
+  std::atomic<uint64_t> gen_{0};
 };
 Registry &registry();
 

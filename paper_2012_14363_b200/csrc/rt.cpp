@@ -356,9 +356,12 @@ void rt_init(int rank, int size, const char *name, int device, int64_t window_by
   cudaGetLastError();
 }
 
+void nbr_reset();
+
 void rt_finalize() {
   if (!g_rt) return;
   rt_barrier();
+  nbr_reset();
   Runtime &R = *g_rt;
   for (auto &kv : R.ipc_cache) cudaIpcCloseMemHandle(kv.second);
   for (int r = 0; r < R.size; ++r)
@@ -1151,6 +1154,13 @@ struct NbrLast {
 
 NbrLast g_last_v, g_last_w;
 
+bool nbr_peers_unchanged(const NbrLast &last) {
+  Runtime &R = rt();
+  for (auto [d, v] : last.peer_ver)
+    if (R.shm->slots[d].layout_ver.load(std::memory_order_acquire) != v) return false;
+  return true;
+}
+
 bool nbr_last_hit(const NbrLast &last, const std::string &sig) {
   if (!last.valid || last.sig != sig) return false;
   Runtime &R = rt();
@@ -1322,6 +1332,30 @@ struct NbrWCacheEntry {
 };
 std::deque<NbrWCacheEntry> g_nbrw_cache;
 
+struct WArgs {
+  const uint8_t *sbuf;
+  const uint8_t *rbuf;
+  std::vector<int64_t> sc, sd, rc, rd;
+  std::vector<int> sources, dests;
+  std::vector<const Committed *> st, rtp;
+  cudaIpcMemHandle_t h;
+  int64_t off;
+  bool operator==(const WArgs &o) const {
+    return sbuf == o.sbuf && rbuf == o.rbuf && sc == o.sc && sd == o.sd && rc == o.rc && rd == o.rd &&
+           sources == o.sources && dests == o.dests && st == o.st && rtp == o.rtp && off == o.off &&
+           std::memcmp(&h, &o.h, sizeof(h)) == 0;
+  }
+};
+
+// the previous call's arguments; the commit records are held so their
+// addresses cannot be reused by other types while they are compared
+struct WLastCall {
+  WArgs args{};
+  std::vector<CommitPtr> keep_s, keep_r;
+  bool valid = false;
+};
+WLastCall g_wlast;
+
 void desc_of(const Committed &c, int64_t count, Desc &d) {
   d.ndims = c.sb.ndims();
   d.start = c.sb.start;
@@ -1336,13 +1370,51 @@ void desc_of(const Committed &c, int64_t count, Desc &d) {
 }
 } // namespace
 
+void rt_neighbor_alltoallw_build(const uint8_t *sendbuf, const std::vector<int64_t> &send_counts,
+                                 const std::vector<int64_t> &send_displs, const std::vector<CommitPtr> &send_types,
+                                 uint8_t *recvbuf, const std::vector<int> &dests, const BatchSignal &bs);
+
+// drops every cached neighbour launch and repeat-call record: they name IPC
+// mappings and peers of the runtime being finalised
+void nbr_reset() {
+  g_last_v = NbrLast{};
+  g_last_w = NbrLast{};
+  g_wlast = WLastCall{};
+  for (auto &e : g_nbr_cache) batch_destroy(e.batch);
+  g_nbr_cache.clear();
+  for (auto &e : g_nbrw_cache) batch_destroy(e.batch);
+  g_nbrw_cache.clear();
+}
+
 void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &send_counts,
                            const std::vector<int64_t> &send_displs, const std::vector<CommitPtr> &send_types,
                            uint8_t *recvbuf, const std::vector<int64_t> &recv_counts,
                            const std::vector<int64_t> &recv_displs, const std::vector<CommitPtr> &recv_types,
                            const std::vector<int> &sources, const std::vector<int> &dests) {
-  Runtime &R = rt();
   if (static_cast<int>(sources.size()) > kMaxWEdges) fail(SP_ERR_UNSUPPORTED, "neighbour alltoallw: indegree > 64");
+  // repeat of the previous call (same buffers, counts, displacements,
+  // neighbours and commit records, and the receive buffer still the same
+  // allocation): this rank's published layout and the cached launch are
+  // current, so only the entry protocol and the launch remain
+  WArgs args{sendbuf, recvbuf, send_counts, send_displs, recv_counts, recv_displs, sources, dests, {}, {}, {}, 0};
+  args.st.reserve(send_types.size());
+  for (const CommitPtr &t : send_types) args.st.push_back(t.get());
+  args.rtp.reserve(recv_types.size());
+  for (const CommitPtr &t : recv_types) args.rtp.push_back(t.get());
+  if (recvbuf && std::any_of(recv_counts.begin(), recv_counts.end(), [](int64_t c) { return c > 0; }))
+    ipc_handle_of(recvbuf, &args.h, &args.off);
+  if (g_wlast.valid && g_wlast.args == args && g_last_w.valid) {
+    const BatchSignal bs = nbr_enter(sources, dests);
+    if (nbr_peers_unchanged(g_last_w)) {
+      nbr_run(g_last_w.batch, bs);
+      return;
+    }
+    g_wlast.valid = false; // a neighbour re-published: rebuild below (entered already)
+    rt_neighbor_alltoallw_build(sendbuf, send_counts, send_displs, send_types, recvbuf, dests, bs);
+    g_wlast = WLastCall{std::move(args), send_types, recv_types, true};
+    return;
+  }
+  g_wlast.valid = false;
   {
     std::vector<Desc> descs(sources.size(), Desc{});
     std::vector<const Desc *> dp(sources.size(), nullptr);
@@ -1360,6 +1432,17 @@ void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &s
     nbr_publish(recvbuf, sources, recv_displs, bytes, &dp);
   }
   const BatchSignal bs = nbr_enter(sources, dests); // replaces a barrier
+  rt_neighbor_alltoallw_build(sendbuf, send_counts, send_displs, send_types, recvbuf, dests, bs);
+  g_wlast = WLastCall{std::move(args), send_types, recv_types, true};
+}
+
+// the send side of an alltoallw call once entered: find (or build) the
+// typed-copy batch for the out-edges against the neighbours' published
+// receive layouts, and run it
+void rt_neighbor_alltoallw_build(const uint8_t *sendbuf, const std::vector<int64_t> &send_counts,
+                                 const std::vector<int64_t> &send_displs, const std::vector<CommitPtr> &send_types,
+                                 uint8_t *recvbuf, const std::vector<int> &dests, const BatchSignal &bs) {
+  Runtime &R = rt();
   std::string sig(reinterpret_cast<const char *>(&sendbuf), sizeof(sendbuf));
   sig.append(reinterpret_cast<const char *>(&recvbuf), sizeof(recvbuf));
   append_bytes(sig, send_counts);

@@ -498,6 +498,14 @@ Entry Registry::get(sp_type h) const {
   return it->second;
 }
 
+CommitPtr Registry::committed(sp_type h) const {
+  std::shared_lock lk(mu_);
+  auto it = map_.find(h);
+  if (it == map_.end()) fail(SP_ERR_INVALID_HANDLE, "unknown type handle " + std::to_string(h));
+  if (!it->second.committed) fail(SP_ERR_INVALID_ARGUMENT, "type is not committed");
+  return it->second.committed;
+}
+
 CommitPtr Registry::commit(sp_type h) {
   Entry e = get(h);
   if (e.committed) return e.committed;
@@ -513,6 +521,7 @@ CommitPtr Registry::commit(sp_type h) {
 void Registry::remove(sp_type h) {
   std::unique_lock lk(mu_);
   if (!map_.erase(h)) fail(SP_ERR_INVALID_HANDLE, "unknown type handle " + std::to_string(h));
+  gen_.fetch_add(1, std::memory_order_release);
 }
 
 Registry &registry() {

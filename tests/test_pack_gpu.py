@@ -519,3 +519,67 @@ def test_cfg3_constructions_identical(sp, cuda):
         outs.append(o)
     for o in outs[1:]:
         assert torch.equal(o, outs[0])
+
+
+def test_concurrent_host_threads_share_committed_types(sp, orc, cuda):
+    """The reference's threading contract (commit.hpp:81-84):
+    committed types are shared read-only and pack/unpack may run from many
+    threads at once given exclusive destinations. Here 8 host threads, each
+    on its own CUDA stream, pack and unpack the same committed types (cfg1
+    and cfg2 shapes, every small-row and word kernel, device and pageable
+    host buffers) while other threads commit; every result is checked
+    against the oracle."""
+    import threading
+    torch = cuda
+    # cfg1 at 4096 blocks and cfg2-shaped subarrays (1024-B pitch, 64 KiB
+    # planes) small enough for the oracle
+    progs = [[2, 4096, 1, 64, 0, 3]] + [[4, 3, 0, 1024, 64, 16, e0, 32, 8, 1, 2, 3, 0, 0]
+                                        for e0 in (1, 4, 16, 64)]
+    cts = [sp.commit_type(sp.from_program(p)) for p in progs]
+    rng = np.random.default_rng(21)
+    hosts = [rng.integers(0, 256, c.span, dtype=np.uint8) for c in cts]
+    wants = []
+    for p, c, h in zip(progs, cts, hosts):
+        w = np.zeros(c.size, np.uint8)
+        assert orc.pack(p, h, 1, w, 0)[0] == 0
+        wants.append(w)
+    srcs = [dev(torch, h) for h in hosts]  # shared, read-only
+    errors = []
+
+    def work(t):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            for it in range(6):
+                k = (t + it) % len(cts)
+                c = cts[k]
+                out = torch.empty(c.size, dtype=torch.uint8, device="cuda")
+                sp.pack(srcs[k], c, 1, out, 0, stream=s)
+                back = torch.zeros(c.span, dtype=torch.uint8, device="cuda")
+                sp.unpack(out, 0, c, 1, back, stream=s)
+                s.synchronize()
+                if not np.array_equal(out.cpu().numpy(), wants[k]):
+                    errors.append((t, it, "pack"))
+                exp = torch.from_numpy(hosts[k]).cuda()
+                mask = torch.zeros(c.span, dtype=torch.uint8)
+                mask_np = mask.numpy()
+                orc.unpack(progs[k], np.ones(c.size, np.uint8), 0, 1, mask_np)
+                m = torch.from_numpy(mask_np).cuda().bool()
+                if not torch.equal(back[m], exp[m]) or back[~m].any():
+                    errors.append((t, it, "unpack"))
+                if t % 4 == 3:  # pageable host destination: staged path
+                    hout = np.zeros(c.size, np.uint8)
+                    sp.pack(hosts[k], c, 1, hout, 0)
+                    if not np.array_equal(hout, wants[k]):
+                        errors.append((t, it, "staged"))
+                if t % 4 == 2:  # commits racing the packs
+                    sp.commit_type(sp.make_vector(1 + it, 1 + t, 8 + t, sp.make_named(sp.NamedKind.Double)))
+        except Exception as e:  # pragma: no cover - surfaced below
+            errors.append((t, repr(e)))
+
+    ths = [threading.Thread(target=work, args=(t,)) for t in range(8)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    assert not errors, errors[:5]

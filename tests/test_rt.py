@@ -300,6 +300,36 @@ def _nbrw(rank, world, job):
         torch.cuda.synchronize()
         ok = ok and bool(torch.equal(recv, want))
         assert ok, (rank, it)
+
+    def expect(shift):
+        lsrc = torch.arange(n, dtype=torch.int64, device="cuda").mul_(7).add_(left + shift).to(torch.uint8)
+        packed = torch.empty(box.size, dtype=torch.uint8, device="cuda")
+        sp.pack(lsrc, box, 1, packed, 0)
+        want = torch.full_like(recv, 0xAB)
+        sp.unpack(packed, 0, dst_a, 1, want)
+        return want
+
+    # identical arguments call after call (the repeat path skips the layout
+    # publication and the launch lookup) while the source bytes change: every
+    # call must move the current bytes
+    recv = torch.full((n,), 0xAB, dtype=torch.uint8, device="cuda")
+    call = rt.NeighborW([(right, 1, box, 0)], [(left, 1, dst_a, 0)])
+    for shift in range(1, 4):
+        src = torch.arange(n, dtype=torch.int64, device="cuda").mul_(7).add_(rank + shift).to(torch.uint8)
+        torch.cuda.synchronize()
+        call(src, recv)
+        torch.cuda.synchronize()
+        assert torch.equal(recv, expect(shift)), (rank, "repeat", shift)
+    rt.finalize()
+    # a new runtime in the same process: the same call must not reuse the
+    # previous runtime's launches (they name its IPC mappings)
+    rt.init(rank, world, job + "b", device=0, window_bytes=1 << 20, host_bytes=1 << 20)
+    recv.fill_(0xAB)
+    src = torch.arange(n, dtype=torch.int64, device="cuda").mul_(7).add_(rank + 9).to(torch.uint8)
+    torch.cuda.synchronize()
+    call(src, recv)
+    torch.cuda.synchronize()
+    assert torch.equal(recv, expect(9)), (rank, "re-init")
     rt.finalize()
     return ok
 
