@@ -102,6 +102,20 @@ int MPI_Type_create_hvector(int count, int blocklength, MPI_Aint stride, MPI_Dat
                             MPI_Datatype *newtype);
 int MPI_Type_create_subarray(int ndims, const int sizes[], const int subsizes[], const int starts[], int order,
                              MPI_Datatype oldtype, MPI_Datatype *newtype);
+/* beyond the reference (MPI-3.1 4.1.4-4.1.7; TEMPI's future work): regular
+ * index patterns canonicalise to strided kernels, irregular ones run on the
+ * device run-table kernel; displacements must be nonnegative */
+int MPI_Type_indexed(int count, const int blocklengths[], const int displacements[], MPI_Datatype oldtype,
+                     MPI_Datatype *newtype);
+int MPI_Type_create_hindexed(int count, const int blocklengths[], const MPI_Aint displacements[],
+                             MPI_Datatype oldtype, MPI_Datatype *newtype);
+int MPI_Type_create_indexed_block(int count, int blocklength, const int displacements[], MPI_Datatype oldtype,
+                                  MPI_Datatype *newtype);
+int MPI_Type_create_hindexed_block(int count, int blocklength, const MPI_Aint displacements[],
+                                   MPI_Datatype oldtype, MPI_Datatype *newtype);
+int MPI_Type_create_struct(int count, const int blocklengths[], const MPI_Aint displacements[],
+                           const MPI_Datatype types[], MPI_Datatype *newtype);
+int MPI_Type_create_resized(MPI_Datatype oldtype, MPI_Aint lb, MPI_Aint extent, MPI_Datatype *newtype);
 int MPI_Type_commit(MPI_Datatype *datatype);
 int MPI_Type_free(MPI_Datatype *datatype);
 int MPI_Type_size(MPI_Datatype datatype, int *size);

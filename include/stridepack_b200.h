@@ -75,6 +75,37 @@ sp_status sp_type_hvector(int64_t count, int64_t blocklength,
 sp_status sp_type_subarray(int64_t ndims, const int64_t *sizes,
                            const int64_t *subsizes, const int64_t *offsets,
                            sp_type inner, int order, sp_type *out);
+/* ---- beyond the reference: MPI-3.1 4.1.2-4.1.7 (the paper's future work,
+ * PAPER.md:1164; the reference has no indexed/struct/resized types).
+ * Displacements must be nonnegative. A type whose blocks are one
+ * arithmetic progression of equal blocks of one member type canonicalises
+ * to a StridedBlock like the constructors above; any other commits to the
+ * block-list form (SP_FORM_UNSUPPORTED, executed by the device run-table
+ * kernel in MPI typemap order; unpack allowed unless bytes repeat).
+ * Struct extents get no alignment padding: resize to set one. */
+/* MPI_Type_indexed (displacements in inner extents) */
+sp_status sp_type_indexed(int64_t count, const int64_t *blocklens,
+                          const int64_t *displs, sp_type inner, sp_type *out);
+/* MPI_Type_create_hindexed (displacements in bytes) */
+sp_status sp_type_hindexed(int64_t count, const int64_t *blocklens,
+                           const int64_t *displs_bytes, sp_type inner,
+                           sp_type *out);
+/* MPI_Type_create_indexed_block / _hindexed_block */
+sp_status sp_type_indexed_block(int64_t count, int64_t blocklen,
+                                const int64_t *displs, sp_type inner,
+                                sp_type *out);
+sp_status sp_type_hindexed_block(int64_t count, int64_t blocklen,
+                                 const int64_t *displs_bytes, sp_type inner,
+                                 sp_type *out);
+/* MPI_Type_create_struct */
+sp_status sp_type_struct(int64_t count, const int64_t *blocklens,
+                         const int64_t *displs_bytes, const sp_type *types,
+                         sp_type *out);
+/* MPI_Type_create_resized: same bytes, new lower bound and extent */
+sp_status sp_type_resized(sp_type inner, int64_t lb, int64_t extent,
+                          sp_type *out);
+/* MPI_Type_get_extent's lb (0 for every reference constructor) */
+sp_status sp_type_lb(sp_type t, int64_t *lb);
 /* releases the handle; definitions that wrap it keep their own reference */
 sp_status sp_type_free(sp_type t);
 /* type_size                  type_def.hpp:198 */

@@ -32,7 +32,8 @@ __all__ = [
     "NoDevice", "InvalidHandle", "InternalError",
     "NamedKind", "ArrayOrder", "CanonForm", "CountStrategy", "Kernel",
     "TypeDef", "make_named", "make_contiguous", "make_vector", "make_hvector",
-    "make_subarray", "type_size", "type_extent", "from_program",
+    "make_subarray", "make_indexed", "make_hindexed", "make_indexed_block", "make_hindexed_block",
+    "make_struct", "make_resized", "type_size", "type_extent", "from_program",
     "StridedBlock", "PackPlan", "CommittedType", "commit_type", "pack", "unpack",
     "last_launch", "kernel_launch_count",
 ]
@@ -164,6 +165,12 @@ class TypeDef:
         _check(lib.sp_type_extent(self.handle, C.byref(v)))
         return v.value
 
+    def lb(self) -> int:
+        """MPI lower bound (0 for every reference constructor)"""
+        v = C.c_int64()
+        _check(lib.sp_type_lb(self.handle, C.byref(v)))
+        return v.value
+
     def str(self) -> str:
         return self._desc
 
@@ -211,6 +218,57 @@ def make_subarray(ndims: int, sizes: Sequence[int], subsizes: Sequence[int],
     return _new(lib.sp_type_subarray, ndims, arr(*sizes), arr(*subsizes), arr(*offsets),
                 inner.handle, int(order),
                 desc=f"subarray({ndims},{lst(sizes)},{lst(subsizes)},{lst(offsets)},{inner})")
+
+
+# ---- beyond the reference (MPI-3.1 4.1.2-4.1.7; PAPER.md:1164 future work)
+def _arr(v):
+    return (C.c_int64 * max(len(v), 1))(*[int(x) for x in v])
+
+
+def _lst(v):
+    return "[" + ",".join(str(int(x)) for x in v) + "]"
+
+
+def make_indexed(blocklengths: Sequence[int], displacements: Sequence[int], inner: TypeDef) -> TypeDef:
+    """MPI_Type_indexed: displacements in inner extents"""
+    if len(blocklengths) != len(displacements):
+        raise InvalidArgument("indexed: one displacement per block")
+    return _new(lib.sp_type_indexed, len(blocklengths), _arr(blocklengths), _arr(displacements), inner.handle,
+                desc=f"indexed({_lst(blocklengths)},{_lst(displacements)},{inner})")
+
+
+def make_hindexed(blocklengths: Sequence[int], displacements: Sequence[int], inner: TypeDef) -> TypeDef:
+    """MPI_Type_create_hindexed: displacements in bytes"""
+    if len(blocklengths) != len(displacements):
+        raise InvalidArgument("hindexed: one displacement per block")
+    return _new(lib.sp_type_hindexed, len(blocklengths), _arr(blocklengths), _arr(displacements), inner.handle,
+                desc=f"hindexed({_lst(blocklengths)},{_lst(displacements)},{inner})")
+
+
+def make_indexed_block(blocklength: int, displacements: Sequence[int], inner: TypeDef) -> TypeDef:
+    """MPI_Type_create_indexed_block"""
+    return _new(lib.sp_type_indexed_block, len(displacements), blocklength, _arr(displacements), inner.handle,
+                desc=f"indexed_block({blocklength},{_lst(displacements)},{inner})")
+
+
+def make_hindexed_block(blocklength: int, displacements: Sequence[int], inner: TypeDef) -> TypeDef:
+    """MPI_Type_create_hindexed_block"""
+    return _new(lib.sp_type_hindexed_block, len(displacements), blocklength, _arr(displacements), inner.handle,
+                desc=f"hindexed_block({blocklength},{_lst(displacements)},{inner})")
+
+
+def make_struct(blocklengths: Sequence[int], displacements: Sequence[int], types: Sequence[TypeDef]) -> TypeDef:
+    """MPI_Type_create_struct: displacements in bytes, one type per block"""
+    if not (len(blocklengths) == len(displacements) == len(types)):
+        raise InvalidArgument("struct: one displacement and one type per block")
+    th = (_capi.sp_type * max(len(types), 1))(*[t.handle for t in types])
+    return _new(lib.sp_type_struct, len(types), _arr(blocklengths), _arr(displacements), th,
+                desc=f"struct({_lst(blocklengths)},{_lst(displacements)},[{','.join(str(t) for t in types)}])")
+
+
+def make_resized(inner: TypeDef, lb: int, extent: int) -> TypeDef:
+    """MPI_Type_create_resized"""
+    return _new(lib.sp_type_resized, inner.handle, lb, extent, desc=f"resized({inner},{lb},{extent})")
 
 
 @dataclass(frozen=True)

@@ -57,6 +57,13 @@ _sig("sp_type_contiguous", C.c_int, i64, sp_type, C.POINTER(sp_type))
 _sig("sp_type_vector", C.c_int, i64, i64, i64, sp_type, C.POINTER(sp_type))
 _sig("sp_type_hvector", C.c_int, i64, i64, i64, sp_type, C.POINTER(sp_type))
 _sig("sp_type_subarray", C.c_int, i64, i64p, i64p, i64p, sp_type, C.c_int, C.POINTER(sp_type))
+_sig("sp_type_indexed", C.c_int, i64, i64p, i64p, sp_type, C.POINTER(sp_type))
+_sig("sp_type_hindexed", C.c_int, i64, i64p, i64p, sp_type, C.POINTER(sp_type))
+_sig("sp_type_indexed_block", C.c_int, i64, i64, i64p, sp_type, C.POINTER(sp_type))
+_sig("sp_type_hindexed_block", C.c_int, i64, i64, i64p, sp_type, C.POINTER(sp_type))
+_sig("sp_type_struct", C.c_int, i64, i64p, i64p, C.POINTER(sp_type), C.POINTER(sp_type))
+_sig("sp_type_resized", C.c_int, sp_type, i64, i64, C.POINTER(sp_type))
+_sig("sp_type_lb", C.c_int, sp_type, i64p)
 _sig("sp_type_free", C.c_int, sp_type)
 _sig("sp_type_size", C.c_int, sp_type, i64p)
 _sig("sp_type_extent", C.c_int, sp_type, i64p)

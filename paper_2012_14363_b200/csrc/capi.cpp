@@ -1,6 +1,7 @@
 // capi.cpp -- extern "C" entry points of libstridepack_b200.so.
 // Every call converts internal errors (spb::Error) into an sp_status and a
 // thread-local message; nothing throws across the ABI.
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <new>
@@ -91,6 +92,64 @@ sp_status sp_type_hvector(int64_t count, int64_t blocklength, int64_t stride_byt
 sp_status sp_type_subarray(int64_t ndims, const int64_t *sizes, const int64_t *subsizes,
                            const int64_t *offsets, sp_type inner, int order, sp_type *out) {
   return guard([&] { add(spb::make_subarray(ndims, sizes, subsizes, offsets, def_of(inner), order), out); });
+}
+
+// ---- beyond the reference (MPI-3.1 4.1.2-4.1.7)
+sp_status sp_type_hindexed(int64_t count, const int64_t *blocklens, const int64_t *displs_bytes, sp_type inner,
+                           sp_type *out) {
+  return guard([&] { add(spb::make_indexed(count, blocklens, displs_bytes, def_of(inner)), out); });
+}
+
+sp_status sp_type_indexed(int64_t count, const int64_t *blocklens, const int64_t *displs, sp_type inner,
+                          sp_type *out) {
+  return guard([&] {
+    spb::DefPtr in = def_of(inner);
+    if (count > 0 && !displs) spb::fail(SP_ERR_INVALID_ARGUMENT, "indexed: null array");
+    std::vector<int64_t> b(displs, displs + std::max<int64_t>(count, 0));
+    for (int64_t &x : b) x *= in->extent;
+    add(spb::make_indexed(count, blocklens, b.data(), std::move(in)), out);
+  });
+}
+
+sp_status sp_type_hindexed_block(int64_t count, int64_t blocklen, const int64_t *displs_bytes, sp_type inner,
+                                 sp_type *out) {
+  return guard([&] {
+    std::vector<int64_t> bl(static_cast<size_t>(std::max<int64_t>(count, 0)), blocklen);
+    add(spb::make_indexed(count, bl.data(), displs_bytes, def_of(inner)), out);
+  });
+}
+
+sp_status sp_type_indexed_block(int64_t count, int64_t blocklen, const int64_t *displs, sp_type inner,
+                                sp_type *out) {
+  return guard([&] {
+    spb::DefPtr in = def_of(inner);
+    if (count > 0 && !displs) spb::fail(SP_ERR_INVALID_ARGUMENT, "indexed_block: null array");
+    std::vector<int64_t> bl(static_cast<size_t>(std::max<int64_t>(count, 0)), blocklen);
+    std::vector<int64_t> b(displs, displs + std::max<int64_t>(count, 0));
+    for (int64_t &x : b) x *= in->extent;
+    add(spb::make_indexed(count, bl.data(), b.data(), std::move(in)), out);
+  });
+}
+
+sp_status sp_type_struct(int64_t count, const int64_t *blocklens, const int64_t *displs_bytes,
+                         const sp_type *types, sp_type *out) {
+  return guard([&] {
+    if (count > 0 && !types) spb::fail(SP_ERR_INVALID_ARGUMENT, "struct: null array");
+    std::vector<spb::DefPtr> m;
+    for (int64_t i = 0; i < count; ++i) m.push_back(def_of(types[i]));
+    add(spb::make_struct(count, blocklens, displs_bytes, m), out);
+  });
+}
+
+sp_status sp_type_resized(sp_type inner, int64_t lb, int64_t extent, sp_type *out) {
+  return guard([&] { add(spb::make_resized(def_of(inner), lb, extent), out); });
+}
+
+sp_status sp_type_lb(sp_type t, int64_t *lb) {
+  return guard([&] {
+    if (!lb) spb::fail(SP_ERR_INVALID_ARGUMENT, "null output");
+    *lb = def_of(t)->lb;
+  });
 }
 
 sp_status sp_type_free(sp_type t) {

@@ -32,7 +32,12 @@ struct Error {
 void set_last_error(const std::string &msg);
 
 // ---------------------------------------------------------------- types
-enum class Kind : uint8_t { Named, Contiguous, Vector, Hvector, Subarray };
+// Named..Subarray are the reference's constructors. Indexed (MPI indexed,
+// hindexed and their _block forms, byte displacements), Struct and Resized
+// go beyond it (MPI-3.1 sections 4.1.2-4.1.7; the paper's future work,
+// PAPER.md:1164): regular ones canonicalise like the rest, irregular ones
+// commit to the block-list form.
+enum class Kind : uint8_t { Named, Contiguous, Vector, Hvector, Subarray, Indexed, Struct, Resized };
 
 // One definition level (type_def.hpp:52-123). Immutable once built.
 struct TypeDef {
@@ -42,9 +47,12 @@ struct TypeDef {
   int64_t blocklength = 0;  // vector/hvector
   int64_t stride = 0;       // vector: inner extents; hvector: bytes
   std::vector<int64_t> sizes, subsizes, offsets; // subarray, dim 0 innermost
-  std::shared_ptr<const TypeDef> inner;
-  // derived once (type_def.hpp:198-250 + block_list span)
-  int64_t size = 0, extent = 0, span = 0;
+  std::vector<int64_t> blocklens, displs;        // indexed/struct: per block, displs in bytes
+  std::shared_ptr<const TypeDef> inner;           // every kind but Named and Struct
+  std::vector<std::shared_ptr<const TypeDef>> members; // struct: type of each block
+  // derived once (type_def.hpp:198-250 + block_list span); lb is MPI's
+  // lower bound (0 for the reference's constructors, which never move it)
+  int64_t size = 0, extent = 0, span = 0, lb = 0;
   int depth = 1;
 };
 using DefPtr = std::shared_ptr<const TypeDef>;
@@ -56,6 +64,14 @@ DefPtr make_hvector(int64_t count, int64_t bl, int64_t stride_b, DefPtr inner);
 DefPtr make_subarray(int64_t ndims, const int64_t *sizes,
                      const int64_t *subsizes, const int64_t *offsets,
                      DefPtr inner, int order);
+// MPI_Type_create_hindexed (displacements in bytes; MPI_Type_indexed and
+// the _block forms scale/replicate before calling)
+DefPtr make_indexed(int64_t count, const int64_t *blocklens, const int64_t *displs_bytes, DefPtr inner);
+// MPI_Type_create_struct
+DefPtr make_struct(int64_t count, const int64_t *blocklens, const int64_t *displs_bytes,
+                   const std::vector<DefPtr> &members);
+// MPI_Type_create_resized
+DefPtr make_resized(DefPtr inner, int64_t lb, int64_t extent);
 
 // ---------------------------------------------------------------- canon
 // Canonical strided form (strided_block.hpp:17-46): counts[0] bytes at
@@ -85,6 +101,7 @@ struct DeviceRuns {
   int64_t *d_dst = nullptr;   // exclusive prefix sum of lengths
   int64_t *d_len = nullptr;
   int64_t n = 0;
+  uint64_t align_or = 0;      // OR of every run offset and length (word choice)
 };
 
 struct Committed {

@@ -21,9 +21,11 @@
 //                      rows into one 16-byte packed word (one STG.128 per
 //                      lane, or one LDG.128 for unpack) and walks the rows by
 //                      carry-increment instead of re-dividing.
-//   k_blocklist<PACK>  definition-order run table on the device, for forms
+//   k_runs<W, PACK>    definition-order run table on the device, for forms
 //                      without a strided canon (zero-stride "Unsupported"
-//                      types) or with more row dims than a kernel carries.
+//                      types, irregular indexed/struct types) or with more
+//                      row dims than a kernel carries; one thread per packed
+//                      word, run found by binary search.
 // W is the largest power of two <= 16 dividing the row length, every row
 // stride, and BOTH buffer addresses (the reference's select_word_size,
 // plan.hpp:47-64, plus the address alignment a GPU load needs).
@@ -345,27 +347,42 @@ __global__ void __launch_bounds__(256) k_shift_unpack(const uint8_t *__restrict_
   }
 }
 
-// ------------------------------------------------------------ k_blocklist
-// One thread per (object, run): byte loop over the run. Used only for
-// definition-order gathers (Unsupported forms, pack.hpp:123-135) and for
-// strided forms with more row dimensions than KMAX.
-template <bool PACK>
-__global__ void __launch_bounds__(256) k_blocklist(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
-                                                   const int64_t *__restrict__ rsrc,
-                                                   const int64_t *__restrict__ rdst,
-                                                   const int64_t *__restrict__ rlen, int64_t nruns,
-                                                   int64_t nobj, int64_t extent, int64_t size) {
-  const int64_t total = nruns * nobj;
+// ------------------------------------------------------------ k_runs
+// Run-table kernel for forms without a strided canon (the reference's
+// zero-stride "Unsupported" types, irregular indexed/struct types) and for
+// strided forms with more row dims than KMAX. One thread per W-byte word of
+// the PACKED stream: the word's run is the last one whose packed offset is
+// <= the word's (binary search over the table, which stays L1/L2-resident
+// and is read by neighbouring lanes at the same addresses), so the packed
+// side is fully coalesced and every run's strided side is walked in order
+// by consecutive lanes. Runs are in definition order, so duplicated source
+// bytes pack with their multiplicity (pack.hpp:123-135).
+template <int W, bool PACK>
+__global__ void __launch_bounds__(256) k_runs(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
+                                              const int64_t *__restrict__ rsrc, const int64_t *__restrict__ rdst,
+                                              int64_t nruns, int64_t nobj, int64_t extent, int64_t size) {
+  using T = typename Word<W>::T;
+  const int64_t wpo = size / W; // words per object
+  const int64_t total = wpo * nobj;
   const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += step) {
-    const int64_t j = t / nruns, k = t - j * nruns;
-    const int64_t so = j * extent + rsrc[k], po = j * size + rdst[k], n = rlen[k];
-    for (int64_t b = 0; b < n; ++b) {
-      if (PACK) {
-        out[po + b] = in[so + b];
+    const int64_t j = t / wpo;
+    const int64_t q = (t - j * wpo) * W;
+    int64_t lo = 0, hi = nruns - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (__ldg(rdst + mid) <= q) {
+        lo = mid;
       } else {
-        out[so + b] = in[po + b];
+        hi = mid - 1;
       }
+    }
+    const int64_t so = j * extent + __ldg(rsrc + lo) + (q - __ldg(rdst + lo));
+    const int64_t po = j * size + q;
+    if (PACK) {
+      st_stream(reinterpret_cast<T *>(out + po), ld_stream(reinterpret_cast<const T *>(in + so)));
+    } else {
+      st_stream(reinterpret_cast<T *>(out + so), ld_stream(reinterpret_cast<const T *>(in + po)));
     }
   }
 }
@@ -556,15 +573,18 @@ const DeviceRuns &device_runs(const Committed &ct, const std::vector<Run> &runs)
   const size_t n = runs.size();
   std::vector<int64_t> hs(n), hd(n), hl(n);
   int64_t acc = 0;
+  uint64_t align_or = 0;
   for (size_t k = 0; k < n; ++k) {
     hs[k] = runs[k].off;
     hd[k] = acc;
     hl[k] = runs[k].len;
     acc += runs[k].len;
+    align_or |= static_cast<uint64_t>(runs[k].off) | static_cast<uint64_t>(runs[k].len);
   }
   DeviceRuns d;
   d.device = cur;
   d.n = static_cast<int64_t>(n);
+  d.align_or = align_or;
   const size_t bytes = std::max<size_t>(n, 1) * sizeof(int64_t);
   cuda_check(cudaMalloc(&d.d_src, bytes), "cudaMalloc(runs)");
   cuda_check(cudaMalloc(&d.d_dst, bytes), "cudaMalloc(runs)");
@@ -615,17 +635,33 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
       runs = &tmp;
     }
     const DeviceRuns &dr = device_runs(ct, *runs);
-    const unsigned grid = grid_for(static_cast<uint64_t>(dr.n * count), 1);
-    if (pack) {
-      k_blocklist<true><<<grid, 256, 0, s>>>(in, out, dr.d_src, dr.d_dst, dr.d_len, dr.n, count, ct.extent,
-                                             ct.size);
-    } else {
-      k_blocklist<false><<<grid, 256, 0, s>>>(in, out, dr.d_src, dr.d_dst, dr.d_len, dr.n, count,
-                                              ct.extent, ct.size);
+    // the word divides every run offset and length, the extent, the object
+    // size and both buffer addresses
+    int w = pow2_align(dr.align_or | static_cast<uint64_t>(ct.extent) | static_cast<uint64_t>(ct.size) |
+                       strided_addr | packed_addr);
+    if (opt.force_word) {
+      if (opt.force_word > w || (opt.force_word & (opt.force_word - 1)))
+        fail(SP_ERR_INVALID_ARGUMENT, "force_word is not legal for these buffers");
+      w = opt.force_word;
     }
-    cuda_check(cudaGetLastError(), "k_blocklist launch");
+    const unsigned grid = grid_for(static_cast<uint64_t>(ct.size / w * count), 1);
+#define SPB_RUNS(WW)                                                                                               \
+  if (pack) {                                                                                                      \
+    k_runs<WW, true><<<grid, 256, 0, s>>>(in, out, dr.d_src, dr.d_dst, dr.n, count, ct.extent, ct.size);          \
+  } else {                                                                                                         \
+    k_runs<WW, false><<<grid, 256, 0, s>>>(in, out, dr.d_src, dr.d_dst, dr.n, count, ct.extent, ct.size);         \
+  }
+    switch (w) {
+    case 16: SPB_RUNS(16) break;
+    case 8: SPB_RUNS(8) break;
+    case 4: SPB_RUNS(4) break;
+    case 2: SPB_RUNS(2) break;
+    default: SPB_RUNS(1) break;
+    }
+#undef SPB_RUNS
+    cuda_check(cudaGetLastError(), "k_runs launch");
     li.kernel = SP_KERNEL_BLOCKLIST;
-    li.word = 1;
+    li.word = w;
     li.launches = 1;
     li.grid = grid;
     li.block = 256;

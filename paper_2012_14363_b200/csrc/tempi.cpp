@@ -296,6 +296,70 @@ int MPI_Type_create_subarray(int ndims, const int sizes[], const int subsizes[],
   return new_type(h, newtype);
 }
 
+// ---- beyond the reference (MPI-3.1 4.1.4-4.1.7): regular patterns are
+// canonicalised like the types above, irregular ones run on the device
+// run-table kernel
+int MPI_Type_indexed(int count, const int blocklengths[], const int displacements[], MPI_Datatype oldtype,
+                     MPI_Datatype *newtype) {
+  TYPE(oldtype, in);
+  if (count < 0 || (count > 0 && (!blocklengths || !displacements))) return MPI_ERR_ARG;
+  std::vector<int64_t> bl(blocklengths, blocklengths + count), d(displacements, displacements + count);
+  sp_type h;
+  TRY(sp_type_indexed(count, bl.data(), d.data(), in, &h));
+  return new_type(h, newtype);
+}
+
+int MPI_Type_create_hindexed(int count, const int blocklengths[], const MPI_Aint displacements[],
+                             MPI_Datatype oldtype, MPI_Datatype *newtype) {
+  TYPE(oldtype, in);
+  if (count < 0 || (count > 0 && (!blocklengths || !displacements))) return MPI_ERR_ARG;
+  std::vector<int64_t> bl(blocklengths, blocklengths + count), d(displacements, displacements + count);
+  sp_type h;
+  TRY(sp_type_hindexed(count, bl.data(), d.data(), in, &h));
+  return new_type(h, newtype);
+}
+
+int MPI_Type_create_indexed_block(int count, int blocklength, const int displacements[], MPI_Datatype oldtype,
+                                  MPI_Datatype *newtype) {
+  TYPE(oldtype, in);
+  if (count < 0 || (count > 0 && !displacements)) return MPI_ERR_ARG;
+  std::vector<int64_t> d(displacements, displacements + count);
+  sp_type h;
+  TRY(sp_type_indexed_block(count, blocklength, d.data(), in, &h));
+  return new_type(h, newtype);
+}
+
+int MPI_Type_create_hindexed_block(int count, int blocklength, const MPI_Aint displacements[],
+                                   MPI_Datatype oldtype, MPI_Datatype *newtype) {
+  TYPE(oldtype, in);
+  if (count < 0 || (count > 0 && !displacements)) return MPI_ERR_ARG;
+  std::vector<int64_t> d(displacements, displacements + count);
+  sp_type h;
+  TRY(sp_type_hindexed_block(count, blocklength, d.data(), in, &h));
+  return new_type(h, newtype);
+}
+
+int MPI_Type_create_struct(int count, const int blocklengths[], const MPI_Aint displacements[],
+                           const MPI_Datatype types[], MPI_Datatype *newtype) {
+  if (count < 0 || (count > 0 && (!blocklengths || !displacements || !types))) return MPI_ERR_ARG;
+  std::vector<int64_t> bl(blocklengths, blocklengths + count), d(displacements, displacements + count);
+  std::vector<sp_type> ts;
+  for (int i = 0; i < count; ++i) {
+    TYPE(types[i], t);
+    ts.push_back(t);
+  }
+  sp_type h;
+  TRY(sp_type_struct(count, bl.data(), d.data(), ts.data(), &h));
+  return new_type(h, newtype);
+}
+
+int MPI_Type_create_resized(MPI_Datatype oldtype, MPI_Aint lb, MPI_Aint extent, MPI_Datatype *newtype) {
+  TYPE(oldtype, in);
+  sp_type h;
+  TRY(sp_type_resized(in, lb, extent, &h));
+  return new_type(h, newtype);
+}
+
 int PMPI_Type_commit(MPI_Datatype *datatype) {
   if (!datatype) return MPI_ERR_ARG;
   TYPE(*datatype, h);
@@ -326,9 +390,10 @@ int MPI_Type_size(MPI_Datatype datatype, int *size) {
 int MPI_Type_get_extent(MPI_Datatype datatype, MPI_Aint *lb, MPI_Aint *extent) {
   TYPE(datatype, h);
   if (!lb || !extent) return MPI_ERR_ARG;
-  int64_t e = 0;
+  int64_t e = 0, l = 0;
   TRY(sp_type_extent(h, &e));
-  *lb = 0;
+  TRY(sp_type_lb(h, &l));
+  *lb = l;
   *extent = e;
   return MPI_SUCCESS;
 }

@@ -46,6 +46,7 @@ DefPtr make_contiguous(int64_t count, DefPtr inner) {
   d->size = count * inner->size;
   d->extent = count * inner->extent;
   d->span = (count == 0 || inner->span == 0) ? 0 : (count - 1) * inner->extent + inner->span;
+  d->lb = count == 0 ? 0 : inner->lb;
   d->depth = inner->depth + 1;
   d->inner = std::move(inner);
   return d;
@@ -74,6 +75,7 @@ static DefPtr make_vec(Kind k, int64_t count, int64_t bl, int64_t stride, DefPtr
   d->span = (count == 0 || bl == 0 || inner->span == 0)
                 ? 0
                 : (count - 1) * step + (bl - 1) * e + inner->span;
+  d->lb = (count == 0 || bl == 0) ? 0 : inner->lb;
   d->depth = inner->depth + 2;
   d->inner = std::move(inner);
   return d;
@@ -120,6 +122,76 @@ DefPtr make_subarray(int64_t ndims, const int64_t *sizes, const int64_t *subsize
   return d;
 }
 
+// ---- beyond the reference: MPI indexed / struct / resized (MPI-3.1
+// 4.1.2-4.1.7). Displacements are bytes from the type's origin and must be
+// nonnegative (the engine addresses from the buffer start, like the
+// reference's nonnegative strides). lb/extent follow MPI: over the blocks
+// that describe bytes, lb = min(disp + member lb) and ub = max(disp +
+// member lb + blocklength * member extent); no alignment padding is added
+// to struct extents (set one with a resized type).
+static DefPtr make_blocks(Kind k, int64_t count, const int64_t *bl, const int64_t *displs,
+                          std::vector<DefPtr> members) {
+  const char *nm = k == Kind::Indexed ? "indexed" : "struct";
+  if (count < 0) fail(SP_ERR_INVALID_ARGUMENT, std::string(nm) + ": count must be >= 0");
+  if (count > 0 && (!bl || !displs)) fail(SP_ERR_INVALID_ARGUMENT, std::string(nm) + ": null array");
+  auto d = std::make_shared<TypeDef>();
+  d->kind = k;
+  d->count = count;
+  d->blocklens.assign(bl, bl + count);
+  d->displs.assign(displs, displs + count);
+  bool any = false;
+  int64_t lo = 0, hi = 0, span = 0, depth = 0;
+  for (int64_t i = 0; i < count; ++i) {
+    const TypeDef &m = *members[static_cast<size_t>(k == Kind::Indexed ? 0 : i)];
+    if (bl[i] < 0) fail(SP_ERR_INVALID_ARGUMENT, std::string(nm) + ": blocklengths must be >= 0");
+    if (displs[i] < 0) fail(SP_ERR_INVALID_ARGUMENT, std::string(nm) + ": negative displacements are not representable");
+    depth = std::max<int64_t>(depth, m.depth);
+    d->size += bl[i] * m.size;
+    if (bl[i] == 0) continue;
+    const int64_t a = displs[i] + m.lb, b = displs[i] + m.lb + bl[i] * m.extent;
+    lo = any ? std::min(lo, a) : a;
+    hi = any ? std::max(hi, b) : b;
+    any = true;
+    if (m.span > 0) span = std::max(span, displs[i] + (bl[i] - 1) * m.extent + m.span);
+  }
+  d->lb = any ? lo : 0;
+  d->extent = any ? hi - lo : 0;
+  d->span = span;
+  d->depth = static_cast<int>(depth) + 2;
+  if (k == Kind::Indexed) {
+    d->inner = std::move(members[0]);
+  } else {
+    d->members = std::move(members);
+  }
+  return d;
+}
+
+DefPtr make_indexed(int64_t count, const int64_t *blocklens, const int64_t *displs_bytes, DefPtr inner) {
+  need_inner(inner);
+  return make_blocks(Kind::Indexed, count, blocklens, displs_bytes, {std::move(inner)});
+}
+
+DefPtr make_struct(int64_t count, const int64_t *blocklens, const int64_t *displs_bytes,
+                   const std::vector<DefPtr> &members) {
+  if (static_cast<int64_t>(members.size()) != count) fail(SP_ERR_INVALID_ARGUMENT, "struct: one type per block");
+  for (const DefPtr &m : members) need_inner(m);
+  return make_blocks(Kind::Struct, count, blocklens, displs_bytes, members);
+}
+
+DefPtr make_resized(DefPtr inner, int64_t lb, int64_t extent) {
+  need_inner(inner);
+  if (extent < 0) fail(SP_ERR_INVALID_ARGUMENT, "resized: negative extents are not representable");
+  auto d = std::make_shared<TypeDef>();
+  d->kind = Kind::Resized;
+  d->size = inner->size;
+  d->span = inner->span;
+  d->lb = lb;
+  d->extent = extent;
+  d->depth = inner->depth;
+  d->inner = std::move(inner);
+  return d;
+}
+
 // ============================================================ canonicalisation
 // The IR chain is stored BASE FIRST: c[0] is the dense base, c.back() the
 // head. Each pass walks bottom-up, which is the order the reference's
@@ -139,34 +211,77 @@ struct Link {
 Link dense_link(int64_t off, int64_t extent) { return {true, off, 0, 0, extent}; }
 Link stream_link(int64_t off, int64_t stride, int64_t count) { return {false, off, stride, count, 0}; }
 
-// translate (ir.hpp:112-147): one link per constructor level
-void translate(const TypeDef &d, std::vector<Link> &c) {
+// The blocks of an indexed/struct level that describe bytes, abutting
+// neighbours (same member, next block starts where this one ends) merged,
+// which keeps the definition order intact.
+struct Block {
+  const TypeDef *member;
+  int64_t disp, count;
+};
+std::vector<Block> live_blocks(const TypeDef &d) {
+  std::vector<Block> out;
+  for (size_t i = 0; i < d.blocklens.size(); ++i) {
+    const TypeDef *m = d.kind == Kind::Indexed ? d.inner.get() : d.members[i].get();
+    if (d.blocklens[i] == 0 || m->size == 0) continue;
+    if (!out.empty() && out.back().member == m && out.back().disp + out.back().count * m->extent == d.displs[i]) {
+      out.back().count += d.blocklens[i];
+    } else {
+      out.push_back({m, d.displs[i], d.blocklens[i]});
+    }
+  }
+  return out;
+}
+
+// translate (ir.hpp:112-147): one link per constructor level. Levels the
+// IR cannot express (indexed/struct blocks that are not one arithmetic
+// progression of equal blocks of one type) return false.
+bool translate(const TypeDef &d, std::vector<Link> &c) {
   switch (d.kind) {
   case Kind::Named:
     c.push_back(dense_link(0, d.size));
-    return;
+    return true;
   case Kind::Contiguous:
-    translate(*d.inner, c);
+    if (!translate(*d.inner, c)) return false;
     c.push_back(stream_link(0, d.inner->extent, d.count));
-    return;
+    return true;
   case Kind::Vector:
   case Kind::Hvector: {
     const int64_t e = d.inner->extent;
-    translate(*d.inner, c);
+    if (!translate(*d.inner, c)) return false;
     c.push_back(stream_link(0, e, d.blocklength));
     c.push_back(stream_link(0, d.kind == Kind::Vector ? d.stride * e : d.stride, d.count));
-    return;
+    return true;
   }
   case Kind::Subarray: {
-    translate(*d.inner, c);
+    if (!translate(*d.inner, c)) return false;
     int64_t stride = d.inner->extent;
     for (size_t i = 0; i < d.sizes.size(); ++i) {
       c.push_back(stream_link(d.offsets[i] * stride, stride, d.subsizes[i]));
       stride *= d.sizes[i];
     }
-    return;
+    return true;
+  }
+  case Kind::Resized: // the inner layout; parents step by the new extent
+    return translate(*d.inner, c);
+  case Kind::Indexed:
+  case Kind::Struct: {
+    const std::vector<Block> b = live_blocks(d);
+    if (b.empty()) { // describes no bytes: an empty element
+      c.push_back(dense_link(0, 0));
+      return true;
+    }
+    const TypeDef *m = b[0].member;
+    const int64_t step = b.size() > 1 ? b[1].disp - b[0].disp : 0;
+    for (size_t i = 1; i < b.size(); ++i)
+      if (b[i].member != m || b[i].count != b[0].count || b[i].disp - b[i - 1].disp != step) return false;
+    if (step < 0) return false;
+    if (!translate(*m, c)) return false;
+    c.push_back(stream_link(0, m->extent, b[0].count));
+    c.push_back(stream_link(b[0].disp, step, static_cast<int64_t>(b.size())));
+    return true;
   }
   }
+  return false;
 }
 
 // dense folding (canon.hpp:22-37): stream over dense with extent == stride
@@ -374,6 +489,18 @@ static std::vector<Run> def_runs(const TypeDef &d) {
       for (int64_t j = 0; j < d.blocklength; ++j) place(in, i * step + j * e);
     break;
   }
+  case Kind::Resized:
+    out = def_runs(*d.inner);
+    break;
+  case Kind::Indexed:
+  case Kind::Struct:
+    for (size_t i = 0; i < d.blocklens.size(); ++i) {
+      const TypeDef &m = d.kind == Kind::Indexed ? *d.inner : *d.members[i];
+      if (d.blocklens[i] == 0) continue;
+      const auto in = def_runs(m);
+      for (int64_t j = 0; j < d.blocklens[i]; ++j) place(in, d.displs[i] + j * m.extent);
+    }
+    break;
   case Kind::Subarray: {
     const auto in = def_runs(*d.inner);
     const size_t nd = d.sizes.size();
@@ -419,8 +546,14 @@ std::vector<Run> flatten_def(const TypeDef &def, bool &overlap) {
 
 static int64_t leaf_bytes(const TypeDef &d) {
   const TypeDef *p = &d;
-  while (p->kind != Kind::Named) p = p->inner.get();
+  while (p->kind != Kind::Named) p = p->kind == Kind::Struct ? p->members[0].get() : p->inner.get();
   return p->size;
+}
+
+// whether the definition uses a constructor the reference does not have
+static bool beyond_reference(const TypeDef &d) {
+  if (d.kind == Kind::Indexed || d.kind == Kind::Struct || d.kind == Kind::Resized) return true;
+  return d.inner && beyond_reference(*d.inner);
 }
 
 // ============================================================ commit
@@ -435,7 +568,18 @@ CommitPtr commit_def(const TypeDef &def) {
   }
   std::vector<Link> c;
   c.reserve(static_cast<size_t>(def.depth));
-  translate(def, c);
+  if (!translate(def, c)) {
+    // an irregular indexed/struct level: the block-list form, in MPI
+    // typemap (definition) order; unpack is allowed unless bytes repeat
+    ct->form = SP_FORM_UNSUPPORTED;
+    ct->runs = def_runs(def);
+    std::vector<Run> sorted = ct->runs;
+    std::sort(sorted.begin(), sorted.end(), [](const Run &a, const Run &b) { return a.off < b.off; });
+    for (size_t i = 1; i < sorted.size() && !ct->overlapping; ++i)
+      ct->overlapping = sorted[i].off < sorted[i - 1].off + sorted[i - 1].len;
+    ct->n_def_runs = static_cast<int64_t>(ct->runs.size());
+    return ct;
+  }
   bool coincident = false; // canon.hpp:118-130
   for (const Link &l : c)
     if (!l.dense && l.count >= 2 && l.stride < 1) coincident = true;
@@ -478,8 +622,8 @@ CommitPtr commit_def(const TypeDef &def) {
   // stream over a non-empty element describes its bytes at least twice.
   ct->form = SP_FORM_UNSUPPORTED;
   ct->overlapping = true;
-  ct->n_def_runs = def.size / leaf_bytes(def);
   ct->runs = def_runs(def);
+  ct->n_def_runs = beyond_reference(def) ? static_cast<int64_t>(ct->runs.size()) : def.size / leaf_bytes(def);
   return ct;
 }
 

@@ -13,7 +13,7 @@ int main(int argc, char **argv) {
   int rank, size;
   MPI_Comm_rank(MPI_COMM_WORLD, &rank);
   MPI_Comm_size(MPI_COMM_WORLD, &size);
-  MPI_Datatype v, sc, sf, hv, row;
+  MPI_Datatype v, sc, sf, hv, row, x;
   CHECK(MPI_Type_vector(131072, 1, 64, MPI_DOUBLE, &v) == MPI_SUCCESS);
   CHECK(MPI_Type_commit(&v) == MPI_SUCCESS);
   int s; MPI_Aint lb, ext;
@@ -34,9 +34,34 @@ int main(int argc, char **argv) {
     CHECK(MPI_Type_size(all[i], &s) == MPI_SUCCESS && s == 400 * 13 * 47);
   }
   CHECK(MPI_Pack_size(3, sc, MPI_COMM_WORLD, &s) == MPI_SUCCESS && s == 3 * 244400);
+  /* beyond the reference: indexed / hindexed / indexed_block / struct / resized */
+  MPI_Datatype ix, hx, ib, st, rs, rv;
+  int bl[3] = {2, 3, 1}, dp[3] = {1, 5, 10};
+  CHECK(MPI_Type_indexed(3, bl, dp, MPI_DOUBLE, &ix) == MPI_SUCCESS && MPI_Type_commit(&ix) == MPI_SUCCESS);
+  CHECK(MPI_Type_size(ix, &s) == MPI_SUCCESS && s == 48);
+  CHECK(MPI_Type_get_extent(ix, &lb, &ext) == MPI_SUCCESS && lb == 8 && ext == 80);
+  MPI_Aint hd[2] = {64, 67};
+  int hbl[2] = {3, 5};
+  CHECK(MPI_Type_create_hindexed(2, hbl, hd, MPI_BYTE, &hx) == MPI_SUCCESS && MPI_Type_commit(&hx) == MPI_SUCCESS);
+  CHECK(MPI_Type_get_extent(hx, &lb, &ext) == MPI_SUCCESS && lb == 64 && ext == 8);
+  int ibd[4] = {0, 16, 32, 48};
+  CHECK(MPI_Type_create_indexed_block(4, 4, ibd, MPI_FLOAT, &ib) == MPI_SUCCESS && MPI_Type_commit(&ib) == MPI_SUCCESS);
+  CHECK(MPI_Type_size(ib, &s) == MPI_SUCCESS && s == 64);
+  CHECK(MPI_Type_get_extent(ib, &lb, &ext) == MPI_SUCCESS && lb == 0 && ext == 208);
+  int sbl[2] = {1, 2};
+  MPI_Aint sd[2] = {0, 8};
+  MPI_Datatype stt[2] = {MPI_INT, MPI_DOUBLE};
+  CHECK(MPI_Type_create_struct(2, sbl, sd, stt, &st) == MPI_SUCCESS && MPI_Type_commit(&st) == MPI_SUCCESS);
+  CHECK(MPI_Type_size(st, &s) == MPI_SUCCESS && s == 20);
+  CHECK(MPI_Type_get_extent(st, &lb, &ext) == MPI_SUCCESS && lb == 0 && ext == 24);
+  CHECK(MPI_Type_create_resized(st, 0, 32, &rs) == MPI_SUCCESS);
+  CHECK(MPI_Type_contiguous(4, rs, &rv) == MPI_SUCCESS && MPI_Type_commit(&rv) == MPI_SUCCESS);
+  CHECK(MPI_Type_get_extent(rv, &lb, &ext) == MPI_SUCCESS && lb == 0 && ext == 128);
+  MPI_Aint neg[1] = {-8};
+  int one[1] = {1};
+  CHECK(MPI_Type_create_hindexed(1, one, neg, MPI_BYTE, &x) == MPI_ERR_ARG);
   /* errors */
   int bad_sizes[1] = {8}, bad_sub[1] = {4}, bad_st[1] = {6};
-  MPI_Datatype x;
   CHECK(MPI_Type_create_subarray(1, bad_sizes, bad_sub, bad_st, MPI_ORDER_C, MPI_BYTE, &x) == MPI_ERR_ARG);
   CHECK(MPI_Type_size(12345, &s) == MPI_ERR_TYPE);
   CHECK(MPI_Type_free(&sc) == MPI_SUCCESS && sc == MPI_DATATYPE_NULL);

@@ -59,6 +59,14 @@ def test_mpi_types_and_topology(tmp_path, np_):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("np_", [1, 2])
+def test_mpi_indexed_struct_resized(cuda, tmp_path, np_):
+    """beyond the reference: irregular MPI_Type_indexed and a resized struct
+    through MPI_Pack/Unpack on device memory and Send/Recv (every method)"""
+    assert "OK" in run(np_, build(tmp_path, "mpi_indexed"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("np_", [1, 2])
 def test_mpi_pack_and_sendrecv(cuda, tmp_path, np_):
     assert "OK" in run(np_, build(tmp_path, "mpi_sendrecv"))
 
