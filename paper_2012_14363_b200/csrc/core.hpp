@@ -95,12 +95,15 @@ struct Run {
 };
 
 // Device copy of the definition-order run table for the block-list kernel.
+// The run table on the device, as pieces: runs in definition order, each
+// split into pieces of at most kPieceMax bytes so no single long run can
+// serialise a kernel.
+constexpr int64_t kPieceMax = int64_t{64} << 10;
 struct DeviceRuns {
   int device = -1;
-  int64_t *d_src = nullptr;   // run source offsets (within one object)
-  int64_t *d_dst = nullptr;   // exclusive prefix sum of lengths
-  int64_t *d_len = nullptr;
-  int64_t n = 0;
+  int64_t *d_src = nullptr;   // piece source offsets (within one object)
+  int64_t *d_dst = nullptr;   // packed offsets: exclusive prefix sum, n + 1 entries
+  int64_t n = 0;              // pieces
   uint64_t align_or = 0;      // OR of every run offset and length (word choice)
 };
 

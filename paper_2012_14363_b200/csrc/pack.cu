@@ -350,40 +350,50 @@ __global__ void __launch_bounds__(256) k_shift_unpack(const uint8_t *__restrict_
 // ------------------------------------------------------------ k_runs
 // Run-table kernel for forms without a strided canon (the reference's
 // zero-stride "Unsupported" types, irregular indexed/struct types) and for
-// strided forms with more row dims than KMAX. One thread per W-byte word of
-// the PACKED stream: the word's run is the last one whose packed offset is
-// <= the word's (binary search over the table, which stays L1/L2-resident
-// and is read by neighbouring lanes at the same addresses), so the packed
-// side is fully coalesced and every run's strided side is walked in order
-// by consecutive lanes. Runs are in definition order, so duplicated source
-// bytes pack with their multiplicity (pack.hpp:123-135).
+// strided forms with more row dims than KMAX. The table holds the runs in
+// definition order as pieces (<= kPieceMax bytes). A group of G = 2^lg
+// lanes takes one (object, piece) item at a time, grid-stride, prefetching
+// the next item's descriptor, and moves its W-byte words lane-strided with
+// four loads in flight per lane: both sides of a piece are contiguous, so a
+// group's accesses coalesce. G is the largest power of two <= the mean
+// piece length in words, capped at 16 (measured best from 16-B to 4-KiB
+// runs: scripts/runs_bench.py, profiles/r01_runs_kernel.md). Duplicated
+// source bytes pack with their multiplicity (pack.hpp:123-135).
 template <int W, bool PACK>
 __global__ void __launch_bounds__(256) k_runs(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
-                                              const int64_t *__restrict__ rsrc, const int64_t *__restrict__ rdst,
-                                              int64_t nruns, int64_t nobj, int64_t extent, int64_t size) {
+                                              const int64_t *__restrict__ psrc, const int64_t *__restrict__ pdst,
+                                              int64_t npieces, int64_t nobj, int64_t extent, int64_t size, int lg) {
   using T = typename Word<W>::T;
-  const int64_t wpo = size / W; // words per object
-  const int64_t total = wpo * nobj;
-  const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += step) {
-    const int64_t j = t / wpo;
-    const int64_t q = (t - j * wpo) * W;
-    int64_t lo = 0, hi = nruns - 1;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi + 1) >> 1;
-      if (__ldg(rdst + mid) <= q) {
-        lo = mid;
-      } else {
-        hi = mid - 1;
-      }
+  const int g = 1 << lg;
+  const int lane = static_cast<int>(threadIdx.x) & (g - 1);
+  const int64_t groups = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> lg;
+  const int64_t total = npieces * nobj;
+  int64_t p = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> lg;
+  if (p >= total) return;
+  // the next item's descriptor is loaded before this item's words move
+  int64_t k = p % npieces;
+  int64_t ns = __ldg(psrc + k), nd = __ldg(pdst + k), ne = __ldg(pdst + k + 1);
+  for (; p < total; p += groups) {
+    const int64_t j = p / npieces;
+    const int64_t s0 = ns, d0 = nd, words = (ne - nd) / W;
+    if (p + groups < total) {
+      k = (p + groups) % npieces;
+      ns = __ldg(psrc + k);
+      nd = __ldg(pdst + k);
+      ne = __ldg(pdst + k + 1);
     }
-    const int64_t so = j * extent + __ldg(rsrc + lo) + (q - __ldg(rdst + lo));
-    const int64_t po = j * size + q;
-    if (PACK) {
-      st_stream(reinterpret_cast<T *>(out + po), ld_stream(reinterpret_cast<const T *>(in + so)));
-    } else {
-      st_stream(reinterpret_cast<T *>(out + so), ld_stream(reinterpret_cast<const T *>(in + po)));
+    const T *sw = reinterpret_cast<const T *>(PACK ? in + j * extent + s0 : in + j * size + d0);
+    T *dw = reinterpret_cast<T *>(PACK ? out + j * size + d0 : out + j * extent + s0);
+    int64_t w = lane;
+    for (; w + 3 * g < words; w += 4 * g) { // four loads in flight before the stores
+      const T a = ld_stream(sw + w), b = ld_stream(sw + w + g), c = ld_stream(sw + w + 2 * g),
+              e = ld_stream(sw + w + 3 * g);
+      st_stream(dw + w, a);
+      st_stream(dw + w + g, b);
+      st_stream(dw + w + 2 * g, c);
+      st_stream(dw + w + 3 * g, e);
     }
+    for (; w < words; w += g) st_stream(dw + w, ld_stream(sw + w));
   }
 }
 
@@ -396,7 +406,6 @@ Committed::~Committed() {
     if (dev.device >= 0) cudaSetDevice(dev.device);
     cudaFree(dev.d_src);
     cudaFree(dev.d_dst);
-    cudaFree(dev.d_len);
     if (cur >= 0) cudaSetDevice(cur);
   }
 }
@@ -567,31 +576,30 @@ const DeviceRuns &device_runs(const Committed &ct, const std::vector<Run> &runs)
   if (ct.dev.d_src) {
     cudaFree(ct.dev.d_src);
     cudaFree(ct.dev.d_dst);
-    cudaFree(ct.dev.d_len);
     ct.dev = DeviceRuns{};
   }
-  const size_t n = runs.size();
-  std::vector<int64_t> hs(n), hd(n), hl(n);
+  std::vector<int64_t> hs, hd;
+  hs.reserve(runs.size());
+  hd.reserve(runs.size() + 1);
   int64_t acc = 0;
   uint64_t align_or = 0;
-  for (size_t k = 0; k < n; ++k) {
-    hs[k] = runs[k].off;
-    hd[k] = acc;
-    hl[k] = runs[k].len;
-    acc += runs[k].len;
-    align_or |= static_cast<uint64_t>(runs[k].off) | static_cast<uint64_t>(runs[k].len);
+  for (const Run &r : runs) {
+    align_or |= static_cast<uint64_t>(r.off) | static_cast<uint64_t>(r.len);
+    for (int64_t o = 0; o < r.len; o += kPieceMax) {
+      hs.push_back(r.off + o);
+      hd.push_back(acc + o);
+    }
+    acc += r.len;
   }
+  hd.push_back(acc);
   DeviceRuns d;
   d.device = cur;
-  d.n = static_cast<int64_t>(n);
+  d.n = static_cast<int64_t>(hs.size());
   d.align_or = align_or;
-  const size_t bytes = std::max<size_t>(n, 1) * sizeof(int64_t);
-  cuda_check(cudaMalloc(&d.d_src, bytes), "cudaMalloc(runs)");
-  cuda_check(cudaMalloc(&d.d_dst, bytes), "cudaMalloc(runs)");
-  cuda_check(cudaMalloc(&d.d_len, bytes), "cudaMalloc(runs)");
-  cuda_check(cudaMemcpy(d.d_src, hs.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice), "upload runs");
-  cuda_check(cudaMemcpy(d.d_dst, hd.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice), "upload runs");
-  cuda_check(cudaMemcpy(d.d_len, hl.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice), "upload runs");
+  cuda_check(cudaMalloc(&d.d_src, std::max<size_t>(hs.size(), 1) * sizeof(int64_t)), "cudaMalloc(runs)");
+  cuda_check(cudaMalloc(&d.d_dst, hd.size() * sizeof(int64_t)), "cudaMalloc(runs)");
+  cuda_check(cudaMemcpy(d.d_src, hs.data(), hs.size() * sizeof(int64_t), cudaMemcpyHostToDevice), "upload runs");
+  cuda_check(cudaMemcpy(d.d_dst, hd.data(), hd.size() * sizeof(int64_t), cudaMemcpyHostToDevice), "upload runs");
   ct.dev = d;
   return ct.dev;
 }
@@ -644,12 +652,17 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
         fail(SP_ERR_INVALID_ARGUMENT, "force_word is not legal for these buffers");
       w = opt.force_word;
     }
-    const unsigned grid = grid_for(static_cast<uint64_t>(ct.size / w * count), 1);
+    // lanes per piece: the largest power of two <= the mean piece length
+    // in words, at most 16
+    const int64_t mean_words = ct.size / w / std::max<int64_t>(dr.n, 1);
+    int lg = 0;
+    while (lg < 4 && (int64_t{2} << lg) <= mean_words) ++lg;
+    const unsigned grid = grid_for(static_cast<uint64_t>(dr.n * count) << lg, 1);
 #define SPB_RUNS(WW)                                                                                               \
   if (pack) {                                                                                                      \
-    k_runs<WW, true><<<grid, 256, 0, s>>>(in, out, dr.d_src, dr.d_dst, dr.n, count, ct.extent, ct.size);          \
+    k_runs<WW, true><<<grid, 256, 0, s>>>(in, out, dr.d_src, dr.d_dst, dr.n, count, ct.extent, ct.size, lg);      \
   } else {                                                                                                         \
-    k_runs<WW, false><<<grid, 256, 0, s>>>(in, out, dr.d_src, dr.d_dst, dr.n, count, ct.extent, ct.size);         \
+    k_runs<WW, false><<<grid, 256, 0, s>>>(in, out, dr.d_src, dr.d_dst, dr.n, count, ct.extent, ct.size, lg);     \
   }
     switch (w) {
     case 16: SPB_RUNS(16) break;
