@@ -487,6 +487,8 @@ namespace {
 // safe; a pool allocation freed on one stream and reused on another would
 // make the stream-ordered allocator insert a cross-stream dependency and
 // serialise the inbound and outbound legs of a pipelined exchange.
+constexpr size_t kStagePad = 32;
+
 uint8_t *stage_buffer(cudaStream_t s, size_t bytes) {
   struct Stage {
     uint8_t *p = nullptr;
@@ -498,9 +500,9 @@ uint8_t *stage_buffer(cudaStream_t s, size_t bytes) {
   cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
   std::lock_guard<std::mutex> lk(mu);
   Stage &st = stages[{dev, s}];
-  if (st.n < bytes) {
+  if (st.n < bytes + kStagePad) {
     if (st.p) cuda_check(cudaFreeAsync(st.p, s), "cudaFreeAsync(stage)");
-    const size_t n = std::max(bytes, st.n * 2);
+    const size_t n = std::max(bytes + kStagePad, st.n * 2);
     cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&st.p), n, s), "cudaMallocAsync(stage)");
     st.n = n;
   }
@@ -719,6 +721,10 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
   if (kernel == SP_KERNEL_SMALLROW && !smallrow_ok) fail(SP_ERR_INVALID_ARGUMENT, "smallrow kernel not applicable");
   // misaligned long rows: the word would be < kShiftBelow only because of
   // addresses / strides, the shift kernel keeps 16-B packed-side accesses
+  // (they read, never write, whole aligned 16-B blocks around the bytes a
+  // layout touches: up to 15 B beyond the span inside the same block, which
+  // cannot leave an allocation's 256-B-granular footprint; the engine's own
+  // staging buffers are padded so the sanitizer's exact bounds hold too)
   const bool shift_ok = rd.c0 >= 16 && fits32 && total_bytes < (1ull << 32);
   if (kernel == SP_KERNEL_WORDS && opt.kernel == SP_KERNEL_AUTO && !opt.force_word && shift_ok &&
       shift_wins(pack, w, rd.c0))
@@ -903,7 +909,9 @@ int64_t execute(const PackArgs &a) {
   }
   if (rs.kind == MemKind::Pageable) {
     staged = must_sync = true;
-    cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&scratch_s), static_cast<size_t>(strided_len), s),
+    // + kStagePad: the shift kernels read whole aligned 16-B blocks around
+    // the bytes a layout touches, which may run past an exact-size end
+    cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&scratch_s), static_cast<size_t>(strided_len) + kStagePad, s),
                "cudaMallocAsync(stage)");
     // pack reads the span; unpack must preserve bytes outside the layout
     cuda_check(cudaMemcpyAsync(scratch_s, strided_user, static_cast<size_t>(strided_len), cudaMemcpyHostToDevice, s),
@@ -912,7 +920,7 @@ int64_t execute(const PackArgs &a) {
   }
   if (rp.kind == MemKind::Pageable) {
     staged = must_sync = true;
-    cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&scratch_p), static_cast<size_t>(packed_len), s),
+    cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&scratch_p), static_cast<size_t>(packed_len) + kStagePad, s),
                "cudaMallocAsync(stage)");
     if (!a.pack)
       cuda_check(cudaMemcpyAsync(scratch_p, static_cast<const uint8_t *>(a.src) + a.position,

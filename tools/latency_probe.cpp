@@ -45,6 +45,10 @@ int main() {
   std::printf("cudaPointerGetAttributes   %8.2f us\n", med_us([&] { cudaPointerGetAttributes(&at, d + 64); }));
   cudaIpcMemHandle_t h;
   std::printf("cudaIpcGetMemHandle        %8.2f us\n", med_us([&] { cudaIpcGetMemHandle(&h, d); }));
+  int ndev = 0;
+  std::printf("cudaGetDeviceCount         %8.2f us\n", med_us([&] { cudaGetDeviceCount(&ndev); }));
+  std::printf("launch empty (enqueue)     %8.2f us\n", med_us([&] { k_empty<<<1, 32, 0, s>>>(); }));
+  cudaStreamSynchronize(s);
   cudaEvent_t ev;
   cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   std::printf("launch empty + sync        %8.2f us\n", med_us([&] {
