@@ -605,10 +605,10 @@ def run_ours(args):
     # A watchdog guarantees the driver its JSON line even if these hang.
     del flush
     torch.cuda.empty_cache()
-    halo = send = None
+    halo = send = irregular = None
     line_box = {}
     if not args.no_halo:
-        from tools.bench_parts import halo_section, send_section, send_self_section
+        from tools.bench_parts import halo_section, irregular_section, send_section, send_self_section
 
         def on_timeout():
             if rank == 0 and "line" in line_box:
@@ -641,6 +641,10 @@ def run_ours(args):
                 send = send_self_section(torch, rank, local, job)
         except Exception as exc:
             send = {"error": f"{type(exc).__name__}: {exc}"}
+        try:
+            irregular = irregular_section(torch) if rank == 0 else None
+        except Exception as exc:
+            irregular = {"error": f"{type(exc).__name__}: {exc}"}
         dog.cancel()
 
     if rank != 0:
@@ -656,6 +660,7 @@ def run_ours(args):
                          "PackOptions.threads=1 (the reference's fastest setting)"}
     line = build_line(args, value, step_ms, world, K, dominant, sweep, e2e_val, Ke, launches, clk, cpu, halo,
                       send, pcie_ms, single, pattern)
+    line["irregular_types"] = irregular
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

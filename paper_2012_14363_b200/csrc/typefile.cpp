@@ -9,6 +9,13 @@
 //   type <name> = subarray(<ndims>, [<sizes>], [<subsizes>], [<offsets>], <ref>)
 //   commit <name>
 //
+// Beyond the reference's grammar (the engine's MPI indexed/struct/resized
+// constructors; a reference parser rejects these lines as unknown):
+//   type <name> = indexed([<blocklengths>], [<displs in inner extents>], <ref>)
+//   type <name> = hindexed([<blocklengths>], [<displs in bytes>], <ref>)
+//   type <name> = struct([<blocklengths>], [<displs in bytes>], [<refs>])
+//   type <name> = resized(<ref>, <lb>, <extent>)
+//
 // <kind> is byte/int/float/double; <ref> a kind or an earlier name. Exactly
 // one commit, as the last statement. Every diagnostic is a ParseError
 // (SP_ERR_PARSE) prefixed "line N: "; constructor argument errors
@@ -145,6 +152,26 @@ private:
                         static_cast<int64_t>(offs.size()) != nd))
           fail(SP_ERR_INVALID_ARGUMENT, "subarray: sizes/subsizes/offsets must have ndims entries");
         def = make_subarray(nd, sizes.data(), subs.data(), offs.data(), std::move(inner), SP_ORDER_C);
+      } else if (ctor == "indexed" || ctor == "hindexed") {
+        arity(3);
+        const auto bl = list(args[0]);
+        auto d = list(args[1]);
+        DefPtr inner = resolve(args[2]);
+        if (bl.size() != d.size()) fail(SP_ERR_INVALID_ARGUMENT, ctor + ": one displacement per block");
+        if (ctor == "indexed")
+          for (int64_t &x : d) x *= inner->extent;
+        def = make_indexed(static_cast<int64_t>(bl.size()), bl.data(), d.data(), std::move(inner));
+      } else if (ctor == "struct") {
+        arity(3);
+        const auto bl = list(args[0]), d = list(args[1]);
+        std::vector<DefPtr> members;
+        for (std::string_view r : items(args[2])) members.push_back(resolve(r));
+        if (bl.size() != d.size() || bl.size() != members.size())
+          fail(SP_ERR_INVALID_ARGUMENT, "struct: one displacement and one type per block");
+        def = make_struct(static_cast<int64_t>(bl.size()), bl.data(), d.data(), members);
+      } else if (ctor == "resized") {
+        arity(3);
+        def = make_resized(resolve(args[0]), integer(args[1]), integer(args[2]));
       } else {
         error("unknown constructor '" + ctor + "'");
       }
@@ -184,11 +211,17 @@ private:
     return v;
   }
 
-  std::vector<int64_t> list(std::string_view s) const {
+  // the items of a [..] list ("[]" is empty)
+  std::vector<std::string_view> items(std::string_view s) const {
     if (s.size() < 2 || s.front() != '[' || s.back() != ']')
       error("expected a [..] list, got '" + std::string(s) + "'");
+    if (strip(s.substr(1, s.size() - 2)).empty()) return {};
+    return split(s.substr(1, s.size() - 2));
+  }
+
+  std::vector<int64_t> list(std::string_view s) const {
     std::vector<int64_t> out;
-    for (std::string_view item : split(s.substr(1, s.size() - 2))) out.push_back(integer(item));
+    for (std::string_view item : items(s)) out.push_back(integer(item));
     return out;
   }
 

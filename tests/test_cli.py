@@ -103,6 +103,29 @@ def test_flatten_marks_overlap(tf):  # test_cli.cpp:139-148
     assert run("flatten", tf("o.types", OVERLAP))[:2] == (0, "0 3472\n# overlap\n")
 
 
+# ---------------------------------------------------------------- beyond the reference
+def test_typefile_indexed_struct_resized(tf, sp):
+    """the engine's extra constructors in the type-file language: a regular
+    indexed type canonicalises, an irregular one reports the block-list form
+    (exit 2, like the reference's unsupported forms), struct + resized
+    flatten to the MPI typemap (oracle/typemap.py)"""
+    from oracle import typemap as tm
+    reg = "type d = named(double)\ntype t = indexed([2,2,2], [0,5,10], d)\ncommit t\n"
+    code, out, _ = run("canon", tf("reg.types", reg))
+    assert code == 0 and out.startswith("sb start=0 counts=[16,3] strides=[1,40]\n")
+    irr = "type t = hindexed([16,24,8], [8,40,80], byte)\ncommit t\n"
+    assert run("canon", tf("irr.types", irr))[:2] == (2, "unsupported blocks=3\n")
+    src = ("type d = named(double)\ntype s = struct([1,2], [0,8], [int, d])\n"
+           "type r = resized(s, 0, 32)\ntype v = contiguous(4, r)\ncommit v\n")
+    code, out, _ = run("flatten", tf("s.types", src))
+    _, _, _, runs = tm.typemap(("contiguous", 4, ("resized", 0, 32,
+                                                  ("struct", [1, 2], [0, 8], [("named", 4), ("named", 8)]))))
+    norm, _ = tm.normalized(runs)
+    assert code == 0 and out == "".join(f"{o} {n}\n" for o, n in norm)
+    code, _, err = run("canon", tf("bad.types", "type t = struct([1], [0, 8], [byte])\ncommit t\n"))
+    assert code == 1 and "line 1" in err
+
+
 # ---------------------------------------------------------------- choose
 def test_choose_prints_method_and_times():  # test_cli.cpp:226-245
     code, out, _ = run("choose", "--object-bytes", 4194304, "--block-bytes", 16, "--profile", PROFILE)

@@ -308,3 +308,60 @@ if __name__ == "__main__":  # one-rank halo section alone: python tools/bench_pa
     import torch
     torch.cuda.set_device(0)
     print(json.dumps(halo_section(torch, 0, 1, 0, uuid.uuid4().hex[:10])))
+
+
+def irregular_section(torch, blocks=(64, 1024, 4096), total=64 << 20, reps=5):
+    """Beyond the reference: irregular MPI_Type_create_hindexed byte types of
+    ~64 MiB (blocks of L/2..3L/2 bytes in multiples of 16 at random 16-B
+    gaps, scrambled definition order) through the run-table kernel, against
+    the regular hvector of the same mean block and pitch on the strided
+    kernels. Cold L2 (512 MiB flush on the timing stream), CUDA events,
+    median of `reps`; GB/s = 2 x packed bytes / kernel time."""
+    import numpy as np
+    import paper_2012_14363_b200 as sp
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    B = sp.make_named(sp.NamedKind.Byte)
+    rng = np.random.default_rng(1)
+
+    def timed(fn):
+        ts = []
+        for _ in range(reps):
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b) * 1e3)
+        return statistics.median(ts)
+
+    rows = []
+    for L in blocks:
+        n = total // L
+        lens = (rng.integers(L // 32, 3 * L // 32 + 1, n).clip(1) * 16).astype(np.int64)
+        gaps = (rng.integers(0, L // 16 + 1, n) * 16).astype(np.int64)
+        displs = np.cumsum(gaps + lens) - lens
+        perm = rng.permutation(n)
+        t = sp.commit_type(sp.make_hindexed(lens[perm].tolist(), displs[perm].tolist(), B))
+        src = torch.randint(0, 256, (t.span,), dtype=torch.uint8, device="cuda")
+        dst = torch.empty(t.size, dtype=torch.uint8, device="cuda")
+        pitch = max(int(np.mean(gaps + lens)) // 16 * 16, L)
+        v = sp.commit_type(sp.make_hvector(total // L, L, pitch, B))
+        vsrc = torch.randint(0, 256, (v.span,), dtype=torch.uint8, device="cuda")
+        vdst = torch.empty(v.size, dtype=torch.uint8, device="cuda")
+        pk = timed(lambda: sp.pack(src, t, 1, dst, 0))
+        li = sp.last_launch()
+        up = timed(lambda: sp.unpack(dst, 0, t, 1, src))
+        vp = timed(lambda: sp.pack(vsrc, v, 1, vdst, 0))
+        vu = timed(lambda: sp.unpack(vdst, 0, v, 1, vsrc))
+        rows.append({"mean_block": L, "runs": int(n), "bytes": int(t.size),
+                     "kernel": f"{li.kernel.name}/w{li.word}",
+                     "pack_GBps": round(2 * t.size / pk / 1e3, 1), "unpack_GBps": round(2 * t.size / up / 1e3, 1),
+                     "strided_pack_GBps": round(2 * v.size / vp / 1e3, 1),
+                     "strided_unpack_GBps": round(2 * v.size / vu / 1e3, 1)})
+        del src, dst, vsrc, vdst
+    del flush
+    torch.cuda.empty_cache()
+    return {"what": "irregular hindexed types (beyond the reference) on the run-table kernel vs the regular "
+                    "hvector of the same mean block and pitch on the strided kernels; cold L2",
+            "rows": rows}
