@@ -516,6 +516,22 @@ unsigned grid_for(uint64_t items, int per_thread) {
   return static_cast<unsigned>(std::max<uint64_t>(1, std::min(blocks, cap)));
 }
 
+// grid of 256-thread CTAs for `items` threads of work, capped at one
+// resident wave of `kern` (occupancy queried once per kernel and device)
+template <class K> unsigned resident_grid(K kern, uint64_t items) {
+  static thread_local int dev = -1, occ = 0;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != dev) {
+    dev = cur;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0) != cudaSuccess || occ < 1) occ = 1;
+  }
+  const uint64_t blocks = (items + 255) / 256;
+  const uint64_t cap = static_cast<uint64_t>(sm_count()) * static_cast<uint64_t>(occ);
+  const uint64_t hcap = t_host_grid_cap ? std::min<uint64_t>(cap, t_host_grid_cap) : cap;
+  return static_cast<unsigned>(std::max<uint64_t>(1, std::min(blocks, hcap)));
+}
+
 template <int W, bool PACK>
 void launch_words(const uint8_t *in, uint8_t *out, const Geom &g, cudaStream_t s, sp_launch_info &li) {
   const bool big = g.total >= static_cast<uint64_t>(sm_count()) * 2048 * 4;
@@ -659,11 +675,16 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
     const int64_t mean_words = ct.size / w / std::max<int64_t>(dr.n, 1);
     int lg = 0;
     while (lg < 4 && (int64_t{2} << lg) <= mean_words) ++lg;
-    const unsigned grid = grid_for(static_cast<uint64_t>(dr.n * count) << lg, 1);
+    // one resident wave: the grid is capped at what fits (48 registers a
+    // thread leave room for 5 CTAs of 256 per SM, not the 8 grid_for assumes)
+    const uint64_t items = static_cast<uint64_t>(dr.n * count) << lg;
+    unsigned grid = 1;
 #define SPB_RUNS(WW)                                                                                               \
   if (pack) {                                                                                                      \
+    grid = resident_grid(k_runs<WW, true>, items);                                                                 \
     k_runs<WW, true><<<grid, 256, 0, s>>>(in, out, dr.d_src, dr.d_dst, dr.n, count, ct.extent, ct.size, lg);      \
   } else {                                                                                                         \
+    grid = resident_grid(k_runs<WW, false>, items);                                                                \
     k_runs<WW, false><<<grid, 256, 0, s>>>(in, out, dr.d_src, dr.d_dst, dr.n, count, ct.extent, ct.size, lg);     \
   }
     switch (w) {

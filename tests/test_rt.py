@@ -330,6 +330,20 @@ def _nbrw(rank, world, job):
     call(src, recv)
     torch.cuda.synchronize()
     assert torch.equal(recv, expect(9)), (rank, "re-init")
+    # a handle freed between calls: the memoised handle lookups must notice
+    # (MPI_ERR_TYPE territory), not reuse the freed type's record
+    from paper_2012_14363_b200 import _capi
+    import ctypes as C
+    extra = sp.make_contiguous(16, B)
+    hs = (_capi.sp_type * 1)(extra.handle)
+    sc = (C.c_int64 * 1)(0)
+    nb = (C.c_int * 1)(rank)
+    lib = _capi.lib
+    assert lib.sp_rt_neighbor_alltoallw(src.data_ptr(), sc, sc, hs, 1, nb, recv.data_ptr(), sc, sc, hs, 1, nb) == 0
+    assert lib.sp_type_free(extra.handle) == 0
+    st = lib.sp_rt_neighbor_alltoallw(src.data_ptr(), sc, sc, hs, 1, nb, recv.data_ptr(), sc, sc, hs, 1, nb)
+    assert st == 11, st  # SP_ERR_INVALID_HANDLE
+    extra.handle = 0  # already freed
     rt.finalize()
     return ok
 

@@ -326,7 +326,8 @@ def irregular_section(torch, blocks=(64, 1024, 4096), total=64 << 20, reps=5):
     def timed(fn):
         ts = []
         for _ in range(reps):
-            flush.fill_(1)
+            flush.fill_(1)  # 512 MiB written, then read back: a cold, clean L2
+            flush.view(torch.int64).sum()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             fn()
