@@ -335,6 +335,7 @@ def _nbrw(rank, world, job):
     from paper_2012_14363_b200 import _capi
     import ctypes as C
     extra = sp.make_contiguous(16, B)
+    assert _capi.lib.sp_type_commit(extra.handle) == 0
     hs = (_capi.sp_type * 1)(extra.handle)
     sc = (C.c_int64 * 1)(0)
     nb = (C.c_int * 1)(rank)
