@@ -250,7 +250,7 @@ sp_status sp_rt_neighbor_alltoallv(const void *sendbuf, const int64_t *sendcount
                             (rtp->form == SP_FORM_STRIDED && rtp->sb.ndims() == 1 && rtp->sb.start == 0 &&
                              rtp->extent == rtp->size);
     if (dense_recv) { // packed receive buffer: pack-to-peer batch
-      rt_neighbor_alltoallv(static_cast<const uint8_t *>(sendbuf), sc, sd, *st, static_cast<uint8_t *>(recvbuf), rc,
+      rt_neighbor_alltoallv(static_cast<const uint8_t *>(sendbuf), sc, sd, st, static_cast<uint8_t *>(recvbuf), rc,
                             rd, *rtp, ss, ds);
       return;
     }

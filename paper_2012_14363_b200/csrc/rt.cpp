@@ -1145,10 +1145,23 @@ void nbr_publish(uint8_t *recvbuf, const std::vector<int> &sources, const std::v
 // Last call of each neighbour collective: when a call repeats it (same
 // arguments, every out-neighbour's layout version unchanged) the cached
 // batch is relaunched without rebuilding jobs or cache keys.
+// An out-edge whose send type has no strided form (an irregular indexed or
+// struct type) into a receive layout that is one dense run: the run-table
+// kernel packs it straight into the receiver's buffer, launched ahead of
+// the call's batch on the same stream (whose completion flags then cover
+// it: stream order puts its stores before the batch's release).
+struct LooseOp {
+  CommitPtr ct;
+  const uint8_t *src;
+  int64_t count;
+  uint8_t *dst; // receiver's bytes for this edge, already at their offset
+};
+
 struct NbrLast {
   std::string sig;
   std::vector<std::pair<int, uint64_t>> peer_ver;
   Batch *batch = nullptr;
+  std::vector<LooseOp> loose;
   bool valid = false;
 };
 
@@ -1169,9 +1182,11 @@ bool nbr_last_hit(const NbrLast &last, const std::string &sig) {
   return true;
 }
 
-void nbr_last_set(NbrLast &last, std::string sig, const std::vector<int> &dests, Batch *b) {
+void nbr_last_set(NbrLast &last, std::string sig, const std::vector<int> &dests, Batch *b,
+                  std::vector<LooseOp> loose) {
   Runtime &R = rt();
   last.sig = std::move(sig);
+  last.loose = std::move(loose);
   last.peer_ver.clear();
   std::vector<char> seen(R.size, 0);
   for (int d : dests)
@@ -1187,9 +1202,12 @@ template <class T> void append_bytes(std::string &s, const std::vector<T> &v) {
   s.append(reinterpret_cast<const char *>(v.data()), v.size() * sizeof(T));
 }
 
-// batch-cache key part of a committed type: its geometry
+// batch-cache key part of a committed type: its geometry (and, for a
+// block-list form, which has no geometry to compare, the record itself --
+// the cached call holds it, so the address cannot be reused meanwhile)
 void append_type_key(std::string &key, const Committed &c) {
-  const int64_t head[5] = {c.form, c.size, c.extent, c.span, c.sb.start};
+  const int64_t head[6] = {c.form, c.size, c.extent, c.span, c.sb.start,
+                           c.form == SP_FORM_STRIDED ? 0 : reinterpret_cast<int64_t>(&c)};
   key.append(reinterpret_cast<const char *>(head), sizeof(head));
   key.append(reinterpret_cast<const char *>(c.sb.counts.data()), c.sb.counts.size() * sizeof(int64_t));
   key.append(reinterpret_cast<const char *>(c.sb.strides.data()), c.sb.strides.size() * sizeof(int64_t));
@@ -1239,8 +1257,22 @@ BatchSignal nbr_enter(const std::vector<int> &sources, const std::vector<int> &d
   return bs;
 }
 
-void nbr_run(Batch *b, const BatchSignal &bs) {
+void nbr_run(Batch *b, const std::vector<LooseOp> &loose, const BatchSignal &bs) {
   Runtime &R = rt();
+  for (const LooseOp &op : loose) {
+    PackArgs a{};
+    a.ct = op.ct.get();
+    a.src = op.src;
+    a.src_bytes = UINT64_MAX;
+    a.dst = op.dst;
+    a.dst_bytes = UINT64_MAX;
+    a.count = op.count;
+    a.position = 0;
+    a.stream = R.stream;
+    a.opt = sp_pack_options{1, SP_KERNEL_AUTO, 0};
+    a.pack = true;
+    execute(a);
+  }
   if (b) {
     batch_execute_signaled(*b, R.stream, bs);
   } else {
@@ -1250,10 +1282,11 @@ void nbr_run(Batch *b, const BatchSignal &bs) {
 }
 
 void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &send_counts,
-                           const std::vector<int64_t> &send_displs, const Committed &st, uint8_t *recvbuf,
+                           const std::vector<int64_t> &send_displs, const CommitPtr &stp, uint8_t *recvbuf,
                            const std::vector<int64_t> &recv_counts, const std::vector<int64_t> &recv_displs,
                            const Committed &rtp, const std::vector<int> &sources, const std::vector<int> &dests) {
   Runtime &R = rt();
+  const Committed &st = *stp;
   if (static_cast<int>(sources.size()) > kMaxEdges) fail(SP_ERR_UNSUPPORTED, "neighbour exchange: indegree > 256");
   const bool dense_recv = rtp.form == SP_FORM_STRIDED && rtp.sb.ndims() == 1 && rtp.sb.start == 0 &&
                           rtp.extent == rtp.size;
@@ -1275,11 +1308,13 @@ void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &s
   append_bytes(sig, dests);
   append_type_key(sig, st);
   if (nbr_last_hit(g_last_v, sig)) {
-    nbr_run(g_last_v.batch, bs);
+    nbr_run(g_last_v.batch, g_last_v.loose, bs);
     return;
   }
   std::string key(reinterpret_cast<const char *>(&sendbuf), sizeof(sendbuf));
   std::vector<BatchSpec> jobs;
+  std::vector<LooseOp> loose;
+  const bool blocklist = st.form != SP_FORM_STRIDED; // irregular send type: run-table packs
   std::vector<int> seen(R.size, 0);
   for (size_t i = 0; i < dests.size(); ++i) {
     const int d = dests[i];
@@ -1296,6 +1331,10 @@ void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &s
     if (bytes > peer.edges[hit][2]) fail(SP_ERR_BUFFER_TOO_SMALL, "neighbour exchange: message truncated");
     if (bytes == 0) continue;
     uint8_t *base = d == R.rank ? recvbuf : open_ipc(peer.xh) + peer.xoff;
+    if (blocklist) {
+      loose.push_back({stp, sendbuf + send_displs[i] * st.extent, send_counts[i], base + peer.edges[hit][1]});
+      continue;
+    }
     jobs.push_back({&st, sendbuf + send_displs[i] * st.extent, UINT64_MAX, send_counts[i], base, UINT64_MAX,
                     peer.edges[hit][1]});
     const int64_t sig[4] = {reinterpret_cast<int64_t>(base), peer.edges[hit][1], send_counts[i], send_displs[i]};
@@ -1314,8 +1353,8 @@ void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &s
       g_nbr_cache.pop_front();
     }
   }
-  nbr_last_set(g_last_v, std::move(sig), dests, b);
-  nbr_run(b, bs); // returns when every block addressed to this rank has landed
+  nbr_run(b, loose, bs); // returns when every block addressed to this rank has landed
+  nbr_last_set(g_last_v, std::move(sig), dests, b, std::move(loose));
 }
 
 // MPI_Neighbor_alltoallw with per-edge datatypes on BOTH sides: each rank
@@ -1406,7 +1445,7 @@ void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &s
   if (g_wlast.valid && g_wlast.args == args && g_last_w.valid) {
     const BatchSignal bs = nbr_enter(sources, dests);
     if (nbr_peers_unchanged(g_last_w)) {
-      nbr_run(g_last_w.batch, bs);
+      nbr_run(g_last_w.batch, g_last_w.loose, bs);
       return;
     }
     g_wlast.valid = false; // a neighbour re-published: rebuild below (entered already)
@@ -1450,11 +1489,12 @@ void rt_neighbor_alltoallw_build(const uint8_t *sendbuf, const std::vector<int64
   append_bytes(sig, dests);
   for (const CommitPtr &t : send_types) append_type_key(sig, *t);
   if (nbr_last_hit(g_last_w, sig)) {
-    nbr_run(g_last_w.batch, bs);
+    nbr_run(g_last_w.batch, g_last_w.loose, bs);
     return;
   }
   std::string key(reinterpret_cast<const char *>(&sendbuf), sizeof(sendbuf));
   std::vector<CopySpec> jobs;
+  std::vector<LooseOp> loose;
   std::vector<std::unique_ptr<Committed>> dst_types;
   std::vector<int> seen(R.size, 0);
   for (size_t i = 0; i < dests.size(); ++i) {
@@ -1475,9 +1515,19 @@ void rt_neighbor_alltoallw_build(const uint8_t *sendbuf, const std::vector<int64
       fail(SP_ERR_INVALID_ARGUMENT, "neighbour alltoallw: send and receive describe different byte counts");
     if (bytes == 0) continue;
     const Desc &wd = peer.wdesc[hit];
+    uint8_t *base = (d == R.rank ? recvbuf : open_ipc(peer.xh) + peer.xoff) + peer.edges[hit][1];
+    if (st.form != SP_FORM_STRIDED) {
+      // an irregular send type: the run-table kernel packs it in place when
+      // the receive layout is one dense run; typed copies between two
+      // irregular layouts are not offered
+      if (wd.ndims != 1 || (wd.count > 1 && wd.extent != wd.size))
+        fail(SP_ERR_UNSUPPORTED,
+             "neighbour alltoallw: an irregular (block-list) send type needs a contiguous receive layout");
+      loose.push_back({send_types[i], sendbuf + send_displs[i], send_counts[i], base + wd.start});
+      continue;
+    }
     auto dc = std::make_unique<Committed>();
     committed_from(wd, *dc);
-    uint8_t *base = (d == R.rank ? recvbuf : open_ipc(peer.xh) + peer.xoff) + peer.edges[hit][1];
     jobs.push_back({&st, sendbuf + send_displs[i], UINT64_MAX, send_counts[i], dc.get(), base, UINT64_MAX, wd.count});
     const int64_t sig[5] = {reinterpret_cast<int64_t>(base), send_counts[i], send_displs[i], wd.count, wd.start};
     key.append(reinterpret_cast<const char *>(sig), sizeof(sig));
@@ -1498,8 +1548,8 @@ void rt_neighbor_alltoallw_build(const uint8_t *sendbuf, const std::vector<int64
       g_nbrw_cache.pop_front();
     }
   }
-  nbr_last_set(g_last_w, std::move(sig), dests, b);
-  nbr_run(b, bs); // returns when every block addressed to this rank has landed
+  nbr_run(b, loose, bs); // returns when every block addressed to this rank has landed
+  nbr_last_set(g_last_w, std::move(sig), dests, b, std::move(loose));
 }
 
 } // namespace spb

@@ -39,7 +39,7 @@ void rt_set_profile(sp_profile_s *p);
 int rt_choose(const Committed &ct, int64_t count);
 void *rt_stream();
 void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &send_counts,
-                           const std::vector<int64_t> &send_displs, const Committed &st, uint8_t *recvbuf,
+                           const std::vector<int64_t> &send_displs, const CommitPtr &stp, uint8_t *recvbuf,
                            const std::vector<int64_t> &recv_counts, const std::vector<int64_t> &recv_displs,
                            const Committed &rtp, const std::vector<int> &sources, const std::vector<int> &dests);
 

@@ -394,6 +394,87 @@ def test_neighbor_alltoallv_packed_and_strided_receive(cuda):
     assert all(_spawn(_nbrv, 3).values())
 
 
+def _nbr_irregular(rank, world, job):
+    """Unstructured-mesh style neighbour exchange: each rank sends an
+    irregular MPI_Type_indexed gather list (different per neighbour, so not
+    one strided form) and receives contiguous ghost runs.
+    MPI_Neighbor_alltoallw (per-edge types) and MPI_Neighbor_alltoallv (one
+    irregular send type, packed receive), repeated (the cached fast path)
+    with changing source data, on a ring of 3."""
+    import numpy as np
+    import torch
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.rt as rt
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=1 << 20, host_bytes=1 << 20)
+    right, left = (rank + 1) % world, (rank - 1) % world
+    D = sp.make_named(sp.NamedKind.Double)
+
+    def gather_list(seed):
+        g = np.random.default_rng(seed)
+        n = 300
+        bl = g.integers(1, 4, n).tolist()
+        slots = g.permutation(1024)[:n]
+        return bl, [int(x) * 4 for x in slots]  # blocks of <= 3 doubles in 4-double slots
+
+    def itype(seed):
+        bl, dp = gather_list(seed)
+        return sp.commit_type(sp.make_indexed(bl, dp, D)), bl, dp
+
+    # edge types keyed by (sender, receiver): both ends build the same list
+    t_r, bl_r, dp_r = itype(100 * rank + right)
+    t_l, bl_l, dp_l = itype(100 * rank + left)
+    _, bl_in_l, dp_in_l = itype(100 * left + rank)    # what the left neighbour sends me
+    _, bl_in_r, dp_in_r = itype(100 * right + rank)
+    n_from_l, n_from_r = sum(bl_in_l), sum(bl_in_r)
+    ghost_l = sp.commit_type(sp.make_contiguous(n_from_l, D))
+    ghost_r = sp.commit_type(sp.make_contiguous(n_from_r, D))
+    N = 4096
+    field = torch.empty(N, dtype=torch.float64, device="cuda")
+    recv = torch.empty(n_from_l + n_from_r + 8, dtype=torch.float64, device="cuda")
+
+    def values(r, it):
+        return torch.arange(N, dtype=torch.float64, device="cuda") * 3 + r * 100000 + it
+
+    def expect_from(r, bl, dp, it):
+        v = values(r, it).cpu().numpy()
+        return np.concatenate([v[d:d + b] for b, d in zip(bl, dp)])
+
+    call = rt.NeighborW([(right, 1, t_r, 0), (left, 1, t_l, 0)],
+                        [(left, 1, ghost_l, 0), (right, 1, ghost_r, 8 * n_from_l)])
+    for it in range(4):
+        field.copy_(values(rank, it))
+        recv.fill_(-1)
+        torch.cuda.synchronize()
+        call(field, recv)
+        torch.cuda.synchronize()
+        got = recv.cpu().numpy()
+        assert np.array_equal(got[:n_from_l], expect_from(left, bl_in_l, dp_in_l, it)), (rank, it, "left")
+        assert np.array_equal(got[n_from_l:n_from_l + n_from_r], expect_from(right, bl_in_r, dp_in_r, it)), (rank, it)
+        assert (got[n_from_l + n_from_r:] == -1).all()
+    # alltoallv: one irregular send type for both neighbours, packed receive
+    tv, blv, dpv = itype(7)  # the same list on every rank
+    nv = sum(blv)
+    packed = sp.commit_type(sp.make_contiguous(8, sp.make_named(sp.NamedKind.Byte)))  # one double
+    for it in range(3):
+        field.copy_(values(rank, 10 + it))
+        recv2 = torch.full((2 * nv,), -1.0, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        rt.neighbor_alltoallv(field, tv, [(right, 1, 0), (left, 1, 0)], recv2, packed,
+                              [(left, nv, 0), (right, nv, nv)])
+        torch.cuda.synchronize()
+        got = recv2.cpu().numpy()
+        assert np.array_equal(got[:nv], expect_from(left, blv, dpv, 10 + it)), (rank, it, "v-left")
+        assert np.array_equal(got[nv:], expect_from(right, blv, dpv, 10 + it)), (rank, it, "v-right")
+    rt.finalize()
+    return True
+
+
+@pytest.mark.gpu
+def test_neighbor_collectives_with_irregular_send_types(cuda):
+    assert all(_spawn(_nbr_irregular, 3).values())
+
+
 def _halo_soak(rank, world, job, ranks, method, iters):
     """many back-to-back iterations with no barrier between them (the
     in-kernel flags alone order the ranks against each other), three rounds
