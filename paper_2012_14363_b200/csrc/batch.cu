@@ -517,14 +517,19 @@ Batch *copy_batch_create(const std::vector<CopySpec> &specs) {
 namespace {
 
 template <int W, int MODE> void launch_batch(const BatchGroup &g, const BatchSig &sig, cudaStream_t s, unsigned &grid) {
-  static thread_local int occ_dev = -1, occ = 0;
+  // one resident wave of the kernel actually launched (the parameter-table
+  // and the smem-staged variants are occupancy-queried separately)
+  static thread_local int occ_dev = -1, occ_t = 0, occ_s = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (occ_dev != dev) {
-    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_batch<W, MODE>, 256, 0), "occupancy");
-    occ = std::max(occ, 1);
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_batch<W, MODE>, 256, 0), "occupancy");
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, k_batchp<W, MODE>, 256, 0), "occupancy");
+    occ_s = std::max(occ_s, 1);
+    occ_t = std::max(occ_t, 1);
     occ_dev = dev;
   }
+  const int occ = g.table ? occ_t : occ_s;
   grid = static_cast<unsigned>(
       std::max<uint64_t>(1, std::min<uint64_t>(g.nchunks, static_cast<uint64_t>(sm_count()) * occ)));
   if (g.table) {

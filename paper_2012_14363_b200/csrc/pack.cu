@@ -517,14 +517,16 @@ unsigned grid_for(uint64_t items, int per_thread) {
 }
 
 // grid of 256-thread CTAs for `items` threads of work, capped at one
-// resident wave of `kern` (occupancy queried once per kernel and device)
-template <class K> unsigned resident_grid(K kern, uint64_t items) {
+// resident wave of kernel K (occupancy queried once per kernel and device;
+// the template parameter is the kernel itself, so every instantiation has
+// its own cache)
+template <auto K> unsigned resident_grid(uint64_t items) {
   static thread_local int dev = -1, occ = 0;
   int cur = 0;
   cudaGetDevice(&cur);
   if (cur != dev) {
     dev = cur;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0) != cudaSuccess || occ < 1) occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K, 256, 0) != cudaSuccess || occ < 1) occ = 1;
   }
   const uint64_t blocks = (items + 255) / 256;
   const uint64_t cap = static_cast<uint64_t>(sm_count()) * static_cast<uint64_t>(occ);
@@ -681,10 +683,10 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
     unsigned grid = 1;
 #define SPB_RUNS(WW)                                                                                               \
   if (pack) {                                                                                                      \
-    grid = resident_grid(k_runs<WW, true>, items);                                                                 \
+    grid = resident_grid<k_runs<WW, true>>(items);                                                                 \
     k_runs<WW, true><<<grid, 256, 0, s>>>(in, out, dr.d_src, dr.d_dst, dr.n, count, ct.extent, ct.size, lg);      \
   } else {                                                                                                         \
-    grid = resident_grid(k_runs<WW, false>, items);                                                                \
+    grid = resident_grid<k_runs<WW, false>>(items);                                                                \
     k_runs<WW, false><<<grid, 256, 0, s>>>(in, out, dr.d_src, dr.d_dst, dr.n, count, ct.extent, ct.size, lg);     \
   }
     switch (w) {
