@@ -637,8 +637,22 @@ void send_stream(Req &q) {
     Committed dst;
     committed_from(d, dst);
     uint8_t *base = q.peer == R.rank ? reinterpret_cast<uint8_t *>(d.raw) : open_ipc(d.h) + d.off;
-    const CopySpec spec{q.ct.get(), q.sbuf, q.buf_bytes, q.count, &dst, base, UINT64_MAX, d.count};
-    copy_execute(spec, 0, static_cast<uint64_t>(q.bytes), s);
+    if (q.ct->form != SP_FORM_STRIDED) { // block-list send type: pack into the dense receive run
+      PackArgs a{};
+      a.ct = q.ct.get();
+      a.src = q.sbuf;
+      a.src_bytes = q.buf_bytes;
+      a.dst = base + d.start;
+      a.dst_bytes = static_cast<uint64_t>(q.bytes);
+      a.count = q.count;
+      a.stream = s;
+      a.opt = sp_pack_options{1, SP_KERNEL_AUTO, 0};
+      a.pack = true;
+      execute(a);
+    } else {
+      const CopySpec spec{q.ct.get(), q.sbuf, q.buf_bytes, q.count, &dst, base, UINT64_MAX, d.count};
+      copy_execute(spec, 0, static_cast<uint64_t>(q.bytes), s);
+    }
     q.chunks.assign(1, {0, q.bytes});
   } else {
     uint8_t *dst = nullptr;
@@ -700,8 +714,19 @@ bool step_send(Req &q) {
     // device-accessible, the receiver accepts when its buffer is device
     // memory, and otherwise the fallback (the model's choice, or DEVICE
     // for an explicit DIRECT) moves the message
-    const bool direct_ok = q.bytes > 0 && q.allow_direct && range_capable(*q.ct, q.count, q.sbuf, q.sbuf);
-    post(q.peer, Msg{kRTS, R.rank, q.tag, q.method, q.bytes, direct_ok ? 1 : 0, static_cast<int64_t>(q.id)});
+    // offer 1: a strided send type (typed copy into any describable
+    // receive layout); offer 2: a block-list send type (run-table pack,
+    // needs a receive layout that is one dense run)
+    int offer = 0;
+    if (q.bytes > 0 && q.allow_direct) {
+      if (q.ct->form == SP_FORM_STRIDED && range_capable(*q.ct, q.count, q.sbuf, q.sbuf)) offer = 1;
+      if (q.ct->form == SP_FORM_UNSUPPORTED) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, q.sbuf) == cudaSuccess && at.type == cudaMemoryTypeDevice) offer = 2;
+        cudaGetLastError();
+      }
+    }
+    post(q.peer, Msg{kRTS, R.rank, q.tag, q.method, q.bytes, offer, static_cast<int64_t>(q.id)});
     q.st = St::WaitCts;
     return true;
   }
@@ -764,8 +789,11 @@ bool step_recv(Req &q) {
       }
       // DIRECT upgrade: the sender can run the copy kernel, the destination
       // is device memory and the type has a publishable canonical form
-      if (!q.err && m.offset == 1 && describable(*q.ct) &&
-          range_capable(*q.ct, m.bytes / q.ct->size, q.rbuf, q.rbuf)) {
+      const int64_t objs = q.ct->size ? m.bytes / q.ct->size : 0;
+      const bool dense = q.ct->form == SP_FORM_STRIDED && q.ct->sb.ndims() == 1 &&
+                         (objs <= 1 || q.ct->extent == q.ct->size);
+      if (!q.err && ((m.offset == 1 && describable(*q.ct) && range_capable(*q.ct, objs, q.rbuf, q.rbuf)) ||
+                     (m.offset == 2 && dense && describable(*q.ct)))) {
         cudaPointerAttributes at{};
         const bool dev = cudaPointerGetAttributes(&at, q.rbuf) == cudaSuccess && at.type == cudaMemoryTypeDevice;
         cudaGetLastError();
@@ -774,7 +802,7 @@ bool step_recv(Req &q) {
         // bytes, where the fallback ships packed full lines and unpacks
         // locally -- accept DIRECT from another GPU only for rows >= 64 B
         const bool remote = R.shm->slots[m.src].device != R.device;
-        const bool rows_ok = !remote || q.ct->sb.counts[0] >= kDirectRemoteMinRow;
+        const bool rows_ok = m.offset == 2 || !remote || q.ct->sb.counts[0] >= kDirectRemoteMinRow;
         if (dev && rows_ok) q.method = SP_METHOD_DIRECT; // a descriptor slot is taken at the grant
       }
       q.st = St::Matched;

@@ -87,6 +87,9 @@ int main(int argc, char **argv) {
         MPI_Status s;
         cudaMemset(dpk, 0, total * 8);
         CHECK(MPI_Recv(dpk, 1, flat, 0, 70 + m, MPI_COMM_WORLD, &s) == MPI_SUCCESS);
+        /* the irregular send lands by DIRECT (run-table pack straight into the
+           contiguous receive buffer) when offered: explicitly and by the model */
+        if (m == 3 || m == -1) CHECK(s.method == 3);
         cudaMemcpy(hp, dpk, total * 8, cudaMemcpyDeviceToHost);
         k = 0;
         for (int i = 0; i < NB; ++i)
