@@ -1419,6 +1419,7 @@ struct WArgs {
 struct WLastCall {
   WArgs args{};
   std::vector<CommitPtr> keep_s, keep_r;
+  uint64_t my_ver = 0; // this rank's layout version right after that call
   bool valid = false;
 };
 WLastCall g_wlast;
@@ -1458,6 +1459,7 @@ void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &s
                            uint8_t *recvbuf, const std::vector<int64_t> &recv_counts,
                            const std::vector<int64_t> &recv_displs, const std::vector<CommitPtr> &recv_types,
                            const std::vector<int> &sources, const std::vector<int> &dests) {
+  const Runtime &R = rt();
   if (static_cast<int>(sources.size()) > kMaxWEdges) fail(SP_ERR_UNSUPPORTED, "neighbour alltoallw: indegree > 64");
   // repeat of the previous call (same buffers, counts, displacements,
   // neighbours and commit records, and the receive buffer still the same
@@ -1470,7 +1472,10 @@ void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &s
   for (const CommitPtr &t : recv_types) args.rtp.push_back(t.get());
   if (recvbuf && std::any_of(recv_counts.begin(), recv_counts.end(), [](int64_t c) { return c > 0; }))
     ipc_handle_of(recvbuf, &args.h, &args.off);
-  if (g_wlast.valid && g_wlast.args == args && g_last_w.valid) {
+  // (another neighbour call publishing a different layout in between moves
+  // this rank's layout version and disables the repeat path)
+  if (g_wlast.valid && g_wlast.args == args && g_last_w.valid &&
+      R.shm->slots[R.rank].layout_ver.load(std::memory_order_relaxed) == g_wlast.my_ver) {
     const BatchSignal bs = nbr_enter(sources, dests);
     if (nbr_peers_unchanged(g_last_w)) {
       nbr_run(g_last_w.batch, g_last_w.loose, bs);
@@ -1478,7 +1483,8 @@ void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &s
     }
     g_wlast.valid = false; // a neighbour re-published: rebuild below (entered already)
     rt_neighbor_alltoallw_build(sendbuf, send_counts, send_displs, send_types, recvbuf, dests, bs);
-    g_wlast = WLastCall{std::move(args), send_types, recv_types, true};
+    g_wlast = WLastCall{std::move(args), send_types, recv_types,
+                        R.shm->slots[R.rank].layout_ver.load(std::memory_order_relaxed), true};
     return;
   }
   g_wlast.valid = false;
@@ -1500,7 +1506,8 @@ void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &s
   }
   const BatchSignal bs = nbr_enter(sources, dests); // replaces a barrier
   rt_neighbor_alltoallw_build(sendbuf, send_counts, send_displs, send_types, recvbuf, dests, bs);
-  g_wlast = WLastCall{std::move(args), send_types, recv_types, true};
+  g_wlast = WLastCall{std::move(args), send_types, recv_types,
+                      R.shm->slots[R.rank].layout_ver.load(std::memory_order_relaxed), true};
 }
 
 // the send side of an alltoallw call once entered: find (or build) the

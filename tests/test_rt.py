@@ -466,6 +466,17 @@ def _nbr_irregular(rank, world, job):
         got = recv2.cpu().numpy()
         assert np.array_equal(got[:nv], expect_from(left, blv, dpv, 10 + it)), (rank, it, "v-left")
         assert np.array_equal(got[nv:], expect_from(right, blv, dpv, 10 + it)), (rank, it, "v-right")
+    # the alltoallw again with identical arguments: the alltoallv in between
+    # published another receive layout, so the repeat path must not skip
+    # re-publishing this call's layout
+    field.copy_(values(rank, 20))
+    recv.fill_(-1)
+    torch.cuda.synchronize()
+    call(field, recv)
+    torch.cuda.synchronize()
+    got = recv.cpu().numpy()
+    assert np.array_equal(got[:n_from_l], expect_from(left, bl_in_l, dp_in_l, 20)), (rank, "w-again")
+    assert np.array_equal(got[n_from_l:n_from_l + n_from_r], expect_from(right, bl_in_r, dp_in_r, 20))
     rt.finalize()
     return True
 
