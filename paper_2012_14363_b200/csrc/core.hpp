@@ -176,6 +176,16 @@ struct PackArgs {
 // validated launch (pack.cu); returns new position
 int64_t execute(const PackArgs &a);
 
+// several block-list packs in one launch (pack.cu): each job packs `count`
+// objects of a block-list form from src to the packed bytes at dst
+struct RunJob {
+  const Committed *ct;
+  const void *src;
+  int64_t count;
+  void *dst;
+};
+void runs_pack_multi(const std::vector<RunJob> &jobs, void *stream);
+
 void set_last_launch(const sp_launch_info &li);
 void cuda_check(int err, const char *what);  // cudaError_t as int
 void require_device();

@@ -397,6 +397,58 @@ __global__ void __launch_bounds__(256) k_runs(const uint8_t *__restrict__ in, ui
   }
 }
 
+// Several run-table packs in one launch (the irregular edges of a
+// neighbour collective): the edge table travels in kernel-parameter space,
+// an item (edge, object, piece) finds its edge by binary search over the
+// edges' first-item indices (constant cache), then moves like k_runs.
+constexpr int kRunEdges = 32;
+struct RunEdge {
+  const int64_t *psrc, *pdst;
+  int64_t npieces, nobj, extent, size, item0;
+  const uint8_t *in;
+  uint8_t *out;
+};
+struct RunTable {
+  RunEdge e[kRunEdges];
+  int n;
+  int64_t total;
+};
+
+template <int W>
+__global__ void __launch_bounds__(256) k_runs_multi(const __grid_constant__ RunTable t, int lg) {
+  using T = typename Word<W>::T;
+  const int g = 1 << lg;
+  const int lane = static_cast<int>(threadIdx.x) & (g - 1);
+  const int64_t groups = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> lg;
+  for (int64_t p = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> lg; p < t.total; p += groups) {
+    int a = 0, b = t.n - 1;
+    while (a < b) {
+      const int m = (a + b + 1) >> 1;
+      if (t.e[m].item0 <= p) {
+        a = m;
+      } else {
+        b = m - 1;
+      }
+    }
+    const RunEdge &e = t.e[a];
+    const int64_t local = p - e.item0;
+    const int64_t j = local / e.npieces, k = local - j * e.npieces;
+    const int64_t s0 = __ldg(e.psrc + k), d0 = __ldg(e.pdst + k), words = (__ldg(e.pdst + k + 1) - d0) / W;
+    const T *sw = reinterpret_cast<const T *>(e.in + j * e.extent + s0);
+    T *dw = reinterpret_cast<T *>(e.out + j * e.size + d0);
+    int64_t w = lane;
+    for (; w + 3 * g < words; w += 4 * g) {
+      const T v0 = ld_stream(sw + w), v1 = ld_stream(sw + w + g), v2 = ld_stream(sw + w + 2 * g),
+              v3 = ld_stream(sw + w + 3 * g);
+      st_stream(dw + w, v0);
+      st_stream(dw + w + g, v1);
+      st_stream(dw + w + 2 * g, v2);
+      st_stream(dw + w + 3 * g, v3);
+    }
+    for (; w < words; w += g) st_stream(dw + w, ld_stream(sw + w));
+  }
+}
+
 // ============================================================ host side
 
 Committed::~Committed() {
@@ -860,6 +912,12 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
+
+template <int W> unsigned launch_runs_multi(const RunTable &t, int lg, cudaStream_t s) {
+  const unsigned grid = resident_grid<k_runs_multi<W>>(static_cast<uint64_t>(t.total) << lg);
+  k_runs_multi<W><<<grid, 256, 0, s>>>(t, lg);
+  return grid;
+}
 } // namespace
 
 
@@ -973,6 +1031,65 @@ int64_t execute(const PackArgs &a) {
   li.staged = staged;
   set_last_launch(li);
   return a.position + packed_len;
+}
+
+// Several run-table packs, one launch per up to kRunEdges jobs: the
+// irregular (block-list) send edges of a neighbour collective, each packed
+// straight into its receiver's dense run. Buffers must be device, pinned or
+// peer-mapped memory; counts of 0 are skipped.
+void runs_pack_multi(const std::vector<RunJob> &jobs, void *stream) {
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<RunEdge> edges;
+  uint64_t align = 0;
+  int64_t bytes = 0, items = 0;
+  for (const RunJob &j : jobs) {
+    if (j.count <= 0 || j.ct->size == 0) continue;
+    if (j.ct->form == SP_FORM_STRIDED) fail(SP_ERR_INTERNAL, "runs_pack_multi: strided form");
+    const Resolved rs = resolve(j.src), rd = resolve(j.dst);
+    if (rs.kind == MemKind::Pageable || rd.kind == MemKind::Pageable)
+      fail(SP_ERR_INVALID_ARGUMENT, "neighbour exchange: buffers must be device, pinned or peer-mapped memory");
+    const DeviceRuns &dr = device_runs(*j.ct, j.ct->runs);
+    RunEdge e{};
+    e.psrc = dr.d_src;
+    e.pdst = dr.d_dst;
+    e.npieces = dr.n;
+    e.nobj = j.count;
+    e.extent = j.ct->extent;
+    e.size = j.ct->size;
+    e.in = rs.dptr;
+    e.out = rd.dptr;
+    align |= dr.align_or | static_cast<uint64_t>(e.extent) | static_cast<uint64_t>(e.size) |
+             reinterpret_cast<uint64_t>(e.in) | reinterpret_cast<uint64_t>(e.out);
+    bytes += e.size * e.nobj;
+    items += e.npieces * e.nobj;
+    edges.push_back(e);
+  }
+  if (edges.empty()) return;
+  require_device();
+  const int w = pow2_align(align);
+  const int64_t mean_words = bytes / w / std::max<int64_t>(items, 1);
+  int lg = 0;
+  while (lg < 4 && (int64_t{2} << lg) <= mean_words) ++lg;
+  for (size_t at = 0; at < edges.size(); at += kRunEdges) {
+    RunTable t{};
+    t.n = static_cast<int>(std::min<size_t>(kRunEdges, edges.size() - at));
+    int64_t acc = 0;
+    for (int i = 0; i < t.n; ++i) {
+      t.e[i] = edges[at + static_cast<size_t>(i)];
+      t.e[i].item0 = acc;
+      acc += t.e[i].npieces * t.e[i].nobj;
+    }
+    t.total = acc;
+    switch (w) {
+    case 16: launch_runs_multi<16>(t, lg, s); break;
+    case 8: launch_runs_multi<8>(t, lg, s); break;
+    case 4: launch_runs_multi<4>(t, lg, s); break;
+    case 2: launch_runs_multi<2>(t, lg, s); break;
+    default: launch_runs_multi<1>(t, lg, s); break;
+    }
+    cuda_check(cudaGetLastError(), "k_runs_multi launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
 }
 
 } // namespace spb

@@ -1175,9 +1175,10 @@ void nbr_publish(uint8_t *recvbuf, const std::vector<int> &sources, const std::v
 // batch is relaunched without rebuilding jobs or cache keys.
 // An out-edge whose send type has no strided form (an irregular indexed or
 // struct type) into a receive layout that is one dense run: the run-table
-// kernel packs it straight into the receiver's buffer, launched ahead of
-// the call's batch on the same stream (whose completion flags then cover
-// it: stream order puts its stores before the batch's release).
+// kernel packs it straight into the receiver's buffer -- all such edges of
+// a call in one launch (k_runs_multi) -- ahead of the call's batch on the
+// same stream, whose completion flags then cover it (stream order puts its
+// stores before the batch's release).
 struct LooseOp {
   CommitPtr ct;
   const uint8_t *src;
@@ -1287,19 +1288,11 @@ BatchSignal nbr_enter(const std::vector<int> &sources, const std::vector<int> &d
 
 void nbr_run(Batch *b, const std::vector<LooseOp> &loose, const BatchSignal &bs) {
   Runtime &R = rt();
-  for (const LooseOp &op : loose) {
-    PackArgs a{};
-    a.ct = op.ct.get();
-    a.src = op.src;
-    a.src_bytes = UINT64_MAX;
-    a.dst = op.dst;
-    a.dst_bytes = UINT64_MAX;
-    a.count = op.count;
-    a.position = 0;
-    a.stream = R.stream;
-    a.opt = sp_pack_options{1, SP_KERNEL_AUTO, 0};
-    a.pack = true;
-    execute(a);
+  if (!loose.empty()) { // every irregular edge in one run-table launch
+    std::vector<RunJob> jobs;
+    jobs.reserve(loose.size());
+    for (const LooseOp &op : loose) jobs.push_back({op.ct.get(), op.src, op.count, op.dst});
+    runs_pack_multi(jobs, R.stream);
   }
   if (b) {
     batch_execute_signaled(*b, R.stream, bs);
