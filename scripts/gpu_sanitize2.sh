@@ -11,3 +11,5 @@ for tool in racecheck synccheck; do
 done
 timeout 1200 $CS --tool memcheck --target-processes all --error-exitcode 86 --print-limit 20 python -m pytest -q -x -m gpu \
   tests/test_rt.py -k "nonblocking or sendrecv or distributed_halo" 2>&1 | tail -4 | tee gpurun_out/memcheck_rt.log
+timeout 1200 $CS --tool memcheck --target-processes all --error-exitcode 86 --print-limit 20 python -m pytest -q -x -m gpu \
+  tests/test_rt.py -k "irregular or layout or alltoallv" 2>&1 | tail -5 | tee gpurun_out/memcheck_rt_irregular.log
