@@ -1112,7 +1112,11 @@ int rt_choose(const Committed &ct, int64_t count) {
   Runtime &R = rt();
   if (!R.cache || ct.size == 0) return SP_METHOD_DEVICE;
   const int64_t obj = ct.size * count;
-  const int64_t blk = ct.form == SP_FORM_STRIDED ? std::min(ct.sb.counts[0], obj) : 1;
+  // block size of the model query (halo.hpp:296 uses counts[0]); a
+  // block-list form contributes its mean run length
+  const int64_t blk = ct.form == SP_FORM_STRIDED
+                          ? std::min(ct.sb.counts[0], obj)
+                          : std::max<int64_t>(1, ct.runs.empty() ? 1 : ct.size / static_cast<int64_t>(ct.runs.size()));
   int m = SP_METHOD_DEVICE;
   if (sp_model_cache_choose(R.cache.get(), obj, blk, &m) != SP_OK) return SP_METHOD_DEVICE;
   return m;
