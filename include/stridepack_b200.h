@@ -254,7 +254,10 @@ typedef struct {
 } sp_copy_job;
 /* one typed copy, one launch, no descriptor upload (the job travels as a
  * kernel parameter): MPI_Sendrecv of two datatypes within one process, or
- * a send to self. Buffers: device, pinned or peer-mapped memory. */
+ * a send to self. Buffers: device, pinned or peer-mapped memory. A
+ * block-list (irregular) layout on one side needs one dense run on the
+ * other (it runs as a run-table pack or unpack); two irregular sides are
+ * SP_ERR_UNSUPPORTED. */
 sp_status sp_copy(const sp_copy_job *job, void *stream);
 sp_status sp_copy_batch_create(const sp_copy_job *jobs, int64_t n,
                                sp_batch *out);

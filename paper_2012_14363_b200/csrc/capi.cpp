@@ -293,12 +293,55 @@ sp_status sp_batch_create(const sp_batch_job *jobs, int64_t n, int unpack, sp_ba
   });
 }
 
+namespace {
+// one dense run per object and objects back to back: the packed format
+bool dense(const spb::Committed &c, int64_t count) {
+  return c.form == SP_FORM_STRIDED && c.sb.ndims() == 1 && (count <= 1 || c.extent == c.size);
+}
+
+// a typed copy with a block-list (irregular) side: a run-table pack into a
+// dense destination, or a run-table unpack from a dense source
+bool copy_blocklist(const sp_copy_job &j, const spb::Committed &cs, const spb::Committed &cd, void *stream) {
+  if (cs.form == SP_FORM_STRIDED && cd.form == SP_FORM_STRIDED) return false;
+  if (j.src_count * cs.size != j.dst_count * cd.size)
+    spb::fail(SP_ERR_INVALID_ARGUMENT, "copy: source and destination describe different byte counts");
+  if (j.src_count * cs.size == 0) return true;
+  spb::PackArgs a{};
+  a.stream = stream;
+  a.opt = sp_pack_options{1, SP_KERNEL_AUTO, 0};
+  if (cs.form != SP_FORM_STRIDED && dense(cd, j.dst_count)) {
+    if (j.dst_bytes < static_cast<uint64_t>(cd.sb.start)) spb::fail(SP_ERR_BUFFER_TOO_SMALL, "copy: destination too small");
+    a.ct = &cs;
+    a.src = j.src;
+    a.src_bytes = j.src_bytes;
+    a.dst = static_cast<uint8_t *>(j.dst) + cd.sb.start;
+    a.dst_bytes = j.dst_bytes - static_cast<uint64_t>(cd.sb.start);
+    a.count = j.src_count;
+    a.pack = true;
+  } else if (cd.form != SP_FORM_STRIDED && dense(cs, j.src_count)) {
+    if (j.src_bytes < static_cast<uint64_t>(cs.sb.start)) spb::fail(SP_ERR_BUFFER_TOO_SMALL, "copy: source too small");
+    a.ct = &cd;
+    a.src = static_cast<const uint8_t *>(j.src) + cs.sb.start;
+    a.src_bytes = j.src_bytes - static_cast<uint64_t>(cs.sb.start);
+    a.dst = j.dst;
+    a.dst_bytes = j.dst_bytes;
+    a.count = j.dst_count;
+    a.pack = false;
+  } else {
+    spb::fail(SP_ERR_UNSUPPORTED, "copy: a block-list (irregular) layout needs a dense run on the other side");
+  }
+  spb::execute(a);
+  return true;
+}
+} // namespace
+
 sp_status sp_copy(const sp_copy_job *job, void *stream) {
   SPB_TRACE("sp_copy");
   return guard([&] {
     if (!job) spb::fail(SP_ERR_INVALID_ARGUMENT, "null job");
     const spb::Entry es = spb::registry().get(job->src_type), ed = spb::registry().get(job->dst_type);
     if (!es.committed || !ed.committed) spb::fail(SP_ERR_INVALID_ARGUMENT, "type is not committed");
+    if (copy_blocklist(*job, *es.committed, *ed.committed, stream)) return;
     const spb::CopySpec spec{es.committed.get(), job->src, job->src_bytes, job->src_count, ed.committed.get(),
                              job->dst, job->dst_bytes, job->dst_count};
     spb::copy_execute(spec, 0, static_cast<uint64_t>(job->src_count * es.committed->size), stream);

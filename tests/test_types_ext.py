@@ -189,3 +189,36 @@ def test_large_irregular_indexed_gpu(sp, cuda, word):
     sp.unpack(dst, 0, c, 2, out, **kw)
     exp = tm.scatter(want, np.zeros(c.extent + span, np.uint8), runs, 2, c.extent)
     assert np.array_equal(out.cpu().numpy(), exp)
+
+
+@pytest.mark.gpu
+def test_typed_copy_with_irregular_side(sp, cuda):
+    """sp.copy (typed copy) with a block-list layout on one side and a dense
+    run on the other: gather (irregular -> contiguous) and scatter
+    (contiguous with a start offset -> irregular), 3 objects each; two
+    irregular sides are refused"""
+    torch = cuda
+    rng = np.random.default_rng(8)
+    D = sp.make_named(sp.NamedKind.Double)
+    desc = ("indexed", [2, 1, 3, 2], [12, 0, 5, 20], ("named", 8))
+    size, _, _, runs = tm.typemap(desc)
+    irr = sp.commit_type(tm.build(sp, desc))
+    assert irr.form == sp.CanonForm.Unsupported
+    n = size // 8
+    flat = sp.commit_type(sp.make_contiguous(n, D))
+    host = rng.integers(0, 256, 3 * irr.extent + irr.span, dtype=np.uint8)
+    want = tm.gather(host, runs, 3, irr.extent, size)
+    src = torch.from_numpy(host).cuda()
+    out = torch.zeros(3 * size, dtype=torch.uint8, device="cuda")
+    sp.copy(src, irr, 3, out, flat, 3)
+    assert np.array_equal(out.cpu().numpy(), want)
+    # contiguous (offset 24, one object of 3*n doubles) -> irregular
+    big = sp.commit_type(sp.make_hindexed([3 * n], [24], D))
+    src2 = torch.zeros(24 + 3 * size, dtype=torch.uint8, device="cuda")
+    src2[24:] = out
+    back = torch.full((host.size,), 0x5A, dtype=torch.uint8, device="cuda")
+    sp.copy(src2, big, 1, back, irr, 3)
+    exp = tm.scatter(want, np.full(host.size, 0x5A, np.uint8), runs, 3, irr.extent)
+    assert np.array_equal(back.cpu().numpy(), exp)
+    with pytest.raises(sp.Unsupported):
+        sp.copy(src, irr, 1, back, irr, 1)
