@@ -481,6 +481,47 @@ def _nbr_irregular(rank, world, job):
     return True
 
 
+def _nbr_many_irregular(rank, world, job):
+    """40 irregular edges to self in one MPI_Neighbor_alltoallw: more than
+    one run-table launch's worth of edges (32 per launch)"""
+    import numpy as np
+    import torch
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.rt as rt
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=1 << 20, host_bytes=1 << 20)
+    D = sp.make_named(sp.NamedKind.Double)
+    g = np.random.default_rng(4)
+    field = torch.randn(1 << 16, dtype=torch.float64, device="cuda")
+    sends, recvs, lists, at = [], [], [], 0
+    for e in range(40):
+        bl = g.integers(1, 4, 50).tolist()
+        dp = [int(x) * 4 for x in g.choice(1 << 14, 50, replace=False)]
+        t = sp.commit_type(sp.make_indexed(bl, dp, D))
+        n = sum(bl)
+        sends.append((rank, 1, t, 0))
+        recvs.append((rank, 1, sp.commit_type(sp.make_contiguous(n, D)), at * 8))
+        lists.append((bl, dp, at))
+        at += n
+    recv = torch.zeros(at, dtype=torch.float64, device="cuda")
+    before = sp.kernel_launch_count()
+    rt.NeighborW(sends, recvs)(field, recv)
+    torch.cuda.synchronize()
+    assert sp.kernel_launch_count() - before == 2  # 32 + 8 edges
+    f = field.cpu().numpy()
+    r = recv.cpu().numpy()
+    for bl, dp, off in lists:
+        want = np.concatenate([f[d:d + b] for b, d in zip(bl, dp)])
+        assert np.array_equal(r[off:off + len(want)], want)
+    rt.finalize()
+    return True
+
+
+@pytest.mark.gpu
+def test_neighbor_alltoallw_many_irregular_edges(cuda):
+    assert all(_spawn(_nbr_many_irregular, 1).values())
+
+
 @pytest.mark.gpu
 def test_neighbor_collectives_with_irregular_send_types(cuda):
     assert all(_spawn(_nbr_irregular, 3).values())
