@@ -222,3 +222,17 @@ def test_typed_copy_with_irregular_side(sp, cuda):
     assert np.array_equal(back.cpu().numpy(), exp)
     with pytest.raises(sp.Unsupported):
         sp.copy(src, irr, 1, back, irr, 1)
+
+
+def test_typed_copy_irregular_validation(sp):
+    """validation before any launch (runs on CPU too): two irregular sides
+    are refused, and byte counts must agree"""
+    import torch
+    D = sp.make_named(sp.NamedKind.Double)
+    irr = sp.commit_type(sp.make_indexed([2, 1], [3, 0], D))
+    flat = sp.commit_type(sp.make_contiguous(3, D))
+    buf = torch.zeros(256, dtype=torch.uint8)
+    with pytest.raises(sp.Unsupported):
+        sp.copy(buf, irr, 1, buf, irr, 1)
+    with pytest.raises(sp.InvalidArgument):
+        sp.copy(buf, irr, 2, buf, flat, 1)
