@@ -358,6 +358,7 @@ def irregular_section(torch, blocks=(64, 1024, 4096), total=64 << 20, reps=5):
         rows.append({"mean_block": L, "runs": int(n), "bytes": int(t.size),
                      "kernel": f"{li.kernel.name}/w{li.word}",
                      "pack_GBps": round(2 * t.size / pk / 1e3, 1), "unpack_GBps": round(2 * t.size / up / 1e3, 1),
+                     "pack_frac_of_hbm": round(2 * t.size / pk / 1e3 / _hbm_peak(), 3),
                      "strided_pack_GBps": round(2 * v.size / vp / 1e3, 1),
                      "strided_unpack_GBps": round(2 * v.size / vu / 1e3, 1)})
         del src, dst, vsrc, vdst
