@@ -176,15 +176,24 @@ struct PackArgs {
 // validated launch (pack.cu); returns new position
 int64_t execute(const PackArgs &a);
 
-// several block-list packs in one launch (pack.cu): each job packs `count`
-// objects of a block-list form from src to the packed bytes at dst
+// several block-list moves in one launch (pack.cu): each job packs `count`
+// objects of a block-list form from src to the packed bytes at dst, or
+// (unpack) scatters packed src through the form into dst. The form is `ct`
+// (its cached device run table) or, when ct is null, an explicit device
+// run table (e.g. a peer's, mapped through CUDA IPC).
 struct RunJob {
   const Committed *ct;
   const void *src;
   int64_t count;
   void *dst;
+  bool unpack = false;
+  const int64_t *psrc = nullptr, *pdst = nullptr;
+  int64_t npieces = 0, size = 0, extent = 0;
+  uint64_t align = 0;
 };
-void runs_pack_multi(const std::vector<RunJob> &jobs, void *stream);
+void runs_multi(const std::vector<RunJob> &jobs, void *stream);
+// the device run table of a block-list form (uploaded once, cached)
+const DeviceRuns &device_run_table(const Committed &ct);
 
 void set_last_launch(const sp_launch_info &li);
 void cuda_check(int err, const char *what);  // cudaError_t as int

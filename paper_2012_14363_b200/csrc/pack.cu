@@ -407,6 +407,7 @@ struct RunEdge {
   int64_t npieces, nobj, extent, size, item0;
   const uint8_t *in;
   uint8_t *out;
+  int64_t unpack; // 0: gather into packed `out`; 1: scatter packed `in`
 };
 struct RunTable {
   RunEdge e[kRunEdges];
@@ -434,8 +435,8 @@ __global__ void __launch_bounds__(256) k_runs_multi(const __grid_constant__ RunT
     const int64_t local = p - e.item0;
     const int64_t j = local / e.npieces, k = local - j * e.npieces;
     const int64_t s0 = __ldg(e.psrc + k), d0 = __ldg(e.pdst + k), words = (__ldg(e.pdst + k + 1) - d0) / W;
-    const T *sw = reinterpret_cast<const T *>(e.in + j * e.extent + s0);
-    T *dw = reinterpret_cast<T *>(e.out + j * e.size + d0);
+    const T *sw = reinterpret_cast<const T *>(e.unpack ? e.in + j * e.size + d0 : e.in + j * e.extent + s0);
+    T *dw = reinterpret_cast<T *>(e.unpack ? e.out + j * e.extent + s0 : e.out + j * e.size + d0);
     int64_t w = lane;
     for (; w + 3 * g < words; w += 4 * g) {
       const T v0 = ld_stream(sw + w), v1 = ld_stream(sw + w + g), v2 = ld_stream(sw + w + 2 * g),
@@ -1033,32 +1034,49 @@ int64_t execute(const PackArgs &a) {
   return a.position + packed_len;
 }
 
-// Several run-table packs, one launch per up to kRunEdges jobs: the
-// irregular (block-list) send edges of a neighbour collective, each packed
-// straight into its receiver's dense run. Buffers must be device, pinned or
+// Several run-table moves, one launch per up to kRunEdges jobs: the
+// irregular (block-list) edges of a neighbour collective, each packed
+// straight into its receiver's dense run, or a dense run scattered through
+// the receiver's published run table. Buffers must be device, pinned or
 // peer-mapped memory; counts of 0 are skipped.
-void runs_pack_multi(const std::vector<RunJob> &jobs, void *stream) {
+const DeviceRuns &device_run_table(const Committed &ct) {
+  if (ct.form == SP_FORM_STRIDED) fail(SP_ERR_INTERNAL, "run table of a strided form");
+  return device_runs(ct, ct.runs);
+}
+
+void runs_multi(const std::vector<RunJob> &jobs, void *stream) {
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
   std::vector<RunEdge> edges;
   uint64_t align = 0;
   int64_t bytes = 0, items = 0;
   for (const RunJob &j : jobs) {
-    if (j.count <= 0 || j.ct->size == 0) continue;
-    if (j.ct->form == SP_FORM_STRIDED) fail(SP_ERR_INTERNAL, "runs_pack_multi: strided form");
+    RunEdge e{};
+    uint64_t table_align = j.align;
+    if (j.ct) {
+      if (j.ct->form == SP_FORM_STRIDED) fail(SP_ERR_INTERNAL, "runs_multi: strided form");
+      const DeviceRuns &dr = device_runs(*j.ct, j.ct->runs);
+      e.psrc = dr.d_src;
+      e.pdst = dr.d_dst;
+      e.npieces = dr.n;
+      e.extent = j.ct->extent;
+      e.size = j.ct->size;
+      table_align = dr.align_or;
+    } else {
+      e.psrc = j.psrc;
+      e.pdst = j.pdst;
+      e.npieces = j.npieces;
+      e.extent = j.extent;
+      e.size = j.size;
+    }
+    if (j.count <= 0 || e.size == 0) continue;
     const Resolved rs = resolve(j.src), rd = resolve(j.dst);
     if (rs.kind == MemKind::Pageable || rd.kind == MemKind::Pageable)
       fail(SP_ERR_INVALID_ARGUMENT, "neighbour exchange: buffers must be device, pinned or peer-mapped memory");
-    const DeviceRuns &dr = device_runs(*j.ct, j.ct->runs);
-    RunEdge e{};
-    e.psrc = dr.d_src;
-    e.pdst = dr.d_dst;
-    e.npieces = dr.n;
     e.nobj = j.count;
-    e.extent = j.ct->extent;
-    e.size = j.ct->size;
     e.in = rs.dptr;
     e.out = rd.dptr;
-    align |= dr.align_or | static_cast<uint64_t>(e.extent) | static_cast<uint64_t>(e.size) |
+    e.unpack = j.unpack ? 1 : 0;
+    align |= table_align | static_cast<uint64_t>(e.extent) | static_cast<uint64_t>(e.size) |
              reinterpret_cast<uint64_t>(e.in) | reinterpret_cast<uint64_t>(e.out);
     bytes += e.size * e.nobj;
     items += e.npieces * e.nobj;

@@ -66,12 +66,17 @@ constexpr int kDescDims = 12;
 constexpr int kMaxWEdges = 64;
 struct Desc {
   int32_t ndims;
-  int32_t pad;
+  int32_t runs; // 1: a block-list layout, described by its device run table below
   int64_t start, size, extent, span, count;
   int64_t counts[kDescDims], strides[kDescDims];
   cudaIpcMemHandle_t h;
   int64_t off;
   uint64_t raw;
+  // runs == 1: the receiver's run table (piece source offsets, packed
+  // prefix) for peers through CUDA IPC, and raw for the receiver itself
+  cudaIpcMemHandle_t hs, hd;
+  int64_t os, od, npieces;
+  uint64_t align, raw_s, raw_d;
 };
 
 struct Slot {
@@ -1188,6 +1193,11 @@ struct LooseOp {
   const uint8_t *src;
   int64_t count;
   uint8_t *dst; // receiver's bytes for this edge, already at their offset
+  // a dense send run scattered through the receiver's run table (ct null)
+  bool unpack = false;
+  const int64_t *psrc = nullptr, *pdst = nullptr;
+  int64_t npieces = 0, size = 0, extent = 0;
+  uint64_t align = 0;
 };
 
 struct NbrLast {
@@ -1295,8 +1305,10 @@ void nbr_run(Batch *b, const std::vector<LooseOp> &loose, const BatchSignal &bs)
   if (!loose.empty()) { // every irregular edge in one run-table launch
     std::vector<RunJob> jobs;
     jobs.reserve(loose.size());
-    for (const LooseOp &op : loose) jobs.push_back({op.ct.get(), op.src, op.count, op.dst});
-    runs_pack_multi(jobs, R.stream);
+    for (const LooseOp &op : loose)
+      jobs.push_back({op.ct.get(), op.src, op.count, op.dst, op.unpack, op.psrc, op.pdst, op.npieces, op.size,
+                      op.extent, op.align});
+    runs_multi(jobs, R.stream);
   }
   if (b) {
     batch_execute_signaled(*b, R.stream, bs);
@@ -1422,6 +1434,22 @@ struct WLastCall {
 WLastCall g_wlast;
 
 void desc_of(const Committed &c, int64_t count, Desc &d) {
+  if (c.form != SP_FORM_STRIDED) { // block-list: publish the device run table
+    const DeviceRuns &dr = device_run_table(c);
+    d.runs = 1;
+    d.ndims = 0;
+    d.size = c.size;
+    d.extent = c.extent;
+    d.span = c.span;
+    d.count = count;
+    d.npieces = dr.n;
+    d.align = dr.align_or;
+    d.raw_s = reinterpret_cast<uint64_t>(dr.d_src);
+    d.raw_d = reinterpret_cast<uint64_t>(dr.d_dst);
+    ipc_handle_of(dr.d_src, &d.hs, &d.os);
+    ipc_handle_of(dr.d_dst, &d.hd, &d.od);
+    return;
+  }
   d.ndims = c.sb.ndims();
   d.start = c.sb.start;
   for (int i = 0; i < d.ndims; ++i) {
@@ -1492,8 +1520,9 @@ void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &s
     for (size_t j = 0; j < sources.size(); ++j) {
       const Committed &rt_ = *recv_types[j];
       bytes[j] = recv_counts[j] * rt_.size;
-      if (bytes[j] > 0 && !describable(rt_))
-        fail(SP_ERR_UNSUPPORTED, "neighbour alltoallw: receive types need a strided, non-overlapping canonical form");
+      const bool runs = rt_.form == SP_FORM_UNSUPPORTED && !rt_.overlapping;
+      if (bytes[j] > 0 && !describable(rt_) && !runs)
+        fail(SP_ERR_UNSUPPORTED, "neighbour alltoallw: receive types need a non-overlapping layout");
       if (bytes[j] > 0) {
         desc_of(rt_, recv_counts[j], descs[j]);
         dp[j] = &descs[j];
@@ -1548,6 +1577,30 @@ void rt_neighbor_alltoallw_build(const uint8_t *sendbuf, const std::vector<int64
     if (bytes == 0) continue;
     const Desc &wd = peer.wdesc[hit];
     uint8_t *base = (d == R.rank ? recvbuf : open_ipc(peer.xh) + peer.xoff) + peer.edges[hit][1];
+    if (wd.runs) {
+      // an irregular receive layout: a dense send run scattered through the
+      // receiver's run table (read over NVLink from the receiver's HBM)
+      const bool dense = st.form == SP_FORM_STRIDED && st.sb.ndims() == 1 &&
+                         (send_counts[i] <= 1 || st.extent == st.size);
+      if (!dense)
+        fail(SP_ERR_UNSUPPORTED,
+             "neighbour alltoallw: an irregular (block-list) receive type needs a contiguous send layout");
+      LooseOp op{};
+      op.src = sendbuf + send_displs[i] + st.sb.start;
+      op.count = wd.count;
+      op.dst = base;
+      op.unpack = true;
+      op.psrc = reinterpret_cast<const int64_t *>(d == R.rank ? reinterpret_cast<uint8_t *>(wd.raw_s)
+                                                               : open_ipc(wd.hs) + wd.os);
+      op.pdst = reinterpret_cast<const int64_t *>(d == R.rank ? reinterpret_cast<uint8_t *>(wd.raw_d)
+                                                               : open_ipc(wd.hd) + wd.od);
+      op.npieces = wd.npieces;
+      op.size = wd.size;
+      op.extent = wd.extent;
+      op.align = wd.align;
+      loose.push_back(op);
+      continue;
+    }
     if (st.form != SP_FORM_STRIDED) {
       // an irregular send type: the run-table kernel packs it in place when
       // the receive layout is one dense run; typed copies between two

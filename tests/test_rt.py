@@ -481,6 +481,71 @@ def _nbr_irregular(rank, world, job):
     return True
 
 
+def _nbr_irregular_recv(rank, world, job):
+    """Scattered ghosts: each rank sends a contiguous run of doubles to each
+    neighbour and receives it through an irregular MPI_Type_indexed
+    (different per neighbour) -- the sender scatters through the receiver's
+    run table published over CUDA IPC. Repeated calls with changing data,
+    ring of 3."""
+    import numpy as np
+    import torch
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.rt as rt
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=1 << 20, host_bytes=1 << 20)
+    right, left = (rank + 1) % world, (rank - 1) % world
+    D = sp.make_named(sp.NamedKind.Double)
+
+    def scatter_list(seed, lo):
+        g = np.random.default_rng(seed)
+        bl = g.integers(1, 4, 200).tolist()
+        slots = g.permutation(512)[:200]
+        return bl, [lo + int(x) * 4 for x in slots]
+
+    # my ghost layout for data from the left lives in [0, 2048) doubles, from the right in [2048, 4096)
+    bl_l, dp_l = scatter_list(100 * rank + left, 0)
+    bl_r, dp_r = scatter_list(100 * rank + right, 2048)
+    g_l = sp.commit_type(sp.make_indexed(bl_l, dp_l, D))
+    g_r = sp.commit_type(sp.make_indexed(bl_r, dp_r, D))
+    # what my neighbours expect from me: the sizes of THEIR lists for me
+    n_to_r = sum(scatter_list(100 * right + rank, 0)[0])
+    n_to_l = sum(scatter_list(100 * left + rank, 2048)[0])
+    s_r = sp.commit_type(sp.make_contiguous(n_to_r, D))
+    s_l = sp.commit_type(sp.make_contiguous(n_to_l, D))
+    src = torch.empty(n_to_r + n_to_l, dtype=torch.float64, device="cuda")
+    ghosts = torch.empty(4096, dtype=torch.float64, device="cuda")
+    call = rt.NeighborW([(right, 1, s_r, 0), (left, 1, s_l, 8 * n_to_r)],
+                        [(left, 1, g_l, 0), (right, 1, g_r, 0)])
+
+    def sent_by(r, to_right, it):
+        # rank r sends [0, n) to its right neighbour and [n, n + m) to its left
+        n = sum(scatter_list(100 * ((r + 1) % world) + r, 0)[0])
+        m = sum(scatter_list(100 * ((r - 1) % world) + r, 2048)[0])
+        v = np.arange(n + m, dtype=np.float64) * 7 + r * 1000 + it
+        return v[:n] if to_right else v[n:]
+
+    for it in range(3):
+        src.copy_(torch.from_numpy(np.arange(n_to_r + n_to_l, dtype=np.float64) * 7 + rank * 1000 + it))
+        ghosts.fill_(-1)
+        torch.cuda.synchronize()
+        call(src, ghosts)
+        torch.cuda.synchronize()
+        want = np.full(4096, -1.0)
+        for bl, dp, vals in ((bl_l, dp_l, sent_by(left, True, it)), (bl_r, dp_r, sent_by(right, False, it))):
+            k = 0
+            for b, d in zip(bl, dp):
+                want[d:d + b] = vals[k:k + b]
+                k += b
+        assert np.array_equal(ghosts.cpu().numpy(), want), (rank, it)
+    rt.finalize()
+    return True
+
+
+@pytest.mark.gpu
+def test_neighbor_alltoallw_irregular_receive_types(cuda):
+    assert all(_spawn(_nbr_irregular_recv, 3).values())
+
+
 def _nbr_many_irregular(rank, world, job):
     """40 irregular edges to self in one MPI_Neighbor_alltoallw: more than
     one run-table launch's worth of edges (32 per launch)"""
