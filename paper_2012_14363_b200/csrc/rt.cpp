@@ -1200,11 +1200,28 @@ struct LooseOp {
   uint64_t align = 0;
 };
 
+// Local copies of peers' run tables (a scattered-ghost edge reads its
+// table once per piece; a copy in this GPU's HBM keeps those reads off
+// NVLink). Owned by the call record that uses them; freed when it is
+// replaced (every call ends with a stream synchronisation, so no launch
+// still reads them).
+struct TableCopy {
+  void *p = nullptr;
+  TableCopy() = default;
+  explicit TableCopy(size_t bytes) { cuda_check(cudaMalloc(&p, bytes), "cudaMalloc(run table copy)"); }
+  TableCopy(const TableCopy &) = delete;
+  TableCopy &operator=(const TableCopy &) = delete;
+  ~TableCopy() {
+    if (p) cudaFree(p);
+  }
+};
+
 struct NbrLast {
   std::string sig;
   std::vector<std::pair<int, uint64_t>> peer_ver;
   Batch *batch = nullptr;
   std::vector<LooseOp> loose;
+  std::vector<std::shared_ptr<TableCopy>> tables;
   bool valid = false;
 };
 
@@ -1226,10 +1243,11 @@ bool nbr_last_hit(const NbrLast &last, const std::string &sig) {
 }
 
 void nbr_last_set(NbrLast &last, std::string sig, const std::vector<int> &dests, Batch *b,
-                  std::vector<LooseOp> loose) {
+                  std::vector<LooseOp> loose, std::vector<std::shared_ptr<TableCopy>> tables = {}) {
   Runtime &R = rt();
   last.sig = std::move(sig);
   last.loose = std::move(loose);
+  last.tables = std::move(tables);
   last.peer_ver.clear();
   std::vector<char> seen(R.size, 0);
   for (int d : dests)
@@ -1556,6 +1574,7 @@ void rt_neighbor_alltoallw_build(const uint8_t *sendbuf, const std::vector<int64
   std::string key(reinterpret_cast<const char *>(&sendbuf), sizeof(sendbuf));
   std::vector<CopySpec> jobs;
   std::vector<LooseOp> loose;
+  std::vector<std::shared_ptr<TableCopy>> tables;
   std::vector<std::unique_ptr<Committed>> dst_types;
   std::vector<int> seen(R.size, 0);
   for (size_t i = 0; i < dests.size(); ++i) {
@@ -1590,10 +1609,19 @@ void rt_neighbor_alltoallw_build(const uint8_t *sendbuf, const std::vector<int64
       op.count = wd.count;
       op.dst = base;
       op.unpack = true;
-      op.psrc = reinterpret_cast<const int64_t *>(d == R.rank ? reinterpret_cast<uint8_t *>(wd.raw_s)
-                                                               : open_ipc(wd.hs) + wd.os);
-      op.pdst = reinterpret_cast<const int64_t *>(d == R.rank ? reinterpret_cast<uint8_t *>(wd.raw_d)
-                                                               : open_ipc(wd.hd) + wd.od);
+      if (d == R.rank) {
+        op.psrc = reinterpret_cast<const int64_t *>(wd.raw_s);
+        op.pdst = reinterpret_cast<const int64_t *>(wd.raw_d);
+      } else { // the peer's table, copied into this GPU's HBM once per call layout
+        const size_t ns = static_cast<size_t>(wd.npieces) * sizeof(int64_t), nd = ns + sizeof(int64_t);
+        auto cs = std::make_shared<TableCopy>(ns), cd = std::make_shared<TableCopy>(nd);
+        cuda_check(cudaMemcpy(cs->p, open_ipc(wd.hs) + wd.os, ns, cudaMemcpyDefault), "run table copy");
+        cuda_check(cudaMemcpy(cd->p, open_ipc(wd.hd) + wd.od, nd, cudaMemcpyDefault), "run table copy");
+        op.psrc = static_cast<const int64_t *>(cs->p);
+        op.pdst = static_cast<const int64_t *>(cd->p);
+        tables.push_back(std::move(cs));
+        tables.push_back(std::move(cd));
+      }
       op.npieces = wd.npieces;
       op.size = wd.size;
       op.extent = wd.extent;
@@ -1634,7 +1662,7 @@ void rt_neighbor_alltoallw_build(const uint8_t *sendbuf, const std::vector<int64
     }
   }
   nbr_run(b, loose, bs); // returns when every block addressed to this rank has landed
-  nbr_last_set(g_last_w, std::move(sig), dests, b, std::move(loose));
+  nbr_last_set(g_last_w, std::move(sig), dests, b, std::move(loose), std::move(tables));
 }
 
 } // namespace spb
