@@ -1538,7 +1538,11 @@ void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &s
     for (size_t j = 0; j < sources.size(); ++j) {
       const Committed &rt_ = *recv_types[j];
       bytes[j] = recv_counts[j] * rt_.size;
-      const bool runs = rt_.form == SP_FORM_UNSUPPORTED && !rt_.overlapping;
+      // irregular (block-list) receive layouts through published run tables
+      // are implemented below but disabled: an intermittent cross-process
+      // failure (ghosts left unwritten) is not yet understood
+      constexpr bool kIrregularRecv = false;
+      const bool runs = kIrregularRecv && rt_.form == SP_FORM_UNSUPPORTED && !rt_.overlapping;
       if (bytes[j] > 0 && !describable(rt_) && !runs)
         fail(SP_ERR_UNSUPPORTED, "neighbour alltoallw: receive types need a non-overlapping layout");
       if (bytes[j] > 0) {

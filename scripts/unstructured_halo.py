@@ -64,6 +64,13 @@ for nblocks in (500, 5000):
     flat = torch.randn(sum(sizes), dtype=torch.float64, device="cuda")
     ghost_field = torch.zeros(N, dtype=torch.float64, device="cuda")
     call2 = rt.NeighborW([(0, 1, g, int(o)) for g, o in zip(ghosts, offs)], [(0, 1, t, 0) for t in types])
+    try:
+        call2(flat, ghost_field)
+    except sp.Unsupported:  # irregular receive layouts are disabled in the engine
+        out[nblocks] = {"bytes": int(sum(sizes) * 8), "alltoallw_us": round(statistics.median(ws) * 1e6, 1),
+                        "per_edge_packs_us": round(statistics.median(ps) * 1e6, 1)}
+        print(json.dumps({nblocks: out[nblocks]}), flush=True)
+        continue
     for _ in range(5):
         call2(flat, ghost_field)
     ws2 = []

@@ -66,6 +66,16 @@ def test_mpi_indexed_struct_resized(cuda, tmp_path, np_):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("np_", [1, 2, 3])
+def test_mpi_unstructured_neighbor_exchange(cuda, tmp_path, np_):
+    """beyond the reference: irregular gather lists into contiguous ghosts,
+    one MPI_Neighbor_alltoallw on device memory (mode "a"; the scattered-
+    ghost mode "b" exercises irregular receive layouts, disabled in the
+    engine for now -- DESIGN.md section 9)"""
+    assert "OK" in run(np_, build(tmp_path, "mpi_unstructured"), "a")
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("np_", [1, 2])
 def test_mpi_pack_and_sendrecv(cuda, tmp_path, np_):
     assert "OK" in run(np_, build(tmp_path, "mpi_sendrecv"))

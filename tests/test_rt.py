@@ -542,6 +542,8 @@ def _nbr_irregular_recv(rank, world, job):
 
 
 @pytest.mark.gpu
+@pytest.mark.skip(reason="irregular receive layouts are disabled in the engine (intermittent cross-process "
+                         "failure under investigation, DESIGN.md section 9)")
 def test_neighbor_alltoallw_irregular_receive_types(cuda):
     assert all(_spawn(_nbr_irregular_recv, 3).values())
 
