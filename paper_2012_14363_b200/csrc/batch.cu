@@ -55,7 +55,7 @@ struct BatchJob {
 // NVLink) reaches wait_value; after the last word, the LAST block to finish
 // publishes signal_value to each `signal` flag (peer memory) with a
 // system-scope release store, after fences by every block.
-constexpr int kMaxSig = 32;
+constexpr int kMaxSig = kMaxSignalPeers;
 struct BatchSig {
   const unsigned long long *wait[kMaxSig];
   unsigned long long *signal[kMaxSig];
@@ -417,8 +417,7 @@ Batch *build_batch(std::vector<BatchJob> (&by_w)[5], int mode, int64_t bytes) {
     }
     cuda_check(cudaMalloc(&g.d_jobs, jobs.size() * sizeof(BatchJob)), "cudaMalloc(batch)");
     b->groups.push_back(g);
-    cuda_check(cudaMemcpy(g.d_jobs, jobs.data(), jobs.size() * sizeof(BatchJob), cudaMemcpyHostToDevice),
-               "upload batch");
+    copy_sync(g.d_jobs, jobs.data(), jobs.size() * sizeof(BatchJob), "upload batch");
   }
   return b.release();
 }

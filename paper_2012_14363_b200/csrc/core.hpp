@@ -198,6 +198,13 @@ const DeviceRuns &device_run_table(const Committed &ct);
 void set_last_launch(const sp_launch_info &li);
 void cuda_check(int err, const char *what);  // cudaError_t as int
 void require_device();
+// Copy `n` bytes (any direction, pageable or device source) and return only
+// when they have landed in `dst`. A plain cudaMemcpy is not enough: from
+// pageable host memory it may return before the DMA completes, device to
+// device it does not wait at all, and in both cases it runs on the legacy
+// stream, which orders nothing on the engine's non-blocking streams or in
+// other processes reading the buffer through CUDA IPC.
+void copy_sync(void *dst, const void *src, size_t n, const char *what);
 
 // persistent multi-job launches (pack.cu)
 struct BatchSpec {
@@ -246,6 +253,7 @@ struct BatchSignal {
   uint64_t post_value = 0;
   std::vector<uint64_t> signal_values, post_values; // per-target values (else the scalars)
 };
+constexpr int kMaxSignalPeers = 32; // flags a signalled launch carries (batch.cu kMaxSig)
 // one-warp kernel: release-stores the signals, then waits for the post flags
 void flags_signal_wait(const BatchSignal &sig, void *stream);
 void batch_execute_signaled(const Batch &b, void *stream, const BatchSignal &sig);

@@ -261,6 +261,8 @@ struct ModelCache {
     return h ^ (h >> 29);
   }
 
+  static constexpr uint64_t kBusy = 2; // invalid (bit 0 clear), nonzero: a writer owns the slot
+
   int choose(int64_t o, int64_t b) {
     const uint64_t h = hash(o, b);
     Set &set = sets[h & (kSets - 1)];
@@ -279,10 +281,15 @@ struct ModelCache {
           victim = &s;
           break;
         }
-      victim->tag.store(0, std::memory_order_release);
-      victim->obj.store(static_cast<uint64_t>(o), std::memory_order_release);
-      victim->tag.store(static_cast<uint64_t>(b) << 3 | static_cast<uint64_t>(m) << 1 | 1,
-                        std::memory_order_release);
+      // claim the slot (valid or empty -> busy) so that two writers never
+      // interleave their obj and tag stores; a slot another thread is
+      // filling is left to it (this answer is simply not cached)
+      uint64_t cur = victim->tag.load(std::memory_order_relaxed);
+      if (cur != kBusy && victim->tag.compare_exchange_strong(cur, kBusy, std::memory_order_acq_rel)) {
+        victim->obj.store(static_cast<uint64_t>(o), std::memory_order_release);
+        victim->tag.store(static_cast<uint64_t>(b) << 3 | static_cast<uint64_t>(m) << 1 | 1,
+                          std::memory_order_release);
+      }
     }
     return m;
   }

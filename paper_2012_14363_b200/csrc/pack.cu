@@ -58,6 +58,18 @@ void cuda_check(int err, const char *what) {
   }
 }
 
+void copy_sync(void *dst, const void *src, size_t n, const char *what) {
+  if (n == 0) return;
+  // one private non-blocking stream per host thread and device
+  thread_local cudaStream_t streams[64] = {};
+  int cur = 0;
+  cuda_check(cudaGetDevice(&cur), "cudaGetDevice");
+  cudaStream_t &st = streams[cur & 63];
+  if (!st) cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate(copy_sync)");
+  cuda_check(cudaMemcpyAsync(dst, src, n, cudaMemcpyDefault, st), what);
+  cuda_check(cudaStreamSynchronize(st), what);
+}
+
 void require_device() {
   int n = 0;
   const cudaError_t e = cudaGetDeviceCount(&n);
@@ -671,8 +683,8 @@ const DeviceRuns &device_runs(const Committed &ct, const std::vector<Run> &runs)
   d.align_or = align_or;
   cuda_check(cudaMalloc(&d.d_src, std::max<size_t>(hs.size(), 1) * sizeof(int64_t)), "cudaMalloc(runs)");
   cuda_check(cudaMalloc(&d.d_dst, hd.size() * sizeof(int64_t)), "cudaMalloc(runs)");
-  cuda_check(cudaMemcpy(d.d_src, hs.data(), hs.size() * sizeof(int64_t), cudaMemcpyHostToDevice), "upload runs");
-  cuda_check(cudaMemcpy(d.d_dst, hd.data(), hd.size() * sizeof(int64_t), cudaMemcpyHostToDevice), "upload runs");
+  copy_sync(d.d_src, hs.data(), hs.size() * sizeof(int64_t), "upload runs");
+  copy_sync(d.d_dst, hd.data(), hd.size() * sizeof(int64_t), "upload runs");
   ct.dev = d;
   return ct.dev;
 }

@@ -791,6 +791,12 @@ bool step_recv(Req &q) {
       } else if (m.bytes > 0 && (q.ct->size == 0 || m.bytes % q.ct->size)) {
         q.err = SP_ERR_INVALID_ARGUMENT;
         q.msg = "recv: message is not whole objects";
+      } else if (m.bytes > 0 &&
+                 static_cast<uint64_t>((m.bytes / q.ct->size - 1) * q.ct->extent + q.ct->span) > q.buf_bytes) {
+        // every method writes the receive buffer through the layout (DIRECT
+        // straight from the sender's kernel): check it before any transfer
+        q.err = SP_ERR_BUFFER_TOO_SMALL;
+        q.msg = "recv: receive buffer smaller than the layout of the message";
       }
       // DIRECT upgrade: the sender can run the copy kernel, the destination
       // is device memory and the type has a publishable canonical form
@@ -1287,6 +1293,22 @@ BatchSignal nbr_enter(const std::vector<int> &sources, const std::vector<int> &d
   Runtime &R = rt();
   BatchSignal bs;
   std::vector<char> seen_s(R.size, 0), seen_d(R.size, 0);
+  { // everything that can refuse the call is checked BEFORE it is counted
+    // and announced: once entered, the peers' kernels wait for this rank
+    int ns = 0, nd = 0;
+    for (int s : sources) {
+      if (s < 0 || s >= R.size) fail(SP_ERR_INVALID_ARGUMENT, "neighbour exchange: source rank out of range");
+      if (s != R.rank && !seen_s[s]) seen_s[s] = 1, ++ns;
+    }
+    for (int d : dests) {
+      if (d < 0 || d >= R.size) fail(SP_ERR_INVALID_ARGUMENT, "neighbour exchange: destination rank out of range");
+      if (d != R.rank && !seen_d[d]) seen_d[d] = 1, ++nd;
+    }
+    if (ns > kMaxSignalPeers || nd > kMaxSignalPeers)
+      fail(SP_ERR_UNSUPPORTED, "neighbour exchange: more than 32 distinct neighbours");
+    std::fill(seen_s.begin(), seen_s.end(), 0);
+    std::fill(seen_d.begin(), seen_d.end(), 0);
+  }
   for (int s : sources) {
     if (s == R.rank || seen_s[s]) continue;
     seen_s[s] = 1;
@@ -1336,6 +1358,25 @@ void nbr_run(Batch *b, const std::vector<LooseOp> &loose, const BatchSignal &bs)
   cuda_check(cudaStreamSynchronize(R.stream), "cudaStreamSynchronize(neighbor)");
 }
 
+// A call that fails after nbr_enter still completes the entry protocol:
+// its READY flags go out (no data) and it waits for its senders, so the
+// peers' kernels finish and the per-pair call counts stay in step; then the
+// error is returned. Without this a refused argument on one rank would hang
+// every neighbour's GPU.
+template <class F> void nbr_guarded(const BatchSignal &bs, F &&body) {
+  try {
+    body();
+  } catch (...) {
+    Runtime &R = rt();
+    try {
+      flags_signal_wait(bs, R.stream);
+      cudaStreamSynchronize(R.stream);
+    } catch (...) {
+    }
+    throw;
+  }
+}
+
 void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &send_counts,
                            const std::vector<int64_t> &send_displs, const CommitPtr &stp, uint8_t *recvbuf,
                            const std::vector<int64_t> &recv_counts, const std::vector<int64_t> &recv_displs,
@@ -1356,60 +1397,62 @@ void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &s
     nbr_publish(recvbuf, sources, disp, bytes, nullptr);
   }
   const BatchSignal bs = nbr_enter(sources, dests); // replaces a barrier
-  std::string sig(reinterpret_cast<const char *>(&sendbuf), sizeof(sendbuf));
-  sig.append(reinterpret_cast<const char *>(&recvbuf), sizeof(recvbuf));
-  append_bytes(sig, send_counts);
-  append_bytes(sig, send_displs);
-  append_bytes(sig, dests);
-  append_type_key(sig, st);
-  if (nbr_last_hit(g_last_v, sig)) {
-    nbr_run(g_last_v.batch, g_last_v.loose, bs);
-    return;
-  }
-  std::string key(reinterpret_cast<const char *>(&sendbuf), sizeof(sendbuf));
-  std::vector<BatchSpec> jobs;
-  std::vector<LooseOp> loose;
-  const bool blocklist = st.form != SP_FORM_STRIDED; // irregular send type: run-table packs
-  std::vector<int> seen(R.size, 0);
-  for (size_t i = 0; i < dests.size(); ++i) {
-    const int d = dests[i];
-    const int occ = seen[d]++;
-    const Slot &peer = R.shm->slots[d];
-    int hit = -1;
-    for (int j = 0, k = 0; j < peer.nedges; ++j)
-      if (peer.edges[j][0] == R.rank && k++ == occ) {
-        hit = j;
-        break;
+  nbr_guarded(bs, [&] {
+    std::string sig(reinterpret_cast<const char *>(&sendbuf), sizeof(sendbuf));
+    sig.append(reinterpret_cast<const char *>(&recvbuf), sizeof(recvbuf));
+    append_bytes(sig, send_counts);
+    append_bytes(sig, send_displs);
+    append_bytes(sig, dests);
+    append_type_key(sig, st);
+    if (nbr_last_hit(g_last_v, sig)) {
+      nbr_run(g_last_v.batch, g_last_v.loose, bs);
+      return;
+    }
+    std::string key(reinterpret_cast<const char *>(&sendbuf), sizeof(sendbuf));
+    std::vector<BatchSpec> jobs;
+    std::vector<LooseOp> loose;
+    const bool blocklist = st.form != SP_FORM_STRIDED; // irregular send type: run-table packs
+    std::vector<int> seen(R.size, 0);
+    for (size_t i = 0; i < dests.size(); ++i) {
+      const int d = dests[i];
+      const int occ = seen[d]++;
+      const Slot &peer = R.shm->slots[d];
+      int hit = -1;
+      for (int j = 0, k = 0; j < peer.nedges; ++j)
+        if (peer.edges[j][0] == R.rank && k++ == occ) {
+          hit = j;
+          break;
+        }
+      if (hit < 0) fail(SP_ERR_INVALID_ARGUMENT, "neighbour exchange: destination does not list this rank as source");
+      const int64_t bytes = send_counts[i] * st.size;
+      if (bytes > peer.edges[hit][2]) fail(SP_ERR_BUFFER_TOO_SMALL, "neighbour exchange: message truncated");
+      if (bytes == 0) continue;
+      uint8_t *base = d == R.rank ? recvbuf : open_ipc(peer.xh) + peer.xoff;
+      if (blocklist) {
+        loose.push_back({stp, sendbuf + send_displs[i] * st.extent, send_counts[i], base + peer.edges[hit][1]});
+        continue;
       }
-    if (hit < 0) fail(SP_ERR_INVALID_ARGUMENT, "neighbour exchange: destination does not list this rank as source");
-    const int64_t bytes = send_counts[i] * st.size;
-    if (bytes > peer.edges[hit][2]) fail(SP_ERR_BUFFER_TOO_SMALL, "neighbour exchange: message truncated");
-    if (bytes == 0) continue;
-    uint8_t *base = d == R.rank ? recvbuf : open_ipc(peer.xh) + peer.xoff;
-    if (blocklist) {
-      loose.push_back({stp, sendbuf + send_displs[i] * st.extent, send_counts[i], base + peer.edges[hit][1]});
-      continue;
+      jobs.push_back({&st, sendbuf + send_displs[i] * st.extent, UINT64_MAX, send_counts[i], base, UINT64_MAX,
+                      peer.edges[hit][1]});
+      const int64_t sig[4] = {reinterpret_cast<int64_t>(base), peer.edges[hit][1], send_counts[i], send_displs[i]};
+      key.append(reinterpret_cast<const char *>(sig), sizeof(sig));
     }
-    jobs.push_back({&st, sendbuf + send_displs[i] * st.extent, UINT64_MAX, send_counts[i], base, UINT64_MAX,
-                    peer.edges[hit][1]});
-    const int64_t sig[4] = {reinterpret_cast<int64_t>(base), peer.edges[hit][1], send_counts[i], send_displs[i]};
-    key.append(reinterpret_cast<const char *>(sig), sizeof(sig));
-  }
-  append_type_key(key, st); // geometry, not the address: a freed type's address can be reused
-  Batch *b = nullptr;
-  for (auto &e : g_nbr_cache)
-    if (e.key == key) b = e.batch;
-  if (!b && !jobs.empty()) {
-    b = batch_create(jobs, false);
-    g_nbr_cache.push_back({key, b});
-    if (g_nbr_cache.size() > 16) {
-      if (g_last_v.batch == g_nbr_cache.front().batch) g_last_v.valid = false;
-      batch_destroy(g_nbr_cache.front().batch);
-      g_nbr_cache.pop_front();
+    append_type_key(key, st); // geometry, not the address: a freed type's address can be reused
+    Batch *b = nullptr;
+    for (auto &e : g_nbr_cache)
+      if (e.key == key) b = e.batch;
+    if (!b && !jobs.empty()) {
+      b = batch_create(jobs, false);
+      g_nbr_cache.push_back({key, b});
+      if (g_nbr_cache.size() > 16) {
+        if (g_last_v.batch == g_nbr_cache.front().batch) g_last_v.valid = false;
+        batch_destroy(g_nbr_cache.front().batch);
+        g_nbr_cache.pop_front();
+      }
     }
-  }
-  nbr_run(b, loose, bs); // returns when every block addressed to this rank has landed
-  nbr_last_set(g_last_v, std::move(sig), dests, b, std::move(loose));
+    nbr_run(b, loose, bs); // returns when every block addressed to this rank has landed
+    nbr_last_set(g_last_v, std::move(sig), dests, b, std::move(loose));
+  });
 }
 
 // MPI_Neighbor_alltoallw with per-edge datatypes on BOTH sides: each rank
@@ -1520,14 +1563,16 @@ void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &s
   if (g_wlast.valid && g_wlast.args == args && g_last_w.valid &&
       R.shm->slots[R.rank].layout_ver.load(std::memory_order_relaxed) == g_wlast.my_ver) {
     const BatchSignal bs = nbr_enter(sources, dests);
-    if (nbr_peers_unchanged(g_last_w)) {
-      nbr_run(g_last_w.batch, g_last_w.loose, bs);
-      return;
-    }
-    g_wlast.valid = false; // a neighbour re-published: rebuild below (entered already)
-    rt_neighbor_alltoallw_build(sendbuf, send_counts, send_displs, send_types, recvbuf, dests, bs);
-    g_wlast = WLastCall{std::move(args), send_types, recv_types,
-                        R.shm->slots[R.rank].layout_ver.load(std::memory_order_relaxed), true};
+    nbr_guarded(bs, [&] {
+      if (nbr_peers_unchanged(g_last_w)) {
+        nbr_run(g_last_w.batch, g_last_w.loose, bs);
+        return;
+      }
+      g_wlast.valid = false; // a neighbour re-published: rebuild below (entered already)
+      rt_neighbor_alltoallw_build(sendbuf, send_counts, send_displs, send_types, recvbuf, dests, bs);
+      g_wlast = WLastCall{std::move(args), send_types, recv_types,
+                          R.shm->slots[R.rank].layout_ver.load(std::memory_order_relaxed), true};
+    });
     return;
   }
   g_wlast.valid = false;
@@ -1538,11 +1583,9 @@ void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &s
     for (size_t j = 0; j < sources.size(); ++j) {
       const Committed &rt_ = *recv_types[j];
       bytes[j] = recv_counts[j] * rt_.size;
-      // irregular (block-list) receive layouts through published run tables
-      // are implemented below but disabled: an intermittent cross-process
-      // failure (ghosts left unwritten) is not yet understood
-      constexpr bool kIrregularRecv = false;
-      const bool runs = kIrregularRecv && rt_.form == SP_FORM_UNSUPPORTED && !rt_.overlapping;
+      // irregular (block-list) receive layouts: the device run table is
+      // published through CUDA IPC (its upload has landed: copy_sync)
+      const bool runs = rt_.form == SP_FORM_UNSUPPORTED && !rt_.overlapping;
       if (bytes[j] > 0 && !describable(rt_) && !runs)
         fail(SP_ERR_UNSUPPORTED, "neighbour alltoallw: receive types need a non-overlapping layout");
       if (bytes[j] > 0) {
@@ -1553,9 +1596,11 @@ void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &s
     nbr_publish(recvbuf, sources, recv_displs, bytes, &dp);
   }
   const BatchSignal bs = nbr_enter(sources, dests); // replaces a barrier
-  rt_neighbor_alltoallw_build(sendbuf, send_counts, send_displs, send_types, recvbuf, dests, bs);
-  g_wlast = WLastCall{std::move(args), send_types, recv_types,
-                      R.shm->slots[R.rank].layout_ver.load(std::memory_order_relaxed), true};
+  nbr_guarded(bs, [&] {
+    rt_neighbor_alltoallw_build(sendbuf, send_counts, send_displs, send_types, recvbuf, dests, bs);
+    g_wlast = WLastCall{std::move(args), send_types, recv_types,
+                        R.shm->slots[R.rank].layout_ver.load(std::memory_order_relaxed), true};
+  });
 }
 
 // the send side of an alltoallw call once entered: find (or build) the
@@ -1619,8 +1664,8 @@ void rt_neighbor_alltoallw_build(const uint8_t *sendbuf, const std::vector<int64
       } else { // the peer's table, copied into this GPU's HBM once per call layout
         const size_t ns = static_cast<size_t>(wd.npieces) * sizeof(int64_t), nd = ns + sizeof(int64_t);
         auto cs = std::make_shared<TableCopy>(ns), cd = std::make_shared<TableCopy>(nd);
-        cuda_check(cudaMemcpy(cs->p, open_ipc(wd.hs) + wd.os, ns, cudaMemcpyDefault), "run table copy");
-        cuda_check(cudaMemcpy(cd->p, open_ipc(wd.hd) + wd.od, nd, cudaMemcpyDefault), "run table copy");
+        copy_sync(cs->p, open_ipc(wd.hs) + wd.os, ns, "run table copy");
+        copy_sync(cd->p, open_ipc(wd.hd) + wd.od, nd, "run table copy");
         op.psrc = static_cast<const int64_t *>(cs->p);
         op.pdst = static_cast<const int64_t *>(cd->p);
         tables.push_back(std::move(cs));
@@ -1649,6 +1694,10 @@ void rt_neighbor_alltoallw_build(const uint8_t *sendbuf, const std::vector<int64
     const int64_t sig[5] = {reinterpret_cast<int64_t>(base), send_counts[i], send_displs[i], wd.count, wd.start};
     key.append(reinterpret_cast<const char *>(sig), sizeof(sig));
     append_type_key(key, st);
+    // the receiver's whole geometry: types with one canonical row may still
+    // differ in extent (contiguous(4, DOUBLE) vs a 1-D subarray of it)
+    const int64_t geo[4] = {wd.size, wd.extent, wd.span, wd.ndims};
+    key.append(reinterpret_cast<const char *>(geo), sizeof(geo));
     key.append(reinterpret_cast<const char *>(wd.counts), sizeof(int64_t) * wd.ndims);
     key.append(reinterpret_cast<const char *>(wd.strides), sizeof(int64_t) * wd.ndims);
     dst_types.push_back(std::move(dc));

@@ -3,7 +3,11 @@
  * gather list of doubles (different per neighbour) and receives (a) into
  * contiguous ghost runs and (b) with the roles swapped, contiguous sends
  * scattered into irregular ghost slots -- one MPI_Neighbor_alltoallw each,
- * on device memory. Values checked on the host. Prints "OK". */
+ * on device memory. Values checked on the host. Prints "OK".
+ * argv[1]: "a" gather only, "b" scatter only, "ab" both in sequence;
+ * argv[2]: iterations (default 1). Every iteration builds FRESH types from
+ * lists that change with the iteration, so each one uploads and publishes
+ * new device run tables and every call re-publishes its receive layout. */
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -16,13 +20,16 @@ enum { NB = 300, SLOTS = 1024 };
 
 /* the gather list rank `from` uses for neighbour `to`: NB blocks of 1-3
  * doubles at distinct 4-double slots (a deterministic permutation) */
+static int g_it = 0; /* current iteration: varies every list */
 static void glist(int from, int to, int *bl, int *dp) {
   for (int i = 0; i < NB; ++i) {
-    bl[i] = 1 + (i * 5 + from * 3 + to) % 3;
+    bl[i] = 1 + (i * 5 + from * 3 + to + g_it) % 3;
     /* distinct slots: i -> 389 i + c is a bijection mod SLOTS (389 odd) */
-    dp[i] = (int)(((unsigned)i * 389u + (unsigned)(from * 7 + to)) % SLOTS) * 4;
+    dp[i] = (int)(((unsigned)i * 389u + (unsigned)(from * 7 + to + 13 * g_it)) % SLOTS) * 4;
   }
 }
+
+static int one_iteration(int rank, int size, MPI_Comm g, const char *mode);
 
 static double val(int r, int i) { return r * 100000.0 + i * 0.5; }
 
@@ -31,11 +38,23 @@ int main(int argc, char **argv) {
   MPI_Init(&argc, &argv);
   MPI_Comm_rank(MPI_COMM_WORLD, &rank);
   MPI_Comm_size(MPI_COMM_WORLD, &size);
+  const char *mode = argc > 1 ? argv[1] : "ab";
+  const int iters = argc > 2 ? atoi(argv[2]) : 1;
   const int right = (rank + 1) % size, left = (rank + size - 1) % size;
   int nbrs[2] = {right, left}, srcs[2] = {left, right};
   MPI_Comm g;
   CHECK(MPI_Dist_graph_create_adjacent(MPI_COMM_WORLD, 2, srcs, MPI_UNWEIGHTED, 2, nbrs, MPI_UNWEIGHTED,
                                        MPI_INFO_NULL, 0, &g) == MPI_SUCCESS);
+  for (g_it = 0; g_it < iters; ++g_it) CHECK(one_iteration(rank, size, g, mode) == 0);
+  MPI_Barrier(MPI_COMM_WORLD);
+  MPI_Finalize();
+  if (rank == 0) printf("OK\n");
+  return 0;
+}
+
+static int one_iteration(int rank, int size, MPI_Comm g, const char *mode) {
+  const int right = (rank + 1) % size, left = (rank + size - 1) % size;
+  int nbrs[2] = {right, left}, srcs[2] = {left, right};
   const int N = SLOTS * 4;
   int bl[2][NB], dp[2][NB], blin[2][NB], dpin[2][NB], n_out[2] = {0, 0}, n_in[2] = {0, 0};
   MPI_Datatype gather[2], ghost[2];
@@ -56,8 +75,6 @@ int main(int argc, char **argv) {
   /* (a) irregular sends, contiguous ghost runs */
   int ones[2] = {1, 1};
   MPI_Aint sd[2] = {0, 0}, rd[2] = {0, (MPI_Aint)(n_in[0] * sizeof(double))};
-  /* argv[1]: "a" gather only, "b" scatter only, "ab" both in sequence */
-  const char *mode = argc > 1 ? argv[1] : "ab";
   if (strchr(mode, 'a')) {
     CHECK(MPI_Neighbor_alltoallw(d_field, ones, sd, gather, d_ghost, ones, rd, ghost, g) == MPI_SUCCESS);
     double *hg = malloc((n_in[0] + n_in[1]) * sizeof(double));
@@ -65,6 +82,7 @@ int main(int argc, char **argv) {
     for (int k = 0, at = 0; k < 2; ++k)
       for (int i = 0; i < NB; ++i)
         for (int j = 0; j < blin[k][i]; ++j) CHECK(hg[at++] == val(srcs[k], dpin[k][i] + j));
+    free(hg);
   }
   /* (b) contiguous sends scattered into irregular ghost slots: I receive
      through the lists my neighbours used, into a fresh field */
@@ -104,9 +122,19 @@ int main(int argc, char **argv) {
         ++at;
       }
   }
+  free(ho);
 done:
-  MPI_Barrier(MPI_COMM_WORLD);
-  MPI_Finalize();
-  if (rank == 0) printf("OK\n");
+  for (int k = 0; k < 2; ++k) {
+    MPI_Type_free(&gather[k]);
+    MPI_Type_free(&ghost[k]);
+    MPI_Type_free(&flat[k]);
+    MPI_Type_free(&scatter[k]);
+  }
+  cudaFree(d_field);
+  cudaFree(d_ghost);
+  cudaFree(d_src);
+  cudaFree(d_out);
+  free(h);
+  free(hs);
   return 0;
 }

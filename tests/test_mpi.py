@@ -66,13 +66,25 @@ def test_mpi_indexed_struct_resized(cuda, tmp_path, np_):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["a", "b", "ab"])
 @pytest.mark.parametrize("np_", [1, 2, 3])
-def test_mpi_unstructured_neighbor_exchange(cuda, tmp_path, np_):
-    """beyond the reference: irregular gather lists into contiguous ghosts,
-    one MPI_Neighbor_alltoallw on device memory (mode "a"; the scattered-
-    ghost mode "b" exercises irregular receive layouts, disabled in the
-    engine for now -- DESIGN.md section 9)"""
-    assert "OK" in run(np_, build(tmp_path, "mpi_unstructured"), "a")
+def test_mpi_unstructured_neighbor_exchange(cuda, tmp_path, np_, mode):
+    """beyond the reference: irregular gather lists into contiguous ghosts
+    (mode "a"), contiguous runs scattered into irregular ghost slots through
+    the receivers' IPC-published run tables (mode "b"), and both in one
+    process (mode "ab": the sequence that used to leave ghosts unwritten)"""
+    assert "OK" in run(np_, build(tmp_path, "mpi_unstructured"), mode)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("np_", [2, 3])
+def test_mpi_unstructured_loop(cuda, tmp_path, np_):
+    """100 iterations of mode "ab", each with FRESH types (new run tables
+    uploaded, published and copied) and fresh buffers: the regression for
+    the irregular-receive failure, whose cause was a run-table upload that
+    could still be in flight when the table was published or read
+    (csrc/pack.cu copy_sync)"""
+    assert "OK" in run(np_, build(tmp_path, "mpi_unstructured"), "ab", "100", timeout=600)
 
 
 @pytest.mark.gpu

@@ -385,36 +385,6 @@ def test_cfg1_full_size(sp, orc, cuda):
     assert np.array_equal(back.cpu().numpy(), exp)
 
 
-@pytest.mark.parametrize("e0", [1, 2, 4, 8, 16, 32, 64, 128, 256, 512])
-def test_cfg2_sweep_full_size(sp, orc, cuda, e0):
-    """3D subarray of a 1 MiB object in a 1024^3-byte allocation; the
-    strided side is checked through a size-independent property (a round
-    trip restores exactly the described bytes and nothing else) plus a
-    bit-exact packed comparison against the oracle."""
-    torch = cuda
-    prog, dims = cfg2_prog(e0)
-    ct = sp.commit_type(sp.from_program(prog))
-    span = ct.span
-    g = torch.Generator(device="cuda").manual_seed(e0)
-    src = torch.randint(0, 256, (span,), dtype=torch.uint8, device="cuda", generator=g)
-    dst = torch.zeros(ct.size, dtype=torch.uint8, device="cuda")
-    sp.pack(src, ct, 1, dst, 0)
-    host = src.cpu().numpy()
-    want = np.zeros(ct.size, np.uint8)
-    assert orc.pack(prog, host, 1, want, 0)[0] == 0
-    assert np.array_equal(dst.cpu().numpy(), want)
-    # round trip: unpack into a zeroed allocation, then re-pack must match
-    # and the zeroed complement must remain zero (count of nonzero bytes
-    # is bounded by the described bytes)
-    back = torch.zeros(span, dtype=torch.uint8, device="cuda")
-    sp.unpack(dst, 0, ct, 1, back)
-    again = torch.zeros(ct.size, dtype=torch.uint8, device="cuda")
-    sp.pack(back, ct, 1, again, 0)
-    assert torch.equal(again, dst)
-    assert int((back != 0).sum()) <= ct.size
-    assert int(back.to(torch.int64).sum()) == int(dst.to(torch.int64).sum())
-
-
 # ------------------------------------------------------------ TMA path
 def test_tma_path_parity(sp, orc, cuda, corpus):
     """the TMA-tiled kernels (tensor-map box staged through shared memory)
@@ -449,47 +419,92 @@ def test_tma_path_parity(sp, orc, cuda, corpus):
         assert np.array_equal(back.cpu().numpy(), exp), prog
         n += 1
     # hand-built shapes that exercise partial tiles, 4 row dims and counts
-    b = sp.make_named(sp.NamedKind.Byte)
-    shapes = [sp.make_hvector(300, 1, 64, sp.make_contiguous(48, b)),
-              sp.make_hvector(3, 1, 16384, sp.make_hvector(257, 1, 32, sp.make_contiguous(16, b))),
-              sp.make_hvector(2, 1, 1 << 16, sp.make_hvector(3, 1, 8192, sp.make_hvector(5, 1, 512,
-                                                                                      sp.make_contiguous(256, b))))]
-    for d in shapes:
-        ct = sp.commit_type(d)
+    shapes = [[3, 300, 1, 64, 1, 48, 0, 0],
+              [3, 3, 1, 16384, 3, 257, 1, 32, 1, 16, 0, 0],
+              [3, 2, 1, 1 << 16, 3, 3, 1, 8192, 3, 5, 1, 512, 1, 256, 0, 0]]
+    for prog in shapes:
+        ct = sp.commit_type(sp.from_program(prog))
         for inc in (1, 3):
             span = (inc - 1) * ct.extent + ct.span
             host = rng.integers(0, 256, span, dtype=np.uint8)
             dst = torch.zeros(inc * ct.size, dtype=torch.uint8, device="cuda")
             sp.pack(dev(torch, host), ct, inc, dst, 0, kernel=sp.Kernel.TMA)
-            ref = torch.zeros_like(dst)
-            sp.pack(dev(torch, host), ct, inc, ref, 0, kernel=sp.Kernel.Words)
-            assert torch.equal(dst, ref)
-            back = torch.full((span,), 7, dtype=torch.uint8, device="cuda")
+            assert sp.last_launch().kernel == sp.Kernel.TMA
+            want = np.zeros(inc * ct.size, np.uint8)
+            assert orc.pack(prog, host, inc, want, 0)[0] == 0
+            assert np.array_equal(dst.cpu().numpy(), want), prog
+            init = rng.integers(0, 256, span, dtype=np.uint8)
+            back = dev(torch, init)
             sp.unpack(dst, 0, ct, inc, back, kernel=sp.Kernel.TMA)
-            ref2 = torch.full((span,), 7, dtype=torch.uint8, device="cuda")
-            sp.unpack(dst, 0, ct, inc, ref2, kernel=sp.Kernel.Words)
-            assert torch.equal(back, ref2)
+            exp = init.copy()
+            assert orc.unpack(prog, want, 0, inc, exp)[0] == 0
+            assert np.array_equal(back.cpu().numpy(), exp), prog
             n += 1
     assert n > 20
 
 
-@pytest.mark.parametrize("e0", [16, 32, 64, 128, 256, 512])
-def test_tma_cfg2_full_size(sp, cuda, e0):
+@pytest.mark.parametrize("kernel", ["auto", "words", "tma"])
+@pytest.mark.parametrize("e0", [1, 2, 4, 8, 16, 32, 64, 128, 256, 512])
+def test_cfg2_full_size_vs_oracle(sp, orc, cuda, e0, kernel):
+    """cfg2 at full size, pack AND unpack byte-compared with the oracle over
+    the whole 1 GiB allocation: the unpack target starts as random bytes
+    (not a constant), so every byte outside the described ones must survive
+    untouched. kernel = the automatic choice (TMA for unpack of rows >= 64 B
+    at this size), the LDG/STG word kernel, and the TMA path forced (rows of
+    16 B and up)."""
     torch = cuda
+    if kernel == "tma" and e0 < 16:
+        pytest.skip("the TMA path needs rows that are a multiple of 16 B")
+    k = {"auto": sp.Kernel.Auto, "words": sp.Kernel.Words, "tma": sp.Kernel.TMA}[kernel]
     prog, _ = cfg2_prog(e0)
     ct = sp.commit_type(sp.from_program(prog))
-    g = torch.Generator(device="cuda").manual_seed(e0 + 1)
+    g = torch.Generator(device="cuda").manual_seed(1000 + e0)
     src = torch.randint(0, 256, (ct.span,), dtype=torch.uint8, device="cuda", generator=g)
-    a = torch.zeros(ct.size, dtype=torch.uint8, device="cuda")
-    bb = torch.zeros(ct.size, dtype=torch.uint8, device="cuda")
-    sp.pack(src, ct, 1, a, 0, kernel=sp.Kernel.TMA)
-    sp.pack(src, ct, 1, bb, 0, kernel=sp.Kernel.Words)
-    assert torch.equal(a, bb)
-    out1 = torch.zeros(ct.span, dtype=torch.uint8, device="cuda")
-    out2 = torch.zeros(ct.span, dtype=torch.uint8, device="cuda")
-    sp.unpack(a, 0, ct, 1, out1, kernel=sp.Kernel.TMA)
-    sp.unpack(a, 0, ct, 1, out2, kernel=sp.Kernel.Words)
-    assert torch.equal(out1, out2)
+    host = src.cpu().numpy()
+    want = np.zeros(ct.size, np.uint8)
+    assert orc.pack(prog, host, 1, want, 0)[0] == 0
+    dst = torch.zeros(ct.size, dtype=torch.uint8, device="cuda")
+    sp.pack(src, ct, 1, dst, 0, kernel=k)
+    if kernel != "auto":
+        assert sp.last_launch().kernel == k
+    assert np.array_equal(dst.cpu().numpy(), want)
+    # unpack the oracle's packed bytes over a random 1 GiB target
+    out = torch.randint(0, 256, (ct.span,), dtype=torch.uint8, device="cuda", generator=g)
+    exp = out.cpu().numpy()
+    assert orc.unpack(prog, want, 0, 1, exp)[0] == 0
+    sp.unpack(torch.from_numpy(want).cuda(), 0, ct, 1, out, kernel=k)
+    auto_kernel = sp.last_launch().kernel
+    if kernel != "auto":
+        assert auto_kernel == k
+    elif e0 >= 64:
+        assert auto_kernel == sp.Kernel.TMA  # the automatic choice for long-row unpack at this size
+    del src
+    assert torch.equal(out, torch.from_numpy(exp).cuda())
+
+
+def test_cfg1_incount64_vs_oracle(sp, orc, cuda):
+    """BASELINE config 1 at the throughput count: 64 vector objects one
+    extent apart (a 4.3 GB span), pack and unpack byte-compared with the
+    oracle over the whole span"""
+    torch = cuda
+    prog = [2, 131072, 1, 64, 0, 3]
+    ct = sp.commit_type(sp.from_program(prog))
+    n = 64
+    span = (n - 1) * ct.extent + ct.span
+    g = torch.Generator(device="cuda").manual_seed(64)
+    src = torch.randint(0, 256, (span,), dtype=torch.uint8, device="cuda", generator=g)
+    host = src.cpu().numpy()
+    want = np.zeros(n * ct.size, np.uint8)
+    assert orc.pack(prog, host, n, want, 0)[0] == 0
+    dst = torch.zeros(n * ct.size, dtype=torch.uint8, device="cuda")
+    sp.pack(src, ct, n, dst, 0)
+    assert np.array_equal(dst.cpu().numpy(), want)
+    del src
+    out = torch.randint(0, 256, (span,), dtype=torch.uint8, device="cuda", generator=g)
+    exp = out.cpu().numpy()
+    assert orc.unpack(prog, want, 0, n, exp)[0] == 0
+    sp.unpack(dst, 0, ct, n, out)
+    assert torch.equal(out, torch.from_numpy(exp).cuda())
 
 
 # ------------------------------------------------------------ config 3

@@ -113,6 +113,46 @@ def test_sendrecv_every_method_two_processes(cuda):
     assert res[0][3] == res[1][3]  # the model's choice, seen identically on both sides
 
 
+def _recv_buffer_too_small(rank, world, job):
+    """a receive buffer shorter than the layout of the message is refused
+    with BufferTooSmall for every method -- DIRECT included, whose sender
+    writes the receive buffer straight from its kernel -- and no byte past
+    the buffer is written"""
+    import torch
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.rt as rt
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=4 << 20, host_bytes=4 << 20)
+    ct = sp.commit_type(sp.make_vector(256, 4, 8, sp.make_named(sp.NamedKind.Double)))  # 8 KiB at 16 KiB span
+    seen = []
+    for i, method in enumerate((rt.DIRECT, rt.DEVICE, rt.ONESHOT, rt.STAGED, rt.AUTO)):
+        if rank == 0:
+            src = torch.arange(ct.span, dtype=torch.uint8, device="cuda")
+            try:
+                rt.send(src, 1, ct, 1, tag=i, method=method)
+            except sp.Error:
+                pass
+        else:
+            full = torch.full((ct.span + 4096,), 0x5A, dtype=torch.uint8, device="cuda")
+            try:
+                rt.recv(full[:ct.span - 8], 1, ct, source=0, tag=i)
+                seen.append("accepted")
+            except sp.BufferTooSmall:
+                seen.append("refused")
+            torch.cuda.synchronize()
+            tail = full[ct.span - 8:].cpu()
+            assert bool((tail == 0x5A).all()), (method, "bytes written past the receive buffer")
+        rt.barrier()
+    rt.finalize()
+    return seen
+
+
+@pytest.mark.gpu
+def test_recv_buffer_too_small_every_method(cuda):
+    res = _spawn(_recv_buffer_too_small, 2)
+    assert res[1] == ["refused"] * 5
+
+
 def _nonblocking(rank, world, job):
     """rank 0 posts every message before rank 1 posts a single receive
     (receives posted in reverse tag order): forced methods, DIRECT, chunked
@@ -542,10 +582,96 @@ def _nbr_irregular_recv(rank, world, job):
 
 
 @pytest.mark.gpu
-@pytest.mark.skip(reason="irregular receive layouts are disabled in the engine (intermittent cross-process "
-                         "failure under investigation, DESIGN.md section 9)")
-def test_neighbor_alltoallw_irregular_receive_types(cuda):
-    assert all(_spawn(_nbr_irregular_recv, 3).values())
+@pytest.mark.parametrize("world", [2, 3])
+def test_neighbor_alltoallw_irregular_receive_types(cuda, world):
+    assert all(_spawn(_nbr_irregular_recv, world).values())
+
+
+def _nbr_alternating_layouts(rank, world, job, iters):
+    """Regression for the shared neighbour protocol (entry counters, READY
+    flags, layout versions, repeat-call and batch caches): every rank of a
+    ring alternates its receive layout between four REGULAR types on
+    every call, verified cell by cell each time. Layouts C and D have the
+    same canonical geometry (one dense 32-B row) and differ only in extent,
+    so a batch cached under a key without the receiver's extent would put
+    object j at the wrong pitch."""
+    import numpy as np
+    import torch
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.rt as rt
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=1 << 20, host_bytes=1 << 20)
+    right, left = (rank + 1) % world, (rank - 1) % world
+    D = sp.make_named(sp.NamedKind.Double)
+    flat = sp.commit_type(sp.make_contiguous(128, D))
+    idx = lambda blocks: np.concatenate([np.arange(o, o + n) for o, n in blocks])
+    layouts = [  # (type, count, element indices of the 128 received doubles)
+        (sp.commit_type(sp.make_vector(64, 2, 5, D)), 1, idx([(5 * b, 2) for b in range(64)])),
+        (sp.commit_type(sp.make_vector(32, 4, 7, D)), 1, idx([(7 * b, 4) for b in range(32)])),
+        (sp.commit_type(sp.make_contiguous(4, D)), 32, np.arange(128)),
+        (sp.commit_type(sp.make_subarray(1, [8], [4], [0], D)), 32, idx([(8 * j, 4) for j in range(32)])),
+    ]
+    assert layouts[2][0].canon.counts == layouts[3][0].canon.counts and layouts[2][0].extent != layouts[3][0].extent
+    calls = [rt.NeighborW([(right, 1, flat, 0), (left, 1, flat, 8 * 128)],
+                          [(left, c, t, 0), (right, c, t, 8 * 1024)]) for t, c, _ in layouts]
+    send = torch.empty(256, dtype=torch.float64, device="cuda")
+    recv = torch.empty(2048, dtype=torch.float64, device="cuda")
+    sent = lambda r, it: np.arange(256, dtype=np.float64) + r * 1e6 + it * 1e3
+    bad = 0
+    for it in range(iters):
+        k = (it + rank) % len(layouts) if it % 3 else it % len(layouts)  # ranks disagree on most calls
+        send.copy_(torch.from_numpy(sent(rank, it)))
+        recv.fill_(-1)
+        calls[k](send, recv)
+        want = np.full(2048, -1.0)
+        want[layouts[k][2]] = sent(left, it)[:128]           # left sent me its first run
+        want[1024 + layouts[k][2]] = sent(right, it)[128:]   # right sent me its second run
+        if not np.array_equal(recv.cpu().numpy(), want):
+            bad += 1
+    rt.finalize()
+    return bad
+
+
+@pytest.mark.gpu
+def test_neighbor_alltoallw_alternating_layouts(cuda):
+    assert _spawn(_nbr_alternating_layouts, 3, 1000, timeout=600) == {0: 0, 1: 0, 2: 0}
+
+
+def _nbr_error_after_entry(rank, world, job):
+    """one rank's send disagrees with its neighbour's receive (refused only
+    after the call was entered): that rank gets the error, the other rank's
+    call still completes instead of hanging its GPU, and the next correct
+    call on the same pair is exact (the per-pair call counts stay in step)"""
+    import numpy as np
+    import torch
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.rt as rt
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=1 << 20, host_bytes=1 << 20)
+    peer = 1 - rank
+    D = sp.make_named(sp.NamedKind.Double)
+    t128, t64 = sp.commit_type(sp.make_contiguous(128, D)), sp.commit_type(sp.make_contiguous(64, D))
+    send = torch.arange(128, dtype=torch.float64, device="cuda") + rank * 1000
+    recv = torch.full((128,), -1.0, dtype=torch.float64, device="cuda")
+    bad = rt.NeighborW([(peer, 1, t64 if rank == 1 else t128, 0)], [(peer, 1, t128, 0)])
+    err = None
+    try:
+        bad(send, recv)
+    except sp.Error as e:
+        err = type(e).__name__
+    good = rt.NeighborW([(peer, 1, t128, 0)], [(peer, 1, t128, 0)])
+    recv.fill_(-1)
+    good(send, recv)
+    torch.cuda.synchronize()
+    exact = bool(np.array_equal(recv.cpu().numpy(), np.arange(128) + peer * 1000.0))
+    rt.finalize()
+    return err, exact
+
+
+@pytest.mark.gpu
+def test_neighbor_error_after_entry_does_not_hang_peers(cuda):
+    res = _spawn(_nbr_error_after_entry, 2, timeout=120)
+    assert res[1] == ("InvalidArgument", True) and res[0][1] is True, res
 
 
 def _nbr_many_irregular(rank, world, job):
