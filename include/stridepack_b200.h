@@ -41,9 +41,12 @@ enum {
   SP_ERR_INTERNAL = 9,
   SP_ERR_INVALID_HANDLE = 11,
   SP_ERR_CUDA = 12,              /* a CUDA runtime call failed */
-  SP_ERR_NO_DEVICE = 13          /* no usable CUDA device: the GPU path is
+  SP_ERR_NO_DEVICE = 13,         /* no usable CUDA device: the GPU path is
                                     the only execution path, there is no
                                     host fallback */
+  SP_ERR_TIMEOUT = 14            /* runtime: a peer rank exited, or did not
+                                    answer within TEMPI_TIMEOUT seconds
+                                    (host waits and in-kernel flag waits) */
 };
 
 /* version of this C-ABI: bumped when a declaration changes incompatibly

@@ -92,9 +92,13 @@ class NoDevice(Error):
     pass
 
 
+class Timeout(Error):
+    """a peer rank exited, or did not answer within TEMPI_TIMEOUT seconds"""
+
+
 _ERRORS = {1: InvalidArgument, 2: UnsupportedOrder, 3: InvalidLayout, 4: BufferTooSmall,
            5: OverlappingLayout, 6: Unsupported, 7: EmptyProfile, 8: ParseError,
-           9: InternalError, 11: InvalidHandle, 12: CudaError, 13: NoDevice}
+           9: InternalError, 11: InvalidHandle, 12: CudaError, 13: NoDevice, 14: Timeout}
 
 
 def _check(status: int) -> None:

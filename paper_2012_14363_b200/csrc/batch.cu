@@ -77,6 +77,10 @@ struct BatchSig {
   // used instead of signal_value / post_value when per_target is set
   unsigned long long signal_vals[kMaxSig], post_vals[kMaxSig];
   int per_target;
+  // bounded waits: a spin that outlives timeout_ns sets *err and gives up
+  // (the host reports SP_ERR_TIMEOUT after its next synchronisation)
+  unsigned long long timeout_ns;
+  int *err;
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
@@ -87,6 +91,28 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 
 __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// spin until *p >= v (acquire, system scope); a peer that never publishes
+// -- it died, or never entered the call -- ends the spin after
+// sig.timeout_ns with *sig.err set instead of hanging this GPU
+__device__ __forceinline__ void wait_flag(const unsigned long long *p, unsigned long long v, const BatchSig &sig,
+                                          unsigned sleep_ns) {
+  if (ld_acquire_sys(p) >= v) return;
+  const unsigned long long t0 = global_ns();
+  while (ld_acquire_sys(p) < v) {
+    __nanosleep(sleep_ns);
+    if (sig.timeout_ns && global_ns() - t0 > sig.timeout_ns) {
+      if (sig.err) atomicExch(sig.err, 1);
+      return;
+    }
+  }
 }
 
 // byte offset of word q on a strided side
@@ -130,8 +156,7 @@ __device__ __forceinline__ void batch_prologue(const BatchSig &sig) {
   if (sig.n_pre && blockIdx.x == 0 && threadIdx.x < static_cast<unsigned>(sig.n_pre))
     st_release_sys(sig.pre[threadIdx.x], sig.pre_value);
   if (sig.n_wait) {
-    if (threadIdx.x < static_cast<unsigned>(sig.n_wait))
-      while (ld_acquire_sys(sig.wait[threadIdx.x]) < sig.wait_value) __nanosleep(64);
+    if (threadIdx.x < static_cast<unsigned>(sig.n_wait)) wait_flag(sig.wait[threadIdx.x], sig.wait_value, sig, 64);
     __syncthreads();
   }
 }
@@ -164,9 +189,7 @@ __device__ __forceinline__ void batch_epilogue(const BatchSig &sig) {
       // cannot starve them; the peers publish before they wait, so the
       // ranks' last blocks cannot wait on each other in a cycle
       if (threadIdx.x < static_cast<unsigned>(sig.n_post))
-        while (ld_acquire_sys(sig.post[threadIdx.x]) <
-               (sig.per_target ? sig.post_vals[threadIdx.x] : sig.post_value))
-          __nanosleep(32);
+        wait_flag(sig.post[threadIdx.x], sig.per_target ? sig.post_vals[threadIdx.x] : sig.post_value, sig, 32);
     }
   }
 }
@@ -552,6 +575,10 @@ void batch_launch(const Batch &b, void *stream, const BatchSignal *bs) {
   for (size_t gi = 0; gi < b.groups.size(); ++gi) {
     const BatchGroup &g = b.groups[gi];
     BatchSig sig{};
+    if (bs) {
+      sig.timeout_ns = bs->timeout_ns;
+      sig.err = bs->err;
+    }
     if (bs) { // pre-signal and wait in the first kernel, signal from the last
       if (bs->wait.size() > static_cast<size_t>(kMaxSig) || bs->signal.size() > static_cast<size_t>(kMaxSig) ||
           bs->pre.size() > static_cast<size_t>(kMaxSig))
@@ -695,8 +722,7 @@ __global__ void k_flag_signal_wait(const BatchSig sig) {
       st_release_sys(sig.signal[i], sig.per_target ? sig.signal_vals[i] : sig.signal_value);
   }
   if (threadIdx.x < static_cast<unsigned>(sig.n_post))
-    while (ld_acquire_sys(sig.post[threadIdx.x]) < (sig.per_target ? sig.post_vals[threadIdx.x] : sig.post_value))
-      __nanosleep(32);
+    wait_flag(sig.post[threadIdx.x], sig.per_target ? sig.post_vals[threadIdx.x] : sig.post_value, sig, 32);
 }
 
 void flags_signal_wait(const BatchSignal &bs, void *stream) {
@@ -704,6 +730,8 @@ void flags_signal_wait(const BatchSignal &bs, void *stream) {
     fail(SP_ERR_UNSUPPORTED, "flag signalling: more than 32 peers");
   if (bs.signal.empty() && bs.post.empty()) return;
   BatchSig sig{};
+  sig.timeout_ns = bs.timeout_ns;
+  sig.err = bs.err;
   sig.n_signal = static_cast<int>(bs.signal.size());
   sig.n_post = static_cast<int>(bs.post.size());
   for (int i = 0; i < sig.n_signal; ++i) sig.signal[i] = reinterpret_cast<unsigned long long *>(bs.signal[i]);

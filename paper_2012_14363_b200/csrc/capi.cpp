@@ -66,6 +66,7 @@ const char *sp_status_string(sp_status s) {
   case SP_ERR_INVALID_HANDLE: return "InvalidHandle";
   case SP_ERR_CUDA: return "CudaError";
   case SP_ERR_NO_DEVICE: return "NoDevice";
+  case SP_ERR_TIMEOUT: return "Timeout";
   default: return "unknown";
   }
 }

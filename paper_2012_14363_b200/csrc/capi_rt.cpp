@@ -441,6 +441,8 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
       // is whole, so no separate wait kernel
       ks.post = ready;
       ks.post_value = it;
+      ks.err = rt_device_err();
+      ks.timeout_ns = rt_device_timeout_ns();
       cuda_check(cudaEventRecord(p->ev[0], s), "cudaEventRecord");
       batch_execute_signaled(*p->pack, s, ks);
       cuda_check(cudaEventRecord(p->ev[3], s), "cudaEventRecord"); // one launch: no phase boundaries
@@ -473,6 +475,8 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
       us.signal_value = it;
       us.done = p->done + 1;
       ps.sys_scope = us.sys_scope = p->remote_peers;
+      ps.err = us.err = rt_device_err();
+      ps.timeout_ns = us.timeout_ns = rt_device_timeout_ns();
       cuda_check(cudaEventRecord(p->ev[0], s), "cudaEventRecord");
       batch_execute_signaled(*p->pack, s, ps);
       cuda_check(cudaEventRecord(p->ev[1], s), "cudaEventRecord");
@@ -504,6 +508,8 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
     // the call only enqueues, and iterations pipeline on the runtime stream
     const bool async = !times && (p->method == SP_HALO_DIRECT || p->method == SP_HALO_FUSED_ASYNC);
     if (!async) cuda_check(cudaEventSynchronize(p->ev[3]), "cudaEventSynchronize");
+    // a flag wait of this (or, enqueue-only, an earlier) iteration gave up
+    rt_check_device_error("halo exchange");
     if (times) {
       float a = 0, b = 0, d = 0, t = 0;
       cudaEventElapsedTime(&t, p->ev[0], p->ev[3]);

@@ -252,6 +252,8 @@ struct BatchSignal {
   std::vector<const uint64_t *> post; // local flags the last block waits for after signalling
   uint64_t post_value = 0;
   std::vector<uint64_t> signal_values, post_values; // per-target values (else the scalars)
+  int *err = nullptr;      // set to 1 by an in-kernel wait that gave up (mapped host memory)
+  uint64_t timeout_ns = 0; // in-kernel wait limit, 0 = unbounded
 };
 constexpr int kMaxSignalPeers = 32; // flags a signalled launch carries (batch.cu kMaxSig)
 // one-warp kernel: release-stores the signals, then waits for the post flags

@@ -17,6 +17,10 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cerrno>
+#include <chrono>
+#include <csignal>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
@@ -123,6 +127,41 @@ void pause_briefly(unsigned &spins) {
   }
 }
 
+// TEMPI_TIMEOUT (seconds, default 300; 0 = wait forever): how long any
+// host wait for a peer and any in-kernel wait for a peer's flag may last
+double timeout_s() {
+  static const double t = [] {
+    const char *e = std::getenv("TEMPI_TIMEOUT");
+    return e && *e ? std::atof(e) : 300.0;
+  }();
+  return t;
+}
+
+struct Runtime;
+Runtime *g_rt = nullptr;
+void check_peers_alive(int peer, const char *what);
+
+// A host wait on other ranks: backs off like pause_briefly, and every few
+// milliseconds checks that the awaited rank(s) still exist and that the
+// wait has not outlived TEMPI_TIMEOUT -- a dead or stuck peer becomes
+// SP_ERR_TIMEOUT (MPI_ERR_OTHER) instead of a hang.
+struct Waiter {
+  unsigned spins = 0;
+  int peer; // the rank waited for, -1: any rank
+  const char *what;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit Waiter(const char *w, int p = -1) : peer(p), what(w) {}
+  void pause() {
+    pause_briefly(spins);
+    if (spins < 4096 || (spins & 127)) return;
+    if (g_rt) check_peers_alive(peer, what);
+    const double lim = timeout_s();
+    if (lim > 0 && std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > lim)
+      fail(SP_ERR_TIMEOUT, std::string(what) + ": no progress within TEMPI_TIMEOUT=" + std::to_string(lim) + " s" +
+                               (peer >= 0 ? " waiting for rank " + std::to_string(peer) : std::string()));
+  }
+};
+
 struct Runtime {
   int rank = -1, size = 0, device = -1;
   std::string name;
@@ -147,17 +186,42 @@ struct Runtime {
   std::vector<uint64_t> pair_sent, pair_recv;
   unsigned *nbr_done = nullptr;
   bool nbr_remote = false;
+  // set (to 1) by an in-kernel flag wait that gave up after TEMPI_TIMEOUT;
+  // mapped pinned memory, read by the host after each synchronisation
+  int *err_host = nullptr, *err_dev = nullptr;
   std::string nbr_layout; // bytes of the last published neighbour layout
   std::unique_ptr<sp_model_cache_s, sp_status (*)(sp_model_cache_s *)> cache{nullptr, sp_model_cache_free};
   sp_profile_s *profile = nullptr;
   std::mutex mu; // the runtime serialises its own calls (MPI_THREAD_SERIALIZED)
 };
 
-Runtime *g_rt = nullptr;
-
 Runtime &rt() {
   if (!g_rt) fail(SP_ERR_INVALID_ARGUMENT, "runtime not initialised (sp_rt_init)");
   return *g_rt;
+}
+
+void check_peers_alive(int peer, const char *what) {
+  Runtime &R = *g_rt;
+  for (int r = peer < 0 ? 0 : peer; r < (peer < 0 ? R.size : peer + 1); ++r) {
+    if (r == R.rank) continue;
+    const int32_t pid = R.shm->slots[r].pid;
+    if (pid <= 0) continue;
+    bool gone = kill(pid, 0) != 0 && errno == ESRCH;
+    if (!gone) { // an exited process nobody has reaped yet is a zombie
+      char path[64], buf[256];
+      std::snprintf(path, sizeof(path), "/proc/%d/stat", static_cast<int>(pid));
+      if (FILE *f = std::fopen(path, "r")) {
+        const size_t n = std::fread(buf, 1, sizeof(buf) - 1, f);
+        std::fclose(f);
+        buf[n] = 0;
+        const char *close_paren = std::strrchr(buf, ')');
+        gone = close_paren && close_paren[1] == ' ' && (close_paren[2] == 'Z' || close_paren[2] == 'X');
+      }
+    }
+    if (gone)
+      fail(SP_ERR_TIMEOUT, std::string(what) + ": rank " + std::to_string(r) + " (pid " + std::to_string(pid) +
+                               ") has exited");
+  }
 }
 
 std::string host_name(const std::string &base, int r) { return base + "_h" + std::to_string(r); }
@@ -192,12 +256,12 @@ void post(int dst, const Msg &m) {
   Runtime &R = rt();
   Mailbox &b = R.shm->box[dst][R.rank];
   const uint64_t t = b.tail.load(std::memory_order_relaxed);
-  unsigned spins = 0;
+  Waiter w("control message (mailbox full)", dst);
   // a full ring: keep draining our own mailboxes so two ranks posting to
   // each other cannot wait on each other
   while (t - b.head.load(std::memory_order_acquire) >= kRing) {
     drain();
-    pause_briefly(spins);
+    w.pause();
   }
   b.ring[t % kRing] = m;
   b.tail.store(t + 1, std::memory_order_release);
@@ -217,7 +281,7 @@ void drain() {
 
 Msg wait_msg(uint32_t kind, int src, int tag) {
   Runtime &R = rt();
-  unsigned spins = 0;
+  Waiter w("control message", src);
   for (;;) {
     drain();
     for (auto it = R.unexpected.begin(); it != R.unexpected.end(); ++it) {
@@ -227,7 +291,7 @@ Msg wait_msg(uint32_t kind, int src, int tag) {
         return m;
       }
     }
-    pause_briefly(spins);
+    w.pause();
   }
 }
 
@@ -310,9 +374,9 @@ void rt_init(int rank, int size, const char *name, int device, int64_t window_by
     std::atomic_thread_fence(std::memory_order_release);
     reinterpret_cast<std::atomic<uint64_t> *>(&G.shm->magic)->store(kMagic, std::memory_order_release);
   } else {
-    unsigned spins = 0;
+    Waiter w("runtime bootstrap (rank 0)");
     while (reinterpret_cast<std::atomic<uint64_t> *>(&G.shm->magic)->load(std::memory_order_acquire) != kMagic)
-      pause_briefly(spins);
+      w.pause();
   }
   Slot &me = G.shm->slots[rank];
   me.pid = static_cast<int32_t>(getpid());
@@ -346,6 +410,11 @@ void rt_init(int rank, int size, const char *name, int device, int64_t window_by
     cuda_check(cudaMemset(G.nbr_flags, 0, kMaxRanks * sizeof(uint64_t)), "cudaMemset(nbr flags)");
     cuda_check(cudaMalloc(&G.nbr_done, sizeof(unsigned)), "cudaMalloc(nbr done)");
     cuda_check(cudaMemset(G.nbr_done, 0, sizeof(unsigned)), "cudaMemset(nbr done)");
+    cuda_check(cudaHostAlloc(reinterpret_cast<void **>(&G.err_host), sizeof(int), cudaHostAllocMapped),
+               "cudaHostAlloc(device wait error flag)");
+    *G.err_host = 0;
+    cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void **>(&G.err_dev), G.err_host, 0),
+               "cudaHostGetDevicePointer");
     cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
   }
   me.ready.store(1, std::memory_order_release);
@@ -378,6 +447,7 @@ void rt_finalize() {
   if (R.window) cudaFree(R.window);
   if (R.nbr_flags) cudaFree(R.nbr_flags);
   if (R.nbr_done) cudaFree(R.nbr_done);
+  if (R.err_host) cudaFreeHost(R.err_host);
   if (R.host) {
     cudaHostUnregister(R.host);
     munmap(R.host, static_cast<size_t>(R.host_bytes));
@@ -394,6 +464,22 @@ void rt_finalize() {
   g_rt = nullptr;
 }
 
+uint64_t rt_device_timeout_ns() {
+  const double t = timeout_s();
+  return t > 0 ? static_cast<uint64_t>(t * 1e9) : 0;
+}
+
+int *rt_device_err() { return rt().err_dev; }
+
+void rt_check_device_error(const char *what) {
+  Runtime &R = rt();
+  if (R.err_host && *reinterpret_cast<volatile int *>(R.err_host)) {
+    *R.err_host = 0;
+    fail(SP_ERR_TIMEOUT, std::string(what) + ": an in-kernel wait for a peer's flag gave up after TEMPI_TIMEOUT=" +
+                             std::to_string(timeout_s()) + " s (a peer rank died or never entered the call)");
+  }
+}
+
 int rt_rank() { return rt().rank; }
 int rt_size() { return rt().size; }
 
@@ -405,10 +491,10 @@ void rt_barrier() {
     R.shm->arrived.store(0, std::memory_order_relaxed);
     R.shm->generation.store(gen + 1, std::memory_order_release);
   } else {
-    unsigned spins = 0;
+    Waiter w("barrier");
     while (R.shm->generation.load(std::memory_order_acquire) == gen) {
       rt_progress(); // pending non-blocking messages keep moving
-      pause_briefly(spins);
+      w.pause();
     }
   }
 }
@@ -1084,8 +1170,8 @@ bool rt_test(uint64_t id, RtStatus *st) {
 }
 
 void rt_wait(uint64_t id, RtStatus *st) {
-  unsigned spins = 0;
-  while (!rt_test(id, st)) pause_briefly(spins);
+  Waiter w("MPI_Wait");
+  while (!rt_test(id, st)) w.pause();
 }
 
 void rt_set_chunk(int64_t bytes) {
@@ -1248,19 +1334,29 @@ bool nbr_last_hit(const NbrLast &last, const std::string &sig) {
   return true;
 }
 
-void nbr_last_set(NbrLast &last, std::string sig, const std::vector<int> &dests, Batch *b,
-                  std::vector<LooseOp> loose, std::vector<std::shared_ptr<TableCopy>> tables = {}) {
+// Layout versions of the distinct out-neighbours, read BEFORE their
+// layouts are: the record of a built call must carry the versions the
+// build saw. Read after the launch instead, a receiver released by this
+// call's READY flags could already have published its next layout, and
+// its new version would then vouch for a batch built from the old one.
+std::vector<std::pair<int, uint64_t>> peer_versions(const std::vector<int> &dests) {
   Runtime &R = rt();
-  last.sig = std::move(sig);
-  last.loose = std::move(loose);
-  last.tables = std::move(tables);
-  last.peer_ver.clear();
+  std::vector<std::pair<int, uint64_t>> out;
   std::vector<char> seen(R.size, 0);
   for (int d : dests)
     if (!seen[d]) {
       seen[d] = 1;
-      last.peer_ver.emplace_back(d, R.shm->slots[d].layout_ver.load(std::memory_order_acquire));
+      out.emplace_back(d, R.shm->slots[d].layout_ver.load(std::memory_order_acquire));
     }
+  return out;
+}
+
+void nbr_last_set(NbrLast &last, std::string sig, std::vector<std::pair<int, uint64_t>> vers, Batch *b,
+                  std::vector<LooseOp> loose, std::vector<std::shared_ptr<TableCopy>> tables = {}) {
+  last.sig = std::move(sig);
+  last.loose = std::move(loose);
+  last.tables = std::move(tables);
+  last.peer_ver = std::move(vers);
   last.batch = b;
   last.valid = true;
 }
@@ -1329,14 +1425,16 @@ BatchSignal nbr_enter(const std::vector<int> &sources, const std::vector<int> &d
     outs.push_back(d);
   }
   for (int d : outs) {
-    unsigned spins = 0;
+    Waiter w("neighbour collective entry", d);
     while (R.shm->slots[d].pair_entered[R.rank].load(std::memory_order_acquire) < R.pair_sent[d]) {
       rt_progress();
-      pause_briefly(spins);
+      w.pause();
     }
   }
   bs.done = R.nbr_done;
   bs.sys_scope = R.nbr_remote;
+  bs.err = R.err_dev;
+  bs.timeout_ns = rt_device_timeout_ns();
   return bs;
 }
 
@@ -1356,6 +1454,7 @@ void nbr_run(Batch *b, const std::vector<LooseOp> &loose, const BatchSignal &bs)
     flags_signal_wait(bs, R.stream);
   }
   cuda_check(cudaStreamSynchronize(R.stream), "cudaStreamSynchronize(neighbor)");
+  rt_check_device_error("neighbour collective");
 }
 
 // A call that fails after nbr_enter still completes the entry protocol:
@@ -1408,6 +1507,7 @@ void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &s
       nbr_run(g_last_v.batch, g_last_v.loose, bs);
       return;
     }
+    auto vers = peer_versions(dests); // before any layout is read
     std::string key(reinterpret_cast<const char *>(&sendbuf), sizeof(sendbuf));
     std::vector<BatchSpec> jobs;
     std::vector<LooseOp> loose;
@@ -1451,7 +1551,7 @@ void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &s
       }
     }
     nbr_run(b, loose, bs); // returns when every block addressed to this rank has landed
-    nbr_last_set(g_last_v, std::move(sig), dests, b, std::move(loose));
+    nbr_last_set(g_last_v, std::move(sig), std::move(vers), b, std::move(loose));
   });
 }
 
@@ -1620,6 +1720,7 @@ void rt_neighbor_alltoallw_build(const uint8_t *sendbuf, const std::vector<int64
     nbr_run(g_last_w.batch, g_last_w.loose, bs);
     return;
   }
+  auto vers = peer_versions(dests); // before any layout is read
   std::string key(reinterpret_cast<const char *>(&sendbuf), sizeof(sendbuf));
   std::vector<CopySpec> jobs;
   std::vector<LooseOp> loose;
@@ -1715,7 +1816,7 @@ void rt_neighbor_alltoallw_build(const uint8_t *sendbuf, const std::vector<int64
     }
   }
   nbr_run(b, loose, bs); // returns when every block addressed to this rank has landed
-  nbr_last_set(g_last_w, std::move(sig), dests, b, std::move(loose), std::move(tables));
+  nbr_last_set(g_last_w, std::move(sig), std::move(vers), b, std::move(loose), std::move(tables));
 }
 
 } // namespace spb

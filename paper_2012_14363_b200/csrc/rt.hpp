@@ -19,6 +19,12 @@ struct RtStatus {
 
 void rt_init(int rank, int size, const char *name, int device, int64_t window_bytes, int64_t host_bytes);
 void rt_finalize();
+// bounded device waits: the limit for in-kernel flag spins (0 = none), the
+// flag such a spin sets when it gives up, and the host-side check that
+// turns it into SP_ERR_TIMEOUT after a synchronisation
+uint64_t rt_device_timeout_ns();
+int *rt_device_err();
+void rt_check_device_error(const char *what);
 int rt_rank();
 int rt_size();
 void rt_barrier();

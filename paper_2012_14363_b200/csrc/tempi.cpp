@@ -61,6 +61,7 @@ int to_mpi(sp_status st) {
   case SP_ERR_OVERLAPPING_LAYOUT: return MPI_ERR_TYPE;
   case SP_ERR_UNSUPPORTED: return MPI_ERR_UNSUPPORTED_OPERATION;
   case SP_ERR_INVALID_HANDLE: return MPI_ERR_TYPE;
+  case SP_ERR_TIMEOUT: return MPI_ERR_OTHER;
   default: return MPI_ERR_INTERN;
   }
 }

@@ -70,6 +70,78 @@ def test_runtime_control_plane(world):
     assert set(_spawn(_control, world).values()) == {"ok"}
 
 
+def _dead_peer(rank, world, job):
+    """rank 1 exits without finalising; rank 0's barrier notices the dead
+    process and raises Timeout (long before TEMPI_TIMEOUT)"""
+    import time
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.rt as rt
+    rt.init(rank, world, job, device=-1)
+    if rank == 1:
+        os._exit(0)
+    t0 = time.time()
+    try:
+        rt.barrier()
+        return "no error"
+    except sp.Timeout as e:
+        return ("Timeout", "exited" in str(e), time.time() - t0 < 30)
+
+
+def _stuck_peer(rank, world, job):
+    """rank 1 is alive but never enters the barrier: rank 0 gives up after
+    TEMPI_TIMEOUT seconds with Timeout"""
+    import time
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.rt as rt
+    rt.init(rank, world, job, device=-1)
+    if rank == 1:
+        time.sleep(6)
+        return "slept"
+    t0 = time.time()
+    try:
+        rt.barrier()
+        return "no error"
+    except sp.Timeout as e:
+        return ("Timeout", "TEMPI_TIMEOUT" in str(e), 0.8 < time.time() - t0 < 5)
+
+
+def _spawn_raw(target, world, want=None, timeout=60):
+    """like _spawn, but only the ranks in `want` must report (a rank that
+    exits without reporting is not an error)"""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    job = uuid.uuid4().hex[:12]
+    ps = [ctx.Process(target=_entry, args=(target, r, world, job, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = {}
+    want = set(range(world)) if want is None else set(want)
+    try:
+        while not want <= set(out):
+            try:
+                r, ok, payload = q.get(timeout=timeout)
+            except Exception:
+                break
+            out[r] = payload if ok else "error: " + payload
+    finally:
+        for p in ps:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    return out
+
+
+def test_runtime_dead_peer_raises_timeout():
+    res = _spawn_raw(_dead_peer, 2, want=[0])
+    assert res.get(0) == ("Timeout", True, True), res
+
+
+def test_runtime_stuck_peer_times_out(monkeypatch):
+    monkeypatch.setenv("TEMPI_TIMEOUT", "1")
+    res = _spawn_raw(_stuck_peer, 2)
+    assert res.get(0) == ("Timeout", True, True), res
+
+
 # ------------------------------------------------------------ GPU data plane
 def _sendrecv(rank, world, job):
     import torch
@@ -777,6 +849,39 @@ def _halo(rank, world, job, ranks, method):
     plan.free()
     rt.finalize()
     return bad, t
+
+
+def _halo_peer_absent(rank, world, job):
+    """rank 1 builds the DIRECT halo plan and then never exchanges: rank 0's
+    exchange kernel waits in its last block for rank 1's READY flag, gives
+    up after TEMPI_TIMEOUT, and the host reports Timeout instead of the GPU
+    spinning forever"""
+    import time
+    import torch
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.halo as H
+    import paper_2012_14363_b200.rt as rt
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=1 << 20, host_bytes=1 << 20)
+    cfg = H.HaloConfig((2, 1, 1), (12, 10, 8), 2, 16)
+    alloc = torch.empty(16 * 14 * 12 * 16, dtype=torch.uint8, device="cuda")
+    plan = rt.HaloPlan(cfg, alloc, 3)
+    if rank == 1:
+        time.sleep(8)
+        return "absent"
+    t0 = time.time()
+    try:
+        plan.exchange()
+        return "no error"
+    except sp.Timeout:
+        return ("Timeout", time.time() - t0 < 7)
+
+
+@pytest.mark.gpu
+def test_device_flag_wait_times_out(cuda, monkeypatch):
+    monkeypatch.setenv("TEMPI_TIMEOUT", "2")
+    res = _spawn_raw(_halo_peer_absent, 2, timeout=120)
+    assert res.get(0) == ("Timeout", True), res
 
 
 @pytest.mark.gpu
