@@ -279,7 +279,11 @@ sp_status sp_batch_free(sp_batch b);
 typedef struct sp_profile_s *sp_profile;
 typedef struct sp_model_cache_s *sp_model_cache;
 enum { SP_CURVE_CPU_CPU = 0, SP_CURVE_GPU_GPU = 1, SP_CURVE_D2H = 2, SP_CURVE_H2D = 3 };
-enum { SP_SURF_GPU_PACK = 0, SP_SURF_GPU_UNPACK = 1, SP_SURF_HOST_PACK = 2, SP_SURF_HOST_UNPACK = 3 };
+enum { SP_SURF_GPU_PACK = 0, SP_SURF_GPU_UNPACK = 1, SP_SURF_HOST_PACK = 2, SP_SURF_HOST_UNPACK = 3,
+       /* B200 extension (optional in the profile text, written only when
+        * measured): one typed-copy launch from the probe layout to the same
+        * layout on this GPU / on a peer GPU over NVLink -- the DIRECT method */
+       SP_SURF_GPU_DIRECT = 4, SP_SURF_GPU_DIRECT_PEER = 5 };
 enum { SP_METHOD_ONESHOT = 0, SP_METHOD_DEVICE = 1, SP_METHOD_STAGED = 2, /* MethodChoice perf_model.hpp:46 */
        SP_METHOD_DIRECT = 3 /* runtime only (sp_rt_*): the device path with the
                                pack, NVLink transfer and unpack fused into one
@@ -311,6 +315,15 @@ sp_status sp_model_times(sp_profile p, int64_t object_size, int64_t block_size,
 /* choose_method          perf_model.hpp:163 */
 sp_status sp_choose_method(sp_profile p, int64_t object_size,
                            int64_t block_size, int *method);
+/* B200 extension of choose_method: Eqs. 1-3 plus Eq. 4 (DIRECT = the
+ * gpu_direct surface when dst_kind = 1, a device buffer on this GPU, or the
+ * gpu_direct_peer surface when dst_kind = 2, a device buffer on a peer GPU;
+ * never for dst_kind = 0, host memory, or an unmeasured surface). Ties
+ * prefer DIRECT, then the reference's order. times (NULL ok) = device,
+ * one-shot, staged, direct (+inf when DIRECT is not a candidate). */
+sp_status sp_choose_method_b200(sp_profile p, int64_t object_size,
+                                int64_t block_size, int dst_kind, int *method,
+                                double times[4]);
 /* ModelCache             perf_model.hpp:184-229 (the profile must outlive
  * nothing: the cache keeps its own reference) */
 sp_status sp_model_cache_create(sp_profile p, sp_model_cache *out);

@@ -104,6 +104,7 @@ _sig("sp_interp_1d", C.c_int, vp, C.c_int, dbl, dblp)
 _sig("sp_interp_2d", C.c_int, vp, C.c_int, dbl, dbl, dblp)
 _sig("sp_model_times", C.c_int, vp, i64, i64, dblp, dblp, dblp)
 _sig("sp_choose_method", C.c_int, vp, i64, i64, C.POINTER(C.c_int))
+_sig("sp_choose_method_b200", C.c_int, vp, i64, i64, C.c_int, C.POINTER(C.c_int), dblp)
 _sig("sp_model_cache_create", C.c_int, vp, C.POINTER(vp))
 _sig("sp_model_cache_choose", C.c_int, vp, i64, i64, C.POINTER(C.c_int))
 _sig("sp_model_cache_free", C.c_int, vp)

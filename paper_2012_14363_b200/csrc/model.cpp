@@ -101,14 +101,33 @@ int choose_method(const Profile &p, int64_t object_size, int64_t block_size) {
   return best;
 }
 
+int choose_method_b200(const Profile &p, int64_t object_size, int64_t block_size, int dst_kind, double times[4]) {
+  const int ref = choose_method(p, object_size, block_size);
+  const ModelTimes t = model_times(p, object_size, block_size);
+  const Surface *direct = dst_kind == kDstSameGpu   ? &p.surf[SP_SURF_GPU_DIRECT]
+                          : dst_kind == kDstPeerGpu ? &p.surf[SP_SURF_GPU_DIRECT_PEER]
+                                                    : nullptr;
+  const double td = direct && !direct->object.empty()
+                        ? interp_2d(*direct, static_cast<double>(object_size), static_cast<double>(block_size))
+                        : HUGE_VAL;
+  if (times) {
+    times[0] = t.device;
+    times[1] = t.oneshot;
+    times[2] = t.staged;
+    times[3] = td;
+  }
+  const double tref = ref == SP_METHOD_DEVICE ? t.device : ref == SP_METHOD_ONESHOT ? t.oneshot : t.staged;
+  return td <= tref ? SP_METHOD_DIRECT : ref;
+}
+
 // ------------------------------------------------------------ text format
 namespace {
 
 const char *kCurveNames[4] = {"cpu_cpu", "gpu_gpu", "d2h", "h2d"};
-const char *kSurfNames[4] = {"gpu_pack", "gpu_unpack", "host_pack", "host_unpack"};
+const char *kSurfNames[6] = {"gpu_pack", "gpu_unpack", "host_pack", "host_unpack", "gpu_direct", "gpu_direct_peer"};
 
-int name_index(const char *const names[4], const std::string &s) {
-  for (int i = 0; i < 4; ++i)
+template <int N> int name_index(const char *const (&names)[N], const std::string &s) {
+  for (int i = 0; i < N; ++i)
     if (s == names[i]) return i;
   return -1;
 }
@@ -159,8 +178,8 @@ Surface grid_of(const std::vector<std::array<double, 3>> &rows, const char *name
 
 Profile parse_profile(const std::string &text) {
   Profile p;
-  std::vector<std::array<double, 3>> rows[4];
-  bool have_rows[4] = {false, false, false, false};
+  std::vector<std::array<double, 3>> rows[6];
+  bool have_rows[6] = {false, false, false, false, false, false};
   int cur_curve = -1, cur_surf = -1;
   std::istringstream in(text);
   std::string line;
@@ -200,7 +219,8 @@ Profile parse_profile(const std::string &text) {
   }
   // curves are validated in name order (the reference iterates a std::map)
   for (int i : {SP_CURVE_CPU_CPU, SP_CURVE_D2H, SP_CURVE_GPU_GPU, SP_CURVE_H2D}) check_curve(p.curve[i], kCurveNames[i]);
-  for (int i : {SP_SURF_GPU_PACK, SP_SURF_GPU_UNPACK, SP_SURF_HOST_PACK, SP_SURF_HOST_UNPACK})
+  for (int i : {SP_SURF_GPU_PACK, SP_SURF_GPU_UNPACK, SP_SURF_HOST_PACK, SP_SURF_HOST_UNPACK, SP_SURF_GPU_DIRECT,
+                SP_SURF_GPU_DIRECT_PEER})
     if (have_rows[i]) p.surf[i] = grid_of(rows[i], kSurfNames[i]);
   return p;
 }
@@ -222,8 +242,9 @@ std::string format_profile(const Profile &p, const std::string &header) {
     for (size_t k = 0; k < p.curve[i].size.size(); ++k)
       out += num(p.curve[i].size[k]) + " " + num(p.curve[i].time[k]) + "\n";
   }
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 6; ++i) {
     const Surface &s = p.surf[i];
+    if (i >= 4 && s.object.empty()) continue; // extension surfaces only when measured
     out += std::string("surface ") + kSurfNames[i] + "\n";
     for (size_t a = 0; a < s.object.size(); ++a)
       for (size_t b = 0; b < s.block.size(); ++b)
@@ -387,7 +408,7 @@ sp_status sp_profile_set_surface(sp_profile p, int surf, const double *object, i
                                  int64_t nblk, const double *time) {
   return guard_m([&] {
     need(p);
-    if (surf < 0 || surf > 3 || nobj < 0 || nblk < 0) spb::fail(SP_ERR_INVALID_ARGUMENT, "bad surface");
+    if (surf < 0 || surf > 5 || nobj < 0 || nblk < 0) spb::fail(SP_ERR_INVALID_ARGUMENT, "bad surface");
     spb::Surface s;
     s.object.assign(object, object + nobj);
     s.block.assign(block, block + nblk);
@@ -409,7 +430,7 @@ sp_status sp_interp_2d(sp_profile p, int surf, double object, double block, doub
   return guard_m([&] {
     need(p);
     need(t);
-    if (surf < 0 || surf > 3) spb::fail(SP_ERR_INVALID_ARGUMENT, "bad surface");
+    if (surf < 0 || surf > 5) spb::fail(SP_ERR_INVALID_ARGUMENT, "bad surface");
     *t = spb::interp_2d(p->p->surf[surf], object, block);
   });
 }
@@ -430,6 +451,16 @@ sp_status sp_choose_method(sp_profile p, int64_t object_size, int64_t block_size
     need(p);
     need(method);
     *method = spb::choose_method(*p->p, object_size, block_size);
+  });
+}
+
+sp_status sp_choose_method_b200(sp_profile p, int64_t object_size, int64_t block_size, int dst_kind, int *method,
+                                double times[4]) {
+  return guard_m([&] {
+    need(p);
+    need(method);
+    if (dst_kind < 0 || dst_kind > 2) spb::fail(SP_ERR_INVALID_ARGUMENT, "dst_kind must be 0, 1 or 2");
+    *method = spb::choose_method_b200(*p->p, object_size, block_size, dst_kind, times);
   });
 }
 

@@ -28,6 +28,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "guard.hpp"
@@ -192,6 +193,7 @@ struct Runtime {
   std::string nbr_layout; // bytes of the last published neighbour layout
   std::unique_ptr<sp_model_cache_s, sp_status (*)(sp_model_cache_s *)> cache{nullptr, sp_model_cache_free};
   sp_profile_s *profile = nullptr;
+  std::map<std::tuple<int64_t, int64_t, int>, bool> direct_cache; // model_prefers_direct answers
   std::mutex mu; // the runtime serialises its own calls (MPI_THREAD_SERIALIZED)
 };
 
@@ -565,7 +567,7 @@ void rt_exchange_ptr(void *local, std::vector<uint8_t *> &out) {
 namespace {
 
 constexpr uint32_t kCHUNK = 5;
-constexpr int64_t kDirectRemoteMinRow = 64; // bytes per destination row for DIRECT across GPUs
+constexpr int64_t kOfferForced = 4; // RTS offer flag: DIRECT was asked for explicitly
 constexpr int64_t kGrantAlign = 256;
 
 struct RangeAlloc {
@@ -616,6 +618,7 @@ struct Req {
   CommitPtr ct;
   int peer = -1, tag = 0, method = 0;
   bool allow_direct = false;
+  bool forced_direct = false; // the sender asked for DIRECT explicitly (no model veto)
   int64_t bytes = 0;
   // sender
   uint64_t rreq = 0;
@@ -817,6 +820,7 @@ bool step_send(Req &q) {
         cudaGetLastError();
       }
     }
+    if (offer && q.forced_direct) offer |= kOfferForced;
     post(q.peer, Msg{kRTS, R.rank, q.tag, q.method, q.bytes, offer, static_cast<int64_t>(q.id)});
     q.st = St::WaitCts;
     return true;
@@ -889,18 +893,18 @@ bool step_recv(Req &q) {
       const int64_t objs = q.ct->size ? m.bytes / q.ct->size : 0;
       const bool dense = q.ct->form == SP_FORM_STRIDED && q.ct->sb.ndims() == 1 &&
                          (objs <= 1 || q.ct->extent == q.ct->size);
-      if (!q.err && ((m.offset == 1 && describable(*q.ct) && range_capable(*q.ct, objs, q.rbuf, q.rbuf)) ||
-                     (m.offset == 2 && dense && describable(*q.ct)))) {
+      const int64_t offer = m.offset & 3;
+      if (!q.err && ((offer == 1 && describable(*q.ct) && range_capable(*q.ct, objs, q.rbuf, q.rbuf)) ||
+                     (offer == 2 && dense && describable(*q.ct)))) {
         cudaPointerAttributes at{};
         const bool dev = cudaPointerGetAttributes(&at, q.rbuf) == cudaSuccess && at.type == cudaMemoryTypeDevice;
         cudaGetLastError();
-        // over NVLink the fused copy stores each destination row as its own
-        // remote write: short rows would cost a link transaction per few
-        // bytes, where the fallback ships packed full lines and unpacks
-        // locally -- accept DIRECT from another GPU only for rows >= 64 B
-        const bool remote = R.shm->slots[m.src].device != R.device;
-        const bool rows_ok = m.offset == 2 || !remote || q.ct->sb.counts[0] >= kDirectRemoteMinRow;
-        if (dev && rows_ok) q.method = SP_METHOD_DIRECT; // a descriptor slot is taken at the grant
+        // the fused copy stores every destination row as its own write (over
+        // NVLink when the sender is on another GPU): the receiver's layout
+        // has a say too -- a model-offered DIRECT is accepted only when the
+        // model, asked with this side's geometry, also prefers it
+        const bool model_ok = (m.offset & kOfferForced) || model_prefers_direct(*q.ct, objs, R.shm->slots[m.src].device);
+        if (dev && model_ok) q.method = SP_METHOD_DIRECT; // a descriptor slot is taken at the grant
       }
       q.st = St::Matched;
       return true;
@@ -1101,7 +1105,11 @@ uint64_t rt_isend(const void *buf, uint64_t buf_bytes, int64_t count, CommitPtr 
   // On B200 the fused copy wins at every size measured (one kernel, no
   // window, no unpack; bench.py `send`), which the paper's three-term
   // model cannot express.
-  bool allow_direct = method < 0 || method == SP_METHOD_DIRECT;
+  // DIRECT is offered when asked for explicitly, or when the B200 model
+  // (Eq. 4, the measured gpu_direct / gpu_direct_peer surface of the
+  // receiver's GPU) puts it ahead of the reference's three methods
+  const bool forced_direct = method == SP_METHOD_DIRECT;
+  bool allow_direct = forced_direct || (method < 0 && model_prefers_direct(*ct, count, R.shm->slots[dest].device));
   if (method < 0) method = rt_choose(*ct, count);
   if (method == SP_METHOD_DIRECT) method = SP_METHOD_DEVICE;
   if (method != SP_METHOD_DEVICE && method != SP_METHOD_ONESHOT && method != SP_METHOD_STAGED)
@@ -1121,6 +1129,7 @@ uint64_t rt_isend(const void *buf, uint64_t buf_bytes, int64_t count, CommitPtr 
   q->tag = tag;
   q->method = method;
   q->allow_direct = allow_direct;
+  q->forced_direct = forced_direct;
   q->bytes = bytes;
   q->st = St::Start;
   const uint64_t id = q->id;
@@ -1196,6 +1205,7 @@ void rt_recv(void *buf, uint64_t buf_bytes, int64_t count, CommitPtr ct, int sou
 void rt_set_profile(sp_profile_s *p) {
   Runtime &R = rt();
   R.profile = p;
+  R.direct_cache.clear();
   sp_model_cache_s *c = nullptr;
   if (p) {
     if (sp_model_cache_create(p, &c) != SP_OK) fail(SP_ERR_INTERNAL, "model cache");
@@ -1217,6 +1227,30 @@ int rt_choose(const Committed &ct, int64_t count) {
   int m = SP_METHOD_DEVICE;
   if (sp_model_cache_choose(R.cache.get(), obj, blk, &m) != SP_OK) return SP_METHOD_DEVICE;
   return m;
+}
+
+// B200 model (Eq. 4) on DIRECT for `count` objects of `ct` moving between
+// this GPU and a device buffer on `peer_device`: true when the measured
+// DIRECT surface of that destination (same GPU or peer GPU) is at least as
+// fast as the reference's best method; without a profile DIRECT is the
+// default (it measured fastest on B200 at every size, bench.py `send`);
+// with a profile that lacks the surface, never.
+bool model_prefers_direct(const Committed &ct, int64_t count, int peer_device) {
+  Runtime &R = rt();
+  if (!R.profile) return true;
+  if (ct.size == 0 || count < 1) return false;
+  const int64_t obj = ct.size * count;
+  const int64_t blk = ct.form == SP_FORM_STRIDED
+                          ? std::min(ct.sb.counts[0], obj)
+                          : std::max<int64_t>(1, ct.runs.empty() ? 1 : ct.size / static_cast<int64_t>(ct.runs.size()));
+  const int kind = peer_device == R.device ? kDstSameGpu : kDstPeerGpu;
+  const auto key = std::make_tuple(obj, blk, kind);
+  auto it = R.direct_cache.find(key);
+  if (it != R.direct_cache.end()) return it->second;
+  const bool yes = choose_method_b200(*R.profile->p, obj, blk, kind, nullptr) == SP_METHOD_DIRECT;
+  if (R.direct_cache.size() > 4096) R.direct_cache.clear();
+  R.direct_cache.emplace(key, yes);
+  return yes;
 }
 
 void *rt_stream() { return rt().stream; }

@@ -43,6 +43,9 @@ void rt_progress();
 void rt_set_chunk(int64_t bytes);
 void rt_set_profile(sp_profile_s *p);
 int rt_choose(const Committed &ct, int64_t count);
+// the B200 model's verdict on DIRECT between this GPU and a device buffer
+// on `peer_device` (Eq. 4 vs the reference's best of Eqs. 1-3)
+bool model_prefers_direct(const Committed &ct, int64_t count, int peer_device);
 void *rt_stream();
 void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &send_counts,
                            const std::vector<int64_t> &send_displs, const CommitPtr &stp, uint8_t *recvbuf,

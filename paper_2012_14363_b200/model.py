@@ -18,7 +18,9 @@ from . import _capi, _check
 from ._capi import lib
 
 CURVES = {"cpu_cpu": 0, "gpu_gpu": 1, "d2h": 2, "h2d": 3}
-SURFACES = {"gpu_pack": 0, "gpu_unpack": 1, "host_pack": 2, "host_unpack": 3}
+SURFACES = {"gpu_pack": 0, "gpu_unpack": 1, "host_pack": 2, "host_unpack": 3,
+            # B200 extension (optional): the DIRECT method's typed copy, same GPU / peer GPU
+            "gpu_direct": 4, "gpu_direct_peer": 5}
 DEFAULT_B200_PROFILE = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                     "profiles", "b200.profile")
 
@@ -27,6 +29,13 @@ class MethodChoice(enum.IntEnum):  # perf_model.hpp:46
     OneShot = 0
     Device = 1
     Staged = 2
+    Direct = 3                     # B200 extension (choose_method_b200 only)
+
+
+class Destination(enum.IntEnum):  # where the receive buffer lives (choose_method_b200)
+    Host = 0
+    SameGpu = 1
+    PeerGpu = 2
 
 
 @dataclass(frozen=True)
@@ -121,6 +130,17 @@ def choose_method(p: MachineProfile, q: ModelQuery) -> MethodChoice:
     m = C.c_int()
     _check(lib.sp_choose_method(p.handle, q.object_size, q.block_size, C.byref(m)))
     return MethodChoice(m.value)
+
+
+def choose_method_b200(p: MachineProfile, q: ModelQuery, dst: Destination):
+    """B200 extension: Eqs. 1-3 plus Eq. 4 (DIRECT = the measured gpu_direct
+    / gpu_direct_peer surface of a device destination). Returns (choice,
+    (t_device, t_oneshot, t_staged, t_direct)); t_direct is inf when DIRECT
+    is not a candidate."""
+    m = C.c_int()
+    t = (C.c_double * 4)()
+    _check(lib.sp_choose_method_b200(p.handle, q.object_size, q.block_size, int(dst), C.byref(m), t))
+    return MethodChoice(m.value), tuple(t)
 
 
 class ModelCache:

@@ -212,3 +212,67 @@ def test_warm_cache_speedup_native(tmp_path):
         if best >= 10:
             break
     assert best >= 10, out
+
+
+# ------------------------------------------------------------ B200 extension (Eq. 4, DIRECT)
+def test_b200_choice_without_direct_surface_is_the_reference_choice(M, prof, gold):
+    """a profile without gpu_direct surfaces (the reference's own fixture)
+    chooses exactly like choose_method for every destination; times agree"""
+    for q in gold["base"][:300]:
+        if q["status"]:
+            continue
+        mq = M.ModelQuery(q["o"], q["b"])
+        for dst in M.Destination:
+            m, t = M.choose_method_b200(prof, mq, dst)
+            assert int(m) == q["method"]
+            assert t[:3] == (q["t_device"], q["t_oneshot"], q["t_staged"]) and t[3] == float("inf")
+
+
+def _with_direct(M, text, local, peer=None):
+    p = M.load_profile(text)
+    objs, blks = [64, 1 << 26], [1, 1 << 20]
+    p.set_surface("gpu_direct", objs, blks, [[local, local], [local, local]])
+    if peer is not None:
+        p.set_surface("gpu_direct_peer", objs, blks, [[peer, peer], [peer, peer]])
+    return p
+
+
+def test_b200_choice_argmin_over_four(M, text, gold):
+    """DIRECT wins exactly when its surface time is <= the reference's best
+    for a device destination; never for host memory; the peer surface
+    governs peer-GPU destinations"""
+    fast = _with_direct(M, text, 1e-9, peer=1.0)   # local DIRECT always fastest, peer never
+    for q in gold["base"][:200]:
+        if q["status"]:
+            continue
+        mq = M.ModelQuery(q["o"], q["b"])
+        assert M.choose_method_b200(fast, mq, M.Destination.SameGpu)[0] == M.MethodChoice.Direct
+        assert int(M.choose_method_b200(fast, mq, M.Destination.PeerGpu)[0]) == q["method"]
+        assert int(M.choose_method_b200(fast, mq, M.Destination.Host)[0]) == q["method"]
+        m, t = M.choose_method_b200(fast, mq, M.Destination.SameGpu)
+        assert t[3] == 1e-9
+    # a tie with the reference's best goes to DIRECT
+    q = M.ModelQuery(1 << 20, 64)
+    best = min(M.model_times(M.load_profile(text), q))
+    tie = _with_direct(M, text, best)
+    assert M.choose_method_b200(tie, q, M.Destination.SameGpu)[0] == M.MethodChoice.Direct
+    slower = _with_direct(M, text, best * 1.0001)
+    assert M.choose_method_b200(slower, q, M.Destination.SameGpu)[0] != M.MethodChoice.Direct
+
+
+def test_b200_direct_surfaces_round_trip(M, text):
+    """the extension surfaces are written only when present and survive a
+    save/load round trip; the reference's fixture text is unchanged"""
+    p = _with_direct(M, text, 2e-6, peer=3e-6)
+    out = M.save_profile(p, "x")
+    assert "surface gpu_direct\n" in out and "surface gpu_direct_peer\n" in out
+    q = M.load_profile(out)
+    assert M.save_profile(q, "x") == out
+    assert M.interp_2d(q, "gpu_direct_peer", 4096, 64) == 3e-6
+    assert "gpu_direct" not in M.save_profile(M.load_profile(text))
+
+
+def test_b200_profile_carries_measured_direct_surface(M):
+    """the shipped B200 profile was measured with the DIRECT surface"""
+    p = M.load_profile_file(M.DEFAULT_B200_PROFILE)
+    assert M.interp_2d(p, "gpu_direct", 1 << 20, 64) > 0

@@ -689,24 +689,30 @@ def _nbr_alternating_layouts(rank, world, job, iters):
     send = torch.empty(256, dtype=torch.float64, device="cuda")
     recv = torch.empty(2048, dtype=torch.float64, device="cuda")
     sent = lambda r, it: np.arange(256, dtype=np.float64) + r * 1e6 + it * 1e3
-    bad = 0
+    bad, detail = 0, []
     for it in range(iters):
         k = (it + rank) % len(layouts) if it % 3 else it % len(layouts)  # ranks disagree on most calls
         send.copy_(torch.from_numpy(sent(rank, it)))
         recv.fill_(-1)
+        torch.cuda.synchronize()  # the buffers are ready before the call (MPI's rule for device buffers)
         calls[k](send, recv)
         want = np.full(2048, -1.0)
         want[layouts[k][2]] = sent(left, it)[:128]           # left sent me its first run
         want[1024 + layouts[k][2]] = sent(right, it)[128:]   # right sent me its second run
-        if not np.array_equal(recv.cpu().numpy(), want):
+        got = recv.cpu().numpy()
+        if not np.array_equal(got, want):
             bad += 1
+            if len(detail) < 4:
+                wrong = np.nonzero(got != want)[0]
+                detail.append((it, k, len(wrong), int(wrong[0]), float(got[wrong[0]]), float(want[wrong[0]])))
     rt.finalize()
-    return bad
+    return bad, detail
 
 
 @pytest.mark.gpu
 def test_neighbor_alltoallw_alternating_layouts(cuda):
-    assert _spawn(_nbr_alternating_layouts, 3, 1000, timeout=600) == {0: 0, 1: 0, 2: 0}
+    res = _spawn(_nbr_alternating_layouts, 3, 1000, timeout=600)
+    assert all(bad == 0 for bad, _ in res.values()), res
 
 
 def _nbr_error_after_entry(rank, world, job):

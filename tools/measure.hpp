@@ -96,6 +96,39 @@ inline int measure_profile(const char *out_path, int reps, bool report) {
       }
     CK(sp_profile_set_surface(prof, surf, ox.data(), ox.size(), bx.data(), bx.size(), t.data()));
   }
+  // B200 extension: the DIRECT method's one typed-copy launch, probe layout
+  // -> the same layout in another buffer on this GPU (gpu_direct) and in a
+  // buffer on device 1 over NVLink (gpu_direct_peer, when visible)
+  uint8_t *dst_local = nullptr, *dst_peer = nullptr;
+  cudaMalloc(&dst_local, 2 * big);
+  if (peer) {
+    cudaSetDevice(1);
+    cudaMalloc(&dst_peer, 2 * big);
+    cudaSetDevice(0);
+  }
+  for (int surf : {SP_SURF_GPU_DIRECT, SP_SURF_GPU_DIRECT_PEER}) {
+    uint8_t *dst = surf == SP_SURF_GPU_DIRECT ? dst_local : dst_peer;
+    if (!dst) continue;
+    std::vector<double> t;
+    for (int64_t o : objects)
+      for (int64_t b0 : blocks) {
+        const int64_t b = std::min(b0, o);
+        sp_type row, t2;
+        CK(sp_type_contiguous(b, byte, &row));
+        CK(sp_type_hvector(o / b, 1, 2 * b, row, &t2));
+        CK(sp_type_commit(t2));
+        const sp_copy_job job{src, static_cast<uint64_t>(2 * big), t2, 1, dst, static_cast<uint64_t>(2 * big), t2, 1};
+        t.push_back(median_s(
+            [&] {
+              CK(sp_copy(&job, s));
+              cudaStreamSynchronize(s);
+            },
+            reps));
+        sp_type_free(row);
+        sp_type_free(t2);
+      }
+    CK(sp_profile_set_surface(prof, surf, ox.data(), ox.size(), bx.data(), bx.size(), t.data()));
+  }
   std::vector<double> sx(sizes.begin(), sizes.end());
   auto curve = [&](int which, auto &&copy) {
     std::vector<double> t;
@@ -126,7 +159,9 @@ inline int measure_profile(const char *out_path, int reps, bool report) {
       "\nsurfaces: median wall time of synchronous sp_pack/sp_unpack (enqueue + completion)," +
       " probe hvector(o/b,1,2b,contiguous(b,BYTE))\n" +
       (peer ? "gpu_gpu: cudaMemcpyPeerAsync device 0 -> 1\n" : "gpu_gpu: same-device copy (one GPU visible)\n") +
-      "cpu_cpu: pinned host memcpy; d2h/h2d: cudaMemcpyAsync pinned";
+      "cpu_cpu: pinned host memcpy; d2h/h2d: cudaMemcpyAsync pinned\n" +
+      "gpu_direct: synchronous sp_copy probe layout -> same layout, same GPU (the DIRECT method, B200 extension)" +
+      (peer ? "\ngpu_direct_peer: the same copy into device 1 over NVLink" : "");
   int64_t len = 0;
   CK(sp_profile_save(prof, header.c_str(), nullptr, 0, &len));
   std::string text(static_cast<size_t>(len) + 1, '\0');
@@ -137,14 +172,14 @@ inline int measure_profile(const char *out_path, int reps, bool report) {
   std::fclose(f);
   if (!report) return 0;
   const int64_t q[][2] = {{1 << 10, 16}, {1 << 16, 8}, {1 << 20, 64}, {4 << 20, 16}, {64 << 20, 4096}};
+  const char *names[4] = {"oneshot", "device", "staged", "direct"};
   for (auto &qq : q) {
-    int m = -1;
-    double td, to, ts;
+    int m = -1, m4 = -1;
+    double t4[4];
     CK(sp_choose_method(prof, qq[0], qq[1], &m));
-    CK(sp_model_times(prof, qq[0], qq[1], &td, &to, &ts));
-    std::printf("object %lld block %lld -> %s  device %.3e oneshot %.3e staged %.3e\n", (long long)qq[0],
-                (long long)qq[1], m == SP_METHOD_DEVICE ? "device" : m == SP_METHOD_ONESHOT ? "oneshot" : "staged",
-                td, to, ts);
+    CK(sp_choose_method_b200(prof, qq[0], qq[1], 1, &m4, t4));
+    std::printf("object %lld block %lld -> %s (b200, same GPU: %s)  device %.3e oneshot %.3e staged %.3e direct %.3e\n",
+                (long long)qq[0], (long long)qq[1], names[m], names[m4], t4[0], t4[1], t4[2], t4[3]);
   }
   return 0;
 }
