@@ -363,6 +363,7 @@ def build_line(args, value, step_ms, world, K, dominant, sweep, e2e_val, Ke, lau
                        f"(the engine stages each message over PCIe: H2D + unpack kernel, pack kernel + "
                        f"D2H); incount={Ke} per E0 message, one stream per E0 so transfers and kernels of "
                        f"different messages overlap",
+                "issue_order": os.environ.get("BENCH_E2E_ORDER", "descending") + " E0",
                 "pcie_bound_ms": round(pcie_ms, 3) if pcie_ms else None,
                 "pcie_bound_note": "the same H2D and D2H bytes as plain pinned copies on two streams at once; "
                                    "e2e ms / this = how far the leg is from the link"},
@@ -632,7 +633,16 @@ def run_ours(args):
     streams = [torch.cuda.Stream() for _ in range(NS)]
     handles = [C.c_void_p(st.cuda_stream) for st in streams]
     items = []  # (type, strided object address, E0 index)
-    for i in sorted(range(len(types)), key=lambda i: -types[i][0]):
+    # issue order of the E0 messages (BENCH_E2E_ORDER): the slow small-E0
+    # kernels want to start early, while later messages' copies keep the
+    # PCIe engines busy
+    order = os.environ.get("BENCH_E2E_ORDER", "descending")
+    idx = sorted(range(len(types)), key=lambda i: types[i][0])
+    if order == "descending":
+        idx = idx[::-1]
+    elif order == "interleaved":  # 1, 512, 2, 256, ...
+        idx = [idx[j // 2] if j % 2 == 0 else idx[-1 - j // 2] for j in range(len(idx))]
+    for i in idx:
         e0, d, ct = types[i]
         items.append((ct, esrc.data_ptr() + xoff[e0], i))
     e2e_t = 0.0

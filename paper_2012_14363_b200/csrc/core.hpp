@@ -18,6 +18,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <cuda_runtime_api.h>
+
 #include "stridepack_b200.h"
 
 namespace spb {
@@ -198,6 +200,9 @@ const DeviceRuns &device_run_table(const Committed &ct);
 void set_last_launch(const sp_launch_info &li);
 void cuda_check(int err, const char *what);  // cudaError_t as int
 void require_device();
+// the engine's stream-ordered memory pool on the current device (scratch and
+// staging buffers; memory stays mapped between uses)
+cudaMemPool_t engine_pool();
 // Copy `n` bytes (any direction, pageable or device source) and return only
 // when they have landed in `dst`. A plain cudaMemcpy is not enough: from
 // pageable host memory it may return before the DMA completes, device to

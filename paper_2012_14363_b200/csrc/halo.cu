@@ -185,7 +185,7 @@ int64_t halo_verify(const HaloCfg &c, int64_t rank, const void *alloc, void *str
   const int64_t cells = g.pad[0] * g.pad[1] * g.pad[2];
   unsigned long long *d_bad = nullptr, h_bad = 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&d_bad), sizeof(*d_bad), s), "cudaMallocAsync");
+  cuda_check(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&d_bad), sizeof(*d_bad), engine_pool(), s), "cudaMallocAsync");
   cuda_check(cudaMemsetAsync(d_bad, 0, sizeof(*d_bad), s), "cudaMemsetAsync");
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>((cells + 255) / 256, 148 * 16));
   k_halo_verify<<<grid, 256, 0, s>>>(static_cast<const uint8_t *>(alloc), g, d_bad);

@@ -70,6 +70,30 @@ void copy_sync(void *dst, const void *src, size_t n, const char *what) {
   cuda_check(cudaStreamSynchronize(st), what);
 }
 
+cudaMemPool_t engine_pool() {
+  // one pool per device for the engine's stream-ordered scratch (staging
+  // buffers, STAGED transfers): its release threshold keeps the memory
+  // mapped across synchronisations. The default pool returns it to the
+  // driver at every sync, so a 64 MiB STAGED message re-mapped its scratch
+  // each time (0.3-10 ms of variance per message).
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(mu);
+  cudaMemPool_t &p = pools[dev & 63];
+  if (!p) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cuda_check(cudaMemPoolCreate(&p, &props), "cudaMemPoolCreate");
+    uint64_t keep = uint64_t{4} << 30; // up to 4 GiB stays mapped between uses
+    cuda_check(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep), "cudaMemPoolSetAttribute");
+  }
+  return p;
+}
+
 void require_device() {
   int n = 0;
   const cudaError_t e = cudaGetDeviceCount(&n);
@@ -568,7 +592,7 @@ uint8_t *stage_buffer(cudaStream_t s, size_t bytes) {
   if (st.n < bytes + kStagePad) {
     if (st.p) cuda_check(cudaFreeAsync(st.p, s), "cudaFreeAsync(stage)");
     const size_t n = std::max(bytes + kStagePad, st.n * 2);
-    cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&st.p), n, s), "cudaMallocAsync(stage)");
+    cuda_check(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&st.p), n, engine_pool(), s), "cudaMallocAsync(stage)");
     st.n = n;
   }
   return st.p;
@@ -906,7 +930,7 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
     if (rd.c0 / w >= (int64_t{1} << 32)) fail(SP_ERR_UNSUPPORTED, "row longer than 64 GiB words");
     g.total = total_bytes / static_cast<uint64_t>(w);
     uint64_t *cnt64 = nullptr;
-    cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&cnt64), KMAX * sizeof(uint64_t), s), "cudaMallocAsync");
+    cuda_check(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&cnt64), KMAX * sizeof(uint64_t), engine_pool(), s), "cudaMallocAsync");
     uint64_t hc[KMAX] = {0};
     for (int k = 0; k < g.nd; ++k) hc[k] = static_cast<uint64_t>(rd.cnt[k]);
     cuda_check(cudaMemcpyAsync(cnt64, hc, sizeof(hc), cudaMemcpyHostToDevice, s), "cudaMemcpyAsync");
@@ -1005,7 +1029,7 @@ int64_t execute(const PackArgs &a) {
     staged = must_sync = true;
     // + kStagePad: the shift kernels read whole aligned 16-B blocks around
     // the bytes a layout touches, which may run past an exact-size end
-    cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&scratch_s), static_cast<size_t>(strided_len) + kStagePad, s),
+    cuda_check(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&scratch_s), static_cast<size_t>(strided_len) + kStagePad, engine_pool(), s),
                "cudaMallocAsync(stage)");
     // pack reads the span; unpack must preserve bytes outside the layout
     cuda_check(cudaMemcpyAsync(scratch_s, strided_user, static_cast<size_t>(strided_len), cudaMemcpyHostToDevice, s),
@@ -1014,7 +1038,7 @@ int64_t execute(const PackArgs &a) {
   }
   if (rp.kind == MemKind::Pageable) {
     staged = must_sync = true;
-    cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&scratch_p), static_cast<size_t>(packed_len) + kStagePad, s),
+    cuda_check(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&scratch_p), static_cast<size_t>(packed_len) + kStagePad, engine_pool(), s),
                "cudaMallocAsync(stage)");
     if (!a.pack)
       cuda_check(cudaMemcpyAsync(scratch_p, static_cast<const uint8_t *>(a.src) + a.position,

@@ -755,7 +755,7 @@ void send_stream(Req &q) {
     } else if (q.method == SP_METHOD_ONESHOT) {
       dst = peer_host(q.peer) + q.grant;
     } else {
-      cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&q.scratch), static_cast<size_t>(q.bytes), s),
+      cuda_check(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&q.scratch), static_cast<size_t>(q.bytes), engine_pool(), s),
                  "cudaMallocAsync(staged)");
       dst = q.scratch;
     }
@@ -967,7 +967,7 @@ bool step_recv(Req &q) {
     }
     q.grant = grant;
     if (q.method == SP_METHOD_STAGED && q.bytes > 0)
-      cuda_check(cudaMallocAsync(reinterpret_cast<void **>(&q.rbuf_stage), static_cast<size_t>(q.bytes), s),
+      cuda_check(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&q.rbuf_stage), static_cast<size_t>(q.bytes), engine_pool(), s),
                  "cudaMallocAsync(staged)");
     const uint8_t *packed = q.method == SP_METHOD_DEVICE   ? R.window + grant
                             : q.method == SP_METHOD_STAGED ? q.rbuf_stage

@@ -25,7 +25,80 @@ if ROOT not in sys.path:
 
 GRIDS = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2), 3: (3, 1, 1), 6: (3, 2, 1)}
 NVLINK_GBPS = 900.0          # per direction per GPU, nominal
-NVLINK_MEASURED_GBPS = 770.0  # peer copy per direction (B200_PROFILING.md)
+NVLINK_FALLBACK_GBPS = 770.0  # B200_PROFILING.md's peer-copy figure: used only when no peer GPU is visible
+
+
+def nvlink_peak(torch, local, peer, nbytes=256 << 20, reps=10):
+    """one-way NVLink bandwidth measured in this run: cudaMemcpyPeerAsync
+    (torch's cross-device copy) of `nbytes` from device `local` to device
+    `peer`, CUDA events on the copying stream, best of `reps`. Also enables
+    peer access between the two devices for this process."""
+    src = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{local}")
+    dst = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{peer}")
+    s = torch.cuda.current_stream(local)
+    best = None
+    for i in range(reps + 2):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        dst.copy_(src, non_blocking=True)
+        b.record(s)
+        b.synchronize()
+        if i >= 2:
+            t = a.elapsed_time(b) * 1e-3
+            best = t if best is None else min(best, t)
+    del src, dst
+    return nbytes / best / 1e9
+
+
+def calibrate_peer(torch, prof, local, peer, reps=5):
+    """Measure, on THIS box, the two model terms that involve a peer GPU and
+    put them into `prof` (a MachineProfile): the gpu_gpu curve (a plain
+    cudaMemcpyPeerAsync of n bytes) and the gpu_direct_peer surface (one
+    typed copy of the profile probe hvector(o/b,1,2b,contiguous(b)) from this
+    GPU into the same layout on the peer, the DIRECT method). Same grids and
+    timing rule as tools/measure_profile: median wall time of synchronous
+    calls."""
+    import time
+    import paper_2012_14363_b200 as sp
+    objects = [1 << k for k in range(10, 27, 2)]
+    blocks = [1, 4, 16, 64, 256, 1024, 4096]
+    big = objects[-1]
+    src = torch.zeros(2 * big, dtype=torch.uint8, device=f"cuda:{local}")
+    dst = torch.zeros(2 * big, dtype=torch.uint8, device=f"cuda:{peer}")
+    B = sp.make_named(sp.NamedKind.Byte)
+    s = torch.cuda.current_stream(local)
+
+    def med(fn):
+        for _ in range(2):
+            fn()
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts)
+
+    grid = []
+    for o in objects:
+        row = []
+        for b0 in blocks:
+            b = min(b0, o)
+            ct = sp.commit_type(sp.make_hvector(o // b, 1, 2 * b, sp.make_contiguous(b, B)))
+            row.append(med(lambda: sp.copy(src, ct, 1, dst, ct, 1, stream=s, sync=True)))
+        grid.append(row)
+    prof.set_surface("gpu_direct_peer", objects, blocks, grid)
+    sizes = [64 << k for k in range(21)]
+    curve = []
+    for n in sizes:
+        def cp():
+            dst[:n].copy_(src[:n], non_blocking=True)
+            s.synchronize()
+        curve.append(med(cp))
+    prof.set_curve("gpu_gpu", sizes, curve)
+    del src, dst
+    torch.cuda.empty_cache()
+    return {"gpu_direct_peer_1MiB_64B_us": round(grid[objects.index(1 << 20)][blocks.index(64)] * 1e6, 2),
+            "gpu_gpu_64MiB_us": round(curve[-1] * 1e6, 1)}
 
 
 def _hbm_peak():
@@ -62,6 +135,12 @@ def halo_section(torch, rank, world, local, job, iters=20, warmup=5, nccl=True):
         return {"skipped": f"no 3D grid for {world} ranks"}
     cfg = H.HaloConfig(grid, (256, 256, 256), 2, 32)
     regions = H.build_halo_types(cfg)
+    ndev = torch.cuda.device_count()
+    if world > 1 and ndev > 1:
+        nv = nvlink_peak(torch, local, (local + 1) % ndev)
+        nv_src = f"measured in this run: cudaMemcpyPeerAsync cuda:{local} -> cuda:{(local + 1) % ndev}"
+    else:
+        nv, nv_src = NVLINK_FALLBACK_GBPS, "B200_PROFILING.md fallback (no peer GPU visible)"
     pad = 260 ** 3 * 32
     seg = [0]
     for r in regions:
@@ -116,12 +195,13 @@ def halo_section(torch, rank, world, local, job, iters=20, warmup=5, nccl=True):
                                 "(in-kernel completion flags to remote neighbours)"},
            "direct_hbm_GBps_per_rank": round(2 * seg[-1] / phase_direct["iteration"] / 1e9, 1),
            "direct_hbm_frac": round(2 * seg[-1] / phase_direct["iteration"] / 1e9 / _hbm_peak(), 3),
-           "direct_frac_of_nvlink_bound": (round(rbytes / (NVLINK_MEASURED_GBPS * 1e9) / phase_direct["iteration"], 3)
+           "direct_frac_of_nvlink_bound": (round(rbytes / (nv * 1e9) / phase_direct["iteration"], 3)
                                            if rbytes else None),
+           "nvlink_peak_GBps": round(nv, 1), "nvlink_peak_source": nv_src,
            "fused_us": {k: round(v * 1e6, 2) for k, v in phase.items()},
            "fused_hostsync_us": {k: round(v * 1e6, 2) for k, v in phase_sync.items()},
            "fused_hbm_GBps_per_rank": round(4 * seg[-1] / phase["iteration"] / 1e9, 1),
-           "nvlink_bound_us": round(rbytes / (NVLINK_MEASURED_GBPS * 1e9) * 1e6, 2)}
+           "nvlink_bound_us": round(rbytes / (nv * 1e9) * 1e6, 2)}
     # the same exchange through the MPI-level call (MPI_Neighbor_alltoallw
     # with the 26 region types): one typed-copy launch per rank plus the
     # per-call entry protocol and a stream synchronisation; wall time
@@ -209,8 +289,18 @@ def send_section(torch, rank, world, local, job, reps=10, warmup=3):
         return {"skipped": "needs 2 ranks"}
     rt.init(rank, world, job + "s", device=local, window_bytes=72 << 20, host_bytes=72 << 20)
     prof_path = os.path.join(ROOT, "profiles", "b200.profile")
-    if os.path.exists(prof_path):
-        rt.set_profile(M.load_profile_file(prof_path))
+    prof = M.load_profile_file(prof_path) if os.path.exists(prof_path) else None
+    nv, nv_src, calib = NVLINK_FALLBACK_GBPS, "B200_PROFILING.md fallback", None
+    if rank <= 1:
+        other = 1 - rank  # rank r runs on device r (LOCAL_RANK)
+        if torch.cuda.device_count() > 1 and local != other:
+            nv = nvlink_peak(torch, local, other)
+            nv_src = f"measured in this run: cudaMemcpyPeerAsync cuda:{local} -> cuda:{other}"
+            if prof is not None:  # the model's peer terms, measured on this box before the sweep
+                calib = calibrate_peer(torch, prof, local, other)
+    if prof is not None:
+        rt.set_profile(prof)
+    rt.barrier()
     rows = []
     import time
     for e0 in (8, 64, 512):
@@ -237,15 +327,39 @@ def send_section(torch, rank, world, local, job, reps=10, warmup=3):
                         ts.append((time.perf_counter() - t0) / 2)
                 if rank <= 1:
                     row[name + "_us"] = round(statistics.median(ts) * 1e6, 2)
+                    row[name + "_frac_of_nvlink"] = round(ct.size / statistics.median(ts) / 1e9 / nv, 3)
                     row[name + "_GBps"] = round(ct.size / statistics.median(ts) / 1e9, 2)
                     if name == "model":
                         row["model_choice"] = {0: "oneshot", 1: "device", 2: "staged", 3: "direct"}[used]
-                        row["model_frac_of_nvlink"] = round(ct.size / statistics.median(ts) / 1e9 /
-                                                            NVLINK_MEASURED_GBPS, 3)
+                        row["model_frac_of_nvlink"] = round(ct.size / statistics.median(ts) / 1e9 / nv, 3)
             rows.append(row)
     rt.finalize()
+    _model_vs_fastest(rows)
     return {"pair": [0, 1], "timing": "half ping-pong wall time (host-synchronous MPI_Send/Recv semantics)",
-            "nvlink_peak_GBps": NVLINK_MEASURED_GBPS, "rows": rows}
+            "nvlink_peak_GBps": round(nv, 1), "nvlink_peak_source": nv_src,
+            "peer_calibration": calib, "checks": _checks(rows), "rows": rows}
+
+
+def _checks(rows):
+    """the send section's own consistency checks: the model within 10% of
+    the fastest fixed method on every row, and STAGED (device pack + D2H +
+    H2D + unpack) no slower than 1.3x ONE-SHOT at 64 MiB"""
+    big = [r for r in rows if r["bytes"] >= (64 << 20) and "staged_us" in r and "oneshot_us" in r]
+    return {"model_within_10pct_of_fastest": all(r.get("model_vs_fastest", 1.0) <= 1.10 for r in rows),
+            "model_worst_vs_fastest": max((r.get("model_vs_fastest", 1.0) for r in rows), default=None),
+            "staged_le_1.3x_oneshot_at_64MiB": all(r["staged_us"] <= 1.3 * r["oneshot_us"] for r in big),
+            "staged_over_oneshot_at_64MiB": [round(r["staged_us"] / r["oneshot_us"], 3) for r in big]}
+
+
+def _model_vs_fastest(rows):
+    """the model's choice against the fastest fixed method of each row"""
+    for row in rows:
+        fixed = {k[:-3]: v for k, v in row.items() if k.endswith("_us") and k[:-3] in
+                 ("device", "oneshot", "staged", "direct")}
+        if fixed and "model_us" in row:
+            best = min(fixed, key=fixed.get)
+            row["fastest_fixed"] = best
+            row["model_vs_fastest"] = round(row["model_us"] / fixed[best], 3)
 
 
 def send_self_section(torch, rank, local, job, reps=7, warmup=2):
@@ -296,9 +410,10 @@ def send_self_section(torch, rank, local, job, reps=7, warmup=2):
                     row["model_choice"] = names[used]
             rows.append(row)
     rt.finalize()
+    _model_vs_fastest(rows)
     return {"pair": [0, 0], "timing": "wall time of Isend+Irecv+Wait to self, median; device buffers; "
                                       "one GPU (no NVLink): protocol + kernels + HBM/PCIe traffic per method",
-            "rows": rows}
+            "checks": _checks(rows), "rows": rows}
 
 
 if __name__ == "__main__":  # one-rank halo section alone: python tools/bench_parts.py
