@@ -192,7 +192,9 @@ struct Runtime {
   int *err_host = nullptr, *err_dev = nullptr;
   std::string nbr_layout; // bytes of the last published neighbour layout
   std::unique_ptr<sp_model_cache_s, sp_status (*)(sp_model_cache_s *)> cache{nullptr, sp_model_cache_free};
-  sp_profile_s *profile = nullptr;
+  // the model's profile: the runtime holds its own reference (the caller's
+  // sp_profile handle may be freed right after sp_rt_set_profile)
+  std::shared_ptr<const Profile> profile;
   std::map<std::tuple<int64_t, int64_t, int>, bool> direct_cache; // model_prefers_direct answers
   std::mutex mu; // the runtime serialises its own calls (MPI_THREAD_SERIALIZED)
 };
@@ -1204,7 +1206,7 @@ void rt_recv(void *buf, uint64_t buf_bytes, int64_t count, CommitPtr ct, int sou
 
 void rt_set_profile(sp_profile_s *p) {
   Runtime &R = rt();
-  R.profile = p;
+  R.profile = p ? p->p : nullptr;
   R.direct_cache.clear();
   sp_model_cache_s *c = nullptr;
   if (p) {
@@ -1247,7 +1249,7 @@ bool model_prefers_direct(const Committed &ct, int64_t count, int peer_device) {
   const auto key = std::make_tuple(obj, blk, kind);
   auto it = R.direct_cache.find(key);
   if (it != R.direct_cache.end()) return it->second;
-  const bool yes = choose_method_b200(*R.profile->p, obj, blk, kind, nullptr) == SP_METHOD_DIRECT;
+  const bool yes = choose_method_b200(*R.profile, obj, blk, kind, nullptr) == SP_METHOD_DIRECT;
   if (R.direct_cache.size() > 4096) R.direct_cache.clear();
   R.direct_cache.emplace(key, yes);
   return yes;
