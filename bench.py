@@ -642,6 +642,10 @@ def run_ours(args):
         idx = idx[::-1]
     elif order == "interleaved":  # 1, 512, 2, 256, ...
         idx = [idx[j // 2] if j % 2 == 0 else idx[-1 - j // 2] for j in range(len(idx))]
+    elif order == "pipelined":  # 512, 1, 2, 4, ..., 256: the D2H engine starts early,
+        # the slow (small-E0) kernels overlap the later messages' H2D, and
+        # the last message's kernel is short
+        idx = [idx[-1]] + idx[:-1]
     for i in idx:
         e0, d, ct = types[i]
         items.append((ct, esrc.data_ptr() + xoff[e0], i))
