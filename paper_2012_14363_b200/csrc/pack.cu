@@ -598,6 +598,37 @@ uint8_t *stage_buffer(cudaStream_t s, size_t bytes) {
   return st.p;
 }
 
+// A DMA lane beside a caller's stream: a copy stream and a ring of events,
+// so the PCIe leg of a large pinned-host message overlaps its kernels chunk
+// by chunk (H2D of chunk k+1 while chunk k unpacks; D2H of chunk k while
+// chunk k+1 packs). One per (device, caller stream), like the stage buffers.
+constexpr int kLaneEvents = 64;
+constexpr int64_t kDmaChunk = int64_t{8} << 20; // packed bytes per pipelined chunk
+struct DmaLane {
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev[kLaneEvents] = {};
+  int next = 0;
+  cudaEvent_t take() {
+    cudaEvent_t e = ev[next];
+    next = (next + 1) % kLaneEvents;
+    return e;
+  }
+};
+
+DmaLane &dma_lane(cudaStream_t s) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, DmaLane> lanes;
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(mu);
+  DmaLane &l = lanes[{dev, s}];
+  if (!l.cs) {
+    cuda_check(cudaStreamCreateWithFlags(&l.cs, cudaStreamNonBlocking), "cudaStreamCreate(dma lane)");
+    for (cudaEvent_t &e : l.ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+  }
+  return l;
+}
+
 unsigned grid_for(uint64_t items, int per_thread) {
   const uint64_t blocks = (items + 256ull * per_thread - 1) / (256ull * per_thread);
   uint64_t cap = static_cast<uint64_t>(sm_count()) * 8; // 8 x 256 = 2048 threads/SM
@@ -1019,11 +1050,7 @@ int64_t execute(const PackArgs &a) {
   if (dma_packed) {
     staged = true;
     dma_stage = scratch_p = stage_buffer(s, static_cast<size_t>(packed_len));
-    if (!a.pack)
-      cuda_check(cudaMemcpyAsync(scratch_p, static_cast<const uint8_t *>(a.src) + a.position,
-                                 static_cast<size_t>(packed_len), cudaMemcpyHostToDevice, s),
-                 "dma packed H2D");
-    packed_dev = scratch_p;
+    packed_dev = scratch_p; // the H2D of an unpack is issued below (whole, or chunked)
   }
   if (rs.kind == MemKind::Pageable) {
     staged = must_sync = true;
@@ -1046,6 +1073,54 @@ int64_t execute(const PackArgs &a) {
                  "stage packed H2D");
     packed_dev = scratch_p;
   }
+  // a large pinned message of several objects: pipeline the DMA against
+  // the kernels in chunks of whole objects on a copy lane beside `s`
+  const int64_t per_chunk = std::max<int64_t>(1, kDmaChunk / std::max<int64_t>(ct.size, 1));
+  const bool pipelined = dma_packed && rs.kind != MemKind::Pageable && a.count >= 2 && per_chunk < a.count;
+  if (pipelined) {
+    DmaLane &lane = dma_lane(s);
+    const uint8_t *host_in = static_cast<const uint8_t *>(a.src) + a.position;
+    uint8_t *host_out = static_cast<uint8_t *>(a.dst) + a.position;
+    // the lane's first copy waits for everything earlier on `s` (the stage
+    // buffer may still be read or written by the previous call)
+    cudaEvent_t e0 = lane.take();
+    cuda_check(cudaEventRecord(e0, s), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(lane.cs, e0, 0), "cudaStreamWaitEvent");
+    int launches = 0;
+    for (int64_t o = 0; o < a.count; o += per_chunk) {
+      const int64_t c = std::min(per_chunk, a.count - o);
+      const size_t off = static_cast<size_t>(o * ct.size), n = static_cast<size_t>(c * ct.size);
+      uint8_t *sd = strided_dev + o * ct.extent;
+      cudaEvent_t e = lane.take();
+      if (a.pack) {
+        launch(ct, c, sd, nullptr, nullptr, packed_dev + off, true, s, a.opt, li);
+        cuda_check(cudaEventRecord(e, s), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(lane.cs, e, 0), "cudaStreamWaitEvent");
+        cuda_check(cudaMemcpyAsync(host_out + off, packed_dev + off, n, cudaMemcpyDeviceToHost, lane.cs),
+                   "dma packed D2H");
+      } else {
+        cuda_check(cudaMemcpyAsync(packed_dev + off, host_in + off, n, cudaMemcpyHostToDevice, lane.cs),
+                   "dma packed H2D");
+        cuda_check(cudaEventRecord(e, lane.cs), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(s, e, 0), "cudaStreamWaitEvent");
+        launch(ct, c, nullptr, sd, packed_dev + off, nullptr, false, s, a.opt, li);
+      }
+      ++launches;
+    }
+    if (a.pack) { // the call completes on `s` when the last D2H has landed
+      cudaEvent_t e = lane.take();
+      cuda_check(cudaEventRecord(e, lane.cs), "cudaEventRecord");
+      cuda_check(cudaStreamWaitEvent(s, e, 0), "cudaStreamWaitEvent");
+    }
+    li.launches = launches;
+    li.staged = true;
+    set_last_launch(li);
+    return a.position + packed_len;
+  }
+  if (dma_packed && !a.pack)
+    cuda_check(cudaMemcpyAsync(scratch_p, static_cast<const uint8_t *>(a.src) + a.position,
+                               static_cast<size_t>(packed_len), cudaMemcpyHostToDevice, s),
+               "dma packed H2D");
   if (a.pack) {
     launch(ct, a.count, strided_dev, nullptr, nullptr, packed_dev, true, s, a.opt, li);
   } else {

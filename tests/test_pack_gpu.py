@@ -360,6 +360,42 @@ def test_pinned_host_oneshot_and_pageable_staged(sp, orc, cuda):
     assert np.array_equal(hb, exp)
 
 
+def test_pinned_message_pipelined_dma(sp, orc, cuda):
+    """a pinned-host packed message of many objects moves by chunked DMA
+    (H2D of chunk k+1 overlapping the unpack of chunk k, D2H of chunk k the
+    pack of chunk k+1, on a copy lane beside the caller's stream): bytes
+    equal the oracle's at a nonzero position, and the call is complete on
+    the caller's stream"""
+    torch = cuda
+    prog = [4, 3, 0, 256, 64, 32, 64, 32, 16, 8, 4, 2, 0, 0]  # 32 KiB objects, 512 KiB extent
+    ct = sp.commit_type(sp.from_program(prog))
+    n, pos = 300, 48  # 9.4 MiB packed: two 8 MiB chunks of whole objects
+    span = (n - 1) * ct.extent + ct.span
+    rng = np.random.default_rng(77)
+    host = rng.integers(0, 256, span, dtype=np.uint8)
+    want = np.zeros(pos + n * ct.size, np.uint8)
+    assert orc.pack(prog, host, n, want, pos)[0] == 0
+    s = torch.cuda.Stream()
+    msg = torch.zeros(pos + n * ct.size, dtype=torch.uint8).pin_memory()
+    src = dev(torch, host)
+    torch.cuda.synchronize()
+    assert sp.pack(src, ct, n, msg, pos, stream=s) == pos + n * ct.size
+    li = sp.last_launch()
+    s.synchronize()  # the caller's stream alone covers the whole call
+    assert li.staged and li.launches == 2
+    assert np.array_equal(msg.numpy(), want)
+    init = rng.integers(0, 256, span, dtype=np.uint8)
+    out = dev(torch, init)
+    inmsg = torch.from_numpy(want.copy()).pin_memory()
+    torch.cuda.synchronize()
+    sp.unpack(inmsg, pos, ct, n, out, stream=s)
+    s.synchronize()
+    assert sp.last_launch().launches == 2
+    exp = init.copy()
+    assert orc.unpack(prog, want, pos, n, exp)[0] == 0
+    assert np.array_equal(out.cpu().numpy(), exp)
+
+
 # ------------------------------------------------------------ BASELINE configs
 def cfg2_prog(e0):
     e2 = 2 ** math.ceil(math.log2((1 << 20) // e0) / 2)
