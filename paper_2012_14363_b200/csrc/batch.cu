@@ -52,15 +52,16 @@ struct BatchJob {
 
 // Optional in-kernel completion protocol (distributed halo): every block
 // first waits until each `wait` flag (local memory, written by peers over
-// NVLink) reaches wait_value; after the last word, the LAST block to finish
-// publishes signal_value to each `signal` flag (peer memory) with a
-// system-scope release store, after fences by every block.
+// NVLink) reaches wait_value; after its last word, EVERY block adds its share
+// of 2^32 to each `signal` counter (peer memory) with a release reduction --
+// the shares of a launch sum to exactly 2^32 whatever the grid, so a
+// receiver waits for calls << 32 without knowing the sender's grid, and no
+// block waits for another to finish before signalling.
 constexpr int kMaxSig = kMaxSignalPeers;
 struct BatchSig {
   const unsigned long long *wait[kMaxSig];
   unsigned long long *signal[kMaxSig];
-  unsigned long long wait_value, signal_value;
-  unsigned *done; // block-completion counter of this launch (device memory)
+  unsigned long long wait_value;
   int n_wait, n_signal;
   int sys_scope;  // some destination lives on another GPU: system-scope fences
   // published by block 0 BEFORE waiting (consumer-side "ready" flags: the
@@ -68,14 +69,14 @@ struct BatchSig {
   unsigned long long *pre[kMaxSig];
   unsigned long long pre_value;
   int n_pre;
-  // waited for by the LAST block after it signalled (completion of the
-  // peers' writes into this rank's memory folded into the same launch)
+  // waited for by block 0 after it signalled (completion of the peers'
+  // writes into this rank's memory folded into the same launch)
   const unsigned long long *post[kMaxSig];
   unsigned long long post_value;
   int n_post;
-  // per-target values (neighbour collectives count calls per peer pair);
-  // used instead of signal_value / post_value when per_target is set
-  unsigned long long signal_vals[kMaxSig], post_vals[kMaxSig];
+  // per-target post values (neighbour collectives count calls per peer
+  // pair); used instead of post_value when per_target is set
+  unsigned long long post_vals[kMaxSig];
   int per_target;
   // bounded waits: a spin that outlives timeout_ns sets *err and gives up
   // (the host reports SP_ERR_TIMEOUT after its next synchronisation)
@@ -91,6 +92,16 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 
 __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// release reduction: the CTA's stores (ordered before this thread by the
+// preceding bar.sync) become visible to whoever acquires the counter
+__device__ __forceinline__ void red_release_add(unsigned long long *p, unsigned long long v, int sys) {
+  if (sys) {
+    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  } else {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  }
 }
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -161,36 +172,27 @@ __device__ __forceinline__ void batch_prologue(const BatchSig &sig) {
   }
 }
 
+// Per-CTA completion: bar.sync orders every thread's stores before the
+// signalling threads, whose release reductions are cumulative over them (GPU
+// scope when every destination is on this device, system scope when some
+// were written over NVLink into a peer GPU). Block b adds
+// floor((b+1)2^32/G) - floor(b 2^32/G), so one launch adds exactly 2^32 to
+// each counter. Block 0 then waits for the post counters: the launch ends
+// only when the peers' writes into this rank have landed. No last-block
+// election, no serialised completion atomic, no system fence chain.
 __device__ __forceinline__ void batch_epilogue(const BatchSig &sig) {
   if (sig.n_signal || sig.n_post) {
-    // bar.sync orders every thread's stores before thread 0 (CTA scope);
-    // thread 0's fence is cumulative over them: GPU scope when every
-    // destination is on this device, system scope when some were written
-    // over NVLink into a peer GPU
     __syncthreads();
-    if (threadIdx.x == 0) {
-      if (sig.sys_scope) {
-        __threadfence_system();
-      } else {
-        __threadfence();
-      }
+    if (threadIdx.x < static_cast<unsigned>(sig.n_signal)) {
+      const unsigned long long g = gridDim.x, b = blockIdx.x;
+      const unsigned long long share = ((b + 1) << 32) / g - (b << 32) / g;
+      red_release_add(sig.signal[threadIdx.x], share, sig.sys_scope);
     }
-    __shared__ int last;
-    if (threadIdx.x == 0) last = atomicAdd(sig.done, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (last) {
-      if (threadIdx.x == 0) {
-        __threadfence_system();
-        for (int i = 0; i < sig.n_signal; ++i)
-          st_release_sys(sig.signal[i], sig.per_target ? sig.signal_vals[i] : sig.signal_value);
-        atomicExch(sig.done, 0u); // ready for the next launch on this stream
-      }
-      // every other block of this launch has finished, so waiting here
-      // cannot starve them; the peers publish before they wait, so the
-      // ranks' last blocks cannot wait on each other in a cycle
-      if (threadIdx.x < static_cast<unsigned>(sig.n_post))
-        wait_flag(sig.post[threadIdx.x], sig.per_target ? sig.post_vals[threadIdx.x] : sig.post_value, sig, 32);
-    }
+    // every peer signals before it waits, so block 0 of two ranks cannot
+    // wait on each other in a cycle; the grid is one resident wave, so the
+    // other blocks run to completion meanwhile
+    if (blockIdx.x == 0 && threadIdx.x < static_cast<unsigned>(sig.n_post))
+      wait_flag(sig.post[threadIdx.x], sig.per_target ? sig.post_vals[threadIdx.x] : sig.post_value, sig, 32);
   }
 }
 
@@ -594,18 +596,15 @@ void batch_launch(const Batch &b, void *stream, const BatchSignal *bs) {
       if (gi + 1 == b.groups.size()) {
         sig.n_signal = static_cast<int>(bs->signal.size());
         for (int i = 0; i < sig.n_signal; ++i) sig.signal[i] = reinterpret_cast<unsigned long long *>(bs->signal[i]);
-        sig.signal_value = bs->signal_value;
-        sig.done = bs->done;
         sig.sys_scope = bs->sys_scope ? 1 : 0;
         if (bs->post.size() > static_cast<size_t>(kMaxSig)) fail(SP_ERR_UNSUPPORTED, "batch signalling: more than 32 peers");
         sig.n_post = static_cast<int>(bs->post.size());
         for (int i = 0; i < sig.n_post; ++i) sig.post[i] = reinterpret_cast<const unsigned long long *>(bs->post[i]);
         sig.post_value = bs->post_value;
-        if (!bs->signal_values.empty() || !bs->post_values.empty()) {
-          if (bs->signal_values.size() != bs->signal.size() || bs->post_values.size() != bs->post.size())
+        if (!bs->post_values.empty()) {
+          if (bs->post_values.size() != bs->post.size())
             fail(SP_ERR_INTERNAL, "batch signalling: per-target values do not match the targets");
           sig.per_target = 1;
-          for (int i = 0; i < sig.n_signal; ++i) sig.signal_vals[i] = bs->signal_values[i];
           for (int i = 0; i < sig.n_post; ++i) sig.post_vals[i] = bs->post_values[i];
         }
       }
@@ -713,14 +712,11 @@ void copy_execute(const CopySpec &spec, uint64_t lo, uint64_t hi, void *stream) 
   launch_range(kModeCopy, w, j, total, lo, hi, static_cast<cudaStream_t>(stream));
 }
 
-// one warp: release-store each signal, then wait for each post flag; the
-// completion protocol of a neighbour call that moves no bytes
+// one warp: add a whole launch's 2^32 to each signal counter, then wait for
+// each post counter; the completion protocol of a neighbour call that moves
+// no bytes
 __global__ void k_flag_signal_wait(const BatchSig sig) {
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    for (int i = 0; i < sig.n_signal; ++i)
-      st_release_sys(sig.signal[i], sig.per_target ? sig.signal_vals[i] : sig.signal_value);
-  }
+  if (threadIdx.x < static_cast<unsigned>(sig.n_signal)) red_release_add(sig.signal[threadIdx.x], 1ull << 32, 1);
   if (threadIdx.x < static_cast<unsigned>(sig.n_post))
     wait_flag(sig.post[threadIdx.x], sig.per_target ? sig.post_vals[threadIdx.x] : sig.post_value, sig, 32);
 }
@@ -736,11 +732,9 @@ void flags_signal_wait(const BatchSignal &bs, void *stream) {
   sig.n_post = static_cast<int>(bs.post.size());
   for (int i = 0; i < sig.n_signal; ++i) sig.signal[i] = reinterpret_cast<unsigned long long *>(bs.signal[i]);
   for (int i = 0; i < sig.n_post; ++i) sig.post[i] = reinterpret_cast<const unsigned long long *>(bs.post[i]);
-  sig.signal_value = bs.signal_value;
   sig.post_value = bs.post_value;
-  if (!bs.signal_values.empty() || !bs.post_values.empty()) {
+  if (!bs.post_values.empty()) {
     sig.per_target = 1;
-    for (int i = 0; i < sig.n_signal; ++i) sig.signal_vals[i] = bs.signal_values[i];
     for (int i = 0; i < sig.n_post; ++i) sig.post_vals[i] = bs.post_values[i];
   }
   k_flag_signal_wait<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(sig);

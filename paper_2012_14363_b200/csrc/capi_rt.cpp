@@ -65,7 +65,6 @@ struct sp_halo_plan_s {
   std::vector<uint8_t *> peer_flags;
   std::vector<int> out_peers, in_peers; // distinct neighbours
   uint64_t iter = 0;
-  unsigned *done = nullptr; // block-completion counters of the pack / unpack launches
   bool remote_peers = true; // some neighbour's memory is on another GPU
   ~sp_halo_plan_s() {
     batch_destroy(pack);
@@ -75,7 +74,6 @@ struct sp_halo_plan_s {
     if (recv) cudaFree(recv);
     if (send) cudaFree(send);
     if (flags) cudaFree(flags);
-    if (done) cudaFree(done);
   }
 };
 
@@ -363,8 +361,6 @@ sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int metho
       const int n = rt_size();
       cuda_check(cudaMalloc(&p->flags, 2 * n * sizeof(uint64_t)), "cudaMalloc(flags)");
       cuda_check(cudaMemset(p->flags, 0, 2 * n * sizeof(uint64_t)), "cudaMemset(flags)");
-      cuda_check(cudaMalloc(&p->done, 2 * sizeof(unsigned)), "cudaMalloc(done)");
-      cuda_check(cudaMemset(p->done, 0, 2 * sizeof(unsigned)), "cudaMemset(done)");
       cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
       rt_exchange_ptr(p->flags, p->peer_flags);
       int mydev = 0;
@@ -381,7 +377,9 @@ sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int metho
       // complete when it ends -- so a 1x1x1 grid runs with no protocol and
       // the periodic self-neighbours of a 2x1x1 / 2x2x1 grid drop out
       std::vector<char> seen_out(n, 0), seen_in(n, 0);
-      seen_out[p->rank] = seen_in[p->rank] = 1;
+      // SPB_HALO_SELF_FLAGS keeps the self edges in the protocol: a one-GPU
+      // measurement of what the flags cost (scripts/protocol_cost.py)
+      if (!std::getenv("SPB_HALO_SELF_FLAGS")) seen_out[p->rank] = seen_in[p->rank] = 1;
       for (int j = 0; j < 26; ++j) {
         const int64_t nb = halo_rank_of(c, p->rank, regions[j].dir);
         if (!seen_out[nb]) {
@@ -411,10 +409,10 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
       // senders that the ghosts of iteration n-1 are consumed (FREE=n-1;
       // everything earlier on the stream has completed), every block waits
       // for FREE=n-1 from its receivers, the regions are stored into the
-      // receivers' ghost cells over NVLink, and the last block publishes
-      // READY=n to each receiver and then waits for READY=n from this
-      // rank's senders, so later work on the stream sees whole ghost
-      // shells.
+      // receivers' ghost cells over NVLink, every block adds its share of
+      // READY=n to each receiver once its stores are done, and block 0 then
+      // waits for READY=n from this rank's senders, so later work on the
+      // stream sees whole ghost shells.
       const int n = rt_size(), me = p->rank;
       const uint64_t it = ++p->iter;
       auto at = [&](uint8_t *base, int kind, int peer) {
@@ -433,14 +431,12 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
         ks.signal.push_back(at(p->peer_flags[q], kReady, me));
       }
       ks.wait_value = it - 1;
-      ks.signal_value = it;
-      ks.done = p->done;
       ks.sys_scope = p->remote_peers;
-      // the last block, after publishing READY=n, waits for READY=n from
+      // block 0, after adding its share of READY=n, waits for READY=n from
       // this rank's senders: the launch completes only when the ghost shell
       // is whole, so no separate wait kernel
       ks.post = ready;
-      ks.post_value = it;
+      ks.post_value = it << 32; // READY counts 2^32 per sender launch
       ks.err = rt_device_err();
       ks.timeout_ns = rt_device_timeout_ns();
       cuda_check(cudaEventRecord(p->ev[0], s), "cudaEventRecord");
@@ -450,7 +446,7 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
       // device-ordered iteration, signalled from inside the kernels: the
       // pack batch waits (in every block) until each receiver has consumed
       // iteration n-1, stores the segments into the receivers' HBM, and its
-      // last block release-stores READY=n into each receiver's flags; the
+      // blocks add their shares of READY=n to each receiver's counter; the
       // unpack batch waits for READY=n from each sender and releases FREE=n
       // back. No host barrier, no stream memory op, no host round trip.
       const int n = rt_size(), me = p->rank;
@@ -464,16 +460,12 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
         ps.wait.push_back(at(mine, kFree, q));
         ps.signal.push_back(at(p->peer_flags[q], kReady, me));
       }
-      ps.wait_value = it - 1;
-      ps.signal_value = it;
-      ps.done = p->done;
+      ps.wait_value = (it - 1) << 32; // FREE and READY count 2^32 per launch
       for (int q : p->in_peers) {
         us.wait.push_back(at(mine, kReady, q));
         us.signal.push_back(at(p->peer_flags[q], kFree, me));
       }
-      us.wait_value = it;
-      us.signal_value = it;
-      us.done = p->done + 1;
+      us.wait_value = it << 32;
       ps.sys_scope = us.sys_scope = p->remote_peers;
       ps.err = us.err = rt_device_err();
       ps.timeout_ns = us.timeout_ns = rt_device_timeout_ns();

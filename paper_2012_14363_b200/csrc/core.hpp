@@ -248,20 +248,18 @@ void batch_destroy(Batch *b);
 struct BatchSignal {
   std::vector<const uint64_t *> wait; // local flags, each must reach wait_value
   uint64_t wait_value = 0;
-  std::vector<uint64_t *> signal;     // (peer) flags set to signal_value at the end
-  uint64_t signal_value = 0;
-  unsigned *done = nullptr;           // device counter, zero-initialised, one per stream
+  std::vector<uint64_t *> signal;     // (peer) counters: every launch adds 2^32 in total
   bool sys_scope = true;              // a destination is on another GPU
   std::vector<uint64_t *> pre;        // (peer) flags set to pre_value BEFORE the wait
   uint64_t pre_value = 0;
-  std::vector<const uint64_t *> post; // local flags the last block waits for after signalling
+  std::vector<const uint64_t *> post; // local counters block 0 waits for after signalling
   uint64_t post_value = 0;
-  std::vector<uint64_t> signal_values, post_values; // per-target values (else the scalars)
+  std::vector<uint64_t> post_values;  // per-target post values (else the scalar)
   int *err = nullptr;      // set to 1 by an in-kernel wait that gave up (mapped host memory)
   uint64_t timeout_ns = 0; // in-kernel wait limit, 0 = unbounded
 };
 constexpr int kMaxSignalPeers = 32; // flags a signalled launch carries (batch.cu kMaxSig)
-// one-warp kernel: release-stores the signals, then waits for the post flags
+// one-warp kernel: adds 2^32 to each signal counter, then waits for the post counters
 void flags_signal_wait(const BatchSignal &sig, void *stream);
 void batch_execute_signaled(const Batch &b, void *stream, const BatchSignal &sig);
 int64_t batch_bytes(const Batch &b);

@@ -185,7 +185,6 @@ struct Runtime {
   uint64_t *nbr_flags = nullptr;
   std::vector<uint8_t *> peer_nbr_flags;
   std::vector<uint64_t> pair_sent, pair_recv;
-  unsigned *nbr_done = nullptr;
   bool nbr_remote = false;
   // set (to 1) by an in-kernel flag wait that gave up after TEMPI_TIMEOUT;
   // mapped pinned memory, read by the host after each synchronisation
@@ -412,8 +411,6 @@ void rt_init(int rank, int size, const char *name, int device, int64_t window_by
   if (device >= 0) {
     cuda_check(cudaMalloc(&G.nbr_flags, kMaxRanks * sizeof(uint64_t)), "cudaMalloc(nbr flags)");
     cuda_check(cudaMemset(G.nbr_flags, 0, kMaxRanks * sizeof(uint64_t)), "cudaMemset(nbr flags)");
-    cuda_check(cudaMalloc(&G.nbr_done, sizeof(unsigned)), "cudaMalloc(nbr done)");
-    cuda_check(cudaMemset(G.nbr_done, 0, sizeof(unsigned)), "cudaMemset(nbr done)");
     cuda_check(cudaHostAlloc(reinterpret_cast<void **>(&G.err_host), sizeof(int), cudaHostAllocMapped),
                "cudaHostAlloc(device wait error flag)");
     *G.err_host = 0;
@@ -450,7 +447,6 @@ void rt_finalize() {
   rt_barrier();
   if (R.window) cudaFree(R.window);
   if (R.nbr_flags) cudaFree(R.nbr_flags);
-  if (R.nbr_done) cudaFree(R.nbr_done);
   if (R.err_host) cudaFreeHost(R.err_host);
   if (R.host) {
     cudaHostUnregister(R.host);
@@ -1418,7 +1414,7 @@ void append_type_key(std::string &key, const Committed &c) {
 // d, count the call and wait until d has entered it -- d's receive buffer
 // then belongs to the call and its layout is readable. The returned signal
 // set makes the data kernel publish READY to each out-neighbour (value =
-// calls on that pair) and wait, in its last block, for READY from each
+// calls on that pair, 2^32 per launch) and wait, in block 0, for READY from each
 // in-neighbour, so the call is complete when the kernel is: no host
 // barrier before or after. Edges to self need no flags (stream order).
 BatchSignal nbr_enter(const std::vector<int> &sources, const std::vector<int> &dests) {
@@ -1446,7 +1442,7 @@ BatchSignal nbr_enter(const std::vector<int> &sources, const std::vector<int> &d
     seen_s[s] = 1;
     const uint64_t n = ++R.pair_recv[s];
     bs.post.push_back(R.nbr_flags + s);
-    bs.post_values.push_back(n);
+    bs.post_values.push_back(n << 32); // a sender launch adds 2^32
   }
   std::atomic_thread_fence(std::memory_order_release); // layout before the announcement
   for (int s = 0; s < R.size; ++s)
@@ -1457,7 +1453,6 @@ BatchSignal nbr_enter(const std::vector<int> &sources, const std::vector<int> &d
     seen_d[d] = 1;
     const uint64_t n = ++R.pair_sent[d];
     bs.signal.push_back(reinterpret_cast<uint64_t *>(R.peer_nbr_flags[d]) + R.rank);
-    bs.signal_values.push_back(n);
     outs.push_back(d);
   }
   for (int d : outs) {
@@ -1467,7 +1462,6 @@ BatchSignal nbr_enter(const std::vector<int> &sources, const std::vector<int> &d
       w.pause();
     }
   }
-  bs.done = R.nbr_done;
   bs.sys_scope = R.nbr_remote;
   bs.err = R.err_dev;
   bs.timeout_ns = rt_device_timeout_ns();
