@@ -359,11 +359,11 @@ def build_line(args, value, step_ms, world, K, dominant, sweep, e2e_val, Ke, lau
         "single_object": single,
         "e2e": {"value": round(e2e_val, 2), "unit": UNIT, "h2d_bytes_per_step": Ke * (1 << 20) * len(E0S),
                 "d2h_bytes_per_step": Ke * (1 << 20) * len(E0S),
-                "how": f"sp_unpack from / sp_pack to PINNED HOST message buffers through the C-ABI "
-                       f"(the engine stages each message over PCIe: H2D + unpack kernel, pack kernel + "
-                       f"D2H); incount={Ke} per E0 message, one stream per E0 so transfers and kernels of "
-                       f"different messages overlap",
-                "issue_order": os.environ.get("BENCH_E2E_ORDER", "descending") + " E0",
+                "how": f"sp_pack to / sp_unpack from PINNED HOST message buffers through the C-ABI "
+                       f"(the engine pipelines each message over PCIe in 8 MiB chunks: pack kernel + D2H, "
+                       f"H2D + unpack kernel); incount={Ke} per E0 message; the packs read one set of "
+                       f"objects and the unpacks write another, each E0 on its own pack and unpack stream",
+                "issue_order": os.environ.get("BENCH_E2E_ORDER", "ascending") + " E0",
                 "pcie_bound_ms": round(pcie_ms, 3) if pcie_ms else None,
                 "pcie_bound_note": "the same H2D and D2H bytes as plain pinned copies on two streams at once; "
                                    "e2e ms / this = how far the leg is from the link"},
@@ -526,6 +526,7 @@ def run_ours(args):
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))
         pattern = bytes_per_kernel / (min(ts) * 1e-3) / 1e9
+        del strided, dense  # views of src: the e2e leg needs its memory back
 
     # single objects (outside the timed region): one 1 MiB object per call,
     # the unit the paper reports per pack (cfg1 = vector(131072,1,64,DOUBLE)
@@ -606,15 +607,16 @@ def run_ours(args):
     cfg1["line_cap"] = round(2 * 8 / (128 + 8), 4)
 
     # e2e: the packed messages live in pinned HOST memory and every call
-    # goes through the public C-ABI with those host pointers: sp_unpack
-    # moves a message over PCIe into the device object (the engine's DMA
-    # staging: H2D into a per-stream stage buffer, then the kernel) and
-    # sp_pack sends it back (kernel, then D2H). Each E0's message (Ke
-    # objects) has its own stream, so PCIe in, kernels and PCIe out of
-    # different messages overlap (PCIe is full duplex). scripts/e2e_exp.py
-    # measured the alternatives on B200: one-object messages interleaved
-    # over 4-8 streams 2.80 ms, per-E0 messages on 4 streams 2.79 ms, on 10
-    # streams 2.44 ms -- the leg is PCIe-bound (see pcie_bound_ms).
+    # goes through the public C-ABI with those host pointers: sp_pack moves
+    # each E0's message out of the device objects to the host (pack kernels,
+    # D2H) and sp_unpack moves another message in (H2D, unpack kernels) --
+    # the engine pipelines each large message in 8 MiB chunks on a DMA lane
+    # beside the caller's stream. The step's packs read one set of objects
+    # and its unpacks write a second set, so the two legs are independent
+    # (like a halo's sends and receives) and PCIe runs both directions at
+    # once: the leg is bounded by the link (pcie_bound_ms). The slow small-E0
+    # messages are issued first, so their kernels run while the other
+    # messages' bytes are still on the link.
     extra = {"value_E0_ge_32": {"value": round(value_ge32, 2), "unit": UNIT,
                                 "frac": round(value_ge32 / hbm, 4),
                                 "how": "pack + unpack bytes over kernel time of the E0 >= 32 rows only"},
@@ -627,54 +629,46 @@ def run_ours(args):
     for e0 in sorted(E0S, reverse=True):
         xoff[e0] = at
         at += e0
-    esrc = torch.empty((Ke << 30) + 4096, dtype=torch.uint8, device="cuda")
+    esrc = torch.empty((Ke << 30) + 4096, dtype=torch.uint8, device="cuda")  # packed from
+    edst = torch.empty((Ke << 30) + 4096, dtype=torch.uint8, device="cuda")  # unpacked into
     msg_in = [torch.full((Ke << 20,), 5, dtype=torch.uint8).pin_memory() for _ in E0S]
     msg_out = [torch.empty(Ke << 20, dtype=torch.uint8).pin_memory() for _ in E0S]
-    streams = [torch.cuda.Stream() for _ in range(NS)]
-    handles = [C.c_void_p(st.cuda_stream) for st in streams]
-    items = []  # (type, strided object address, E0 index)
-    # issue order of the E0 messages (BENCH_E2E_ORDER): the slow small-E0
-    # kernels want to start early, while later messages' copies keep the
-    # PCIe engines busy
-    order = os.environ.get("BENCH_E2E_ORDER", "descending")
+    pstreams = [torch.cuda.Stream() for _ in range(NS)]
+    ustreams = [torch.cuda.Stream() for _ in range(NS)]
+    phandles = [C.c_void_p(st.cuda_stream) for st in pstreams]
+    uhandles = [C.c_void_p(st.cuda_stream) for st in ustreams]
+    order = os.environ.get("BENCH_E2E_ORDER", "ascending")
     idx = sorted(range(len(types)), key=lambda i: types[i][0])
     if order == "descending":
         idx = idx[::-1]
-    elif order == "interleaved":  # 1, 512, 2, 256, ...
-        idx = [idx[j // 2] if j % 2 == 0 else idx[-1 - j // 2] for j in range(len(idx))]
-    elif order == "pipelined":  # 512, 1, 2, 4, ..., 256: the D2H engine starts early,
-        # the slow (small-E0) kernels overlap the later messages' H2D, and
-        # the last message's kernel is short
-        idx = [idx[-1]] + idx[:-1]
-    for i in idx:
-        e0, d, ct = types[i]
-        items.append((ct, esrc.data_ptr() + xoff[e0], i))
+    items = [(types[i][2], xoff[types[i][0]], i) for i in idx]  # (type, object offset, E0 index)
+    all_streams = pstreams + ustreams
     e2e_t = 0.0
     for it in range(args.warmup + args.steps):
         torch.cuda.synchronize()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
-        a.record(streams[0])
-        for st in streams[1:]:
+        a.record(all_streams[0])
+        for st in all_streams[1:]:
             st.wait_event(a)
-        for n, (ct, obj, i) in enumerate(items):
-            h = handles[n % NS]
+        for n, (ct, off, i) in enumerate(items):
             pos.value = 0
-            st = lib.sp_unpack(msg_in[i].data_ptr(), msg_in[i].numel(), C.byref(pos), ct.handle, Ke, obj,
-                               esrc.numel() - (obj - esrc.data_ptr()), h)
+            st = lib.sp_pack(esrc.data_ptr() + off, esrc.numel() - off, ct.handle, Ke, msg_out[i].data_ptr(),
+                             msg_out[i].numel(), C.byref(pos), phandles[n % NS])
             assert st == 0, lib.sp_last_error()
             pos.value = 0
-            st = lib.sp_pack(obj, esrc.numel() - (obj - esrc.data_ptr()), ct.handle, Ke, msg_out[i].data_ptr(),
-                             msg_out[i].numel(), C.byref(pos), h)
+            st = lib.sp_unpack(msg_in[i].data_ptr(), msg_in[i].numel(), C.byref(pos), ct.handle, Ke,
+                               edst.data_ptr() + off, edst.numel() - off, uhandles[n % NS])
             assert st == 0, lib.sp_last_error()
-        for st in streams[1:]:
+        for st in all_streams[1:]:
             ev = torch.cuda.Event()
             ev.record(st)
-            streams[0].wait_event(ev)
-        b.record(streams[0])
+            all_streams[0].wait_event(ev)
+        b.record(all_streams[0])
         torch.cuda.synchronize()
         if it >= args.warmup:
             e2e_t += a.elapsed_time(b)
+    streams = all_streams
     # PCIe bound of the leg: the same bytes in both directions at once,
     # plain pinned copies on two streams (no kernels)
     dev_buf = torch.empty(2 * (Ke << 20) * len(E0S), dtype=torch.uint8, device="cuda")
@@ -704,7 +698,7 @@ def run_ours(args):
     e2e_ms = barrier_max(torch, world, e2e_t / args.steps)
     e2e_bytes = 2 * Ke * (1 << 20) * 2 * len(E0S)
     e2e_val = barrier_sum(torch, world, e2e_bytes) / (e2e_ms * 1e-3) / 1e9
-    del esrc, msg_in, msg_out
+    del esrc, edst, msg_in, msg_out
 
     # multi-GPU rows: halo exchange (config 5) and model-selected send (config 4).
     # A watchdog guarantees the driver its JSON line even if these hang.

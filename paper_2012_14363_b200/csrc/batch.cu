@@ -1,6 +1,7 @@
 // batch.cu -- many-job launches (pack, unpack, typed copy), single-job
 // ranged launches (pipelined message chunks, sp_copy) and the in-kernel
 // completion protocol of the distributed halo and neighbour collectives.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -50,9 +51,17 @@ struct BatchJob {
   int same;          // COPY with gd == gs: destination offset = source offset
 };
 
-// Optional in-kernel completion protocol (distributed halo): every block
-// first waits until each `wait` flag (local memory, written by peers over
-// NVLink) reaches wait_value; after its last word, EVERY block adds its share
+// Optional completion protocol (distributed halo). Before any word moves,
+// the `pre` flags are published and each `wait` flag (local memory, written
+// by peers over NVLink) must reach wait_value, in one of two places:
+//  * in the kernel (every rank on its own GPU): block 0 release-stores the
+//    pre flags, every block spins on an acquire load of the wait flags;
+//  * in the stream (ranks share a GPU -- MPS, time slicing): stream memory
+//    operations ahead of the launch (stream_flag_ops) publish and then hold
+//    the stream in its front end, on no SM, so a rank's spinning full-wave
+//    grid can never starve the peer kernel it waits for; the blocks' acquire
+//    loads then no longer spin.
+// After its last word, EVERY block adds its share
 // of 2^32 to each `signal` counter (peer memory) with a release reduction --
 // the shares of a launch sum to exactly 2^32 whatever the grid, so a
 // receiver waits for calls << 32 without knowing the sender's grid, and no
@@ -64,8 +73,7 @@ struct BatchSig {
   unsigned long long wait_value;
   int n_wait, n_signal;
   int sys_scope;  // some destination lives on another GPU: system-scope fences
-  // published by block 0 BEFORE waiting (consumer-side "ready" flags: the
-  // stream order guarantees everything before this launch has completed)
+  // in-kernel mode only: published by block 0 BEFORE any block waits
   unsigned long long *pre[kMaxSig];
   unsigned long long pre_value;
   int n_pre;
@@ -166,6 +174,8 @@ template <int W, int MODE> __device__ __forceinline__ void move_chunk(const Batc
 __device__ __forceinline__ void batch_prologue(const BatchSig &sig) {
   if (sig.n_pre && blockIdx.x == 0 && threadIdx.x < static_cast<unsigned>(sig.n_pre))
     st_release_sys(sig.pre[threadIdx.x], sig.pre_value);
+  // stream mode: satisfied before the launch, one acquire load each;
+  // in-kernel mode (every rank on its own GPU): spins until the peers publish
   if (sig.n_wait) {
     if (threadIdx.x < static_cast<unsigned>(sig.n_wait)) wait_flag(sig.wait[threadIdx.x], sig.wait_value, sig, 64);
     __syncthreads();
@@ -571,6 +581,56 @@ template <int W> void launch_batch_w(const BatchGroup &g, const BatchSig &sig, c
   }
 }
 
+struct FlagStore {
+  unsigned long long *p[kMaxSig];
+  unsigned long long v;
+  int n;
+};
+
+// release-stores v to each flag (system scope): the pre flags of a launch
+// whose peers are on other GPUs
+__global__ void k_flag_store(const FlagStore f) {
+  if (threadIdx.x < static_cast<unsigned>(f.n)) st_release_sys(f.p[threadIdx.x], f.v);
+}
+
+// Stream memory operations (one cuStreamBatchMemOp): write `value` to each
+// `writes` flag (ordered after all earlier work on the stream, with the
+// write's memory barrier), then block the stream until each `waits` flag
+// reaches wait_value (cyclic >=). The wait is held by the stream's front end:
+// no SM is occupied while a peer has still to run.
+void stream_flag_ops(cudaStream_t s, const std::vector<uint64_t *> &writes, uint64_t value,
+                     const std::vector<const uint64_t *> &waits, uint64_t wait_value) {
+  if (writes.empty() && waits.empty()) return;
+  using BatchMemOp = CUresult (*)(CUstream, unsigned, CUstreamBatchMemOpParams *, unsigned);
+  static BatchMemOp fn = [] {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuStreamBatchMemOp", &f, cudaEnableDefault, &q);
+    return reinterpret_cast<BatchMemOp>(f);
+  }();
+  if (!fn) fail(SP_ERR_CUDA, "cuStreamBatchMemOp is not available");
+  if (writes.size() + waits.size() >= 256) fail(SP_ERR_UNSUPPORTED, "stream flag ops: too many peers");
+  std::vector<CUstreamBatchMemOpParams> ops(writes.size() + waits.size());
+  std::memset(ops.data(), 0, ops.size() * sizeof(CUstreamBatchMemOpParams));
+  size_t k = 0;
+  for (uint64_t *w : writes) {
+    ops[k].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_64;
+    ops[k].writeValue.address = reinterpret_cast<CUdeviceptr>(w);
+    ops[k].writeValue.value64 = value;
+    ops[k].writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+    ++k;
+  }
+  for (const uint64_t *w : waits) {
+    ops[k].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_64;
+    ops[k].waitValue.address = reinterpret_cast<CUdeviceptr>(w);
+    ops[k].waitValue.value64 = wait_value;
+    ops[k].waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+    ++k;
+  }
+  const CUresult r = fn(reinterpret_cast<CUstream>(s), static_cast<unsigned>(ops.size()), ops.data(), 0);
+  if (r != CUDA_SUCCESS) fail(SP_ERR_CUDA, "cuStreamBatchMemOp failed (" + std::to_string(static_cast<int>(r)) + ")");
+}
+
 void batch_launch(const Batch &b, void *stream, const BatchSignal *bs) {
   sp_launch_info li{};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -585,10 +645,29 @@ void batch_launch(const Batch &b, void *stream, const BatchSignal *bs) {
       if (bs->wait.size() > static_cast<size_t>(kMaxSig) || bs->signal.size() > static_cast<size_t>(kMaxSig) ||
           bs->pre.size() > static_cast<size_t>(kMaxSig))
         fail(SP_ERR_UNSUPPORTED, "batch signalling: more than 32 peers");
-      if (gi == 0) {
+      if (gi == 0 && !bs->stream_waits) { // every rank on its own GPU: all in the kernel
+        if (bs->pre.size() > static_cast<size_t>(kMaxSig)) fail(SP_ERR_UNSUPPORTED, "batch signalling: more than 32 peers");
         sig.n_pre = static_cast<int>(bs->pre.size());
         for (int i = 0; i < sig.n_pre; ++i) sig.pre[i] = reinterpret_cast<unsigned long long *>(bs->pre[i]);
         sig.pre_value = bs->pre_value;
+      } else if (gi == 0) {
+        if (bs->sys_scope && !bs->pre.empty()) {
+          // pre flags in another GPU's memory: stored from an SM (a
+          // system-scope release over NVLink), not by a stream memory op
+          if (bs->pre.size() > static_cast<size_t>(kMaxSig)) fail(SP_ERR_UNSUPPORTED, "batch signalling: more than 32 peers");
+          FlagStore fs{};
+          fs.n = static_cast<int>(bs->pre.size());
+          for (int i = 0; i < fs.n; ++i) fs.p[i] = reinterpret_cast<unsigned long long *>(bs->pre[i]);
+          fs.v = bs->pre_value;
+          k_flag_store<<<1, 32, 0, s>>>(fs);
+          cuda_check(cudaGetLastError(), "k_flag_store launch");
+          g_launches.fetch_add(1, std::memory_order_relaxed);
+          stream_flag_ops(s, {}, 0, bs->wait, bs->wait_value);
+        } else {
+          stream_flag_ops(s, bs->pre, bs->pre_value, bs->wait, bs->wait_value);
+        }
+      }
+      if (gi == 0) {
         sig.n_wait = static_cast<int>(bs->wait.size());
         for (int i = 0; i < sig.n_wait; ++i) sig.wait[i] = reinterpret_cast<const unsigned long long *>(bs->wait[i]);
         sig.wait_value = bs->wait_value;

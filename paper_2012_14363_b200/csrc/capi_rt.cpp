@@ -435,6 +435,7 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
       // block 0, after adding its share of READY=n, waits for READY=n from
       // this rank's senders: the launch completes only when the ghost shell
       // is whole, so no separate wait kernel
+      ks.stream_waits = rt_flag_waits_in_stream();
       ks.post = ready;
       ks.post_value = it << 32; // READY counts 2^32 per sender launch
       ks.err = rt_device_err();
@@ -467,6 +468,7 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
       }
       us.wait_value = it << 32;
       ps.sys_scope = us.sys_scope = p->remote_peers;
+      ps.stream_waits = us.stream_waits = rt_flag_waits_in_stream();
       ps.err = us.err = rt_device_err();
       ps.timeout_ns = us.timeout_ns = rt_device_timeout_ns();
       cuda_check(cudaEventRecord(p->ev[0], s), "cudaEventRecord");
@@ -499,7 +501,7 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
     // device-ordered methods need no host synchronisation: without timings
     // the call only enqueues, and iterations pipeline on the runtime stream
     const bool async = !times && (p->method == SP_HALO_DIRECT || p->method == SP_HALO_FUSED_ASYNC);
-    if (!async) cuda_check(cudaEventSynchronize(p->ev[3]), "cudaEventSynchronize");
+    if (!async) rt_sync_event(p->ev[3], "halo exchange");
     // a flag wait of this (or, enqueue-only, an earlier) iteration gave up
     rt_check_device_error("halo exchange");
     if (times) {

@@ -255,6 +255,7 @@ struct BatchSignal {
   std::vector<const uint64_t *> post; // local counters block 0 waits for after signalling
   uint64_t post_value = 0;
   std::vector<uint64_t> post_values;  // per-target post values (else the scalar)
+  bool stream_waits = true; // pre/wait through stream memory ops (else block 0 / every block in-kernel)
   int *err = nullptr;      // set to 1 by an in-kernel wait that gave up (mapped host memory)
   uint64_t timeout_ns = 0; // in-kernel wait limit, 0 = unbounded
 };

@@ -603,7 +603,15 @@ uint8_t *stage_buffer(cudaStream_t s, size_t bytes) {
 // by chunk (H2D of chunk k+1 while chunk k unpacks; D2H of chunk k while
 // chunk k+1 packs). One per (device, caller stream), like the stage buffers.
 constexpr int kLaneEvents = 64;
-constexpr int64_t kDmaChunk = int64_t{8} << 20; // packed bytes per pipelined chunk
+// packed bytes per pipelined chunk (TEMPI_DMA_CHUNK overrides, >= 64 KiB)
+int64_t dma_chunk() {
+  static const int64_t c = [] {
+    const char *e = std::getenv("TEMPI_DMA_CHUNK");
+    const int64_t v = e && *e ? std::atoll(e) : 0;
+    return v >= (int64_t{64} << 10) ? v : int64_t{8} << 20;
+  }();
+  return c;
+}
 struct DmaLane {
   cudaStream_t cs = nullptr;
   cudaEvent_t ev[kLaneEvents] = {};
@@ -1075,7 +1083,7 @@ int64_t execute(const PackArgs &a) {
   }
   // a large pinned message of several objects: pipeline the DMA against
   // the kernels in chunks of whole objects on a copy lane beside `s`
-  const int64_t per_chunk = std::max<int64_t>(1, kDmaChunk / std::max<int64_t>(ct.size, 1));
+  const int64_t per_chunk = std::max<int64_t>(1, dma_chunk() / std::max<int64_t>(ct.size, 1));
   const bool pipelined = dma_packed && rs.kind != MemKind::Pageable && a.count >= 2 && per_chunk < a.count;
   if (pipelined) {
     DmaLane &lane = dma_lane(s);

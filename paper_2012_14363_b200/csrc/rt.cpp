@@ -89,6 +89,7 @@ struct Slot {
   int32_t pid;
   int32_t device;
   int32_t pad;
+  uint8_t uuid[16];           // the GPU's UUID (ordinals differ between processes)
   cudaIpcMemHandle_t window;  // device receive window (DEVICE method)
   int64_t window_bytes;
   int64_t host_bytes;         // shared pinned host region (ONESHOT/STAGED)
@@ -186,6 +187,7 @@ struct Runtime {
   std::vector<uint8_t *> peer_nbr_flags;
   std::vector<uint64_t> pair_sent, pair_recv;
   bool nbr_remote = false;
+  bool shared_device = false; // another rank of the job runs on this rank's GPU
   // set (to 1) by an in-kernel flag wait that gave up after TEMPI_TIMEOUT;
   // mapped pinned memory, read by the host after each synchronisation
   int *err_host = nullptr, *err_dev = nullptr;
@@ -330,27 +332,42 @@ uint8_t *peer_host(int r) {
 }
 
 void ipc_handle_of(const void *ptr, cudaIpcMemHandle_t *h, int64_t *offset) {
-  // handles name whole allocations; carry the offset inside it separately
-  cudaPointerAttributes at{};
-  cuda_check(cudaPointerGetAttributes(&at, ptr), "cudaPointerGetAttributes");
-  if (at.type != cudaMemoryTypeDevice) fail(SP_ERR_INVALID_ARGUMENT, "IPC export needs device memory");
-  void *base = nullptr;
-  size_t range = 0;
-  // the runtime API has no range query; find the base by probing the handle
-  // of the pointer itself first (cudaMalloc'd bases), else via the driver
-  using GetRange = int (*)(uint64_t *, size_t *, uint64_t);
-  static GetRange get_range = [] {
+  // handles name whole allocations; carry the offset inside it separately.
+  // One driver query gives the allocation's process-unique buffer id, its
+  // base and its memory type; the handle itself (cudaIpcGetMemHandle, the
+  // expensive part) is cached per buffer id -- ids are never reused, so a
+  // freed and re-made allocation at the same address gets a fresh handle.
+  // A repeated neighbour call asks for its receive buffer's handle each time.
+  using GetAttrs = int (*)(unsigned, int *, void **, uint64_t);
+  static GetAttrs get_attrs = [] {
     void *fn = nullptr;
     cudaDriverEntryPointQueryResult q;
-    cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q);
-    return reinterpret_cast<GetRange>(fn);
+    cudaGetDriverEntryPoint("cuPointerGetAttributes", &fn, cudaEnableDefault, &q);
+    return reinterpret_cast<GetAttrs>(fn);
   }();
-  uint64_t b = 0;
-  if (!get_range || get_range(&b, &range, reinterpret_cast<uint64_t>(ptr)) != 0)
-    fail(SP_ERR_CUDA, "cuMemGetAddressRange failed");
-  base = reinterpret_cast<void *>(b);
-  cuda_check(cudaIpcGetMemHandle(h, base), "cudaIpcGetMemHandle");
-  *offset = static_cast<const uint8_t *>(ptr) - static_cast<const uint8_t *>(base);
+  constexpr int kMemoryType = 2, kBufferId = 7, kRangeStart = 11, kDeviceMemory = 2; // cuda.h enums
+  unsigned mtype = 0;
+  unsigned long long id = 0;
+  uint64_t base = 0;
+  int which[3] = {kMemoryType, kBufferId, kRangeStart};
+  void *vals[3] = {&mtype, &id, &base};
+  if (!get_attrs || get_attrs(3, which, vals, reinterpret_cast<uint64_t>(ptr)) != 0)
+    fail(SP_ERR_CUDA, "cuPointerGetAttributes failed");
+  if (mtype != kDeviceMemory || !base) fail(SP_ERR_INVALID_ARGUMENT, "IPC export needs device memory");
+  static std::mutex mu;
+  static std::map<unsigned long long, cudaIpcMemHandle_t> cache;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(id);
+    if (it == cache.end()) {
+      cudaIpcMemHandle_t nh{};
+      cuda_check(cudaIpcGetMemHandle(&nh, reinterpret_cast<void *>(base)), "cudaIpcGetMemHandle");
+      if (cache.size() >= 4096) cache.clear();
+      it = cache.emplace(id, nh).first;
+    }
+    *h = it->second;
+  }
+  *offset = static_cast<const uint8_t *>(ptr) - reinterpret_cast<const uint8_t *>(base);
 }
 
 } // namespace
@@ -386,6 +403,9 @@ void rt_init(int rank, int size, const char *name, int device, int64_t window_by
   me.device = device;
   if (device >= 0) {
     cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop{};
+    cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    std::memcpy(me.uuid, prop.uuid.bytes, sizeof(me.uuid));
     cuda_check(cudaStreamCreateWithFlags(&G.stream, cudaStreamNonBlocking), "cudaStreamCreate");
     cuda_check(cudaStreamCreateWithFlags(&G.rstream, cudaStreamNonBlocking), "cudaStreamCreate");
     if (window_bytes > 0) {
@@ -420,6 +440,10 @@ void rt_init(int rank, int size, const char *name, int device, int64_t window_by
   }
   me.ready.store(1, std::memory_order_release);
   rt_barrier();
+  if (device >= 0)
+    for (int r = 0; r < size; ++r)
+      if (r != rank && G.shm->slots[r].device >= 0 && !std::memcmp(G.shm->slots[r].uuid, me.uuid, sizeof(me.uuid)))
+        G.shared_device = true;
   rt_exchange_ptr(G.nbr_flags, G.peer_nbr_flags);
   if (device >= 0)
     for (int r = 0; r < size; ++r) {
@@ -478,6 +502,37 @@ void rt_check_device_error(const char *what) {
     fail(SP_ERR_TIMEOUT, std::string(what) + ": an in-kernel wait for a peer's flag gave up after TEMPI_TIMEOUT=" +
                              std::to_string(timeout_s()) + " s (a peer rank died or never entered the call)");
   }
+}
+
+// Stream work that waits on peers' flags (stream memory operations) cannot
+// time out on the device: the host polls its completion event like any other
+// wait on the peers, so a dead or absent peer becomes SP_ERR_TIMEOUT.
+void rt_sync_event(cudaEvent_t e, const char *what) {
+  Waiter w(what);
+  for (;;) {
+    const cudaError_t q = cudaEventQuery(e);
+    if (q == cudaSuccess) return;
+    if (q != cudaErrorNotReady) cuda_check(q, what);
+    w.pause();
+  }
+}
+
+// Where a launch waits for its peers' flags. In the kernel (every block
+// spins on an acquire load) is the fastest, and safe when every rank has its
+// own GPU: a peer's grid never competes for this GPU's SMs. When ranks share
+// a GPU (MPS, or time-sliced processes), one rank's spinning full-wave grid
+// can hold every SM the peer's kernel needs, so the waits move into the
+// stream's front end (stream memory operations). TEMPI_FLAG_WAIT=stream |
+// kernel overrides the choice.
+bool rt_flag_waits_in_stream() {
+  static const int forced = [] {
+    const char *e = std::getenv("TEMPI_FLAG_WAIT");
+    if (!e || !*e) return -1;
+    if (!std::strcmp(e, "stream")) return 1;
+    if (!std::strcmp(e, "kernel")) return 0;
+    return -1;
+  }();
+  return forced >= 0 ? forced == 1 : rt().shared_device;
 }
 
 int rt_rank() { return rt().rank; }
@@ -1451,7 +1506,7 @@ BatchSignal nbr_enter(const std::vector<int> &sources, const std::vector<int> &d
   for (int d : dests) {
     if (d == R.rank || seen_d[d]) continue;
     seen_d[d] = 1;
-    const uint64_t n = ++R.pair_sent[d];
+    ++R.pair_sent[d];
     bs.signal.push_back(reinterpret_cast<uint64_t *>(R.peer_nbr_flags[d]) + R.rank);
     outs.push_back(d);
   }

@@ -25,6 +25,12 @@ void rt_finalize();
 uint64_t rt_device_timeout_ns();
 int *rt_device_err();
 void rt_check_device_error(const char *what);
+// halo / neighbour flag waits in the stream front end (ranks share a GPU)
+// rather than in the kernel (every rank on its own GPU); TEMPI_FLAG_WAIT
+bool rt_flag_waits_in_stream();
+// polls a completion event with the peer-liveness checks and TEMPI_TIMEOUT
+// of a host wait (stream work that waits on peers' flags)
+void rt_sync_event(cudaEvent_t e, const char *what);
 int rt_rank();
 int rt_size();
 void rt_barrier();
