@@ -1,9 +1,12 @@
 """MPI-3.1 typemap restatement -- TEST INFRASTRUCTURE ONLY (imported by tests/,
 never by the product path).
 
-Parity unpinned: the reference has no indexed, struct or resized datatypes
-(PAPER.md:1164 lists them as future work), so
-there are no reference golden vectors for them. This module restates the
+No reference vectors: the reference has no indexed, struct or resized
+datatypes (PAPER.md:1164 lists them as future
+work). Pinned instead to an external source: the worked typemap examples of
+the MPI-3.1 standard (section 4.1.2: contiguous, vector, indexed, struct),
+transcribed in tests/golden/mpi31_typemap_examples.json and checked by
+tests/test_mpi31_examples.py against this module AND the engine. This module restates the
 MPI-3.1 definitions directly (sections 4.1.2 contiguous, 4.1.3 vector and
 hvector, 4.1.4 indexed/hindexed, 4.1.5 indexed_block/hindexed_block, 4.1.6
 struct, 4.1.7 resized, 4.1.3 subarray) in pure Python, small sizes only:

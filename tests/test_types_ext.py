@@ -1,8 +1,9 @@
 """Datatypes beyond the reference: MPI indexed / hindexed / indexed_block /
 struct / resized (MPI-3.1 4.1.2-4.1.7; PAPER.md:1164 lists them as TEMPI's
 future work). The reference has none of them, so
-parity is pinned to the MPI typemap restatement in oracle/typemap.py, not to
-reference vectors.
+parity rests on the MPI typemap restatement in oracle/typemap.py, which is
+itself pinned to the MPI-3.1 standard's worked examples
+(tests/test_mpi31_examples.py), not to reference vectors.
 
 CPU: size / lb / extent / span / flattened runs / overlap against the
 restatement over thousands of random nested descriptions, canonicalisation

@@ -140,11 +140,53 @@ int main() {
                                                                 cudaStreamSynchronize(s);
                                                               },
                                                               500));
-    sp_batch_free(b);
     auto call = [&] {
       sp_rt_neighbor_alltoallw(a, one, zero, hs, 26, nb, a, one, zero, rtyp, 26, nb);
     };
     std::printf("halo alltoallw (1 rank)    %8.2f us\n", med_us(call, 500));
+    // the same two with a cold L2 (a 512 MiB memset before each call, waited
+    // for and not timed), as bench.py measures them; and the kernel alone
+    // by events, so host cost = wall - kernel
+    {
+      uint8_t *fl = nullptr;
+      cudaMalloc(&fl, size_t{512} << 20);
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      auto cold_med = [&](auto &&f, int reps) {
+        std::vector<double> t;
+        for (int i = 0; i < reps + 5; ++i) {
+          cudaMemsetAsync(fl, i & 0xff, size_t{512} << 20, s);
+          cudaStreamSynchronize(s);
+          const auto t0 = std::chrono::steady_clock::now();
+          f();
+          const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+          if (i >= 5) t.push_back(us);
+        }
+        std::sort(t.begin(), t.end());
+        return t[t.size() / 2];
+      };
+      std::printf("cold: copy batch + sync    %8.2f us\n", cold_med([&] {
+                    sp_batch_execute(b, s);
+                    cudaStreamSynchronize(s);
+                  }, 100));
+      std::vector<double> kt;
+      for (int i = 0; i < 105; ++i) {
+        cudaMemsetAsync(fl, i & 0xff, size_t{512} << 20, s);
+        cudaEventRecord(e0, s);
+        sp_batch_execute(b, s);
+        cudaEventRecord(e1, s);
+        cudaStreamSynchronize(s);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (i >= 5) kt.push_back(ms * 1e3);
+      }
+      std::sort(kt.begin(), kt.end());
+      std::printf("cold: copy batch (events)  %8.2f us\n", kt[kt.size() / 2]);
+      std::printf("cold: alltoallw (1 rank)   %8.2f us\n", cold_med(call, 100));
+      cudaFree(fl);
+    }
+    sp_batch_free(b);
     // host side only: the same call with every count zero launches no copy
     std::printf("alltoallw, zero counts     %8.2f us\n", med_us(
                                                               [&] {
