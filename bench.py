@@ -606,6 +606,56 @@ def run_ours(args):
         cfg1[f"{tag}_kernel"] = f"{li.kernel.name}/w{li.word}"
     cfg1["line_cap"] = round(2 * 8 / (128 + 8), 4)
 
+    # cfg3 (outside the timed region): the cfg2 object at E0 = 32 built five
+    # ways -- subarray, vector of hvector, hvector of vector of hvector,
+    # hvector of contiguous, nested subarrays. Every construction must reach
+    # the same StridedBlock (so the same kernel and rate); its commit time
+    # is reported beside the reference's brute-force commit (SURVEY.md
+    # 8(a) T7: 38-103 ms for a cfg2 object).
+
+    e0c, e1c, e2c = 32, 128, 256
+    byte = sp.make_named(sp.NamedKind.Byte)
+    ways = {
+        "subarray": lambda: sp.make_subarray(3, [1024] * 3, [e0c, e1c, e2c], [0, 0, 0], byte),
+        "hvector(vector)": lambda: sp.make_hvector(e2c, 1, 1 << 20, sp.make_vector(e1c, e0c, 1024, byte)),
+        "hvector(vector(hvector))": lambda: sp.make_hvector(
+            e2c, 1, 1 << 20, sp.make_vector(e1c, 1, 1024 // e0c, sp.make_hvector(e0c, 1, 1, byte))),
+        "hvector(hvector(contiguous))": lambda: sp.make_hvector(
+            e2c, 1, 1 << 20, sp.make_hvector(e1c, 1, 1024, sp.make_contiguous(e0c, byte))),
+        "subarray(subarray)": lambda: sp.make_subarray(
+            1, [1024], [e2c], [0], sp.make_subarray(2, [1024, 1024], [e0c, e1c], [0, 0], byte)),
+    }
+    cfg3 = {"object": "cfg2 E0=32 (32 x 128 x 256 B in 1024^3 B)", "incount": K, "rows": []}
+    canons = set()
+    for name, mk in ways.items():
+        tc = []
+        for _ in range(20):
+            d3 = mk()
+            t0 = time.perf_counter()
+            c3 = sp.commit_type(d3)
+            tc.append(time.perf_counter() - t0)
+        canons.add((c3.canon, c3.plan))
+        row = {"construction": name, "commit_us": round(statistics.median(tc) * 1e6, 1)}
+        for pack in (True, False):
+            ts = []
+            for i in range(5):
+                flush_l2(i)
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                if pack:
+                    call(True, c3, K, src.data_ptr(), src.numel(), packed.data_ptr(), packed.numel())
+                else:
+                    call(False, c3, K, packed.data_ptr(), packed.numel(), src.data_ptr(), src.numel())
+                b.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            tag = "pack" if pack else "unpack"
+            row[f"{tag}_GBps"] = round(2 * K * c3.size / (statistics.median(ts) * 1e-3) / 1e9, 1)
+        cfg3["rows"].append(row)
+    cfg3["one_canonical_form"] = len(canons) == 1
+    cfg3["canon"] = str(next(iter(canons))[0]) if len(canons) == 1 else None
+
     # e2e: the packed messages live in pinned HOST memory and every call
     # goes through the public C-ABI with those host pointers: sp_pack moves
     # each E0's message out of the device objects to the host (pack kernels,
@@ -620,7 +670,7 @@ def run_ours(args):
     extra = {"value_E0_ge_32": {"value": round(value_ge32, 2), "unit": UNIT,
                                 "frac": round(value_ge32 / hbm, 4),
                                 "how": "pack + unpack bytes over kernel time of the E0 >= 32 rows only"},
-             "cfg1_throughput": cfg1}
+             "cfg1_throughput": cfg1, "cfg3": cfg3}
     del src, packed
     torch.cuda.empty_cache()
     Ke = min(K, args.e2e_incount)

@@ -404,6 +404,13 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
   return guarded([&] {
     need(p);
     cudaStream_t s = static_cast<cudaStream_t>(rt_stream());
+    // the flag values of an exchange are per iteration (FREE=n-1, READY=n):
+    // a captured launch replayed from a CUDA graph would reuse them and
+    // return before the peers' ghosts land, so capture is refused
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cuda_check(cudaStreamIsCapturing(s, &cap), "cudaStreamIsCapturing");
+    if (cap != cudaStreamCaptureStatusNone)
+      fail(SP_ERR_UNSUPPORTED, "halo exchange: cannot be captured into a CUDA graph (per-iteration flag values)");
     if (p->method == SP_HALO_DIRECT) {
       // one copy launch per iteration: block 0 first tells this rank's
       // senders that the ghosts of iteration n-1 are consumed (FREE=n-1;

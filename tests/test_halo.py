@@ -248,3 +248,33 @@ def test_copy_batch_counts_and_errors(sp, orc, cuda):
         Batch.copies([(src, sp.commit_type(sp.make_contiguous(8, sp.make_named(sp.NamedKind.Byte))), 1, dst, ov, 1)])
     with pytest.raises(sp.BufferTooSmall):
         Batch.copies([(src[:10], a, 1, dst, b, 1)])
+
+
+@pytest.mark.gpu
+def test_halo_exchange_refuses_graph_capture(sp, cuda):
+    """an exchange's flag values change every iteration, so a captured launch
+    replayed from a graph would not wait for the peers: the engine refuses
+    the capture instead of recording it"""
+    import uuid
+    torch = cuda
+    import paper_2012_14363_b200.halo as H
+    import paper_2012_14363_b200.rt as rt
+    rt.init(0, 1, "cap" + uuid.uuid4().hex[:8], device=0, window_bytes=1 << 20, host_bytes=1 << 20)
+    try:
+        cfg = H.HaloConfig((1, 1, 1), (12, 10, 8), 2, 16)
+        alloc = torch.zeros(16 * 14 * 12 * 16, dtype=torch.uint8, device="cuda")
+        plan = rt.HaloPlan(cfg, alloc, H.DIRECT)
+        plan.exchange()
+        rs = torch.cuda.ExternalStream(rt.stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(rs):
+            g.capture_begin()
+            try:
+                with pytest.raises(sp.Unsupported):
+                    plan.exchange(timed=False)
+            finally:
+                g.capture_end()
+        plan.exchange()  # still usable outside a capture
+        plan.free()
+    finally:
+        rt.finalize()

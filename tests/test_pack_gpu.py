@@ -631,3 +631,47 @@ def test_concurrent_host_threads_share_committed_types(sp, orc, cuda):
     for th in ths:
         th.join()
     assert not errors, errors[:5]
+
+
+@pytest.mark.gpu
+def test_pack_unpack_replay_from_cuda_graph(sp, orc, cuda):
+    """CUDA graphs instead of a tracing compiler: sp_pack / sp_unpack of
+    device buffers enqueue only kernels, so an application can capture them
+    (here a cfg2-shaped subarray and the cfg1 vector, pack then unpack) into
+    one graph and replay it; every replay with fresh source bytes matches
+    the oracle, and bytes outside the layout keep the sentinel"""
+    torch = cuda
+    progs = [[4, 3, 0, 1024, 64, 16, 16, 32, 8, 1, 2, 3, 0, 0], [2, 4096, 1, 64, 0, 3]]
+    cts = [sp.commit_type(sp.from_program(p)) for p in progs]
+    srcs = [torch.empty(c.span, dtype=torch.uint8, device="cuda") for c in cts]
+    packs = [torch.empty(c.size, dtype=torch.uint8, device="cuda") for c in cts]
+    backs = [torch.empty(c.span, dtype=torch.uint8, device="cuda") for c in cts]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):  # first launches (module load, occupancy queries) outside the capture
+        for c, a, p, b in zip(cts, srcs, packs, backs):
+            sp.pack(a, c, 1, p, 0)
+            sp.unpack(p, 0, c, 1, b)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for c, a, p, b in zip(cts, srcs, packs, backs):
+            sp.pack(a, c, 1, p, 0)
+            sp.unpack(p, 0, c, 1, b)
+    rng = np.random.default_rng(77)
+    for rep in range(3):
+        hosts = [rng.integers(0, 256, c.span, dtype=np.uint8) for c in cts]
+        for a, b, h in zip(srcs, backs, hosts):
+            a.copy_(torch.from_numpy(h))
+            b.fill_(0xC3)
+        torch.cuda.synchronize()
+        before = sp.kernel_launch_count()
+        g.replay()
+        torch.cuda.synchronize()
+        assert sp.kernel_launch_count() == before  # replayed by the driver, not re-enqueued by the engine
+        for prog, c, p, b, h in zip(progs, cts, packs, backs, hosts):
+            want = np.zeros(c.size, np.uint8)
+            assert orc.pack(prog, h, 1, want, 0)[0] == 0
+            assert np.array_equal(p.cpu().numpy(), want), (rep, prog)
+            exp = np.full(c.span, 0xC3, np.uint8)
+            assert orc.unpack(prog, want, 0, 1, exp)[0] == 0
+            assert np.array_equal(b.cpu().numpy(), exp), (rep, prog)
