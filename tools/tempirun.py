@@ -5,13 +5,15 @@
 
 Sets TEMPI_RANK / TEMPI_SIZE / TEMPI_LOCAL_RANK / TEMPI_JOB for each process
 (rank r uses GPU r % device_count unless TEMPI_DEVICE is set), waits for all
-of them and exits with the first nonzero status. torchrun works too: the
+of them and exits with the first nonzero status (the other ranks are
+killed then: they may be blocked on the one that failed). torchrun works too: the
 library reads RANK / WORLD_SIZE / LOCAL_RANK / TORCHELASTIC_RUN_ID.
 """
 import argparse
 import os
 import subprocess
 import sys
+import time
 import uuid
 
 
@@ -26,15 +28,24 @@ def main():
     for r in range(a.np):
         env = dict(os.environ, TEMPI_RANK=str(r), TEMPI_SIZE=str(a.np), TEMPI_LOCAL_RANK=str(r), TEMPI_JOB=job)
         procs.append(subprocess.Popen(a.cmd, env=env))
+    # the first nonzero exit ends the job (its peers may be blocked on it)
     rc = 0
-    try:
-        for p in procs:
-            p.wait(timeout=a.timeout)
-            rc = rc or p.returncode
-    except subprocess.TimeoutExpired:
-        for p in procs:
-            p.kill()
-        rc = 124
+    deadline = time.monotonic() + a.timeout
+    live = list(procs)
+    while live:
+        for p in list(live):
+            if p.poll() is not None:
+                live.remove(p)
+                rc = rc or p.returncode
+        if rc or time.monotonic() > deadline:
+            for p in live:
+                p.kill()
+            for p in live:
+                p.wait()
+            if not rc:
+                rc = 124
+            break
+        time.sleep(0.01)
     sys.exit(rc)
 
 
