@@ -754,10 +754,11 @@ def run_ours(args):
     # A watchdog guarantees the driver its JSON line even if these hang.
     del flush
     torch.cuda.empty_cache()
-    halo = send = irregular = None
+    halo = send = irregular = interpose = None
     line_box = {}
     if not args.no_halo:
-        from tools.bench_parts import halo_section, irregular_section, send_section, send_self_section
+        from tools.bench_parts import (halo_section, interpose_section, irregular_section, send_section,
+                                       send_self_section)
 
         def on_timeout():
             if rank == 0 and "line" in line_box:
@@ -794,6 +795,10 @@ def run_ours(args):
             irregular = irregular_section(torch) if rank == 0 else None
         except Exception as exc:
             irregular = {"error": f"{type(exc).__name__}: {exc}"}
+        try:  # the drop-in over a system MPI: same binary with / without the interposer
+            interpose = interpose_section() if world == 1 and not args.no_interpose else None
+        except Exception as exc:
+            interpose = {"error": f"{type(exc).__name__}: {exc}"}
         dog.cancel()
 
     if rank != 0:
@@ -810,6 +815,7 @@ def run_ours(args):
     line = build_line(args, value, step_ms, world, K, dominant, sweep, e2e_val, Ke, launches, clk, cpu, halo,
                       send, pcie_ms, single, pattern, extra)
     line["irregular_types"] = irregular
+    line["interpose"] = interpose
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -828,6 +834,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-halo", action="store_true", help="skip the halo / send sections")
+    ap.add_argument("--no-interpose", action="store_true",
+                    help="skip the interposer-over-a-system-MPI section (N=1 only)")
     ap.add_argument("--section-timeout", type=float, default=420.0,
                     help="watchdog (s) for the halo/send sections; the bench line is printed regardless")
     args = ap.parse_args()

@@ -130,9 +130,17 @@ static void copy_bytes(void *dst, const void *src, int64_t n, int dev) {
     memcpy(dst, src, (size_t)n);
 }
 
+/* one run that fills its extent: `count` objects are one contiguous block
+ * (every MPI takes this path for contiguous data) */
+static int dense(const Type *t) { return t->nruns == 1 && t->off[0] == 0 && t->len[0] == t->extent; }
+
 /* gather `count` objects of `t` at buf into out (type-signature byte order) */
 static void gather(const Type *t, const void *buf, int64_t count, uint8_t *out) {
   const int dev = is_device(buf) || is_device(out);
+  if (dense(t)) {
+    copy_bytes(out, buf, count * t->extent, dev);
+    return;
+  }
   int64_t pos = 0;
   for (int64_t e = 0; e < count; ++e)
     for (int64_t i = 0; i < t->nruns; ++i) {
@@ -143,6 +151,10 @@ static void gather(const Type *t, const void *buf, int64_t count, uint8_t *out) 
 
 static void scatter(const Type *t, const uint8_t *in, int64_t count, void *buf) {
   const int dev = is_device(buf) || is_device(in);
+  if (dense(t)) {
+    copy_bytes(buf, in, count * t->extent, dev);
+    return;
+  }
   int64_t pos = 0;
   for (int64_t e = 0; e < count; ++e)
     for (int64_t i = 0; i < t->nruns; ++i) {

@@ -482,3 +482,79 @@ def irregular_section(torch, blocks=(64, 1024, 4096), total=64 << 20, reps=5):
     return {"what": "irregular hindexed types (beyond the reference) on the run-table kernel vs the regular "
                     "hvector of the same mean block and pitch on the strided kernels; cold L2",
             "rows": rows}
+
+
+def interpose_section(timeout_s=240.0, budget_s=2.0):
+    """TEMPI as a PMPI interposer over a system MPI: two
+    portable MPI programs on the stand-in system MPI (tests/native/minimpi.c:
+    a CUDA-aware MPI whose device derived types move one cudaMemcpy per
+    contiguous run, the generic path) alone, then the same binaries with
+    LD_PRELOAD=libtempi_interpose.so. 2 ranks on this GPU.
+      * tools/interpose_bench.c: MPI_Pack / MPI_Unpack of the cfg1 vector and
+        cfg2 subarrays (E0 = 64, 512) on device memory, MPI_Send/Recv of the
+        cfg1 object;
+      * tests/native/mpi_halo.c: the config-5 halo (256^3, r = 2, 32 B, rank
+        grid 2x1x1) as MPI_Pack x26 + MPI_Neighbor_alltoallv + MPI_Unpack
+        x26, and as one MPI_Neighbor_alltoallw of the region types; every
+        ghost cell verified.
+    Returns {case: {bytes, system_mpi_us, tempi_us, speedup}}."""
+    import json
+    import re
+    import subprocess
+    import tempfile
+
+    pkg = os.path.join(ROOT, "paper_2012_14363_b200")
+    inc = ["-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include"]
+    cuda = "/usr/local/cuda/lib64"
+    legs = {"system_mpi": {}, "tempi": {}}
+    with tempfile.TemporaryDirectory() as d:
+        lib = os.path.join(d, "libminimpi.so")
+        subprocess.run(["/usr/bin/gcc", "-O2", "-fPIC", "-shared", "-pthread"] + inc +
+                       [os.path.join(ROOT, "tests", "native", "minimpi.c"), "-o", lib, "-L" + cuda, "-lcudart",
+                        "-Wl,-rpath," + cuda], check=True)
+        exes = {}
+        for name, src in (("interpose_bench", os.path.join(ROOT, "tools", "interpose_bench.c")),
+                          ("mpi_halo", os.path.join(ROOT, "tests", "native", "mpi_halo.c"))):
+            exes[name] = os.path.join(d, name)
+            subprocess.run(["/usr/bin/gcc", "-O2"] + inc + [src, "-o", exes[name], "-L" + d, "-lminimpi",
+                            "-L" + pkg, "-lstridepack_b200", "-L" + cuda, "-lcudart", "-Wl,-rpath," + d,
+                            "-Wl,-rpath," + pkg, "-Wl,-rpath," + cuda], check=True)
+
+        def launch(leg, args):
+            env = dict(os.environ)
+            if leg == "tempi":
+                env["LD_PRELOAD"] = os.path.join(pkg, "libtempi_interpose.so")
+            p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "tempirun.py"), "-n", "2", "--timeout",
+                                str(timeout_s)] + args, capture_output=True, text=True, env=env,
+                               timeout=timeout_s + 30)
+            if p.returncode != 0:
+                raise RuntimeError(f"{leg} {os.path.basename(args[0])}: rc {p.returncode}: "
+                                   f"{p.stdout[-300:]} {p.stderr[-300:]}")
+            return p.stdout
+
+        for leg in legs:
+            out = launch(leg, [exes["interpose_bench"], str(budget_s)])
+            legs[leg] = {r["what"]: r for r in map(json.loads, filter(None, out.splitlines()))}
+            for mode in (0, 1):
+                out = launch(leg, [exes["mpi_halo"], "2", "1", "1", "256", "2", "32", "2", str(mode)])
+                m = re.search(r"pack ([\d.]+) us alltoallv ([\d.]+) us unpack ([\d.]+) us bytes/rank (\d+)", out)
+                if not m or "OK" not in out:
+                    raise RuntimeError(f"{leg} mpi_halo mode {mode}: {out[-300:]}")
+                tp, tx, tu, nb = float(m[1]), float(m[2]), float(m[3]), int(m[4])
+                if mode == 0:
+                    legs[leg]["halo 2x1x1 MPI_Pack x26"] = {"bytes": nb, "us": tp}
+                    legs[leg]["halo 2x1x1 MPI_Neighbor_alltoallv (MPI_PACKED)"] = {"bytes": nb, "us": tx}
+                    legs[leg]["halo 2x1x1 MPI_Unpack x26"] = {"bytes": nb, "us": tu}
+                else:
+                    legs[leg]["halo 2x1x1 MPI_Neighbor_alltoallw (26 region types)"] = {"bytes": nb, "us": tx}
+    out = {}
+    for what, r in legs["tempi"].items():
+        s = legs["system_mpi"].get(what)
+        out[what] = {"bytes": r["bytes"], "system_mpi_us": s["us"] if s else None, "tempi_us": r["us"],
+                     "speedup": round(s["us"] / r["us"], 1) if s and r["us"] > 0 else None}
+    return {"how": "2 ranks on one GPU, same binaries with and without LD_PRELOAD=libtempi_interpose.so; "
+                   "system MPI = tests/native/minimpi.c (contiguous data in one cudaMemcpy, device derived "
+                   "types one cudaMemcpy per contiguous run, socket transport); tools/interpose_bench.c: best "
+                   "of <=5 warm calls; tests/native/mpi_halo.c 2x1x1 256^3 r=2 32 B: wall time of the second "
+                   "of 2 iterations, every ghost cell verified",
+            "cases": out}
