@@ -103,6 +103,65 @@ struct Scratch {
   }
 };
 
+// per-request message buffers, recycled: a non-blocking message takes one
+// at Isend/Irecv and returns it at completion (cudaMalloc / cudaMallocHost
+// on every request would cost more than the pack itself)
+class Pool {
+ public:
+  explicit Pool(bool pinned) : pinned_(pinned) {}
+  void *take(size_t n) {
+    n = std::max<size_t>(n, 1);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      auto it = free_.lower_bound(n);
+      if (it != free_.end() && it->first <= 2 * n) { // no more than 2x waste
+        void *p = it->second;
+        const size_t have = it->first;
+        cached_ -= have;
+        free_.erase(it);
+        size_[p] = have;
+        return p;
+      }
+    }
+    void *p = nullptr;
+    if ((pinned_ ? cudaMallocHost(&p, n) : cudaMalloc(&p, n)) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    std::lock_guard<std::mutex> lk(mu_);
+    size_[p] = n;
+    return p;
+  }
+  void give(void *p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(mu_);
+    const size_t n = size_[p];
+    size_.erase(p);
+    free_.emplace(n, p);
+    cached_ += n;
+    while (cached_ > kCap && !free_.empty()) { // drop the largest first
+      auto last = std::prev(free_.end());
+      cached_ -= last->first;
+      pinned_ ? cudaFreeHost(last->second) : cudaFree(last->second);
+      free_.erase(last);
+    }
+  }
+  void clear() {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (auto &kv : free_) pinned_ ? cudaFreeHost(kv.second) : cudaFree(kv.second);
+    free_.clear();
+    cached_ = 0;
+  }
+
+ private:
+  static constexpr size_t kCap = size_t{1} << 30; // idle bytes kept per pool
+  const bool pinned_;
+  std::mutex mu_;
+  std::multimap<size_t, void *> free_;
+  std::unordered_map<void *, size_t> size_;
+  size_t cached_ = 0;
+};
+
 // the packed copy of one non-blocking message, alive until its request completes
 struct Pending {
   bool recv = false;
@@ -134,12 +193,13 @@ struct State {
   std::unordered_map<MPI_Comm, std::pair<int, int>> degree; // comm -> (indegree, outdegree)
   std::unordered_map<MPI_Request, Pending> pending;
   std::map<BatchKey, sp_batch> batches;
-  cudaStream_t stream = nullptr;
+  std::unordered_map<int, cudaStream_t> streams; // one per device the application uses
   sp_profile profile = nullptr;
   sp_model_cache model = nullptr;
   int forced = -1;
   bool cuda_aware = true, gpu = false, stats_on = false;
   Scratch dev_s, dev_r, host_s{nullptr, 0, true}, host_r{nullptr, 0, true};
+  Pool dev_pool{false}, host_pool{true};
   Stats st;
 };
 
@@ -171,7 +231,18 @@ int to_mpi(sp_status st) {
     }                                                                                                            \
   } while (0)
 
-int stream_sync() { return cudaStreamSynchronize(S().stream) == cudaSuccess ? MPI_SUCCESS : MPI_ERR_INTERN; }
+// the interposer's stream on the application's CURRENT device (an
+// application may select its GPU after MPI_Init)
+cudaStream_t cur_stream() {
+  int d = 0;
+  cudaGetDevice(&d);
+  std::lock_guard<std::mutex> lk(S().mu);
+  cudaStream_t &st = S().streams[d];
+  if (!st) cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  return st;
+}
+
+int stream_sync() { return cudaStreamSynchronize(cur_stream()) == cudaSuccess ? MPI_SUCCESS : MPI_ERR_INTERN; }
 
 bool mirror_of(MPI_Datatype t, sp_type *h) {
   std::lock_guard<std::mutex> lk(S().mu);
@@ -179,6 +250,23 @@ bool mirror_of(MPI_Datatype t, sp_type *h) {
   if (it == S().types.end()) return false;
   *h = it->second.h;
   return true;
+}
+
+// the message buffers of a non-blocking request's method
+bool take_buffers(Pending &p, size_t bytes) {
+  if (p.method != SP_METHOD_ONESHOT && !(p.dev = S().dev_pool.take(bytes))) return false;
+  if (p.method != SP_METHOD_DEVICE && !(p.host = S().host_pool.take(bytes))) {
+    S().dev_pool.give(p.dev);
+    p.dev = nullptr;
+    return false;
+  }
+  return true;
+}
+
+void give_buffers(Pending &p) {
+  S().dev_pool.give(p.dev);
+  S().host_pool.give(p.host);
+  p.dev = p.host = nullptr;
 }
 
 // a committed mirror, or nothing
@@ -228,13 +316,13 @@ int pack_message(const Mirror &m, const void *buf, int count, int method, void *
   const int64_t bytes = m.size * count;
   int64_t pos = 0;
   if (method == SP_METHOD_ONESHOT) { // the kernel writes the pinned buffer (zero-copy or chunked DMA)
-    TRY(sp_pack(buf, UINT64_MAX, m.h, count, host, bytes, &pos, S().stream));
+    TRY(sp_pack(buf, UINT64_MAX, m.h, count, host, bytes, &pos, cur_stream()));
     *msg = host;
   } else {
-    TRY(sp_pack(buf, UINT64_MAX, m.h, count, dev, bytes, &pos, S().stream));
+    TRY(sp_pack(buf, UINT64_MAX, m.h, count, dev, bytes, &pos, cur_stream()));
     *msg = dev;
     if (method == SP_METHOD_STAGED) {
-      if (cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, S().stream) != cudaSuccess) return MPI_ERR_INTERN;
+      if (cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, cur_stream()) != cudaSuccess) return MPI_ERR_INTERN;
       *msg = host;
     }
   }
@@ -249,12 +337,12 @@ int unpack_message(const Mirror &m, void *buf, int64_t bytes, int method, void *
   if (n == 0) return MPI_SUCCESS;
   int64_t pos = 0;
   if (method == SP_METHOD_ONESHOT) {
-    TRY(sp_unpack(host, bytes, &pos, m.h, n, buf, UINT64_MAX, S().stream));
+    TRY(sp_unpack(host, bytes, &pos, m.h, n, buf, UINT64_MAX, cur_stream()));
   } else {
     if (method == SP_METHOD_STAGED &&
-        cudaMemcpyAsync(dev, host, n * m.size, cudaMemcpyHostToDevice, S().stream) != cudaSuccess)
+        cudaMemcpyAsync(dev, host, n * m.size, cudaMemcpyHostToDevice, cur_stream()) != cudaSuccess)
       return MPI_ERR_INTERN;
-    TRY(sp_unpack(dev, bytes, &pos, m.h, n, buf, UINT64_MAX, S().stream));
+    TRY(sp_unpack(dev, bytes, &pos, m.h, n, buf, UINT64_MAX, cur_stream()));
   }
   S().st.unpacks++;
   S().st.recvs[method]++;
@@ -308,12 +396,12 @@ void setup() {
     }
   }
   if (!s.gpu) return;
-  // like the engine's own runtime: rank r uses GPU r % ndev unless the
-  // application already chose one (TEMPI_DEVICE overrides)
+  // like the engine's own runtime: local rank r starts on GPU r % ndev
+  // (TEMPI_DEVICE overrides); an application that selects another GPU later
+  // is followed (cur_stream)
   const int local = env_int("TEMPI_LOCAL_RANK", env_int("LOCAL_RANK", env_int("OMPI_COMM_WORLD_LOCAL_RANK", -1)));
   const int dev = env_int("TEMPI_DEVICE", local >= 0 ? local % ndev : -1);
   if (dev >= 0) cudaSetDevice(dev);
-  cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
   const std::string prof = std::getenv("TEMPI_PROFILE") ? std::getenv("TEMPI_PROFILE") : default_profile_path();
   if (!prof.empty() && sp_profile_load(prof.c_str(), &s.profile) == SP_OK)
     sp_model_cache_create(s.profile, &s.model);
@@ -359,15 +447,15 @@ int run_segments(const std::vector<Segment> &segs, bool unpack) {
     }
   }
   if (b) {
-    TRY(sp_batch_execute(b, S().stream));
+    TRY(sp_batch_execute(b, cur_stream()));
   } else { // a form without a strided canon (block-list runs): one call per segment
     for (const auto &g : segs) {
       if (g.count <= 0) continue;
       int64_t pos = g.position;
       if (unpack) {
-        TRY(sp_unpack(g.src, UINT64_MAX, &pos, g.type, g.count, g.dst, UINT64_MAX, S().stream));
+        TRY(sp_unpack(g.src, UINT64_MAX, &pos, g.type, g.count, g.dst, UINT64_MAX, cur_stream()));
       } else {
-        TRY(sp_pack(g.src, UINT64_MAX, g.type, g.count, g.dst, UINT64_MAX, &pos, S().stream));
+        TRY(sp_pack(g.src, UINT64_MAX, g.type, g.count, g.dst, UINT64_MAX, &pos, cur_stream()));
       }
     }
   }
@@ -440,12 +528,14 @@ int MPI_Finalize(void) {
   for (auto &kv : s.batches) sp_batch_free(kv.second);
   s.batches.clear();
   for (Scratch *b : {&s.dev_s, &s.dev_r, &s.host_s, &s.host_r}) b->release();
+  s.dev_pool.clear();
+  s.host_pool.clear();
   if (s.model) sp_model_cache_free(s.model);
   if (s.profile) sp_profile_free(s.profile);
-  if (s.stream) cudaStreamDestroy(s.stream);
+  for (auto &kv : s.streams) cudaStreamDestroy(kv.second);
+  s.streams.clear();
   s.model = nullptr;
   s.profile = nullptr;
-  s.stream = nullptr;
   return REAL(Finalize)();
 }
 
@@ -590,7 +680,7 @@ int MPI_Pack(const void *in, int incount, MPI_Datatype dt, void *out, int outsiz
   }
   if (outsize < 0) return MPI_ERR_ARG;
   int64_t pos = *position;
-  TRY(sp_pack(in, UINT64_MAX, m.h, incount, out, static_cast<uint64_t>(outsize), &pos, S().stream));
+  TRY(sp_pack(in, UINT64_MAX, m.h, incount, out, static_cast<uint64_t>(outsize), &pos, cur_stream()));
   const int rc = stream_sync();
   S().st.packs++;
   *position = static_cast<int>(pos);
@@ -606,7 +696,7 @@ int MPI_Unpack(const void *in, int insize, int *position, void *out, int outcoun
   }
   if (insize < 0) return MPI_ERR_ARG;
   int64_t pos = *position;
-  TRY(sp_unpack(in, static_cast<uint64_t>(insize), &pos, m.h, outcount, out, UINT64_MAX, S().stream));
+  TRY(sp_unpack(in, static_cast<uint64_t>(insize), &pos, m.h, outcount, out, UINT64_MAX, cur_stream()));
   const int rc = stream_sync();
   S().st.unpacks++;
   *position = static_cast<int>(pos);
@@ -662,17 +752,12 @@ int MPI_Isend(const void *buf, int count, MPI_Datatype dt, int dest, int tag, MP
   Pending p;
   p.method = choose(m, count);
   const size_t bytes = static_cast<size_t>(m.size * count);
-  if (p.method != SP_METHOD_ONESHOT && cudaMalloc(&p.dev, bytes) != cudaSuccess) return MPI_ERR_NO_MEM;
-  if (p.method != SP_METHOD_DEVICE && cudaMallocHost(&p.host, bytes) != cudaSuccess) {
-    if (p.dev) cudaFree(p.dev);
-    return MPI_ERR_NO_MEM;
-  }
+  if (!take_buffers(p, bytes)) return MPI_ERR_NO_MEM;
   void *msg = nullptr;
   int rc = pack_message(m, buf, count, p.method, p.dev, p.host, &msg);
   if (rc == MPI_SUCCESS) rc = REAL(Isend)(msg, static_cast<int>(bytes), MPI_BYTE, dest, tag, comm, req);
   if (rc != MPI_SUCCESS) {
-    if (p.dev) cudaFree(p.dev);
-    if (p.host) cudaFreeHost(p.host);
+    give_buffers(p);
     return rc;
   }
   std::lock_guard<std::mutex> lk(S().mu);
@@ -695,16 +780,11 @@ int MPI_Irecv(void *buf, int count, MPI_Datatype dt, int source, int tag, MPI_Co
   p.size = m.size;
   p.method = choose(m, count);
   const size_t bytes = static_cast<size_t>(m.size * count);
-  if (p.method != SP_METHOD_ONESHOT && cudaMalloc(&p.dev, bytes) != cudaSuccess) return MPI_ERR_NO_MEM;
-  if (p.method != SP_METHOD_DEVICE && cudaMallocHost(&p.host, bytes) != cudaSuccess) {
-    if (p.dev) cudaFree(p.dev);
-    return MPI_ERR_NO_MEM;
-  }
+  if (!take_buffers(p, bytes)) return MPI_ERR_NO_MEM;
   const int rc = REAL(Irecv)(recv_target(p.method, p.dev, p.host), static_cast<int>(bytes), MPI_BYTE, source, tag,
                              comm, req);
   if (rc != MPI_SUCCESS) {
-    if (p.dev) cudaFree(p.dev);
-    if (p.host) cudaFreeHost(p.host);
+    give_buffers(p);
     return rc;
   }
   std::lock_guard<std::mutex> lk(S().mu);
@@ -733,8 +813,7 @@ int finish(MPI_Request key, MPI_Status *status, int rc) {
     rc = unpack_message(m, p.user, received(status), p.method, p.dev, p.host);
     status->method = p.method;
   }
-  if (p.dev) cudaFree(p.dev);
-  if (p.host) cudaFreeHost(p.host);
+  give_buffers(p);
   return rc;
 }
 
@@ -840,6 +919,7 @@ int exchange(const void *sbuf, const int scounts[], const int64_t *sdisp_b, cons
   if (!s.accel && !r.accel) return MPI_SUCCESS;
   *done = true;
   State &st = S();
+  st.st.exchanges++;
   std::lock_guard<std::mutex> lk(st.scratch_mu);
   // packed segments stay on the device for a CUDA-aware system MPI, else
   // they are written to (read from) pinned memory by the same launch
@@ -878,7 +958,6 @@ int exchange(const void *sbuf, const int scounts[], const int64_t *sdisp_b, cons
     segs.push_back({rp, r.m[j].h, rcounts[j], static_cast<uint8_t *>(rbuf) + rdisp_b[j], r.offs[j]});
   rc = run_segments(segs, true);
   if (rc == MPI_SUCCESS) rc = stream_sync();
-  st.st.exchanges++;
   return rc;
 }
 

@@ -15,8 +15,9 @@
  *    semantics (lb/ub from the displacements, subarray resized to the full
  *    array);
  *  * CUDA-aware the way a generic MPI is for derived types on device
- *    memory: one cudaMemcpy per contiguous run (the per-block path TEMPI
- *    replaces);
+ *    memory: one cudaMemcpy per contiguous run on the device, the packed
+ *    bytes then crossing to or from host memory in one copy (the per-block
+ *    path TEMPI replaces); contiguous data in one copy;
  *  * transport: UNIX-domain sockets under /tmp/minimpi-<job>/, one
  *    reader thread per incoming connection feeding a FIFO mailbox; every
  *    send is eager (buffered), so MPI_Send never blocks on the receiver.
@@ -134,33 +135,50 @@ static void copy_bytes(void *dst, const void *src, int64_t n, int dev) {
  * (every MPI takes this path for contiguous data) */
 static int dense(const Type *t) { return t->nruns == 1 && t->off[0] == 0 && t->len[0] == t->extent; }
 
-/* gather `count` objects of `t` at buf into out (type-signature byte order) */
+/* gather `count` objects of `t` at buf into out (type-signature byte order).
+ * Device data moves one cudaMemcpy per run on the device; when the other
+ * side is host memory the packed bytes then cross in one copy (what a
+ * CUDA-aware MPI without datatype kernels does) */
 static void gather(const Type *t, const void *buf, int64_t count, uint8_t *out) {
-  const int dev = is_device(buf) || is_device(out);
+  const int dbuf = is_device(buf), dout = is_device(out), dev = dbuf || dout;
   if (dense(t)) {
     copy_bytes(out, buf, count * t->extent, dev);
     return;
   }
+  uint8_t *dst = out, *stage = NULL;
+  if (dbuf && !dout && count * t->size > 0 && cudaMalloc((void **)&stage, (size_t)(count * t->size)) == cudaSuccess)
+    dst = stage;
   int64_t pos = 0;
   for (int64_t e = 0; e < count; ++e)
     for (int64_t i = 0; i < t->nruns; ++i) {
-      copy_bytes(out + pos, (const uint8_t *)buf + e * t->extent + t->off[i], t->len[i], dev);
+      copy_bytes(dst + pos, (const uint8_t *)buf + e * t->extent + t->off[i], t->len[i], dev);
       pos += t->len[i];
     }
+  if (stage) {
+    cudaMemcpy(out, stage, (size_t)pos, cudaMemcpyDeviceToHost);
+    cudaFree(stage);
+  }
 }
 
 static void scatter(const Type *t, const uint8_t *in, int64_t count, void *buf) {
-  const int dev = is_device(buf) || is_device(in);
+  const int dbuf = is_device(buf), din = is_device(in), dev = dbuf || din;
   if (dense(t)) {
     copy_bytes(buf, in, count * t->extent, dev);
     return;
   }
+  uint8_t *stage = NULL;
+  const uint8_t *src = in;
+  if (dbuf && !din && count * t->size > 0 && cudaMalloc((void **)&stage, (size_t)(count * t->size)) == cudaSuccess) {
+    cudaMemcpy(stage, in, (size_t)(count * t->size), cudaMemcpyHostToDevice);
+    src = stage;
+  }
   int64_t pos = 0;
   for (int64_t e = 0; e < count; ++e)
     for (int64_t i = 0; i < t->nruns; ++i) {
-      copy_bytes((uint8_t *)buf + e * t->extent + t->off[i], in + pos, t->len[i], dev);
+      copy_bytes((uint8_t *)buf + e * t->extent + t->off[i], src + pos, t->len[i], dev);
       pos += t->len[i];
     }
+  if (stage) cudaFree(stage);
 }
 
 /* ------------------------------------------------------------ processes, comms */

@@ -171,3 +171,25 @@ def test_interposed_halo_exchange(cuda, sysmpi, grid, mode):
     for s in st.values():  # 3 iterations
         assert s["packs"] == 26 * 3 and s["unpacks"] == 26 * 3 and s["kernels"] > 0
         assert s["exchanges"] == (3 if mode == 1 else 0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("np_", [2, 3])
+def test_interposed_nonblocking_ring(cuda, sysmpi, np_):
+    """tests/native/mpi_isend.c unchanged (written for the engine's own MPI):
+    a ring of Irecv/Isend of 3-D subarrays with every forced method, MPI_Test
+    polling, MPI_Waitall, MPI_Sendrecv, over the system MPI"""
+    _, st = run(np_, build(sysmpi, "mpi_isend", interposed=True))
+    for s in st.values():
+        assert s["packs"] > 0 and s["unpacks"] > 0 and s["kernels"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["a", "b", "ab"])
+def test_interposed_unstructured_exchange(cuda, sysmpi, mode):
+    """tests/native/mpi_unstructured.c unchanged: irregular MPI_Type_indexed
+    gather lists and scattered ghost layouts through MPI_Neighbor_alltoallw
+    (block-list forms: one pack or unpack call per segment) over the system MPI"""
+    _, st = run(2, build(sysmpi, "mpi_unstructured", interposed=False), mode, "3", preload=True)
+    for s in st.values():
+        assert s["exchanges"] >= 3 and s["kernels"] > 0

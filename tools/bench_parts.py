@@ -493,10 +493,12 @@ def interpose_section(timeout_s=240.0, budget_s=2.0):
       * tools/interpose_bench.c: MPI_Pack / MPI_Unpack of the cfg1 vector and
         cfg2 subarrays (E0 = 64, 512) on device memory, MPI_Send/Recv of the
         cfg1 object;
-      * tests/native/mpi_halo.c: the config-5 halo (256^3, r = 2, 32 B, rank
-        grid 2x1x1) as MPI_Pack x26 + MPI_Neighbor_alltoallv + MPI_Unpack
-        x26, and as one MPI_Neighbor_alltoallw of the region types; every
-        ghost cell verified.
+      * tests/native/mpi_halo.c: the config-5 halo (256^3, r = 2, 32 B) on
+        one rank (periodic: all 26 neighbours are the rank itself; two
+        processes on one GPU would time-slice) as MPI_Pack x26 +
+        MPI_Neighbor_alltoallv (MPI_PACKED, forwarded in both legs) +
+        MPI_Unpack x26, and as one MPI_Neighbor_alltoallw of the region
+        types; every ghost cell verified.
     Returns {case: {bytes, system_mpi_us, tempi_us, speedup}}."""
     import json
     import re
@@ -520,11 +522,11 @@ def interpose_section(timeout_s=240.0, budget_s=2.0):
                             "-L" + pkg, "-lstridepack_b200", "-L" + cuda, "-lcudart", "-Wl,-rpath," + d,
                             "-Wl,-rpath," + pkg, "-Wl,-rpath," + cuda], check=True)
 
-        def launch(leg, args):
+        def launch(leg, args, n=2):
             env = dict(os.environ)
             if leg == "tempi":
                 env["LD_PRELOAD"] = os.path.join(pkg, "libtempi_interpose.so")
-            p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "tempirun.py"), "-n", "2", "--timeout",
+            p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "tempirun.py"), "-n", str(n), "--timeout",
                                 str(timeout_s)] + args, capture_output=True, text=True, env=env,
                                timeout=timeout_s + 30)
             if p.returncode != 0:
@@ -536,25 +538,26 @@ def interpose_section(timeout_s=240.0, budget_s=2.0):
             out = launch(leg, [exes["interpose_bench"], str(budget_s)])
             legs[leg] = {r["what"]: r for r in map(json.loads, filter(None, out.splitlines()))}
             for mode in (0, 1):
-                out = launch(leg, [exes["mpi_halo"], "2", "1", "1", "256", "2", "32", "2", str(mode)])
+                out = launch(leg, [exes["mpi_halo"], "1", "1", "1", "256", "2", "32", "2", str(mode)], n=1)
                 m = re.search(r"pack ([\d.]+) us alltoallv ([\d.]+) us unpack ([\d.]+) us bytes/rank (\d+)", out)
                 if not m or "OK" not in out:
                     raise RuntimeError(f"{leg} mpi_halo mode {mode}: {out[-300:]}")
                 tp, tx, tu, nb = float(m[1]), float(m[2]), float(m[3]), int(m[4])
                 if mode == 0:
-                    legs[leg]["halo 2x1x1 MPI_Pack x26"] = {"bytes": nb, "us": tp}
-                    legs[leg]["halo 2x1x1 MPI_Neighbor_alltoallv (MPI_PACKED)"] = {"bytes": nb, "us": tx}
-                    legs[leg]["halo 2x1x1 MPI_Unpack x26"] = {"bytes": nb, "us": tu}
+                    legs[leg]["halo 1x1x1 MPI_Pack x26"] = {"bytes": nb, "us": tp}
+                    legs[leg]["halo 1x1x1 MPI_Neighbor_alltoallv (MPI_PACKED)"] = {"bytes": nb, "us": tx}
+                    legs[leg]["halo 1x1x1 MPI_Unpack x26"] = {"bytes": nb, "us": tu}
                 else:
-                    legs[leg]["halo 2x1x1 MPI_Neighbor_alltoallw (26 region types)"] = {"bytes": nb, "us": tx}
+                    legs[leg]["halo 1x1x1 MPI_Neighbor_alltoallw (26 region types)"] = {"bytes": nb, "us": tx}
     out = {}
     for what, r in legs["tempi"].items():
         s = legs["system_mpi"].get(what)
         out[what] = {"bytes": r["bytes"], "system_mpi_us": s["us"] if s else None, "tempi_us": r["us"],
                      "speedup": round(s["us"] / r["us"], 1) if s and r["us"] > 0 else None}
-    return {"how": "2 ranks on one GPU, same binaries with and without LD_PRELOAD=libtempi_interpose.so; "
-                   "system MPI = tests/native/minimpi.c (contiguous data in one cudaMemcpy, device derived "
-                   "types one cudaMemcpy per contiguous run, socket transport); tools/interpose_bench.c: best "
-                   "of <=5 warm calls; tests/native/mpi_halo.c 2x1x1 256^3 r=2 32 B: wall time of the second "
-                   "of 2 iterations, every ghost cell verified",
+    return {"how": "same binaries with and without LD_PRELOAD=libtempi_interpose.so; system MPI = "
+                   "tests/native/minimpi.c (contiguous data in one cudaMemcpy, device derived types one "
+                   "cudaMemcpy per contiguous run to or from its pageable message buffers, socket transport); "
+                   "tools/interpose_bench.c on 2 ranks (rank 0 packs; Send/Recv 0 -> 1): best of <=5 warm "
+                   "calls; tests/native/mpi_halo.c 1x1x1 256^3 r=2 32 B on 1 rank: wall time of the second of "
+                   "2 iterations, every ghost cell verified",
             "cases": out}
