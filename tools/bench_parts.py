@@ -555,8 +555,9 @@ def interpose_section(timeout_s=240.0, budget_s=2.0):
         out[what] = {"bytes": r["bytes"], "system_mpi_us": s["us"] if s else None, "tempi_us": r["us"],
                      "speedup": round(s["us"] / r["us"], 1) if s and r["us"] > 0 else None}
     return {"how": "same binaries with and without LD_PRELOAD=libtempi_interpose.so; system MPI = "
-                   "tests/native/minimpi.c (contiguous data in one cudaMemcpy, device derived types one "
-                   "cudaMemcpy per contiguous run to or from its pageable message buffers, socket transport); "
+                   "tests/native/minimpi.c (contiguous data in one cudaMemcpy; device derived types one "
+                   "cudaMemcpy per contiguous run on the device, then one copy to or from its host message "
+                   "buffer; socket transport); "
                    "tools/interpose_bench.c on 2 ranks (rank 0 packs; Send/Recv 0 -> 1): best of <=5 warm "
                    "calls; tests/native/mpi_halo.c 1x1x1 256^3 r=2 32 B on 1 rank: wall time of the second of "
                    "2 iterations, every ghost cell verified",
