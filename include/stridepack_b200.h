@@ -185,8 +185,12 @@ enum {
   SP_KERNEL_WORDS64 = 5,  /* generic kernel with 64-bit indexing (chosen
                              automatically beyond 2^32 words or rows) */
   SP_KERNEL_BATCH = 6,    /* many jobs in one launch (sp_batch_*) */
-  SP_KERNEL_SHIFT = 7     /* misaligned rows >= 16 B: aligned 16-B packed
+  SP_KERNEL_SHIFT = 7,    /* misaligned rows >= 16 B: aligned 16-B packed
                              chunks assembled by funnel shifts */
+  SP_KERNEL_DMA = 8       /* no kernel: the copy engines move the rows as
+                             pitched 3-D copies (cudaMemcpy3DAsync; at most
+                             4096 calls, strided forms only) -- the paper's
+                             "GPU DMA engine for non-contiguous data" */
 };
 typedef struct {
   int allow_fallback; /* PackOptions.allow_fallback (default 1) */

@@ -140,6 +140,7 @@ class Kernel(enum.IntEnum):
     Words64 = 5
     Batch = 6
     Shift = 7
+    DMA = 8
 
 
 # ------------------------------------------------------------------ types

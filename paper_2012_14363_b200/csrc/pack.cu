@@ -769,6 +769,53 @@ std::vector<Run> strided_runs(const StridedBlock &sb) {
 
 // Launch on device-accessible pointers. strided: object base (no start);
 // packed: packed buffer base + position.
+// The copy engines instead of SMs (future work: "evaluate
+// the use of the GPU DMA engine for non-contiguous data (e.g.
+// cudaMemcpy2D)"): the row geometry as pitched 3-D copies, a third
+// dimension folded in when its stride is a whole number of pitches, one call
+// per remaining outer index. No SM is used, so the copy can run beside an
+// application's kernels; its rate is set by the copy engines.
+constexpr int64_t kDmaMaxCalls = 4096;
+
+void dma_copy(const RowDims &r, const uint8_t *src, uint8_t *dst, bool pack, cudaStream_t s, sp_launch_info &li) {
+  const size_t w = static_cast<size_t>(r.c0);
+  if (r.cnt.empty()) { // one contiguous row
+    cuda_check(cudaMemcpyAsync(dst, src, w, cudaMemcpyDefault, s), "cudaMemcpyAsync(dma)");
+    li.launches = 1;
+    return;
+  }
+  const int64_t h = r.cnt[0], pitch = r.str[0];
+  if (pitch < r.c0) fail(SP_ERR_UNSUPPORTED, "DMA path: rows overlap (pitch below the row length)");
+  const bool three = r.cnt.size() >= 2 && r.str[1] % pitch == 0 && r.str[1] / pitch >= h;
+  const size_t inner = three ? 2 : 1;
+  const int64_t depth = three ? r.cnt[1] : 1;
+  int64_t outer = 1;
+  for (size_t k = inner; k < r.cnt.size(); ++k) outer *= r.cnt[k];
+  if (outer > kDmaMaxCalls) fail(SP_ERR_UNSUPPORTED, "DMA path: more than 4096 pitched copies");
+  const int64_t block = static_cast<int64_t>(w) * h * depth; // packed bytes per call
+  std::vector<int64_t> idx(r.cnt.size(), 0);
+  for (int64_t o = 0; o < outer; ++o) {
+    int64_t soff = 0;
+    for (size_t k = inner; k < r.cnt.size(); ++k) soff += idx[k] * r.str[k];
+    const uint8_t *strided = (pack ? src : dst) + soff;
+    uint8_t *packed = (pack ? dst : const_cast<uint8_t *>(src)) + o * block;
+    cudaMemcpy3DParms p{};
+    const cudaPitchedPtr sp = make_cudaPitchedPtr(const_cast<uint8_t *>(strided), static_cast<size_t>(pitch), w,
+                                                  three ? static_cast<size_t>(r.str[1] / pitch) : static_cast<size_t>(h));
+    const cudaPitchedPtr pp = make_cudaPitchedPtr(packed, w, w, static_cast<size_t>(h));
+    p.srcPtr = pack ? sp : pp;
+    p.dstPtr = pack ? pp : sp;
+    p.extent = make_cudaExtent(w, static_cast<size_t>(h), static_cast<size_t>(depth));
+    p.kind = cudaMemcpyDefault;
+    cuda_check(cudaMemcpy3DAsync(&p, s), "cudaMemcpy3DAsync(dma)");
+    for (size_t k = inner; k < r.cnt.size(); ++k) { // odometer over the outer dims
+      if (++idx[k] < r.cnt[k]) break;
+      idx[k] = 0;
+    }
+  }
+  li.launches = static_cast<int>(outer);
+}
+
 void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8_t *strided_out,
             const uint8_t *packed_in, uint8_t *packed_out, bool pack, cudaStream_t s,
             const sp_pack_options &opt, sp_launch_info &li) {
@@ -777,6 +824,15 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
   const uint64_t strided_addr = reinterpret_cast<uint64_t>(pack ? strided_in : strided_out);
   const uint64_t packed_addr = reinterpret_cast<uint64_t>(pack ? packed_out : packed_in);
 
+  if (opt.kernel == SP_KERNEL_DMA) {
+    if (ct.form != SP_FORM_STRIDED) fail(SP_ERR_UNSUPPORTED, "DMA path: the type has no strided form");
+    dma_copy(row_dims(ct, count), pack ? strided_in + ct.sb.start : packed_in,
+             pack ? packed_out : strided_out + ct.sb.start, pack, s, li);
+    li.kernel = SP_KERNEL_DMA;
+    li.word = 0;
+    li.grid = li.block = 0;
+    return;
+  }
   bool blocklist = ct.form != SP_FORM_STRIDED || opt.kernel == SP_KERNEL_BLOCKLIST;
   RowDims rd;
   if (!blocklist) {
@@ -1047,7 +1103,8 @@ int64_t execute(const PackArgs &a) {
   // the whole GPU (zero-copy kernels would hold SMs hostage to PCIe latency,
   // and two streams could not overlap inbound and outbound traffic). Small
   // messages keep the zero-copy one-shot path (lowest latency).
-  const bool dma_packed = rp.kind == MemKind::Pinned && packed_len >= kDmaStageMin;
+  // (the copy-engine path reads and writes pinned memory itself)
+  const bool dma_packed = rp.kind == MemKind::Pinned && packed_len >= kDmaStageMin && a.opt.kernel != SP_KERNEL_DMA;
   struct CapGuard {
     explicit CapGuard(bool on) { t_host_grid_cap = on ? kHostGridCap : 0; }
     ~CapGuard() { t_host_grid_cap = 0; }
