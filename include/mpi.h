@@ -170,6 +170,18 @@ int MPI_Neighbor_alltoallw(const void *sendbuf, const int sendcounts[], const MP
                            const MPI_Datatype sendtypes[], void *recvbuf, const int recvcounts[],
                            const MPI_Aint rdispls[], const MPI_Datatype recvtypes[], MPI_Comm comm);
 
+/* all-to-all with derived datatypes (beyond the paper, whose future work
+ * lists collectives): the neighbour machinery over the
+ * complete graph of the communicator -- one typed-copy launch per rank
+ * stores every block at its final strided place in the receiver's buffer.
+ * Alltoallv displacements are in extents, Alltoallw's in bytes (MPI-3.1
+ * 5.8). */
+int MPI_Alltoallv(const void *sendbuf, const int sendcounts[], const int sdispls[], MPI_Datatype sendtype,
+                  void *recvbuf, const int recvcounts[], const int rdispls[], MPI_Datatype recvtype, MPI_Comm comm);
+int MPI_Alltoallw(const void *sendbuf, const int sendcounts[], const int sdispls[], const MPI_Datatype sendtypes[],
+                  void *recvbuf, const int recvcounts[], const int rdispls[], const MPI_Datatype recvtypes[],
+                  MPI_Comm comm);
+
 /* profiling interface: the base implementations under the interposer */
 int PMPI_Init(int *argc, char ***argv);
 int PMPI_Finalize(void);
@@ -195,6 +207,12 @@ int PMPI_Neighbor_alltoallv(const void *sendbuf, const int sendcounts[], const i
 int PMPI_Neighbor_alltoallw(const void *sendbuf, const int sendcounts[], const MPI_Aint sdispls[],
                             const MPI_Datatype sendtypes[], void *recvbuf, const int recvcounts[],
                             const MPI_Aint rdispls[], const MPI_Datatype recvtypes[], MPI_Comm comm);
+
+int PMPI_Alltoallv(const void *sendbuf, const int sendcounts[], const int sdispls[], MPI_Datatype sendtype,
+                   void *recvbuf, const int recvcounts[], const int rdispls[], MPI_Datatype recvtype, MPI_Comm comm);
+int PMPI_Alltoallw(const void *sendbuf, const int sendcounts[], const int sdispls[], const MPI_Datatype sendtypes[],
+                   void *recvbuf, const int recvcounts[], const int rdispls[], const MPI_Datatype recvtypes[],
+                   MPI_Comm comm);
 
 /* TEMPI-specific controls (not MPI): force a transfer method for MPI_Send /
  * MPI_Isend (-1 = model-selected, the default; 0 one-shot, 1 device, 2

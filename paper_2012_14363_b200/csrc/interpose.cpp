@@ -24,9 +24,10 @@
 //    performance model (perf_model.hpp:139-179; Eqs. 1-3, the reference's
 //    three methods -- DIRECT needs the engine's own transport and is not a
 //    candidate here);
-//  * MPI_Neighbor_alltoallv / alltoallw with mirrored types on device
-//    buffers: all segments of a side packed (unpacked) by ONE batched launch
-//    around a single MPI_BYTE exchange of the system MPI.
+//  * MPI_Neighbor_alltoallv / alltoallw and MPI_Alltoallv / Alltoallw with
+//    mirrored types on device buffers: all segments of a side packed
+//    (unpacked) by ONE batched launch around a single MPI_BYTE exchange of
+//    the system MPI.
 // TEMPI_CUDA_AWARE=0 declares a system MPI that cannot read device memory:
 // device-resident packed messages are then staged through pinned memory.
 #include <cuda_runtime.h>
@@ -909,10 +910,12 @@ bool degrees(MPI_Comm comm, int *in, int *out) {
   return true;
 }
 
-// a neighbour exchange with packed MPI_BYTE sides where accelerated
+// a neighbour exchange (all = false) or an all-to-all over the whole
+// communicator (all = true) with packed MPI_BYTE sides where accelerated
 int exchange(const void *sbuf, const int scounts[], const int64_t *sdisp_b, const MPI_Datatype *stypes,
              MPI_Datatype stype, void *rbuf, const int rcounts[], const int64_t *rdisp_b,
-             const MPI_Datatype *rtypes, MPI_Datatype rtype, int indeg, int outdeg, MPI_Comm comm, bool *done) {
+             const MPI_Datatype *rtypes, MPI_Datatype rtype, int indeg, int outdeg, MPI_Comm comm, bool all,
+             bool *done) {
   *done = false;
   Side s = plan_side(sbuf, outdeg, scounts, stypes, stype);
   Side r = plan_side(rbuf, indeg, rcounts, rtypes, rtype);
@@ -950,8 +953,15 @@ int exchange(const void *sbuf, const int scounts[], const int64_t *sdisp_b, cons
     rdb.push_back(r.accel ? r.offs[j] : rdisp_b[j]);
     rtb.push_back(r.accel ? MPI_BYTE : rtypes ? rtypes[j] : rtype);
   }
-  int rc = REAL(Neighbor_alltoallw)(s.accel ? sp : sbuf, scb.data(), sdb.data(), stb.data(), r.accel ? rp : rbuf,
-                                    rcb.data(), rdb.data(), rtb.data(), comm);
+  int rc = MPI_SUCCESS;
+  if (all) { // MPI_Alltoallw: int byte displacements
+    const std::vector<int> sdi(sdb.begin(), sdb.end()), rdi(rdb.begin(), rdb.end());
+    rc = REAL(Alltoallw)(s.accel ? sp : sbuf, scb.data(), sdi.data(), stb.data(), r.accel ? rp : rbuf, rcb.data(),
+                         rdi.data(), rtb.data(), comm);
+  } else {
+    rc = REAL(Neighbor_alltoallw)(s.accel ? sp : sbuf, scb.data(), sdb.data(), stb.data(), r.accel ? rp : rbuf,
+                                  rcb.data(), rdb.data(), rtb.data(), comm);
+  }
   if (rc != MPI_SUCCESS || !r.accel) return rc;
   std::vector<Segment> segs;
   for (int j = 0; j < indeg; ++j)
@@ -975,7 +985,7 @@ int MPI_Neighbor_alltoallv(const void *sbuf, const int scounts[], const int sdis
     for (int j = 0; j < indeg; ++j) rd[j] = static_cast<int64_t>(rdispls[j]) * rm.extent;
     bool done = false;
     const int rc = exchange(sbuf, scounts, sd.data(), nullptr, stype, rbuf, rcounts, rd.data(), nullptr, rtype, indeg,
-                            outdeg, comm, &done);
+                            outdeg, comm, false, &done);
     if (done) return rc;
   }
   S().st.forwarded++;
@@ -990,11 +1000,45 @@ int MPI_Neighbor_alltoallw(const void *sbuf, const int scounts[], const MPI_Aint
     std::vector<int64_t> sd(sdispls, sdispls + outdeg), rd(rdispls, rdispls + indeg);
     bool done = false;
     const int rc = exchange(sbuf, scounts, sd.data(), stypes, MPI_DATATYPE_NULL, rbuf, rcounts, rd.data(), rtypes,
-                            MPI_DATATYPE_NULL, indeg, outdeg, comm, &done);
+                            MPI_DATATYPE_NULL, indeg, outdeg, comm, false, &done);
     if (done) return rc;
   }
   S().st.forwarded++;
   return REAL(Neighbor_alltoallw)(sbuf, scounts, sdispls, stypes, rbuf, rcounts, rdispls, rtypes, comm);
+}
+
+// ============================================================ all-to-all (MPI-3.1 5.8)
+int MPI_Alltoallv(const void *sbuf, const int scounts[], const int sdispls[], MPI_Datatype stype, void *rbuf,
+                  const int rcounts[], const int rdispls[], MPI_Datatype rtype, MPI_Comm comm) {
+  int n = 0;
+  Mirror sm, rm;
+  if (REAL(Comm_size)(comm, &n) == MPI_SUCCESS && committed(stype, &sm) && committed(rtype, &rm)) {
+    std::vector<int64_t> sd(n), rd(n);
+    for (int i = 0; i < n; ++i) {
+      sd[i] = static_cast<int64_t>(sdispls[i]) * sm.extent;
+      rd[i] = static_cast<int64_t>(rdispls[i]) * rm.extent;
+    }
+    bool done = false;
+    const int rc = exchange(sbuf, scounts, sd.data(), nullptr, stype, rbuf, rcounts, rd.data(), nullptr, rtype, n, n,
+                            comm, true, &done);
+    if (done) return rc;
+  }
+  S().st.forwarded++;
+  return REAL(Alltoallv)(sbuf, scounts, sdispls, stype, rbuf, rcounts, rdispls, rtype, comm);
+}
+
+int MPI_Alltoallw(const void *sbuf, const int scounts[], const int sdispls[], const MPI_Datatype stypes[], void *rbuf,
+                  const int rcounts[], const int rdispls[], const MPI_Datatype rtypes[], MPI_Comm comm) {
+  int n = 0;
+  if (REAL(Comm_size)(comm, &n) == MPI_SUCCESS) {
+    std::vector<int64_t> sd(sdispls, sdispls + n), rd(rdispls, rdispls + n);
+    bool done = false;
+    const int rc = exchange(sbuf, scounts, sd.data(), stypes, MPI_DATATYPE_NULL, rbuf, rcounts, rd.data(), rtypes,
+                            MPI_DATATYPE_NULL, n, n, comm, true, &done);
+    if (done) return rc;
+  }
+  S().st.forwarded++;
+  return REAL(Alltoallw)(sbuf, scounts, sdispls, stypes, rbuf, rcounts, rdispls, rtypes, comm);
 }
 
 // ============================================================ TEMPI controls

@@ -719,6 +719,14 @@ int MPI_Comm_free(MPI_Comm *comm) {
 }
 
 // ============================================================ neighbour exchange
+// contiguous bytes: the packed-segment receive of the neighbour alltoallv path
+static bool dense_type(sp_type h) {
+  sp_type_info info{};
+  return sp_type_query(h, &info, nullptr, nullptr, 0) == SP_OK &&
+         (info.form == SP_FORM_EMPTY ||
+          (info.form == SP_FORM_STRIDED && info.ndims == 1 && info.start == 0 && info.extent == info.size));
+}
+
 int PMPI_Neighbor_alltoallv(const void *sendbuf, const int sendcounts[], const int sdispls[], MPI_Datatype sendtype,
                             void *recvbuf, const int recvcounts[], const int rdispls[], MPI_Datatype recvtype,
                             MPI_Comm comm) {
@@ -741,6 +749,20 @@ int PMPI_Neighbor_alltoallv(const void *sendbuf, const int sendcounts[], const i
       rcount.push_back(recvcounts[j]);
       rdisp.push_back(rdispls[j]);
     }
+  if (!dense_type(hr)) {
+    // a strided receive type: every block is a typed copy to its strided
+    // place (the alltoallw path, byte displacements)
+    int64_t se = 0, re = 0;
+    TRY(sp_type_extent(hs, &se));
+    TRY(sp_type_extent(hr, &re));
+    for (auto &d : sdisp) d *= se;
+    for (auto &d : rdisp) d *= re;
+    const std::vector<sp_type> st(dst.size(), hs), rt(src.size(), hr);
+    TRY(sp_rt_neighbor_alltoallw(sendbuf, scount.data(), sdisp.data(), st.data(), static_cast<int64_t>(dst.size()),
+                                 dst.data(), recvbuf, rcount.data(), rdisp.data(), rt.data(),
+                                 static_cast<int64_t>(src.size()), src.data()));
+    return MPI_SUCCESS;
+  }
   TRY(sp_rt_neighbor_alltoallv(sendbuf, scount.data(), sdisp.data(), static_cast<int64_t>(dst.size()), dst.data(),
                                hs, recvbuf, rcount.data(), rdisp.data(), static_cast<int64_t>(src.size()),
                                src.data(), hr));
@@ -789,6 +811,74 @@ int MPI_Neighbor_alltoallw(const void *sendbuf, const int sendcounts[], const MP
                            const MPI_Aint rdispls[], const MPI_Datatype recvtypes[], MPI_Comm comm) {
   return PMPI_Neighbor_alltoallw(sendbuf, sendcounts, sdispls, sendtypes, recvbuf, recvcounts, rdispls, recvtypes,
                                  comm);
+}
+
+// ============================================================ all-to-all
+// MPI_Alltoallv / MPI_Alltoallw (MPI-3.1 5.8) over the communicator's
+// complete graph: the neighbour alltoallw path (one typed-copy launch per
+// rank, blocks stored at their strided place in the receivers' buffers).
+static int alltoall_impl(const void *sendbuf, const int sendcounts[], const std::vector<int64_t> &sdisp_b,
+                         const std::vector<sp_type> &stypes, void *recvbuf, const int recvcounts[],
+                         const std::vector<int64_t> &rdisp_b, const std::vector<sp_type> &rtypes, MPI_Comm comm) {
+  std::vector<int> ranks;
+  if (comm == MPI_COMM_SELF) {
+    ranks.push_back(S().rank);
+  } else {
+    for (int r = 0; r < S().size; ++r) ranks.push_back(r);
+  }
+  const int64_t n = static_cast<int64_t>(ranks.size());
+  if (n > 64) return MPI_ERR_UNSUPPORTED_OPERATION; // the typed-copy path's edge limit
+  std::vector<int64_t> sc(sendcounts, sendcounts + n), rc(recvcounts, recvcounts + n);
+  TRY(sp_rt_neighbor_alltoallw(sendbuf, sc.data(), sdisp_b.data(), stypes.data(), n, ranks.data(), recvbuf,
+                               rc.data(), rdisp_b.data(), rtypes.data(), n, ranks.data()));
+  return MPI_SUCCESS;
+}
+
+int PMPI_Alltoallv(const void *sendbuf, const int sendcounts[], const int sdispls[], MPI_Datatype sendtype,
+                   void *recvbuf, const int recvcounts[], const int rdispls[], MPI_Datatype recvtype, MPI_Comm comm) {
+  if (!comm_of(comm)) return MPI_ERR_COMM;
+  if (!sendcounts || !sdispls || !recvcounts || !rdispls) return MPI_ERR_ARG;
+  TYPE(sendtype, hs);
+  TYPE(recvtype, hr);
+  int64_t se = 0, re = 0;
+  TRY(sp_type_extent(hs, &se));
+  TRY(sp_type_extent(hr, &re));
+  const int n = comm == MPI_COMM_SELF ? 1 : S().size;
+  std::vector<int64_t> sd(n), rd(n);
+  for (int i = 0; i < n; ++i) {
+    sd[i] = static_cast<int64_t>(sdispls[i]) * se;
+    rd[i] = static_cast<int64_t>(rdispls[i]) * re;
+  }
+  return alltoall_impl(sendbuf, sendcounts, sd, std::vector<sp_type>(n, hs), recvbuf, recvcounts, rd,
+                       std::vector<sp_type>(n, hr), comm);
+}
+int MPI_Alltoallv(const void *sendbuf, const int sendcounts[], const int sdispls[], MPI_Datatype sendtype,
+                  void *recvbuf, const int recvcounts[], const int rdispls[], MPI_Datatype recvtype, MPI_Comm comm) {
+  return PMPI_Alltoallv(sendbuf, sendcounts, sdispls, sendtype, recvbuf, recvcounts, rdispls, recvtype, comm);
+}
+
+int PMPI_Alltoallw(const void *sendbuf, const int sendcounts[], const int sdispls[], const MPI_Datatype sendtypes[],
+                   void *recvbuf, const int recvcounts[], const int rdispls[], const MPI_Datatype recvtypes[],
+                   MPI_Comm comm) {
+  if (!comm_of(comm)) return MPI_ERR_COMM;
+  if (!sendcounts || !sdispls || !sendtypes || !recvcounts || !rdispls || !recvtypes) return MPI_ERR_ARG;
+  const int n = comm == MPI_COMM_SELF ? 1 : S().size;
+  std::vector<int64_t> sd(sdispls, sdispls + n), rd(rdispls, rdispls + n);
+  std::vector<sp_type> st, rt;
+  for (int i = 0; i < n; ++i) {
+    TYPE(sendtypes[i], h);
+    st.push_back(h);
+  }
+  for (int j = 0; j < n; ++j) {
+    TYPE(recvtypes[j], h);
+    rt.push_back(h);
+  }
+  return alltoall_impl(sendbuf, sendcounts, sd, st, recvbuf, recvcounts, rd, rt, comm);
+}
+int MPI_Alltoallw(const void *sendbuf, const int sendcounts[], const int sdispls[], const MPI_Datatype sendtypes[],
+                  void *recvbuf, const int recvcounts[], const int rdispls[], const MPI_Datatype recvtypes[],
+                  MPI_Comm comm) {
+  return PMPI_Alltoallw(sendbuf, sendcounts, sdispls, sendtypes, recvbuf, recvcounts, rdispls, recvtypes, comm);
 }
 
 // ============================================================ TEMPI controls

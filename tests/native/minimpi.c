@@ -131,6 +131,13 @@ static void copy_bytes(void *dst, const void *src, int64_t n, int dev) {
     memcpy(dst, src, (size_t)n);
 }
 
+/* a cudaMemcpy from pageable memory may return before its DMA into device
+ * memory has landed: the data must be in place when an MPI call returns,
+ * also for a consumer on a non-blocking stream */
+static void settle(int dev) {
+  if (dev) cudaStreamSynchronize(0);
+}
+
 /* one run that fills its extent: `count` objects are one contiguous block
  * (every MPI takes this path for contiguous data) */
 static int dense(const Type *t) { return t->nruns == 1 && t->off[0] == 0 && t->len[0] == t->extent; }
@@ -143,6 +150,7 @@ static void gather(const Type *t, const void *buf, int64_t count, uint8_t *out) 
   const int dbuf = is_device(buf), dout = is_device(out), dev = dbuf || dout;
   if (dense(t)) {
     copy_bytes(out, buf, count * t->extent, dev);
+    settle(dev);
     return;
   }
   uint8_t *dst = out, *stage = NULL;
@@ -158,12 +166,14 @@ static void gather(const Type *t, const void *buf, int64_t count, uint8_t *out) 
     cudaMemcpy(out, stage, (size_t)pos, cudaMemcpyDeviceToHost);
     cudaFree(stage);
   }
+  settle(dev);
 }
 
 static void scatter(const Type *t, const uint8_t *in, int64_t count, void *buf) {
   const int dbuf = is_device(buf), din = is_device(in), dev = dbuf || din;
   if (dense(t)) {
     copy_bytes(buf, in, count * t->extent, dev);
+    settle(dev);
     return;
   }
   uint8_t *stage = NULL;
@@ -179,6 +189,7 @@ static void scatter(const Type *t, const uint8_t *in, int64_t count, void *buf) 
       pos += t->len[i];
     }
   if (stage) cudaFree(stage);
+  settle(dev);
 }
 
 /* ------------------------------------------------------------ processes, comms */
@@ -466,6 +477,7 @@ int MPI_Finalize(void) ALIAS(MPI_Finalize);
 int PMPI_Abort(MPI_Comm comm, int code) {
   (void)comm;
   fprintf(stderr, "minimpi: MPI_Abort(%d) on rank %d\n", code, G.rank);
+  fflush(NULL); /* the caller's diagnostics on a piped stdout */
   _exit(code ? code : 1);
 }
 int MPI_Abort(MPI_Comm comm, int code) ALIAS(MPI_Abort);
@@ -1072,3 +1084,65 @@ int PMPI_Neighbor_alltoallw(const void *sbuf, const int scounts[], const MPI_Ain
 int MPI_Neighbor_alltoallw(const void *sbuf, const int scounts[], const MPI_Aint sdispls[],
                            const MPI_Datatype stypes[], void *rbuf, const int rcounts[], const MPI_Aint rdispls[],
                            const MPI_Datatype rtypes[], MPI_Comm comm) ALIAS(MPI_Neighbor_alltoallw);
+
+/* ------------------------------------------------------------ all-to-all (MPI-3.1 5.8) */
+#define A2A_TAG (1 << 30) /* apart from the neighbour collectives' occurrence tags */
+
+static int a2a(const void *sbuf, const int scounts[], const int64_t sdisp_b[], const MPI_Datatype stypes[],
+               void *rbuf, const int rcounts[], const int64_t rdisp_b[], const MPI_Datatype rtypes[], MPI_Comm comm) {
+  if (!comm_of(comm)) return MPI_ERR_COMM;
+  const int n = comm == MPI_COMM_SELF ? 1 : G.size, ctx = ctx_of(comm) + 1;
+  for (int i = 0; i < n; ++i) {
+    const Type *t = type_of(stypes[i]);
+    if (!t) return MPI_ERR_TYPE;
+    const int rc = send_typed((const uint8_t *)sbuf + sdisp_b[i], scounts[i], t, world_rank(comm, i), A2A_TAG, ctx);
+    if (rc != MPI_SUCCESS) return rc;
+  }
+  for (int j = 0; j < n; ++j) {
+    const Type *t = type_of(rtypes[j]);
+    if (!t) return MPI_ERR_TYPE;
+    const int rc = recv_typed((uint8_t *)rbuf + rdisp_b[j], rcounts[j], t, world_rank(comm, j), A2A_TAG, ctx, NULL);
+    if (rc != MPI_SUCCESS) return rc;
+  }
+  return MPI_SUCCESS;
+}
+
+int PMPI_Alltoallv(const void *sbuf, const int scounts[], const int sdispls[], MPI_Datatype stype, void *rbuf,
+                   const int rcounts[], const int rdispls[], MPI_Datatype rtype, MPI_Comm comm) {
+  const Type *st = type_of(stype), *rt = type_of(rtype);
+  if (!st || !rt) return MPI_ERR_TYPE;
+  const int n = comm == MPI_COMM_SELF ? 1 : G.size;
+  int64_t *sd = malloc(sizeof(int64_t) * n), *rd = malloc(sizeof(int64_t) * n);
+  MPI_Datatype *sts = malloc(sizeof(MPI_Datatype) * n), *rts = malloc(sizeof(MPI_Datatype) * n);
+  for (int i = 0; i < n; ++i) {
+    sd[i] = (int64_t)sdispls[i] * st->extent;
+    rd[i] = (int64_t)rdispls[i] * rt->extent;
+    sts[i] = stype;
+    rts[i] = rtype;
+  }
+  const int rc = a2a(sbuf, scounts, sd, sts, rbuf, rcounts, rd, rts, comm);
+  free(sd);
+  free(rd);
+  free(sts);
+  free(rts);
+  return rc;
+}
+int MPI_Alltoallv(const void *sbuf, const int scounts[], const int sdispls[], MPI_Datatype stype, void *rbuf,
+                  const int rcounts[], const int rdispls[], MPI_Datatype rtype, MPI_Comm comm) ALIAS(MPI_Alltoallv);
+
+int PMPI_Alltoallw(const void *sbuf, const int scounts[], const int sdispls[], const MPI_Datatype stypes[],
+                   void *rbuf, const int rcounts[], const int rdispls[], const MPI_Datatype rtypes[], MPI_Comm comm) {
+  const int n = comm == MPI_COMM_SELF ? 1 : G.size;
+  int64_t *sd = malloc(sizeof(int64_t) * n), *rd = malloc(sizeof(int64_t) * n);
+  for (int i = 0; i < n; ++i) {
+    sd[i] = sdispls[i];
+    rd[i] = rdispls[i];
+  }
+  const int rc = a2a(sbuf, scounts, sd, stypes, rbuf, rcounts, rd, rtypes, comm);
+  free(sd);
+  free(rd);
+  return rc;
+}
+int MPI_Alltoallw(const void *sbuf, const int scounts[], const int sdispls[], const MPI_Datatype stypes[],
+                  void *rbuf, const int rcounts[], const int rdispls[], const MPI_Datatype rtypes[], MPI_Comm comm)
+    ALIAS(MPI_Alltoallw);

@@ -35,7 +35,7 @@ INTERCEPTED = {
     "MPI_Type_commit", "MPI_Type_free", "MPI_Pack", "MPI_Unpack",
     "MPI_Send", "MPI_Recv", "MPI_Isend", "MPI_Irecv", "MPI_Wait", "MPI_Waitall", "MPI_Test", "MPI_Sendrecv",
     "MPI_Dist_graph_create_adjacent", "MPI_Cart_create", "MPI_Comm_free",
-    "MPI_Neighbor_alltoallv", "MPI_Neighbor_alltoallw",
+    "MPI_Neighbor_alltoallv", "MPI_Neighbor_alltoallw", "MPI_Alltoallv", "MPI_Alltoallw",
 }
 
 
@@ -193,3 +193,14 @@ def test_interposed_unstructured_exchange(cuda, sysmpi, mode):
     _, st = run(2, build(sysmpi, "mpi_unstructured", interposed=False), mode, "3", preload=True)
     for s in st.values():
         assert s["exchanges"] >= 3 and s["kernels"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("np_", [1, 2, 3])
+def test_interposed_alltoall(cuda, sysmpi, np_):
+    """tests/native/mpi_alltoall.c unchanged over the system MPI: MPI_Alltoallv
+    and MPI_Alltoallw with strided device types, one batched pack and unpack
+    launch around the system MPI's byte all-to-all"""
+    _, st = run(np_, build(sysmpi, "mpi_alltoall", interposed=False), preload=True)
+    for s in st.values():
+        assert s["exchanges"] == 3 and s["kernels"] > 0

@@ -88,6 +88,15 @@ def test_mpi_unstructured_loop(cuda, tmp_path, np_):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("np_", [1, 2, 3])
+def test_mpi_alltoallv_alltoallw(cuda, tmp_path, np_):
+    """beyond the paper (its future work names collectives): MPI_Alltoallv
+    and MPI_Alltoallw with strided send or receive types, per-peer types,
+    over the neighbour typed-copy machinery on the complete graph"""
+    assert "OK" in run(np_, build(tmp_path, "mpi_alltoall"))
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("np_", [1, 2])
 def test_mpi_pack_and_sendrecv(cuda, tmp_path, np_):
     assert "OK" in run(np_, build(tmp_path, "mpi_sendrecv"))
