@@ -66,7 +66,9 @@ struct sp_halo_plan_s {
   std::vector<int> out_peers, in_peers; // distinct neighbours
   uint64_t iter = 0;
   bool remote_peers = true; // some neighbour's memory is on another GPU
+  std::vector<uint8_t *> pinned; // peer mappings held for the plan's lifetime
   ~sp_halo_plan_s() {
+    rt_pin_ptrs(pinned, -1);
     batch_destroy(pack);
     batch_destroy(unpack);
     for (auto e : ev)
@@ -325,6 +327,8 @@ sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int metho
       // padded allocation of the rank at +d_j, through its IPC mapping
       std::vector<uint8_t *> peer_alloc;
       rt_exchange_ptr(alloc, peer_alloc);
+      rt_pin_ptrs(peer_alloc, 1);
+      p->pinned.insert(p->pinned.end(), peer_alloc.begin(), peer_alloc.end());
       std::vector<CopySpec> copies;
       for (int j = 0; j < 26; ++j) {
         const int64_t to = halo_rank_of(c, p->rank, regions[j].dir);
@@ -337,7 +341,13 @@ sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int metho
     if (method == SP_HALO_COPY) cuda_check(cudaMalloc(&p->send, static_cast<size_t>(p->seg_total)), "cudaMalloc");
     std::vector<uint8_t *> peer_recv;
     rt_exchange_ptr(p->recv, peer_recv);
-    if (method == SP_HALO_COPY) rt_exchange_ptr(p->send, p->peer_send);
+    rt_pin_ptrs(peer_recv, 1);
+    p->pinned.insert(p->pinned.end(), peer_recv.begin(), peer_recv.end());
+    if (method == SP_HALO_COPY) {
+      rt_exchange_ptr(p->send, p->peer_send);
+      rt_pin_ptrs(p->peer_send, 1);
+      p->pinned.insert(p->pinned.end(), p->peer_send.begin(), p->peer_send.end());
+    }
     for (int j = 0; j < 26; ++j) {
       if (method != SP_HALO_COPY) {
         // segment j of this rank is segment 25-j of the rank at +d_j,
@@ -363,6 +373,8 @@ sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int metho
       cuda_check(cudaMemset(p->flags, 0, 2 * n * sizeof(uint64_t)), "cudaMemset(flags)");
       cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
       rt_exchange_ptr(p->flags, p->peer_flags);
+      rt_pin_ptrs(p->peer_flags, 1);
+      p->pinned.insert(p->pinned.end(), p->peer_flags.begin(), p->peer_flags.end());
       int mydev = 0;
       cuda_check(cudaGetDevice(&mydev), "cudaGetDevice");
       p->remote_peers = false;

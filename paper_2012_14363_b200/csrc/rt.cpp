@@ -37,6 +37,8 @@
 
 namespace spb {
 
+void nbr_reset();
+
 void engine_init(int64_t window_bytes, int64_t host_bytes);
 void engine_fini();
 
@@ -177,7 +179,17 @@ struct Runtime {
   // peers' resources, opened lazily
   std::vector<uint8_t *> peer_window;
   std::vector<uint8_t *> peer_host;
-  std::map<std::string, uint8_t *> ipc_cache; // handle bytes -> mapped base
+  // peers' allocations mapped through CUDA IPC, by handle bytes; `pins`
+  // counts long-lived users (halo plans), unpinned entries are a cache
+  struct IpcMap {
+    uint8_t *p = nullptr;
+    int peer = -1;
+    int pins = 0;
+    uint64_t used = 0; // ipc_clock at the last open_ipc that returned it
+  };
+  std::map<std::string, IpcMap> ipc_cache;
+  uint64_t ipc_clock = 0, ipc_call_mark = 0; // mappings used since the mark belong to the call in progress
+  std::map<const uint8_t *, std::string> exchanged; // rt_exchange_ptr result -> its mapping
   std::deque<Msg> unexpected;
   cudaStream_t stream = nullptr;  // sends, batches, halo plans
   cudaStream_t rstream = nullptr; // receives (unpack of arriving chunks)
@@ -300,21 +312,77 @@ Msg wait_msg(uint32_t kind, int src, int tag) {
   }
 }
 
-uint8_t *open_ipc(const cudaIpcMemHandle_t &h) {
+// A peer that frees an allocation and makes a new one at the same address
+// exports a new handle that the driver refuses to map while this process
+// still maps the old one (cudaErrorAlreadyMapped). The old allocation is
+// gone on the peer's side, so its mapping here is stale: the unpinned
+// mappings of that peer are closed one by one (after the device drained,
+// and with every cached neighbour launch that could name them dropped)
+// until the new handle opens. Mappings the call in progress already uses
+// (since ipc_call_mark) are never closed.
+uint8_t *open_ipc(const cudaIpcMemHandle_t &h, int peer) {
   Runtime &R = rt();
   const std::string key(reinterpret_cast<const char *>(&h), sizeof(h));
+  ++R.ipc_clock;
   auto it = R.ipc_cache.find(key);
-  if (it != R.ipc_cache.end()) return it->second;
+  if (it != R.ipc_cache.end()) {
+    it->second.used = R.ipc_clock;
+    return it->second.p;
+  }
   void *p = nullptr;
-  cuda_check(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
-  R.ipc_cache[key] = static_cast<uint8_t *>(p);
+  cudaError_t err = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+  if (err == cudaErrorAlreadyMapped) {
+    cudaGetLastError();
+    cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize(stale IPC mappings)");
+    nbr_reset();
+    for (auto e = R.ipc_cache.begin(); e != R.ipc_cache.end() && err == cudaErrorAlreadyMapped;) {
+      if (e->second.peer != peer || e->second.pins > 0 || e->second.used > R.ipc_call_mark) {
+        ++e;
+        continue;
+      }
+      cudaIpcCloseMemHandle(e->second.p);
+      for (auto x = R.exchanged.begin(); x != R.exchanged.end();)
+        x = x->second == e->first ? R.exchanged.erase(x) : std::next(x);
+      e = R.ipc_cache.erase(e);
+      err = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+      if (err == cudaErrorAlreadyMapped) cudaGetLastError();
+    }
+  }
+  cuda_check(err, "cudaIpcOpenMemHandle");
+  R.ipc_cache[key] = Runtime::IpcMap{static_cast<uint8_t *>(p), peer, 0, R.ipc_clock};
   return static_cast<uint8_t *>(p);
 }
+
+} // namespace
+
+// a halo plan holds the peer mappings rt_exchange_ptr gave it for its
+// lifetime (pin = +1 at creation, -1 when the plan is freed)
+// marks the start of a call whose mappings must survive stale-mapping eviction
+void ipc_call_begin() {
+  if (g_rt) g_rt->ipc_call_mark = g_rt->ipc_clock;
+}
+
+void rt_pin_ptrs(const std::vector<uint8_t *> &ptrs, int delta) {
+  if (!g_rt) return;
+  Runtime &R = rt();
+  for (const uint8_t *q : ptrs) {
+    auto x = R.exchanged.find(q);
+    if (x == R.exchanged.end()) continue;
+    auto e = R.ipc_cache.find(x->second);
+    if (e != R.ipc_cache.end()) e->second.pins = std::max(0, e->second.pins + delta);
+  }
+}
+
+namespace {
 
 uint8_t *peer_window(int r) {
   Runtime &R = rt();
   if (r == R.rank) return R.window;
-  if (!R.peer_window[r]) R.peer_window[r] = open_ipc(R.shm->slots[r].window);
+  if (!R.peer_window[r]) {
+    R.peer_window[r] = open_ipc(R.shm->slots[r].window, r);
+    const std::string key(reinterpret_cast<const char *>(&R.shm->slots[r].window), sizeof(cudaIpcMemHandle_t));
+    R.ipc_cache[key].pins = 1 << 20; // the runtime's own windows stay mapped until finalize
+  }
   return R.peer_window[r];
 }
 
@@ -445,6 +513,7 @@ void rt_init(int rank, int size, const char *name, int device, int64_t window_by
       if (r != rank && G.shm->slots[r].device >= 0 && !std::memcmp(G.shm->slots[r].uuid, me.uuid, sizeof(me.uuid)))
         G.shared_device = true;
   rt_exchange_ptr(G.nbr_flags, G.peer_nbr_flags);
+  rt_pin_ptrs(G.peer_nbr_flags, 1 << 20); // the neighbour READY counters stay mapped until finalize
   if (device >= 0)
     for (int r = 0; r < size; ++r) {
       cudaPointerAttributes at{};
@@ -462,7 +531,7 @@ void rt_finalize() {
   rt_barrier();
   nbr_reset();
   Runtime &R = *g_rt;
-  for (auto &kv : R.ipc_cache) cudaIpcCloseMemHandle(kv.second);
+  for (auto &kv : R.ipc_cache) cudaIpcCloseMemHandle(kv.second.p);
   for (int r = 0; r < R.size; ++r)
     if (R.peer_host[r] && r != R.rank) {
       cudaHostUnregister(R.peer_host[r]);
@@ -572,6 +641,7 @@ int64_t rt_host_recv(int src, int tag, void *data, int64_t cap) {
 // them mapped into this process (own pointer for self)
 void rt_exchange_ptr(void *local, std::vector<uint8_t *> &out) {
   Runtime &R = rt();
+  ipc_call_begin();
   Slot &me = R.shm->slots[R.rank];
   if (local) {
     ipc_handle_of(local, &me.xh, &me.xoff);
@@ -585,7 +655,8 @@ void rt_exchange_ptr(void *local, std::vector<uint8_t *> &out) {
     if (r == R.rank) {
       out[r] = static_cast<uint8_t *>(local);
     } else if (R.shm->slots[r].xbytes) {
-      out[r] = open_ipc(R.shm->slots[r].xh) + R.shm->slots[r].xoff;
+      out[r] = open_ipc(R.shm->slots[r].xh, r) + R.shm->slots[r].xoff;
+      R.exchanged[out[r]] = std::string(reinterpret_cast<const char *>(&R.shm->slots[r].xh), sizeof(cudaIpcMemHandle_t));
     }
   }
   rt_barrier();
@@ -776,6 +847,7 @@ bool describable(const Committed &ct) {
 // ---- sender
 void send_stream(Req &q) {
   Runtime &R = rt();
+  ipc_call_begin();
   const cudaStream_t s = R.stream;
   if (q.bytes == 0) {
     q.chunks.assign(1, {0, 0});
@@ -783,7 +855,7 @@ void send_stream(Req &q) {
     const Desc &d = R.shm->slots[q.peer].desc[q.grant];
     Committed dst;
     committed_from(d, dst);
-    uint8_t *base = q.peer == R.rank ? reinterpret_cast<uint8_t *>(d.raw) : open_ipc(d.h) + d.off;
+    uint8_t *base = q.peer == R.rank ? reinterpret_cast<uint8_t *>(d.raw) : open_ipc(d.h, q.peer) + d.off;
     if (q.ct->form != SP_FORM_STRIDED) { // block-list send type: pack into the dense receive run
       PackArgs a{};
       a.ct = q.ct.get();
@@ -1566,6 +1638,7 @@ void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &s
                            const std::vector<int64_t> &recv_counts, const std::vector<int64_t> &recv_displs,
                            const Committed &rtp, const std::vector<int> &sources, const std::vector<int> &dests) {
   Runtime &R = rt();
+  ipc_call_begin();
   const Committed &st = *stp;
   if (static_cast<int>(sources.size()) > kMaxEdges) fail(SP_ERR_UNSUPPORTED, "neighbour exchange: indegree > 256");
   const bool dense_recv = rtp.form == SP_FORM_STRIDED && rtp.sb.ndims() == 1 && rtp.sb.start == 0 &&
@@ -1612,7 +1685,7 @@ void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &s
       const int64_t bytes = send_counts[i] * st.size;
       if (bytes > peer.edges[hit][2]) fail(SP_ERR_BUFFER_TOO_SMALL, "neighbour exchange: message truncated");
       if (bytes == 0) continue;
-      uint8_t *base = d == R.rank ? recvbuf : open_ipc(peer.xh) + peer.xoff;
+      uint8_t *base = d == R.rank ? recvbuf : open_ipc(peer.xh, d) + peer.xoff;
       if (blocklist) {
         loose.push_back({stp, sendbuf + send_displs[i] * st.extent, send_counts[i], base + peer.edges[hit][1]});
         continue;
@@ -1730,6 +1803,7 @@ void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &s
                            uint8_t *recvbuf, const std::vector<int64_t> &recv_counts,
                            const std::vector<int64_t> &recv_displs, const std::vector<CommitPtr> &recv_types,
                            const std::vector<int> &sources, const std::vector<int> &dests) {
+  ipc_call_begin();
   const Runtime &R = rt();
   if (static_cast<int>(sources.size()) > kMaxWEdges) fail(SP_ERR_UNSUPPORTED, "neighbour alltoallw: indegree > 64");
   // repeat of the previous call (same buffers, counts, displacements,
@@ -1830,7 +1904,7 @@ void rt_neighbor_alltoallw_build(const uint8_t *sendbuf, const std::vector<int64
       fail(SP_ERR_INVALID_ARGUMENT, "neighbour alltoallw: send and receive describe different byte counts");
     if (bytes == 0) continue;
     const Desc &wd = peer.wdesc[hit];
-    uint8_t *base = (d == R.rank ? recvbuf : open_ipc(peer.xh) + peer.xoff) + peer.edges[hit][1];
+    uint8_t *base = (d == R.rank ? recvbuf : open_ipc(peer.xh, d) + peer.xoff) + peer.edges[hit][1];
     if (wd.runs) {
       // an irregular receive layout: a dense send run scattered through the
       // receiver's run table (read over NVLink from the receiver's HBM)
@@ -1850,8 +1924,8 @@ void rt_neighbor_alltoallw_build(const uint8_t *sendbuf, const std::vector<int64
       } else { // the peer's table, copied into this GPU's HBM once per call layout
         const size_t ns = static_cast<size_t>(wd.npieces) * sizeof(int64_t), nd = ns + sizeof(int64_t);
         auto cs = std::make_shared<TableCopy>(ns), cd = std::make_shared<TableCopy>(nd);
-        copy_sync(cs->p, open_ipc(wd.hs) + wd.os, ns, "run table copy");
-        copy_sync(cd->p, open_ipc(wd.hd) + wd.od, nd, "run table copy");
+        copy_sync(cs->p, open_ipc(wd.hs, d) + wd.os, ns, "run table copy");
+        copy_sync(cd->p, open_ipc(wd.hd, d) + wd.od, nd, "run table copy");
         op.psrc = static_cast<const int64_t *>(cs->p);
         op.pdst = static_cast<const int64_t *>(cd->p);
         tables.push_back(std::move(cs));

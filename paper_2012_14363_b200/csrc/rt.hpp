@@ -37,6 +37,9 @@ void rt_barrier();
 void rt_host_send(int dst, int tag, const void *data, int64_t bytes);
 int64_t rt_host_recv(int src, int tag, void *data, int64_t cap);
 void rt_exchange_ptr(void *local, std::vector<uint8_t *> &out);
+// hold (delta > 0) or release (delta < 0) the peer mappings rt_exchange_ptr
+// returned: held mappings are never evicted as stale
+void rt_pin_ptrs(const std::vector<uint8_t *> &ptrs, int delta);
 void rt_send(const void *buf, uint64_t buf_bytes, int64_t count, CommitPtr ct, int dest, int tag, int method,
              RtTrace *trace);
 void rt_recv(void *buf, uint64_t buf_bytes, int64_t count, CommitPtr ct, int source, int tag, RtStatus *st);

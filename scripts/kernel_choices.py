@@ -69,8 +69,7 @@ def main():
     # irregular hindexed: 65536 blocks of 512-1536 B at random gaps
     rng = np.random.default_rng(5)
     bl = rng.integers(512, 1537, 65536)
-    disp = np.cumsum(bl + rng.integers(16, 2048, 65536)) - bl[0]
-    disp[0] = 0
+    disp = np.concatenate([[0], np.cumsum(bl + rng.integers(16, 2048, 65536))[:-1]])
     it = sp.commit_type(sp.make_hindexed([int(x) for x in bl], [int(x) for x in disp],
                                          sp.make_named(sp.NamedKind.Byte)))
     src = torch.empty(it.span, dtype=torch.uint8, device="cuda")

@@ -3,9 +3,9 @@ usage: python scripts/kernel_choices_table.py <ncu csv> <driver stdout> <out.md>
 
 Per launch: time, algorithmic GB/s (read + write of the described bytes) and
 its fraction of the copy peak, DRAM bytes per algorithmic byte, and sector
-efficiency = useful bytes per 32-B sector the kernel's global loads / stores
-touched (smsp__sass_average_data_bytes_per_sector_mem_global_op_{ld,st}, in
-% of 32 B; TMA launches move data outside the LSU pipe, so they have none)."""
+efficiency = useful bytes / (32 B x global load / store sectors,
+l1tex__t_sectors_pipe_lsu_mem_global_op_{ld,st}); TMA launches move data
+outside the LSU pipe, so they have none."""
 import csv
 import sys
 from collections import OrderedDict
@@ -39,8 +39,9 @@ def main(csv_path, log_path, out_path, peak=6547.2):
            "* alg. GB/s = read + write of the described bytes / time;",
            f"* % peak = alg. GB/s / {peak} (measured copy peak, MEASURED_PEAKS.json);",
            "* DRAM / alg. = (DRAM read + write bytes) / algorithmic bytes (1.0 = no wasted traffic);",
-           "* ld / st eff. = useful bytes per 32-B sector touched by global loads / stores, in % (LSU",
-           "  path only; TMA launches are `-`).", "",
+           "* ld / st eff. = sector efficiency of the global loads / stores: useful bytes (half the",
+           "  algorithmic bytes on each side) / (32 B x l1tex__t_sectors_pipe_lsu_mem_global_op_{ld,st}),",
+           "  in % (LSU path only; TMA moves data outside it, so those launches show `-`).", "",
            "| case | chosen | kernel | us | alg. GB/s | % peak | DRAM GB/s | DRAM / alg. | ld eff. % | st eff. % |",
            "|---|---|---|---:|---:|---:|---:|---:|---:|---:|"]
     for (i, label, nbytes, chosen), m in zip(labels, launches):
@@ -52,12 +53,12 @@ def main(csv_path, log_path, out_path, peak=6547.2):
 
         def eff(name):
             v = m.get(name)
-            return f"{100 * v / 32:.0f}" if isinstance(v, float) and v > 0 else "-"
+            return f"{100 * (alg / 2) / (32 * v):.1f}" if isinstance(v, float) and v > 0 else "-"
 
         out.append(f"| {label} | {chosen} | `{m['kernel'][:28]}` | {us:.1f} | {gbs:.0f} | {100 * gbs / peak:.1f} | "
                    f"{dgbs:.0f} | {dram / alg:.2f} | "
-                   f"{eff('smsp__sass_average_data_bytes_per_sector_mem_global_op_ld')} | "
-                   f"{eff('smsp__sass_average_data_bytes_per_sector_mem_global_op_st')} |")
+                   f"{eff('l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum')} | "
+                   f"{eff('l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum')} |")
     out.append("")
     open(out_path, "w").write("\n".join(out))
 
