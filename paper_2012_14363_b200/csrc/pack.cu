@@ -272,6 +272,8 @@ __global__ void __launch_bounds__(256) k_smallrow(const uint8_t *__restrict__ in
 // below this the LDG/STG kernel wins the TMA unpack (1 MiB single objects:
 // 6.1 vs 8.1 us, bench.py single_object); the sweep's 64 MiB calls keep TMA
 constexpr uint64_t kTmaMinBytes = uint64_t{8} << 20;
+// mean run length from which misaligned runs (word < 8) take k_runs_shift
+constexpr int64_t kRunsShiftMin = 32;
 
 static bool shift_wins(bool pack, int w, int64_t c0) {
   if (pack) return w <= 2 || (w == 4 && c0 % 16 == 0);
@@ -430,6 +432,62 @@ __global__ void __launch_bounds__(256) k_runs(const uint8_t *__restrict__ in, ui
       st_stream(dw + w + 3 * g, e);
     }
     for (; w < words; w += g) st_stream(dw + w, ld_stream(sw + w));
+  }
+}
+
+// Runs whose offsets only allow 1-, 2- or 4-byte words (byte-granular
+// hindexed / struct displacements): the shift technique of k_shift_* per
+// piece. A group of G lanes takes an (object, piece) item; its work unit is
+// an aligned 16-B block of the WRITTEN side, assembled from the aligned 16-B
+// blocks of the read side that hold those bytes (funnel shifts,
+// load_window); the blocks at the two ends of a run are stored masked. Two
+// blocks per lane per step keep up to four 16-B loads in flight.
+template <bool PACK>
+__global__ void __launch_bounds__(256) k_runs_shift(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
+                                                    const int64_t *__restrict__ psrc,
+                                                    const int64_t *__restrict__ pdst, int64_t npieces, int64_t nobj,
+                                                    int64_t extent, int64_t size, int lg) {
+  const int g = 1 << lg;
+  const int lane = static_cast<int>(threadIdx.x) & (g - 1);
+  const int64_t groups = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> lg;
+  const int64_t total = npieces * nobj;
+  for (int64_t p = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> lg; p < total; p += groups) {
+    const int64_t j = p / npieces, k = p - j * npieces;
+    const int64_t s0 = __ldg(psrc + k), d0 = __ldg(pdst + k), len = __ldg(pdst + k + 1) - d0;
+    const uint8_t *src = PACK ? in + j * extent + s0 : in + j * size + d0;
+    uint8_t *dst = PACK ? out + j * size + d0 : out + j * extent + s0;
+    const uintptr_t A = reinterpret_cast<uintptr_t>(dst), E = A + static_cast<uintptr_t>(len);
+    const uintptr_t first = A & ~uintptr_t{15};
+    const int64_t nblk = static_cast<int64_t>(((E + 15) & ~uintptr_t{15}) - first) / 16;
+    auto block = [&](int64_t b, uint4 &z, uintptr_t &B, uintptr_t &vlo, uintptr_t &vhi) {
+      B = first + 16 * static_cast<uintptr_t>(b);
+      vlo = B > A ? B : A;
+      vhi = B + 16 < E ? B + 16 : E;
+      z = load_window(src + static_cast<intptr_t>(B - A), src + (vlo - A), src + (vhi - A));
+    };
+    auto put = [&](const uint4 &z, uintptr_t B, uintptr_t vlo, uintptr_t vhi) {
+      uint8_t *blk = reinterpret_cast<uint8_t *>(B);
+      if (vlo == B && vhi == B + 16) {
+        st_stream(reinterpret_cast<uint4 *>(blk), z);
+      } else {
+        store_masked(blk, z, static_cast<unsigned>(vlo - B), static_cast<unsigned>(vhi - B));
+      }
+    };
+    int64_t b = lane;
+    for (; b + g < nblk; b += 2 * g) { // both windows loaded before either store
+      uint4 z0, z1;
+      uintptr_t B0, l0, h0, B1, l1, h1;
+      block(b, z0, B0, l0, h0);
+      block(b + g, z1, B1, l1, h1);
+      put(z0, B0, l0, h0);
+      put(z1, B1, l1, h1);
+    }
+    if (b < nblk) {
+      uint4 z;
+      uintptr_t B, l, h;
+      block(b, z, B, l, h);
+      put(z, B, l, h);
+    }
   }
 }
 
@@ -855,6 +913,30 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
       if (opt.force_word > w || (opt.force_word & (opt.force_word - 1)))
         fail(SP_ERR_INVALID_ARGUMENT, "force_word is not legal for these buffers");
       w = opt.force_word;
+    }
+    // misaligned runs (word < 8) of 32 B and more on average: 16-B blocks of
+    // the written side assembled by funnel shifts (profiles/r02_kernel_choices.md)
+    const int64_t mean_bytes = ct.size / std::max<int64_t>(dr.n, 1);
+    if (w < 8 && mean_bytes >= kRunsShiftMin && !opt.force_word && opt.kernel != SP_KERNEL_BLOCKLIST) {
+      int lg = 0; // lanes per piece: largest power of two <= the mean blocks per piece, at most 16
+      while (lg < 4 && (int64_t{2} << lg) <= mean_bytes / 16) ++lg;
+      const uint64_t items = static_cast<uint64_t>(dr.n * count) << lg;
+      unsigned grid = 1;
+      if (pack) {
+        grid = resident_grid<k_runs_shift<true>>(items);
+        k_runs_shift<true><<<grid, 256, 0, s>>>(in, out, dr.d_src, dr.d_dst, dr.n, count, ct.extent, ct.size, lg);
+      } else {
+        grid = resident_grid<k_runs_shift<false>>(items);
+        k_runs_shift<false><<<grid, 256, 0, s>>>(in, out, dr.d_src, dr.d_dst, dr.n, count, ct.extent, ct.size, lg);
+      }
+      cuda_check(cudaGetLastError(), "k_runs_shift launch");
+      li.kernel = SP_KERNEL_BLOCKLIST;
+      li.word = 16;
+      li.launches = 1;
+      li.grid = grid;
+      li.block = 256;
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      return;
     }
     // lanes per piece: the largest power of two <= the mean piece length
     // in words, at most 16

@@ -7,7 +7,8 @@ Launch order (the table script relies on it):
   cfg2 E0 = 1..512, K = 64: pack, unpack           (20 launches)
   cfg1 vector(131072,1,64,DOUBLE), K = 64: pack, unpack  (2)
   misaligned subarray (rows of 256 B, start at byte 3), K = 16: pack, unpack (2)
-  irregular hindexed, ~64 MiB, mean block 1 KiB: pack, unpack  (2)
+  irregular hindexed, ~64 MiB, mean block 1 KiB, byte-aligned: pack, unpack  (2)
+  the same rounded to 16 B: pack, unpack  (2)
   halo 256^3 r=2 32 B, one rank: the DIRECT typed-copy batch  (1)
 Each line printed: index, label, algorithmic bytes, kernel/word chosen.
 """
@@ -74,8 +75,18 @@ def main():
                                          sp.make_named(sp.NamedKind.Byte)))
     src = torch.empty(it.span, dtype=torch.uint8, device="cuda")
     dst = torch.zeros(it.size, dtype=torch.uint8, device="cuda")
-    run("irregular hindexed 1 KiB pack", 2 * it.size, lambda: sp.pack(src, it, 1, dst, 0))
-    run("irregular hindexed 1 KiB unpack", 2 * it.size, lambda: sp.unpack(dst, 0, it, 1, src))
+    run("irregular hindexed 1 KiB, byte-aligned pack", 2 * it.size, lambda: sp.pack(src, it, 1, dst, 0))
+    run("irregular hindexed 1 KiB, byte-aligned unpack", 2 * it.size, lambda: sp.unpack(dst, 0, it, 1, src))
+    del src, dst
+    # the same sizes rounded to 16 B: the plain run kernel at word 16
+    bl16 = (bl + 15) // 16 * 16
+    d16 = np.concatenate([[0], np.cumsum(bl16 + rng.integers(1, 128, 65536) * 16)[:-1]])
+    it = sp.commit_type(sp.make_hindexed([int(x) for x in bl16], [int(x) for x in d16],
+                                         sp.make_named(sp.NamedKind.Byte)))
+    src = torch.empty(it.span, dtype=torch.uint8, device="cuda")
+    dst = torch.zeros(it.size, dtype=torch.uint8, device="cuda")
+    run("irregular hindexed 1 KiB, 16-B aligned pack", 2 * it.size, lambda: sp.pack(src, it, 1, dst, 0))
+    run("irregular hindexed 1 KiB, 16-B aligned unpack", 2 * it.size, lambda: sp.unpack(dst, 0, it, 1, src))
     del src, dst
     # halo DIRECT at one rank: the 26 region types as one typed-copy batch
     cfg = H.HaloConfig((1, 1, 1), (256, 256, 256), 2, 32)

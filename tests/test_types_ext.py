@@ -193,6 +193,50 @@ def test_large_irregular_indexed_gpu(sp, cuda, word):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("lens", [(1, 40), (20, 300), (200, 3000)])
+def test_misaligned_runs_shift_kernel(sp, cuda, lens):
+    """byte-granular hindexed displacements and lengths (word 1): runs of 32 B
+    and more on average take k_runs_shift (16-B blocks of the written side
+    assembled by funnel shifts), shorter ones the plain run kernel; pack and
+    unpack of 3 objects vs the MPI typemap restatement, an unaligned packed
+    position, and the bytes between runs untouched"""
+    torch = cuda
+    rng = np.random.default_rng(lens[1])
+    n = 4000
+    bls = rng.integers(lens[0], lens[1] + 1, n).tolist()
+    gaps = rng.integers(0, 97, n).tolist()
+    displs, at = [], 3
+    for b, g in zip(bls, gaps):
+        at += g
+        displs.append(at)
+        at += b
+    perm = rng.permutation(n)
+    bls = [bls[i] for i in perm]
+    displs = [displs[i] for i in perm]
+    c = sp.commit_type(sp.make_hindexed(bls, displs, sp.make_named(sp.NamedKind.Byte)))
+    assert c.form == sp.CanonForm.Unsupported and not c.overlapping
+    runs = list(zip(displs, bls))
+    inc, pos = 3, 5
+    span = (inc - 1) * c.extent + c.span
+    host = rng.integers(0, 256, span, dtype=np.uint8)
+    want = tm.gather(host, runs, inc, c.extent, c.size)
+    dst = torch.full((pos + inc * c.size + 16,), 0xEE, dtype=torch.uint8, device="cuda")
+    sp.pack(torch.from_numpy(host).cuda(), c, inc, dst, pos)
+    li = sp.last_launch()
+    shifted = c.size / n >= 32
+    assert li.kernel == sp.Kernel.BlockList and li.word == (16 if shifted else 1), (li, c.size / n)
+    got = dst.cpu().numpy()
+    assert np.array_equal(got[pos:pos + inc * c.size], want)
+    assert (got[:pos] == 0xEE).all() and (got[pos + inc * c.size:] == 0xEE).all()
+    init = rng.integers(0, 256, span, dtype=np.uint8)
+    out = torch.from_numpy(init.copy()).cuda()
+    sp.unpack(dst, pos, c, inc, out)
+    assert sp.last_launch().word == (16 if shifted else 1)
+    exp = tm.scatter(want, init.copy(), runs, inc, c.extent)
+    assert np.array_equal(out.cpu().numpy(), exp)
+
+
+@pytest.mark.gpu
 def test_typed_copy_with_irregular_side(sp, cuda):
     """sp.copy (typed copy) with a block-list layout on one side and a dense
     run on the other: gather (irregular -> contiguous) and scatter
