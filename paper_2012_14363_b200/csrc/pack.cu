@@ -273,7 +273,10 @@ __global__ void __launch_bounds__(256) k_smallrow(const uint8_t *__restrict__ in
 // 6.1 vs 8.1 us, bench.py single_object); the sweep's 64 MiB calls keep TMA
 constexpr uint64_t kTmaMinBytes = uint64_t{8} << 20;
 // mean run length from which misaligned runs (word < 8) take k_runs_shift
-constexpr int64_t kRunsShiftMin = 32;
+// (scripts/runs_bench.py --misaligned: pack wins from 32 B; unpack, whose
+// run ends are masked stores, from 256 B -- below it the byte-word kernel
+// ties or wins)
+constexpr int64_t kRunsShiftMinPack = 32, kRunsShiftMinUnpack = 256;
 
 static bool shift_wins(bool pack, int w, int64_t c0) {
   if (pack) return w <= 2 || (w == 4 && c0 % 16 == 0);
@@ -435,13 +438,37 @@ __global__ void __launch_bounds__(256) k_runs(const uint8_t *__restrict__ in, ui
   }
 }
 
+// the 16 bytes starting d bytes into x0, continuing into x1 (d < 16)
+__device__ __forceinline__ uint4 funnel16(const uint4 &x0, const uint4 &x1, unsigned d) {
+  const uint32_t W[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+  const unsigned q = d >> 2, sh = (d & 3) * 8;
+  uint32_t v[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) { // v[k] = W[k + q], selects instead of local memory
+    const uint32_t a = k + 0 < 8 ? W[k] : 0, b = k + 1 < 8 ? W[k + 1] : 0;
+    const uint32_t c = k + 2 < 8 ? W[k + 2] : 0, e = k + 3 < 8 ? W[k + 3] : 0;
+    v[k] = q == 0 ? a : q == 1 ? b : q == 2 ? c : e;
+  }
+  return make_uint4(__funnelshift_r(v[0], v[1], sh), __funnelshift_r(v[1], v[2], sh),
+                    __funnelshift_r(v[2], v[3], sh), __funnelshift_r(v[3], v[4], sh));
+}
+
+__device__ __forceinline__ uint4 shfl_down4(unsigned mask, const uint4 &x, int width) {
+  return make_uint4(__shfl_down_sync(mask, x.x, 1, width), __shfl_down_sync(mask, x.y, 1, width),
+                    __shfl_down_sync(mask, x.z, 1, width), __shfl_down_sync(mask, x.w, 1, width));
+}
+
 // Runs whose offsets only allow 1-, 2- or 4-byte words (byte-granular
 // hindexed / struct displacements): the shift technique of k_shift_* per
-// piece. A group of G lanes takes an (object, piece) item; its work unit is
-// an aligned 16-B block of the WRITTEN side, assembled from the aligned 16-B
-// blocks of the read side that hold those bytes (funnel shifts,
-// load_window); the blocks at the two ends of a run are stored masked. Two
-// blocks per lane per step keep up to four 16-B loads in flight.
+// piece. A group of G lanes takes an (object, piece) item; lane l of the
+// group owns aligned 16-B block c*G + l of the WRITTEN side. Consecutive
+// written blocks read consecutive aligned 16-B blocks of the read side at
+// one fixed byte shift, so each lane loads ONE aligned read block and takes
+// the next one from its neighbour lane (a shuffle; the group's last lane
+// loads its own), then assembles its 16 bytes with funnel shifts. Only read
+// blocks that intersect the run are loaded; the blocks at the two ends of a
+// run are stored masked. Every lane of a group runs the same trip count,
+// so the shuffles name just the group's lanes.
 template <bool PACK>
 __global__ void __launch_bounds__(256) k_runs_shift(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
                                                     const int64_t *__restrict__ psrc,
@@ -449,23 +476,37 @@ __global__ void __launch_bounds__(256) k_runs_shift(const uint8_t *__restrict__ 
                                                     int64_t extent, int64_t size, int lg) {
   const int g = 1 << lg;
   const int lane = static_cast<int>(threadIdx.x) & (g - 1);
+  const unsigned gmask = (g == 32 ? 0xffffffffu : ((1u << g) - 1u)) << ((threadIdx.x & 31) & ~(g - 1));
   const int64_t groups = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> lg;
   const int64_t total = npieces * nobj;
+  const uint4 zero = make_uint4(0, 0, 0, 0);
   for (int64_t p = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> lg; p < total; p += groups) {
     const int64_t j = p / npieces, k = p - j * npieces;
     const int64_t s0 = __ldg(psrc + k), d0 = __ldg(pdst + k), len = __ldg(pdst + k + 1) - d0;
     const uint8_t *src = PACK ? in + j * extent + s0 : in + j * size + d0;
     uint8_t *dst = PACK ? out + j * size + d0 : out + j * extent + s0;
     const uintptr_t A = reinterpret_cast<uintptr_t>(dst), E = A + static_cast<uintptr_t>(len);
+    const uintptr_t S = reinterpret_cast<uintptr_t>(src), SE = S + static_cast<uintptr_t>(len);
     const uintptr_t first = A & ~uintptr_t{15};
     const int64_t nblk = static_cast<int64_t>(((E + 15) & ~uintptr_t{15}) - first) / 16;
-    auto block = [&](int64_t b, uint4 &z, uintptr_t &B, uintptr_t &vlo, uintptr_t &vhi) {
-      B = first + 16 * static_cast<uintptr_t>(b);
-      vlo = B > A ? B : A;
-      vhi = B + 16 < E ? B + 16 : E;
-      z = load_window(src + static_cast<intptr_t>(B - A), src + (vlo - A), src + (vhi - A));
+    // read address of written block B is B + (S - A): a fixed byte shift
+    const uintptr_t r0 = first + (S - A);
+    const unsigned d = static_cast<unsigned>(r0 & 15);
+    // written block b: its aligned read block, the next one (neighbour lane
+    // or own load), the assembled 16 bytes, the (masked) store
+    auto load = [&](int64_t b, uint4 &x0, uint4 &x1) {
+      const uintptr_t rb = (r0 & ~uintptr_t{15}) + 16 * static_cast<uintptr_t>(b);
+      x0 = b < nblk && rb < SE && rb + 16 > S ? ld_stream(reinterpret_cast<const uint4 *>(rb)) : zero;
+      const uintptr_t nb = rb + 16;
+      const bool own = lane == g - 1 || b + 1 >= nblk;
+      x1 = own && b < nblk && d && nb < SE && nb + 16 > S ? ld_stream(reinterpret_cast<const uint4 *>(nb)) : zero;
     };
-    auto put = [&](const uint4 &z, uintptr_t B, uintptr_t vlo, uintptr_t vhi) {
+    auto put = [&](int64_t b, const uint4 &x0, uint4 x1, const uint4 &nx) {
+      if (!(lane == g - 1 || b + 1 >= nblk)) x1 = nx;
+      if (b >= nblk) return;
+      const uint4 z = d ? funnel16(x0, x1, d) : x0;
+      const uintptr_t B = first + 16 * static_cast<uintptr_t>(b);
+      const uintptr_t vlo = B > A ? B : A, vhi = B + 16 < E ? B + 16 : E;
       uint8_t *blk = reinterpret_cast<uint8_t *>(B);
       if (vlo == B && vhi == B + 16) {
         st_stream(reinterpret_cast<uint4 *>(blk), z);
@@ -473,20 +514,20 @@ __global__ void __launch_bounds__(256) k_runs_shift(const uint8_t *__restrict__ 
         store_masked(blk, z, static_cast<unsigned>(vlo - B), static_cast<unsigned>(vhi - B));
       }
     };
-    int64_t b = lane;
-    for (; b + g < nblk; b += 2 * g) { // both windows loaded before either store
-      uint4 z0, z1;
-      uintptr_t B0, l0, h0, B1, l1, h1;
-      block(b, z0, B0, l0, h0);
-      block(b + g, z1, B1, l1, h1);
-      put(z0, B0, l0, h0);
-      put(z1, B1, l1, h1);
+    int64_t c = 0;
+    for (; c + g < nblk; c += 2 * g) { // two chunks of G blocks: up to four loads in flight per lane
+      uint4 a0, a1, b0, b1;
+      load(c + lane, a0, a1);
+      load(c + g + lane, b0, b1);
+      const uint4 na = shfl_down4(gmask, a0, g), nb = shfl_down4(gmask, b0, g);
+      put(c + lane, a0, a1, na);
+      put(c + g + lane, b0, b1, nb);
     }
-    if (b < nblk) {
-      uint4 z;
-      uintptr_t B, l, h;
-      block(b, z, B, l, h);
-      put(z, B, l, h);
+    if (c < nblk) {
+      uint4 a0, a1;
+      load(c + lane, a0, a1);
+      const uint4 na = shfl_down4(gmask, a0, g);
+      put(c + lane, a0, a1, na);
     }
   }
 }
@@ -917,9 +958,13 @@ void launch(const Committed &ct, int64_t count, const uint8_t *strided_in, uint8
     // misaligned runs (word < 8) of 32 B and more on average: 16-B blocks of
     // the written side assembled by funnel shifts (profiles/r02_kernel_choices.md)
     const int64_t mean_bytes = ct.size / std::max<int64_t>(dr.n, 1);
-    if (w < 8 && mean_bytes >= kRunsShiftMin && !opt.force_word && opt.kernel != SP_KERNEL_BLOCKLIST) {
-      int lg = 0; // lanes per piece: largest power of two <= the mean blocks per piece, at most 16
-      while (lg < 4 && (int64_t{2} << lg) <= mean_bytes / 16) ++lg;
+    if (w < 8 && mean_bytes >= (pack ? kRunsShiftMinPack : kRunsShiftMinUnpack) && !opt.force_word &&
+        opt.kernel != SP_KERNEL_BLOCKLIST) {
+      // lanes per piece: the largest power of two G with 2G <= the mean
+      // 16-B blocks per piece (each lane moves two chunks of G blocks per
+      // step), at most 16
+      int lg = 0;
+      while (lg < 4 && (int64_t{4} << lg) <= mean_bytes / 16) ++lg;
       const uint64_t items = static_cast<uint64_t>(dr.n * count) << lg;
       unsigned grid = 1;
       if (pack) {
