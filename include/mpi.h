@@ -26,6 +26,7 @@ extern "C" {
 typedef int MPI_Datatype;
 typedef int MPI_Comm;
 typedef int MPI_Request;
+typedef int MPI_Info;
 typedef int64_t MPI_Aint;
 typedef int64_t MPI_Count;
 
@@ -72,7 +73,7 @@ typedef struct {
 #define MPI_STATUSES_IGNORE ((MPI_Status *)0)
 #define MPI_REQUEST_NULL ((MPI_Request)0)
 #define MPI_UNWEIGHTED ((int *)0)
-#define MPI_INFO_NULL 0
+#define MPI_INFO_NULL ((MPI_Info)0)
 #define MPI_ORDER_C 56
 #define MPI_ORDER_FORTRAN 57
 #define MPI_THREAD_SINGLE 0
@@ -142,6 +143,13 @@ int MPI_Irecv(void *buf, int count, MPI_Datatype datatype, int source, int tag, 
 int MPI_Wait(MPI_Request *request, MPI_Status *status);
 int MPI_Waitall(int count, MPI_Request requests[], MPI_Status statuses[]);
 int MPI_Test(MPI_Request *request, int *flag, MPI_Status *status);
+/* completion of any / some / all of a set (MPI-3.1 3.7.5); MPI_Request_free
+ * of an active request completes it first */
+int MPI_Waitany(int count, MPI_Request requests[], int *index, MPI_Status *status);
+int MPI_Waitsome(int incount, MPI_Request requests[], int *outcount, int indices[], MPI_Status statuses[]);
+int MPI_Testany(int count, MPI_Request requests[], int *index, int *flag, MPI_Status *status);
+int MPI_Testall(int count, MPI_Request requests[], int *flag, MPI_Status statuses[]);
+int MPI_Request_free(MPI_Request *request);
 int MPI_Sendrecv(const void *sendbuf, int sendcount, MPI_Datatype sendtype, int dest, int sendtag, void *recvbuf,
                  int recvcount, MPI_Datatype recvtype, int source, int recvtag, MPI_Comm comm,
                  MPI_Status *status);
@@ -149,7 +157,7 @@ int MPI_Sendrecv(const void *sendbuf, int sendcount, MPI_Datatype sendtype, int 
 /* topologies + neighbourhood exchange (accelerated: fused pack-to-peer) */
 int MPI_Dist_graph_create_adjacent(MPI_Comm comm_old, int indegree, const int sources[],
                                    const int sourceweights[], int outdegree, const int destinations[],
-                                   const int destweights[], int info, int reorder, MPI_Comm *comm_dist_graph);
+                                   const int destweights[], MPI_Info info, int reorder, MPI_Comm *comm_dist_graph);
 int MPI_Dist_graph_neighbors_count(MPI_Comm comm, int *indegree, int *outdegree, int *weighted);
 int MPI_Dist_graph_neighbors(MPI_Comm comm, int maxindegree, int sources[], int sourceweights[],
                              int maxoutdegree, int destinations[], int destweights[]);

@@ -233,13 +233,16 @@ int to_mpi(sp_status st) {
   } while (0)
 
 // the interposer's stream on the application's CURRENT device (an
-// application may select its GPU after MPI_Init)
+// application may select its GPU after MPI_Init). A blocking stream: the
+// kernels of an MPI call run after everything the application issued
+// before it on the legacy default stream (a cudaMemset of the receive
+// buffer, say), as users of a CUDA-aware MPI expect.
 cudaStream_t cur_stream() {
   int d = 0;
   cudaGetDevice(&d);
   std::lock_guard<std::mutex> lk(S().mu);
   cudaStream_t &st = S().streams[d];
-  if (!st) cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (!st) cudaStreamCreate(&st);
   return st;
 }
 
@@ -348,6 +351,17 @@ int unpack_message(const Mirror &m, void *buf, int64_t bytes, int method, void *
   S().st.unpacks++;
   S().st.recvs[method]++;
   return stream_sync();
+}
+
+// the transfer method of a receive, in the status field this image's mpi.h
+// has for it; a vendor MPI_Status has no such field
+void report_method(MPI_Status *st, int method) {
+#ifdef TEMPI_B200_MPI_H
+  st->method = method;
+#else
+  (void)st;
+  (void)method;
+#endif
 }
 
 // bytes a completed receive of MPI_BYTE delivered, asked of the system MPI
@@ -738,7 +752,7 @@ int MPI_Recv(void *buf, int count, MPI_Datatype dt, int source, int tag, MPI_Com
   MPI_Status st{};
   int rc = REAL(Recv)(recv_target(method, dev, host), static_cast<int>(bytes), MPI_BYTE, source, tag, comm, &st);
   if (rc == MPI_SUCCESS) rc = unpack_message(m, buf, received(&st), method, dev, host);
-  st.method = method;
+  report_method(&st, method);
   if (status) *status = st;
   return rc;
 }
@@ -812,7 +826,7 @@ int finish(MPI_Request key, MPI_Status *status, int rc) {
     m.h = p.type;
     m.size = p.size;
     rc = unpack_message(m, p.user, received(status), p.method, p.dev, p.host);
-    status->method = p.method;
+    report_method(status, p.method);
   }
   give_buffers(p);
   return rc;
@@ -853,6 +867,74 @@ int MPI_Waitall(int n, MPI_Request reqs[], MPI_Status statuses[]) {
   return first;
 }
 
+// the set forms of MPI-3.1 3.7.5: the system MPI completes, the interposer
+// then unpacks the receives among the completed requests (their handles
+// are saved first: completion resets them to MPI_REQUEST_NULL)
+int MPI_Waitany(int n, MPI_Request reqs[], int *index, MPI_Status *status) {
+  if (n < 0 || (n && !reqs) || !index) return MPI_ERR_ARG;
+  const std::vector<MPI_Request> keys(reqs, reqs + n);
+  MPI_Status st{};
+  const int rc = REAL(Waitany)(n, reqs, index, &st);
+  int out = rc;
+  if (*index != MPI_UNDEFINED && *index >= 0 && *index < n) out = finish(keys[*index], &st, rc);
+  if (status) *status = st;
+  return out;
+}
+
+int MPI_Testany(int n, MPI_Request reqs[], int *index, int *flag, MPI_Status *status) {
+  if (n < 0 || (n && !reqs) || !index || !flag) return MPI_ERR_ARG;
+  const std::vector<MPI_Request> keys(reqs, reqs + n);
+  MPI_Status st{};
+  const int rc = REAL(Testany)(n, reqs, index, flag, &st);
+  int out = rc;
+  if (*flag && *index != MPI_UNDEFINED && *index >= 0 && *index < n) out = finish(keys[*index], &st, rc);
+  if (status) *status = st;
+  return out;
+}
+
+int MPI_Waitsome(int n, MPI_Request reqs[], int *outcount, int indices[], MPI_Status statuses[]) {
+  if (n < 0 || (n && !reqs) || !outcount) return MPI_ERR_ARG;
+  const std::vector<MPI_Request> keys(reqs, reqs + n);
+  std::vector<MPI_Status> st(std::max(n, 1));
+  const int rc = REAL(Waitsome)(n, reqs, outcount, indices, st.data());
+  int out = rc;
+  if (*outcount != MPI_UNDEFINED)
+    for (int i = 0; i < *outcount; ++i) {
+      const int r = finish(keys[indices[i]], &st[i], rc);
+      if (r != MPI_SUCCESS && out == MPI_SUCCESS) out = r;
+      if (statuses) statuses[i] = st[i];
+    }
+  return out;
+}
+
+int MPI_Testall(int n, MPI_Request reqs[], int *flag, MPI_Status statuses[]) {
+  if (n < 0 || (n && !reqs) || !flag) return MPI_ERR_ARG;
+  const std::vector<MPI_Request> keys(reqs, reqs + n);
+  std::vector<MPI_Status> st(std::max(n, 1));
+  const int rc = REAL(Testall)(n, reqs, flag, st.data());
+  int out = rc;
+  if (*flag)
+    for (int i = 0; i < n; ++i) {
+      const int r = finish(keys[i], &st[i], rc);
+      if (r != MPI_SUCCESS && out == MPI_SUCCESS) out = r;
+      if (statuses) statuses[i] = st[i];
+    }
+  return out;
+}
+
+// an interposed request must still unpack (a receive) or keep its packed
+// buffer until the system MPI is done with it (a send): it is completed here
+int MPI_Request_free(MPI_Request *req) {
+  if (!req) return MPI_ERR_ARG;
+  bool ours = false;
+  {
+    std::lock_guard<std::mutex> lk(S().mu);
+    ours = S().pending.count(*req) != 0;
+  }
+  if (!ours) return REAL(Request_free)(req);
+  return MPI_Wait(req, MPI_STATUS_IGNORE);
+}
+
 // through the intercepted non-blocking calls, so both halves are accelerated
 int MPI_Sendrecv(const void *sbuf, int scount, MPI_Datatype stype, int dest, int stag, void *rbuf, int rcount,
                  MPI_Datatype rtype, int source, int rtag, MPI_Comm comm, MPI_Status *status) {
@@ -871,7 +953,7 @@ int MPI_Sendrecv(const void *sbuf, int scount, MPI_Datatype stype, int dest, int
 
 // ============================================================ topologies (degrees recorded for the exchanges)
 int MPI_Dist_graph_create_adjacent(MPI_Comm old, int indeg, const int sources[], const int sw[], int outdeg,
-                                   const int dests[], const int dw[], int info, int reorder, MPI_Comm *out) {
+                                   const int dests[], const int dw[], MPI_Info info, int reorder, MPI_Comm *out) {
   const int rc = REAL(Dist_graph_create_adjacent)(old, indeg, sources, sw, outdeg, dests, dw, info, reorder, out);
   if (rc == MPI_SUCCESS && out) {
     std::lock_guard<std::mutex> lk(S().mu);

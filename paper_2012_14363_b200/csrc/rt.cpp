@@ -474,8 +474,13 @@ void rt_init(int rank, int size, const char *name, int device, int64_t window_by
     cudaDeviceProp prop{};
     cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
     std::memcpy(me.uuid, prop.uuid.bytes, sizeof(me.uuid));
-    cuda_check(cudaStreamCreateWithFlags(&G.stream, cudaStreamNonBlocking), "cudaStreamCreate");
-    cuda_check(cudaStreamCreateWithFlags(&G.rstream, cudaStreamNonBlocking), "cudaStreamCreate");
+    // blocking streams: a call that writes or reads a user buffer runs after
+    // everything the application issued before it on the legacy default
+    // stream (cudaMemset / cudaMemcpy / <<<>>> launches), as users of a
+    // CUDA-aware MPI expect; work on the application's own non-blocking
+    // streams still needs the application's synchronisation
+    cuda_check(cudaStreamCreate(&G.stream), "cudaStreamCreate");
+    cuda_check(cudaStreamCreate(&G.rstream), "cudaStreamCreate");
     if (window_bytes > 0) {
       cuda_check(cudaMalloc(&G.window, static_cast<size_t>(window_bytes)), "cudaMalloc(window)");
       cuda_check(cudaIpcGetMemHandle(&me.window, G.window), "cudaIpcGetMemHandle(window)");

@@ -39,7 +39,16 @@ struct State {
   std::unordered_map<int, Comm> comms;
   int next_comm = 100;
   int forced_method = -1;
-  std::unordered_map<int, sp_request> requests; // MPI_Request -> engine request
+  // MPI_Request -> engine request, and its outcome once the engine reported
+  // it complete but the MPI handle has not been released yet (MPI_Testall
+  // must leave every request untouched until all are done)
+  struct Pending {
+    sp_request r = 0;
+    bool done = false;
+    sp_status rc = SP_OK;
+    int64_t st[4] = {0, 0, 0, 0};
+  };
+  std::unordered_map<int, Pending> requests;
   int next_request = 1;
   sp_profile profile = nullptr;
   cudaStream_t stream = nullptr;
@@ -165,7 +174,7 @@ int PMPI_Init(int *, char ***) {
   }
   if (s.device >= 0) {
     cudaSetDevice(s.device);
-    cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
+    cudaStreamCreate(&s.stream); // blocking: ordered after the application's legacy-stream work
   }
   std::string prof = std::getenv("TEMPI_PROFILE") ? std::getenv("TEMPI_PROFILE") : default_profile_path();
   if (!prof.empty() && sp_profile_load(prof.c_str(), &s.profile) == SP_OK) sp_rt_set_profile(s.profile);
@@ -503,7 +512,7 @@ static int isend_impl(const void *buf, int count, MPI_Datatype datatype, int des
   TRY(sp_rt_isend(buf, UINT64_MAX, count, h, dest, tag, method, &r));
   std::lock_guard<std::mutex> lk(S().mu);
   const int id = S().next_request++;
-  S().requests[id] = r;
+  S().requests[id].r = r;
   *request = id;
   return MPI_SUCCESS;
 }
@@ -530,7 +539,7 @@ int PMPI_Irecv(void *buf, int count, MPI_Datatype datatype, int source, int tag,
   TRY(sp_rt_irecv(buf, UINT64_MAX, count, h, source, tag, &r));
   std::lock_guard<std::mutex> lk(S().mu);
   const int id = S().next_request++;
-  S().requests[id] = r;
+  S().requests[id].r = r;
   *request = id;
   return MPI_SUCCESS;
 }
@@ -540,6 +549,27 @@ int MPI_Irecv(void *buf, int count, MPI_Datatype datatype, int source, int tag, 
   return PMPI_Irecv(buf, count, datatype, source, tag, comm, request);
 }
 
+// asks the engine whether a request is done (waiting for it when `block`)
+// and records the outcome on the request; the MPI handle stays valid
+static int progress(MPI_Request request, bool block, bool *done) {
+  State::Pending p;
+  {
+    std::lock_guard<std::mutex> lk(S().mu);
+    auto it = S().requests.find(request);
+    if (it == S().requests.end()) return MPI_ERR_ARG;
+    p = it->second;
+  }
+  if (!p.done) {
+    int d = 1;
+    p.rc = block ? sp_rt_wait(p.r, p.st) : sp_rt_test(p.r, &d, p.st);
+    p.done = d || p.rc != SP_OK;
+    std::lock_guard<std::mutex> lk(S().mu);
+    S().requests[request] = p;
+  }
+  *done = p.done;
+  return MPI_SUCCESS;
+}
+
 static int complete(MPI_Request *request, MPI_Status *status, bool block, int *flag) {
   if (!request) return MPI_ERR_ARG;
   if (*request == MPI_REQUEST_NULL) { // null or PROC_NULL request: empty status
@@ -547,26 +577,21 @@ static int complete(MPI_Request *request, MPI_Status *status, bool block, int *f
     if (flag) *flag = 1;
     return MPI_SUCCESS;
   }
-  sp_request r = 0;
-  {
-    std::lock_guard<std::mutex> lk(S().mu);
-    auto it = S().requests.find(*request);
-    if (it == S().requests.end()) return MPI_ERR_ARG;
-    r = it->second;
-  }
-  int64_t st[4] = {0, 0, 0, 0};
-  int done = 1;
-  sp_status rc = block ? sp_rt_wait(r, st) : sp_rt_test(r, &done, st);
+  bool done = false;
+  const int prc = progress(*request, block, &done);
+  if (prc != MPI_SUCCESS) return prc;
   if (flag) *flag = done;
-  if (!done && rc == SP_OK) return MPI_SUCCESS;
+  if (!done) return MPI_SUCCESS;
+  State::Pending p;
   {
     std::lock_guard<std::mutex> lk(S().mu);
+    p = S().requests[*request];
     S().requests.erase(*request);
   }
   *request = MPI_REQUEST_NULL;
-  TRY(rc);
-  if (status) *status = MPI_Status{static_cast<int>(st[0]), static_cast<int>(st[1]), MPI_SUCCESS,
-                                   static_cast<int>(st[3]), st[2]};
+  TRY(p.rc);
+  if (status) *status = MPI_Status{static_cast<int>(p.st[0]), static_cast<int>(p.st[1]), MPI_SUCCESS,
+                                   static_cast<int>(p.st[3]), p.st[2]};
   return MPI_SUCCESS;
 }
 
@@ -588,6 +613,89 @@ int MPI_Waitall(int count, MPI_Request requests[], MPI_Status statuses[]) {
   return first_err;
 }
 
+// MPI-3.1 3.7.5: the set forms poll every active request with MPI_Test
+// (which progresses the runtime) until their condition holds
+static bool all_null(int n, const MPI_Request r[]) {
+  for (int i = 0; i < n; ++i)
+    if (r[i] != MPI_REQUEST_NULL) return false;
+  return true;
+}
+
+int MPI_Testany(int count, MPI_Request requests[], int *index, int *flag, MPI_Status *status) {
+  if (count < 0 || (count && !requests) || !index || !flag) return MPI_ERR_ARG;
+  *index = MPI_UNDEFINED;
+  *flag = 0;
+  if (all_null(count, requests)) { // no active request: flag true, index undefined
+    *flag = 1;
+    if (status) *status = MPI_Status{MPI_ANY_SOURCE, MPI_ANY_TAG, MPI_SUCCESS, 0, 0};
+    return MPI_SUCCESS;
+  }
+  for (int i = 0; i < count; ++i) {
+    if (requests[i] == MPI_REQUEST_NULL) continue;
+    int done = 0;
+    const int rc = complete(&requests[i], status, false, &done);
+    if (rc != MPI_SUCCESS || done) {
+      *index = i;
+      *flag = 1;
+      return rc;
+    }
+  }
+  return MPI_SUCCESS;
+}
+
+int MPI_Waitany(int count, MPI_Request requests[], int *index, MPI_Status *status) {
+  int flag = 0;
+  for (;;) {
+    const int rc = MPI_Testany(count, requests, index, &flag, status);
+    if (rc != MPI_SUCCESS || flag) return rc;
+  }
+}
+
+int MPI_Testall(int count, MPI_Request requests[], int *flag, MPI_Status statuses[]) {
+  if (count < 0 || (count && !requests) || !flag) return MPI_ERR_ARG;
+  // all or nothing: no handle changes until every request is done
+  for (int i = 0; i < count; ++i) {
+    if (requests[i] == MPI_REQUEST_NULL) continue;
+    bool done = false;
+    const int rc = progress(requests[i], false, &done);
+    if (rc != MPI_SUCCESS) return rc;
+    if (!done) {
+      *flag = 0;
+      return MPI_SUCCESS;
+    }
+  }
+  *flag = 1;
+  return MPI_Waitall(count, requests, statuses); // every one is done: releases them
+}
+
+int MPI_Waitsome(int incount, MPI_Request requests[], int *outcount, int indices[], MPI_Status statuses[]) {
+  if (incount < 0 || (incount && !requests) || !outcount || (incount && !indices)) return MPI_ERR_ARG;
+  if (all_null(incount, requests)) {
+    *outcount = MPI_UNDEFINED;
+    return MPI_SUCCESS;
+  }
+  for (;;) {
+    int n = 0, first = MPI_SUCCESS;
+    for (int i = 0; i < incount; ++i) {
+      if (requests[i] == MPI_REQUEST_NULL) continue;
+      int done = 0;
+      const int rc = complete(&requests[i], statuses ? &statuses[n] : nullptr, false, &done);
+      if (rc != MPI_SUCCESS && first == MPI_SUCCESS) first = rc;
+      if (done || rc != MPI_SUCCESS) indices[n++] = i;
+    }
+    if (n) {
+      *outcount = n;
+      return first;
+    }
+  }
+}
+
+int MPI_Request_free(MPI_Request *request) {
+  if (!request) return MPI_ERR_ARG;
+  if (*request == MPI_REQUEST_NULL) return MPI_ERR_ARG;
+  return complete(request, nullptr, true, nullptr); // completes it, then the handle is released
+}
+
 int MPI_Sendrecv(const void *sendbuf, int sendcount, MPI_Datatype sendtype, int dest, int sendtag, void *recvbuf,
                  int recvcount, MPI_Datatype recvtype, int source, int recvtag, MPI_Comm comm,
                  MPI_Status *status) {
@@ -606,7 +714,7 @@ int MPI_Sendrecv(const void *sendbuf, int sendcount, MPI_Datatype sendtype, int 
 
 // ============================================================ topologies
 int MPI_Dist_graph_create_adjacent(MPI_Comm comm_old, int indegree, const int sources[], const int *,
-                                   int outdegree, const int destinations[], const int *, int, int,
+                                   int outdegree, const int destinations[], const int *, MPI_Info, int,
                                    MPI_Comm *comm_dist_graph) {
   if (!comm_of(comm_old) || !comm_dist_graph) return MPI_ERR_COMM;
   if (indegree < 0 || outdegree < 0) return MPI_ERR_ARG;

@@ -857,6 +857,90 @@ int PMPI_Waitall(int n, MPI_Request rs[], MPI_Status sts[]) {
 }
 int MPI_Waitall(int n, MPI_Request rs[], MPI_Status sts[]) ALIAS(MPI_Waitall);
 
+static int all_null(int n, const MPI_Request r[]) {
+  for (int i = 0; i < n; ++i)
+    if (r[i] != MPI_REQUEST_NULL) return 0;
+  return 1;
+}
+
+int PMPI_Testany(int n, MPI_Request rs[], int *index, int *flag, MPI_Status *st) {
+  *index = MPI_UNDEFINED;
+  *flag = 0;
+  if (all_null(n, rs)) {
+    *flag = 1;
+    if (st) *st = (MPI_Status){MPI_ANY_SOURCE, MPI_ANY_TAG, MPI_SUCCESS, -1, 0};
+    return MPI_SUCCESS;
+  }
+  for (int i = 0; i < n; ++i) {
+    if (rs[i] == MPI_REQUEST_NULL) continue;
+    int done = 0;
+    const int rc = complete(&rs[i], st, 0, &done);
+    if (rc != MPI_SUCCESS || done) {
+      *index = i;
+      *flag = 1;
+      return rc;
+    }
+  }
+  return MPI_SUCCESS;
+}
+int MPI_Testany(int n, MPI_Request rs[], int *index, int *flag, MPI_Status *st) ALIAS(MPI_Testany);
+
+int PMPI_Waitany(int n, MPI_Request rs[], int *index, MPI_Status *st) {
+  for (;;) {
+    int flag = 0;
+    const int rc = PMPI_Testany(n, rs, index, &flag, st);
+    if (rc != MPI_SUCCESS || flag) return rc;
+    pthread_mutex_lock(&g_mu); /* wait for the next arrival rather than spin */
+    struct timespec ts;
+    clock_gettime(CLOCK_REALTIME, &ts);
+    ts.tv_nsec += 1000000;
+    if (ts.tv_nsec >= 1000000000) {
+      ts.tv_sec += 1;
+      ts.tv_nsec -= 1000000000;
+    }
+    pthread_cond_timedwait(&g_cv, &g_mu, &ts);
+    pthread_mutex_unlock(&g_mu);
+  }
+}
+int MPI_Waitany(int n, MPI_Request rs[], int *index, MPI_Status *st) ALIAS(MPI_Waitany);
+
+int PMPI_Testall(int n, MPI_Request rs[], int *flag, MPI_Status sts[]) {
+  /* all or nothing (MPI-3.1 3.7.5): complete only when every one can */
+  for (int i = 0; i < n; ++i) {
+    if (rs[i] == MPI_REQUEST_NULL || !g_reqs[rs[i]].is_recv) continue;
+    const Req *q = &g_reqs[rs[i]];
+    pthread_mutex_lock(&g_mu);
+    const int ready = match_locked(q->src, q->tag, q->ctx, 0) != NULL;
+    pthread_mutex_unlock(&g_mu);
+    if (!ready) {
+      *flag = 0;
+      return MPI_SUCCESS;
+    }
+  }
+  *flag = 1;
+  return PMPI_Waitall(n, rs, sts);
+}
+int MPI_Testall(int n, MPI_Request rs[], int *flag, MPI_Status sts[]) ALIAS(MPI_Testall);
+
+int PMPI_Waitsome(int n, MPI_Request rs[], int *outcount, int indices[], MPI_Status sts[]) {
+  if (all_null(n, rs)) {
+    *outcount = MPI_UNDEFINED;
+    return MPI_SUCCESS;
+  }
+  int index = 0;
+  const int rc = PMPI_Waitany(n, rs, &index, sts ? &sts[0] : NULL);
+  indices[0] = index;
+  *outcount = 1;
+  return rc;
+}
+int MPI_Waitsome(int n, MPI_Request rs[], int *outcount, int indices[], MPI_Status sts[]) ALIAS(MPI_Waitsome);
+
+int PMPI_Request_free(MPI_Request *r) {
+  if (!r || *r == MPI_REQUEST_NULL) return MPI_ERR_ARG;
+  return complete(r, NULL, 1, NULL);
+}
+int MPI_Request_free(MPI_Request *r) ALIAS(MPI_Request_free);
+
 int PMPI_Sendrecv(const void *sbuf, int scount, MPI_Datatype stype, int dest, int stag, void *rbuf, int rcount,
                   MPI_Datatype rtype, int source, int rtag, MPI_Comm comm, MPI_Status *st) {
   const int rc = PMPI_Send(sbuf, scount, stype, dest, stag, comm);
@@ -882,7 +966,7 @@ static int *dup_ints(const int *a, int n) {
 }
 
 int PMPI_Dist_graph_create_adjacent(MPI_Comm old, int indeg, const int sources[], const int *sw, int outdeg,
-                                    const int dests[], const int *dw, int info, int reorder, MPI_Comm *out) {
+                                    const int dests[], const int *dw, MPI_Info info, int reorder, MPI_Comm *out) {
   (void)sw;
   (void)dw;
   (void)info;
@@ -901,7 +985,7 @@ int PMPI_Dist_graph_create_adjacent(MPI_Comm old, int indeg, const int sources[]
   return new_comm(&c, out);
 }
 int MPI_Dist_graph_create_adjacent(MPI_Comm old, int indeg, const int sources[], const int *sw, int outdeg,
-                                   const int dests[], const int *dw, int info, int reorder, MPI_Comm *out)
+                                   const int dests[], const int *dw, MPI_Info info, int reorder, MPI_Comm *out)
     ALIAS(MPI_Dist_graph_create_adjacent);
 
 int PMPI_Dist_graph_neighbors_count(MPI_Comm comm, int *indeg, int *outdeg, int *weighted) {

@@ -47,7 +47,7 @@ int main(int argc, char **argv) {
   CHECK(MPI_Pack(d, 1, ix, dpk, (int)(total * 8), &pos, MPI_COMM_WORLD) == MPI_SUCCESS && pos == total * 8);
   cudaMemcpy(hp, dpk, total * 8, cudaMemcpyDeviceToHost);
   CHECK(memcmp(hp, want, total * 8) == 0);
-  cudaMemset(d, 0, N * 8);
+  cudaMemset(d, 0, N * 8); cudaDeviceSynchronize();
   pos = 0;
   CHECK(MPI_Unpack(dpk, (int)(total * 8), &pos, d, 1, ix, MPI_COMM_WORLD) == MPI_SUCCESS);
   double *back = malloc(N * 8);
@@ -85,7 +85,7 @@ int main(int argc, char **argv) {
         CHECK(MPI_Send(d, 1, ix, 1, 70 + m, MPI_COMM_WORLD) == MPI_SUCCESS);
       } else if (rank == 1) {
         MPI_Status s;
-        cudaMemset(dpk, 0, total * 8);
+        cudaMemset(dpk, 0, total * 8); cudaDeviceSynchronize();
         CHECK(MPI_Recv(dpk, 1, flat, 0, 70 + m, MPI_COMM_WORLD, &s) == MPI_SUCCESS);
         /* the irregular send lands by DIRECT (run-table pack straight into the
            contiguous receive buffer) when offered: explicitly and by the model */

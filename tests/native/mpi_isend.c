@@ -45,7 +45,7 @@ int main(int argc, char **argv) {
     cudaMalloc((void **)&d_src[k], n[k]);
     cudaMalloc((void **)&d_dst[k], n[k]);
     cudaMemcpy(d_src[k], h, n[k], cudaMemcpyHostToDevice);
-    cudaMemset(d_dst[k], 0xA5, n[k]);
+    cudaMemset(d_dst[k], 0xA5, n[k]); cudaDeviceSynchronize();
     free(h);
   }
   MPI_Request req[2 * NMSG];
@@ -76,7 +76,7 @@ int main(int argc, char **argv) {
     free(h);
   }
   /* MPI_Sendrecv around the ring with message 1's type */
-  cudaMemset(d_dst[1], 0, n[1]);
+  cudaMemset(d_dst[1], 0, n[1]); cudaDeviceSynchronize();
   MPI_Status ss;
   CHECK(MPI_Sendrecv(d_src[1], 1, t[1], right, 7, d_dst[1], 1, t[1], left, 7, MPI_COMM_WORLD, &ss) == MPI_SUCCESS);
   CHECK(ss.MPI_SOURCE == left && ss.MPI_TAG == 7);

@@ -38,7 +38,7 @@ int main(int argc, char **argv) {
   CHECK(MPI_Pack(d, 1, t, dp, (int)P, &pos, MPI_COMM_WORLD) == MPI_SUCCESS && pos == P);
   cudaMemcpy(hp, dp, P, cudaMemcpyDeviceToHost);
   CHECK(memcmp(hp, want, P) == 0);
-  cudaMemset(d, 0xCD, N);
+  cudaMemset(d, 0xCD, N); cudaDeviceSynchronize();
   pos = 0;
   CHECK(MPI_Unpack(dp, (int)P, &pos, d, 1, t, MPI_COMM_WORLD) == MPI_SUCCESS && pos == P);
   cudaMemcpy(h, d, N, cudaMemcpyDeviceToHost);
@@ -57,7 +57,7 @@ int main(int argc, char **argv) {
         CHECK(MPI_Send(d, 1, t, 1, 40 + m, MPI_COMM_WORLD) == MPI_SUCCESS);
       } else if (rank == 1) {
         MPI_Status s;
-        cudaMemset(d, 0x5A, N);
+        cudaMemset(d, 0x5A, N); cudaDeviceSynchronize();
         CHECK(MPI_Recv(d, 1, t, MPI_ANY_SOURCE, 40 + m, MPI_COMM_WORLD, &s) == MPI_SUCCESS);
         CHECK(s.MPI_SOURCE == 0 && s.MPI_TAG == 40 + m && s.bytes == P);
         if (m >= 0) CHECK(s.method == m);

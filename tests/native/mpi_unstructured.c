@@ -98,7 +98,7 @@ static int one_iteration(int rank, int size, MPI_Comm g, const char *mode) {
   cudaMalloc((void **)&d_src, (n_out[0] + n_out[1]) * sizeof(double));
   cudaMalloc((void **)&d_out, 2 * N * sizeof(double));
   cudaMemcpy(d_src, hs, (n_out[0] + n_out[1]) * sizeof(double), cudaMemcpyHostToDevice);
-  cudaMemset(d_out, 0, 2 * N * sizeof(double));
+  cudaMemset(d_out, 0, 2 * N * sizeof(double)); cudaDeviceSynchronize();
   MPI_Aint sd2[2] = {0, (MPI_Aint)(n_out[0] * sizeof(double))}, rd2[2] = {0, (MPI_Aint)(N * sizeof(double))};
   if (!strchr(mode, 'b')) goto done;
   CHECK(MPI_Neighbor_alltoallw(d_src, ones, sd2, flat, d_out, ones, rd2, scatter, g) == MPI_SUCCESS);

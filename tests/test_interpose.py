@@ -34,6 +34,7 @@ INTERCEPTED = {
     "MPI_Type_create_hindexed_block", "MPI_Type_create_struct", "MPI_Type_create_resized",
     "MPI_Type_commit", "MPI_Type_free", "MPI_Pack", "MPI_Unpack",
     "MPI_Send", "MPI_Recv", "MPI_Isend", "MPI_Irecv", "MPI_Wait", "MPI_Waitall", "MPI_Test", "MPI_Sendrecv",
+    "MPI_Waitany", "MPI_Waitsome", "MPI_Testany", "MPI_Testall", "MPI_Request_free",
     "MPI_Dist_graph_create_adjacent", "MPI_Cart_create", "MPI_Comm_free",
     "MPI_Neighbor_alltoallv", "MPI_Neighbor_alltoallw", "MPI_Alltoallv", "MPI_Alltoallw",
 }
@@ -204,3 +205,15 @@ def test_interposed_alltoall(cuda, sysmpi, np_):
     _, st = run(np_, build(sysmpi, "mpi_alltoall", interposed=False), preload=True)
     for s in st.values():
         assert s["exchanges"] == 3 and s["kernels"] > 0
+
+
+def test_interposer_builds_against_pointer_handle_mpi_h():
+    """a site rebuilds interpose.cpp against its own MPI's mpi.h: it compiles
+    against an Open MPI-style header (opaque pointer handles, predefined
+    datatypes as object addresses, a standard MPI_Status without this
+    image's extra fields; tests/native/ompi_style/mpi.h)"""
+    p = subprocess.run(["/usr/bin/g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Wextra", "-Werror",
+                        "-Wno-unused-parameter", "-I" + os.path.join(NATIVE, "ompi_style"),
+                        "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include",
+                        os.path.join(PKG, "csrc", "interpose.cpp")], capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr

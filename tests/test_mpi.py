@@ -88,6 +88,16 @@ def test_mpi_unstructured_loop(cuda, tmp_path, np_):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("np_", [1, 2])
+def test_mpi_portable_program(cuda, tmp_path, np_):
+    """tests/native/mpi_interpose.c -- the portable program the interposer is
+    tested with over a system MPI -- on the engine's own MPI: device
+    pack/unpack checked against host pack/unpack, every send method, the
+    set completions (Waitany, Waitsome, Testall, Testany, Request_free)"""
+    assert "OK" in run(np_, build(tmp_path, "mpi_interpose"))
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("np_", [1, 2, 3])
 def test_mpi_alltoallv_alltoallw(cuda, tmp_path, np_):
     """beyond the paper (its future work names collectives): MPI_Alltoallv
