@@ -469,6 +469,73 @@ __device__ __forceinline__ uint4 shfl_down4(unsigned mask, const uint4 &x, int w
 // blocks that intersect the run are loaded; the blocks at the two ends of a
 // run are stored masked. Every lane of a group runs the same trip count,
 // so the shuffles name just the group's lanes.
+// one run of `len` bytes from src to dst by a group of g lanes (lane l of
+// the group, `gmask` names the group's lanes in the warp): the body of
+// k_runs_shift and k_runs_multi_shift
+__device__ __forceinline__ void shift_run(const uint8_t *src, uint8_t *dst, int64_t len, int g, int lane,
+                                          unsigned gmask) {
+  const uint4 zero = make_uint4(0, 0, 0, 0);
+  const uintptr_t A = reinterpret_cast<uintptr_t>(dst), E = A + static_cast<uintptr_t>(len);
+  const uintptr_t S = reinterpret_cast<uintptr_t>(src), SE = S + static_cast<uintptr_t>(len);
+  const uintptr_t first = A & ~uintptr_t{15};
+  const int64_t nblk = static_cast<int64_t>(((E + 15) & ~uintptr_t{15}) - first) / 16;
+  // read address of written block B is B + (S - A): a fixed byte shift
+  const uintptr_t r0 = first + (S - A);
+  const unsigned d = static_cast<unsigned>(r0 & 15);
+  // written block b: its aligned read block, the next one (neighbour lane
+  // or own load), the assembled 16 bytes, the (masked) store
+  auto load = [&](int64_t b, uint4 &x0, uint4 &x1) {
+    const uintptr_t rb = (r0 & ~uintptr_t{15}) + 16 * static_cast<uintptr_t>(b);
+    x0 = b < nblk && rb < SE && rb + 16 > S ? ld_stream(reinterpret_cast<const uint4 *>(rb)) : zero;
+    const uintptr_t nb = rb + 16;
+    const bool own = lane == g - 1 || b + 1 >= nblk;
+    x1 = own && b < nblk && d && nb < SE && nb + 16 > S ? ld_stream(reinterpret_cast<const uint4 *>(nb)) : zero;
+  };
+  auto put = [&](int64_t b, const uint4 &x0, uint4 x1, const uint4 &nx) {
+    if (!(lane == g - 1 || b + 1 >= nblk)) x1 = nx;
+    if (b >= nblk) return;
+    const uint4 z = d ? funnel16(x0, x1, d) : x0;
+    const uintptr_t B = first + 16 * static_cast<uintptr_t>(b);
+    const uintptr_t vlo = B > A ? B : A, vhi = B + 16 < E ? B + 16 : E;
+    uint8_t *blk = reinterpret_cast<uint8_t *>(B);
+    if (vlo == B && vhi == B + 16) {
+      st_stream(reinterpret_cast<uint4 *>(blk), z);
+    } else {
+      store_masked(blk, z, static_cast<unsigned>(vlo - B), static_cast<unsigned>(vhi - B));
+    }
+  };
+  int64_t c = 0;
+  for (; c + g < nblk; c += 2 * g) { // two chunks of G blocks: up to four loads in flight per lane
+    uint4 a0, a1, b0, b1;
+    load(c + lane, a0, a1);
+    load(c + g + lane, b0, b1);
+    const uint4 na = shfl_down4(gmask, a0, g), nb = shfl_down4(gmask, b0, g);
+    put(c + lane, a0, a1, na);
+    put(c + g + lane, b0, b1, nb);
+  }
+  if (c < nblk) {
+    uint4 a0, a1;
+    load(c + lane, a0, a1);
+    const uint4 na = shfl_down4(gmask, a0, g);
+    put(c + lane, a0, a1, na);
+  }
+}
+
+__device__ __forceinline__ unsigned group_mask(int g) {
+  return (g == 32 ? 0xffffffffu : ((1u << g) - 1u)) << ((threadIdx.x & 31) & ~(g - 1));
+}
+
+// Runs whose offsets only allow 1-, 2- or 4-byte words (byte-granular
+// hindexed / struct displacements): the shift technique of k_shift_* per
+// piece. A group of G lanes takes an (object, piece) item; lane l of the
+// group owns aligned 16-B block c*G + l of the WRITTEN side. Consecutive
+// written blocks read consecutive aligned 16-B blocks of the read side at
+// one fixed byte shift, so each lane loads ONE aligned read block and takes
+// the next one from its neighbour lane (a shuffle; the group's last lane
+// loads its own), then assembles its 16 bytes with funnel shifts. Only read
+// blocks that intersect the run are loaded; the blocks at the two ends of a
+// run are stored masked. Every lane of a group runs the same trip count,
+// so the shuffles name just the group's lanes.
 template <bool PACK>
 __global__ void __launch_bounds__(256) k_runs_shift(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
                                                     const int64_t *__restrict__ psrc,
@@ -476,59 +543,14 @@ __global__ void __launch_bounds__(256) k_runs_shift(const uint8_t *__restrict__ 
                                                     int64_t extent, int64_t size, int lg) {
   const int g = 1 << lg;
   const int lane = static_cast<int>(threadIdx.x) & (g - 1);
-  const unsigned gmask = (g == 32 ? 0xffffffffu : ((1u << g) - 1u)) << ((threadIdx.x & 31) & ~(g - 1));
+  const unsigned gmask = group_mask(g);
   const int64_t groups = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> lg;
   const int64_t total = npieces * nobj;
-  const uint4 zero = make_uint4(0, 0, 0, 0);
   for (int64_t p = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> lg; p < total; p += groups) {
     const int64_t j = p / npieces, k = p - j * npieces;
     const int64_t s0 = __ldg(psrc + k), d0 = __ldg(pdst + k), len = __ldg(pdst + k + 1) - d0;
-    const uint8_t *src = PACK ? in + j * extent + s0 : in + j * size + d0;
-    uint8_t *dst = PACK ? out + j * size + d0 : out + j * extent + s0;
-    const uintptr_t A = reinterpret_cast<uintptr_t>(dst), E = A + static_cast<uintptr_t>(len);
-    const uintptr_t S = reinterpret_cast<uintptr_t>(src), SE = S + static_cast<uintptr_t>(len);
-    const uintptr_t first = A & ~uintptr_t{15};
-    const int64_t nblk = static_cast<int64_t>(((E + 15) & ~uintptr_t{15}) - first) / 16;
-    // read address of written block B is B + (S - A): a fixed byte shift
-    const uintptr_t r0 = first + (S - A);
-    const unsigned d = static_cast<unsigned>(r0 & 15);
-    // written block b: its aligned read block, the next one (neighbour lane
-    // or own load), the assembled 16 bytes, the (masked) store
-    auto load = [&](int64_t b, uint4 &x0, uint4 &x1) {
-      const uintptr_t rb = (r0 & ~uintptr_t{15}) + 16 * static_cast<uintptr_t>(b);
-      x0 = b < nblk && rb < SE && rb + 16 > S ? ld_stream(reinterpret_cast<const uint4 *>(rb)) : zero;
-      const uintptr_t nb = rb + 16;
-      const bool own = lane == g - 1 || b + 1 >= nblk;
-      x1 = own && b < nblk && d && nb < SE && nb + 16 > S ? ld_stream(reinterpret_cast<const uint4 *>(nb)) : zero;
-    };
-    auto put = [&](int64_t b, const uint4 &x0, uint4 x1, const uint4 &nx) {
-      if (!(lane == g - 1 || b + 1 >= nblk)) x1 = nx;
-      if (b >= nblk) return;
-      const uint4 z = d ? funnel16(x0, x1, d) : x0;
-      const uintptr_t B = first + 16 * static_cast<uintptr_t>(b);
-      const uintptr_t vlo = B > A ? B : A, vhi = B + 16 < E ? B + 16 : E;
-      uint8_t *blk = reinterpret_cast<uint8_t *>(B);
-      if (vlo == B && vhi == B + 16) {
-        st_stream(reinterpret_cast<uint4 *>(blk), z);
-      } else {
-        store_masked(blk, z, static_cast<unsigned>(vlo - B), static_cast<unsigned>(vhi - B));
-      }
-    };
-    int64_t c = 0;
-    for (; c + g < nblk; c += 2 * g) { // two chunks of G blocks: up to four loads in flight per lane
-      uint4 a0, a1, b0, b1;
-      load(c + lane, a0, a1);
-      load(c + g + lane, b0, b1);
-      const uint4 na = shfl_down4(gmask, a0, g), nb = shfl_down4(gmask, b0, g);
-      put(c + lane, a0, a1, na);
-      put(c + g + lane, b0, b1, nb);
-    }
-    if (c < nblk) {
-      uint4 a0, a1;
-      load(c + lane, a0, a1);
-      const uint4 na = shfl_down4(gmask, a0, g);
-      put(c + lane, a0, a1, na);
-    }
+    shift_run(PACK ? in + j * extent + s0 : in + j * size + d0, PACK ? out + j * size + d0 : out + j * extent + s0,
+              len, g, lane, gmask);
   }
 }
 
@@ -582,6 +604,32 @@ __global__ void __launch_bounds__(256) k_runs_multi(const __grid_constant__ RunT
       st_stream(dw + w + 3 * g, v3);
     }
     for (; w < words; w += g) st_stream(dw + w, ld_stream(sw + w));
+  }
+}
+
+// k_runs_multi with the shift technique: misaligned irregular edges of a
+// neighbour collective (byte-granular runs, mean >= kRunsShiftMin*)
+__global__ void __launch_bounds__(256) k_runs_multi_shift(const __grid_constant__ RunTable t, int lg) {
+  const int g = 1 << lg;
+  const int lane = static_cast<int>(threadIdx.x) & (g - 1);
+  const unsigned gmask = group_mask(g);
+  const int64_t groups = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> lg;
+  for (int64_t p = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> lg; p < t.total; p += groups) {
+    int a = 0, b = t.n - 1;
+    while (a < b) {
+      const int m = (a + b + 1) >> 1;
+      if (t.e[m].item0 <= p) {
+        a = m;
+      } else {
+        b = m - 1;
+      }
+    }
+    const RunEdge &e = t.e[a];
+    const int64_t local = p - e.item0;
+    const int64_t j = local / e.npieces, k = local - j * e.npieces;
+    const int64_t s0 = __ldg(e.psrc + k), d0 = __ldg(e.pdst + k), len = __ldg(e.pdst + k + 1) - d0;
+    shift_run(e.unpack ? e.in + j * e.size + d0 : e.in + j * e.extent + s0,
+              e.unpack ? e.out + j * e.extent + s0 : e.out + j * e.size + d0, len, g, lane, gmask);
   }
 }
 
@@ -1391,6 +1439,15 @@ void runs_multi(const std::vector<RunJob> &jobs, void *stream) {
   const int64_t mean_words = bytes / w / std::max<int64_t>(items, 1);
   int lg = 0;
   while (lg < 4 && (int64_t{2} << lg) <= mean_words) ++lg;
+  // misaligned runs: the shift variant, at the stricter threshold when any
+  // edge scatters (k_runs_shift's measured crossovers)
+  const bool any_unpack = std::any_of(edges.begin(), edges.end(), [](const RunEdge &e) { return e.unpack != 0; });
+  const int64_t mean_bytes = bytes / std::max<int64_t>(items, 1);
+  const bool shift = w < 8 && mean_bytes >= (any_unpack ? kRunsShiftMinUnpack : kRunsShiftMinPack);
+  if (shift) {
+    lg = 0;
+    while (lg < 4 && (int64_t{4} << lg) <= mean_bytes / 16) ++lg;
+  }
   for (size_t at = 0; at < edges.size(); at += kRunEdges) {
     RunTable t{};
     t.n = static_cast<int>(std::min<size_t>(kRunEdges, edges.size() - at));
@@ -1401,12 +1458,17 @@ void runs_multi(const std::vector<RunJob> &jobs, void *stream) {
       acc += t.e[i].npieces * t.e[i].nobj;
     }
     t.total = acc;
-    switch (w) {
-    case 16: launch_runs_multi<16>(t, lg, s); break;
-    case 8: launch_runs_multi<8>(t, lg, s); break;
-    case 4: launch_runs_multi<4>(t, lg, s); break;
-    case 2: launch_runs_multi<2>(t, lg, s); break;
-    default: launch_runs_multi<1>(t, lg, s); break;
+    if (shift) {
+      const unsigned grid = resident_grid<k_runs_multi_shift>(static_cast<uint64_t>(t.total) << lg);
+      k_runs_multi_shift<<<grid, 256, 0, s>>>(t, lg);
+    } else {
+      switch (w) {
+      case 16: launch_runs_multi<16>(t, lg, s); break;
+      case 8: launch_runs_multi<8>(t, lg, s); break;
+      case 4: launch_runs_multi<4>(t, lg, s); break;
+      case 2: launch_runs_multi<2>(t, lg, s); break;
+      default: launch_runs_multi<1>(t, lg, s); break;
+      }
     }
     cuda_check(cudaGetLastError(), "k_runs_multi launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -659,6 +659,89 @@ def test_neighbor_alltoallw_irregular_receive_types(cuda, world):
     assert all(_spawn(_nbr_irregular_recv, world).values())
 
 
+def _nbr_misaligned_runs(rank, world, job):
+    """Byte-granular irregular edges (hindexed of MPI_BYTE, odd lengths and
+    displacements, mean run > 256 B): the shift variant of the run-table
+    kernel (k_runs_multi_shift) for gathers into contiguous ghosts (first
+    call) and for scatters of contiguous runs through the receivers'
+    published run tables (second call); ring, verified byte by byte."""
+    import numpy as np
+    import torch
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.rt as rt
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=1 << 20, host_bytes=1 << 20)
+    right, left = (rank + 1) % world, (rank - 1) % world
+    B = sp.make_named(sp.NamedKind.Byte)
+
+    def runs(seed, lo):  # 60 runs of 200-700 B at odd, non-overlapping offsets inside [lo, lo + 65536)
+        g = np.random.default_rng(seed)
+        bl = g.integers(200, 701, 60)
+        at = lo + 3 + np.concatenate([[0], np.cumsum(bl + g.integers(1, 300, 60))[:-1]])
+        perm = g.permutation(60)
+        return [int(x) for x in bl[perm]], [int(x) for x in at[perm]]
+
+    def expect(bl, dp, vals, base, n):
+        want = np.full(n, 0xEE, np.uint8)
+        k = 0
+        for b, d in zip(bl, dp):
+            want[d - base:d - base + b] = vals[k:k + b]
+            k += b
+        return want
+
+    field = torch.from_numpy((np.arange(1 << 17) * 7 + rank * 31).astype(np.uint8)).cuda()
+    host_field = lambda r: (np.arange(1 << 17) * 7 + r * 31).astype(np.uint8)
+    # 1. gathers: my irregular lists for each neighbour -> their contiguous ghosts
+    bl_r, dp_r = runs(10 * rank + right, 0)
+    bl_l, dp_l = runs(10 * rank + left, 65536)
+    in_l, in_r = runs(10 * left + rank, 0), runs(10 * right + rank, 65536)
+    n_l, n_r = sum(in_l[0]), sum(in_r[0])
+    call = rt.NeighborW([(right, 1, sp.commit_type(sp.make_hindexed(bl_r, dp_r, B)), 0),
+                         (left, 1, sp.commit_type(sp.make_hindexed(bl_l, dp_l, B)), 0)],
+                        [(left, 1, sp.commit_type(sp.make_contiguous(n_l, B)), 0),
+                         (right, 1, sp.commit_type(sp.make_contiguous(n_r, B)), n_l)])
+    ghosts = torch.full((n_l + n_r,), 0xEE, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    call(field, ghosts)
+    torch.cuda.synchronize()
+    got = ghosts.cpu().numpy()
+    want_l = np.concatenate([host_field(left)[d:d + b] for b, d in zip(*in_l)])
+    want_r = np.concatenate([host_field(right)[d:d + b] for b, d in zip(*in_r)])
+    assert np.array_equal(got[:n_l], want_l) and np.array_equal(got[n_l:], want_r), rank
+    # 2. scatters: contiguous runs -> my irregular ghost layouts
+    g_l, g_r = runs(20 * rank + left, 0), runs(20 * rank + right, 65536)
+    out_r, out_l = runs(20 * right + rank, 0), runs(20 * left + rank, 65536)  # my neighbours' layouts for me
+    m_r, m_l = sum(out_r[0]), sum(out_l[0])
+    call2 = rt.NeighborW([(right, 1, sp.commit_type(sp.make_contiguous(m_r, B)), 0),
+                          (left, 1, sp.commit_type(sp.make_contiguous(m_l, B)), m_r)],
+                         [(left, 1, sp.commit_type(sp.make_hindexed(*g_l, B)), 0),
+                          (right, 1, sp.commit_type(sp.make_hindexed(*g_r, B)), 0)])
+    src = torch.from_numpy((np.arange(m_r + m_l) * 5 + rank).astype(np.uint8)).cuda()
+    recv = torch.full((1 << 17,), 0xEE, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    call2(src, recv)
+    torch.cuda.synchronize()
+    sent = lambda r, n, off: (np.arange(off, off + n) * 5 + r).astype(np.uint8)
+    # the left neighbour's block for its right (me) is its first; the right
+    # neighbour's block for its left (me) follows its block for ITS right
+    vals_l = sent(left, sum(g_l[0]), 0)
+    vals_r = sent(right, sum(g_r[0]), sum(runs(20 * ((right + 1) % world) + right, 0)[0]))
+    want = expect(*g_l, vals_l, 0, 1 << 17)
+    k = 0
+    for b, d in zip(*g_r):
+        want[d:d + b] = vals_r[k:k + b]
+        k += b
+    assert np.array_equal(recv.cpu().numpy(), want), rank
+    rt.finalize()
+    return True
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_neighbor_misaligned_irregular_runs(cuda, world):
+    assert all(_spawn(_nbr_misaligned_runs, world).values())
+
+
 def _nbr_alternating_layouts(rank, world, job, iters):
     """Regression for the shared neighbour protocol (entry counters, READY
     flags, layout versions, repeat-call and batch caches): every rank of a
