@@ -44,6 +44,7 @@
 #include <string>
 #include <tuple>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "mpi.h"
@@ -193,6 +194,11 @@ struct State {
   std::unordered_map<MPI_Datatype, Mirror> types;
   std::unordered_map<MPI_Comm, std::pair<int, int>> degree; // comm -> (indegree, outdegree)
   std::unordered_map<MPI_Request, Pending> pending;
+  // mirrors still named by a pending receive, and the ones among them whose
+  // MPI type was freed (MPI lets a pending operation outlive its datatype):
+  // released when the last such receive completes
+  std::unordered_map<sp_type, int> in_flight;
+  std::unordered_set<sp_type> retired;
   std::map<BatchKey, sp_batch> batches;
   std::unordered_map<int, cudaStream_t> streams; // one per device the application uses
   sp_profile profile = nullptr;
@@ -678,7 +684,12 @@ int MPI_Type_free(MPI_Datatype *dt) {
     std::lock_guard<std::mutex> lk(S().mu);
     auto it = S().types.find(*dt);
     if (it != S().types.end()) {
-      sp_type_free(it->second.h);
+      const sp_type h = it->second.h;
+      if (S().in_flight.count(h)) {
+        S().retired.insert(h); // a pending receive still unpacks with it
+      } else {
+        sp_type_free(h);
+      }
       S().types.erase(it);
     }
   }
@@ -804,6 +815,7 @@ int MPI_Irecv(void *buf, int count, MPI_Datatype dt, int source, int tag, MPI_Co
   }
   std::lock_guard<std::mutex> lk(S().mu);
   S().pending[*req] = p;
+  ++S().in_flight[p.type];
   return MPI_SUCCESS;
 }
 
@@ -821,6 +833,18 @@ int finish(MPI_Request key, MPI_Status *status, int rc) {
     p = it->second;
     S().pending.erase(it);
   }
+  struct Release { // the receive's mirror, once nothing pending names it
+    sp_type h;
+    ~Release() {
+      if (!h) return;
+      std::lock_guard<std::mutex> lk(S().mu);
+      auto f = S().in_flight.find(h);
+      if (f != S().in_flight.end() && --f->second == 0) {
+        S().in_flight.erase(f);
+        if (S().retired.erase(h)) sp_type_free(h);
+      }
+    }
+  } release{p.recv ? p.type : 0};
   if (p.recv && rc == MPI_SUCCESS && status) {
     Mirror m;
     m.h = p.type;

@@ -642,8 +642,7 @@ int MPI_Type_commit(MPI_Datatype *dt) ALIAS(MPI_Type_commit);
 int PMPI_Type_free(MPI_Datatype *dt) {
   Type *t = dt ? type_of(*dt) : NULL;
   if (!t || *dt <= MPI_UNSIGNED_CHAR) return MPI_ERR_TYPE;
-  free(t->off);
-  free(t->len);
+  /* the run arrays are kept: a pending receive may still hold the type */
   t->used = 0;
   *dt = MPI_DATATYPE_NULL;
   return MPI_SUCCESS;
@@ -764,7 +763,7 @@ int MPI_Recv(void *buf, int count, MPI_Datatype dt, int source, int tag, MPI_Com
  * MPI_Wait/MPI_Test */
 typedef struct {
   int used, is_recv, count, src, tag, ctx;
-  MPI_Datatype dt;
+  Type ty; /* a copy: the datatype may be freed while the receive is pending */
   void *buf;
 } Req;
 static Req g_reqs[4096];
@@ -805,7 +804,7 @@ int PMPI_Irecv(void *buf, int count, MPI_Datatype dt, int source, int tag, MPI_C
   q->src = source == MPI_ANY_SOURCE ? MPI_ANY_SOURCE : world_rank(comm, source);
   q->tag = tag;
   q->ctx = ctx_of(comm);
-  q->dt = dt;
+  q->ty = *type_of(dt);
   q->buf = buf;
   return MPI_SUCCESS;
 }
@@ -832,7 +831,7 @@ static int complete(MPI_Request *r, MPI_Status *st, int block, int *flag) {
         return MPI_SUCCESS;
       }
     }
-    rc = recv_typed(q->buf, q->count, type_of(q->dt), q->src, q->tag, q->ctx, st);
+    rc = recv_typed(q->buf, q->count, &q->ty, q->src, q->tag, q->ctx, st);
   } else if (st) {
     *st = (MPI_Status){MPI_ANY_SOURCE, MPI_ANY_TAG, MPI_SUCCESS, -1, 0};
   }

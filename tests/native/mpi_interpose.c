@@ -243,6 +243,17 @@ int main(int argc, char **argv) {
         CHECK(MPI_Wait(&rr[2], MPI_STATUS_IGNORE) == MPI_SUCCESS);
         cudaMemcpy(back, r3[2], span, cudaMemcpyDeviceToHost);
         CHECK(memcmp(back, hd, span) == 0);
+        /* a datatype freed while a receive using it is pending (MPI-3.1
+         * 4.1.9: the operation completes normally) */
+        MPI_Datatype tmp2;
+        CHECK(MPI_Type_contiguous(1, t[k], &tmp2) == MPI_SUCCESS && MPI_Type_commit(&tmp2) == MPI_SUCCESS);
+        cudaMemset(r3[1], 0xCD, span); cudaDeviceSynchronize();
+        CHECK(MPI_Irecv(r3[1] + base, COUNT, tmp2, peer, 60, MPI_COMM_WORLD, &rr[1]) == MPI_SUCCESS);
+        CHECK(MPI_Type_free(&tmp2) == MPI_SUCCESS);
+        CHECK(MPI_Send(d + base, COUNT, t[k], peer, 60, MPI_COMM_WORLD) == MPI_SUCCESS);
+        CHECK(MPI_Wait(&rr[1], MPI_STATUS_IGNORE) == MPI_SUCCESS);
+        cudaMemcpy(back, r3[1], span, cudaMemcpyDeviceToHost);
+        CHECK(memcmp(back, hd, span) == 0);
         for (int i = 0; i < 3; ++i) cudaFree(r3[i]);
       }
     }
