@@ -274,9 +274,9 @@ __global__ void __launch_bounds__(256) k_smallrow(const uint8_t *__restrict__ in
 constexpr uint64_t kTmaMinBytes = uint64_t{8} << 20;
 // mean run length from which misaligned runs (word < 8) take k_runs_shift
 // (scripts/runs_bench.py --misaligned: pack wins from 32 B; unpack, whose
-// run ends are masked stores, from 256 B -- below it the byte-word kernel
-// ties or wins)
-constexpr int64_t kRunsShiftMinPack = 32, kRunsShiftMinUnpack = 256;
+// run ends are masked stores, from 1 KiB -- at 256 B the byte-word kernel
+// still ties or wins)
+constexpr int64_t kRunsShiftMinPack = 32, kRunsShiftMinUnpack = 512;
 
 static bool shift_wins(bool pack, int w, int64_t c0) {
   if (pack) return w <= 2 || (w == 4 && c0 % 16 == 0);
@@ -453,6 +453,27 @@ __device__ __forceinline__ uint4 funnel16(const uint4 &x0, const uint4 &x1, unsi
                     __funnelshift_r(v[2], v[3], sh), __funnelshift_r(v[3], v[4], sh));
 }
 
+// funnel16 with the word offset q = d >> 2 known to be uniform across the
+// group (one shift per run): a switch on q picks compile-time word indices,
+// so each output word is one funnel shift instead of a select chain
+__device__ __forceinline__ uint4 funnel16_uniform(const uint4 &x0, const uint4 &x1, unsigned d) {
+  const unsigned sh = (d & 3) * 8;
+  switch (d >> 2) {
+  case 0:
+    return make_uint4(__funnelshift_r(x0.x, x0.y, sh), __funnelshift_r(x0.y, x0.z, sh),
+                      __funnelshift_r(x0.z, x0.w, sh), __funnelshift_r(x0.w, x1.x, sh));
+  case 1:
+    return make_uint4(__funnelshift_r(x0.y, x0.z, sh), __funnelshift_r(x0.z, x0.w, sh),
+                      __funnelshift_r(x0.w, x1.x, sh), __funnelshift_r(x1.x, x1.y, sh));
+  case 2:
+    return make_uint4(__funnelshift_r(x0.z, x0.w, sh), __funnelshift_r(x0.w, x1.x, sh),
+                      __funnelshift_r(x1.x, x1.y, sh), __funnelshift_r(x1.y, x1.z, sh));
+  default:
+    return make_uint4(__funnelshift_r(x0.w, x1.x, sh), __funnelshift_r(x1.x, x1.y, sh),
+                      __funnelshift_r(x1.y, x1.z, sh), __funnelshift_r(x1.z, x1.w, sh));
+  }
+}
+
 __device__ __forceinline__ uint4 shfl_down4(unsigned mask, const uint4 &x, int width) {
   return make_uint4(__shfl_down_sync(mask, x.x, 1, width), __shfl_down_sync(mask, x.y, 1, width),
                     __shfl_down_sync(mask, x.z, 1, width), __shfl_down_sync(mask, x.w, 1, width));
@@ -494,7 +515,7 @@ __device__ __forceinline__ void shift_run(const uint8_t *src, uint8_t *dst, int6
   auto put = [&](int64_t b, const uint4 &x0, uint4 x1, const uint4 &nx) {
     if (!(lane == g - 1 || b + 1 >= nblk)) x1 = nx;
     if (b >= nblk) return;
-    const uint4 z = d ? funnel16(x0, x1, d) : x0;
+    const uint4 z = d ? funnel16_uniform(x0, x1, d) : x0;
     const uintptr_t B = first + 16 * static_cast<uintptr_t>(b);
     const uintptr_t vlo = B > A ? B : A, vhi = B + 16 < E ? B + 16 : E;
     uint8_t *blk = reinterpret_cast<uint8_t *>(B);

@@ -661,7 +661,7 @@ def test_neighbor_alltoallw_irregular_receive_types(cuda, world):
 
 def _nbr_misaligned_runs(rank, world, job):
     """Byte-granular irregular edges (hindexed of MPI_BYTE, odd lengths and
-    displacements, mean run > 256 B): the shift variant of the run-table
+    displacements, mean run ~1 KiB): the shift variant of the run-table
     kernel (k_runs_multi_shift) for gathers into contiguous ghosts (first
     call) and for scatters of contiguous runs through the receivers'
     published run tables (second call); ring, verified byte by byte."""
@@ -674,11 +674,11 @@ def _nbr_misaligned_runs(rank, world, job):
     right, left = (rank + 1) % world, (rank - 1) % world
     B = sp.make_named(sp.NamedKind.Byte)
 
-    def runs(seed, lo):  # 60 runs of 200-700 B at odd, non-overlapping offsets inside [lo, lo + 65536)
+    def runs(seed, lo):  # 35 runs of 600-1400 B at odd, non-overlapping offsets inside [lo, lo + 65536)
         g = np.random.default_rng(seed)
-        bl = g.integers(200, 701, 60)
-        at = lo + 3 + np.concatenate([[0], np.cumsum(bl + g.integers(1, 300, 60))[:-1]])
-        perm = g.permutation(60)
+        bl = g.integers(600, 1401, 35)
+        at = lo + 3 + np.concatenate([[0], np.cumsum(bl + g.integers(1, 300, 35))[:-1]])
+        perm = g.permutation(35)
         return [int(x) for x in bl[perm]], [int(x) for x in at[perm]]
 
     def expect(bl, dp, vals, base, n):

@@ -223,7 +223,7 @@ def test_misaligned_runs_shift_kernel(sp, cuda, lens):
     dst = torch.full((pos + inc * c.size + 16,), 0xEE, dtype=torch.uint8, device="cuda")
     sp.pack(torch.from_numpy(host).cuda(), c, inc, dst, pos)
     li = sp.last_launch()
-    shifted = c.size / n >= 32  # pack from a 32-B mean run, unpack from 256 B
+    shifted = c.size / n >= 32  # pack from a 32-B mean run, unpack from 512 B
     assert li.kernel == sp.Kernel.BlockList and li.word == (16 if shifted else 1), (li, c.size / n)
     got = dst.cpu().numpy()
     assert np.array_equal(got[pos:pos + inc * c.size], want)
@@ -231,7 +231,7 @@ def test_misaligned_runs_shift_kernel(sp, cuda, lens):
     init = rng.integers(0, 256, span, dtype=np.uint8)
     out = torch.from_numpy(init.copy()).cuda()
     sp.unpack(dst, pos, c, inc, out)
-    assert sp.last_launch().word == (16 if c.size / n >= 256 else 1)
+    assert sp.last_launch().word == (16 if c.size / n >= 512 else 1)
     exp = tm.scatter(want, init.copy(), runs, inc, c.extent)
     assert np.array_equal(out.cpu().numpy(), exp)
 
