@@ -283,6 +283,28 @@ static bool shift_wins(bool pack, int w, int64_t c0) {
   return w <= 2 && c0 >= 128;
 }
 
+// the 16 bytes starting d bytes into x0, continuing into x1 (d < 16): a
+// switch on the word offset d >> 2 picks compile-time word indices, so each
+// output word is one funnel shift (no select chain; when the offset is
+// uniform across a warp -- one shift per run -- there is no divergence)
+__device__ __forceinline__ uint4 funnel16(const uint4 &x0, const uint4 &x1, unsigned d) {
+  const unsigned sh = (d & 3) * 8;
+  switch (d >> 2) {
+  case 0:
+    return make_uint4(__funnelshift_r(x0.x, x0.y, sh), __funnelshift_r(x0.y, x0.z, sh),
+                      __funnelshift_r(x0.z, x0.w, sh), __funnelshift_r(x0.w, x1.x, sh));
+  case 1:
+    return make_uint4(__funnelshift_r(x0.y, x0.z, sh), __funnelshift_r(x0.z, x0.w, sh),
+                      __funnelshift_r(x0.w, x1.x, sh), __funnelshift_r(x1.x, x1.y, sh));
+  case 2:
+    return make_uint4(__funnelshift_r(x0.z, x0.w, sh), __funnelshift_r(x0.w, x1.x, sh),
+                      __funnelshift_r(x1.x, x1.y, sh), __funnelshift_r(x1.y, x1.z, sh));
+  default:
+    return make_uint4(__funnelshift_r(x0.w, x1.x, sh), __funnelshift_r(x1.x, x1.y, sh),
+                      __funnelshift_r(x1.y, x1.z, sh), __funnelshift_r(x1.z, x1.w, sh));
+  }
+}
+
 // the 16 bytes starting at (window), of which only [lo, hi) are meaningful;
 // aligned 16-B blocks not intersecting [lo, hi) are never read
 __device__ __forceinline__ uint4 load_window(const uint8_t *window, const uint8_t *lo, const uint8_t *hi) {
@@ -293,17 +315,7 @@ __device__ __forceinline__ uint4 load_window(const uint8_t *window, const uint8_
   if (l < b0 + 16 && h > b0) x0 = ld_stream(reinterpret_cast<const uint4 *>(b0));
   const unsigned d = static_cast<unsigned>(w & 15);
   if (d && l < b1 + 16 && h > b1) x1 = ld_stream(reinterpret_cast<const uint4 *>(b1));
-  const uint32_t W[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-  const unsigned q = d >> 2, sh = (d & 3) * 8;
-  uint32_t v[5];
-#pragma unroll
-  for (int k = 0; k < 5; ++k) { // v[k] = W[k + q], selects instead of local memory
-    const uint32_t a = k + 0 < 8 ? W[k] : 0, b = k + 1 < 8 ? W[k + 1] : 0;
-    const uint32_t c = k + 2 < 8 ? W[k + 2] : 0, e = k + 3 < 8 ? W[k + 3] : 0;
-    v[k] = q == 0 ? a : q == 1 ? b : q == 2 ? c : e;
-  }
-  return make_uint4(__funnelshift_r(v[0], v[1], sh), __funnelshift_r(v[1], v[2], sh),
-                    __funnelshift_r(v[2], v[3], sh), __funnelshift_r(v[3], v[4], sh));
+  return funnel16(x0, x1, d); // a warp whose rows disagree on d >> 2 runs the cases in turn
 }
 
 __device__ __forceinline__ uint4 merge_bytes(uint4 a, uint4 b, unsigned n) { // bytes [0,n) of a, rest of b
@@ -438,42 +450,6 @@ __global__ void __launch_bounds__(256) k_runs(const uint8_t *__restrict__ in, ui
   }
 }
 
-// the 16 bytes starting d bytes into x0, continuing into x1 (d < 16)
-__device__ __forceinline__ uint4 funnel16(const uint4 &x0, const uint4 &x1, unsigned d) {
-  const uint32_t W[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-  const unsigned q = d >> 2, sh = (d & 3) * 8;
-  uint32_t v[5];
-#pragma unroll
-  for (int k = 0; k < 5; ++k) { // v[k] = W[k + q], selects instead of local memory
-    const uint32_t a = k + 0 < 8 ? W[k] : 0, b = k + 1 < 8 ? W[k + 1] : 0;
-    const uint32_t c = k + 2 < 8 ? W[k + 2] : 0, e = k + 3 < 8 ? W[k + 3] : 0;
-    v[k] = q == 0 ? a : q == 1 ? b : q == 2 ? c : e;
-  }
-  return make_uint4(__funnelshift_r(v[0], v[1], sh), __funnelshift_r(v[1], v[2], sh),
-                    __funnelshift_r(v[2], v[3], sh), __funnelshift_r(v[3], v[4], sh));
-}
-
-// funnel16 with the word offset q = d >> 2 known to be uniform across the
-// group (one shift per run): a switch on q picks compile-time word indices,
-// so each output word is one funnel shift instead of a select chain
-__device__ __forceinline__ uint4 funnel16_uniform(const uint4 &x0, const uint4 &x1, unsigned d) {
-  const unsigned sh = (d & 3) * 8;
-  switch (d >> 2) {
-  case 0:
-    return make_uint4(__funnelshift_r(x0.x, x0.y, sh), __funnelshift_r(x0.y, x0.z, sh),
-                      __funnelshift_r(x0.z, x0.w, sh), __funnelshift_r(x0.w, x1.x, sh));
-  case 1:
-    return make_uint4(__funnelshift_r(x0.y, x0.z, sh), __funnelshift_r(x0.z, x0.w, sh),
-                      __funnelshift_r(x0.w, x1.x, sh), __funnelshift_r(x1.x, x1.y, sh));
-  case 2:
-    return make_uint4(__funnelshift_r(x0.z, x0.w, sh), __funnelshift_r(x0.w, x1.x, sh),
-                      __funnelshift_r(x1.x, x1.y, sh), __funnelshift_r(x1.y, x1.z, sh));
-  default:
-    return make_uint4(__funnelshift_r(x0.w, x1.x, sh), __funnelshift_r(x1.x, x1.y, sh),
-                      __funnelshift_r(x1.y, x1.z, sh), __funnelshift_r(x1.z, x1.w, sh));
-  }
-}
-
 __device__ __forceinline__ uint4 shfl_down4(unsigned mask, const uint4 &x, int width) {
   return make_uint4(__shfl_down_sync(mask, x.x, 1, width), __shfl_down_sync(mask, x.y, 1, width),
                     __shfl_down_sync(mask, x.z, 1, width), __shfl_down_sync(mask, x.w, 1, width));
@@ -515,7 +491,7 @@ __device__ __forceinline__ void shift_run(const uint8_t *src, uint8_t *dst, int6
   auto put = [&](int64_t b, const uint4 &x0, uint4 x1, const uint4 &nx) {
     if (!(lane == g - 1 || b + 1 >= nblk)) x1 = nx;
     if (b >= nblk) return;
-    const uint4 z = d ? funnel16_uniform(x0, x1, d) : x0;
+    const uint4 z = d ? funnel16(x0, x1, d) : x0;
     const uintptr_t B = first + 16 * static_cast<uintptr_t>(b);
     const uintptr_t vlo = B > A ? B : A, vhi = B + 16 < E ? B + 16 : E;
     uint8_t *blk = reinterpret_cast<uint8_t *>(B);
