@@ -90,7 +90,21 @@ struct BatchSig {
   // (the host reports SP_ERR_TIMEOUT after its next synchronisation)
   unsigned long long timeout_ns;
   int *err;
+  // device iteration numbering (BatchSignal::iter): values (it + add) << shift
+  const unsigned long long *iter;
+  long long pre_add, wait_add, post_add;
+  int pre_shift, wait_shift, post_shift;
+  unsigned long long *iter_store; // block 0 records iter_value here
+  unsigned long long iter_value;
 };
+
+// a protocol value: the host's, or derived from the device iteration number
+__device__ __forceinline__ unsigned long long sig_value(const BatchSig &sig, unsigned long long host, long long add,
+                                                        int shift) {
+  if (!sig.iter) return host;
+  const unsigned long long it = *reinterpret_cast<const volatile unsigned long long *>(sig.iter);
+  return (it + static_cast<unsigned long long>(add)) << shift;
+}
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
   unsigned long long v;
@@ -172,12 +186,14 @@ template <int W, int MODE> __device__ __forceinline__ void move_chunk(const Batc
 }
 
 __device__ __forceinline__ void batch_prologue(const BatchSig &sig) {
+  if (sig.iter_store && blockIdx.x == 0 && threadIdx.x == 0) *sig.iter_store = sig.iter_value;
   if (sig.n_pre && blockIdx.x == 0 && threadIdx.x < static_cast<unsigned>(sig.n_pre))
-    st_release_sys(sig.pre[threadIdx.x], sig.pre_value);
+    st_release_sys(sig.pre[threadIdx.x], sig_value(sig, sig.pre_value, sig.pre_add, sig.pre_shift));
   // stream mode: satisfied before the launch, one acquire load each;
   // in-kernel mode (every rank on its own GPU): spins until the peers publish
   if (sig.n_wait) {
-    if (threadIdx.x < static_cast<unsigned>(sig.n_wait)) wait_flag(sig.wait[threadIdx.x], sig.wait_value, sig, 64);
+    if (threadIdx.x < static_cast<unsigned>(sig.n_wait))
+      wait_flag(sig.wait[threadIdx.x], sig_value(sig, sig.wait_value, sig.wait_add, sig.wait_shift), sig, 64);
     __syncthreads();
   }
 }
@@ -202,7 +218,10 @@ __device__ __forceinline__ void batch_epilogue(const BatchSig &sig) {
     // wait on each other in a cycle; the grid is one resident wave, so the
     // other blocks run to completion meanwhile
     if (blockIdx.x == 0 && threadIdx.x < static_cast<unsigned>(sig.n_post))
-      wait_flag(sig.post[threadIdx.x], sig.per_target ? sig.post_vals[threadIdx.x] : sig.post_value, sig, 32);
+      wait_flag(sig.post[threadIdx.x],
+                sig.per_target ? sig.post_vals[threadIdx.x]
+                               : sig_value(sig, sig.post_value, sig.post_add, sig.post_shift),
+                sig, 32);
   }
 }
 
@@ -631,6 +650,8 @@ void stream_flag_ops(cudaStream_t s, const std::vector<uint64_t *> &writes, uint
   if (r != CUDA_SUCCESS) fail(SP_ERR_CUDA, "cuStreamBatchMemOp failed (" + std::to_string(static_cast<int>(r)) + ")");
 }
 
+__global__ void k_iter_tick(unsigned long long *c) { *c += 1; }
+
 void batch_launch(const Batch &b, void *stream, const BatchSignal *bs) {
   sp_launch_info li{};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -640,6 +661,19 @@ void batch_launch(const Batch &b, void *stream, const BatchSignal *bs) {
     if (bs) {
       sig.timeout_ns = bs->timeout_ns;
       sig.err = bs->err;
+      if (bs->iter && bs->stream_waits)
+        fail(SP_ERR_UNSUPPORTED, "device iteration numbers need in-kernel flag waits");
+      sig.iter = reinterpret_cast<const unsigned long long *>(bs->iter);
+      sig.pre_add = bs->pre_add;
+      sig.wait_add = bs->wait_add;
+      sig.post_add = bs->post_add;
+      sig.pre_shift = bs->pre_shift;
+      sig.wait_shift = bs->wait_shift;
+      sig.post_shift = bs->post_shift;
+      if (gi == 0) {
+        sig.iter_store = reinterpret_cast<unsigned long long *>(bs->iter_store);
+        sig.iter_value = bs->iter_value;
+      }
     }
     if (bs) { // pre-signal and wait in the first kernel, signal from the last
       if (bs->wait.size() > static_cast<size_t>(kMaxSig) || bs->signal.size() > static_cast<size_t>(kMaxSig) ||
@@ -826,6 +860,12 @@ void batch_execute(const Batch &b, void *stream) { batch_launch(b, stream, nullp
 void batch_execute_signaled(const Batch &b, void *stream, const BatchSignal &sig) {
   if (b.groups.empty()) fail(SP_ERR_UNSUPPORTED, "batch signalling needs at least one non-empty job");
   batch_launch(b, stream, &sig);
+}
+
+void iter_tick(uint64_t *counter, void *stream) {
+  k_iter_tick<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<unsigned long long *>(counter));
+  cuda_check(cudaGetLastError(), "k_iter_tick launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void batch_destroy(Batch *b) { delete b; }

@@ -65,6 +65,11 @@ struct sp_halo_plan_s {
   std::vector<uint8_t *> peer_flags;
   std::vector<int> out_peers, in_peers; // distinct neighbours
   uint64_t iter = 0;
+  // device iteration number: recorded by every host-numbered launch,
+  // advanced on the device (iter_tick) once the plan was captured into a CUDA
+  // graph -- from then on every exchange is numbered on the device
+  uint64_t *dev_iter = nullptr;
+  bool graph_mode = false;
   bool remote_peers = true; // some neighbour's memory is on another GPU
   std::vector<uint8_t *> pinned; // peer mappings held for the plan's lifetime
   ~sp_halo_plan_s() {
@@ -76,6 +81,7 @@ struct sp_halo_plan_s {
     if (recv) cudaFree(recv);
     if (send) cudaFree(send);
     if (flags) cudaFree(flags);
+    if (dev_iter) cudaFree(dev_iter);
   }
 };
 
@@ -368,6 +374,8 @@ sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int metho
     }
     for (auto &e : p->ev) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
     if (method == SP_HALO_FUSED_ASYNC || method == SP_HALO_DIRECT) {
+      cuda_check(cudaMalloc(&p->dev_iter, sizeof(uint64_t)), "cudaMalloc(iteration counter)");
+      cuda_check(cudaMemset(p->dev_iter, 0, sizeof(uint64_t)), "cudaMemset(iteration counter)");
       const int n = rt_size();
       cuda_check(cudaMalloc(&p->flags, 2 * n * sizeof(uint64_t)), "cudaMalloc(flags)");
       cuda_check(cudaMemset(p->flags, 0, 2 * n * sizeof(uint64_t)), "cudaMemset(flags)");
@@ -416,13 +424,48 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
   return guarded([&] {
     need(p);
     cudaStream_t s = static_cast<cudaStream_t>(rt_stream());
-    // the flag values of an exchange are per iteration (FREE=n-1, READY=n):
-    // a captured launch replayed from a CUDA graph would reuse them and
-    // return before the peers' ghosts land, so capture is refused
+    // The flag values of an exchange are per iteration (FREE=n-1, READY=n).
+    // A launch captured into a CUDA graph is replayed with its parameters
+    // frozen, so a captured exchange numbers its iterations on the device
+    // instead: a one-thread tick kernel advances the plan's counter and the
+    // copy kernels derive FREE/READY from it. That needs the flag waits in
+    // the kernels (every rank on its own GPU, or TEMPI_FLAG_WAIT=kernel);
+    // stream memory operations carry fixed values. A plan with no peer (a
+    // 1x1x1 grid: no flags at all) captures in either mode.
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cuda_check(cudaStreamIsCapturing(s, &cap), "cudaStreamIsCapturing");
-    if (cap != cudaStreamCaptureStatusNone)
-      fail(SP_ERR_UNSUPPORTED, "halo exchange: cannot be captured into a CUDA graph (per-iteration flag values)");
+    const bool capturing = cap != cudaStreamCaptureStatusNone;
+    const bool peers = !p->out_peers.empty() || !p->in_peers.empty();
+    if (capturing) {
+      if (p->method != SP_HALO_DIRECT && p->method != SP_HALO_FUSED_ASYNC)
+        fail(SP_ERR_UNSUPPORTED, "halo exchange capture: only the device-ordered methods (DIRECT, FUSED_ASYNC)");
+      if (times) fail(SP_ERR_INVALID_ARGUMENT, "halo exchange capture: a captured exchange only enqueues (times == NULL)");
+      if (peers && rt_flag_waits_in_stream())
+        fail(SP_ERR_UNSUPPORTED, "halo exchange capture: needs in-kernel flag waits (each rank on its own GPU, "
+                                 "or TEMPI_FLAG_WAIT=kernel); stream memory operations carry fixed values");
+      p->graph_mode = true;
+    }
+    // one iteration's protocol values: host-numbered (recorded on the
+    // device), or device-numbered after a tick
+    auto number = [&](BatchSignal &b, int64_t pre_add, int64_t wait_add, int wait_shift, int64_t post_add,
+                      int post_shift, uint64_t it, bool first) {
+      if (p->graph_mode && peers) { // (no peer: no flag, nothing to number)
+        b.iter = p->dev_iter;
+        b.pre_add = pre_add;
+        b.wait_add = wait_add;
+        b.wait_shift = wait_shift;
+        b.post_add = post_add;
+        b.post_shift = post_shift;
+      } else if (first) {
+        b.iter_store = p->dev_iter;
+        b.iter_value = it;
+      }
+    };
+    if (p->graph_mode && peers) iter_tick(p->dev_iter, s);
+    // timing events only outside a capture (a captured exchange is untimed)
+    auto mark = [&](int k) {
+      if (!capturing) cuda_check(cudaEventRecord(p->ev[k], s), "cudaEventRecord");
+    };
     if (p->method == SP_HALO_DIRECT) {
       // one copy launch per iteration: block 0 first tells this rank's
       // senders that the ghosts of iteration n-1 are consumed (FREE=n-1;
@@ -459,9 +502,10 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
       ks.post_value = it << 32; // READY counts 2^32 per sender launch
       ks.err = rt_device_err();
       ks.timeout_ns = rt_device_timeout_ns();
-      cuda_check(cudaEventRecord(p->ev[0], s), "cudaEventRecord");
+      number(ks, -1, -1, 0, 0, 32, it, true); // FREE = n-1, READY = n << 32
+      mark(0);
       batch_execute_signaled(*p->pack, s, ks);
-      cuda_check(cudaEventRecord(p->ev[3], s), "cudaEventRecord"); // one launch: no phase boundaries
+      mark(3); // one launch: no phase boundaries
     } else if (p->method == SP_HALO_FUSED_ASYNC) {
       // device-ordered iteration, signalled from inside the kernels: the
       // pack batch waits (in every block) until each receiver has consumed
@@ -490,12 +534,14 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
       ps.stream_waits = us.stream_waits = rt_flag_waits_in_stream();
       ps.err = us.err = rt_device_err();
       ps.timeout_ns = us.timeout_ns = rt_device_timeout_ns();
-      cuda_check(cudaEventRecord(p->ev[0], s), "cudaEventRecord");
+      number(ps, 0, -1, 32, 0, 0, it, true); // the pack waits FREE = (n-1) << 32
+      number(us, 0, 0, 32, 0, 0, it, false); // the unpack waits READY = n << 32
+      mark(0);
       batch_execute_signaled(*p->pack, s, ps);
-      cuda_check(cudaEventRecord(p->ev[1], s), "cudaEventRecord");
-      cuda_check(cudaEventRecord(p->ev[2], s), "cudaEventRecord");
+      mark(1);
+      mark(2);
       batch_execute_signaled(*p->unpack, s, us);
-      cuda_check(cudaEventRecord(p->ev[3], s), "cudaEventRecord");
+      mark(3);
     } else {
     rt_barrier(); // every neighbour has consumed the previous iteration
     cuda_check(cudaEventRecord(p->ev[0], s), "cudaEventRecord");

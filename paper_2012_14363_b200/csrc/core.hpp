@@ -258,11 +258,25 @@ struct BatchSignal {
   bool stream_waits = true; // pre/wait through stream memory ops (else block 0 / every block in-kernel)
   int *err = nullptr;      // set to 1 by an in-kernel wait that gave up (mapped host memory)
   uint64_t timeout_ns = 0; // in-kernel wait limit, 0 = unbounded
+  // Device-side iteration numbers (a launch replayed from a CUDA graph): when
+  // `iter` is set the kernels read it = *iter (advanced by iter_tick ahead of
+  // the launch) and use value = (it + add) << shift for pre / wait / post
+  // instead of the values above. In-kernel waits only.
+  const uint64_t *iter = nullptr;
+  int64_t pre_add = 0, wait_add = 0, post_add = 0;
+  int pre_shift = 0, wait_shift = 0, post_shift = 0;
+  // host-numbered launches record their iteration here (block 0), so a
+  // later switch to device numbering continues from it
+  uint64_t *iter_store = nullptr;
+  uint64_t iter_value = 0;
 };
 constexpr int kMaxSignalPeers = 32; // flags a signalled launch carries (batch.cu kMaxSig)
 // one-warp kernel: adds 2^32 to each signal counter, then waits for the post counters
 void flags_signal_wait(const BatchSignal &sig, void *stream);
 void batch_execute_signaled(const Batch &b, void *stream, const BatchSignal &sig);
+// one-thread kernel: *counter += 1 (the device iteration number of a
+// graph-replayable exchange)
+void iter_tick(uint64_t *counter, void *stream);
 int64_t batch_bytes(const Batch &b);
 
 } // namespace spb

@@ -251,10 +251,11 @@ def test_copy_batch_counts_and_errors(sp, orc, cuda):
 
 
 @pytest.mark.gpu
-def test_halo_exchange_refuses_graph_capture(sp, cuda):
-    """an exchange's flag values change every iteration, so a captured launch
-    replayed from a graph would not wait for the peers: the engine refuses
-    the capture instead of recording it"""
+@pytest.mark.parametrize("method", [3, 2])  # DIRECT, FUSED_ASYNC
+def test_halo_exchange_graph_capture_one_rank(sp, cuda, method):
+    """a 1x1x1 plan has no peer flags: its exchange captures into a CUDA
+    graph as is; each replay rewrites every ghost cell (the shell is reset
+    between replays), and the plan stays usable eagerly afterwards"""
     import uuid
     torch = cuda
     import paper_2012_14363_b200.halo as H
@@ -263,18 +264,28 @@ def test_halo_exchange_refuses_graph_capture(sp, cuda):
     try:
         cfg = H.HaloConfig((1, 1, 1), (12, 10, 8), 2, 16)
         alloc = torch.zeros(16 * 14 * 12 * 16, dtype=torch.uint8, device="cuda")
-        plan = rt.HaloPlan(cfg, alloc, H.DIRECT)
+        plan = rt.HaloPlan(cfg, alloc, method)
         plan.exchange()
         rs = torch.cuda.ExternalStream(rt.stream())
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(rs):
             g.capture_begin()
             try:
-                with pytest.raises(sp.Unsupported):
-                    plan.exchange(timed=False)
+                plan.exchange(timed=False)
             finally:
                 g.capture_end()
-        plan.exchange()  # still usable outside a capture
+        for _ in range(3):
+            H.fill(cfg, 0, alloc)
+            torch.cuda.synchronize()
+            with torch.cuda.stream(rs):
+                g.replay()
+            rs.synchronize()
+            assert H.verify(cfg, 0, alloc) == 0
+        H.fill(cfg, 0, alloc)
+        torch.cuda.synchronize()
+        plan.exchange()
+        assert H.verify(cfg, 0, alloc) == 0
+        del g
         plan.free()
     finally:
         rt.finalize()

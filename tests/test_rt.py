@@ -940,6 +940,86 @@ def _halo(rank, world, job, ranks, method):
     return bad, t
 
 
+def _halo_graph(rank, world, job, ranks, method, flag_wait):
+    """a distributed exchange captured into a CUDA graph: with in-kernel flag
+    waits the plan numbers its iterations on the device (a tick kernel
+    advances its counter, the copy kernels derive FREE/READY from it), so
+    replays order the ranks like eager calls; host-numbered iterations
+    before the capture and eager ones after it continue the same count.
+    With stream flag waits (fixed values) the capture is refused."""
+    import os
+    os.environ["TEMPI_FLAG_WAIT"] = flag_wait
+    import torch
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.halo as H
+    import paper_2012_14363_b200.rt as rt
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=1 << 20, host_bytes=1 << 20)
+    cfg = H.HaloConfig(ranks, (10, 12, 8), 2, 8)
+    alloc = torch.empty(14 * 16 * 12 * 8, dtype=torch.uint8, device="cuda")
+    plan = rt.HaloPlan(cfg, alloc, method)
+    rs = torch.cuda.ExternalStream(rt.stream())
+    H.fill(cfg, rank, alloc)
+    torch.cuda.synchronize()
+    rt.barrier()
+    for _ in range(2):  # host-numbered iterations first
+        plan.exchange(timed=False)
+    rs.synchronize()
+    bad = H.verify(cfg, rank, alloc)
+    g = torch.cuda.CUDAGraph()
+    refused = False
+    with torch.cuda.stream(rs):
+        g.capture_begin()
+        try:
+            plan.exchange(timed=False)
+        except sp.Unsupported:
+            refused = True
+        finally:
+            g.capture_end()
+    if refused:
+        plan.exchange()  # still usable eagerly
+        bad += H.verify(cfg, rank, alloc)
+        plan.free()
+        rt.finalize()
+        return bad, "refused"
+    for _ in range(4):
+        H.fill(cfg, rank, alloc)  # reset the ghosts: each replay must rewrite them
+        torch.cuda.synchronize()
+        rt.barrier()
+        with torch.cuda.stream(rs):
+            g.replay()
+        rs.synchronize()
+        bad += H.verify(cfg, rank, alloc)
+    for _ in range(3):  # several replays back to back, no host sync between them
+        with torch.cuda.stream(rs):
+            g.replay()
+    rs.synchronize()
+    H.fill(cfg, rank, alloc)
+    torch.cuda.synchronize()
+    rt.barrier()
+    plan.exchange(timed=False)  # eager again: device-numbered from now on
+    rs.synchronize()
+    bad += H.verify(cfg, rank, alloc)
+    del g
+    plan.free()
+    rt.finalize()
+    return bad, "captured"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ranks,method", [((2, 1, 1), 3), ((2, 1, 1), 2), ((2, 2, 1), 3)])
+def test_distributed_halo_graph_capture(cuda, ranks, method):
+    world = ranks[0] * ranks[1] * ranks[2]
+    res = _spawn(_halo_graph, world, ranks, method, "kernel", timeout=400)
+    assert all(v == (0, "captured") for v in res.values()), res
+
+
+@pytest.mark.gpu
+def test_distributed_halo_graph_capture_refused_in_stream_mode(cuda):
+    res = _spawn(_halo_graph, 2, (2, 1, 1), 3, "stream", timeout=300)
+    assert all(v == (0, "refused") for v in res.values()), res
+
+
 def _halo_peer_absent(rank, world, job):
     """rank 1 builds the DIRECT halo plan and then never exchanges: rank 0's
     exchange kernel waits in its last block for rank 1's READY flag, gives

@@ -225,7 +225,77 @@ def halo_section(torch, rank, world, local, job, iters=20, warmup=5, nccl=True):
     out["verified"] = out["verified"] and _reduce(torch, world, float(bad_w), MAX) == 0
     if nccl and world > 1 and dist.is_initialized() and dist.get_backend() == "nccl":
         out["nccl"] = _nccl_halo(torch, cfg, regions, seg, alloc, rank, world, iters, warmup, cold)
+    out["steady_state"] = _halo_steady(torch, rt, H, cfg, alloc, rank, world)
     rt.finalize()
+    return out
+
+
+def _halo_steady(torch, rt, H, cfg, alloc, rank, world, iters=200, per_graph=10):
+    """the iterations of a time loop: exchanges back to back with no host
+    synchronisation and no L2 flush between them, enqueued eagerly, or
+    replayed from a CUDA graph holding `per_graph` exchanges (the plan then
+    numbers its iterations on the device). Wall time per iteration over
+    `iters` iterations, max over ranks; every ghost verified after a
+    replay. With ranks sharing a GPU (stream flag waits) a plan with peers
+    refuses the capture."""
+    import time
+    import paper_2012_14363_b200 as sp
+    import torch.distributed as dist
+    MAX = dist.ReduceOp.MAX if dist.is_initialized() else None
+    rs = torch.cuda.ExternalStream(rt.stream())
+    out = {"how": f"{iters} back-to-back exchanges, warm L2, wall time per iteration (max over ranks); "
+                  f"graph = replays of a CUDA graph of {per_graph} exchanges"}
+    for method, name in ((H.DIRECT, "direct"), (H.FUSED_ASYNC, "fused_async")):
+        H.fill(cfg, rank, alloc)
+        torch.cuda.synchronize()
+        rt.barrier()
+        plan = rt.HaloPlan(cfg, alloc, method)
+        for _ in range(5):
+            plan.exchange(timed=False)
+        rs.synchronize()
+        rt.barrier()
+        t0 = time.perf_counter()
+        for _ in range(iters):
+            plan.exchange(timed=False)
+        rs.synchronize()
+        eager = _reduce(torch, world, (time.perf_counter() - t0) / iters, MAX)
+        row = {"eager_us": round(eager * 1e6, 2)}
+        g = torch.cuda.CUDAGraph()
+        refused = False
+        with torch.cuda.stream(rs):
+            g.capture_begin()
+            try:
+                for _ in range(per_graph):
+                    plan.exchange(timed=False)
+            except sp.Unsupported:
+                refused = True
+            finally:
+                g.capture_end()
+        if refused:
+            row["graph"] = "refused (ranks share a GPU: stream flag waits)"
+        else:
+            with torch.cuda.stream(rs):
+                g.replay()
+            rs.synchronize()
+            rt.barrier()
+            t0 = time.perf_counter()
+            with torch.cuda.stream(rs):
+                for _ in range(iters // per_graph):
+                    g.replay()
+            rs.synchronize()
+            graph = _reduce(torch, world, (time.perf_counter() - t0) / iters, MAX)
+            H.fill(cfg, rank, alloc)
+            torch.cuda.synchronize()
+            rt.barrier()
+            with torch.cuda.stream(rs):
+                g.replay()
+            rs.synchronize()
+            bad = _reduce(torch, world, float(H.verify(cfg, rank, alloc)), MAX)
+            row.update({"graph_us": round(graph * 1e6, 2), "speedup": round(eager / graph, 2),
+                        "verified": bad == 0})
+        del g
+        plan.free()
+        out[name] = row
     return out
 
 
