@@ -462,9 +462,10 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
       }
     };
     if (p->graph_mode && peers) iter_tick(p->dev_iter, s);
-    // timing events only outside a capture (a captured exchange is untimed)
+    // the device-ordered methods record their events only for timings (an
+    // enqueue-only call, captured or not, never reads them)
     auto mark = [&](int k) {
-      if (!capturing) cuda_check(cudaEventRecord(p->ev[k], s), "cudaEventRecord");
+      if (times) cuda_check(cudaEventRecord(p->ev[k], s), "cudaEventRecord");
     };
     if (p->method == SP_HALO_DIRECT) {
       // one copy launch per iteration: block 0 first tells this rank's
