@@ -150,6 +150,14 @@ int MPI_Waitsome(int incount, MPI_Request requests[], int *outcount, int indices
 int MPI_Testany(int count, MPI_Request requests[], int *index, int *flag, MPI_Status *status);
 int MPI_Testall(int count, MPI_Request requests[], int *flag, MPI_Status statuses[]);
 int MPI_Request_free(MPI_Request *request);
+/* persistent requests (MPI-3.1 3.9): MPI_Start / MPI_Startall begin the
+ * recorded operation; completion leaves the request inactive, not freed */
+int MPI_Send_init(const void *buf, int count, MPI_Datatype datatype, int dest, int tag, MPI_Comm comm,
+                  MPI_Request *request);
+int MPI_Recv_init(void *buf, int count, MPI_Datatype datatype, int source, int tag, MPI_Comm comm,
+                  MPI_Request *request);
+int MPI_Start(MPI_Request *request);
+int MPI_Startall(int count, MPI_Request requests[]);
 int MPI_Sendrecv(const void *sendbuf, int sendcount, MPI_Datatype sendtype, int dest, int sendtag, void *recvbuf,
                  int recvcount, MPI_Datatype recvtype, int source, int recvtag, MPI_Comm comm,
                  MPI_Status *status);

@@ -194,6 +194,9 @@ struct State {
   std::unordered_map<MPI_Datatype, Mirror> types;
   std::unordered_map<MPI_Comm, std::pair<int, int>> degree; // comm -> (indegree, outdegree)
   std::unordered_map<MPI_Request, Pending> pending;
+  // persistent requests of accelerated types (MPI_Send_init / MPI_Recv_init):
+  // their packed message buffers live until MPI_Request_free
+  std::unordered_map<MPI_Request, Pending> persist;
   // mirrors still named by a pending receive, and the ones among them whose
   // MPI type was freed (MPI lets a pending operation outlive its datatype):
   // released when the last such receive completes
@@ -826,12 +829,29 @@ namespace {
 // a request the system MPI just completed: unpack a receive, free its scratch
 int finish(MPI_Request key, MPI_Status *status, int rc) {
   Pending p;
+  bool persistent = false;
   {
     std::lock_guard<std::mutex> lk(S().mu);
     auto it = S().pending.find(key);
-    if (it == S().pending.end()) return rc;
-    p = it->second;
-    S().pending.erase(it);
+    if (it == S().pending.end()) {
+      auto q = S().persist.find(key);
+      if (q == S().persist.end()) return rc;
+      p = q->second; // a persistent request: unpack a receive, keep the buffers
+      persistent = true;
+    } else {
+      p = it->second;
+      S().pending.erase(it);
+    }
+  }
+  if (persistent) {
+    if (p.recv && rc == MPI_SUCCESS && status) {
+      Mirror m;
+      m.h = p.type;
+      m.size = p.size;
+      rc = unpack_message(m, p.user, received(status), p.method, p.dev, p.host);
+      report_method(status, p.method);
+    }
+    return rc;
   }
   struct Release { // the receive's mirror, once nothing pending names it
     sp_type h;
@@ -950,13 +970,123 @@ int MPI_Testall(int n, MPI_Request reqs[], int *flag, MPI_Status statuses[]) {
 // buffer until the system MPI is done with it (a send): it is completed here
 int MPI_Request_free(MPI_Request *req) {
   if (!req) return MPI_ERR_ARG;
-  bool ours = false;
+  bool ours = false, persistent = false;
   {
     std::lock_guard<std::mutex> lk(S().mu);
     ours = S().pending.count(*req) != 0;
+    persistent = S().persist.count(*req) != 0;
+  }
+  if (persistent) { // complete an operation still in flight, then release the buffers
+    const MPI_Request key = *req;
+    int rc = MPI_Wait(req, MPI_STATUS_IGNORE);
+    const int rf = REAL(Request_free)(req);
+    Pending p;
+    {
+      std::lock_guard<std::mutex> lk(S().mu);
+      p = S().persist[key];
+      S().persist.erase(key);
+      if (p.recv) {
+        auto f = S().in_flight.find(p.type);
+        if (f != S().in_flight.end() && --f->second == 0) {
+          S().in_flight.erase(f);
+          if (S().retired.erase(p.type)) sp_type_free(p.type);
+        }
+      }
+    }
+    give_buffers(p);
+    return rc != MPI_SUCCESS ? rc : rf;
   }
   if (!ours) return REAL(Request_free)(req);
   return MPI_Wait(req, MPI_STATUS_IGNORE);
+}
+
+// ---- persistent requests (MPI-3.1 3.9): the system MPI's persistent
+// request moves the packed MPI_BYTE message; MPI_Start packs first
+int MPI_Send_init(const void *buf, int count, MPI_Datatype dt, int dest, int tag, MPI_Comm comm, MPI_Request *req) {
+  Mirror m;
+  if (!req) return MPI_ERR_ARG;
+  if (!accel(dt, buf, count, &m) || m.size * count > INT32_MAX) {
+    S().st.forwarded++;
+    return REAL(Send_init)(buf, count, dt, dest, tag, comm, req);
+  }
+  Pending p;
+  p.user = const_cast<void *>(buf);
+  p.count = count;
+  p.type = m.h;
+  p.size = m.size;
+  p.method = choose(m, count);
+  const size_t bytes = static_cast<size_t>(m.size * count);
+  if (!take_buffers(p, bytes)) return MPI_ERR_NO_MEM;
+  // the buffer the system MPI sends from: pinned for one-shot / staged
+  void *msg = p.method == SP_METHOD_DEVICE ? p.dev : p.host;
+  const int rc = REAL(Send_init)(msg, static_cast<int>(bytes), MPI_BYTE, dest, tag, comm, req);
+  if (rc != MPI_SUCCESS) {
+    give_buffers(p);
+    return rc;
+  }
+  std::lock_guard<std::mutex> lk(S().mu);
+  S().persist[*req] = p;
+  return MPI_SUCCESS;
+}
+
+int MPI_Recv_init(void *buf, int count, MPI_Datatype dt, int source, int tag, MPI_Comm comm, MPI_Request *req) {
+  Mirror m;
+  if (!req) return MPI_ERR_ARG;
+  if (!accel(dt, buf, count, &m) || m.size * count > INT32_MAX) {
+    S().st.forwarded++;
+    return REAL(Recv_init)(buf, count, dt, source, tag, comm, req);
+  }
+  Pending p;
+  p.recv = true;
+  p.user = buf;
+  p.count = count;
+  p.type = m.h;
+  p.size = m.size;
+  p.method = choose(m, count);
+  const size_t bytes = static_cast<size_t>(m.size * count);
+  if (!take_buffers(p, bytes)) return MPI_ERR_NO_MEM;
+  const int rc = REAL(Recv_init)(recv_target(p.method, p.dev, p.host), static_cast<int>(bytes), MPI_BYTE, source,
+                                 tag, comm, req);
+  if (rc != MPI_SUCCESS) {
+    give_buffers(p);
+    return rc;
+  }
+  std::lock_guard<std::mutex> lk(S().mu);
+  S().persist[*req] = p;
+  ++S().in_flight[p.type];
+  return MPI_SUCCESS;
+}
+
+int MPI_Start(MPI_Request *req) {
+  if (!req) return MPI_ERR_ARG;
+  Pending p;
+  bool ours = false;
+  {
+    std::lock_guard<std::mutex> lk(S().mu);
+    auto it = S().persist.find(*req);
+    if (it != S().persist.end()) {
+      ours = true;
+      p = it->second;
+    }
+  }
+  if (ours && !p.recv) { // pack this round's data into the registered message buffer
+    Mirror m;
+    m.h = p.type;
+    m.size = p.size;
+    void *msg = nullptr;
+    const int rc = pack_message(m, p.user, static_cast<int>(p.count), p.method, p.dev, p.host, &msg);
+    if (rc != MPI_SUCCESS) return rc;
+  }
+  return REAL(Start)(req);
+}
+
+int MPI_Startall(int n, MPI_Request reqs[]) {
+  if (n < 0 || (n && !reqs)) return MPI_ERR_ARG;
+  for (int i = 0; i < n; ++i) {
+    const int rc = MPI_Start(&reqs[i]);
+    if (rc != MPI_SUCCESS) return rc;
+  }
+  return MPI_SUCCESS;
 }
 
 // through the intercepted non-blocking calls, so both halves are accelerated

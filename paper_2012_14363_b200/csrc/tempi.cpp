@@ -47,6 +47,13 @@ struct State {
     bool done = false;
     sp_status rc = SP_OK;
     int64_t st[4] = {0, 0, 0, 0};
+    // persistent requests (MPI_Send_init / MPI_Recv_init, MPI-3.1 3.9): the
+    // operation's arguments, and whether a started one is in flight
+    bool persistent = false, active = false, is_send = false;
+    const void *buf = nullptr;
+    int count = 0, peer = 0, tag = 0;
+    MPI_Datatype dt = 0;
+    MPI_Comm comm = 0;
   };
   std::unordered_map<int, Pending> requests;
   int next_request = 1;
@@ -559,6 +566,10 @@ static int progress(MPI_Request request, bool block, bool *done) {
     if (it == S().requests.end()) return MPI_ERR_ARG;
     p = it->second;
   }
+  if (p.persistent && !p.active) { // an inactive persistent request is complete
+    *done = true;
+    return MPI_SUCCESS;
+  }
   if (!p.done) {
     int d = 1;
     p.rc = block ? sp_rt_wait(p.r, p.st) : sp_rt_test(p.r, &d, p.st);
@@ -585,13 +596,104 @@ static int complete(MPI_Request *request, MPI_Status *status, bool block, int *f
   State::Pending p;
   {
     std::lock_guard<std::mutex> lk(S().mu);
-    p = S().requests[*request];
-    S().requests.erase(*request);
+    State::Pending &e = S().requests[*request];
+    p = e;
+    if (e.persistent) { // completes, and stays allocated (inactive) for the next MPI_Start
+      e.active = false;
+      e.done = false;
+      e.r = 0;
+    } else {
+      S().requests.erase(*request);
+    }
   }
-  *request = MPI_REQUEST_NULL;
+  if (!p.persistent) *request = MPI_REQUEST_NULL;
+  if (p.persistent && !p.active) { // inactive: an empty status
+    if (status) *status = MPI_Status{MPI_ANY_SOURCE, MPI_ANY_TAG, MPI_SUCCESS, 0, 0};
+    return MPI_SUCCESS;
+  }
   TRY(p.rc);
   if (status) *status = MPI_Status{static_cast<int>(p.st[0]), static_cast<int>(p.st[1]), MPI_SUCCESS,
                                    static_cast<int>(p.st[3]), p.st[2]};
+  return MPI_SUCCESS;
+}
+
+// MPI_REQUEST_NULL or an inactive persistent request: skipped by the set
+// completions (MPI-3.1 3.7.5)
+static bool inactive(MPI_Request r) {
+  if (r == MPI_REQUEST_NULL) return true;
+  std::lock_guard<std::mutex> lk(S().mu);
+  auto it = S().requests.find(r);
+  return it != S().requests.end() && it->second.persistent && !it->second.active;
+}
+
+// ---- persistent requests (MPI-3.1 3.9)
+static int persistent_init(bool is_send, const void *buf, int count, MPI_Datatype dt, int peer, int tag,
+                           MPI_Comm comm, MPI_Request *request) {
+  if (!request) return MPI_ERR_ARG;
+  if (!comm_of(comm)) return MPI_ERR_COMM;
+  if (count < 0) return MPI_ERR_COUNT;
+  if (is_send && tag < 0) return MPI_ERR_TAG;
+  if (peer != MPI_PROC_NULL && (is_send || peer != MPI_ANY_SOURCE) && (peer < 0 || peer >= S().size))
+    return MPI_ERR_RANK;
+  TYPE(dt, h);
+  (void)h;
+  std::lock_guard<std::mutex> lk(S().mu);
+  const int id = S().next_request++;
+  State::Pending &e = S().requests[id];
+  e.persistent = true;
+  e.is_send = is_send;
+  e.buf = buf;
+  e.count = count;
+  e.dt = dt;
+  e.peer = peer;
+  e.tag = tag;
+  e.comm = comm;
+  *request = id;
+  return MPI_SUCCESS;
+}
+
+int MPI_Send_init(const void *buf, int count, MPI_Datatype datatype, int dest, int tag, MPI_Comm comm,
+                  MPI_Request *request) {
+  return persistent_init(true, buf, count, datatype, dest, tag, comm, request);
+}
+
+int MPI_Recv_init(void *buf, int count, MPI_Datatype datatype, int source, int tag, MPI_Comm comm,
+                  MPI_Request *request) {
+  return persistent_init(false, buf, count, datatype, source, tag, comm, request);
+}
+
+int MPI_Start(MPI_Request *request) {
+  if (!request || *request == MPI_REQUEST_NULL) return MPI_ERR_ARG;
+  State::Pending p;
+  {
+    std::lock_guard<std::mutex> lk(S().mu);
+    auto it = S().requests.find(*request);
+    if (it == S().requests.end() || !it->second.persistent || it->second.active) return MPI_ERR_ARG;
+    p = it->second;
+  }
+  if (p.peer == MPI_PROC_NULL) return MPI_SUCCESS; // completes at once
+  TYPE(p.dt, h);
+  sp_request r = 0;
+  if (p.is_send) {
+    TRY(sp_rt_isend(p.buf, UINT64_MAX, p.count, h, p.peer, p.tag, S().forced_method, &r));
+  } else {
+    TRY(sp_rt_irecv(const_cast<void *>(p.buf), UINT64_MAX, p.count, h, p.peer, p.tag, &r));
+  }
+  std::lock_guard<std::mutex> lk(S().mu);
+  State::Pending &e = S().requests[*request];
+  e.r = r;
+  e.active = true;
+  e.done = false;
+  e.rc = SP_OK;
+  return MPI_SUCCESS;
+}
+
+int MPI_Startall(int count, MPI_Request requests[]) {
+  if (count < 0 || (count && !requests)) return MPI_ERR_ARG;
+  for (int i = 0; i < count; ++i) {
+    const int rc = MPI_Start(&requests[i]);
+    if (rc != MPI_SUCCESS) return rc;
+  }
   return MPI_SUCCESS;
 }
 
@@ -617,7 +719,7 @@ int MPI_Waitall(int count, MPI_Request requests[], MPI_Status statuses[]) {
 // (which progresses the runtime) until their condition holds
 static bool all_null(int n, const MPI_Request r[]) {
   for (int i = 0; i < n; ++i)
-    if (r[i] != MPI_REQUEST_NULL) return false;
+    if (!inactive(r[i])) return false;
   return true;
 }
 
@@ -631,7 +733,7 @@ int MPI_Testany(int count, MPI_Request requests[], int *index, int *flag, MPI_St
     return MPI_SUCCESS;
   }
   for (int i = 0; i < count; ++i) {
-    if (requests[i] == MPI_REQUEST_NULL) continue;
+    if (inactive(requests[i])) continue;
     int done = 0;
     const int rc = complete(&requests[i], status, false, &done);
     if (rc != MPI_SUCCESS || done) {
@@ -677,7 +779,7 @@ int MPI_Waitsome(int incount, MPI_Request requests[], int *outcount, int indices
   for (;;) {
     int n = 0, first = MPI_SUCCESS;
     for (int i = 0; i < incount; ++i) {
-      if (requests[i] == MPI_REQUEST_NULL) continue;
+      if (inactive(requests[i])) continue;
       int done = 0;
       const int rc = complete(&requests[i], statuses ? &statuses[n] : nullptr, false, &done);
       if (rc != MPI_SUCCESS && first == MPI_SUCCESS) first = rc;
@@ -693,7 +795,13 @@ int MPI_Waitsome(int incount, MPI_Request requests[], int *outcount, int indices
 int MPI_Request_free(MPI_Request *request) {
   if (!request) return MPI_ERR_ARG;
   if (*request == MPI_REQUEST_NULL) return MPI_ERR_ARG;
-  return complete(request, nullptr, true, nullptr); // completes it, then the handle is released
+  const int rc = complete(request, nullptr, true, nullptr); // completes it, then the handle is released
+  if (*request != MPI_REQUEST_NULL) { // persistent: released here
+    std::lock_guard<std::mutex> lk(S().mu);
+    S().requests.erase(*request);
+    *request = MPI_REQUEST_NULL;
+  }
+  return rc;
 }
 
 int MPI_Sendrecv(const void *sendbuf, int sendcount, MPI_Datatype sendtype, int dest, int sendtag, void *recvbuf,

@@ -765,6 +765,9 @@ typedef struct {
   int used, is_recv, count, src, tag, ctx;
   Type ty; /* a copy: the datatype may be freed while the receive is pending */
   void *buf;
+  /* persistent requests (MPI_Send_init / MPI_Recv_init): recorded, started
+   * by MPI_Start, inactive again once complete */
+  int persistent, active;
 } Req;
 static Req g_reqs[4096];
 
@@ -821,6 +824,10 @@ static int complete(MPI_Request *r, MPI_Status *st, int block, int *flag) {
   if (*r < 0 || *r >= 4096 || !g_reqs[*r].used) return MPI_ERR_ARG;
   Req *q = &g_reqs[*r];
   int rc = MPI_SUCCESS;
+  if (q->persistent && !q->active) { /* inactive: complete, empty status */
+    if (st) *st = (MPI_Status){MPI_ANY_SOURCE, MPI_ANY_TAG, MPI_SUCCESS, -1, 0};
+    return MPI_SUCCESS;
+  }
   if (q->is_recv) {
     if (!block) {
       pthread_mutex_lock(&g_mu);
@@ -835,8 +842,12 @@ static int complete(MPI_Request *r, MPI_Status *st, int block, int *flag) {
   } else if (st) {
     *st = (MPI_Status){MPI_ANY_SOURCE, MPI_ANY_TAG, MPI_SUCCESS, -1, 0};
   }
-  q->used = 0;
-  *r = MPI_REQUEST_NULL;
+  if (q->persistent) {
+    q->active = 0;
+  } else {
+    q->used = 0;
+    *r = MPI_REQUEST_NULL;
+  }
   return rc;
 }
 
@@ -856,9 +867,13 @@ int PMPI_Waitall(int n, MPI_Request rs[], MPI_Status sts[]) {
 }
 int MPI_Waitall(int n, MPI_Request rs[], MPI_Status sts[]) ALIAS(MPI_Waitall);
 
+static int inactive(MPI_Request r) {
+  return r == MPI_REQUEST_NULL || (g_reqs[r].persistent && !g_reqs[r].active);
+}
+
 static int all_null(int n, const MPI_Request r[]) {
   for (int i = 0; i < n; ++i)
-    if (r[i] != MPI_REQUEST_NULL) return 0;
+    if (!inactive(r[i])) return 0;
   return 1;
 }
 
@@ -871,7 +886,7 @@ int PMPI_Testany(int n, MPI_Request rs[], int *index, int *flag, MPI_Status *st)
     return MPI_SUCCESS;
   }
   for (int i = 0; i < n; ++i) {
-    if (rs[i] == MPI_REQUEST_NULL) continue;
+    if (inactive(rs[i])) continue;
     int done = 0;
     const int rc = complete(&rs[i], st, 0, &done);
     if (rc != MPI_SUCCESS || done) {
@@ -906,7 +921,7 @@ int MPI_Waitany(int n, MPI_Request rs[], int *index, MPI_Status *st) ALIAS(MPI_W
 int PMPI_Testall(int n, MPI_Request rs[], int *flag, MPI_Status sts[]) {
   /* all or nothing (MPI-3.1 3.7.5): complete only when every one can */
   for (int i = 0; i < n; ++i) {
-    if (rs[i] == MPI_REQUEST_NULL || !g_reqs[rs[i]].is_recv) continue;
+    if (inactive(rs[i]) || !g_reqs[rs[i]].is_recv) continue;
     const Req *q = &g_reqs[rs[i]];
     pthread_mutex_lock(&g_mu);
     const int ready = match_locked(q->src, q->tag, q->ctx, 0) != NULL;
@@ -936,8 +951,68 @@ int MPI_Waitsome(int n, MPI_Request rs[], int *outcount, int indices[], MPI_Stat
 
 int PMPI_Request_free(MPI_Request *r) {
   if (!r || *r == MPI_REQUEST_NULL) return MPI_ERR_ARG;
-  return complete(r, NULL, 1, NULL);
+  const int rc = complete(r, NULL, 1, NULL);
+  if (*r != MPI_REQUEST_NULL) { /* persistent: released here */
+    g_reqs[*r].used = 0;
+    *r = MPI_REQUEST_NULL;
+  }
+  return rc;
 }
+
+/* persistent requests: a send starts eagerly (like MPI_Isend), a receive is
+ * matched at completion */
+static int persist(int is_recv, void *buf, int count, MPI_Datatype dt, int peer, int tag, MPI_Comm comm,
+                   MPI_Request *r) {
+  if (!r || !type_of(dt)) return MPI_ERR_ARG;
+  if (!comm_of(comm)) return MPI_ERR_COMM;
+  const int rc = new_req(r);
+  if (rc != MPI_SUCCESS) return rc;
+  Req *q = &g_reqs[*r];
+  q->persistent = 1;
+  q->is_recv = is_recv;
+  q->count = count;
+  q->src = peer == MPI_ANY_SOURCE || peer == MPI_PROC_NULL ? peer : world_rank(comm, peer);
+  q->tag = tag;
+  q->ctx = ctx_of(comm);
+  q->ty = *type_of(dt);
+  q->buf = buf;
+  return MPI_SUCCESS;
+}
+
+int PMPI_Send_init(const void *buf, int count, MPI_Datatype dt, int dest, int tag, MPI_Comm comm, MPI_Request *r) {
+  return persist(0, (void *)buf, count, dt, dest, tag, comm, r);
+}
+int MPI_Send_init(const void *buf, int count, MPI_Datatype dt, int dest, int tag, MPI_Comm comm, MPI_Request *r)
+    ALIAS(MPI_Send_init);
+
+int PMPI_Recv_init(void *buf, int count, MPI_Datatype dt, int source, int tag, MPI_Comm comm, MPI_Request *r) {
+  return persist(1, buf, count, dt, source, tag, comm, r);
+}
+int MPI_Recv_init(void *buf, int count, MPI_Datatype dt, int source, int tag, MPI_Comm comm, MPI_Request *r)
+    ALIAS(MPI_Recv_init);
+
+int PMPI_Start(MPI_Request *r) {
+  if (!r || *r <= 0 || *r >= 4096 || !g_reqs[*r].used || !g_reqs[*r].persistent || g_reqs[*r].active)
+    return MPI_ERR_ARG;
+  Req *q = &g_reqs[*r];
+  if (q->src == MPI_PROC_NULL) return MPI_SUCCESS;
+  if (!q->is_recv) {
+    const int rc = send_typed(q->buf, q->count, &q->ty, q->src, q->tag, q->ctx);
+    if (rc != MPI_SUCCESS) return rc;
+  }
+  q->active = 1;
+  return MPI_SUCCESS;
+}
+int MPI_Start(MPI_Request *r) ALIAS(MPI_Start);
+
+int PMPI_Startall(int n, MPI_Request rs[]) {
+  for (int i = 0; i < n; ++i) {
+    const int rc = PMPI_Start(&rs[i]);
+    if (rc != MPI_SUCCESS) return rc;
+  }
+  return MPI_SUCCESS;
+}
+int MPI_Startall(int n, MPI_Request rs[]) ALIAS(MPI_Startall);
 int MPI_Request_free(MPI_Request *r) ALIAS(MPI_Request_free);
 
 int PMPI_Sendrecv(const void *sbuf, int scount, MPI_Datatype stype, int dest, int stag, void *rbuf, int rcount,

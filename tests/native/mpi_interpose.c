@@ -14,8 +14,9 @@
  *     a receive into HOST memory with the derived type (the wire format is
  *     the type signature, so a receiver without the interposer reads it),
  *     MPI_Isend / MPI_Irecv / MPI_Waitall in both directions, MPI_Sendrecv,
- *     and the set completions (Waitany, Waitsome, Testall, Testany,
- *     Request_free) on device receives of every type.
+ *     the set completions (Waitany, Waitsome, Testall, Testany,
+ *     Request_free) on device receives of every type, and persistent
+ *     requests (Send_init / Recv_init / Startall) over three rounds.
  * Without a GPU only the host paths run (everything is forwarded): the same
  * types packed, unpacked and sent between ranks from host memory.
  * As with any CUDA-aware MPI, a device buffer is ready (its cudaMemset has
@@ -254,6 +255,39 @@ int main(int argc, char **argv) {
         CHECK(MPI_Wait(&rr[1], MPI_STATUS_IGNORE) == MPI_SUCCESS);
         cudaMemcpy(back, r3[1], span, cudaMemcpyDeviceToHost);
         CHECK(memcmp(back, hd, span) == 0);
+        /* persistent requests (MPI-3.1 3.9): three rounds of Startall +
+         * Waitall on the same requests, the send data changing between
+         * rounds (each MPI_Start packs the current contents) */
+        MPI_Request pr[2];
+        CHECK(MPI_Recv_init(r3[0] + base, COUNT, t[k], peer, 70, MPI_COMM_WORLD, &pr[0]) == MPI_SUCCESS);
+        CHECK(MPI_Send_init(d + base, COUNT, t[k], peer, 70, MPI_COMM_WORLD, &pr[1]) == MPI_SUCCESS);
+        for (int round = 0; round < 3; ++round) {
+          for (long i = 0; i < span; ++i) h[i] = pat(i, k + 7 * round + 1);
+          cudaMemcpy(d, h, span, cudaMemcpyHostToDevice);
+          cudaMemset(r3[0], 0xCD, span); cudaDeviceSynchronize();
+          MPI_Barrier(MPI_COMM_WORLD);
+          CHECK(MPI_Startall(2, pr) == MPI_SUCCESS);
+          MPI_Status ps[2];
+          CHECK(MPI_Waitall(2, pr, ps) == MPI_SUCCESS);
+          CHECK(pr[0] != MPI_REQUEST_NULL && pr[1] != MPI_REQUEST_NULL); /* inactive, not freed */
+          /* expected: the host unpack of this round's pattern */
+          int q = 0;
+          unsigned char *hp2 = malloc(P), *exp2 = malloc(span);
+          CHECK(MPI_Pack(h + base, COUNT, t[k], hp2, P, &q, MPI_COMM_WORLD) == MPI_SUCCESS);
+          memset(exp2, 0xCD, span);
+          q = 0;
+          CHECK(MPI_Unpack(hp2, P, &q, exp2 + base, COUNT, t[k], MPI_COMM_WORLD) == MPI_SUCCESS);
+          cudaMemcpy(back, r3[0], span, cudaMemcpyDeviceToHost);
+          CHECK(memcmp(back, exp2, span) == 0);
+          free(hp2);
+          free(exp2);
+        }
+        int f2 = 0;
+        CHECK(MPI_Test(&pr[0], &f2, MPI_STATUS_IGNORE) == MPI_SUCCESS && f2); /* inactive: complete */
+        CHECK(MPI_Request_free(&pr[0]) == MPI_SUCCESS && pr[0] == MPI_REQUEST_NULL);
+        CHECK(MPI_Request_free(&pr[1]) == MPI_SUCCESS && pr[1] == MPI_REQUEST_NULL);
+        for (long i = 0; i < span; ++i) h[i] = pat(i, k); /* restore the source */
+        cudaMemcpy(d, h, span, cudaMemcpyHostToDevice);
         for (int i = 0; i < 3; ++i) cudaFree(r3[i]);
       }
     }

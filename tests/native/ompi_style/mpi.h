@@ -76,6 +76,10 @@ int MPI_Waitsome(int, MPI_Request[], int *, int[], MPI_Status[]);
 int MPI_Testany(int, MPI_Request[], int *, int *, MPI_Status *);
 int MPI_Testall(int, MPI_Request[], int *, MPI_Status[]);
 int MPI_Request_free(MPI_Request *);
+int MPI_Send_init(const void *, int, MPI_Datatype, int, int, MPI_Comm, MPI_Request *);
+int MPI_Recv_init(void *, int, MPI_Datatype, int, int, MPI_Comm, MPI_Request *);
+int MPI_Start(MPI_Request *);
+int MPI_Startall(int, MPI_Request[]);
 int MPI_Sendrecv(const void *, int, MPI_Datatype, int, int, void *, int, MPI_Datatype, int, int, MPI_Comm,
                  MPI_Status *);
 int MPI_Dist_graph_create_adjacent(MPI_Comm, int, const int[], const int[], int, const int[], const int[], MPI_Info,

@@ -35,6 +35,7 @@ INTERCEPTED = {
     "MPI_Type_commit", "MPI_Type_free", "MPI_Pack", "MPI_Unpack",
     "MPI_Send", "MPI_Recv", "MPI_Isend", "MPI_Irecv", "MPI_Wait", "MPI_Waitall", "MPI_Test", "MPI_Sendrecv",
     "MPI_Waitany", "MPI_Waitsome", "MPI_Testany", "MPI_Testall", "MPI_Request_free",
+    "MPI_Send_init", "MPI_Recv_init", "MPI_Start", "MPI_Startall",
     "MPI_Dist_graph_create_adjacent", "MPI_Cart_create", "MPI_Comm_free",
     "MPI_Neighbor_alltoallv", "MPI_Neighbor_alltoallw", "MPI_Alltoallv", "MPI_Alltoallw",
 }
