@@ -144,6 +144,20 @@ int main() {
       sp_rt_neighbor_alltoallw(a, one, zero, hs, 26, nb, a, one, zero, rtyp, 26, nb);
     };
     std::printf("halo alltoallw (1 rank)    %8.2f us\n", med_us(call, 500));
+    // the distributed plan's DIRECT exchange, enqueue only (a time loop's
+    // host cost per iteration), against enqueueing the same 26 typed copies
+    {
+      sp_halo_plan plan = nullptr;
+      CK(sp_halo_plan_create(&hc, a, SP_HALO_DIRECT, &plan));
+      void *rs = nullptr;
+      CK(sp_rt_stream(&rs));
+      std::printf("halo plan exchange enqueue %8.2f us\n",
+                  med_us([&] { sp_halo_plan_exchange(plan, nullptr); }, 300));
+      cudaStreamSynchronize(static_cast<cudaStream_t>(rs));
+      std::printf("halo copy batch enqueue    %8.2f us\n", med_us([&] { sp_batch_execute(b, s); }, 300));
+      cudaStreamSynchronize(s);
+      sp_halo_plan_free(plan);
+    }
     // the same two with a cold L2 (a 512 MiB memset before each call, waited
     // for and not timed), as bench.py measures them; and the kernel alone
     // by events, so host cost = wall - kernel
