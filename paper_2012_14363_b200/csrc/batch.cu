@@ -612,6 +612,17 @@ __global__ void k_flag_store(const FlagStore f) {
   if (threadIdx.x < static_cast<unsigned>(f.n)) st_release_sys(f.p[threadIdx.x], f.v);
 }
 
+// one warp: publish the pre flags, then wait for the wait flags -- the
+// prologue of a device-numbered launch when ranks share a GPU (stream memory
+// operations carry fixed values, and a full-wave grid spinning here could
+// starve the peer kernel it waits for; one warp cannot)
+__global__ void k_flag_pre_wait(const BatchSig sig) {
+  if (threadIdx.x < static_cast<unsigned>(sig.n_pre))
+    st_release_sys(sig.pre[threadIdx.x], sig_value(sig, sig.pre_value, sig.pre_add, sig.pre_shift));
+  if (threadIdx.x < static_cast<unsigned>(sig.n_wait))
+    wait_flag(sig.wait[threadIdx.x], sig_value(sig, sig.wait_value, sig.wait_add, sig.wait_shift), sig, 256);
+}
+
 // Stream memory operations (one cuStreamBatchMemOp): write `value` to each
 // `writes` flag (ordered after all earlier work on the stream, with the
 // write's memory barrier), then block the stream until each `waits` flag
@@ -661,8 +672,6 @@ void batch_launch(const Batch &b, void *stream, const BatchSignal *bs) {
     if (bs) {
       sig.timeout_ns = bs->timeout_ns;
       sig.err = bs->err;
-      if (bs->iter && bs->stream_waits)
-        fail(SP_ERR_UNSUPPORTED, "device iteration numbers need in-kernel flag waits");
       sig.iter = reinterpret_cast<const unsigned long long *>(bs->iter);
       sig.pre_add = bs->pre_add;
       sig.wait_add = bs->wait_add;
@@ -679,7 +688,23 @@ void batch_launch(const Batch &b, void *stream, const BatchSignal *bs) {
       if (bs->wait.size() > static_cast<size_t>(kMaxSig) || bs->signal.size() > static_cast<size_t>(kMaxSig) ||
           bs->pre.size() > static_cast<size_t>(kMaxSig))
         fail(SP_ERR_UNSUPPORTED, "batch signalling: more than 32 peers");
-      if (gi == 0 && !bs->stream_waits) { // every rank on its own GPU: all in the kernel
+      if (gi == 0 && bs->stream_waits && bs->iter) {
+        // device-numbered iterations with ranks sharing a GPU: a one-warp
+        // kernel publishes and waits ahead of the batch
+        BatchSig w = sig;
+        w.n_pre = static_cast<int>(bs->pre.size());
+        for (int i = 0; i < w.n_pre; ++i) w.pre[i] = reinterpret_cast<unsigned long long *>(bs->pre[i]);
+        w.pre_value = bs->pre_value;
+        w.n_wait = static_cast<int>(bs->wait.size());
+        for (int i = 0; i < w.n_wait; ++i) w.wait[i] = reinterpret_cast<const unsigned long long *>(bs->wait[i]);
+        w.wait_value = bs->wait_value;
+        w.iter_store = nullptr;
+        if (w.n_pre || w.n_wait) {
+          k_flag_pre_wait<<<1, 32, 0, s>>>(w);
+          cuda_check(cudaGetLastError(), "k_flag_pre_wait launch");
+          g_launches.fetch_add(1, std::memory_order_relaxed);
+        }
+      } else if (gi == 0 && !bs->stream_waits) { // every rank on its own GPU: all in the kernel
         if (bs->pre.size() > static_cast<size_t>(kMaxSig)) fail(SP_ERR_UNSUPPORTED, "batch signalling: more than 32 peers");
         sig.n_pre = static_cast<int>(bs->pre.size());
         for (int i = 0; i < sig.n_pre; ++i) sig.pre[i] = reinterpret_cast<unsigned long long *>(bs->pre[i]);
@@ -701,7 +726,7 @@ void batch_launch(const Batch &b, void *stream, const BatchSignal *bs) {
           stream_flag_ops(s, bs->pre, bs->pre_value, bs->wait, bs->wait_value);
         }
       }
-      if (gi == 0) {
+      if (gi == 0 && !(bs->stream_waits && bs->iter)) { // (else waited for by k_flag_pre_wait)
         sig.n_wait = static_cast<int>(bs->wait.size());
         for (int i = 0; i < sig.n_wait; ++i) sig.wait[i] = reinterpret_cast<const unsigned long long *>(bs->wait[i]);
         sig.wait_value = bs->wait_value;

@@ -428,10 +428,11 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
     // A launch captured into a CUDA graph is replayed with its parameters
     // frozen, so a captured exchange numbers its iterations on the device
     // instead: a one-thread tick kernel advances the plan's counter and the
-    // copy kernels derive FREE/READY from it. That needs the flag waits in
-    // the kernels (every rank on its own GPU, or TEMPI_FLAG_WAIT=kernel);
-    // stream memory operations carry fixed values. A plan with no peer (a
-    // 1x1x1 grid: no flags at all) captures in either mode.
+    // copy kernels derive FREE/READY from it. With every rank on its own GPU
+    // the waits are in the copy kernels as usual; with ranks sharing a GPU
+    // (whose stream memory operations carry fixed values) a one-warp kernel
+    // publishes and waits ahead of each launch instead. A plan with no peer
+    // (a 1x1x1 grid) has no flags at all.
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cuda_check(cudaStreamIsCapturing(s, &cap), "cudaStreamIsCapturing");
     const bool capturing = cap != cudaStreamCaptureStatusNone;
@@ -440,9 +441,6 @@ sp_status sp_halo_plan_exchange(sp_halo_plan p, double times[4]) {
       if (p->method != SP_HALO_DIRECT && p->method != SP_HALO_FUSED_ASYNC)
         fail(SP_ERR_UNSUPPORTED, "halo exchange capture: only the device-ordered methods (DIRECT, FUSED_ASYNC)");
       if (times) fail(SP_ERR_INVALID_ARGUMENT, "halo exchange capture: a captured exchange only enqueues (times == NULL)");
-      if (peers && rt_flag_waits_in_stream())
-        fail(SP_ERR_UNSUPPORTED, "halo exchange capture: needs in-kernel flag waits (each rank on its own GPU, "
-                                 "or TEMPI_FLAG_WAIT=kernel); stream memory operations carry fixed values");
       p->graph_mode = true;
     }
     // one iteration's protocol values: host-numbered (recorded on the

@@ -941,12 +941,12 @@ def _halo(rank, world, job, ranks, method):
 
 
 def _halo_graph(rank, world, job, ranks, method, flag_wait):
-    """a distributed exchange captured into a CUDA graph: with in-kernel flag
-    waits the plan numbers its iterations on the device (a tick kernel
-    advances its counter, the copy kernels derive FREE/READY from it), so
-    replays order the ranks like eager calls; host-numbered iterations
-    before the capture and eager ones after it continue the same count.
-    With stream flag waits (fixed values) the capture is refused."""
+    """a distributed exchange captured into a CUDA graph: the plan numbers
+    its iterations on the device (a tick kernel advances its counter, the
+    copy kernels -- or, with ranks sharing a GPU, a one-warp wait kernel
+    ahead of them -- derive FREE/READY from it), so replays order the ranks
+    like eager calls; host-numbered iterations before the capture and eager
+    ones after it continue the same count."""
     import os
     os.environ["TEMPI_FLAG_WAIT"] = flag_wait
     import torch
@@ -1015,9 +1015,11 @@ def test_distributed_halo_graph_capture(cuda, ranks, method):
 
 
 @pytest.mark.gpu
-def test_distributed_halo_graph_capture_refused_in_stream_mode(cuda):
-    res = _spawn(_halo_graph, 2, (2, 1, 1), 3, "stream", timeout=300)
-    assert all(v == (0, "refused") for v in res.values()), res
+@pytest.mark.parametrize("method", [3, 2])
+def test_distributed_halo_graph_capture_stream_mode(cuda, method):
+    """ranks sharing a GPU (stream flag waits, the default here)"""
+    res = _spawn(_halo_graph, 2, (2, 1, 1), method, "stream", timeout=300)
+    assert all(v == (0, "captured") for v in res.values()), res
 
 
 def _halo_peer_absent(rank, world, job):

@@ -236,8 +236,7 @@ def _halo_steady(torch, rt, H, cfg, alloc, rank, world, iters=200, per_graph=10)
     replayed from a CUDA graph holding `per_graph` exchanges (the plan then
     numbers its iterations on the device). Wall time per iteration over
     `iters` iterations, max over ranks; every ghost verified after a
-    replay. With ranks sharing a GPU (stream flag waits) a plan with peers
-    refuses the capture."""
+    replay."""
     import time
     import paper_2012_14363_b200 as sp
     import torch.distributed as dist
@@ -272,7 +271,7 @@ def _halo_steady(torch, rt, H, cfg, alloc, rank, world, iters=200, per_graph=10)
             finally:
                 g.capture_end()
         if refused:
-            row["graph"] = "refused (ranks share a GPU: stream flag waits)"
+            row["graph"] = "refused"
         else:
             with torch.cuda.stream(rs):
                 g.replay()
