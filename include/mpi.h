@@ -186,6 +186,20 @@ int MPI_Neighbor_alltoallw(const void *sendbuf, const int sendcounts[], const MP
                            const MPI_Datatype sendtypes[], void *recvbuf, const int recvcounts[],
                            const MPI_Aint rdispls[], const MPI_Datatype recvtypes[], MPI_Comm comm);
 
+/* persistent neighbourhood collectives (MPI-4.0 7.10.2): start with
+ * MPI_Start / MPI_Startall, complete with the MPI_Wait family, release with
+ * MPI_Request_free. Compiled once into one signalled typed-copy launch per
+ * start (no host entry protocol); the starts capture into CUDA graphs on
+ * sp_rt_stream. Types the engine cannot compile (irregular layouts) re-run
+ * the collective at every start. */
+int MPI_Neighbor_alltoallw_init(const void *sendbuf, const int sendcounts[], const MPI_Aint sdispls[],
+                                const MPI_Datatype sendtypes[], void *recvbuf, const int recvcounts[],
+                                const MPI_Aint rdispls[], const MPI_Datatype recvtypes[], MPI_Comm comm,
+                                MPI_Info info, MPI_Request *request);
+int MPI_Neighbor_alltoallv_init(const void *sendbuf, const int sendcounts[], const int sdispls[],
+                                MPI_Datatype sendtype, void *recvbuf, const int recvcounts[], const int rdispls[],
+                                MPI_Datatype recvtype, MPI_Comm comm, MPI_Info info, MPI_Request *request);
+
 /* all-to-all with derived datatypes (beyond the paper, whose future work
  * lists collectives): the neighbour machinery over the
  * complete graph of the communicator -- one typed-copy launch per rank

@@ -485,6 +485,24 @@ sp_status sp_rt_neighbor_alltoallw(const void *sendbuf,
                                    const sp_type *recvtypes, int64_t indegree,
                                    const int *sources);
 
+/* persistent neighbour alltoallw (MPI-4.0 MPI_Neighbor_alltoallw_init;
+ * collective): the typed-copy batch is built once against the receivers'
+ * layouts, each start is ONE launch carrying the halo plans' device
+ * protocol (no host entry protocol), and starts capture into CUDA graphs.
+ * Strided types only (SP_ERR_UNSUPPORTED otherwise, on every rank). The
+ * buffers stay bound to the plan. start enqueues on sp_rt_stream; test /
+ * wait complete a start (this rank's sends done, its receives landed). */
+typedef struct sp_nbr_plan_s *sp_nbr_plan;
+sp_status sp_rt_neighbor_alltoallw_init(const void *sendbuf, const int64_t *sendcounts, const int64_t *sdispls,
+                                        const sp_type *sendtypes, int64_t outdegree, const int *dests,
+                                        void *recvbuf, const int64_t *recvcounts, const int64_t *rdispls,
+                                        const sp_type *recvtypes, int64_t indegree, const int *sources,
+                                        sp_nbr_plan *out);
+sp_status sp_nbr_plan_start(sp_nbr_plan p);
+sp_status sp_nbr_plan_test(sp_nbr_plan p, int *done);
+sp_status sp_nbr_plan_wait(sp_nbr_plan p);
+sp_status sp_nbr_plan_free(sp_nbr_plan p);
+
 /* distributed halo exchange: one rank per process (grid size == runtime
  * size); `alloc` is this rank's padded allocation on its device. */
 typedef struct sp_halo_plan_s *sp_halo_plan;

@@ -290,6 +290,63 @@ sp_status sp_rt_neighbor_alltoallw(const void *sendbuf, const int64_t *sendcount
   });
 }
 
+struct sp_nbr_plan_s {
+  NbrPlan *p = nullptr;
+  ~sp_nbr_plan_s() { rt_nbr_plan_free(p); }
+};
+
+sp_status sp_rt_neighbor_alltoallw_init(const void *sendbuf, const int64_t *sendcounts, const int64_t *sdispls,
+                                        const sp_type *sendtypes, int64_t outdegree, const int *dests,
+                                        void *recvbuf, const int64_t *recvcounts, const int64_t *rdispls,
+                                        const sp_type *recvtypes, int64_t indegree, const int *sources,
+                                        sp_nbr_plan *out) {
+  SPB_TRACE("sp_rt_neighbor_alltoallw_init");
+  return guarded([&] {
+    need(out);
+    if (outdegree < 0 || indegree < 0) fail(SP_ERR_INVALID_ARGUMENT, "negative degree");
+    if ((outdegree && (!sendcounts || !sdispls || !sendtypes || !dests)) ||
+        (indegree && (!recvcounts || !rdispls || !recvtypes || !sources)))
+      fail(SP_ERR_INVALID_ARGUMENT, "null edge arrays");
+    std::vector<int64_t> sc(sendcounts, sendcounts + outdegree), sd(sdispls, sdispls + outdegree);
+    std::vector<int64_t> rc(recvcounts, recvcounts + indegree), rd(rdispls, rdispls + indegree);
+    std::vector<CommitPtr> st, rtp;
+    for (int64_t i = 0; i < outdegree; ++i) st.push_back(committed_of(sendtypes[i]));
+    for (int64_t j = 0; j < indegree; ++j) rtp.push_back(committed_of(recvtypes[j]));
+    std::vector<int> ds(dests, dests + outdegree), ss(sources, sources + indegree);
+    auto h = std::make_unique<sp_nbr_plan_s>();
+    h->p = rt_nbr_plan_create(static_cast<const uint8_t *>(sendbuf), sc, sd, st, static_cast<uint8_t *>(recvbuf), rc,
+                              rd, rtp, ss, ds);
+    *out = h.release();
+  });
+}
+
+sp_status sp_nbr_plan_start(sp_nbr_plan p) {
+  return guarded([&] {
+    need(p);
+    rt_nbr_plan_start(p->p);
+  });
+}
+
+sp_status sp_nbr_plan_test(sp_nbr_plan p, int *done) {
+  return guarded([&] {
+    need(p);
+    need(done);
+    *done = rt_nbr_plan_test(p->p) ? 1 : 0;
+  });
+}
+
+sp_status sp_nbr_plan_wait(sp_nbr_plan p) {
+  return guarded([&] {
+    need(p);
+    rt_nbr_plan_wait(p->p);
+  });
+}
+
+sp_status sp_nbr_plan_free(sp_nbr_plan p) {
+  delete p;
+  return SP_OK;
+}
+
 sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int method, sp_halo_plan *out) {
   return guarded([&] {
     need(cfgp);

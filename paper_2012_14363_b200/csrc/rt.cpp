@@ -357,6 +357,13 @@ uint8_t *open_ipc(const cudaIpcMemHandle_t &h, int peer) {
 
 // a halo plan holds the peer mappings rt_exchange_ptr gave it for its
 // lifetime (pin = +1 at creation, -1 when the plan is freed)
+// hold (delta > 0) or release a mapping by its handle (persistent plans)
+void ipc_pin_handle(const cudaIpcMemHandle_t &h, int delta) {
+  if (!g_rt) return;
+  auto e = g_rt->ipc_cache.find(std::string(reinterpret_cast<const char *>(&h), sizeof(h)));
+  if (e != g_rt->ipc_cache.end()) e->second.pins = std::max(0, e->second.pins + delta);
+}
+
 // marks the start of a call whose mappings must survive stale-mapping eviction
 void ipc_call_begin() {
   if (g_rt) g_rt->ipc_call_mark = g_rt->ipc_clock;
@@ -648,6 +655,9 @@ void rt_exchange_ptr(void *local, std::vector<uint8_t *> &out) {
   Runtime &R = rt();
   ipc_call_begin();
   Slot &me = R.shm->slots[R.rank];
+  // the publication area is the one a neighbour collective's receive layout
+  // uses: the next collective must publish its layout again
+  R.nbr_layout.clear();
   if (local) {
     ipc_handle_of(local, &me.xh, &me.xoff);
     me.xbytes = 1;
@@ -1865,6 +1875,214 @@ void rt_neighbor_alltoallw(const uint8_t *sendbuf, const std::vector<int64_t> &s
     g_wlast = WLastCall{std::move(args), send_types, recv_types,
                         R.shm->slots[R.rank].layout_ver.load(std::memory_order_relaxed), true};
   });
+}
+
+// ---- persistent neighbour alltoallw (MPI-4 MPI_Neighbor_alltoallw_init)
+// The call's typed-copy batch is built once, against the receivers'
+// layouts published at creation, and every start is one signalled launch
+// with the halo plans' device protocol instead of the host entry protocol:
+// block 0 tells this rank's senders that the receive buffer is free for
+// iteration n (FREE = n-1), every block waits for FREE = n-1 from its
+// receivers, stores its blocks, adds its share of READY = n, and block 0
+// waits for READY = n from its senders -- so the launch completes when
+// this rank's receives have landed. Starts are numbered on the host, or on
+// the device once captured into a CUDA graph (like the halo plans).
+namespace {
+constexpr int kPlanReady = 0, kPlanFree = 1;
+bool all_ranks_ok(bool ok) { // every rank learns whether every rank succeeded
+  Runtime &R = rt();
+  constexpr int kTag = 0x7e5a;
+  int32_t v = ok ? 1 : 0;
+  if (R.rank == 0) {
+    for (int r = 1; r < R.size; ++r) {
+      int32_t o = 0;
+      rt_host_recv(r, kTag, &o, sizeof(o));
+      v &= o;
+    }
+    for (int r = 1; r < R.size; ++r) rt_host_send(r, kTag + 1, &v, sizeof(v));
+  } else {
+    rt_host_send(0, kTag, &v, sizeof(v));
+    rt_host_recv(0, kTag + 1, &v, sizeof(v));
+  }
+  return v != 0;
+}
+} // namespace
+
+struct NbrPlan {
+  Batch *batch = nullptr;
+  std::vector<std::unique_ptr<Committed>> dst_types; // the receivers' geometries
+  std::vector<CommitPtr> keep;
+  std::vector<cudaIpcMemHandle_t> pinned;            // peers' receive buffers
+  uint64_t *flags = nullptr;                         // [READY n][FREE n]
+  std::vector<uint8_t *> peer_flags;
+  std::vector<int> out_peers, in_peers;
+  uint64_t iter = 0, *dev_iter = nullptr;
+  bool graph_mode = false;
+  cudaEvent_t done = nullptr;
+  ~NbrPlan() {
+    for (const auto &h : pinned) ipc_pin_handle(h, -1);
+    rt_pin_ptrs(peer_flags, -1);
+    batch_destroy(batch);
+    if (flags) cudaFree(flags);
+    if (dev_iter) cudaFree(dev_iter);
+    if (done) cudaEventDestroy(done);
+  }
+};
+
+NbrPlan *rt_nbr_plan_create(const uint8_t *sendbuf, const std::vector<int64_t> &send_counts,
+                            const std::vector<int64_t> &send_displs, const std::vector<CommitPtr> &send_types,
+                            uint8_t *recvbuf, const std::vector<int64_t> &recv_counts,
+                            const std::vector<int64_t> &recv_displs, const std::vector<CommitPtr> &recv_types,
+                            const std::vector<int> &sources, const std::vector<int> &dests) {
+  Runtime &R = rt();
+  ipc_call_begin();
+  auto p = std::make_unique<NbrPlan>();
+  // local checks first, agreed by every rank before anything is published
+  std::string why;
+  std::vector<Desc> descs(sources.size(), Desc{});
+  std::vector<const Desc *> dp(sources.size(), nullptr);
+  std::vector<int64_t> bytes(sources.size());
+  for (size_t j = 0; j < sources.size() && why.empty(); ++j) {
+    const Committed &rt_ = *recv_types[j];
+    bytes[j] = recv_counts[j] * rt_.size;
+    if (bytes[j] > 0 && !describable(rt_)) why = "receive types need a strided non-overlapping layout";
+    if (bytes[j] > 0 && why.empty()) {
+      desc_of(rt_, recv_counts[j], descs[j]);
+      dp[j] = &descs[j];
+    }
+  }
+  for (size_t i = 0; i < dests.size() && why.empty(); ++i)
+    if (send_counts[i] > 0 && send_types[i]->form != SP_FORM_STRIDED) why = "send types need a strided form";
+  if (sources.size() > static_cast<size_t>(kMaxWEdges) || dests.size() > static_cast<size_t>(kMaxWEdges))
+    why = "more than 64 edges";
+  { // the start launch carries the protocol: a rank with peers must send something
+    bool peer = false, sends = false;
+    for (int d : dests) peer |= d != R.rank;
+    for (int q : sources) peer |= q != R.rank;
+    for (size_t i = 0; i < dests.size(); ++i) sends |= send_counts[i] > 0 && send_types[i]->size > 0;
+    if (peer && !sends && why.empty()) why = "a rank with neighbours but nothing to send";
+  }
+  if (!all_ranks_ok(why.empty()))
+    fail(SP_ERR_UNSUPPORTED, "persistent neighbour alltoallw: " + (why.empty() ? std::string("another rank's types") : why));
+  nbr_publish(recvbuf, sources, recv_displs, bytes, &dp);
+  rt_barrier(); // every receive layout published
+  std::vector<CopySpec> jobs;
+  std::vector<int> seen(R.size, 0);
+  for (size_t i = 0; i < dests.size() && why.empty(); ++i) {
+    const int d = dests[i];
+    const int occ = seen[d]++;
+    const Slot &peer = R.shm->slots[d];
+    int hit = -1;
+    for (int j = 0, k = 0; j < peer.nedges; ++j)
+      if (peer.edges[j][0] == R.rank && k++ == occ) {
+        hit = j;
+        break;
+      }
+    const Committed &st = *send_types[i];
+    const int64_t b = send_counts[i] * st.size;
+    if (hit < 0) {
+      why = "a destination does not list this rank as a source";
+    } else if (b != peer.edges[hit][2]) {
+      why = "send and receive describe different byte counts";
+    } else if (b > 0) {
+      const Desc &wd = peer.wdesc[hit];
+      uint8_t *base = d == R.rank ? recvbuf : open_ipc(peer.xh, d) + peer.xoff;
+      if (d != R.rank) {
+        ipc_pin_handle(peer.xh, 1);
+        p->pinned.push_back(peer.xh);
+      }
+      auto dc = std::make_unique<Committed>();
+      committed_from(wd, *dc);
+      jobs.push_back({&st, sendbuf + send_displs[i], UINT64_MAX, send_counts[i], dc.get(),
+                      base + peer.edges[hit][1], UINT64_MAX, wd.count});
+      p->dst_types.push_back(std::move(dc));
+    }
+  }
+  rt_barrier(); // every layout read before a later call republishes
+  if (!all_ranks_ok(why.empty())) fail(SP_ERR_INVALID_ARGUMENT, "persistent neighbour alltoallw: " + why);
+  p->keep = send_types;
+  if (!jobs.empty()) p->batch = copy_batch_create(jobs);
+  const int n = R.size;
+  cuda_check(cudaMalloc(&p->flags, 2 * n * sizeof(uint64_t)), "cudaMalloc(plan flags)");
+  cuda_check(cudaMemset(p->flags, 0, 2 * n * sizeof(uint64_t)), "cudaMemset(plan flags)");
+  cuda_check(cudaMalloc(&p->dev_iter, sizeof(uint64_t)), "cudaMalloc(plan counter)");
+  cuda_check(cudaMemset(p->dev_iter, 0, sizeof(uint64_t)), "cudaMemset(plan counter)");
+  cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+  rt_exchange_ptr(p->flags, p->peer_flags);
+  rt_pin_ptrs(p->peer_flags, 1);
+  std::vector<char> so(n, 0), si(n, 0);
+  for (int d : dests)
+    if (d != R.rank && !so[d]) so[d] = 1, p->out_peers.push_back(d);
+  for (int s : sources)
+    if (s != R.rank && !si[s]) si[s] = 1, p->in_peers.push_back(s);
+  cuda_check(cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming), "cudaEventCreate");
+  return p.release();
+}
+
+void rt_nbr_plan_start(NbrPlan *p) {
+  Runtime &R = rt();
+  cudaStream_t s = R.stream;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cuda_check(cudaStreamIsCapturing(s, &cap), "cudaStreamIsCapturing");
+  const bool peers = !p->out_peers.empty() || !p->in_peers.empty();
+  if (cap != cudaStreamCaptureStatusNone) p->graph_mode = true;
+  if (!p->batch) return; // nothing to move and no peer
+  const int n = R.size, me = R.rank;
+  const uint64_t it = ++p->iter;
+  auto at = [&](uint8_t *base, int kind, int peer) {
+    return reinterpret_cast<uint64_t *>(base + static_cast<size_t>(kind * n + peer) * sizeof(uint64_t));
+  };
+  uint8_t *mine = reinterpret_cast<uint8_t *>(p->flags);
+  BatchSignal ks;
+  for (int q : p->in_peers) {
+    ks.pre.push_back(at(p->peer_flags[q], kPlanFree, me));
+    ks.post.push_back(at(mine, kPlanReady, q));
+  }
+  ks.pre_value = it - 1;
+  for (int q : p->out_peers) {
+    ks.wait.push_back(at(mine, kPlanFree, q));
+    ks.signal.push_back(at(p->peer_flags[q], kPlanReady, me));
+  }
+  ks.wait_value = it - 1;
+  ks.post_value = it << 32;
+  ks.sys_scope = R.nbr_remote;
+  ks.stream_waits = rt_flag_waits_in_stream();
+  ks.err = rt_device_err();
+  ks.timeout_ns = rt_device_timeout_ns();
+  if (p->graph_mode && peers) {
+    iter_tick(p->dev_iter, s);
+    ks.iter = p->dev_iter;
+    ks.pre_add = -1;
+    ks.wait_add = -1;
+    ks.post_shift = 32;
+  } else {
+    ks.iter_store = p->dev_iter;
+    ks.iter_value = it;
+  }
+  batch_execute_signaled(*p->batch, s, ks);
+  if (cap == cudaStreamCaptureStatusNone) cuda_check(cudaEventRecord(p->done, s), "cudaEventRecord");
+}
+
+bool rt_nbr_plan_test(NbrPlan *p) {
+  const cudaError_t e = cudaEventQuery(p->done);
+  if (e == cudaErrorNotReady) {
+    cudaGetLastError();
+    rt_progress();
+    return false;
+  }
+  cuda_check(e, "cudaEventQuery");
+  rt_check_device_error("persistent neighbour alltoallw");
+  return true;
+}
+
+void rt_nbr_plan_wait(NbrPlan *p) {
+  rt_sync_event(p->done, "persistent neighbour alltoallw");
+  rt_check_device_error("persistent neighbour alltoallw");
+}
+
+void rt_nbr_plan_free(NbrPlan *p) {
+  if (p && p->done) cudaEventSynchronize(p->done);
+  delete p;
 }
 
 // the send side of an alltoallw call once entered: find (or build) the

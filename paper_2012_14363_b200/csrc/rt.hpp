@@ -56,6 +56,18 @@ int rt_choose(const Committed &ct, int64_t count);
 // on `peer_device` (Eq. 4 vs the reference's best of Eqs. 1-3)
 bool model_prefers_direct(const Committed &ct, int64_t count, int peer_device);
 void *rt_stream();
+// persistent neighbour alltoallw (MPI-4 MPI_Neighbor_alltoallw_init):
+// built once (collective), started as one signalled launch per call
+struct NbrPlan;
+NbrPlan *rt_nbr_plan_create(const uint8_t *sendbuf, const std::vector<int64_t> &send_counts,
+                            const std::vector<int64_t> &send_displs, const std::vector<CommitPtr> &send_types,
+                            uint8_t *recvbuf, const std::vector<int64_t> &recv_counts,
+                            const std::vector<int64_t> &recv_displs, const std::vector<CommitPtr> &recv_types,
+                            const std::vector<int> &sources, const std::vector<int> &dests);
+void rt_nbr_plan_start(NbrPlan *p);
+bool rt_nbr_plan_test(NbrPlan *p);
+void rt_nbr_plan_wait(NbrPlan *p);
+void rt_nbr_plan_free(NbrPlan *p);
 void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &send_counts,
                            const std::vector<int64_t> &send_displs, const CommitPtr &stp, uint8_t *recvbuf,
                            const std::vector<int64_t> &recv_counts, const std::vector<int64_t> &recv_displs,

@@ -15,6 +15,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -54,6 +56,11 @@ struct State {
     int count = 0, peer = 0, tag = 0;
     MPI_Datatype dt = 0;
     MPI_Comm comm = 0;
+    // persistent neighbour collective (MPI-4 MPI_Neighbor_alltoallw_init):
+    // the engine's compiled plan, or -- types it cannot compile -- the call
+    // itself, re-run by every start
+    sp_nbr_plan plan = nullptr;
+    std::shared_ptr<std::function<sp_status()>> rerun;
   };
   std::unordered_map<int, Pending> requests;
   int next_request = 1;
@@ -570,6 +577,13 @@ static int progress(MPI_Request request, bool block, bool *done) {
     *done = true;
     return MPI_SUCCESS;
   }
+  if (!p.done && p.plan) { // a started persistent neighbour collective
+    int d = 1;
+    p.rc = block ? sp_nbr_plan_wait(p.plan) : sp_nbr_plan_test(p.plan, &d);
+    p.done = d || p.rc != SP_OK;
+    std::lock_guard<std::mutex> lk(S().mu);
+    S().requests[request] = p;
+  }
   if (!p.done) {
     int d = 1;
     p.rc = block ? sp_rt_wait(p.r, p.st) : sp_rt_test(p.r, &d, p.st);
@@ -670,6 +684,16 @@ int MPI_Start(MPI_Request *request) {
     auto it = S().requests.find(*request);
     if (it == S().requests.end() || !it->second.persistent || it->second.active) return MPI_ERR_ARG;
     p = it->second;
+  }
+  if (p.plan || p.rerun) { // a persistent neighbour collective
+    const sp_status rc = p.plan ? sp_nbr_plan_start(p.plan) : (*p.rerun)();
+    std::lock_guard<std::mutex> lk(S().mu);
+    State::Pending &e = S().requests[*request];
+    e.active = true;
+    e.done = !p.plan || rc != SP_OK; // the re-run call has completed already
+    e.rc = rc;
+    for (auto &v : e.st) v = 0;
+    return MPI_SUCCESS;
   }
   if (p.peer == MPI_PROC_NULL) return MPI_SUCCESS; // completes at once
   TYPE(p.dt, h);
@@ -797,8 +821,13 @@ int MPI_Request_free(MPI_Request *request) {
   if (*request == MPI_REQUEST_NULL) return MPI_ERR_ARG;
   const int rc = complete(request, nullptr, true, nullptr); // completes it, then the handle is released
   if (*request != MPI_REQUEST_NULL) { // persistent: released here
-    std::lock_guard<std::mutex> lk(S().mu);
-    S().requests.erase(*request);
+    sp_nbr_plan plan = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(S().mu);
+      plan = S().requests[*request].plan;
+      S().requests.erase(*request);
+    }
+    if (plan) sp_nbr_plan_free(plan);
     *request = MPI_REQUEST_NULL;
   }
   return rc;
@@ -1027,6 +1056,84 @@ int MPI_Neighbor_alltoallw(const void *sendbuf, const int sendcounts[], const MP
                            const MPI_Aint rdispls[], const MPI_Datatype recvtypes[], MPI_Comm comm) {
   return PMPI_Neighbor_alltoallw(sendbuf, sendcounts, sdispls, sendtypes, recvbuf, recvcounts, rdispls, recvtypes,
                                  comm);
+}
+
+// ---- persistent neighbour collectives (MPI-4.0 7.10.2): compiled once
+// into one signalled typed-copy launch per start, capturable into CUDA
+// graphs; types the engine cannot compile re-run the call at every start
+static int nbr_init(const void *sendbuf, const int sendcounts[], const std::vector<int64_t> &sdisp_b,
+                    const std::vector<MPI_Datatype> &stypes, void *recvbuf, const int recvcounts[],
+                    const std::vector<int64_t> &rdisp_b, const std::vector<MPI_Datatype> &rtypes, MPI_Comm comm,
+                    MPI_Request *request) {
+  const Comm *c = comm_of(comm);
+  if (!c || c->kind == 0) return MPI_ERR_COMM;
+  if (!request) return MPI_ERR_ARG;
+  std::vector<int> src, dst;
+  std::vector<int64_t> scount, sdisp, rcount, rdisp;
+  std::vector<sp_type> st, rt;
+  for (size_t i = 0; i < c->dests.size(); ++i)
+    if (c->dests[i] != MPI_PROC_NULL) {
+      TYPE(stypes[i], h);
+      dst.push_back(c->dests[i]);
+      scount.push_back(sendcounts[i]);
+      sdisp.push_back(sdisp_b[i]);
+      st.push_back(h);
+    }
+  for (size_t j = 0; j < c->sources.size(); ++j)
+    if (c->sources[j] != MPI_PROC_NULL) {
+      TYPE(rtypes[j], h);
+      src.push_back(c->sources[j]);
+      rcount.push_back(recvcounts[j]);
+      rdisp.push_back(rdisp_b[j]);
+      rt.push_back(h);
+    }
+  sp_nbr_plan plan = nullptr;
+  const sp_status rc = sp_rt_neighbor_alltoallw_init(sendbuf, scount.data(), sdisp.data(), st.data(),
+                                                     static_cast<int64_t>(dst.size()), dst.data(), recvbuf,
+                                                     rcount.data(), rdisp.data(), rt.data(),
+                                                     static_cast<int64_t>(src.size()), src.data(), &plan);
+  if (rc != SP_OK && rc != SP_ERR_UNSUPPORTED) TRY(rc);
+  std::lock_guard<std::mutex> lk(S().mu);
+  const int id = S().next_request++;
+  State::Pending &e = S().requests[id];
+  e.persistent = true;
+  e.plan = plan;
+  if (!plan) // every rank agreed the types cannot be compiled: re-run the call
+    e.rerun = std::make_shared<std::function<sp_status()>>([=] {
+      return sp_rt_neighbor_alltoallw(sendbuf, scount.data(), sdisp.data(), st.data(),
+                                      static_cast<int64_t>(dst.size()), dst.data(), recvbuf, rcount.data(),
+                                      rdisp.data(), rt.data(), static_cast<int64_t>(src.size()), src.data());
+    });
+  *request = id;
+  return MPI_SUCCESS;
+}
+
+int MPI_Neighbor_alltoallw_init(const void *sendbuf, const int sendcounts[], const MPI_Aint sdispls[],
+                                const MPI_Datatype sendtypes[], void *recvbuf, const int recvcounts[],
+                                const MPI_Aint rdispls[], const MPI_Datatype recvtypes[], MPI_Comm comm, MPI_Info,
+                                MPI_Request *request) {
+  const Comm *c = comm_of(comm);
+  if (!c || c->kind == 0) return MPI_ERR_COMM;
+  std::vector<int64_t> sd(sdispls, sdispls + c->dests.size()), rd(rdispls, rdispls + c->sources.size());
+  std::vector<MPI_Datatype> st(sendtypes, sendtypes + c->dests.size()), rt(recvtypes, recvtypes + c->sources.size());
+  return nbr_init(sendbuf, sendcounts, sd, st, recvbuf, recvcounts, rd, rt, comm, request);
+}
+
+int MPI_Neighbor_alltoallv_init(const void *sendbuf, const int sendcounts[], const int sdispls[],
+                                MPI_Datatype sendtype, void *recvbuf, const int recvcounts[], const int rdispls[],
+                                MPI_Datatype recvtype, MPI_Comm comm, MPI_Info, MPI_Request *request) {
+  const Comm *c = comm_of(comm);
+  if (!c || c->kind == 0) return MPI_ERR_COMM;
+  TYPE(sendtype, hs);
+  TYPE(recvtype, hr);
+  int64_t se = 0, re = 0;
+  TRY(sp_type_extent(hs, &se));
+  TRY(sp_type_extent(hr, &re));
+  std::vector<int64_t> sd, rd;
+  for (size_t i = 0; i < c->dests.size(); ++i) sd.push_back(static_cast<int64_t>(sdispls[i]) * se);
+  for (size_t j = 0; j < c->sources.size(); ++j) rd.push_back(static_cast<int64_t>(rdispls[j]) * re);
+  return nbr_init(sendbuf, sendcounts, sd, std::vector<MPI_Datatype>(c->dests.size(), sendtype), recvbuf, recvcounts,
+                  rd, std::vector<MPI_Datatype>(c->sources.size(), recvtype), comm, request);
 }
 
 // ============================================================ all-to-all

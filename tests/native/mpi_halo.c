@@ -6,7 +6,9 @@
  * With MODE = 1 the exchange is ONE MPI_Neighbor_alltoallw call on the
  * padded allocation itself: send types = the interior regions, receive
  * types = the ghost regions, byte displacements 0 (ghost writes, no packed
- * buffers).
+ * buffers). MODE = 2 is the same exchange as an MPI-4 persistent
+ * collective: MPI_Neighbor_alltoallw_init once, then MPI_Start + MPI_Wait
+ * per iteration (the ghosts reset before the last one).
  * usage: mpi_halo RX RY RZ N RADIUS ELEM ITERS [MODE]  (RX*RY*RZ == ranks)
  * prints per-phase wall times of the last iteration and "OK". */
 #include <stdio.h>
@@ -78,6 +80,30 @@ int main(int argc, char **argv) {
   CHECK(sp_halo_fill(&cfg, rank, alloc, NULL) == SP_OK);
   cudaDeviceSynchronize();
   double tp = 0, tx = 0, tu = 0;
+  if (mode == 2) {
+    int ones[26];
+    MPI_Aint zeros[26];
+    MPI_Datatype rtypes[26];
+    for (int i = 0; i < 26; ++i) {
+      ones[i] = 1;
+      zeros[i] = 0;
+      rtypes[i] = recv_t[25 - i];
+    }
+    MPI_Request req;
+    CHECK(MPI_Neighbor_alltoallw_init(alloc, ones, zeros, send_t, alloc, ones, zeros, rtypes, g, MPI_INFO_NULL, &req) ==
+          MPI_SUCCESS);
+    for (int it = 0; it < iters; ++it) {
+      if (it + 1 == iters) CHECK(sp_halo_fill(&cfg, rank, alloc, NULL) == SP_OK && cudaDeviceSynchronize() == cudaSuccess);
+      MPI_Barrier(MPI_COMM_WORLD);
+      const double t0 = MPI_Wtime();
+      CHECK(MPI_Start(&req) == MPI_SUCCESS);
+      CHECK(MPI_Wait(&req, MPI_STATUS_IGNORE) == MPI_SUCCESS);
+      tx = MPI_Wtime() - t0;
+      CHECK(req != MPI_REQUEST_NULL); /* inactive, reusable */
+    }
+    CHECK(MPI_Request_free(&req) == MPI_SUCCESS && req == MPI_REQUEST_NULL);
+    iters = 0;
+  }
   if (mode == 1) {
     /* edge i brings the neighbour's region i into my ghost region 25-i */
     int ones[26];
