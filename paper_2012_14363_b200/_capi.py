@@ -172,6 +172,12 @@ _sig("sp_rt_neighbor_alltoallv", C.c_int, vp, i64p, i64p, i64, C.POINTER(C.c_int
      C.POINTER(C.c_int), sp_type)
 _sig("sp_rt_neighbor_alltoallw", C.c_int, vp, i64p, i64p, C.POINTER(sp_type), i64, C.POINTER(C.c_int), vp, i64p,
      i64p, C.POINTER(sp_type), i64, C.POINTER(C.c_int))
+_sig("sp_rt_neighbor_alltoallw_init", C.c_int, vp, i64p, i64p, C.POINTER(sp_type), i64, C.POINTER(C.c_int), vp,
+     i64p, i64p, C.POINTER(sp_type), i64, C.POINTER(C.c_int), C.POINTER(vp))
+_sig("sp_nbr_plan_start", C.c_int, vp)
+_sig("sp_nbr_plan_test", C.c_int, vp, C.POINTER(C.c_int))
+_sig("sp_nbr_plan_wait", C.c_int, vp)
+_sig("sp_nbr_plan_free", C.c_int, vp)
 _sig("sp_halo_plan_create", C.c_int, C.POINTER(HaloConfig), vp, C.c_int, C.POINTER(vp))
 _sig("sp_halo_plan_exchange", C.c_int, vp, dblp)
 _sig("sp_halo_plan_free", C.c_int, vp)

@@ -165,6 +165,45 @@ class NeighborW:
                                             self.rt, self.ni, self.src))
 
 
+class NeighborPlan:
+    """MPI_Neighbor_alltoallw_init (MPI-4, collective): the exchange of a
+    NeighborW argument set compiled once for fixed buffers. start() enqueues
+    one signalled launch on the runtime stream (capturable into a CUDA
+    graph); wait() completes it."""
+
+    def __init__(self, sends, recvs, sendbuf, recvbuf):
+        w = NeighborW(sends, recvs)
+        self._w = w
+        sa = sendbuf if isinstance(sendbuf, int) else sendbuf.data_ptr()
+        ra = recvbuf if isinstance(recvbuf, int) else recvbuf.data_ptr()
+        h = C.c_void_p()
+        _check(lib.sp_rt_neighbor_alltoallw_init(sa, w.sc, w.sd, w.st, w.no, w.dst, ra, w.rc, w.rd, w.rt, w.ni, w.src,
+                                                 C.byref(h)))
+        self.handle = h.value
+
+    def start(self):
+        _check(lib.sp_nbr_plan_start(self.handle))
+
+    def test(self) -> bool:
+        d = C.c_int()
+        _check(lib.sp_nbr_plan_test(self.handle, C.byref(d)))
+        return bool(d.value)
+
+    def wait(self):
+        _check(lib.sp_nbr_plan_wait(self.handle))
+
+    def free(self):
+        if self.handle:
+            lib.sp_nbr_plan_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 def neighbor_alltoallv(sendbuf, sendtype, sends, recvbuf, recvtype, recvs):
     """MPI_Neighbor_alltoallv (collective): sends = [(dest, count,
     displacement in sendtype extents)], recvs = [(source, count,

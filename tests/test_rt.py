@@ -1022,6 +1022,61 @@ def test_distributed_halo_graph_capture_stream_mode(cuda, method):
     assert all(v == (0, "captured") for v in res.values()), res
 
 
+def _nbr_plan_graph(rank, world, job, ranks, flag_wait):
+    """MPI-4 persistent neighbour alltoallw (rt.NeighborPlan): the halo's 26
+    region types compiled once, started eagerly, then captured into a CUDA
+    graph and replayed; every ghost verified after each round"""
+    import os
+    os.environ["TEMPI_FLAG_WAIT"] = flag_wait
+    import torch
+    import paper_2012_14363_b200.halo as H
+    import paper_2012_14363_b200.rt as rt
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=1 << 20, host_bytes=1 << 20)
+    cfg = H.HaloConfig(ranks, (10, 12, 8), 2, 8)
+    regions = H.build_halo_types(cfg)
+    alloc = torch.empty(14 * 16 * 12 * 8, dtype=torch.uint8, device="cuda")
+    sends = [(H.neighbor(cfg, rank, r.dir), 1, r.send, 0) for r in regions]
+    recvs = [(H.neighbor(cfg, rank, tuple(-x for x in r.dir)), 1, regions[25 - j].recv, 0)
+             for j, r in enumerate(regions)]
+    plan = rt.NeighborPlan(sends, recvs, alloc, alloc)
+    rs = torch.cuda.ExternalStream(rt.stream())
+    bad = 0
+    for _ in range(3):  # eager starts
+        H.fill(cfg, rank, alloc)
+        torch.cuda.synchronize()
+        rt.barrier()
+        plan.start()
+        plan.wait()
+        bad += H.verify(cfg, rank, alloc)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(rs):
+        g.capture_begin()
+        plan.start()
+        g.capture_end()
+    for _ in range(3):  # replays
+        H.fill(cfg, rank, alloc)
+        torch.cuda.synchronize()
+        rt.barrier()
+        with torch.cuda.stream(rs):
+            g.replay()
+        rs.synchronize()
+        bad += H.verify(cfg, rank, alloc)
+    del g
+    plan.free()
+    rt.finalize()
+    return bad
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ranks,flag_wait", [((1, 1, 1), "stream"), ((2, 1, 1), "stream"), ((2, 2, 1), "stream"),
+                                             ((2, 1, 1), "kernel")])
+def test_persistent_neighbor_plan_eager_and_graph(cuda, ranks, flag_wait):
+    world = ranks[0] * ranks[1] * ranks[2]
+    res = _spawn(_nbr_plan_graph, world, ranks, flag_wait, timeout=400)
+    assert all(v == 0 for v in res.values()), res
+
+
 def _halo_peer_absent(rank, world, job):
     """rank 1 builds the DIRECT halo plan and then never exchanges: rank 0's
     exchange kernel waits in its last block for rank 1's READY flag, gives
