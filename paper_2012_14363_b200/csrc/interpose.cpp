@@ -62,6 +62,12 @@ template <class F> F next_sym(const char *name) {
   return reinterpret_cast<F>(p);
 }
 #define REAL(fn) (*([] { static const auto f = next_sym<decltype(&MPI_##fn)>("PMPI_" #fn); return f; }()))
+// a PMPI_* an older system MPI may lack (MPI-4 calls): null when absent
+#define REAL_OPT(fn)                                                                                             \
+  ([] {                                                                                                          \
+    static const auto f = reinterpret_cast<decltype(&MPI_##fn)>(dlsym(RTLD_NEXT, "PMPI_" #fn));                 \
+    return f;                                                                                                    \
+  }())
 
 enum class Mem { Device, Pinned, Pageable };
 
@@ -188,6 +194,16 @@ struct BatchKey {
   bool operator<(const BatchKey &o) const { return k < o.k; }
 };
 
+// one segment of a neighbour exchange side: `count` objects of `type`
+// between the caller's buffer and a packed buffer at `position`
+struct Segment {
+  const void *src;
+  sp_type type;
+  int64_t count;
+  void *dst;
+  int64_t position;
+};
+
 struct State {
   std::mutex mu;         // tables
   std::mutex scratch_mu; // the reusable scratch buffers (one blocking call at a time)
@@ -197,6 +213,14 @@ struct State {
   // persistent requests of accelerated types (MPI_Send_init / MPI_Recv_init):
   // their packed message buffers live until MPI_Request_free
   std::unordered_map<MPI_Request, Pending> persist;
+  // persistent neighbour collectives (MPI-4): packed segments on both
+  // sides, packed at MPI_Start and unpacked at completion
+  struct Coll {
+    std::vector<Segment> pack, unpack;
+    void *sp = nullptr, *rp = nullptr;
+    bool pinned = false, started = false;
+  };
+  std::unordered_map<MPI_Request, Coll> colls;
   // mirrors still named by a pending receive, and the ones among them whose
   // MPI type was freed (MPI lets a pending operation outlive its datatype):
   // released when the last such receive completes
@@ -433,14 +457,6 @@ void setup() {
 
 // the pack (or unpack) of every accelerated segment of one exchange side in
 // one launch; plans are cached on the call's full argument list
-struct Segment {
-  const void *src;
-  sp_type type;
-  int64_t count;
-  void *dst;
-  int64_t position;
-};
-
 int run_segments(const std::vector<Segment> &segs, bool unpack) {
   if (segs.empty()) return MPI_SUCCESS;
   BatchKey key;
@@ -828,6 +844,26 @@ namespace {
 
 // a request the system MPI just completed: unpack a receive, free its scratch
 int finish(MPI_Request key, MPI_Status *status, int rc) {
+  { // a persistent neighbour collective: unpack what its start received
+    std::vector<Segment> unpack;
+    bool ours = false;
+    {
+      std::lock_guard<std::mutex> lk(S().mu);
+      auto c = S().colls.find(key);
+      if (c != S().colls.end()) {
+        ours = true;
+        if (c->second.started) unpack = c->second.unpack; // (a wait on an inactive request moves nothing)
+        c->second.started = false;
+      }
+    }
+    if (ours) {
+      if (rc == MPI_SUCCESS && !unpack.empty()) {
+        rc = run_segments(unpack, true);
+        if (rc == MPI_SUCCESS) rc = stream_sync();
+      }
+      return rc;
+    }
+  }
   Pending p;
   bool persistent = false;
   {
@@ -970,6 +1006,28 @@ int MPI_Testall(int n, MPI_Request reqs[], int *flag, MPI_Status statuses[]) {
 // buffer until the system MPI is done with it (a send): it is completed here
 int MPI_Request_free(MPI_Request *req) {
   if (!req) return MPI_ERR_ARG;
+  {
+    bool coll = false;
+    {
+      std::lock_guard<std::mutex> lk(S().mu);
+      coll = S().colls.count(*req) != 0;
+    }
+    if (coll) { // complete a start still in flight, then release its packed buffers
+      const MPI_Request key = *req;
+      const int rc = MPI_Wait(req, MPI_STATUS_IGNORE);
+      *req = key;
+      const int rf = REAL(Request_free)(req);
+      State::Coll c;
+      {
+        std::lock_guard<std::mutex> lk(S().mu);
+        c = S().colls[key];
+        S().colls.erase(key);
+      }
+      for (void *b : {c.sp, c.rp})
+        if (b) c.pinned ? cudaFreeHost(b) : cudaFree(b);
+      return rc != MPI_SUCCESS ? rc : rf;
+    }
+  }
   bool ours = false, persistent = false;
   {
     std::lock_guard<std::mutex> lk(S().mu);
@@ -1068,6 +1126,22 @@ int MPI_Start(MPI_Request *req) {
       ours = true;
       p = it->second;
     }
+  }
+  std::vector<Segment> pack;
+  bool coll = false;
+  {
+    std::lock_guard<std::mutex> lk(S().mu);
+    auto c = S().colls.find(*req);
+    if (c != S().colls.end()) {
+      coll = true;
+      pack = c->second.pack;
+      c->second.started = true;
+    }
+  }
+  if (coll && !pack.empty()) { // the send side's segments into its packed buffer
+    int rc = run_segments(pack, false);
+    if (rc == MPI_SUCCESS) rc = stream_sync();
+    if (rc != MPI_SUCCESS) return rc;
   }
   if (ours && !p.recv) { // pack this round's data into the registered message buffer
     Mirror m;
@@ -1241,6 +1315,71 @@ int MPI_Neighbor_alltoallw(const void *sbuf, const int scounts[], const MPI_Aint
   }
   S().st.forwarded++;
   return REAL(Neighbor_alltoallw)(sbuf, scounts, sdispls, stypes, rbuf, rcounts, rdispls, rtypes, comm);
+}
+
+// MPI-4.0 persistent neighbour collective: the system MPI's persistent
+// byte exchange between packed buffers owned by the request; MPI_Start
+// packs every accelerated send segment in one launch first, completion
+// unpacks every accelerated receive segment in one launch
+int MPI_Neighbor_alltoallw_init(const void *sbuf, const int scounts[], const MPI_Aint sdispls[],
+                                const MPI_Datatype stypes[], void *rbuf, const int rcounts[],
+                                const MPI_Aint rdispls[], const MPI_Datatype rtypes[], MPI_Comm comm, MPI_Info info,
+                                MPI_Request *req) {
+  int indeg = 0, outdeg = 0;
+  if (!req) return MPI_ERR_ARG;
+  const auto real_init = REAL_OPT(Neighbor_alltoallw_init);
+  if (!real_init) return MPI_ERR_UNSUPPORTED_OPERATION; // an MPI-3 system library
+  if (!degrees(comm, &indeg, &outdeg))
+    return real_init(sbuf, scounts, sdispls, stypes, rbuf, rcounts, rdispls, rtypes, comm, info, req);
+  Side s = plan_side(sbuf, outdeg, scounts, stypes, MPI_DATATYPE_NULL);
+  Side r = plan_side(rbuf, indeg, rcounts, rtypes, MPI_DATATYPE_NULL);
+  if (!s.accel && !r.accel) {
+    S().st.forwarded++;
+    return real_init(sbuf, scounts, sdispls, stypes, rbuf, rcounts, rdispls, rtypes, comm, info, req);
+  }
+  State::Coll c;
+  c.pinned = !S().cuda_aware;
+  auto alloc = [&](int64_t n) -> void * {
+    void *p = nullptr;
+    const size_t b = static_cast<size_t>(std::max<int64_t>(n, 1));
+    if ((c.pinned ? cudaMallocHost(&p, b) : cudaMalloc(&p, b)) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    return p;
+  };
+  if (s.accel && !(c.sp = alloc(s.total))) return MPI_ERR_NO_MEM;
+  if (r.accel && !(c.rp = alloc(r.total))) {
+    if (c.sp) c.pinned ? cudaFreeHost(c.sp) : cudaFree(c.sp);
+    return MPI_ERR_NO_MEM;
+  }
+  std::vector<int> scb, rcb;
+  std::vector<MPI_Aint> sdb, rdb;
+  std::vector<MPI_Datatype> stb, rtb;
+  for (int i = 0; i < outdeg; ++i) {
+    scb.push_back(s.accel ? s.bytes[i] : scounts[i]);
+    sdb.push_back(s.accel ? s.offs[i] : sdispls[i]);
+    stb.push_back(s.accel ? MPI_BYTE : stypes[i]);
+    if (s.accel)
+      c.pack.push_back({static_cast<const uint8_t *>(sbuf) + sdispls[i], s.m[i].h, scounts[i], c.sp, s.offs[i]});
+  }
+  for (int j = 0; j < indeg; ++j) {
+    rcb.push_back(r.accel ? r.bytes[j] : rcounts[j]);
+    rdb.push_back(r.accel ? r.offs[j] : rdispls[j]);
+    rtb.push_back(r.accel ? MPI_BYTE : rtypes[j]);
+    if (r.accel)
+      c.unpack.push_back({c.rp, r.m[j].h, rcounts[j], static_cast<uint8_t *>(rbuf) + rdispls[j], r.offs[j]});
+  }
+  const int rc = real_init(s.accel ? c.sp : sbuf, scb.data(), sdb.data(), stb.data(), r.accel ? c.rp : rbuf,
+                           rcb.data(), rdb.data(), rtb.data(), comm, info, req);
+  if (rc != MPI_SUCCESS) {
+    for (void *b : {c.sp, c.rp})
+      if (b) c.pinned ? cudaFreeHost(b) : cudaFree(b);
+    return rc;
+  }
+  std::lock_guard<std::mutex> lk(S().mu);
+  S().colls[*req] = std::move(c);
+  return MPI_SUCCESS;
 }
 
 // ============================================================ all-to-all (MPI-3.1 5.8)

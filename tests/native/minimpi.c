@@ -768,6 +768,7 @@ typedef struct {
   /* persistent requests (MPI_Send_init / MPI_Recv_init): recorded, started
    * by MPI_Start, inactive again once complete */
   int persistent, active;
+  void *coll; /* a persistent neighbour collective (MPI-4): its arguments */
 } Req;
 static Req g_reqs[4096];
 
@@ -953,6 +954,8 @@ int PMPI_Request_free(MPI_Request *r) {
   if (!r || *r == MPI_REQUEST_NULL) return MPI_ERR_ARG;
   const int rc = complete(r, NULL, 1, NULL);
   if (*r != MPI_REQUEST_NULL) { /* persistent: released here */
+    free(g_reqs[*r].coll);
+    g_reqs[*r].coll = NULL;
     g_reqs[*r].used = 0;
     *r = MPI_REQUEST_NULL;
   }
@@ -991,10 +994,17 @@ int PMPI_Recv_init(void *buf, int count, MPI_Datatype dt, int source, int tag, M
 int MPI_Recv_init(void *buf, int count, MPI_Datatype dt, int source, int tag, MPI_Comm comm, MPI_Request *r)
     ALIAS(MPI_Recv_init);
 
+static int coll_start(void *coll);
+
 int PMPI_Start(MPI_Request *r) {
   if (!r || *r <= 0 || *r >= 4096 || !g_reqs[*r].used || !g_reqs[*r].persistent || g_reqs[*r].active)
     return MPI_ERR_ARG;
   Req *q = &g_reqs[*r];
+  if (q->coll) { /* a persistent collective runs at its start (blocking) */
+    const int rc = coll_start(q->coll);
+    if (rc == MPI_SUCCESS) q->active = 1;
+    return rc;
+  }
   if (q->src == MPI_PROC_NULL) return MPI_SUCCESS;
   if (!q->is_recv) {
     const int rc = send_typed(q->buf, q->count, &q->ty, q->src, q->tag, q->ctx);
@@ -1304,3 +1314,67 @@ int PMPI_Alltoallw(const void *sbuf, const int scounts[], const int sdispls[], c
 int MPI_Alltoallw(const void *sbuf, const int scounts[], const int sdispls[], const MPI_Datatype stypes[],
                   void *rbuf, const int rcounts[], const int rdispls[], const MPI_Datatype rtypes[], MPI_Comm comm)
     ALIAS(MPI_Alltoallw);
+
+/* ------------------------------------------------------------ persistent neighbour collective (MPI-4.0 7.10.2) */
+typedef struct {
+  const void *sbuf;
+  void *rbuf;
+  MPI_Comm comm;
+  int n_out, n_in;
+  int *scounts, *rcounts;
+  int64_t *sd, *rd;
+  MPI_Datatype *st, *rt;
+} Coll;
+
+static int coll_start(void *p) {
+  Coll *c = p;
+  return nbr_exchange(c->sbuf, c->scounts, c->sd, c->st, c->rbuf, c->rcounts, c->rd, c->rt, c->comm);
+}
+
+int PMPI_Neighbor_alltoallw_init(const void *sbuf, const int scounts[], const MPI_Aint sdispls[],
+                                 const MPI_Datatype stypes[], void *rbuf, const int rcounts[],
+                                 const MPI_Aint rdispls[], const MPI_Datatype rtypes[], MPI_Comm comm, MPI_Info info,
+                                 MPI_Request *r) {
+  (void)info;
+  const Comm *cm = comm_of(comm);
+  if (!cm || cm->kind == 0) return MPI_ERR_COMM;
+  if (!r) return MPI_ERR_ARG;
+  const int no = cm->ndst, ni = cm->nsrc;
+  /* one allocation: the struct, then its arrays */
+  const size_t bytes = sizeof(Coll) + (size_t)(no + ni) * (sizeof(int) + sizeof(int64_t) + sizeof(MPI_Datatype));
+  Coll *c = calloc(1, bytes);
+  uint8_t *at = (uint8_t *)(c + 1);
+  c->sd = (int64_t *)at;
+  c->rd = c->sd + no;
+  c->scounts = (int *)(c->rd + ni);
+  c->rcounts = c->scounts + no;
+  c->st = (MPI_Datatype *)(c->rcounts + ni);
+  c->rt = c->st + no;
+  c->sbuf = sbuf;
+  c->rbuf = rbuf;
+  c->comm = comm;
+  c->n_out = no;
+  c->n_in = ni;
+  for (int i = 0; i < no; ++i) {
+    c->sd[i] = sdispls[i];
+    c->scounts[i] = scounts[i];
+    c->st[i] = stypes[i];
+  }
+  for (int j = 0; j < ni; ++j) {
+    c->rd[j] = rdispls[j];
+    c->rcounts[j] = rcounts[j];
+    c->rt[j] = rtypes[j];
+  }
+  const int rc = new_req(r);
+  if (rc != MPI_SUCCESS) {
+    free(c);
+    return rc;
+  }
+  g_reqs[*r].persistent = 1;
+  g_reqs[*r].coll = c;
+  return MPI_SUCCESS;
+}
+int MPI_Neighbor_alltoallw_init(const void *sbuf, const int scounts[], const MPI_Aint sdispls[],
+                                const MPI_Datatype stypes[], void *rbuf, const int rcounts[], const MPI_Aint rdispls[],
+                                const MPI_Datatype rtypes[], MPI_Comm comm, MPI_Info info, MPI_Request *r)
+    ALIAS(MPI_Neighbor_alltoallw_init);

@@ -35,7 +35,7 @@ INTERCEPTED = {
     "MPI_Type_commit", "MPI_Type_free", "MPI_Pack", "MPI_Unpack",
     "MPI_Send", "MPI_Recv", "MPI_Isend", "MPI_Irecv", "MPI_Wait", "MPI_Waitall", "MPI_Test", "MPI_Sendrecv",
     "MPI_Waitany", "MPI_Waitsome", "MPI_Testany", "MPI_Testall", "MPI_Request_free",
-    "MPI_Send_init", "MPI_Recv_init", "MPI_Start", "MPI_Startall",
+    "MPI_Send_init", "MPI_Recv_init", "MPI_Start", "MPI_Startall", "MPI_Neighbor_alltoallw_init",
     "MPI_Dist_graph_create_adjacent", "MPI_Cart_create", "MPI_Comm_free",
     "MPI_Neighbor_alltoallv", "MPI_Neighbor_alltoallw", "MPI_Alltoallv", "MPI_Alltoallw",
 }
@@ -159,14 +159,16 @@ def test_interposed_not_cuda_aware(cuda, sysmpi):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1, 2])
 @pytest.mark.parametrize("grid", [(1, 1, 1), (2, 1, 1), (2, 2, 1)])
 def test_interposed_halo_exchange(cuda, sysmpi, grid, mode):
     """the paper's halo exchange, unmodified source: mode 0 = MPI_Pack x26
     (interposer kernels) + MPI_Neighbor_alltoallv of MPI_PACKED (forwarded) +
     MPI_Unpack x26; mode 1 = one MPI_Neighbor_alltoallw of the 26 region
     types (one batched pack launch, the system MPI's byte exchange, one
-    batched unpack launch); every ghost cell verified"""
+    batched unpack launch); mode 2 = the same as an MPI-4 persistent
+    collective (MPI_Neighbor_alltoallw_init, MPI_Start + MPI_Wait); every
+    ghost cell verified"""
     exe = build(sysmpi, "mpi_halo", interposed=False)
     n = grid[0] * grid[1] * grid[2]
     _, st = run(n, exe, *map(str, grid), "12", "2", "16", "3", str(mode), preload=True)
