@@ -1382,6 +1382,27 @@ int MPI_Neighbor_alltoallw_init(const void *sbuf, const int scounts[], const MPI
   return MPI_SUCCESS;
 }
 
+// the v form: one type per side, displacements in extents -- the w form's
+// arguments (byte displacements, the type on every edge)
+int MPI_Neighbor_alltoallv_init(const void *sbuf, const int scounts[], const int sdispls[], MPI_Datatype stype,
+                                void *rbuf, const int rcounts[], const int rdispls[], MPI_Datatype rtype,
+                                MPI_Comm comm, MPI_Info info, MPI_Request *req) {
+  int indeg = 0, outdeg = 0;
+  Mirror sm, rm;
+  if (!degrees(comm, &indeg, &outdeg) || !committed(stype, &sm) || !committed(rtype, &rm)) {
+    const auto real_v = REAL_OPT(Neighbor_alltoallv_init);
+    if (!real_v) return MPI_ERR_UNSUPPORTED_OPERATION;
+    S().st.forwarded++;
+    return real_v(sbuf, scounts, sdispls, stype, rbuf, rcounts, rdispls, rtype, comm, info, req);
+  }
+  std::vector<MPI_Aint> sd(outdeg), rd(indeg);
+  for (int i = 0; i < outdeg; ++i) sd[i] = static_cast<MPI_Aint>(sdispls[i]) * sm.extent;
+  for (int j = 0; j < indeg; ++j) rd[j] = static_cast<MPI_Aint>(rdispls[j]) * rm.extent;
+  const std::vector<MPI_Datatype> st(outdeg, stype), rt(indeg, rtype);
+  return MPI_Neighbor_alltoallw_init(sbuf, scounts, sd.data(), st.data(), rbuf, rcounts, rd.data(), rt.data(), comm,
+                                     info, req);
+}
+
 // ============================================================ all-to-all (MPI-3.1 5.8)
 int MPI_Alltoallv(const void *sbuf, const int scounts[], const int sdispls[], MPI_Datatype stype, void *rbuf,
                   const int rcounts[], const int rdispls[], MPI_Datatype rtype, MPI_Comm comm) {

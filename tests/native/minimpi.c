@@ -1378,3 +1378,32 @@ int MPI_Neighbor_alltoallw_init(const void *sbuf, const int scounts[], const MPI
                                 const MPI_Datatype stypes[], void *rbuf, const int rcounts[], const MPI_Aint rdispls[],
                                 const MPI_Datatype rtypes[], MPI_Comm comm, MPI_Info info, MPI_Request *r)
     ALIAS(MPI_Neighbor_alltoallw_init);
+
+int PMPI_Neighbor_alltoallv_init(const void *sbuf, const int scounts[], const int sdispls[], MPI_Datatype stype,
+                                 void *rbuf, const int rcounts[], const int rdispls[], MPI_Datatype rtype,
+                                 MPI_Comm comm, MPI_Info info, MPI_Request *r) {
+  const Comm *cm = comm_of(comm);
+  const Type *st = type_of(stype), *rt = type_of(rtype);
+  if (!cm || cm->kind == 0) return MPI_ERR_COMM;
+  if (!st || !rt) return MPI_ERR_TYPE;
+  const int no = cm->ndst, ni = cm->nsrc;
+  MPI_Aint *sd = malloc(sizeof(MPI_Aint) * (no + 1)), *rd = malloc(sizeof(MPI_Aint) * (ni + 1));
+  MPI_Datatype *sts = malloc(sizeof(MPI_Datatype) * (no + 1)), *rts = malloc(sizeof(MPI_Datatype) * (ni + 1));
+  for (int i = 0; i < no; ++i) {
+    sd[i] = (MPI_Aint)sdispls[i] * st->extent;
+    sts[i] = stype;
+  }
+  for (int j = 0; j < ni; ++j) {
+    rd[j] = (MPI_Aint)rdispls[j] * rt->extent;
+    rts[j] = rtype;
+  }
+  const int rc = PMPI_Neighbor_alltoallw_init(sbuf, scounts, sd, sts, rbuf, rcounts, rd, rts, comm, info, r);
+  free(sd);
+  free(rd);
+  free(sts);
+  free(rts);
+  return rc;
+}
+int MPI_Neighbor_alltoallv_init(const void *sbuf, const int scounts[], const int sdispls[], MPI_Datatype stype,
+                                void *rbuf, const int rcounts[], const int rdispls[], MPI_Datatype rtype, MPI_Comm comm,
+                                MPI_Info info, MPI_Request *r) ALIAS(MPI_Neighbor_alltoallv_init);

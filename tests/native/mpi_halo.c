@@ -8,7 +8,9 @@
  * types = the ghost regions, byte displacements 0 (ghost writes, no packed
  * buffers). MODE = 2 is the same exchange as an MPI-4 persistent
  * collective: MPI_Neighbor_alltoallw_init once, then MPI_Start + MPI_Wait
- * per iteration (the ghosts reset before the last one).
+ * per iteration (the ghosts reset before the last one). MODE = 3 is mode 0
+ * with the MPI_Neighbor_alltoallv of the packed segments made persistent
+ * (MPI_Neighbor_alltoallv_init once, MPI_Start + MPI_Wait per iteration).
  * usage: mpi_halo RX RY RZ N RADIUS ELEM ITERS [MODE]  (RX*RY*RZ == ranks)
  * prints per-phase wall times of the last iteration and "OK". */
 #include <stdio.h>
@@ -17,8 +19,9 @@
 #include <mpi.h>
 #include "stridepack_b200.h"
 
-/* MPI-4 (mode 2): weak, so the program still links against an MPI-3 library */
+/* MPI-4 (modes 2, 3): weak, so the program still links against an MPI-3 library */
 #pragma weak MPI_Neighbor_alltoallw_init
+#pragma weak MPI_Neighbor_alltoallv_init
 
 #define CHECK(c) do { if (!(c)) { printf("FAIL rank %d line %d: %s\n", rank, __LINE__, #c); MPI_Abort(MPI_COMM_WORLD, 1); } } while (0)
 
@@ -83,8 +86,8 @@ int main(int argc, char **argv) {
   CHECK(sp_halo_fill(&cfg, rank, alloc, NULL) == SP_OK);
   cudaDeviceSynchronize();
   double tp = 0, tx = 0, tu = 0;
-  if (mode == 2 && !MPI_Neighbor_alltoallw_init) {
-    if (rank == 0) printf("MPI_Neighbor_alltoallw_init: not in this MPI library\nOK\n");
+  if ((mode == 2 && !MPI_Neighbor_alltoallw_init) || (mode == 3 && !MPI_Neighbor_alltoallv_init)) {
+    if (rank == 0) printf("MPI-4 persistent collectives: not in this MPI library\nOK\n");
     MPI_Finalize();
     return 0;
   }
@@ -131,13 +134,21 @@ int main(int argc, char **argv) {
     }
     iters = 0;
   }
+  MPI_Request vreq = MPI_REQUEST_NULL;
+  if (mode == 3)
+    CHECK(MPI_Neighbor_alltoallv_init(sbuf, sizes, off, MPI_PACKED, rbuf, sizes, off, MPI_PACKED, g, MPI_INFO_NULL,
+                                      &vreq) == MPI_SUCCESS);
   for (int it = 0; it < iters; ++it) {
     MPI_Barrier(MPI_COMM_WORLD);
     const double t0 = MPI_Wtime();
     int pos = 0;
     for (int i = 0; i < 26; ++i) CHECK(MPI_Pack(alloc, 1, send_t[i], sbuf, off[26], &pos, MPI_COMM_WORLD) == MPI_SUCCESS);
     const double t1 = MPI_Wtime();
-    CHECK(MPI_Neighbor_alltoallv(sbuf, sizes, off, MPI_PACKED, rbuf, sizes, off, MPI_PACKED, g) == MPI_SUCCESS);
+    if (mode == 3) {
+      CHECK(MPI_Start(&vreq) == MPI_SUCCESS && MPI_Wait(&vreq, MPI_STATUS_IGNORE) == MPI_SUCCESS);
+    } else {
+      CHECK(MPI_Neighbor_alltoallv(sbuf, sizes, off, MPI_PACKED, rbuf, sizes, off, MPI_PACKED, g) == MPI_SUCCESS);
+    }
     const double t2 = MPI_Wtime();
     pos = 0;
     for (int i = 0; i < 26; ++i) {
@@ -148,6 +159,7 @@ int main(int argc, char **argv) {
     const double t3 = MPI_Wtime();
     tp = t1 - t0; tx = t2 - t1; tu = t3 - t2;
   }
+  if (vreq != MPI_REQUEST_NULL) CHECK(MPI_Request_free(&vreq) == MPI_SUCCESS);
   int64_t bad = -1;
   CHECK(sp_halo_verify(&cfg, rank, alloc, NULL, &bad) == SP_OK);
   CHECK(bad == 0);

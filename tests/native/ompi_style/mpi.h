@@ -92,6 +92,8 @@ int MPI_Neighbor_alltoallw(const void *, const int[], const MPI_Aint[], const MP
 int MPI_Neighbor_alltoallw_init(const void *, const int[], const MPI_Aint[], const MPI_Datatype[], void *,
                                 const int[], const MPI_Aint[], const MPI_Datatype[], MPI_Comm, MPI_Info,
                                 MPI_Request *);
+int MPI_Neighbor_alltoallv_init(const void *, const int[], const int[], MPI_Datatype, void *, const int[],
+                                const int[], MPI_Datatype, MPI_Comm, MPI_Info, MPI_Request *);
 int MPI_Alltoallv(const void *, const int[], const int[], MPI_Datatype, void *, const int[], const int[],
                   MPI_Datatype, MPI_Comm);
 int MPI_Alltoallw(const void *, const int[], const int[], const MPI_Datatype[], void *, const int[], const int[],

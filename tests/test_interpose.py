@@ -36,6 +36,7 @@ INTERCEPTED = {
     "MPI_Send", "MPI_Recv", "MPI_Isend", "MPI_Irecv", "MPI_Wait", "MPI_Waitall", "MPI_Test", "MPI_Sendrecv",
     "MPI_Waitany", "MPI_Waitsome", "MPI_Testany", "MPI_Testall", "MPI_Request_free",
     "MPI_Send_init", "MPI_Recv_init", "MPI_Start", "MPI_Startall", "MPI_Neighbor_alltoallw_init",
+    "MPI_Neighbor_alltoallv_init",
     "MPI_Dist_graph_create_adjacent", "MPI_Cart_create", "MPI_Comm_free",
     "MPI_Neighbor_alltoallv", "MPI_Neighbor_alltoallw", "MPI_Alltoallv", "MPI_Alltoallw",
 }
@@ -159,7 +160,7 @@ def test_interposed_not_cuda_aware(cuda, sysmpi):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
 @pytest.mark.parametrize("grid", [(1, 1, 1), (2, 1, 1), (2, 2, 1)])
 def test_interposed_halo_exchange(cuda, sysmpi, grid, mode):
     """the paper's halo exchange, unmodified source: mode 0 = MPI_Pack x26

@@ -124,13 +124,14 @@ def test_mpi_nonblocking_ring(cuda, tmp_path, np_):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
 @pytest.mark.parametrize("grid", [(1, 1, 1), (2, 1, 1), (2, 2, 1), (2, 2, 2)])
 def test_mpi_halo_exchange(cuda, tmp_path, grid, mode):
     """mode 0: MPI_Pack x26 + MPI_Neighbor_alltoallv + MPI_Unpack x26;
     mode 1: one MPI_Neighbor_alltoallw with the 26 region types;
     mode 2: the same as an MPI-4 persistent collective
-    (MPI_Neighbor_alltoallw_init, MPI_Start + MPI_Wait per iteration)"""
+    (MPI_Neighbor_alltoallw_init, MPI_Start + MPI_Wait per iteration);
+    mode 3: mode 0 with a persistent MPI_Neighbor_alltoallv_init"""
     exe = build(tmp_path, "mpi_halo")
     out = run(grid[0] * grid[1] * grid[2], exe, *map(str, grid), "12", "2", "16", "3", str(mode))
     assert "OK" in out
