@@ -1077,6 +1077,51 @@ def test_persistent_neighbor_plan_eager_and_graph(cuda, ranks, flag_wait):
     assert all(v == 0 for v in res.values()), res
 
 
+def _nbr_plan_refused(rank, world, job):
+    """only rank 0 has a receive type the plan cannot compile (an irregular
+    indexed layout): every rank must refuse the plan together (a rank that
+    went on alone would wait forever in the creation's barriers), and an
+    ordinary call still works afterwards"""
+    import numpy as np
+    import torch
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.rt as rt
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=1 << 20, host_bytes=1 << 20)
+    peer = 1 - rank
+    D = sp.make_named(sp.NamedKind.Double)
+    flat = sp.commit_type(sp.make_contiguous(6, D))
+    irregular = sp.commit_type(sp.make_indexed([2, 1, 3], [9, 0, 4], D))
+    recv_t = irregular if rank == 0 else flat
+    src = torch.arange(6, dtype=torch.float64, device="cuda") + 100 * rank
+    dst = torch.full((16,), -1.0, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    refused = False
+    try:
+        rt.NeighborPlan([(peer, 1, flat, 0)], [(peer, 1, recv_t, 0)], src, dst)
+    except sp.Unsupported:
+        refused = True
+    rt.NeighborW([(peer, 1, flat, 0)], [(peer, 1, recv_t, 0)])(src, dst)
+    torch.cuda.synchronize()
+    got = dst.cpu().numpy()
+    sent = np.arange(6) + 100 * peer
+    if rank == 0:
+        want = np.full(16, -1.0)
+        k = 0
+        for b, d in zip([2, 1, 3], [9, 0, 4]):
+            want[d:d + b] = sent[k:k + b]
+            k += b
+    else:
+        want = np.concatenate([sent, np.full(10, -1.0)])
+    rt.finalize()
+    return refused and bool(np.array_equal(got, want))
+
+
+@pytest.mark.gpu
+def test_persistent_neighbor_plan_refused_together(cuda):
+    assert all(_spawn(_nbr_plan_refused, 2, timeout=200).values())
+
+
 def _halo_peer_absent(rank, world, job):
     """rank 1 builds the DIRECT halo plan and then never exchanges: rank 0's
     exchange kernel waits in its last block for rank 1's READY flag, gives
