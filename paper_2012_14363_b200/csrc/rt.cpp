@@ -79,6 +79,7 @@ struct Desc {
   cudaIpcMemHandle_t h;
   int64_t off;
   uint64_t raw;
+  uint64_t hr[2], sr[2], dr[2]; // the exporter's allocation (base, bytes) behind h, hs, hd
   // runs == 1: the receiver's run table (piece source offsets, packed
   // prefix) for peers through CUDA IPC, and raw for the receiver itself
   cudaIpcMemHandle_t hs, hd;
@@ -97,6 +98,7 @@ struct Slot {
   int64_t host_bytes;         // shared pinned host region (ONESHOT/STAGED)
   cudaIpcMemHandle_t xh;      // publication area of sp_rt_exchange_ptr
   int64_t xoff;
+  uint64_t xr[2];             // the allocation behind xh in the publisher's address space (base, bytes)
   int64_t xbytes;
   int32_t nedges;             // neighbour-exchange in-edges: (src, offset, bytes)
   int32_t pad2;
@@ -186,6 +188,7 @@ struct Runtime {
     int peer = -1;
     int pins = 0;
     uint64_t used = 0; // ipc_clock at the last open_ipc that returned it
+    uint64_t base = 0, bytes = 0; // the allocation in the peer's address space (0: unknown)
   };
   std::map<std::string, IpcMap> ipc_cache;
   uint64_t ipc_clock = 0, ipc_call_mark = 0; // mappings used since the mark belong to the call in progress
@@ -320,7 +323,13 @@ Msg wait_msg(uint32_t kind, int src, int tag) {
 // and with every cached neighbour launch that could name them dropped)
 // until the new handle opens. Mappings the call in progress already uses
 // (since ipc_call_mark) are never closed.
-uint8_t *open_ipc(const cudaIpcMemHandle_t &h, int peer) {
+// When the publisher also sent the allocation's range in its own address
+// space (`range` = base, bytes), a cached mapping of the same peer whose
+// range overlaps it under another handle is known to be stale before the
+// open is tried (the peer can only reuse addresses it freed): it is closed
+// first, and the driver never sees the conflicting open. The retry loop
+// stays for publishers that give no range.
+uint8_t *open_ipc(const cudaIpcMemHandle_t &h, int peer, const uint64_t *range = nullptr) {
   Runtime &R = rt();
   const std::string key(reinterpret_cast<const char *>(&h), sizeof(h));
   ++R.ipc_clock;
@@ -329,6 +338,36 @@ uint8_t *open_ipc(const cudaIpcMemHandle_t &h, int peer) {
     it->second.used = R.ipc_clock;
     return it->second.p;
   }
+  auto evictable = [&](const Runtime::IpcMap &m) {
+    return m.peer == peer && m.pins == 0 && m.used <= R.ipc_call_mark;
+  };
+  auto close_entry = [&](std::map<std::string, Runtime::IpcMap>::iterator e) {
+    cudaIpcCloseMemHandle(e->second.p);
+    for (auto x = R.exchanged.begin(); x != R.exchanged.end();)
+      x = x->second == e->first ? R.exchanged.erase(x) : std::next(x);
+    return R.ipc_cache.erase(e);
+  };
+  const uint64_t base = range ? range[0] : 0, bytes = range ? range[1] : 0;
+  auto overlaps = [&](const Runtime::IpcMap &m) {
+    if (!m.base) return false;
+    if (!m.bytes || !bytes) return m.base == base;
+    return base < m.base + m.bytes && m.base < base + bytes;
+  };
+  if (base) {
+    bool drained = false;
+    for (auto e = R.ipc_cache.begin(); e != R.ipc_cache.end();) {
+      if (!overlaps(e->second) || !evictable(e->second)) {
+        ++e;
+        continue;
+      }
+      if (!drained) {
+        cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize(stale IPC mappings)");
+        nbr_reset();
+        drained = true;
+      }
+      e = close_entry(e);
+    }
+  }
   void *p = nullptr;
   cudaError_t err = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
   if (err == cudaErrorAlreadyMapped) {
@@ -336,20 +375,17 @@ uint8_t *open_ipc(const cudaIpcMemHandle_t &h, int peer) {
     cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize(stale IPC mappings)");
     nbr_reset();
     for (auto e = R.ipc_cache.begin(); e != R.ipc_cache.end() && err == cudaErrorAlreadyMapped;) {
-      if (e->second.peer != peer || e->second.pins > 0 || e->second.used > R.ipc_call_mark) {
+      if (!evictable(e->second)) {
         ++e;
         continue;
       }
-      cudaIpcCloseMemHandle(e->second.p);
-      for (auto x = R.exchanged.begin(); x != R.exchanged.end();)
-        x = x->second == e->first ? R.exchanged.erase(x) : std::next(x);
-      e = R.ipc_cache.erase(e);
+      e = close_entry(e);
       err = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
       if (err == cudaErrorAlreadyMapped) cudaGetLastError();
     }
   }
   cuda_check(err, "cudaIpcOpenMemHandle");
-  R.ipc_cache[key] = Runtime::IpcMap{static_cast<uint8_t *>(p), peer, 0, R.ipc_clock};
+  R.ipc_cache[key] = Runtime::IpcMap{static_cast<uint8_t *>(p), peer, 0, R.ipc_clock, base, bytes};
   return static_cast<uint8_t *>(p);
 }
 
@@ -406,7 +442,9 @@ uint8_t *peer_host(int r) {
   return R.peer_host[r];
 }
 
-void ipc_handle_of(const void *ptr, cudaIpcMemHandle_t *h, int64_t *offset) {
+// `range` (optional) receives the allocation's base and size in this
+// process, published beside the handle so importers can tell stale mappings
+void ipc_handle_of(const void *ptr, cudaIpcMemHandle_t *h, int64_t *offset, uint64_t *range = nullptr) {
   // handles name whole allocations; carry the offset inside it separately.
   // One driver query gives the allocation's process-unique buffer id, its
   // base and its memory type; the handle itself (cudaIpcGetMemHandle, the
@@ -420,13 +458,14 @@ void ipc_handle_of(const void *ptr, cudaIpcMemHandle_t *h, int64_t *offset) {
     cudaGetDriverEntryPoint("cuPointerGetAttributes", &fn, cudaEnableDefault, &q);
     return reinterpret_cast<GetAttrs>(fn);
   }();
-  constexpr int kMemoryType = 2, kBufferId = 7, kRangeStart = 11, kDeviceMemory = 2; // cuda.h enums
+  constexpr int kMemoryType = 2, kBufferId = 7, kRangeStart = 11, kRangeSize = 12, kDeviceMemory = 2; // cuda.h enums
   unsigned mtype = 0;
   unsigned long long id = 0;
   uint64_t base = 0;
-  int which[3] = {kMemoryType, kBufferId, kRangeStart};
-  void *vals[3] = {&mtype, &id, &base};
-  if (!get_attrs || get_attrs(3, which, vals, reinterpret_cast<uint64_t>(ptr)) != 0)
+  size_t span = 0;
+  int which[4] = {kMemoryType, kBufferId, kRangeStart, kRangeSize};
+  void *vals[4] = {&mtype, &id, &base, &span};
+  if (!get_attrs || get_attrs(4, which, vals, reinterpret_cast<uint64_t>(ptr)) != 0)
     fail(SP_ERR_CUDA, "cuPointerGetAttributes failed");
   if (mtype != kDeviceMemory || !base) fail(SP_ERR_INVALID_ARGUMENT, "IPC export needs device memory");
   static std::mutex mu;
@@ -443,6 +482,10 @@ void ipc_handle_of(const void *ptr, cudaIpcMemHandle_t *h, int64_t *offset) {
     *h = it->second;
   }
   *offset = static_cast<const uint8_t *>(ptr) - reinterpret_cast<const uint8_t *>(base);
+  if (range) {
+    range[0] = base;
+    range[1] = span;
+  }
 }
 
 } // namespace
@@ -659,7 +702,7 @@ void rt_exchange_ptr(void *local, std::vector<uint8_t *> &out) {
   // uses: the next collective must publish its layout again
   R.nbr_layout.clear();
   if (local) {
-    ipc_handle_of(local, &me.xh, &me.xoff);
+    ipc_handle_of(local, &me.xh, &me.xoff, me.xr);
     me.xbytes = 1;
   } else {
     me.xbytes = 0;
@@ -670,7 +713,8 @@ void rt_exchange_ptr(void *local, std::vector<uint8_t *> &out) {
     if (r == R.rank) {
       out[r] = static_cast<uint8_t *>(local);
     } else if (R.shm->slots[r].xbytes) {
-      out[r] = open_ipc(R.shm->slots[r].xh, r) + R.shm->slots[r].xoff;
+      const Slot &sl = R.shm->slots[r];
+      out[r] = open_ipc(sl.xh, r, sl.xr) + sl.xoff;
       R.exchanged[out[r]] = std::string(reinterpret_cast<const char *>(&R.shm->slots[r].xh), sizeof(cudaIpcMemHandle_t));
     }
   }
@@ -870,7 +914,7 @@ void send_stream(Req &q) {
     const Desc &d = R.shm->slots[q.peer].desc[q.grant];
     Committed dst;
     committed_from(d, dst);
-    uint8_t *base = q.peer == R.rank ? reinterpret_cast<uint8_t *>(d.raw) : open_ipc(d.h, q.peer) + d.off;
+    uint8_t *base = q.peer == R.rank ? reinterpret_cast<uint8_t *>(d.raw) : open_ipc(d.h, q.peer, d.hr) + d.off;
     if (q.ct->form != SP_FORM_STRIDED) { // block-list send type: pack into the dense receive run
       PackArgs a{};
       a.ct = q.ct.get();
@@ -1082,7 +1126,7 @@ bool step_recv(Req &q) {
       d.span = c.span;
       d.count = q.bytes / c.size;
       d.raw = reinterpret_cast<uint64_t>(q.rbuf);
-      ipc_handle_of(q.rbuf, &d.h, &d.off);
+      ipc_handle_of(q.rbuf, &d.h, &d.off, d.hr);
       E.desc_used |= 1u << slot;
       q.region = 3;
       grant = slot;
@@ -1156,17 +1200,23 @@ bool step_recv(Req &q) {
         cuda_check(cudaFreeAsync(q.rbuf_stage, s), "cudaFreeAsync(staged)");
         q.rbuf_stage = nullptr;
       }
-      q.last = get_event();
-      cuda_check(cudaEventRecord(q.last, s), "cudaEventRecord");
+      if (q.bytes > 0 && q.method != SP_METHOD_DIRECT) {
+        q.last = get_event();
+        cuda_check(cudaEventRecord(q.last, s), "cudaEventRecord");
+      }
+      // DIRECT (and an empty message) enqueued nothing here: the sender's
+      // kernel had completed before its CHUNK was posted
       q.st = St::Draining;
       moved = true;
     }
     return moved;
   }
   case St::Draining: {
-    if (!event_done(q.last)) return false;
-    put_event(q.last);
-    q.last = nullptr;
+    if (q.last) {
+      if (!event_done(q.last)) return false;
+      put_event(q.last);
+      q.last = nullptr;
+    }
     if (q.region == 1) E.win.give(q.grant, q.bytes);
     if (q.region == 2) E.host.give(q.grant, q.bytes);
     if (q.region == 3) E.desc_used &= ~(1u << q.grant);
@@ -1421,7 +1471,8 @@ void nbr_publish(uint8_t *recvbuf, const std::vector<int> &sources, const std::v
   cudaIpcMemHandle_t h{};
   int64_t off = 0;
   const bool any = recvbuf != nullptr && std::any_of(bytes.begin(), bytes.end(), [](int64_t b) { return b > 0; });
-  if (any) ipc_handle_of(recvbuf, &h, &off);
+  uint64_t xr[2] = {0, 0};
+  if (any) ipc_handle_of(recvbuf, &h, &off, xr);
   std::string lay(reinterpret_cast<const char *>(&h), sizeof(h));
   lay.append(reinterpret_cast<const char *>(&off), sizeof(off));
   lay.push_back(any ? 1 : 0);
@@ -1433,6 +1484,8 @@ void nbr_publish(uint8_t *recvbuf, const std::vector<int> &sources, const std::v
   if (lay == R.nbr_layout) return; // unchanged: peers keep their cached plans
   me.xh = h;
   me.xoff = off;
+  me.xr[0] = xr[0];
+  me.xr[1] = xr[1];
   me.xbytes = any ? 1 : 0;
   me.nedges = static_cast<int32_t>(sources.size());
   for (size_t j = 0; j < sources.size(); ++j) {
@@ -1700,7 +1753,7 @@ void rt_neighbor_alltoallv(const uint8_t *sendbuf, const std::vector<int64_t> &s
       const int64_t bytes = send_counts[i] * st.size;
       if (bytes > peer.edges[hit][2]) fail(SP_ERR_BUFFER_TOO_SMALL, "neighbour exchange: message truncated");
       if (bytes == 0) continue;
-      uint8_t *base = d == R.rank ? recvbuf : open_ipc(peer.xh, d) + peer.xoff;
+      uint8_t *base = d == R.rank ? recvbuf : open_ipc(peer.xh, d, peer.xr) + peer.xoff;
       if (blocklist) {
         loose.push_back({stp, sendbuf + send_displs[i] * st.extent, send_counts[i], base + peer.edges[hit][1]});
         continue;
@@ -1780,8 +1833,8 @@ void desc_of(const Committed &c, int64_t count, Desc &d) {
     d.align = dr.align_or;
     d.raw_s = reinterpret_cast<uint64_t>(dr.d_src);
     d.raw_d = reinterpret_cast<uint64_t>(dr.d_dst);
-    ipc_handle_of(dr.d_src, &d.hs, &d.os);
-    ipc_handle_of(dr.d_dst, &d.hd, &d.od);
+    ipc_handle_of(dr.d_src, &d.hs, &d.os, d.sr);
+    ipc_handle_of(dr.d_dst, &d.hd, &d.od, d.dr);
     return;
   }
   d.ndims = c.sb.ndims();
@@ -1986,7 +2039,7 @@ NbrPlan *rt_nbr_plan_create(const uint8_t *sendbuf, const std::vector<int64_t> &
       why = "send and receive describe different byte counts";
     } else if (b > 0) {
       const Desc &wd = peer.wdesc[hit];
-      uint8_t *base = d == R.rank ? recvbuf : open_ipc(peer.xh, d) + peer.xoff;
+      uint8_t *base = d == R.rank ? recvbuf : open_ipc(peer.xh, d, peer.xr) + peer.xoff;
       if (d != R.rank) {
         ipc_pin_handle(peer.xh, 1);
         p->pinned.push_back(peer.xh);
@@ -2127,7 +2180,7 @@ void rt_neighbor_alltoallw_build(const uint8_t *sendbuf, const std::vector<int64
       fail(SP_ERR_INVALID_ARGUMENT, "neighbour alltoallw: send and receive describe different byte counts");
     if (bytes == 0) continue;
     const Desc &wd = peer.wdesc[hit];
-    uint8_t *base = (d == R.rank ? recvbuf : open_ipc(peer.xh, d) + peer.xoff) + peer.edges[hit][1];
+    uint8_t *base = (d == R.rank ? recvbuf : open_ipc(peer.xh, d, peer.xr) + peer.xoff) + peer.edges[hit][1];
     if (wd.runs) {
       // an irregular receive layout: a dense send run scattered through the
       // receiver's run table (read over NVLink from the receiver's HBM)
@@ -2147,8 +2200,8 @@ void rt_neighbor_alltoallw_build(const uint8_t *sendbuf, const std::vector<int64
       } else { // the peer's table, copied into this GPU's HBM once per call layout
         const size_t ns = static_cast<size_t>(wd.npieces) * sizeof(int64_t), nd = ns + sizeof(int64_t);
         auto cs = std::make_shared<TableCopy>(ns), cd = std::make_shared<TableCopy>(nd);
-        copy_sync(cs->p, open_ipc(wd.hs, d) + wd.os, ns, "run table copy");
-        copy_sync(cd->p, open_ipc(wd.hd, d) + wd.od, nd, "run table copy");
+        copy_sync(cs->p, open_ipc(wd.hs, d, wd.sr) + wd.os, ns, "run table copy");
+        copy_sync(cd->p, open_ipc(wd.hd, d, wd.dr) + wd.od, nd, "run table copy");
         op.psrc = static_cast<const int64_t *>(cs->p);
         op.pdst = static_cast<const int64_t *>(cd->p);
         tables.push_back(std::move(cs));

@@ -1077,6 +1077,66 @@ def test_persistent_neighbor_plan_eager_and_graph(cuda, ranks, flag_wait):
     assert all(v == 0 for v in res.values()), res
 
 
+def _realloc_receivers(rank, world, job):
+    """Receivers that free their buffer and allocate a new one (a real
+    cudaFree + cudaMalloc: empty_cache between, so the new buffer usually
+    lands at the old address with a new IPC handle). The sender's cached
+    mapping of the old allocation is stale; it must be closed before the new
+    handle is opened, for a DIRECT point-to-point destination (published with
+    its pointer in the descriptor) and for a neighbour call's receive buffer
+    (published in the rank's slot). Every round is checked element by
+    element; returns (bad rounds, distinct receive addresses seen)."""
+    import numpy as np
+    import torch
+    import paper_2012_14363_b200 as sp
+    import paper_2012_14363_b200.rt as rt
+    torch.cuda.set_device(0)
+    rt.init(rank, world, job, device=0, window_bytes=1 << 20, host_bytes=1 << 20)
+    peer = 1 - rank
+    n = 1 << 16
+    D = sp.make_named(sp.NamedKind.Double)
+    dense = sp.commit_type(sp.make_contiguous(n, D))
+    every_other = sp.commit_type(sp.make_vector(n, 1, 2, D))
+    bad, addrs = 0, set()
+    for it in range(6):
+        # point to point, rank 0 -> rank 1, DIRECT into a strided layout
+        if rank == 0:
+            src = torch.arange(n, dtype=torch.float64, device="cuda") + 1000.0 * it
+            torch.cuda.synchronize()
+            rt.send(src, 1, dense, 1, tag=it, method=rt.DIRECT)
+            del src
+        else:
+            dst = torch.full((2 * n,), -1.0, dtype=torch.float64, device="cuda")
+            torch.cuda.synchronize()
+            addrs.add(dst.data_ptr())
+            st = rt.recv(dst, 1, every_other, 0, it)
+            h = dst.cpu().numpy()
+            bad += not (st["method"] == rt.DIRECT and np.array_equal(h[0::2], np.arange(n) + 1000.0 * it)
+                        and (h[1::2] == -1).all())
+            del dst
+        torch.cuda.empty_cache()
+        rt.barrier()
+        # a neighbour alltoallw both ways into fresh receive buffers
+        src = torch.arange(n, dtype=torch.float64, device="cuda") + 1e6 * rank + it
+        dst = torch.full((2 * n,), -1.0, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        rt.NeighborW([(peer, 1, dense, 0)], [(peer, 1, every_other, 0)])(src, dst)
+        torch.cuda.synchronize()
+        h = dst.cpu().numpy()
+        bad += not (np.array_equal(h[0::2], np.arange(n) + 1e6 * peer + it) and (h[1::2] == -1).all())
+        del src, dst
+        torch.cuda.empty_cache()
+        rt.barrier()
+    rt.finalize()
+    return bad, len(addrs)
+
+
+@pytest.mark.gpu
+def test_receivers_reallocating_buffers(cuda):
+    res = _spawn(_realloc_receivers, 2, timeout=300)
+    assert all(v[0] == 0 for v in res.values()), res
+
+
 def _nbr_plan_refused(rank, world, job):
     """only rank 0 has a receive type the plan cannot compile (an irregular
     indexed layout): every rank must refuse the plan together (a rank that
