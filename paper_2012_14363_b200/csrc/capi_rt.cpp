@@ -442,7 +442,7 @@ sp_status sp_halo_plan_create(const sp_halo_config *cfgp, void *alloc, int metho
       p->pinned.insert(p->pinned.end(), p->peer_flags.begin(), p->peer_flags.end());
       int mydev = 0;
       cuda_check(cudaGetDevice(&mydev), "cudaGetDevice");
-      p->remote_peers = false;
+      p->remote_peers = rt_peers_remote();
       for (uint8_t *pf : p->peer_flags) {
         cudaPointerAttributes at{};
         if (pf && cudaPointerGetAttributes(&at, pf) == cudaSuccess && at.device != mydev) p->remote_peers = true;

@@ -569,8 +569,13 @@ void rt_init(int rank, int size, const char *name, int device, int64_t window_by
         G.shared_device = true;
   rt_exchange_ptr(G.nbr_flags, G.peer_nbr_flags);
   rt_pin_ptrs(G.peer_nbr_flags, 1 << 20); // the neighbour READY counters stay mapped until finalize
+  // system-scope flags whenever any peer runs on another GPU: by UUID (device
+  // ordinals are per process under CUDA_VISIBLE_DEVICES), and by where the
+  // peer's mapped flags live
   if (device >= 0)
     for (int r = 0; r < size; ++r) {
+      if (r != rank && G.shm->slots[r].device >= 0 && std::memcmp(G.shm->slots[r].uuid, me.uuid, sizeof(me.uuid)))
+        G.nbr_remote = true;
       cudaPointerAttributes at{};
       if (G.peer_nbr_flags[r] && cudaPointerGetAttributes(&at, G.peer_nbr_flags[r]) == cudaSuccess &&
           at.device != device)
@@ -618,6 +623,8 @@ uint64_t rt_device_timeout_ns() {
 }
 
 int *rt_device_err() { return rt().err_dev; }
+
+bool rt_peers_remote() { return rt().nbr_remote; }
 
 void rt_check_device_error(const char *what) {
   Runtime &R = rt();
@@ -1087,7 +1094,7 @@ bool step_recv(Req &q) {
         // NVLink when the sender is on another GPU): the receiver's layout
         // has a say too -- a model-offered DIRECT is accepted only when the
         // model, asked with this side's geometry, also prefers it
-        const bool model_ok = (m.offset & kOfferForced) || model_prefers_direct(*q.ct, objs, R.shm->slots[m.src].device);
+        const bool model_ok = (m.offset & kOfferForced) || model_prefers_direct(*q.ct, objs, m.src);
         if (dev && model_ok) q.method = SP_METHOD_DIRECT; // a descriptor slot is taken at the grant
       }
       q.st = St::Matched;
@@ -1299,7 +1306,7 @@ uint64_t rt_isend(const void *buf, uint64_t buf_bytes, int64_t count, CommitPtr 
   // (Eq. 4, the measured gpu_direct / gpu_direct_peer surface of the
   // receiver's GPU) puts it ahead of the reference's three methods
   const bool forced_direct = method == SP_METHOD_DIRECT;
-  bool allow_direct = forced_direct || (method < 0 && model_prefers_direct(*ct, count, R.shm->slots[dest].device));
+  bool allow_direct = forced_direct || (method < 0 && model_prefers_direct(*ct, count, dest));
   if (method < 0) method = rt_choose(*ct, count);
   if (method == SP_METHOD_DIRECT) method = SP_METHOD_DEVICE;
   if (method != SP_METHOD_DEVICE && method != SP_METHOD_ONESHOT && method != SP_METHOD_STAGED)
@@ -1420,12 +1427,13 @@ int rt_choose(const Committed &ct, int64_t count) {
 }
 
 // B200 model (Eq. 4) on DIRECT for `count` objects of `ct` moving between
-// this GPU and a device buffer on `peer_device`: true when the measured
-// DIRECT surface of that destination (same GPU or peer GPU) is at least as
+// this GPU and a device buffer of rank `peer` (same GPU or peer GPU, told
+// apart by UUID: ordinals are per process): true when the measured
+// DIRECT surface of that destination is at least as
 // fast as the reference's best method; without a profile DIRECT is the
 // default (it measured fastest on B200 at every size, bench.py `send`);
 // with a profile that lacks the surface, never.
-bool model_prefers_direct(const Committed &ct, int64_t count, int peer_device) {
+bool model_prefers_direct(const Committed &ct, int64_t count, int peer) {
   Runtime &R = rt();
   if (!R.profile) return true;
   if (ct.size == 0 || count < 1) return false;
@@ -1433,7 +1441,8 @@ bool model_prefers_direct(const Committed &ct, int64_t count, int peer_device) {
   const int64_t blk = ct.form == SP_FORM_STRIDED
                           ? std::min(ct.sb.counts[0], obj)
                           : std::max<int64_t>(1, ct.runs.empty() ? 1 : ct.size / static_cast<int64_t>(ct.runs.size()));
-  const int kind = peer_device == R.device ? kDstSameGpu : kDstPeerGpu;
+  const bool same = peer == R.rank || !std::memcmp(R.shm->slots[peer].uuid, R.shm->slots[R.rank].uuid, 16);
+  const int kind = same ? kDstSameGpu : kDstPeerGpu;
   const auto key = std::make_tuple(obj, blk, kind);
   auto it = R.direct_cache.find(key);
   if (it != R.direct_cache.end()) return it->second;

@@ -28,6 +28,8 @@ void rt_check_device_error(const char *what);
 // halo / neighbour flag waits in the stream front end (ranks share a GPU)
 // rather than in the kernel (every rank on its own GPU); TEMPI_FLAG_WAIT
 bool rt_flag_waits_in_stream();
+// true when any other rank runs on another GPU (compared by UUID)
+bool rt_peers_remote();
 // polls a completion event with the peer-liveness checks and TEMPI_TIMEOUT
 // of a host wait (stream work that waits on peers' flags)
 void rt_sync_event(cudaEvent_t e, const char *what);
