@@ -113,8 +113,16 @@ class ClockSampler:
         try:
             pynvml, h = self._nvml_handle()
             self.source = "nvml-2ms"
+            # the timed loop is a tight Python loop: a short GIL switch
+            # interval lets the poller run every ~2 ms inside it, and the
+            # region starts only once the poller has taken its first sample
+            self._switch = sys.getswitchinterval()
+            sys.setswitchinterval(0.0002)
             self.t = threading.Thread(target=self._poll, args=(pynvml, h), daemon=True)
             self.t.start()
+            t0 = time.perf_counter()
+            while not self.nvml and time.perf_counter() - t0 < 1.0:
+                time.sleep(0.001)
             return self
         except Exception:
             pass
@@ -136,6 +144,8 @@ class ClockSampler:
 
     def __exit__(self, *a):
         self._stop.set()
+        if getattr(self, "_switch", None):
+            sys.setswitchinterval(self._switch)
         if self.proc is not None:
             self.proc.terminate()
             try:
