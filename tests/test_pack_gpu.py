@@ -603,6 +603,51 @@ def test_cfg3_constructions_identical(sp, cuda):
         assert torch.equal(o, outs[0])
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("e0", [1, 2, 4, 8, 16, 64, 128, 256, 512])
+def test_cfg3_constructions_identical_every_e0(sp, cuda, e0):
+    """BASELINE config 3 across the whole E0 sweep of config 2 (E0 = 32 is
+    the test above): the five constructions reach one StridedBlock and plan,
+    pack to identical bytes, and unpack those bytes to identical buffers
+    (each through the kernel the engine picks for that E0)"""
+    torch = cuda
+    e2 = 2 ** math.ceil(math.log2((1 << 20) // e0) / 2)
+    e1 = (1 << 20) // (e0 * e2)
+    b = sp.make_named(sp.NamedKind.Byte)
+    ways = [
+        sp.make_subarray(3, [1024] * 3, [e0, e1, e2], [0, 0, 0], b),
+        sp.make_hvector(e2, 1, 1 << 20, sp.make_vector(e1, e0, 1024, b)),
+        sp.make_hvector(e2, 1, 1 << 20, sp.make_vector(e1, 1, 1024 // e0, sp.make_hvector(e0, 1, 1, b))),
+        sp.make_hvector(e2, 1, 1 << 20, sp.make_hvector(e1, 1, 1024, sp.make_contiguous(e0, b))),
+        sp.make_subarray(1, [1024], [e2], [0], sp.make_subarray(2, [1024, 1024], [e0, e1], [0, 0], b)),
+    ]
+    cts = [sp.commit_type(w) for w in ways]
+    assert len({(c.canon, c.plan) for c in cts}) == 1, [c.canon for c in cts]
+    span = max(c.span for c in cts)
+    g = torch.Generator(device="cuda").manual_seed(300 + e0)
+    src = torch.randint(0, 256, (span,), dtype=torch.uint8, device="cuda", generator=g)
+    outs = []
+    for c in cts:
+        o = torch.empty(c.size, dtype=torch.uint8, device="cuda")
+        sp.pack(src, c, 1, o, 0)
+        outs.append(o)
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+    # unpack: the described bytes land, everything else keeps its sentinel
+    first = None
+    for c in cts:
+        dst = torch.full((span,), 0xA5, dtype=torch.uint8, device="cuda")
+        sp.unpack(outs[0], 0, c, 1, dst)
+        if first is None:
+            first = dst
+            assert int((dst != 0xA5).sum()) <= c.size
+            assert torch.equal(dst.view(-1)[: e0], src[: e0])
+        else:
+            assert torch.equal(dst, first)
+            del dst
+    del src, first
+
+
 def test_concurrent_host_threads_share_committed_types(sp, orc, cuda):
     """The reference's threading contract (commit.hpp:81-84):
     committed types are shared read-only and pack/unpack may run from many
