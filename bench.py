@@ -590,7 +590,7 @@ def run_ours(args):
     # cfg1 at the throughput count: 64 vector objects (8-B blocks at 512-B
     # pitch) per call, one extent apart, pack + unpack, cold L2
     ct1 = sp.commit_type(sp.from_program([2, 131072, 1, 64, 0, 3]))
-    n1 = 64
+    n1 = min(64, K)  # the packed buffer holds K MiB (--incount below 64)
     cfg1 = {"object": "cfg1 vector(131072,1,64,DOUBLE)", "incount": n1}
     for pack in (True, False):
         ts = []
